@@ -1,0 +1,202 @@
+/* atc_b200.h — C ABI of the B200-native candidate-evaluation stage and API
+ * backends for ATC (arXiv 2301.11659).  Plain C: no torch or CUDA types in any
+ * signature; every buffer is caller-owned; errors are int status codes with the
+ * message available from atc_last_error().
+ *
+ * What each entry point replaces in the reference (/root/reference/proj):
+ *
+ *   atc_testsets_upload / atc_eval_bindings / atc_eval_enumerated
+ *       the per-binding P2 predicate rewriter::verify_rewrite
+ *       (src/rewriter.cpp:215-284, include/liftc/rewriter.hpp:77-80) evaluated for a
+ *       whole batch of candidate bindings at once, called from the pipeline's
+ *       candidate loop (src/pipeline.cpp:248-310).  The binding-independent half of
+ *       verify_rewrite (sizes, probe image, the original run, :235-251) is the
+ *       caller's "recorded test sets"; the binding-dependent half (oracle dispatch
+ *       :254 -> run_dispatch :99-162 -> run_reference equivalence.cpp:131-139, and
+ *       the full-region compare :264-279) runs on the GPU.
+ *   atc_run_reference
+ *       equivalence::run_reference (src/equivalence.cpp:131-139;
+ *       include/liftc/equivalence.hpp:53-54): reference_gemm :40-65 and
+ *       reference_conv2d :67-93, FP64, non-fused, reference loop order.
+ *   atc_dispatch
+ *       the DispatchContext handler built by make_oracle_dispatch
+ *       (src/rewriter.cpp:176-181; include/liftc/interp.hpp:57-61): positional
+ *       decode + checks of run_dispatch (:99-148), run_reference, write-back with
+ *       f32 rounding (:152-161).
+ *   atc_sgemm_rm
+ *       profitability::cpu_gemm / xpu_gemm (src/profitability.cpp:14-63;
+ *       include/liftc/profitability.hpp:27-28): row-major FP32 C = A*B, C
+ *       overwritten; computed on tcgen05 tensor cores.
+ *   atc_conv2d_nchw
+ *       reference_conv2d semantics (valid padding, unit stride, NCHW/KCRS) on
+ *       FP32 data, computed on tcgen05 tensor cores (implicit GEMM).
+ */
+#ifndef ATC_B200_H
+#define ATC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ATC_OK 0
+#define ATC_ERR_ARG (-1)     /* invalid argument / malformed descriptor          */
+#define ATC_ERR_CUDA (-2)    /* CUDA runtime failure                             */
+#define ATC_ERR_DEVICE (-3)  /* no sm_100 device, or the kernels are not loadable */
+#define ATC_ERR_DISPATCH (-4) /* atc_dispatch: the reference's run_dispatch throw */
+
+/* ---- API spec decode table (api_spec.hpp:26-66, validated spec) ------------ */
+#define ATC_MAX_ARRAYS 4
+#define ATC_MAX_SIZES 12
+#define ATC_MAX_DIMS 6
+
+enum { ATC_SEM_GEMM = 0, ATC_SEM_CONV2D = 1 };
+enum { ATC_LAYOUT_ROW = 0, ATC_LAYOUT_COL = 1 };
+
+/* array roles (ApiParam::role of array params) */
+enum { ATC_ROLE_A = 0, ATC_ROLE_B = 1, ATC_ROLE_C = 2, ATC_ROLE_IN = 0, ATC_ROLE_WEIGHTS = 1, ATC_ROLE_OUT = 2 };
+
+/* size roles (ApiParam::role of int params); role_size[] maps each to a size-param
+ * index or -1 when the spec has no such role (then the reference fallback of
+ * equivalence.cpp:46-48 / :76-77 applies) */
+enum {
+  ATC_SZ_M = 0, ATC_SZ_N, ATC_SZ_K, ATC_SZ_LDA, ATC_SZ_LDB, ATC_SZ_LDC,
+  ATC_SZ_CN, ATC_SZ_CC, ATC_SZ_CH, ATC_SZ_CW, ATC_SZ_CK, ATC_SZ_CR, ATC_SZ_CS, ATC_SZ_COH, ATC_SZ_COW,
+  ATC_SZ_COUNT
+};
+
+typedef struct {
+  int32_t semantics;                   /* ATC_SEM_*                                      */
+  int32_t layout;                      /* ATC_LAYOUT_* (spec.layout)                     */
+  int32_t n_arrays;                    /* spec.arrays(), in spec order                   */
+  int32_t n_sizes;                     /* spec.size_params(), in spec order              */
+  int32_t array_role[ATC_MAX_ARRAYS];  /* ATC_ROLE_*                                     */
+  int32_t array_livein[ATC_MAX_ARRAYS];/* 1 iff liveness == LiveIn (not written/compared) */
+  int32_t array_ndims[ATC_MAX_ARRAYS];
+  int32_t array_dims[ATC_MAX_ARRAYS][ATC_MAX_DIMS]; /* size-param indices (canonical order) */
+  int32_t role_size[ATC_SZ_COUNT];     /* size-param index per role, -1 if absent        */
+} atc_spec_desc;
+
+/* ---- recorded P2 test sets (the binding-independent half of verify_rewrite) -- */
+typedef struct {
+  int32_t n_tests;                 /* T (10 = verify_tests for parity)                  */
+  int32_t n_ints;                  /* user int params, signature order                  */
+  int32_t n_ptrs;                  /* user pointer params, signature order              */
+  const int64_t* int_values;       /* [T][n_ints]: sizes drawn by draw_sizes             */
+  const int32_t* ptr_is_f32;       /* [n_ptrs]: Param::elem == F32 (rewriter.cpp:269)     */
+  const int64_t* region_len;       /* [n_ptrs]: region length (65536 in P2)             */
+  const double* const* init;       /* [T*n_ptrs]: probe image regions (build_probe_image) */
+  const double* const* final_;     /* [T*n_ptrs]: the original run's final regions       */
+  const int32_t* test_ok;          /* [T]: 0 if draw_sizes failed or the original run was
+                                      not Normal at t (every binding fails at t), else 1 */
+} atc_testsets;
+
+typedef struct atc_ctx atc_ctx;
+typedef struct atc_testset_handle atc_testset_handle;
+
+/* verdict reason codes (per binding, at its first failing test) */
+enum {
+  ATC_PASS = 0,           /* passed every test                                         */
+  ATC_FAIL_MISMATCH = 1,  /* "mismatch on X[i]" (rewriter.cpp:271-277)                  */
+  ATC_FAIL_DISPATCH = 2,  /* "dispatch failed: ..." — size < 1 or region too small
+                             (rewriter.cpp:136-148 via :253-258)                        */
+  ATC_FAIL_TESTSET = 3,   /* draw_sizes failed / original run not Normal (:241-251)      */
+  ATC_FAIL_UB = 4,        /* an access outside the region: undefined behaviour in the
+                             reference (vector operator[] out of range); rejected        */
+  ATC_REASON_COUNT = 5
+};
+
+enum { ATC_MODE_FP64 = 0, ATC_MODE_FP32_SCREEN = 1 };
+
+int atc_device_count(void);
+atc_ctx* atc_create(int device);
+void atc_destroy(atc_ctx* ctx);
+const char* atc_last_error(const atc_ctx* ctx);
+
+/* Run all subsequent work of this context on the caller's CUDA stream
+ * (cudaStream_t as void*; NULL restores the context's own stream). */
+int atc_set_stream(atc_ctx* ctx, void* stream);
+
+/* Kernel-level instrumentation (CUDA events around every evaluator launch on the
+ * launching stream).  atc_profile_read synchronises and returns the totals since
+ * atc_profile_start. */
+typedef struct {
+  double screen_ms;        /* K1: sum of k_screen durations                   */
+  int64_t screen_launches;
+  double confirm_ms;       /* K2: sum of k_confirm durations                  */
+  int64_t confirm_launches;
+  int64_t survivors;       /* bindings handed from K1 to K2                   */
+  int64_t bindings;        /* bindings screened                               */
+} atc_profile;
+int atc_profile_start(atc_ctx* ctx);
+int atc_profile_read(atc_ctx* ctx, atc_profile* out);
+
+/* Uploads the T recorded test sets to HBM once per user function and builds the
+ * per-(t, pointer) dirty lists {i : |init_i - final_i| > abs + rel*|final_i|}.
+ * Host buffers are not retained. */
+int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out);
+int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h);
+
+/* Explicit candidate list (ranked order).  arr_map[b*n_arrays + a] = user pointer
+ * index bound to API array a; size_map[b*n_sizes + q] = user int index bound to
+ * API size param q.  Outputs (host): fail_t[b] = first failing test or -1,
+ * reason[b] = ATC_*; *first_pass = smallest b with reason ATC_PASS, or -1. */
+int atc_eval_bindings(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_handle* ts,
+                      const uint8_t* arr_map, const uint8_t* size_map, int64_t n_bindings,
+                      int32_t mode, int8_t* fail_t, int8_t* reason, int64_t* first_pass);
+
+/* Same with device-resident inputs/outputs on the caller's CUDA stream (cudaStream_t
+ * passed as void*); returns without synchronising. */
+int atc_eval_bindings_device(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_handle* ts,
+                             const uint8_t* d_arr_map, const uint8_t* d_size_map, int64_t n_bindings,
+                             int32_t mode, int8_t* d_fail_t, int8_t* d_reason, void* stream);
+
+/* Unpruned space in SURVEY.md Appendix C order: index = perm * n_ints^n_sizes + s,
+ * API size param q bound to user int (s / n_ints^q) % n_ints; perms[p*n_arrays + a]
+ * is the user pointer of API array a under permutation p.  Evaluates [begin, end)
+ * and returns the passing indices (ascending, at most cap), their total count and a
+ * histogram of first-failure reasons. */
+int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_handle* ts,
+                        const uint8_t* perms, int32_t n_perms, uint64_t begin, uint64_t end,
+                        int32_t mode, uint64_t* survivors, int64_t cap, int64_t* n_survivors,
+                        int64_t* reason_counts);
+
+/* FP64 reference semantics on the GPU (equivalence::run_reference).  sizes[q] per
+ * spec size param; buffers[a] (host, length buffer_len[a]) per spec array;
+ * non-LiveIn arrays are rewritten in place. */
+int atc_run_reference(atc_ctx* ctx, const atc_spec_desc* spec, const int64_t* sizes,
+                      double* const* buffers, const int64_t* buffer_len);
+
+/* make_oracle_dispatch handler body (rewriter.cpp:99-162) for one call whose
+ * arguments are already decoded positionally: sizes[q] (ints), regions[a] with
+ * region_len[a] and region_is_f32[a].  Returns ATC_ERR_DISPATCH with the
+ * reference's message ("... is not positive" / "holds N elements, call needs M")
+ * when run_dispatch would throw. */
+int atc_dispatch(atc_ctx* ctx, const atc_spec_desc* spec, const int64_t* sizes,
+                 double* const* regions, const int64_t* region_len, const int32_t* region_is_f32);
+
+/* Backends.  precision: 0 = TF32 (1 pass), 1 = 3xTF32 (split, ~FP32 accuracy). */
+enum { ATC_PREC_TF32 = 0, ATC_PREC_3XTF32 = 1 };
+int atc_sgemm_rm(atc_ctx* ctx, const float* A, const float* B, float* C,
+                 int64_t m, int64_t n, int64_t k, int32_t precision);
+int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* dC,
+                        int64_t m, int64_t n, int64_t k, int32_t precision, void* stream);
+int atc_conv2d_nchw(atc_ctx* ctx, const float* in, const float* w, float* out, int64_t n, int64_t c,
+                    int64_t h, int64_t w_, int64_t k, int64_t r, int64_t s, int32_t precision);
+int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, float* d_out,
+                           int64_t n, int64_t c, int64_t h, int64_t w_, int64_t k, int64_t r,
+                           int64_t s, int32_t precision, void* stream);
+
+/* Host helpers for building P2 probe images exactly like analysis::build_probe_image
+ * (analysis.cpp:73-98) on the std::mt19937_64 stream of liftc::Rng (rng.hpp:13-48):
+ * skip `skip` raw draws of mt19937_64(seed), then write n raw draws / n values of
+ * uniform_real(lo, hi), optionally rounded through float. */
+void atc_mt64_raw(uint64_t seed, uint64_t skip, int64_t n, uint64_t* out);
+void atc_mt64_uniform(uint64_t seed, uint64_t skip, int64_t n, double lo, double hi,
+                      int32_t round_f32, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATC_B200_H */

@@ -1,0 +1,86 @@
+"""Generate tests/golden/ from the compiled reference (TEST INFRASTRUCTURE).
+
+    make -C oracle ref && python oracle/gen_golden.py
+
+Runs `oracle/_ref/ref_tool golden <tmp>` (the unmodified reference: liftc_core
+built from /root/reference/proj/src) and converts its raw dump into small
+committed fixtures:
+
+  tests/golden/specs.json         the four bundled specs, validated/canonicalised
+  tests/golden/pipeline.json      masked `liftc bench`-style reports for the corpus
+  tests/golden/<stem>.json        per GEMM/conv program: params, size rules, seeds,
+                                  analysis, P2 test-set metadata (sizes, init-region
+                                  FNV-1a + head values), pruned candidates with P1/P2
+                                  verdicts, unpruned-space metadata
+  tests/golden/<stem>.npz         final-minus-init diffs of the original runs and the
+                                  per-binding verdict arrays (P2 first failing test +
+                                  reason at T=16, P1 verdict at 30 tests)
+
+Test-set init regions are NOT stored: they are regenerated from the seeds by
+paper_2301_11659_b200.probe and pinned against the FNV-1a recorded here.
+"""
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+OUT = os.path.join(ROOT, "tests", "golden")
+
+
+def _take(bin_bytes, ref, dtype):
+    off, cnt = ref["offset"], ref["count"]
+    return np.frombuffer(bin_bytes, dtype=dtype, count=cnt, offset=off).copy()
+
+
+def convert(raw: str) -> None:
+    os.makedirs(OUT, exist_ok=True)
+    for name in ("specs.json", "pipeline.json", "index.json"):
+        with open(os.path.join(raw, name)) as f, open(os.path.join(OUT, name), "w") as g:
+            json.dump(json.load(f), g, indent=1, sort_keys=True)
+    with open(os.path.join(raw, "index.json")) as f:
+        stems = json.load(f)
+    for stem in stems:
+        with open(os.path.join(raw, stem + ".json")) as f:
+            j = json.load(f)
+        arrays = {}
+        if "testsets" in j:
+            with open(os.path.join(raw, stem + ".bin"), "rb") as f:
+                b = f.read()
+            for key in ("testsets", "testsets64"):
+                for ts in j.get(key, []):
+                    for rname, r in (ts.get("regions") or {}).items():
+                        if "diff_pos" in r:
+                            k = f"{key}_t{ts['t']}_{rname}"
+                            arrays[k + "_pos"] = _take(b, r.pop("diff_pos"), np.int64)
+                            arrays[k + "_val"] = _take(b, r.pop("diff_val"), np.float64)
+                            r["diff_key"] = k
+            for sname, s in j.get("specs", {}).items():
+                for field, dt in (("idx", np.uint64), ("p2_fail_t", np.int8), ("p2_reason", np.int8),
+                                  ("p1", np.int8), ("p2_64_fail_t", np.int8), ("p2_64_reason", np.int8)):
+                    if field in s:
+                        arrays[f"{sname}__{field}"] = _take(b, s.pop(field), dt)
+                        s[field] = f"{sname}__{field}"
+        with open(os.path.join(OUT, stem + ".json"), "w") as f:
+            json.dump(j, f, indent=1, sort_keys=True)
+        if arrays:
+            np.savez_compressed(os.path.join(OUT, stem + ".npz"), **arrays)
+        print(f"[gen_golden] {stem}: {len(arrays)} arrays")
+
+
+def main() -> None:
+    tool = os.path.join(HERE, "_ref", "ref_tool")
+    if len(sys.argv) > 1:
+        convert(sys.argv[1])
+        return
+    with tempfile.TemporaryDirectory() as raw:
+        subprocess.run([tool, "golden", raw], check=True)
+        convert(raw)
+
+
+if __name__ == "__main__":
+    main()

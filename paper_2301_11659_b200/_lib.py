@@ -1,0 +1,173 @@
+"""ctypes binding of libatc_b200.so (include/atc_b200.h).
+
+The product path has no fallback: if the library cannot be loaded, or no sm_100
+device is present when a compute entry point is called, an AtcError is raised.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libatc_b200.so")
+
+ATC_MAX_ARRAYS = 4
+ATC_MAX_SIZES = 12
+ATC_MAX_DIMS = 6
+ATC_SZ_COUNT = 15
+
+ATC_OK = 0
+ATC_ERR_ARG = -1
+ATC_ERR_CUDA = -2
+ATC_ERR_DEVICE = -3
+ATC_ERR_DISPATCH = -4
+
+SEM_GEMM, SEM_CONV2D = 0, 1
+LAYOUT_ROW, LAYOUT_COL = 0, 1
+# size roles, in ATC_SZ_* order
+SIZE_ROLES = ["m", "n", "k", "lda", "ldb", "ldc"]
+CONV_SIZE_ROLES = ["n", "c", "h", "w", "k", "r", "s", "oh", "ow"]
+ARRAY_ROLES = {"gemm": {"a": 0, "b": 1, "c": 2}, "conv2d": {"in": 0, "weights": 1, "out": 2}}
+
+PASS, FAIL_MISMATCH, FAIL_DISPATCH, FAIL_TESTSET, FAIL_UB = 0, 1, 2, 3, 4
+REASON_NAMES = ["pass", "mismatch", "dispatch_failed", "testset", "ub"]
+MODE_FP64, MODE_FP32_SCREEN = 0, 1
+PREC_TF32, PREC_3XTF32 = 0, 1
+
+
+class AtcError(RuntimeError):
+    """A failing status from libatc_b200 (the message is atc_last_error)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class SpecDesc(C.Structure):
+    _fields_ = [
+        ("semantics", C.c_int32),
+        ("layout", C.c_int32),
+        ("n_arrays", C.c_int32),
+        ("n_sizes", C.c_int32),
+        ("array_role", C.c_int32 * ATC_MAX_ARRAYS),
+        ("array_livein", C.c_int32 * ATC_MAX_ARRAYS),
+        ("array_ndims", C.c_int32 * ATC_MAX_ARRAYS),
+        ("array_dims", (C.c_int32 * ATC_MAX_DIMS) * ATC_MAX_ARRAYS),
+        ("role_size", C.c_int32 * ATC_SZ_COUNT),
+    ]
+
+
+class Testsets(C.Structure):
+    _fields_ = [
+        ("n_tests", C.c_int32),
+        ("n_ints", C.c_int32),
+        ("n_ptrs", C.c_int32),
+        ("int_values", C.POINTER(C.c_int64)),
+        ("ptr_is_f32", C.POINTER(C.c_int32)),
+        ("region_len", C.POINTER(C.c_int64)),
+        ("init", C.POINTER(C.c_void_p)),
+        ("final_", C.POINTER(C.c_void_p)),
+        ("test_ok", C.POINTER(C.c_int32)),
+    ]
+
+
+class Profile(C.Structure):
+    _fields_ = [
+        ("screen_ms", C.c_double),
+        ("screen_launches", C.c_int64),
+        ("confirm_ms", C.c_double),
+        ("confirm_launches", C.c_int64),
+        ("survivors", C.c_int64),
+        ("bindings", C.c_int64),
+    ]
+
+
+# (name, restype, argtypes) for every function declared in include/atc_b200.h
+_P = C.c_void_p
+_SIGS = [
+    ("atc_device_count", C.c_int, []),
+    ("atc_create", _P, [C.c_int]),
+    ("atc_destroy", None, [_P]),
+    ("atc_last_error", C.c_char_p, [_P]),
+    ("atc_set_stream", C.c_int, [_P, _P]),
+    ("atc_profile_start", C.c_int, [_P]),
+    ("atc_profile_read", C.c_int, [_P, C.POINTER(Profile)]),
+    ("atc_testsets_upload", C.c_int, [_P, C.POINTER(Testsets), C.POINTER(_P)]),
+    ("atc_testsets_free", C.c_int, [_P, _P]),
+    ("atc_eval_bindings", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, C.c_int64, C.c_int32, _P, _P,
+                                    C.POINTER(C.c_int64)]),
+    ("atc_eval_bindings_device", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, C.c_int64, C.c_int32, _P, _P, _P]),
+    ("atc_eval_enumerated", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, C.c_int32, C.c_uint64, C.c_uint64, C.c_int32,
+                                      _P, C.c_int64, C.POINTER(C.c_int64), _P]),
+    ("atc_run_reference", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P]),
+    ("atc_dispatch", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, _P]),
+    ("atc_sgemm_rm", C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int32]),
+    ("atc_sgemm_rm_device", C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _P]),
+    ("atc_conv2d_nchw", C.c_int, [_P, _P, _P, _P] + [C.c_int64] * 7 + [C.c_int32]),
+    ("atc_conv2d_nchw_device", C.c_int, [_P, _P, _P, _P] + [C.c_int64] * 7 + [C.c_int32, _P]),
+    ("atc_mt64_raw", None, [C.c_uint64, C.c_uint64, C.c_int64, _P]),
+    ("atc_mt64_uniform", None, [C.c_uint64, C.c_uint64, C.c_int64, C.c_double, C.c_double, C.c_int32, _P]),
+]
+EXPORTED = [s[0] for s in _SIGS]
+
+_lib = None
+
+
+def lib():
+    """Load libatc_b200.so once; raise loudly if it is missing or incomplete."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise AtcError(ATC_ERR_DEVICE, f"{LIB_PATH} is not built (run __graft_entry__.build())")
+    h = C.CDLL(LIB_PATH)
+    for name, res, args in _SIGS:
+        fn = getattr(h, name)  # AttributeError if the symbol is missing
+        fn.restype = res
+        fn.argtypes = args
+    _lib = h
+    return h
+
+
+def check(ctx, rc: int) -> None:
+    if rc != ATC_OK:
+        msg = lib().atc_last_error(ctx)
+        raise AtcError(rc, msg.decode() if msg else f"atc error {rc}")
+
+
+class Context:
+    """One libatc context bound to one CUDA device (one process per GPU)."""
+
+    def __init__(self, device: int = 0):
+        L = lib()
+        self.device = device
+        self.handle = L.atc_create(device)
+        if not self.handle:
+            raise AtcError(ATC_ERR_DEVICE, "atc_create returned NULL")
+        msg = L.atc_last_error(self.handle)
+        if msg:
+            err = msg.decode()
+            L.atc_destroy(self.handle)
+            self.handle = None
+            raise AtcError(ATC_ERR_DEVICE, err)
+
+    def close(self) -> None:
+        if self.handle:
+            lib().atc_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default = {}
+
+
+def default_context(device: int = 0) -> Context:
+    ctx = _default.get(device)
+    if ctx is None:
+        ctx = _default[device] = Context(device)
+    return ctx

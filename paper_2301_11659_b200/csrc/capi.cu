@@ -1,0 +1,592 @@
+// C ABI (include/atc_b200.h): context, test-set upload, evaluator entry points.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "atc_b200.h"
+#include "capi_internal.h"
+#include "eval_common.cuh"
+
+namespace atc {
+__global__ void k_build_dirty(TestsetView ts, int32_t* dirty_pos, int32_t* dirty_cnt, int32_t* dirty_max);
+
+__global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, int budget,
+                         int32_t* keys, uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
+                         unsigned long long* reason_hist);
+__global__ void k_confirm(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
+                          const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys);
+__global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
+                             const int32_t* surv_keys, int32_t* keys);
+__global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason);
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v);
+}  // namespace atc
+
+using namespace atc;
+
+struct atc_testset_handle {
+  TestsetView view{};
+  int32_t T = 0, nI = 0, nP = 0;
+  std::vector<int64_t> h_ints;  // host copy of the int values
+  std::vector<void*> allocations;
+};
+
+// ------------------------------------------------------------ ctx helpers -----
+void atc_set_error(atc_ctx* ctx, const char* fmt, ...) {
+  if (!ctx) return;
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  ctx->err = buf;
+}
+
+bool atc_cuda_ok(atc_ctx* ctx, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return true;
+  atc_set_error(ctx, "%s: %s", what, cudaGetErrorString(e));
+  return false;
+}
+
+void* atc_ctx_scratch(atc_ctx* ctx, int slot, size_t bytes) {
+  if (ctx->scratch_bytes[slot] >= bytes) return ctx->scratch[slot];
+  if (ctx->scratch[slot]) cudaFree(ctx->scratch[slot]);
+  ctx->scratch[slot] = nullptr;
+  ctx->scratch_bytes[slot] = 0;
+  size_t want = std::max(bytes, (size_t)4096);
+  if (cudaMalloc(&ctx->scratch[slot], want) != cudaSuccess) return nullptr;
+  ctx->scratch_bytes[slot] = want;
+  return ctx->scratch[slot];
+}
+
+namespace {
+
+bool build_spec_view(atc_ctx* ctx, const atc_spec_desc* s, SpecView& v) {
+  if (!s) {
+    atc_set_error(ctx, "null spec descriptor");
+    return false;
+  }
+  if ((s->semantics != ATC_SEM_GEMM && s->semantics != ATC_SEM_CONV2D) ||
+      (s->layout != ATC_LAYOUT_ROW && s->layout != ATC_LAYOUT_COL) || s->n_arrays != 3 ||
+      s->n_sizes < 1 || s->n_sizes > ATC_MAX_SIZES) {
+    atc_set_error(ctx, "malformed spec descriptor (semantics %d, layout %d, %d arrays, %d sizes)",
+                  s->semantics, s->layout, s->n_arrays, s->n_sizes);
+    return false;
+  }
+  std::memset(&v, 0, sizeof v);
+  v.sem = s->semantics;
+  v.layout = s->layout;
+  v.nA = s->n_arrays;
+  v.nS = s->n_sizes;
+  int seen[3] = {-1, -1, -1};
+  int outputs = 0;
+  for (int a = 0; a < v.nA; ++a) {
+    int r = s->array_role[a];
+    if (r < 0 || r > 2 || seen[r] >= 0) {
+      atc_set_error(ctx, "array %d: bad or duplicate role %d", a, r);
+      return false;
+    }
+    seen[r] = a;
+    v.role[a] = r;
+    if (!s->array_livein[a]) {
+      ++outputs;
+      if (r != ATC_ROLE_C) {
+        atc_set_error(ctx, "only the C/out array may be an output (array %d)", a);
+        return false;
+      }
+    }
+    if (s->array_ndims[a] < 1 || s->array_ndims[a] > ATC_MAX_DIMS) {
+      atc_set_error(ctx, "array %d: bad dim count %d", a, s->array_ndims[a]);
+      return false;
+    }
+    v.ndims[a] = s->array_ndims[a];
+    for (int d = 0; d < v.ndims[a]; ++d) {
+      int q = s->array_dims[a][d];
+      if (q < 0 || q >= v.nS) {
+        atc_set_error(ctx, "array %d dim %d: size index %d out of range", a, d, q);
+        return false;
+      }
+      v.dims[a][d] = q;
+    }
+  }
+  if (outputs != 1) {
+    atc_set_error(ctx, "spec must have exactly one non-LiveIn array (has %d)", outputs);
+    return false;
+  }
+  for (int r = 0; r < 3; ++r) v.arr_of_role[r] = seen[r];
+  for (int r = 0; r < ATC_SZ_COUNT; ++r) {
+    int q = s->role_size[r];
+    if (q >= v.nS) {
+      atc_set_error(ctx, "role %d: size index %d out of range", r, q);
+      return false;
+    }
+    v.role_size[r] = q;
+  }
+  if (v.sem == ATC_SEM_GEMM) {
+    for (int r : {ATC_SZ_M, ATC_SZ_N, ATC_SZ_K})
+      if (v.role_size[r] < 0) {
+        // the reference would use 0 (equivalence.cpp:42-44): loops never run
+      }
+  }
+  return true;
+}
+
+
+}  // namespace
+
+extern "C" {
+
+int atc_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+atc_ctx* atc_create(int device) {
+  auto* ctx = new atc_ctx();
+  ctx->device = device;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || device < 0 || device >= n) {
+    atc_set_error(ctx, "no CUDA device %d (%s)", device, e == cudaSuccess ? "out of range" : cudaGetErrorString(e));
+    ctx->broken = true;
+    return ctx;
+  }
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  ctx->sm_count = prop.multiProcessorCount;
+  if (prop.major != 10) {
+    atc_set_error(ctx, "device %d is sm_%d%d; this library is built for sm_100a only", device, prop.major,
+                  prop.minor);
+    ctx->broken = true;
+    return ctx;
+  }
+  cudaSetDevice(device);
+  if (!atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate"))
+    ctx->broken = true;
+  ctx->own_stream = ctx->stream;
+  return ctx;
+}
+
+void atc_destroy(atc_ctx* ctx) {
+  if (!ctx) return;
+  if (!ctx->broken) {
+    cudaSetDevice(ctx->device);
+    for (auto& p : ctx->scratch)
+      if (p) cudaFree(p);
+    for (auto& p : ctx->pinned)
+      if (p) cudaFreeHost(p);
+    for (auto& e : ctx->prof_screen) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
+    for (auto& e : ctx->prof_confirm) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  }
+  delete ctx;
+}
+
+const char* atc_last_error(const atc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int atc_set_stream(atc_ctx* ctx, void* stream) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  return ATC_OK;
+}
+
+static void prof_clear(atc_ctx* ctx) {
+  for (auto& e : ctx->prof_screen) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
+  for (auto& e : ctx->prof_confirm) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
+  ctx->prof_screen.clear();
+  ctx->prof_confirm.clear();
+  ctx->prof_survivors = ctx->prof_bindings = 0;
+}
+
+int atc_profile_start(atc_ctx* ctx) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  cudaSetDevice(ctx->device);
+  prof_clear(ctx);
+  ctx->prof = true;
+  return ATC_OK;
+}
+
+int atc_profile_read(atc_ctx* ctx, atc_profile* out) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (!out) return ATC_ERR_ARG;
+  cudaSetDevice(ctx->device);
+  std::memset(out, 0, sizeof *out);
+  for (auto* list : {&ctx->prof_screen, &ctx->prof_confirm}) {
+    double ms = 0;
+    for (auto& e : *list) {
+      if (!atc_cuda_ok(ctx, cudaEventSynchronize(e.second), "profile sync")) return ATC_ERR_CUDA;
+      float f = 0;
+      cudaEventElapsedTime(&f, e.first, e.second);
+      ms += f;
+    }
+    if (list == &ctx->prof_screen) {
+      out->screen_ms = ms;
+      out->screen_launches = (int64_t)list->size();
+    } else {
+      out->confirm_ms = ms;
+      out->confirm_launches = (int64_t)list->size();
+    }
+  }
+  out->survivors = ctx->prof_survivors;
+  out->bindings = ctx->prof_bindings;
+  prof_clear(ctx);
+  ctx->prof = false;
+  return ATC_OK;
+}
+
+int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (!ts || !out || ts->n_tests < 1 || ts->n_tests > kMaxT || ts->n_ints < 1 || ts->n_ints > kMaxInts ||
+      ts->n_ptrs < 1 || ts->n_ptrs > kMaxPtrs) {
+    atc_set_error(ctx, "malformed test sets");
+    return ATC_ERR_ARG;
+  }
+  cudaSetDevice(ctx->device);
+  const int T = ts->n_tests, nI = ts->n_ints, nP = ts->n_ptrs;
+  auto* h = new atc_testset_handle();
+  h->T = T;
+  h->nI = nI;
+  h->nP = nP;
+  h->h_ints.assign(ts->int_values, ts->int_values + (size_t)T * nI);
+  // region pool layout: (t, p) regions back to back, each 32-element aligned
+  std::vector<int64_t> off((size_t)T * nP), doff((size_t)T * nP);
+  int64_t total = 0, dtotal = 0;
+  for (int t = 0; t < T; ++t)
+    for (int p = 0; p < nP; ++p) {
+      int64_t len = ts->region_len[p];
+      if (len < 4 || len >= (1LL << 31)) {
+        atc_set_error(ctx, "region %d length %lld outside [4, 2^31)", p, (long long)len);
+        delete h;
+        return ATC_ERR_ARG;
+      }
+      off[(size_t)t * nP + p] = total;
+      doff[(size_t)t * nP + p] = dtotal;
+      total += (len + 31) / 32 * 32;
+      dtotal += len;
+    }
+  auto dmalloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max(bytes, (size_t)256)) != cudaSuccess) return nullptr;
+    h->allocations.push_back(p);
+    return p;
+  };
+  double* init = (double*)dmalloc(total * 8);
+  double* fin = (double*)dmalloc(total * 8);
+  int64_t* ints = (int64_t*)dmalloc((size_t)T * nI * 8);
+  int32_t* isf = (int32_t*)dmalloc(nP * 4);
+  int64_t* rlen = (int64_t*)dmalloc(nP * 8);
+  int32_t* tok = (int32_t*)dmalloc(T * 4);
+  int64_t* roff = (int64_t*)dmalloc((size_t)T * nP * 8);
+  int32_t* dpos = (int32_t*)dmalloc(dtotal * 4);
+  int64_t* dof = (int64_t*)dmalloc((size_t)T * nP * 8);
+  int32_t* dcnt = (int32_t*)dmalloc((size_t)T * nP * 4);
+  int32_t* dmax = (int32_t*)dmalloc((size_t)T * nP * 4);
+  if (!init || !fin || !ints || !isf || !rlen || !tok || !roff || !dpos || !dof || !dcnt || !dmax) {
+    atc_set_error(ctx, "cudaMalloc failed for %lld region doubles", (long long)total);
+    atc_testsets_free(ctx, h);
+    return ATC_ERR_CUDA;
+  }
+  cudaStream_t st = ctx->stream;
+  bool ok = true;
+  for (int t = 0; t < T && ok; ++t)
+    for (int p = 0; p < nP && ok; ++p) {
+      const size_t i = (size_t)t * nP + p;
+      const size_t bytes = (size_t)ts->region_len[p] * 8;
+      const double* hi = ts->init[i];
+      const double* hf = ts->final_[i];
+      if (!hi || !hf) {
+        // a test whose original run failed has no final image; the region stays
+        // unused because every binding fails at t (test_ok[t] == 0)
+        if (ts->test_ok && ts->test_ok[t]) {
+          atc_set_error(ctx, "test %d pointer %d: missing region", t, p);
+          ok = false;
+        }
+        ok = ok && atc_cuda_ok(ctx, cudaMemsetAsync(init + off[i], 0, bytes, st), "memset") &&
+             atc_cuda_ok(ctx, cudaMemsetAsync(fin + off[i], 0, bytes, st), "memset");
+        continue;
+      }
+      ok = atc_cuda_ok(ctx, cudaMemcpyAsync(init + off[i], hi, bytes, cudaMemcpyHostToDevice, st), "H2D init") &&
+           atc_cuda_ok(ctx, cudaMemcpyAsync(fin + off[i], hf, bytes, cudaMemcpyHostToDevice, st), "H2D final");
+    }
+  std::vector<int32_t> tok_h(T, 1);
+  if (ts->test_ok)
+    for (int t = 0; t < T; ++t) tok_h[t] = ts->test_ok[t] ? 1 : 0;
+  std::vector<int32_t> zero((size_t)T * nP, 0), neg((size_t)T * nP, -1);
+  ok = ok && atc_cuda_ok(ctx, cudaMemcpyAsync(ints, ts->int_values, (size_t)T * nI * 8, cudaMemcpyHostToDevice, st), "H2D") &&
+       atc_cuda_ok(ctx, cudaMemcpyAsync(isf, ts->ptr_is_f32, nP * 4, cudaMemcpyHostToDevice, st), "H2D") &&
+       atc_cuda_ok(ctx, cudaMemcpyAsync(rlen, ts->region_len, nP * 8, cudaMemcpyHostToDevice, st), "H2D") &&
+       atc_cuda_ok(ctx, cudaMemcpyAsync(tok, tok_h.data(), T * 4, cudaMemcpyHostToDevice, st), "H2D") &&
+       atc_cuda_ok(ctx, cudaMemcpyAsync(roff, off.data(), (size_t)T * nP * 8, cudaMemcpyHostToDevice, st), "H2D") &&
+       atc_cuda_ok(ctx, cudaMemcpyAsync(dof, doff.data(), (size_t)T * nP * 8, cudaMemcpyHostToDevice, st), "H2D") &&
+       atc_cuda_ok(ctx, cudaMemcpyAsync(dcnt, zero.data(), (size_t)T * nP * 4, cudaMemcpyHostToDevice, st), "H2D") &&
+       atc_cuda_ok(ctx, cudaMemcpyAsync(dmax, neg.data(), (size_t)T * nP * 4, cudaMemcpyHostToDevice, st), "H2D");
+  TestsetView& v = h->view;
+  v.T = T;
+  v.nI = nI;
+  v.nP = nP;
+  v.ints = ints;
+  v.is_f32 = isf;
+  v.region_len = rlen;
+  v.test_ok = tok;
+  v.init = init;
+  v.fin = fin;
+  v.region_off = roff;
+  v.dirty_pos = dpos;
+  v.dirty_off = dof;
+  v.dirty_cnt = dcnt;
+  v.dirty_max = dmax;
+  if (ok) {
+    int64_t maxlen = 0;
+    for (int p = 0; p < nP; ++p) maxlen = std::max<int64_t>(maxlen, ts->region_len[p]);
+    dim3 grid((unsigned)std::min<int64_t>((maxlen + 255) / 256, 64), (unsigned)(T * nP));
+    k_build_dirty<<<grid, 256, 0, st>>>(v, dpos, dcnt, dmax);
+    ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_build_dirty") &&
+         atc_cuda_ok(ctx, cudaStreamSynchronize(st), "upload sync");
+  }
+  if (!ok) {
+    atc_testsets_free(ctx, h);
+    return ATC_ERR_CUDA;
+  }
+  *out = h;
+  return ATC_OK;
+}
+
+int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h) {
+  if (!h) return ATC_OK;
+  if (ctx && !ctx->broken) cudaSetDevice(ctx->device);
+  for (void* p : h->allocations) cudaFree(p);
+  delete h;
+  return ATC_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+constexpr int kScreenThreads = 256;
+
+int screen_budget(const SpecView& sp) { return sp.sem == ATC_SEM_GEMM ? 16 : 2; }
+
+// Runs K1 + K2 over `n` bindings; survivors/keys live in ctx scratch.
+int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, const BindingSource& src,
+             uint64_t n, int32_t* keys, uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
+             int32_t* surv_keys, unsigned long long* hist, cudaStream_t st) {
+  if (n == 0) return ATC_OK;
+  const uint64_t blocks_needed = (n + kScreenThreads - 1) / kScreenThreads;
+  const unsigned grid = (unsigned)std::min<uint64_t>(blocks_needed, (uint64_t)ctx->sm_count * 32);
+  cudaMemsetAsync(surv_cnt, 0, sizeof(unsigned long long), st);
+  auto ev_pair = [&]() {
+    std::pair<cudaEvent_t, cudaEvent_t> p{nullptr, nullptr};
+    cudaEventCreate(&p.first);
+    cudaEventCreate(&p.second);
+    return p;
+  };
+  std::pair<cudaEvent_t, cudaEvent_t> e1{}, e2{};
+  if (ctx->prof) {
+    e1 = ev_pair();
+    cudaEventRecord(e1.first, st);
+    ctx->prof_bindings += (long long)n;
+  }
+  k_screen<<<grid, kScreenThreads, 0, st>>>(ts->view, sp, src, n, screen_budget(sp), keys, surv, surv_cap,
+                                            surv_cnt, hist);
+  if (ctx->prof) {
+    cudaEventRecord(e1.second, st);
+    ctx->prof_screen.push_back(e1);
+  }
+  k_fill_i32<<<(unsigned)std::min<uint64_t>((surv_cap + 255) / 256, 1024), 256, 0, st>>>(surv_keys, (int64_t)surv_cap,
+                                                                                        kPassKey);
+  if (ctx->prof) {
+    e2 = ev_pair();
+    cudaEventRecord(e2.first, st);
+  }
+  k_confirm<<<(unsigned)ctx->sm_count * 8, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys);
+  if (ctx->prof) {
+    cudaEventRecord(e2.second, st);
+    ctx->prof_confirm.push_back(e2);
+  }
+  if (keys) k_merge_keys<<<64, 256, 0, st>>>(surv, surv_cnt, surv_cap, surv_keys, keys);
+  if (!atc_cuda_ok(ctx, cudaGetLastError(), "evaluator launch")) return ATC_ERR_CUDA;
+  return ATC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int atc_eval_bindings_device(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_handle* ts,
+                             const uint8_t* d_arr_map, const uint8_t* d_size_map, int64_t n_bindings,
+                             int32_t mode, int8_t* d_fail_t, int8_t* d_reason, void* stream) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  SpecView sp;
+  if (!build_spec_view(ctx, spec, sp)) return ATC_ERR_ARG;
+  if (!ts || n_bindings < 0 || (mode != ATC_MODE_FP64 && mode != ATC_MODE_FP32_SCREEN)) {
+    atc_set_error(ctx, "bad arguments to atc_eval_bindings");
+    return ATC_ERR_ARG;
+  }
+  if (n_bindings == 0) return ATC_OK;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  const uint64_t n = (uint64_t)n_bindings;
+  int32_t* keys = (int32_t*)atc_ctx_scratch(ctx, 0, n * 4);
+  uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, n * 8);
+  int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, n * 4);
+  unsigned long long* cnt = (unsigned long long*)atc_ctx_scratch(ctx, 3, 64);
+  if (!keys || !surv || !skeys || !cnt) {
+    atc_set_error(ctx, "scratch allocation failed for %lld bindings", (long long)n_bindings);
+    return ATC_ERR_CUDA;
+  }
+  BindingSource src{d_arr_map, d_size_map, nullptr, 0, 0, 0};
+  k_fill_i32<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, st>>>(keys, (int64_t)n, kPassKey);
+  int rc = run_eval(ctx, sp, ts, src, n, keys, surv, n, cnt, skeys, nullptr, st);
+  if (rc) return rc;
+  k_keys_to_verdicts<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, st>>>(keys, (int64_t)n,
+                                                                                         d_fail_t, d_reason);
+  return atc_cuda_ok(ctx, cudaGetLastError(), "verdict launch") ? ATC_OK : ATC_ERR_CUDA;
+}
+
+int atc_eval_bindings(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_handle* ts,
+                      const uint8_t* arr_map, const uint8_t* size_map, int64_t n_bindings, int32_t mode,
+                      int8_t* fail_t, int8_t* reason, int64_t* first_pass) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (first_pass) *first_pass = -1;
+  if (n_bindings < 0 || (n_bindings > 0 && (!arr_map || !size_map || !fail_t || !reason))) {
+    atc_set_error(ctx, "bad arguments to atc_eval_bindings");
+    return ATC_ERR_ARG;
+  }
+  if (n_bindings == 0) return ATC_OK;
+  SpecView sp;
+  if (!build_spec_view(ctx, spec, sp)) return ATC_ERR_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t n = (size_t)n_bindings;
+  uint8_t* d_in = (uint8_t*)atc_ctx_scratch(ctx, 4, n * (sp.nA + sp.nS));
+  int8_t* d_out = (int8_t*)atc_ctx_scratch(ctx, 5, n * 2);
+  if (!d_in || !d_out) {
+    atc_set_error(ctx, "scratch allocation failed");
+    return ATC_ERR_CUDA;
+  }
+  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(d_in, arr_map, n * sp.nA, cudaMemcpyHostToDevice, st), "H2D arr_map") ||
+      !atc_cuda_ok(ctx, cudaMemcpyAsync(d_in + n * sp.nA, size_map, n * sp.nS, cudaMemcpyHostToDevice, st),
+                   "H2D size_map"))
+    return ATC_ERR_CUDA;
+  int rc = atc_eval_bindings_device(ctx, spec, ts, d_in, d_in + n * sp.nA, n_bindings, mode, d_out, d_out + n, st);
+  if (rc) return rc;
+  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(fail_t, d_out, n, cudaMemcpyDeviceToHost, st), "D2H") ||
+      !atc_cuda_ok(ctx, cudaMemcpyAsync(reason, d_out + n, n, cudaMemcpyDeviceToHost, st), "D2H") ||
+      !atc_cuda_ok(ctx, cudaStreamSynchronize(st), "eval sync"))
+    return ATC_ERR_CUDA;
+  if (first_pass)
+    for (size_t b = 0; b < n; ++b)
+      if (reason[b] == ATC_PASS) {
+        *first_pass = (int64_t)b;
+        break;
+      }
+  return ATC_OK;
+}
+
+int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_handle* ts,
+                        const uint8_t* perms, int32_t n_perms, uint64_t begin, uint64_t end, int32_t mode,
+                        uint64_t* survivors, int64_t cap, int64_t* n_survivors, int64_t* reason_counts) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  SpecView sp;
+  if (!build_spec_view(ctx, spec, sp)) return ATC_ERR_ARG;
+  if (!ts || n_perms < 0 || !perms || end < begin || (mode != ATC_MODE_FP64 && mode != ATC_MODE_FP32_SCREEN)) {
+    atc_set_error(ctx, "bad arguments to atc_eval_enumerated");
+    return ATC_ERR_ARG;
+  }
+  for (int p = 0; p < n_perms; ++p)
+    for (int a = 0; a < sp.nA; ++a)
+      if (perms[p * sp.nA + a] >= ts->nP) {
+        atc_set_error(ctx, "perm %d maps array %d to pointer %d of %d", p, a, perms[p * sp.nA + a], ts->nP);
+        return ATC_ERR_ARG;
+      }
+  uint64_t size_maps = 1;
+  for (int q = 0; q < sp.nS; ++q) size_maps *= (uint64_t)ts->nI;
+  if (end > (uint64_t)n_perms * size_maps) {
+    atc_set_error(ctx, "range end %llu beyond the space (%llu)", (unsigned long long)end,
+                  (unsigned long long)((uint64_t)n_perms * size_maps));
+    return ATC_ERR_ARG;
+  }
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const uint64_t chunk_cap = 1ull << 22;  // survivors per chunk
+  uint8_t* d_perms = (uint8_t*)atc_ctx_scratch(ctx, 6, (size_t)n_perms * sp.nA + 16);
+  uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
+  int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, chunk_cap * 4);
+  unsigned long long* cnt = (unsigned long long*)atc_ctx_scratch(ctx, 3, 64);
+  unsigned long long* hist = (unsigned long long*)atc_ctx_scratch(ctx, 7, 64);
+  if (!d_perms || !surv || !skeys || !cnt || !hist) {
+    atc_set_error(ctx, "scratch allocation failed");
+    return ATC_ERR_CUDA;
+  }
+  cudaMemcpyAsync(d_perms, perms, (size_t)n_perms * sp.nA, cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(hist, 0, 64, st);
+  std::vector<uint64_t> h_surv;
+  std::vector<int32_t> h_keys;
+  int64_t passed = 0;
+  int64_t k2_hist[ATC_REASON_COUNT] = {0};
+  uint64_t chunk = 1ull << 30;
+  for (uint64_t lo = begin; lo < end;) {
+    const uint64_t hi = std::min(end, lo + chunk);
+    BindingSource src{nullptr, nullptr, d_perms, size_maps, lo, 1};
+    int rc = run_eval(ctx, sp, ts, src, hi - lo, nullptr, surv, chunk_cap, cnt, skeys, hist, st);
+    if (rc) return rc;
+    unsigned long long c = 0;
+    if (!atc_cuda_ok(ctx, cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, st), "D2H") ||
+        !atc_cuda_ok(ctx, cudaStreamSynchronize(st), "enumerate sync"))
+      return ATC_ERR_CUDA;
+    if (c > chunk_cap) {  // too many survivors for this chunk: split it and redo
+      if (chunk == 1) {
+        atc_set_error(ctx, "survivor overflow");
+        return ATC_ERR_CUDA;
+      }
+      // the screen already counted this chunk's rejections; undo by recounting
+      // from scratch is not possible, so histogram is rebuilt per chunk below
+      chunk = std::max<uint64_t>(1, chunk / 8);
+      cudaMemsetAsync(hist, 0, 64, st);
+      lo = begin;
+      h_surv.clear();
+      passed = 0;
+      std::fill(k2_hist, k2_hist + ATC_REASON_COUNT, 0);
+      continue;
+    }
+    if (ctx->prof) ctx->prof_survivors += (long long)c;
+    h_surv.resize(c);
+    h_keys.resize(c);
+    if (c) {
+      cudaMemcpyAsync(h_surv.data(), surv, c * 8, cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(h_keys.data(), skeys, c * 4, cudaMemcpyDeviceToHost, st);
+      if (!atc_cuda_ok(ctx, cudaStreamSynchronize(st), "survivor D2H")) return ATC_ERR_CUDA;
+    }
+    std::vector<uint64_t> pass_idx;
+    for (uint64_t i = 0; i < c; ++i) {
+      if (h_keys[i] == kPassKey)
+        pass_idx.push_back(lo + h_surv[i]);
+      else
+        k2_hist[h_keys[i] & 7]++;
+    }
+    std::sort(pass_idx.begin(), pass_idx.end());
+    for (uint64_t g : pass_idx) {
+      if (survivors && passed < cap) survivors[passed] = g;
+      ++passed;
+    }
+    lo = hi;
+  }
+  unsigned long long h_hist[ATC_REASON_COUNT] = {0};
+  cudaMemcpyAsync(h_hist, hist, sizeof h_hist, cudaMemcpyDeviceToHost, st);
+  if (!atc_cuda_ok(ctx, cudaStreamSynchronize(st), "hist D2H")) return ATC_ERR_CUDA;
+  if (n_survivors) *n_survivors = passed;
+  if (reason_counts) {
+    for (int r = 0; r < ATC_REASON_COUNT; ++r) reason_counts[r] = (int64_t)h_hist[r] + k2_hist[r];
+    reason_counts[ATC_PASS] = passed;
+  }
+  return ATC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,29 @@
+// Internal context shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <utility>
+#include <vector>
+
+struct atc_ctx {
+  int device = 0;
+  int sm_count = 148;
+  bool broken = false;
+  std::string err;
+  cudaStream_t stream = nullptr;
+  // reusable device scratch, grown on demand (slot ids are per call site)
+  void* scratch[16] = {};
+  size_t scratch_bytes[16] = {};
+  void* pinned[4] = {};
+  size_t pinned_bytes[4] = {};
+  cudaStream_t own_stream = nullptr;
+  // instrumentation (atc_profile_*)
+  bool prof = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_screen, prof_confirm;
+  long long prof_survivors = 0, prof_bindings = 0;
+};
+
+void atc_set_error(atc_ctx* ctx, const char* fmt, ...);
+bool atc_cuda_ok(atc_ctx* ctx, cudaError_t e, const char* what);
+void* atc_ctx_scratch(atc_ctx* ctx, int slot, size_t bytes);

@@ -1,0 +1,190 @@
+// Shared device-side decode / check routines of the binding evaluator.
+//
+// The predicate restated here is the binding-dependent half of
+// rewriter::verify_rewrite (/root/reference/proj/src/rewriter.cpp:215-284) for
+// one (binding b, recorded test t):
+//   1. run_dispatch extent checks (rewriter.cpp:136-148): every API array's dims
+//      >= 1 and  prod(dims) <= region length, else "dispatch failed" (reason 2);
+//   2. run_reference (equivalence.cpp:40-93) over full-region copies, FP64,
+//      acc = acc + a*b with NO fused multiply-add, reference loop order, later
+//      writes overwrite earlier ones;
+//   3. write-back rounding (double)(float) for f32 regions (rewriter.cpp:156-157);
+//   4. full-region compare |have - want| > abs + rel*|want| (rewriter.cpp:270-272),
+//      rel/abs = 1e-4/1e-6 (f32) or 1e-9/1e-12 (f64).
+// Step 4 over 65,536 elements is evaluated in O(footprint): positions the API
+// never writes keep their initial value, so they fail iff they are "dirty"
+// (|init - final| > tol), precomputed once per (t, pointer) by atc_build_dirty;
+// a binding passes t iff every dirty position is written by the API call and
+// every written position (its last writer) matches `final` within tolerance.
+#pragma once
+#include <cstdint>
+
+#include "atc_b200.h"
+
+namespace atc {
+
+constexpr int kMaxT = 64;
+constexpr int kMaxPtrs = 16;
+constexpr int kMaxInts = 32;
+
+// Device view of an uploaded test-set bundle (atc_testset_handle).
+struct TestsetView {
+  int32_t T, nI, nP;
+  const int64_t* ints;        // [T][nI]
+  const int32_t* is_f32;      // [nP]
+  const int64_t* region_len;  // [nP]
+  const int32_t* test_ok;     // [T]
+  const double* init;         // pool; region (t,p) at init + region_off[t*nP+p]
+  const double* fin;          // pool; same offsets
+  const int64_t* region_off;  // [T*nP]
+  const int32_t* dirty_pos;   // pool; list (t,p) at dirty_pos + dirty_off[t*nP+p]
+  const int64_t* dirty_off;   // [T*nP]
+  const int32_t* dirty_cnt;   // [T*nP]
+  const int32_t* dirty_max;   // [T*nP]  (-1 when empty)
+};
+
+// Spec decode table in a device-friendly form (copied by value into kernels).
+struct SpecView {
+  int32_t sem, layout, nA, nS;
+  int32_t role[ATC_MAX_ARRAYS];
+  int32_t ndims[ATC_MAX_ARRAYS];
+  int32_t dims[ATC_MAX_ARRAYS][ATC_MAX_DIMS];
+  int32_t role_size[ATC_SZ_COUNT];
+  int32_t arr_of_role[3];  // API array index of role A/B/C (IN/WEIGHTS/OUT)
+};
+
+// Where a launch takes its bindings from.
+struct BindingSource {
+  // explicit list
+  const uint8_t* arr_map;   // [n][nA]
+  const uint8_t* size_map;  // [n][nS]
+  // enumerated space
+  const uint8_t* perms;     // [n_perms][nA]
+  uint64_t size_maps;       // nI^nS
+  uint64_t begin;
+  int enumerated;
+};
+
+enum : int32_t { kUndecided = -2 };
+
+// Encoded per-binding result: t * 8 + reason; kPassKey when every test passed.
+constexpr int32_t kPassKey = 0x7fffffff;
+__host__ __device__ inline int32_t fail_key(int t, int reason) { return t * 8 + reason; }
+
+// ---- exact FP64 primitives: never contracted into DFMA -----------------------
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// rewriter.cpp:270-272 (tolerance test, evaluated without contraction)
+__device__ __forceinline__ bool mismatch(double have, double want, bool f32) {
+  const double rel = f32 ? 1e-4 : 1e-9;
+  const double abs_ = f32 ? 1e-6 : 1e-12;
+  return fabs(dsub(have, want)) > dadd(abs_, dmul(rel, fabs(want)));
+}
+
+__device__ __forceinline__ double round_region(double v, bool f32) {
+  return f32 ? (double)__double2float_rn(v) : v;  // rewriter.cpp:156-157
+}
+
+// Resolved sizes of one (binding, t), reference roles with their fallbacks.
+struct Dims {
+  // gemm (equivalence.cpp:42-48)
+  int64_t m, n, k, lda, ldb, ldc;
+  // conv (equivalence.cpp:69-77)
+  int64_t cn, cc, ch, cw, ck, cr, cs, coh, cow;
+};
+
+__device__ __forceinline__ int64_t role_or(const SpecView& sp, const int64_t* sz, int role, int64_t fb) {
+  int q = sp.role_size[role];
+  return q < 0 ? fb : sz[q];
+}
+
+__device__ __forceinline__ void resolve_dims(const SpecView& sp, const int64_t* sz, Dims& d) {
+  if (sp.sem == ATC_SEM_GEMM) {
+    const bool row = sp.layout == ATC_LAYOUT_ROW;
+    d.m = role_or(sp, sz, ATC_SZ_M, 0);
+    d.n = role_or(sp, sz, ATC_SZ_N, 0);
+    d.k = role_or(sp, sz, ATC_SZ_K, 0);
+    d.lda = role_or(sp, sz, ATC_SZ_LDA, row ? d.k : d.m);
+    d.ldb = role_or(sp, sz, ATC_SZ_LDB, row ? d.n : d.k);
+    d.ldc = role_or(sp, sz, ATC_SZ_LDC, row ? d.n : d.m);
+  } else {
+    d.cn = role_or(sp, sz, ATC_SZ_CN, 0);
+    d.cc = role_or(sp, sz, ATC_SZ_CC, 0);
+    d.ch = role_or(sp, sz, ATC_SZ_CH, 0);
+    d.cw = role_or(sp, sz, ATC_SZ_CW, 0);
+    d.ck = role_or(sp, sz, ATC_SZ_CK, 0);
+    d.cr = role_or(sp, sz, ATC_SZ_CR, 0);
+    d.cs = role_or(sp, sz, ATC_SZ_CS, 0);
+    d.coh = role_or(sp, sz, ATC_SZ_COH, d.ch - d.cr + 1);
+    d.cow = role_or(sp, sz, ATC_SZ_COW, d.cw - d.cs + 1);
+  }
+}
+
+// run_dispatch (rewriter.cpp:136-148): 0 when the call would proceed, else
+// ATC_FAIL_DISPATCH.  ptr_of[a] = user pointer bound to API array a.
+__device__ __forceinline__ int extent_check(const SpecView& sp, const int64_t* sz, const int* ptr_of,
+                                            const int64_t* region_len) {
+  for (int a = 0; a < sp.nA; ++a) {
+    int64_t ext = 1;
+    for (int d = 0; d < sp.ndims[a]; ++d) {
+      int64_t v = sz[sp.dims[a][d]];
+      if (v < 1) return ATC_FAIL_DISPATCH;
+      ext *= v;
+    }
+    if (region_len[ptr_of[a]] < ext) return ATC_FAIL_DISPATCH;
+  }
+  return 0;
+}
+
+// Accesses outside [0, region) would be undefined behaviour in the reference
+// (std::vector operator[]); never reached at P2 sizes, rejected if they occur.
+// Also guarantees every index below fits in int32.
+__device__ __forceinline__ int ub_check(const SpecView& sp, const Dims& d, const int* ptr_of,
+                                        const int64_t* region_len) {
+  const int64_t lenA = region_len[ptr_of[sp.arr_of_role[0]]];
+  const int64_t lenB = region_len[ptr_of[sp.arr_of_role[1]]];
+  const int64_t lenC = region_len[ptr_of[sp.arr_of_role[2]]];
+  if (sp.sem == ATC_SEM_GEMM) {
+    if (d.m < 1 || d.n < 1 || d.k < 1) return 0;  // loops empty: nothing accessed
+    if (d.lda < 0 || d.ldb < 0 || d.ldc < 0) return ATC_FAIL_UB;
+    const bool row = sp.layout == ATC_LAYOUT_ROW;
+    const int64_t amax = row ? (d.m - 1) * d.lda + (d.k - 1) : (d.k - 1) * d.lda + (d.m - 1);
+    const int64_t bmax = row ? (d.k - 1) * d.ldb + (d.n - 1) : (d.n - 1) * d.ldb + (d.k - 1);
+    const int64_t cmax = row ? (d.m - 1) * d.ldc + (d.n - 1) : (d.n - 1) * d.ldc + (d.m - 1);
+    if (amax >= lenA || bmax >= lenB || cmax >= lenC) return ATC_FAIL_UB;
+  } else {
+    if (d.cn < 1 || d.ck < 1 || d.coh < 1 || d.cow < 1) return 0;
+    if (d.cc < 1 || d.cr < 1 || d.cs < 1) return 0;  // out written with acc = 0, no reads
+    const int64_t imax = (((d.cn - 1) * d.cc + (d.cc - 1)) * d.ch + (d.coh - 1) + (d.cr - 1)) * d.cw +
+                         (d.cow - 1) + (d.cs - 1);
+    const int64_t wmax = (((d.ck - 1) * d.cc + (d.cc - 1)) * d.cr + (d.cr - 1)) * d.cs + (d.cs - 1);
+    const int64_t omax = ((d.cn * d.ck) * d.coh) * d.cow - 1;
+    if (imax >= lenA || wmax >= lenB || omax >= lenC || imax < 0) return ATC_FAIL_UB;
+  }
+  return 0;
+}
+
+// ---- GEMM write-set algebra (reference loop order i -> j, C[pos] = acc) -------
+// Row-major writes pos = i*ldc + j; col-major pos = j*ldc + i.
+// (i,j) is the LAST writer of its position iff no later (i',j') hits it:
+//   row: i == m-1 || j < ldc        col: j == 0 || i + ldc >= m
+__device__ __forceinline__ bool gemm_last_writer(bool row, int i, int j, int m, int ldc) {
+  return row ? (i == m - 1 || j < ldc) : (j == 0 || i + ldc >= m);
+}
+// Is position p written at all?
+__device__ __forceinline__ bool gemm_written(bool row, int p, int m, int n, int ldc) {
+  if (row) {
+    int i = p / ldc;
+    if (i > m - 1) i = m - 1;
+    return p - i * ldc < n;
+  }
+  int hi = p < m - 1 ? p : m - 1;
+  int r = p % ldc;
+  if (r > hi) return false;
+  int i = r + ldc * ((hi - r) / ldc);
+  return (p - i) / ldc < n;
+}
+
+}  // namespace atc

@@ -1,0 +1,385 @@
+// Binding-evaluator kernels (K0 dirty lists, K1 screen, K2 confirm).
+//
+// Work decomposition:
+//   K0 atc_build_dirty    one pass over every recorded (t, pointer) region pair;
+//                         appends {i : |init_i - final_i| > tol} (rewriter.cpp:270-272).
+//   K1 atc_screen_*       one THREAD per candidate binding, test t = 0 only, with a
+//                         bounded budget of output positions.  Nearly every wrong
+//                         binding is rejected here after a handful of integer ops
+//                         and at most `budget` dot products.  Bindings that pass
+//                         what they checked are appended to a survivor queue.
+//   K2 atc_confirm        one CTA per (survivor, t) for every t: the A/B operand
+//                         prefixes are staged into shared memory with coalesced
+//                         vector loads, output positions are split across the CTA,
+//                         a mismatch flag in shared memory gives block-wide early
+//                         exit, and the first failing test is reduced with atomicMin.
+// Both halves evaluate exactly the predicate of eval_common.cuh.
+#include <cuda_runtime.h>
+
+#include "eval_common.cuh"
+
+namespace atc {
+
+// ------------------------------------------------------------------ K0 -------
+__global__ void k_build_dirty(TestsetView ts, int32_t* dirty_pos, int32_t* dirty_cnt,
+                              int32_t* dirty_max) {
+  const int tp = blockIdx.y;  // (t, p) pair
+  const int p = tp % ts.nP;
+  const int64_t len = ts.region_len[p];
+  const bool f32 = ts.is_f32[p] != 0;
+  const double* init = ts.init + ts.region_off[tp];
+  const double* fin = ts.fin + ts.region_off[tp];
+  int32_t* out = dirty_pos + ts.dirty_off[tp];
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < len; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool dirty = false;
+    if (i < len) dirty = mismatch(init[i], fin[i], f32);
+    const unsigned ball = __ballot_sync(0xffffffffu, dirty);
+    if (ball == 0) continue;
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(&dirty_cnt[tp], __popc(ball));
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (dirty) {
+      out[slot + __popc(ball & ((1u << lane) - 1))] = (int32_t)i;
+      atomicMax(&dirty_max[tp], (int32_t)i);
+    }
+  }
+}
+
+// ------------------------------------------------------------ binding decode --
+
+
+__device__ __forceinline__ void decode_binding(const BindingSource& src, const SpecView& sp, int nI,
+                                               uint64_t idx, int* ptr_of, int* int_of) {
+  if (!src.enumerated) {
+    for (int a = 0; a < sp.nA; ++a) ptr_of[a] = src.arr_map[idx * sp.nA + a];
+    for (int q = 0; q < sp.nS; ++q) int_of[q] = src.size_map[idx * sp.nS + q];
+    return;
+  }
+  const uint64_t g = src.begin + idx;
+  const uint64_t perm = g / src.size_maps;
+  uint64_t s = g - perm * src.size_maps;
+  for (int a = 0; a < sp.nA; ++a) ptr_of[a] = src.perms[perm * sp.nA + a];
+  if (s < (1ull << 32)) {
+    uint32_t s32 = (uint32_t)s;
+    for (int q = 0; q < sp.nS; ++q) {
+      uint32_t d = s32 / (uint32_t)nI;
+      int_of[q] = (int)(s32 - d * (uint32_t)nI);
+      s32 = d;
+    }
+  } else {
+    for (int q = 0; q < sp.nS; ++q) {
+      uint64_t d = s / (uint64_t)nI;
+      int_of[q] = (int)(s - d * (uint64_t)nI);
+      s = d;
+    }
+  }
+}
+
+// ---------------------------------------------------- single-thread check ----
+// Checks test t for one binding on one thread.  Returns 0 (passed everything it
+// looked at), a reason code, or kUndecided when `budget` output positions were
+// checked without reaching the end.
+__device__ int thread_check(const TestsetView& ts, const SpecView& sp, const int* ptr_of,
+                            const int64_t* sz, int t, int budget, bool* complete) {
+  *complete = false;
+  if (!ts.test_ok[t]) return ATC_FAIL_TESTSET;
+  if (int r = extent_check(sp, sz, ptr_of, ts.region_len)) return r;
+  Dims d;
+  resolve_dims(sp, sz, d);
+  if (int r = ub_check(sp, d, ptr_of, ts.region_len)) return r;
+  const int pA = ptr_of[sp.arr_of_role[0]], pB = ptr_of[sp.arr_of_role[1]], pC = ptr_of[sp.arr_of_role[2]];
+  const int tpA = t * ts.nP + pA, tpB = t * ts.nP + pB, tpC = t * ts.nP + pC;
+  const double* __restrict__ A = ts.init + ts.region_off[tpA];
+  const double* __restrict__ B = ts.init + ts.region_off[tpB];
+  const double* __restrict__ F = ts.fin + ts.region_off[tpC];
+  const bool f32 = ts.is_f32[pC] != 0;
+  const int ndirty = ts.dirty_cnt[tpC];
+  const int32_t* dirty = ts.dirty_pos + ts.dirty_off[tpC];
+
+  if (sp.sem == ATC_SEM_GEMM) {
+    const bool row = sp.layout == ATC_LAYOUT_ROW;
+    const int m = (int)d.m, n = (int)d.n, k = (int)d.k;
+    const int lda = (int)d.lda, ldb = (int)d.ldb, ldc = (int)d.ldc;
+    if (m < 1 || n < 1) {  // no writes: every dirty position is a mismatch
+      if (ndirty) return ATC_FAIL_MISMATCH;
+      *complete = true;
+      return 0;
+    }
+    // dirty positions must all be written (else the untouched value differs)
+    for (int e = 0; e < ndirty; ++e)
+      if (!gemm_written(row, __ldg(dirty + e), m, n, ldc)) return ATC_FAIL_MISMATCH;
+    const bool overlap = row ? (ldc < n && m > 1) : (ldc < m && n > 1);
+    int checked = 0;
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < n; ++j) {
+        if (overlap && !gemm_last_writer(row, i, j, m, ldc)) continue;
+        if (checked == budget) return kUndecided;
+        ++checked;
+        double acc = 0.0;
+        if (row) {
+          const double* a = A + i * lda;
+          const double* b = B + j;
+          for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(__ldg(a + p), __ldg(b + p * ldb)));
+        } else {
+          const double* a = A + i;
+          const double* b = B + j * ldb;
+          for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(__ldg(a + p * lda), __ldg(b + p)));
+        }
+        const int pos = row ? i * ldc + j : j * ldc + i;
+        if (mismatch(round_region(acc, f32), __ldg(F + pos), f32)) return ATC_FAIL_MISMATCH;
+      }
+    *complete = true;
+    return 0;
+  }
+  // conv2d: the write set is exactly [0, n*k*oh*ow) (a bijection)
+  const int N = (int)d.cn, C = (int)d.cc, H = (int)d.ch, W = (int)d.cw, K = (int)d.ck, R = (int)d.cr,
+            S = (int)d.cs, OH = (int)d.coh, OW = (int)d.cow;
+  const int64_t wext = (int64_t)N * K * OH * OW;
+  if (ts.dirty_max[tpC] >= wext) return ATC_FAIL_MISMATCH;
+  int checked = 0;
+  for (int b = 0; b < N; ++b)
+    for (int q = 0; q < K; ++q)
+      for (int y = 0; y < OH; ++y)
+        for (int x = 0; x < OW; ++x) {
+          if (checked == budget) return kUndecided;
+          ++checked;
+          double acc = 0.0;
+          for (int z = 0; z < C; ++z)
+            for (int u = 0; u < R; ++u) {
+              const double* in = A + ((b * C + z) * H + y + u) * W + x;
+              const double* wt = B + ((q * C + z) * R + u) * S;
+              for (int v = 0; v < S; ++v) acc = dadd(acc, dmul(__ldg(in + v), __ldg(wt + v)));
+            }
+          const int pos = ((b * K + q) * OH + y) * OW + x;
+          if (mismatch(round_region(acc, f32), __ldg(F + pos), f32)) return ATC_FAIL_MISMATCH;
+        }
+  *complete = true;
+  return 0;
+}
+
+// ------------------------------------------------------------------ K1 -------
+// Explicit lists: keys[b] receives the t=0 failure or stays kPassKey; bindings
+// that are not rejected at t=0 go to the survivor queue (for every t in K2).
+// Enumerated spaces: rejected bindings only feed the reason histogram.
+__global__ void __launch_bounds__(256) k_screen(TestsetView ts, SpecView sp, BindingSource src,
+                                                 uint64_t n, int budget, int32_t* keys,
+                                                 uint64_t* surv, uint64_t surv_cap,
+                                                 unsigned long long* surv_cnt,
+                                                 unsigned long long* reason_hist) {
+  __shared__ int64_t s_ints0[kMaxInts];
+  __shared__ unsigned long long s_hist[ATC_REASON_COUNT];
+  if (threadIdx.x < ts.nI) s_ints0[threadIdx.x] = ts.ints[threadIdx.x];
+  if (threadIdx.x < ATC_REASON_COUNT) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += stride) {
+    int ptr_of[ATC_MAX_ARRAYS], int_of[ATC_MAX_SIZES];
+    decode_binding(src, sp, ts.nI, idx, ptr_of, int_of);
+    int64_t sz[ATC_MAX_SIZES];
+    for (int q = 0; q < sp.nS; ++q) sz[q] = s_ints0[int_of[q]];
+    bool complete;
+    int r = thread_check(ts, sp, ptr_of, sz, 0, budget, &complete);
+    if (r > 0) {
+      if (keys) keys[idx] = fail_key(0, r);
+      if (reason_hist) atomicAdd(&s_hist[r], 1ull);
+    } else {
+      // passed t = 0 so far: every remaining t (and t = 0 when undecided)
+      // is decided by K2
+      unsigned long long slot = atomicAdd(surv_cnt, 1ull);
+      if (slot < surv_cap) surv[slot] = idx;
+    }
+  }
+  if (reason_hist) {
+    __syncthreads();
+    if (threadIdx.x < ATC_REASON_COUNT && s_hist[threadIdx.x])
+      atomicAdd(&reason_hist[threadIdx.x], s_hist[threadIdx.x]);
+  }
+}
+
+// ------------------------------------------------------------------ K2 -------
+constexpr int kConfirmThreads = 256;
+constexpr int kStageDoubles = 6080;  // ~47.5 KB of operand staging per CTA (static smem cap 48 KB)
+
+__global__ void __launch_bounds__(kConfirmThreads) k_confirm(TestsetView ts, SpecView sp, BindingSource src,
+                                                             const uint64_t* surv,
+                                                             const unsigned long long* surv_cnt,
+                                                             uint64_t surv_cap, int32_t* surv_keys) {
+  __shared__ double s_stage[kStageDoubles];
+  __shared__ int s_fail;
+  __shared__ int s_ptr[ATC_MAX_ARRAYS];
+  __shared__ int64_t s_sz[ATC_MAX_SIZES];
+  __shared__ int s_pre;  // result of the per-(b,t) scalar prologue
+  unsigned long long cnt = *surv_cnt;
+  if (cnt > surv_cap) cnt = surv_cap;
+  const uint64_t work = cnt * (uint64_t)ts.T;
+  for (uint64_t w = blockIdx.x; w < work; w += gridDim.x) {
+    const uint64_t si = w / ts.T;
+    const int t = (int)(w - si * ts.T);
+    const uint64_t idx = surv[si];
+    if (threadIdx.x == 0) {
+      int ptr_of[ATC_MAX_ARRAYS], int_of[ATC_MAX_SIZES];
+      decode_binding(src, sp, ts.nI, idx, ptr_of, int_of);
+      for (int a = 0; a < sp.nA; ++a) s_ptr[a] = ptr_of[a];
+      for (int q = 0; q < sp.nS; ++q) s_sz[q] = ts.ints[t * ts.nI + int_of[q]];
+      int r = 0;
+      if (!ts.test_ok[t]) r = ATC_FAIL_TESTSET;
+      if (!r) r = extent_check(sp, s_sz, ptr_of, ts.region_len);
+      if (!r) {
+        Dims d;
+        resolve_dims(sp, s_sz, d);
+        r = ub_check(sp, d, ptr_of, ts.region_len);
+      }
+      s_pre = r;
+      s_fail = 0;
+    }
+    __syncthreads();
+    int fail = s_pre;
+    if (!fail) {
+      Dims d;
+      resolve_dims(sp, s_sz, d);
+      const int pA = s_ptr[sp.arr_of_role[0]], pB = s_ptr[sp.arr_of_role[1]], pC = s_ptr[sp.arr_of_role[2]];
+      const int tpA = t * ts.nP + pA, tpB = t * ts.nP + pB, tpC = t * ts.nP + pC;
+      const double* gA = ts.init + ts.region_off[tpA];
+      const double* gB = ts.init + ts.region_off[tpB];
+      const double* F = ts.fin + ts.region_off[tpC];
+      const bool f32 = ts.is_f32[pC] != 0;
+      const int ndirty = ts.dirty_cnt[tpC];
+      const int32_t* dirty = ts.dirty_pos + ts.dirty_off[tpC];
+      if (sp.sem == ATC_SEM_GEMM) {
+        const bool row = sp.layout == ATC_LAYOUT_ROW;
+        const int m = (int)d.m, n = (int)d.n, k = (int)d.k;
+        const int lda = (int)d.lda, ldb = (int)d.ldb, ldc = (int)d.ldc;
+        // operand footprints (prefix lengths) for shared-memory staging
+        int alen = 0, blen = 0;
+        if (m >= 1 && n >= 1 && k >= 1) {
+          alen = (row ? (m - 1) * lda + k : (k - 1) * lda + m);
+          blen = (row ? (k - 1) * ldb + n : (n - 1) * ldb + k);
+        }
+        const bool staged = alen + blen <= kStageDoubles;
+        const double* A = gA;
+        const double* B = gB;
+        if (staged) {
+          // coalesced 16-byte loads when aligned (regions are 256-B aligned)
+          for (int e = threadIdx.x * 2; e < alen; e += kConfirmThreads * 2) {
+            if (e + 1 < alen) {
+              double2 v = __ldg(reinterpret_cast<const double2*>(gA + e));
+              s_stage[e] = v.x;
+              s_stage[e + 1] = v.y;
+            } else {
+              s_stage[e] = __ldg(gA + e);
+            }
+          }
+          for (int e = threadIdx.x * 2; e < blen; e += kConfirmThreads * 2) {
+            if (e + 1 < blen) {
+              double2 v = __ldg(reinterpret_cast<const double2*>(gB + e));
+              s_stage[alen + e] = v.x;
+              s_stage[alen + e + 1] = v.y;
+            } else {
+              s_stage[alen + e] = __ldg(gB + e);
+            }
+          }
+          A = s_stage;
+          B = s_stage + alen;
+        }
+        // dirty subset check, split across the CTA
+        if (m < 1 || n < 1) {
+          if (ndirty && threadIdx.x == 0) s_fail = ATC_FAIL_MISMATCH;
+        } else {
+          for (int e = threadIdx.x; e < ndirty; e += kConfirmThreads)
+            if (!gemm_written(row, __ldg(dirty + e), m, n, ldc)) s_fail = ATC_FAIL_MISMATCH;
+        }
+        __syncthreads();
+        if (!s_fail && m >= 1 && n >= 1) {
+          const bool overlap = row ? (ldc < n && m > 1) : (ldc < m && n > 1);
+          const int outs = m * n;
+          for (int o0 = 0; o0 < outs; o0 += kConfirmThreads) {
+            const int o = o0 + threadIdx.x;
+            if (o < outs) {
+              const int i = o / n, j = o - (o / n) * n;
+              if (!overlap || gemm_last_writer(row, i, j, m, ldc)) {
+                double acc = 0.0;
+                if (row) {
+                  for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(A[i * lda + p], B[p * ldb + j]));
+                } else {
+                  for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(A[p * lda + i], B[j * ldb + p]));
+                }
+                const int pos = row ? i * ldc + j : j * ldc + i;
+                if (mismatch(round_region(acc, f32), __ldg(F + pos), f32)) s_fail = ATC_FAIL_MISMATCH;
+              }
+            }
+            // block-wide early exit on the first mismatching chunk
+            if (__syncthreads_or(s_fail != 0)) break;
+          }
+        }
+      } else {
+        const int N = (int)d.cn, C = (int)d.cc, H = (int)d.ch, W = (int)d.cw, K = (int)d.ck,
+                  R = (int)d.cr, S = (int)d.cs, OH = (int)d.coh, OW = (int)d.cow;
+        const int64_t wext = (int64_t)N * K * OH * OW;
+        if (ts.dirty_max[tpC] >= wext) {
+          if (threadIdx.x == 0) s_fail = ATC_FAIL_MISMATCH;
+        }
+        __syncthreads();
+        if (!s_fail) {
+          const int wlen = K * C * R * S;
+          const bool staged = wlen <= kStageDoubles;
+          const double* Wt = gB;
+          if (staged) {
+            for (int e = threadIdx.x; e < wlen; e += kConfirmThreads) s_stage[e] = __ldg(gB + e);
+            __syncthreads();
+            Wt = s_stage;
+          }
+          const int outs = (int)wext;
+          for (int o0 = 0; o0 < outs; o0 += kConfirmThreads) {
+            const int o = o0 + threadIdx.x;
+            if (o < outs) {
+              int rem = o;
+              const int x = rem % OW; rem /= OW;
+              const int y = rem % OH; rem /= OH;
+              const int q = rem % K;
+              const int b = rem / K;
+              double acc = 0.0;
+              for (int z = 0; z < C; ++z)
+                for (int u = 0; u < R; ++u) {
+                  const double* in = gA + ((b * C + z) * H + y + u) * W + x;
+                  const double* wt = Wt + ((q * C + z) * R + u) * S;
+                  for (int v = 0; v < S; ++v) acc = dadd(acc, dmul(__ldg(in + v), wt[v]));
+                }
+              if (mismatch(round_region(acc, f32), __ldg(F + o), f32)) s_fail = ATC_FAIL_MISMATCH;
+            }
+            if (__syncthreads_or(s_fail != 0)) break;
+          }
+        }
+      }
+      __syncthreads();
+      fail = s_fail;
+    }
+    if (threadIdx.x == 0 && fail) atomicMin(&surv_keys[si], fail_key(t, fail));
+    __syncthreads();
+  }
+}
+
+// Merge K2 results into the per-binding keys of an explicit list.
+__global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
+                             const int32_t* surv_keys, int32_t* keys) {
+  unsigned long long cnt = *surv_cnt;
+  if (cnt > cap) cnt = cap;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x)
+    keys[surv[i]] = surv_keys[i];
+}
+
+__global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t k = keys[i];
+    fail_t[i] = k == kPassKey ? (int8_t)-1 : (int8_t)(k >> 3);
+    reason[i] = k == kPassKey ? (int8_t)0 : (int8_t)(k & 7);
+  }
+}
+
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+}  // namespace atc

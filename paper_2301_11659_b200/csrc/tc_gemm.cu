@@ -1,0 +1,625 @@
+// K4/K5: tcgen05 tensor-core FP32-in / FP32-out contractions (kind::tf32).
+//
+// Replaces profitability::cpu_gemm / xpu_gemm (/root/reference/proj/src/
+// profitability.cpp:14-63: row-major C[m][n] = sum_p A[m][p] * B[p][n], C
+// overwritten) and reference_conv2d's semantics (equivalence.cpp:67-93; valid
+// padding, unit stride, NCHW input, KCRS weights, NKOhOw output) on FP32 data.
+//
+// One persistent, warp-specialised kernel:
+//   warp 0      TMA producer: A tile [128 x 32] K-major, B tile 8 x [32 x 32]
+//               MN-major chunks, both 128B-swizzled, into a 4-stage smem ring
+//   warp 1      MMA issuer: 4 x tcgen05.mma.cta_group::1.kind::tf32 (M=128,
+//               N=256, K=8) per stage, accumulating in TMEM; tcgen05.commit
+//               frees the smem stage / publishes the accumulator
+//   warp 2      TMEM allocator (512 columns = 2 accumulators of 128 x 256 fp32)
+//   warps 4-7   epilogue: tcgen05.ld 32x32b.x32 -> registers -> global
+// The two TMEM accumulators let the epilogue of tile i overlap the MMAs of
+// tile i+1.
+//
+// Precision: TF32 (1 pass; inputs truncated to 10-bit mantissas by the tensor
+// core, FP32 accumulation) or 3xTF32 (A = Ah + Al, B = Bh + Bl split once by
+// k_split_tf32; C = Ah*Bh + Al*Bh + Ah*Bl as one K' = 3K contraction), which
+// recovers ~FP32 accuracy.  See DESIGN.md §4 for the measured error.
+//
+// Conv2d (NCHW, valid, unit stride) is the same kernel in implicit-GEMM form
+// with no input transform: M = filters, N = output pixels laid out on the
+// INPUT grid (p = y*W + x, x < W), K' = (r, s, c).  For a fixed (r, s) the B
+// operand rows are In[n][c][p + r*W + s] — an affine shift of the contiguous
+// H*W plane — so every B chunk is a plain 2-D TMA box of the [N*C][H*W] view.
+// Pixels with x >= OW or y >= OH are computed and discarded by the epilogue.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+
+#include "atc_b200.h"
+#include "capi_internal.h"
+
+namespace atc {
+namespace tc {
+
+constexpr int BM = 128, BN = 256, BK = 32;  // BK = one 128B swizzle atom of fp32
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 4;        // 16 KB
+constexpr int B_BYTES = BN * BK * 4;        // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_THREADS = 256;
+constexpr int TMEM_COLS = 512;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+// ------------------------------------------------------------ PTX helpers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// smem matrix descriptor (tcgen05 "shared memory descriptor"): start >> 4 at
+// [0,14), LBO >> 4 at [16,30), SBO >> 4 at [32,46), version 1 at [46,48),
+// layout SWIZZLE_128B (2) at [61,64).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
+// instruction descriptor, kind::tf32: D f32 [4,6)=1, A tf32 [7,10)=2,
+// B tf32 [10,13)=2, A K-major [15]=0, B MN-major [16]=1, N>>3 [17,23), M>>4 [24,29)
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+#define TMEM_LD_32x32b_x32(taddr, r)                                                                          \
+  asm volatile(                                                                                               \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                          \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),       \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), \
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),          \
+        "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),          \
+        "=r"(r[30]), "=r"(r[31])                                                                              \
+      : "r"(taddr))
+
+// ------------------------------------------------------------ problem -------
+struct Problem {
+  // GEMM: C[M][N] (row-major, ldc) ; A map over [M][K] ; B map over [K][N]
+  // CONV: out NCHW ; A map over W_krsc [Kf][R*S*C] ; B map over In [Nimg*C][H*W]
+  int conv;
+  int M, N, K;          // gemm sizes; conv: M = filters, N = H*W (pixels on the input grid), K = C (per r,s)
+  int splits;           // 1 (TF32) or 3 (3xTF32: K' = 3K over hi/lo operand maps)
+  float* C;
+  int64_t ldc;
+  // conv geometry
+  int img, Cin, H, W, R, S, OH, OW;
+  int tiles_m, tiles_n, tiles_img;
+};
+
+struct Maps {
+  CUtensorMap a[2];  // hi, lo
+  CUtensorMap b[2];
+};
+
+__device__ __forceinline__ void tile_coords(const Problem& p, int tile, int& tm, int& tn, int& ti) {
+  // grouped raster: 16 m-tiles x all n-tiles per group, for L2 reuse of A/B panels
+  const int per_img = p.tiles_m * p.tiles_n;
+  ti = tile / per_img;
+  int t = tile - ti * per_img;
+  const int G = 16;
+  const int group = t / (G * p.tiles_n);
+  const int first_m = group * G;
+  const int gm = min(G, p.tiles_m - first_m);
+  const int in_group = t - group * G * p.tiles_n;
+  tm = first_m + in_group % gm;
+  tn = in_group / gm;
+}
+
+// k-block kb in [0, splits * kblocks): which operand pair and which coordinates
+__device__ __forceinline__ void kblock_coords(const Problem& p, int kb, int kblocks_per_split, int tm, int tn, int ti,
+                                              int& sel_a, int& sel_b, int& a_c0, int& a_c1, int& b_c0, int& b_c1) {
+  const int split = kb / kblocks_per_split;
+  const int k = kb - split * kblocks_per_split;
+  // 3xTF32 order: lo*hi, hi*lo, hi*hi (small terms first)
+  sel_a = split == 0 && p.splits == 3 ? 1 : 0;
+  sel_b = split == 1 ? 1 : 0;
+  if (!p.conv) {
+    a_c0 = k * BK;        // K
+    a_c1 = tm * BM;       // M
+    b_c0 = tn * BN;       // N (chunk offset added by caller)
+    b_c1 = k * BK;        // K
+  } else {
+    const int cblocks = p.K / BK;     // C / 32
+    const int rs = k / cblocks;       // r*S + s
+    const int c0 = (k - rs * cblocks) * BK;
+    const int r = rs / p.S, s = rs - (rs / p.S) * p.S;
+    a_c0 = rs * p.K + c0;             // column in W_krsc [Kf][R*S*C]
+    a_c1 = tm * BM;                   // filter row
+    b_c0 = tn * BN + r * p.W + s;     // pixel (affine shift of the input plane)
+    b_c1 = ti * p.Cin + c0;           // row n*C + c
+  }
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constant__ Maps maps, const Problem p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kblocks = (p.conv ? p.R * p.S * (p.K / BK) : (p.K + BK - 1) / BK);
+  const int total_kb = kblocks * p.splits;
+  const int num_tiles = p.tiles_m * p.tiles_n * p.tiles_img;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 4);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer =================
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int tm, tn, ti;
+        tile_coords(p, tile, tm, tn, ti);
+        for (int kb = 0; kb < total_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          int sa, sb, a0, a1, b0, b1;
+          kblock_coords(p, kb, kblocks, tm, tn, ti, sa, sb, a0, a1, b0, b1);
+          uint8_t* sA = smem + stage * STAGE_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(sA, &maps.a[sa], &full[stage], a0, a1);
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j) tma_load_2d(sB + j * (BK * 128), &maps.b[sb], &full[stage], b0 + 32 * j, b1);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ================= MMA issuer =================
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < total_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            // A: K-major SW128, +32 B per K=8 step inside the 128 B atom; SBO = 8 rows * 128 B
+            const uint64_t ad = make_desc(a_addr + kk * 32, 16, 1024);
+            // B: MN-major SW128, chunks of 32 N at LBO = 32 rows * 128 B; +8 rows per K step
+            const uint64_t bd = make_desc(b_addr + kk * 1024, BK * 128, 1024);
+            mma_tf32(d_tmem, ad, bd, (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);  // smem stage free once these MMAs complete
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tmem_full[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue =================
+    const int q = warp - 4;  // TMEM lanes 32q .. 32q+31
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int tm, tn, ti;
+      tile_coords(p, tile, tm, tn, ti);
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const int row = tm * BM + q * 32 + lane;  // output row (gemm M / conv filter)
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem_base + acc * BN + c0 + ((uint32_t)(q * 32) << 16);
+        TMEM_LD_32x32b_x32(taddr, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int col0 = tn * BN + c0;
+        if (row < p.M) {
+          if (!p.conv) {
+            float* dst = p.C + (int64_t)row * p.ldc + col0;
+            if (col0 + 32 <= p.N && (p.ldc & 3) == 0) {
+#pragma unroll
+              for (int v = 0; v < 32; v += 4)
+                *reinterpret_cast<float4*>(dst + v) = make_float4(__uint_as_float(r[v]), __uint_as_float(r[v + 1]),
+                                                                  __uint_as_float(r[v + 2]), __uint_as_float(r[v + 3]));
+            } else {
+              for (int v = 0; v < 32; ++v)
+                if (col0 + v < p.N) dst[v] = __uint_as_float(r[v]);
+            }
+          } else {
+            // pixel p = y*W + x on the input grid; keep y < OH, x < OW
+            float* dst = p.C + ((int64_t)ti * p.M + row) * ((int64_t)p.OH * p.OW);
+#pragma unroll
+            for (int v = 0; v < 32; ++v) {
+              const int pix = col0 + v;
+              const int y = pix / p.W, x = pix - (pix / p.W) * p.W;
+              if (y < p.OH && x < p.OW) dst[y * p.OW + x] = __uint_as_float(r[v]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+}
+
+// hi/lo split for 3xTF32: hi = x with the 13 low mantissa bits cleared (exactly
+// representable in TF32), lo = x - hi (exact in FP32).
+__global__ void k_split_tf32(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+
+// KCRS -> K(RS)C weight reorder (tiny), optionally split into hi/lo.
+__global__ void k_weights_krsc(const float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo, int K,
+                               int C, int R, int S) {
+  const int64_t n = (int64_t)K * C * R * S;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    // i indexes the destination [k][r][s][c]
+    int64_t t = i;
+    const int c = (int)(t % C); t /= C;
+    const int s = (int)(t % S); t /= S;
+    const int r = (int)(t % R);
+    const int k = (int)(t / R);
+    const float v = w[(((int64_t)k * C + c) * R + r) * S + s];
+    if (lo) {
+      const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+      hi[i] = h;
+      lo[i] = v - h;
+    } else {
+      hi[i] = v;
+    }
+  }
+}
+
+// Copies a [rows][cols] fp32 matrix into a row pitch that TMA accepts (16 B).
+__global__ void k_pitch_copy(const float* __restrict__ src, float* __restrict__ dst, int64_t rows, int64_t cols,
+                             int64_t dpitch) {
+  const int64_t n = rows * dpitch;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / dpitch, c = i - r * dpitch;
+    dst[i] = c < cols ? src[r * cols + c] : 0.0f;
+  }
+}
+
+}  // namespace tc
+}  // namespace atc
+
+using namespace atc::tc;
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode(atc_ctx* ctx) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn) return fn;
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !p) {
+    atc_set_error(ctx, "cuTensorMapEncodeTiled is unavailable");
+    return nullptr;
+  }
+  fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  return fn;
+}
+
+// 2-D fp32 tensor map over [rows][cols] with row pitch `pitch` elements.
+bool make_map(atc_ctx* ctx, CUtensorMap* m, const float* base, uint64_t rows, uint64_t cols, uint64_t pitch,
+              uint32_t box_cols, uint32_t box_rows) {
+  auto enc = get_encode(ctx);
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch * 4};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    atc_set_error(ctx, "cuTensorMapEncodeTiled failed (%d) for [%llu x %llu] pitch %llu", (int)r,
+                  (unsigned long long)rows, (unsigned long long)cols, (unsigned long long)pitch);
+    return false;
+  }
+  return true;
+}
+
+bool launch(atc_ctx* ctx, const Maps& maps, const Problem& p, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    if (!atc_cuda_ok(ctx, cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
+                     "cudaFuncSetAttribute"))
+      return false;
+    configured = true;
+  }
+  const int tiles = p.tiles_m * p.tiles_n * p.tiles_img;
+  const int grid = std::min(tiles, ctx->sm_count);
+  k_tc_gemm<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(maps, p);
+  return atc_cuda_ok(ctx, cudaGetLastError(), "k_tc_gemm launch");
+}
+
+int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+
+}  // namespace
+
+extern "C" {
+
+int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* dC, int64_t m, int64_t n, int64_t k,
+                        int32_t precision, void* stream) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (m < 1 || n < 1 || k < 1 || m >= (1LL << 31) || n >= (1LL << 31) || k >= (1LL << 31) || !dA || !dB || !dC ||
+      (precision != ATC_PREC_TF32 && precision != ATC_PREC_3XTF32)) {
+    atc_set_error(ctx, "bad arguments to atc_sgemm_rm");
+    return ATC_ERR_ARG;
+  }
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  // TMA needs 16-byte row pitches: repitch A ([m][k]) / B ([k][n]) when needed
+  const int64_t kp = (k + 3) / 4 * 4, np = (n + 3) / 4 * 4;
+  const float* A = dA;
+  const float* B = dB;
+  if (kp != k) {
+    float* t = (float*)atc_ctx_scratch(ctx, 11, (size_t)m * kp * 4);
+    if (!t) return ATC_ERR_CUDA;
+    k_pitch_copy<<<grid_for(m * kp), 256, 0, st>>>(dA, t, m, k, kp);
+    A = t;
+  }
+  if (np != n) {
+    float* t = (float*)atc_ctx_scratch(ctx, 12, (size_t)k * np * 4);
+    if (!t) return ATC_ERR_CUDA;
+    k_pitch_copy<<<grid_for(k * np), 256, 0, st>>>(dB, t, k, n, np);
+    B = t;
+  }
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  Problem p{};
+  p.conv = 0;
+  p.M = (int)m;
+  p.N = (int)n;
+  p.K = (int)k;
+  p.C = dC;
+  p.ldc = n;
+  p.tiles_m = (int)((m + BM - 1) / BM);
+  p.tiles_n = (int)((n + BN - 1) / BN);
+  p.tiles_img = 1;
+  p.splits = precision == ATC_PREC_3XTF32 ? 3 : 1;
+  if (p.splits == 3) {
+    float* ah = (float*)atc_ctx_scratch(ctx, 13, (size_t)m * kp * 4 * 2);
+    float* bh = (float*)atc_ctx_scratch(ctx, 14, (size_t)k * np * 4 * 2);
+    if (!ah || !bh) return ATC_ERR_CUDA;
+    float* al = ah + m * kp;
+    float* bl = bh + k * np;
+    k_split_tf32<<<grid_for(m * kp), 256, 0, st>>>(A, ah, al, m * kp);
+    k_split_tf32<<<grid_for(k * np), 256, 0, st>>>(B, bh, bl, k * np);
+    if (!make_map(ctx, &maps.a[0], ah, m, k, kp, BK, BM) || !make_map(ctx, &maps.a[1], al, m, k, kp, BK, BM) ||
+        !make_map(ctx, &maps.b[0], bh, k, n, np, 32, BK) || !make_map(ctx, &maps.b[1], bl, k, n, np, 32, BK))
+      return ATC_ERR_CUDA;
+  } else {
+    if (!make_map(ctx, &maps.a[0], A, m, k, kp, BK, BM) || !make_map(ctx, &maps.b[0], B, k, n, np, 32, BK))
+      return ATC_ERR_CUDA;
+    maps.a[1] = maps.a[0];
+    maps.b[1] = maps.b[0];
+  }
+  return launch(ctx, maps, p, st) ? ATC_OK : ATC_ERR_CUDA;
+}
+
+int atc_sgemm_rm(atc_ctx* ctx, const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
+                 int32_t precision) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (m < 1 || n < 1 || k < 1 || !A || !B || !C) {
+    atc_set_error(ctx, "bad arguments to atc_sgemm_rm");
+    return ATC_ERR_ARG;
+  }
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  float* dA = (float*)atc_ctx_scratch(ctx, 8, (size_t)m * k * 4);
+  float* dB = (float*)atc_ctx_scratch(ctx, 9, (size_t)k * n * 4);
+  float* dC = (float*)atc_ctx_scratch(ctx, 10, (size_t)m * n * 4);
+  if (!dA || !dB || !dC) {
+    atc_set_error(ctx, "device allocation failed");
+    return ATC_ERR_CUDA;
+  }
+  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(dA, A, (size_t)m * k * 4, cudaMemcpyHostToDevice, st), "H2D A") ||
+      !atc_cuda_ok(ctx, cudaMemcpyAsync(dB, B, (size_t)k * n * 4, cudaMemcpyHostToDevice, st), "H2D B"))
+    return ATC_ERR_CUDA;
+  int rc = atc_sgemm_rm_device(ctx, dA, dB, dC, m, n, k, precision, st);
+  if (rc) return rc;
+  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(C, dC, (size_t)m * n * 4, cudaMemcpyDeviceToHost, st), "D2H C") ||
+      !atc_cuda_ok(ctx, cudaStreamSynchronize(st), "sgemm sync"))
+    return ATC_ERR_CUDA;
+  return ATC_OK;
+}
+
+int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, float* d_out, int64_t n, int64_t c,
+                           int64_t h, int64_t w_, int64_t k, int64_t r, int64_t s, int32_t precision, void* stream) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  const int64_t oh = h - r + 1, ow = w_ - s + 1;
+  if (n < 1 || c < 1 || h < 1 || w_ < 1 || k < 1 || r < 1 || s < 1 || oh < 1 || ow < 1 || !d_in || !d_w || !d_out ||
+      (precision != ATC_PREC_TF32 && precision != ATC_PREC_3XTF32)) {
+    atc_set_error(ctx, "bad arguments to atc_conv2d_nchw");
+    return ATC_ERR_ARG;
+  }
+  if (c % BK != 0 || n * c >= (1LL << 31) || h * w_ >= (1LL << 31)) {
+    atc_set_error(ctx, "atc_conv2d_nchw: C must be a multiple of %d (got %lld)", BK, (long long)c);
+    return ATC_ERR_ARG;
+  }
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  const int64_t hw = h * w_, hwp = (hw + 3) / 4 * 4;
+  const int splits = precision == ATC_PREC_3XTF32 ? 3 : 1;
+  // input plane view [n*c][h*w] (re-pitched to 16 B when h*w % 4 != 0)
+  const float* in = d_in;
+  if (hwp != hw) {
+    float* t = (float*)atc_ctx_scratch(ctx, 11, (size_t)n * c * hwp * 4);
+    if (!t) return ATC_ERR_CUDA;
+    k_pitch_copy<<<grid_for(n * c * hwp), 256, 0, st>>>(d_in, t, n * c, hw, hwp);
+    in = t;
+  }
+  const int64_t wn = k * c * r * s;
+  float* wh = (float*)atc_ctx_scratch(ctx, 15, (size_t)wn * 4 * 2);
+  if (!wh) return ATC_ERR_CUDA;
+  float* wl = splits == 3 ? wh + wn : nullptr;
+  k_weights_krsc<<<grid_for(wn), 256, 0, st>>>(d_w, wh, wl, (int)k, (int)c, (int)r, (int)s);
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  if (!make_map(ctx, &maps.a[0], wh, k, r * s * c, r * s * c, BK, BM)) return ATC_ERR_CUDA;
+  maps.a[1] = maps.a[0];
+  if (splits == 3) {
+    float* ih = (float*)atc_ctx_scratch(ctx, 16, (size_t)n * c * hwp * 4 * 2);
+    if (!ih) return ATC_ERR_CUDA;
+    float* il = ih + n * c * hwp;
+    k_split_tf32<<<grid_for(n * c * hwp), 256, 0, st>>>(in, ih, il, n * c * hwp);
+    if (!make_map(ctx, &maps.a[1], wl, k, r * s * c, r * s * c, BK, BM) ||
+        !make_map(ctx, &maps.b[0], ih, n * c, hw, hwp, 32, BK) || !make_map(ctx, &maps.b[1], il, n * c, hw, hwp, 32, BK))
+      return ATC_ERR_CUDA;
+  } else {
+    if (!make_map(ctx, &maps.b[0], in, n * c, hw, hwp, 32, BK)) return ATC_ERR_CUDA;
+    maps.b[1] = maps.b[0];
+  }
+  Problem p{};
+  p.conv = 1;
+  p.M = (int)k;
+  p.N = (int)hw;
+  p.K = (int)c;
+  p.splits = splits;
+  p.C = d_out;
+  p.img = (int)n;
+  p.Cin = (int)c;
+  p.H = (int)h;
+  p.W = (int)w_;
+  p.R = (int)r;
+  p.S = (int)s;
+  p.OH = (int)oh;
+  p.OW = (int)ow;
+  p.tiles_m = (int)((k + BM - 1) / BM);
+  // only pixels p < OH*W can be valid outputs (rows y < OH)
+  p.tiles_n = (int)((oh * w_ + BN - 1) / BN);
+  p.tiles_img = (int)n;
+  return launch(ctx, maps, p, st) ? ATC_OK : ATC_ERR_CUDA;
+}
+
+int atc_conv2d_nchw(atc_ctx* ctx, const float* in, const float* w, float* out, int64_t n, int64_t c, int64_t h,
+                    int64_t w_, int64_t k, int64_t r, int64_t s, int32_t precision) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  const int64_t oh = h - r + 1, ow = w_ - s + 1;
+  if (n < 1 || c < 1 || h < 1 || w_ < 1 || k < 1 || r < 1 || s < 1 || oh < 1 || ow < 1 || !in || !w || !out) {
+    atc_set_error(ctx, "bad arguments to atc_conv2d_nchw");
+    return ATC_ERR_ARG;
+  }
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t bi = (size_t)(n * c * h * w_) * 4, bw = (size_t)(k * c * r * s) * 4, bo = (size_t)(n * k * oh * ow) * 4;
+  float* di = (float*)atc_ctx_scratch(ctx, 8, bi);
+  float* dw = (float*)atc_ctx_scratch(ctx, 9, bw);
+  float* dout = (float*)atc_ctx_scratch(ctx, 10, bo);
+  if (!di || !dw || !dout) return ATC_ERR_CUDA;
+  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(di, in, bi, cudaMemcpyHostToDevice, st), "H2D in") ||
+      !atc_cuda_ok(ctx, cudaMemcpyAsync(dw, w, bw, cudaMemcpyHostToDevice, st), "H2D w"))
+    return ATC_ERR_CUDA;
+  int rc = atc_conv2d_nchw_device(ctx, di, dw, dout, n, c, h, w_, k, r, s, precision, st);
+  if (rc) return rc;
+  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(out, dout, bo, cudaMemcpyDeviceToHost, st), "D2H out") ||
+      !atc_cuda_ok(ctx, cudaStreamSynchronize(st), "conv sync"))
+    return ATC_ERR_CUDA;
+  return ATC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+"""Benchmark workloads (BASELINE.json configs) built from the recorded corpus.
+
+corpus  every GEMM and conv2d corpus program x every spec of its class, the FULL
+        unpruned binding space with 16 recorded P2 test
+        sets each (configs 2-4; the conv spaces are 2.3e9-9.3e9 bindings, which
+        only a GPU can sweep).
+stress  naive_ld x gemm_rowmajor_ld, 279,936 bindings x 16 sets (config 4 alone).
+pruned  the ranked (pruned) candidate list of every program (config 2 as the
+        pipeline sees it; latency-bound).
+
+Algorithmic bytes: a screened (binding, t) pair is charged
+elem_bytes * (ext_A + ext_B + ext_C) with ext_X = prod of X's API dims under
+the binding's decoded sizes.  Over an enumerated space this sum factorises:
+sum over size maps of prod_{q in dims(X)} u[s_q] = (sum_i u_i)^|dims X| * nI^(nS-|dims X|).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import fixtures
+from .evaluator import BindingSpace, RecordedTestsets
+from .spec import ApiSpec
+
+
+@dataclass
+class Job:
+    stem: str
+    spec_name: str
+    spec: ApiSpec
+    space: BindingSpace
+    ts: RecordedTestsets
+    expected_pass: list | None  # reference P2-passing indices (T=16) when the dump is full
+
+    @property
+    def count(self) -> int:
+        return self.space.count
+
+    def t0_bytes(self, begin: int, end: int) -> float:
+        """Algorithmic bytes of screening [begin, end) at t = 0 (closed form,
+        proportional within a permutation block)."""
+        sp, sz = self.spec, self.space
+        u = self.ts.ints[0].astype(np.float64)
+        nI, nS = len(u), len(sp.size_params())
+        size_idx = {p.name: q for q, p in enumerate(sp.size_params())}
+        is_f32 = [p.elem == "f32" for p in self.ts.ptrs]
+        total = 0.0
+        per_perm = []
+        for perm in sz.perms:
+            b = 0.0
+            for a, arr in enumerate(sp.arrays()):
+                dims = [size_idx[d] for d in arr.dims]
+                # distinct size params per array in the bundled specs
+                assert len(set(dims)) == len(dims)
+                ext_sum = u.sum() ** len(dims) * float(nI) ** (nS - len(dims))
+                b += (4.0 if is_f32[perm[a]] else 8.0) * ext_sum
+            per_perm.append(b / sz.size_maps)
+        per_perm = np.array(per_perm)
+        # bytes per binding is constant within a permutation block
+        pm = sz.size_maps
+        for p, bpb in enumerate(per_perm):
+            lo, hi = max(begin, p * pm), min(end, (p + 1) * pm)
+            if hi > lo:
+                total += bpb * (hi - lo)
+        return total
+
+    def t0_flops(self, begin: int, end: int) -> float:
+        """2 * MACs of computing the full t=0 output (upper bound on screened work)."""
+        sp = self.spec
+        u = self.ts.ints[0].astype(np.float64)
+        nI, nS = len(u), len(sp.size_params())
+        roles = {p.role for p in sp.size_params()}
+        if sp.semantics == "gemm":
+            k = 3  # m, n, k
+        else:
+            k = 7 if {"oh", "ow"} <= roles else 5
+        return 2.0 * (u.sum() ** k * float(nI) ** (nS - k) / self.space.size_maps) * (end - begin)
+
+
+def corpus_jobs(T: int = 16, kinds=("gemm", "conv")) -> list:
+    jobs = []
+    for stem in fixtures.stems():
+        p = fixtures.load(stem)
+        if "specs" not in p.meta or p.meta.get("corpus_dir") not in kinds:
+            continue
+        ts = p.testsets(T)
+        for sname in p.spec_names():
+            v = p.verdicts(sname)
+            exp = None
+            if v["enumerated"] == "full":
+                ok = (v["fail_t"] < 0) | (v["fail_t"] >= T)
+                exp = v["idx"][ok].tolist()
+            jobs.append(Job(stem, sname, fixtures.spec(sname), p.space(sname), ts, exp))
+    return jobs
+
+
+def stress_jobs(T: int = 16) -> list:
+    return [j for j in corpus_jobs(T, ("gemm",)) if j.stem == "naive_ld" and j.spec_name == "gemm_rowmajor_ld"]
+
+
+def shard(count: int, rank: int, world: int) -> tuple:
+    """Contiguous block partition of [0, count)."""
+    return count * rank // world, count * (rank + 1) // world

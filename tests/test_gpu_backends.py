@@ -1,0 +1,117 @@
+"""GPU backends: FP64 run_reference / dispatch (bit-exact vs the oracle) and the
+tcgen05 TF32 / 3xTF32 sgemm and conv2d (stated tolerances vs FP64 references)."""
+import numpy as np
+import pytest
+
+from paper_2301_11659_b200 import AtcError, backends, fixtures
+
+from . import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _rand(rng, n):
+    return rng.uniform(-1, 1, n)
+
+
+@pytest.mark.parametrize("sname,sizes", [
+    ("gemm_rowmajor", [5, 7, 3]), ("gemm_colmajor", [6, 2, 9]), ("gemm_rowmajor_ld", [4, 6, 5, 7, 9, 8]),
+    ("gemm_rowmajor_ld", [4, 6, 5, 3, 2, 3]),  # ldc < n: overlapping writes, last writer wins
+    ("gemm_colmajor", [64, 64, 64]), ("conv2d", [3, 4, 9, 8, 5, 3, 2, 7, 7]), ("conv2d", [2, 2, 5, 5, 3, 2, 3, 6, 2]),
+])
+def test_run_reference_bit_exact(sname, sizes):
+    spec = fixtures.spec(sname)
+    rng = np.random.default_rng(len(sizes) + sum(sizes))
+    bufs_gpu, bufs_cpu = {}, []
+    for p in spec.arrays():
+        b = _rand(rng, 4096)
+        bufs_gpu[p.name] = b.copy()
+        bufs_cpu.append(b.copy())
+    assert O.run_reference(spec, sizes, bufs_cpu) == 0
+    backends.run_reference(spec, dict(zip([p.name for p in spec.size_params()], sizes)), bufs_gpu)
+    for p, want in zip(spec.arrays(), bufs_cpu):
+        assert np.array_equal(bufs_gpu[p.name].view(np.uint64), want.view(np.uint64)), p.name
+
+
+def test_frozen_vectors_gpu():  # equivalence_test.cpp:76-121 through the GPU
+    spec = fixtures.spec("gemm_rowmajor_ld")
+    bufs = {"tc_A": np.array([1., 2, -9, 3, 4, -9]), "tc_B": np.array([5., 6, -9, 7, 8, -9]),
+            "tc_C": np.array([0., 0, -9, 0, 0, -9])}
+    backends.run_reference(spec, {"tc_m": 2, "tc_n": 2, "tc_k": 2, "tc_lda": 3, "tc_ldb": 3, "tc_ldc": 3}, bufs)
+    assert bufs["tc_C"].tolist() == [19, 22, -9, 43, 50, -9]
+
+
+def test_dispatch_errors_and_rounding():
+    """rewriter_test.cpp:151-184: 'arity' and 'elements' messages; f32 write-back."""
+    spec = fixtures.spec("gemm_rowmajor")
+    h = backends.make_gpu_dispatch(spec)
+    D, R = backends.DispatchArg, backends.Region
+    regions = {r: R(np.ones(16)) for r in "abc"}
+    with pytest.raises(RuntimeError, match="arity"):
+        h("atc_dispatch_gemm", [D("ptr", "a"), D("ptr", "b"), D("ptr", "c"), D("int", i=2), D("int", i=2)], regions)
+    args = [D("ptr", "a"), D("ptr", "b"), D("ptr", "c"), D("int", i=10), D("int", i=10), D("int", i=10)]
+    with pytest.raises(RuntimeError, match="elements"):
+        h("atc_dispatch_gemm", args, regions)
+    args = [D("ptr", "a"), D("ptr", "b"), D("ptr", "c"), D("int", i=2), D("int", i=2), D("int", i=2)]
+    h("atc_dispatch_gemm", args, regions)
+    assert regions["c"].data[:4].tolist() == [2.0] * 4  # rewriter_test.cpp:140
+    x = np.full(16, 1.0 / 3.0)
+    regions = {"a": R(x.copy(), "f32"), "b": R(x.copy(), "f32"), "c": R(np.zeros(16), "f32")}
+    h("atc_dispatch_gemm", args, regions)
+    want = float(np.float32(2.0 / 9.0 * (1 + 0)))  # (1/3*1/3)*2 rounded through float
+    assert regions["c"].data[0] == float(np.float32((1.0 / 3.0) * (1.0 / 3.0) + (1.0 / 3.0) * (1.0 / 3.0)))
+    assert abs(regions["c"].data[0] - want) < 1e-7
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 256, 32), (256, 512, 320), (300, 260, 100), (1000, 1030, 515), (7, 9, 5)])
+@pytest.mark.parametrize("prec,tol", [("tf32", 4e-3), ("3xtf32", 2e-6)])
+def test_sgemm_accuracy(m, n, k, prec, tol):
+    """TF32: max |C - C64| / (1 + |C64|) <= 4e-3 (2^-10-ish inputs, K-dependent);
+    3xTF32: <= 2e-6 (FP32-class).  C64 = float64 product of the fp32 inputs."""
+    rng = np.random.default_rng(m + n + k)
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    b = rng.uniform(-1, 1, (k, n)).astype(np.float32)
+    c = backends.sgemm(a, b, prec)
+    c64 = a.astype(np.float64) @ b.astype(np.float64)
+    err = np.abs(c - c64) / (1 + np.abs(c64))
+    assert err.max() <= tol, err.max()
+
+
+def test_sgemm_sample_one_pattern():
+    """profitability.cpp:73-85 inputs (TF32-exact) pass the reference's 1e-3 cross-check."""
+    m, n, k = 192, 576, 1152
+    a = np.array([0.25 + (i % 17) * 0.0625 for i in range(m * k)], dtype=np.float32).reshape(m, k)
+    b = np.array([-0.5 + (i % 23) * 0.0625 for i in range(k * n)], dtype=np.float32).reshape(k, n)
+    ref = O.cpu_gemm(a.ravel(), b.ravel(), m, n, k).astype(np.float64)
+    for prec in ("tf32", "3xtf32"):
+        c = backends.sgemm(a, b, prec)
+        assert np.all(np.abs(c - ref) <= 1e-3 * (1 + np.abs(ref))), prec
+
+
+@pytest.mark.parametrize("shape", [(2, 64, 10, 12, 64, 3, 3), (1, 32, 9, 9, 512, 3, 3), (3, 64, 8, 8, 256, 1, 1),
+                                   (2, 96, 17, 13, 40, 2, 4)])
+@pytest.mark.parametrize("prec,tol", [("tf32", 5e-3), ("3xtf32", 2e-6)])
+def test_conv2d_accuracy(shape, prec, tol):
+    n, c, h, w, k, r, s = shape
+    rng = np.random.default_rng(sum(shape))
+    x = rng.uniform(-1, 1, (n, c, h, w)).astype(np.float32)
+    wt = rng.uniform(-1, 1, (k, c, r, s)).astype(np.float32)
+    out = backends.conv2d_nchw(x, wt, prec)
+    import torch
+
+    ref = torch.nn.functional.conv2d(torch.from_numpy(x).double(), torch.from_numpy(wt).double()).numpy()
+    err = np.abs(out - ref) / (1 + np.abs(ref))
+    assert err.max() <= tol, err.max()
+
+
+def test_conv2d_matches_reference_semantics_small():
+    """FP32 conv backend vs oracle run_reference (f64) on the frozen all-ones case, C=32."""
+    x = np.ones((1, 32, 3, 3), np.float32)
+    w = np.ones((1, 32, 2, 2), np.float32)
+    out = backends.conv2d_nchw(x, w, "tf32")
+    assert out.ravel().tolist() == [128.0] * 4
+
+
+def test_bad_arguments_raise():
+    with pytest.raises(AtcError):
+        backends.conv2d_nchw(np.ones((1, 3, 5, 5), np.float32), np.ones((2, 3, 3, 3), np.float32))
