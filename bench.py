@@ -180,7 +180,10 @@ def main():
     from paper_2301_11659_b200.evaluator import Evaluator
 
     ctx = _lib.Context(local)
-    stream = torch.cuda.current_stream()
+    # a real (non-legacy) stream: every library launch and every CUDA event of
+    # the timed region go to this one stream
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     _lib.check(ctx.handle, _lib.lib().atc_set_stream(ctx.handle, C.c_void_p(stream.cuda_stream)))
     ev = Evaluator(ctx)
     shards = [workloads.shard(j.count, rank, world) for j in jobs]

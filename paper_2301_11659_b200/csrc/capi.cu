@@ -54,6 +54,10 @@ bool atc_cuda_ok(atc_ctx* ctx, cudaError_t e, const char* what) {
 }
 
 void* atc_ctx_scratch(atc_ctx* ctx, int slot, size_t bytes) {
+  if (slot < 0 || slot >= atc_ctx::kSlots) {
+    atc_set_error(ctx, "internal: scratch slot %d out of range", slot);
+    return nullptr;
+  }
   if (ctx->scratch_bytes[slot] >= bytes) return ctx->scratch[slot];
   if (ctx->scratch[slot]) cudaFree(ctx->scratch[slot]);
   ctx->scratch[slot] = nullptr;

@@ -13,8 +13,9 @@ struct atc_ctx {
   std::string err;
   cudaStream_t stream = nullptr;
   // reusable device scratch, grown on demand (slot ids are per call site)
-  void* scratch[16] = {};
-  size_t scratch_bytes[16] = {};
+  static constexpr int kSlots = 32;
+  void* scratch[kSlots] = {};
+  size_t scratch_bytes[kSlots] = {};
   void* pinned[4] = {};
   size_t pinned_bytes[4] = {};
   cudaStream_t own_stream = nullptr;

@@ -21,12 +21,13 @@
 // k_split_tf32; C = Ah*Bh + Al*Bh + Ah*Bl as one K' = 3K contraction), which
 // recovers ~FP32 accuracy.  See DESIGN.md §4 for the measured error.
 //
-// Conv2d (NCHW, valid, unit stride) is the same kernel in implicit-GEMM form
-// with no input transform: M = filters, N = output pixels laid out on the
-// INPUT grid (p = y*W + x, x < W), K' = (r, s, c).  For a fixed (r, s) the B
-// operand rows are In[n][c][p + r*W + s] — an affine shift of the contiguous
-// H*W plane — so every B chunk is a plain 2-D TMA box of the [N*C][H*W] view.
-// Pixels with x >= OW or y >= OH are computed and discarded by the epilogue.
+// Conv2d (NCHW, valid, unit stride) is the same kernel in implicit-GEMM form:
+// M = filters, N = output pixels laid out on the INPUT grid (p = y*W + x),
+// K' = (r, s, c).  The input is transposed once to NHWC (k_nchw_to_nhwc), so
+// for a fixed (r, s) the B operand is rows p + r*W + s of the [N*H*W][C] view —
+// an affine row shift, i.e. one plain K-major 2-D TMA box per stage, with no
+// im2col buffer.  Pixels with x >= OW or y >= OH are computed and discarded by
+// the epilogue (waste (R-1)/H + (S-1)/W), which writes NCHW directly.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -85,28 +86,37 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 
 // smem matrix descriptor (tcgen05 "shared memory descriptor"): start >> 4 at
 // [0,14), LBO >> 4 at [16,30), SBO >> 4 at [32,46), version 1 at [46,48),
-// layout SWIZZLE_128B (2) at [61,64).
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// layout at [61,64): 2 = SWIZZLE_128B (16 B granules ^= row % 8), 1 =
+// SWIZZLE_128B_BASE32B (32 B granules ^= row % 4).  32-bit MN-major operands
+// need the BASE32B form (TMA: CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B); a plain
+// 128B swizzle on an MN-major tf32 operand makes the MMA produce zeros
+// (measured with .gpu_scripts/tc_probe2).
+constexpr uint32_t kSw128 = 2, kSw128Base32 = 1;
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= 1ull << 46;
-  d |= 2ull << 61;
+  d |= (uint64_t)layout << 61;
   return d;
 }
 
 // instruction descriptor, kind::tf32: D f32 [4,6)=1, A tf32 [7,10)=2,
-// B tf32 [10,13)=2, A K-major [15]=0, B MN-major [16]=1, N>>3 [17,23), M>>4 [24,29)
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
-                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// B tf32 [10,13)=2, A K-major [15]=0, B major [16] (1 = MN-major for the sgemm's
+// row-major B, 0 = K-major for the conv's NHWC input), N>>3 [17,23), M>>4 [24,29)
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t b_mn_major) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (b_mn_major << 16) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -177,8 +187,8 @@ __device__ __forceinline__ void kblock_coords(const Problem& p, int kb, int kblo
     const int r = rs / p.S, s = rs - (rs / p.S) * p.S;
     a_c0 = rs * p.K + c0;             // column in W_krsc [Kf][R*S*C]
     a_c1 = tm * BM;                   // filter row
-    b_c0 = tn * BN + r * p.W + s;     // pixel (affine shift of the input plane)
-    b_c1 = ti * p.Cin + c0;           // row n*C + c
+    b_c0 = c0;                        // channel block of the NHWC input [N*H*W][C]
+    b_c1 = ti * p.H * p.W + tn * BN + r * p.W + s;  // pixel row: affine shift on the input grid
   }
 }
 
@@ -234,8 +244,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           uint8_t* sB = sA + A_BYTES;
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           tma_load_2d(sA, &maps.a[sa], &full[stage], a0, a1);
+          if (p.conv) {
+            // K-major: 256 pixel rows x 32 channels (128 B) in one box
+            tma_load_2d(sB, &maps.b[sb], &full[stage], b0, b1);
+          } else {
+            // MN-major: 8 chunks of [32 K rows x 32 N]
 #pragma unroll
-          for (int j = 0; j < BN / 32; ++j) tma_load_2d(sB + j * (BK * 128), &maps.b[sb], &full[stage], b0 + 32 * j, b1);
+            for (int j = 0; j < BN / 32; ++j)
+              tma_load_2d(sB + j * (BK * 128), &maps.b[sb], &full[stage], b0 + 32 * j, b1);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -262,10 +279,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             // A: K-major SW128, +32 B per K=8 step inside the 128 B atom; SBO = 8 rows * 128 B
-            const uint64_t ad = make_desc(a_addr + kk * 32, 16, 1024);
-            // B: MN-major SW128, chunks of 32 N at LBO = 32 rows * 128 B; +8 rows per K step
-            const uint64_t bd = make_desc(b_addr + kk * 1024, BK * 128, 1024);
-            mma_tf32(d_tmem, ad, bd, (kb > 0 || kk > 0) ? 1u : 0u);
+            const uint64_t ad = make_desc(a_addr + kk * 32, 16, 1024, kSw128);
+            // B (sgemm): MN-major SW128 with 32 B atoms: chunks of 32 N at LBO = 32 rows *
+            // 128 B, 4-row K groups at SBO = 512 B; +8 rows (1 KB) per K step.
+            // B (conv): K-major SW128 like A.
+            const uint64_t bd = p.conv ? make_desc(b_addr + kk * 32, 16, 1024, kSw128)
+                                       : make_desc(b_addr + kk * 1024, BK * 128, 512, kSw128Base32);
+            mma_tf32(d_tmem, ad, bd, p.conv ? idesc_tf32(0) : idesc_tf32(1), (kb > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&empty[stage]);  // smem stage free once these MMAs complete
           if (++stage == STAGES) {
@@ -381,6 +401,36 @@ __global__ void k_pitch_copy(const float* __restrict__ src, float* __restrict__ 
   }
 }
 
+// NCHW -> NHWC, optionally split into TF32 hi/lo (3xTF32).  Block (32, 8):
+// a [32 channels x 32 pixels] tile through padded shared memory, coalesced
+// 128 B reads along pixels and 128 B writes along channels.
+__global__ void k_nchw_to_nhwc(const float* __restrict__ in, float* __restrict__ hi, float* __restrict__ lo, int C,
+                               int64_t HW) {
+  __shared__ float tile[32][33];
+  const int64_t p0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  const int64_t img = blockIdx.z;
+  const float* src = in + (img * C + c0) * HW + p0;
+  for (int cy = threadIdx.y; cy < 32; cy += 8) {
+    const int64_t p = p0 + threadIdx.x;
+    tile[cy][threadIdx.x] = p < HW ? src[(int64_t)cy * HW + threadIdx.x] : 0.0f;
+  }
+  __syncthreads();
+  for (int py = threadIdx.y; py < 32; py += 8) {
+    const int64_t p = p0 + py;
+    if (p >= HW) continue;
+    const float v = tile[threadIdx.x][py];
+    const int64_t o = (img * HW + p) * C + c0 + threadIdx.x;
+    if (lo) {
+      const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+      hi[o] = h;
+      lo[o] = v - h;
+    } else {
+      hi[o] = v;
+    }
+  }
+}
+
 }  // namespace tc
 }  // namespace atc
 
@@ -404,7 +454,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode(atc_ctx* ctx) {
 
 // 2-D fp32 tensor map over [rows][cols] with row pitch `pitch` elements.
 bool make_map(atc_ctx* ctx, CUtensorMap* m, const float* base, uint64_t rows, uint64_t cols, uint64_t pitch,
-              uint32_t box_cols, uint32_t box_rows) {
+              uint32_t box_cols, uint32_t box_rows, bool mn_major) {
   auto enc = get_encode(ctx);
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};
@@ -412,7 +462,9 @@ bool make_map(atc_ctx* ctx, CUtensorMap* m, const float* base, uint64_t rows, ui
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     atc_set_error(ctx, "cuTensorMapEncodeTiled failed (%d) for [%llu x %llu] pitch %llu", (int)r,
@@ -489,11 +541,11 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
     float* bl = bh + k * np;
     k_split_tf32<<<grid_for(m * kp), 256, 0, st>>>(A, ah, al, m * kp);
     k_split_tf32<<<grid_for(k * np), 256, 0, st>>>(B, bh, bl, k * np);
-    if (!make_map(ctx, &maps.a[0], ah, m, k, kp, BK, BM) || !make_map(ctx, &maps.a[1], al, m, k, kp, BK, BM) ||
-        !make_map(ctx, &maps.b[0], bh, k, n, np, 32, BK) || !make_map(ctx, &maps.b[1], bl, k, n, np, 32, BK))
+    if (!make_map(ctx, &maps.a[0], ah, m, k, kp, BK, BM, false) || !make_map(ctx, &maps.a[1], al, m, k, kp, BK, BM, false) ||
+        !make_map(ctx, &maps.b[0], bh, k, n, np, 32, BK, true) || !make_map(ctx, &maps.b[1], bl, k, n, np, 32, BK, true))
       return ATC_ERR_CUDA;
   } else {
-    if (!make_map(ctx, &maps.a[0], A, m, k, kp, BK, BM) || !make_map(ctx, &maps.b[0], B, k, n, np, 32, BK))
+    if (!make_map(ctx, &maps.a[0], A, m, k, kp, BK, BM, false) || !make_map(ctx, &maps.b[0], B, k, n, np, 32, BK, true))
       return ATC_ERR_CUDA;
     maps.a[1] = maps.a[0];
     maps.b[1] = maps.b[0];
@@ -543,15 +595,20 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
   }
   cudaSetDevice(ctx->device);
   cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
-  const int64_t hw = h * w_, hwp = (hw + 3) / 4 * 4;
+  const int64_t hw = h * w_;
   const int splits = precision == ATC_PREC_3XTF32 ? 3 : 1;
-  // input plane view [n*c][h*w] (re-pitched to 16 B when h*w % 4 != 0)
-  const float* in = d_in;
-  if (hwp != hw) {
-    float* t = (float*)atc_ctx_scratch(ctx, 11, (size_t)n * c * hwp * 4);
-    if (!t) return ATC_ERR_CUDA;
-    k_pitch_copy<<<grid_for(n * c * hwp), 256, 0, st>>>(d_in, t, n * c, hw, hwp);
-    in = t;
+  // NCHW -> NHWC once per call (one read + one write of the input; fused with
+  // the hi/lo split in 3xTF32 mode).  Channels-innermost makes the conv's B
+  // operand K-major, so the (r, s) pixel shift is a row offset of a 2-D TMA box
+  // (any offset is legal) instead of a sub-16-byte column offset (illegal for
+  // swizzled TMA boxes).
+  const int64_t in_elems = n * c * hw;
+  float* ih = (float*)atc_ctx_scratch(ctx, 16, (size_t)in_elems * 4 * (splits == 3 ? 2 : 1));
+  if (!ih) return ATC_ERR_CUDA;
+  float* il = splits == 3 ? ih + in_elems : nullptr;
+  {
+    dim3 grid((unsigned)((hw + 31) / 32), (unsigned)(c / 32), (unsigned)n);
+    k_nchw_to_nhwc<<<grid, dim3(32, 8), 0, st>>>(d_in, ih, il, (int)c, hw);
   }
   const int64_t wn = k * c * r * s;
   float* wh = (float*)atc_ctx_scratch(ctx, 15, (size_t)wn * 4 * 2);
@@ -560,20 +617,14 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
   k_weights_krsc<<<grid_for(wn), 256, 0, st>>>(d_w, wh, wl, (int)k, (int)c, (int)r, (int)s);
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
-  if (!make_map(ctx, &maps.a[0], wh, k, r * s * c, r * s * c, BK, BM)) return ATC_ERR_CUDA;
+  if (!make_map(ctx, &maps.a[0], wh, k, r * s * c, r * s * c, BK, BM, false) ||
+      !make_map(ctx, &maps.b[0], ih, n * hw, c, c, BK, BN, false))
+    return ATC_ERR_CUDA;
   maps.a[1] = maps.a[0];
-  if (splits == 3) {
-    float* ih = (float*)atc_ctx_scratch(ctx, 16, (size_t)n * c * hwp * 4 * 2);
-    if (!ih) return ATC_ERR_CUDA;
-    float* il = ih + n * c * hwp;
-    k_split_tf32<<<grid_for(n * c * hwp), 256, 0, st>>>(in, ih, il, n * c * hwp);
-    if (!make_map(ctx, &maps.a[1], wl, k, r * s * c, r * s * c, BK, BM) ||
-        !make_map(ctx, &maps.b[0], ih, n * c, hw, hwp, 32, BK) || !make_map(ctx, &maps.b[1], il, n * c, hw, hwp, 32, BK))
-      return ATC_ERR_CUDA;
-  } else {
-    if (!make_map(ctx, &maps.b[0], in, n * c, hw, hwp, 32, BK)) return ATC_ERR_CUDA;
-    maps.b[1] = maps.b[0];
-  }
+  maps.b[1] = maps.b[0];
+  if (splits == 3 && (!make_map(ctx, &maps.a[1], wl, k, r * s * c, r * s * c, BK, BM, false) ||
+                      !make_map(ctx, &maps.b[1], il, n * hw, c, c, BK, BN, false)))
+    return ATC_ERR_CUDA;
   Problem p{};
   p.conv = 1;
   p.M = (int)k;
