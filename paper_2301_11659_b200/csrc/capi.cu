@@ -19,6 +19,18 @@ __global__ void k_build_dirty(TestsetView ts, int32_t* dirty_pos, int32_t* dirty
 __global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, int budget,
                          int32_t* keys, uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                          unsigned long long* reason_hist);
+constexpr int kMaxPos0Roles = 5;
+struct Pos0Table {
+  int R;
+  int q[kMaxPos0Roles];
+  uint64_t per_perm;
+  const uint8_t* table;
+};
+__global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
+                             uint8_t* out);
+__global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
+                              uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
+                              unsigned long long* reason_hist);
 __global__ void k_confirm(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                           const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys);
 __global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
@@ -380,7 +392,7 @@ int screen_budget(const SpecView& sp) { return sp.sem == ATC_SEM_GEMM ? 16 : 2; 
 // Runs K1 + K2 over `n` bindings; survivors/keys live in ctx scratch.
 int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, const BindingSource& src,
              uint64_t n, int32_t* keys, uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
-             int32_t* surv_keys, unsigned long long* hist, cudaStream_t st) {
+             int32_t* surv_keys, unsigned long long* hist, cudaStream_t st, const Pos0Table* pt = nullptr) {
   if (n == 0) return ATC_OK;
   const uint64_t blocks_needed = (n + kScreenThreads - 1) / kScreenThreads;
   const unsigned grid = (unsigned)std::min<uint64_t>(blocks_needed, (uint64_t)ctx->sm_count * 32);
@@ -397,8 +409,15 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     cudaEventRecord(e1.first, st);
     ctx->prof_bindings += (long long)n;
   }
-  k_screen<<<grid, kScreenThreads, 0, st>>>(ts->view, sp, src, n, screen_budget(sp), keys, surv, surv_cap,
-                                            surv_cnt, hist);
+  if (pt) {
+    const uint64_t runs = (n + 15) / 16;
+    const unsigned g2 = (unsigned)std::min<uint64_t>((runs + kScreenThreads - 1) / kScreenThreads,
+                                                     (uint64_t)ctx->sm_count * 16);
+    k_screen_enum<<<g2, kScreenThreads, 0, st>>>(ts->view, sp, src, n, *pt, surv, surv_cap, surv_cnt, hist);
+  } else {
+    k_screen<<<grid, kScreenThreads, 0, st>>>(ts->view, sp, src, n, screen_budget(sp), keys, surv, surv_cap,
+                                              surv_cnt, hist);
+  }
   if (ctx->prof) {
     cudaEventRecord(e1.second, st);
     ctx->prof_screen.push_back(e1);
@@ -531,6 +550,38 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
   }
   cudaMemcpyAsync(d_perms, perms, (size_t)n_perms * sp.nA, cudaMemcpyHostToDevice, st);
   cudaMemsetAsync(hist, 0, 64, st);
+  // position-0 table (k_pos0_table): roles the first output element depends on
+  Pos0Table pt{};
+  bool use_table = true;
+  if (sp.sem == ATC_SEM_GEMM) {
+    const bool row = sp.layout == ATC_LAYOUT_ROW;
+    const int ld = row ? (sp.role_size[ATC_SZ_LDB] >= 0 ? sp.role_size[ATC_SZ_LDB] : sp.role_size[ATC_SZ_N])
+                       : (sp.role_size[ATC_SZ_LDA] >= 0 ? sp.role_size[ATC_SZ_LDA] : sp.role_size[ATC_SZ_M]);
+    pt.R = 2;
+    pt.q[0] = sp.role_size[ATC_SZ_K];
+    pt.q[1] = ld;
+  } else {
+    pt.R = 5;
+    const int roles[5] = {ATC_SZ_CC, ATC_SZ_CH, ATC_SZ_CW, ATC_SZ_CR, ATC_SZ_CS};
+    for (int r = 0; r < 5; ++r) pt.q[r] = sp.role_size[roles[r]];
+  }
+  pt.per_perm = 1;
+  for (int r = 0; r < pt.R; ++r) {
+    if (pt.q[r] < 0) use_table = false;
+    pt.per_perm *= (uint64_t)ts->nI;
+  }
+  const uint64_t table_bytes = pt.per_perm * (uint64_t)n_perms;
+  if (table_bytes > (256ull << 20)) use_table = false;
+  if (use_table) {
+    uint8_t* tab = (uint8_t*)atc_ctx_scratch(ctx, 17, table_bytes + 16);
+    if (!tab) {
+      atc_set_error(ctx, "scratch allocation failed (table)");
+      return ATC_ERR_CUDA;
+    }
+    pt.table = tab;
+    k_pos0_table<<<(unsigned)std::min<uint64_t>((table_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16), 256, 0,
+                   st>>>(ts->view, sp, d_perms, n_perms, pt, tab);
+  }
   std::vector<uint64_t> h_surv;
   std::vector<int32_t> h_keys;
   int64_t passed = 0;
@@ -539,7 +590,8 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
   for (uint64_t lo = begin; lo < end;) {
     const uint64_t hi = std::min(end, lo + chunk);
     BindingSource src{nullptr, nullptr, d_perms, size_maps, lo, 1};
-    int rc = run_eval(ctx, sp, ts, src, hi - lo, nullptr, surv, chunk_cap, cnt, skeys, hist, st);
+    int rc = run_eval(ctx, sp, ts, src, hi - lo, nullptr, surv, chunk_cap, cnt, skeys, hist, st,
+                      use_table ? &pt : nullptr);
     if (rc) return rc;
     unsigned long long c = 0;
     if (!atc_cuda_ok(ctx, cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, st), "D2H") ||

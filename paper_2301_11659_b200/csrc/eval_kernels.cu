@@ -198,6 +198,199 @@ __global__ void __launch_bounds__(256) k_screen(TestsetView ts, SpecView sp, Bin
   }
 }
 
+// --------------------------------------------- K1 for enumerated spaces ------
+// Factorised screen.  Position 0 of the output is written by the first loop
+// iteration of run_reference (gemm (i,j) = (0,0); conv (b,q,y,x) = 0) and is
+// always its own last writer.  Its value depends only on the array permutation
+// and a few size roles:
+//   gemm row-major  sum_p A[p] * B[p*ldb]      roles (k, ldb)   [ldb falls back to n]
+//   gemm col-major  sum_p A[p*lda] * B[p]      roles (k, lda)   [lda falls back to m]
+//   conv2d          sum_{z,u,v} in[(z*h+u)*w+v] * wt[(z*r+u)*s+v]   roles (c, h, w, r, s)
+// so the t = 0 verdict of position 0 is tabulated once per (permutation,
+// user ints bound to those roles) — e.g. 6 x 9^5 entries for a 2.3e9-binding
+// conv space — with exactly the FP64 non-fused arithmetic of thread_check.
+// The per-binding screen is then integer-only: run_dispatch extent checks,
+// access bounds, the dirty-set (write-set) check, one table lookup.  Bindings
+// that pass all of it go to K2, which re-checks every test completely.
+constexpr int kMaxPos0Roles = 5;
+
+struct Pos0Table {
+  int R;                       // number of roles the position-0 value depends on
+  int q[kMaxPos0Roles];        // size-param index of each role
+  uint64_t per_perm;           // nI^R
+  const uint8_t* table;        // [n_perms][nI^R]: 0 match, 1 mismatch, 2 not tabulated (read outside region)
+};
+
+__global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
+                             uint8_t* out) {
+  const uint64_t total = (uint64_t)n_perms * pt.per_perm;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t perm = e / pt.per_perm;
+    uint64_t rem = e - perm * pt.per_perm;
+    int64_t v[kMaxPos0Roles];
+    for (int r = 0; r < pt.R; ++r) {
+      v[r] = ts.ints[rem % ts.nI];  // t = 0 values
+      rem /= ts.nI;
+    }
+    const int pA = perms[perm * sp.nA + sp.arr_of_role[0]];
+    const int pB = perms[perm * sp.nA + sp.arr_of_role[1]];
+    const int pC = perms[perm * sp.nA + sp.arr_of_role[2]];
+    const double* A = ts.init + ts.region_off[pA];
+    const double* B = ts.init + ts.region_off[pB];
+    const double want = ts.fin[ts.region_off[pC]];
+    const bool f32 = ts.is_f32[pC] != 0;
+    const int64_t lenA = ts.region_len[pA], lenB = ts.region_len[pB];
+    uint8_t res = 2;
+    double acc = 0.0;
+    if (sp.sem == ATC_SEM_GEMM) {
+      const int64_t k = v[0], ld = v[1];  // ld = ldb (row) or lda (col)
+      const bool row = sp.layout == ATC_LAYOUT_ROW;
+      if (k >= 1 && ld >= 0) {
+        const int64_t amax = row ? k - 1 : (k - 1) * ld, bmax = row ? (k - 1) * ld : k - 1;
+        if (amax < lenA && bmax < lenB) {
+          for (int64_t p = 0; p < k; ++p) acc = dadd(acc, dmul(row ? A[p] : A[p * ld], row ? B[p * ld] : B[p]));
+          res = mismatch(round_region(acc, f32), want, f32) ? 1 : 0;
+        }
+      } else if (k < 1) {
+        res = mismatch(round_region(0.0, f32), want, f32) ? 1 : 0;
+      }
+    } else {
+      const int64_t c = v[0], h = v[1], w = v[2], r = v[3], s = v[4];
+      if (c >= 1 && r >= 1 && s >= 1 && h >= 0 && w >= 0) {
+        const int64_t imax = ((c - 1) * h + (r - 1)) * w + (s - 1), wmax = c * r * s - 1;
+        if (imax >= 0 && imax < lenA && wmax < lenB) {
+          for (int64_t z = 0; z < c; ++z)
+            for (int64_t u = 0; u < r; ++u)
+              for (int64_t t = 0; t < s; ++t)
+                acc = dadd(acc, dmul(A[(z * h + u) * w + t], B[(z * r + u) * s + t]));
+          res = mismatch(round_region(acc, f32), want, f32) ? 1 : 0;
+        }
+      } else {
+        res = mismatch(round_region(0.0, f32), want, f32) ? 1 : 0;
+      }
+    }
+    out[e] = res;
+  }
+}
+
+// Per-binding integer screen over [begin, begin + n) of the Appendix C space.
+// Each thread walks a run of consecutive indices with an odometer over the
+// size-map digits (no per-binding division).  Rejections are counted per reason
+// in registers and reduced per warp / block; survivors are queued for K2.
+constexpr int kRun = 16;
+
+__global__ void __launch_bounds__(256) k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n,
+                                                      Pos0Table pt, uint64_t* surv, uint64_t surv_cap,
+                                                      unsigned long long* surv_cnt,
+                                                      unsigned long long* reason_hist) {
+  __shared__ int64_t s_u0[kMaxInts];
+  __shared__ unsigned int s_hist[ATC_REASON_COUNT];
+  if (threadIdx.x < ts.nI) s_u0[threadIdx.x] = ts.ints[threadIdx.x];
+  if (threadIdx.x < ATC_REASON_COUNT) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int nI = ts.nI, nS = sp.nS;
+  const int tpC_base = 0;  // t = 0
+  unsigned int cnt[ATC_REASON_COUNT] = {0, 0, 0, 0, 0};
+  const uint64_t runs = (n + kRun - 1) / kRun;
+  for (uint64_t run = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; run < runs;
+       run += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t lo = run * kRun;
+    const int len = (int)min((uint64_t)kRun, n - lo);
+    // decode the first index of the run
+    const uint64_t g = src.begin + lo;
+    uint64_t perm = g / src.size_maps;
+    uint64_t s = g - perm * src.size_maps;
+    int digit[ATC_MAX_SIZES];
+#pragma unroll
+    for (int q = 0; q < ATC_MAX_SIZES; ++q) {
+      if (q < nS) {
+        const uint64_t d = s / (uint64_t)nI;
+        digit[q] = (int)(s - d * (uint64_t)nI);
+        s = d;
+      }
+    }
+    for (int j = 0; j < len; ++j) {
+      int ptr_of[ATC_MAX_ARRAYS];
+#pragma unroll
+      for (int a = 0; a < ATC_MAX_ARRAYS; ++a)
+        if (a < sp.nA) ptr_of[a] = src.perms[perm * sp.nA + a];
+      int64_t sz[ATC_MAX_SIZES];
+#pragma unroll
+      for (int q = 0; q < ATC_MAX_SIZES; ++q)
+        if (q < nS) sz[q] = s_u0[digit[q]];
+      int r = 0;
+      if (!ts.test_ok[0]) r = ATC_FAIL_TESTSET;
+      if (!r) r = extent_check(sp, sz, ptr_of, ts.region_len);
+      Dims d;
+      if (!r) {
+        resolve_dims(sp, sz, d);
+        r = ub_check(sp, d, ptr_of, ts.region_len);
+      }
+      if (!r) {
+        // write-set check: every dirty position must be written
+        const int pC = ptr_of[sp.arr_of_role[2]];
+        const int tpC = tpC_base + pC;
+        if (sp.sem == ATC_SEM_GEMM) {
+          const bool row = sp.layout == ATC_LAYOUT_ROW;
+          const int m = (int)d.m, nn = (int)d.n, ldc = (int)d.ldc;
+          const int nd = ts.dirty_cnt[tpC];
+          const int32_t* dirty = ts.dirty_pos + ts.dirty_off[tpC];
+          if (m < 1 || nn < 1) {
+            if (nd) r = ATC_FAIL_MISMATCH;
+          } else {
+            for (int e = 0; e < nd; ++e)
+              if (!gemm_written(row, __ldg(dirty + e), m, nn, ldc)) {
+                r = ATC_FAIL_MISMATCH;
+                break;
+              }
+          }
+          if (!r && m >= 1 && nn >= 1) {
+            uint64_t key = 0, mul = 1;
+            for (int k = 0; k < pt.R; ++k) {
+              key += (uint64_t)digit[pt.q[k]] * mul;
+              mul *= (uint64_t)nI;
+            }
+            if (__ldg(pt.table + perm * pt.per_perm + key) == 1) r = ATC_FAIL_MISMATCH;
+          }
+        } else {
+          const int64_t wext = d.cn * d.ck * d.coh * d.cow;
+          if (ts.dirty_max[tpC] >= wext) r = ATC_FAIL_MISMATCH;
+          if (!r && wext > 0) {
+            uint64_t key = 0, mul = 1;
+            for (int k = 0; k < pt.R; ++k) {
+              key += (uint64_t)digit[pt.q[k]] * mul;
+              mul *= (uint64_t)nI;
+            }
+            if (__ldg(pt.table + perm * pt.per_perm + key) == 1) r = ATC_FAIL_MISMATCH;
+          }
+        }
+      }
+      if (r > 0) {
+        cnt[r]++;
+      } else {
+        const unsigned long long slot = atomicAdd(surv_cnt, 1ull);
+        if (slot < surv_cap) surv[slot] = lo + j;
+      }
+      // odometer: next size map (digit 0 fastest), carrying into the permutation
+      for (int q = 0; q < nS; ++q) {
+        if (++digit[q] < nI) break;
+        digit[q] = 0;
+        if (q == nS - 1) ++perm;
+      }
+    }
+  }
+  // per-reason reduction: warp shuffle, one shared atomic per warp, one global per block
+#pragma unroll
+  for (int r = 1; r < ATC_REASON_COUNT; ++r) {
+    unsigned int v = cnt[r];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_hist[r], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < ATC_REASON_COUNT && s_hist[threadIdx.x])
+    atomicAdd(&reason_hist[threadIdx.x], (unsigned long long)s_hist[threadIdx.x]);
+}
+
 // ------------------------------------------------------------------ K2 -------
 constexpr int kConfirmThreads = 256;
 constexpr int kStageDoubles = 6080;  // ~47.5 KB of operand staging per CTA (static smem cap 48 KB)
