@@ -225,23 +225,20 @@ def main():
     bindings = sum(j.count for j in jobs)
     value = bindings / (ms_per_step / 1e3)
 
-    # ---- correctness of what was timed: gather passing sets, MIN-reduce first pass
+    # ---- correctness of what was timed: NCCL all-reduce MIN of the first passing
+    # index and all-gather of the passing sets (paper_2301_11659_b200.shard)
+    from paper_2301_11659_b200 import shard
+
     correct = True
-    firsts = torch.tensor([int(r[0][0]) if r[1] else (1 << 62) for r in results], dtype=torch.int64, device="cuda")
-    passing = [r[0].tolist() for r in results]
-    if dist:
-        dist.all_reduce(firsts, op=dist.ReduceOp.MIN)
-        gathered = [None] * world
-        dist.all_gather_object(gathered, passing)
-        passing = [sorted(sum((g[i] for g in gathered), [])) for i in range(len(jobs))]
     summary = {}
-    for j, pl, fp in zip(jobs, passing, firsts.tolist()):
+    for j, r in zip(jobs, results):
+        pl, first, _ = shard.reduce_results(r[0].tolist(), r[2], dist, device="cuda")
         if j.expected_pass is not None and pl != j.expected_pass:
+            correct = False
+        if (first if first >= 0 else None) != (pl[0] if pl else None):
             correct = False
         if pl:
             summary[f"{j.stem}x{j.spec_name}"] = pl[:4]
-        if pl and fp != pl[0]:
-            correct = False
 
     # ---- e2e through the C ABI with host buffers (pinned), uploads inside the region
     e2e_ms, h2d, d2h = _e2e(args, ctx, jobs, shards, stream, torch, dist)

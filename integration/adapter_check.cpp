@@ -1,0 +1,310 @@
+// adapter_check — end-to-end check of the reference-side adapter on the GPU box.
+//
+// Built by `make -C oracle adapter` against the UNMODIFIED reference (headers from
+// /root/reference/proj/include, liftc_core from oracle/_ref) and libatc_b200.so;
+// it is test infrastructure (oracle/_ref/adapter_check), run by
+// tests/test_integration.py.
+//
+//   adapter_check corpus
+//       for every GEMM/conv corpus program: the reference's own
+//       pipeline::lift_program vs. the same analysis + matching + ranking followed
+//       by liftc::gpu::first_accepted (GPU P2 batch + host P1 on survivors);
+//       prints one JSON line per program with both winners.
+//   adapter_check unpruned <stem> <spec> [tests]
+//       the full unpruned binding space of one program in Appendix C order as the
+//       ranked list: GPU P2 over all of it + host P1 on survivors, timed.
+//   adapter_check dispatch
+//       the lifted program run with make_gpu_dispatch vs make_oracle_dispatch.
+#include <chrono>
+#include <cstdio>
+#include <functional>
+#include <iostream>
+#include <json.hpp>
+
+#include "atc_liftc_adapter.hpp"
+#include "liftc/classifier.hpp"
+#include "liftc/equivalence.hpp"
+#include "liftc/pipeline.hpp"
+#include "liftc/rewriter.hpp"
+#include "liftc/rng.hpp"
+
+extern const std::map<std::string, std::string>& embedded_files();
+
+using namespace liftc;
+using json = nlohmann::json;
+
+namespace {
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+std::vector<api::ApiSpec> default_specs() {
+  std::vector<api::ApiSpec> specs;
+  for (const char* n : {"gemm_rowmajor", "gemm_colmajor", "gemm_rowmajor_ld", "conv2d"})
+    specs.push_back(api::parse_api_spec(embedded_files().at(std::string("specs/") + n + ".json")));
+  return specs;
+}
+
+struct Prog {
+  std::string key, tag, stem, dir, function;
+  minilang::Program prog;
+  pipeline::FixtureMeta meta;
+};
+
+std::vector<Prog> corpus() {
+  std::vector<Prog> out;
+  for (const auto& [k, v] : embedded_files()) {
+    if (k.rfind("corpus/", 0) != 0 || k.substr(k.size() - 3) != ".ml") continue;
+    Prog p;
+    p.key = k;
+    p.tag = k.substr(k.rfind('/') + 1);
+    p.stem = p.tag.substr(0, p.tag.size() - 3);
+    p.dir = k.substr(7, k.rfind('/') - 7);
+    if (p.dir != "gemm" && p.dir != "conv") continue;
+    p.prog = minilang::parse_program(v);
+    auto side = embedded_files().find(k.substr(0, k.size() - 3) + ".json");
+    if (side != embedded_files().end()) p.meta = pipeline::parse_fixture_meta(side->second);
+    p.function = p.meta.function.empty() ? p.prog.functions[0].name : p.meta.function;
+    out.push_back(std::move(p));
+  }
+  return out;
+}
+
+// the analysis half of pipeline.cpp:164-221 (same calls, same order)
+analysis::AnalyzedFunction analyze(const Prog& p, uint64_t fseed, const std::vector<const api::ApiSpec*>& specs) {
+  const auto* f = p.prog.find(p.function);
+  auto live = analysis::detect_liveness(p.prog, *f, fseed, p.meta.rules);
+  analysis::AnalyzedFunction fn;
+  fn.name = p.function;
+  for (const auto& q : f->params) {
+    if (q.kind == minilang::ParamKind::IntScalar) fn.int_params.push_back(q.name);
+    if (q.kind == minilang::ParamKind::FloatScalar) fn.float_params.push_back(q.name);
+  }
+  int max_rank = p.meta.max_rank;
+  for (const auto* s : specs)
+    if (!p.meta.max_rank) max_rank = std::max(max_rank, s->max_rank());
+  auto probe = analysis::assign_probe_values(fn.int_params, p.meta.rules, p.meta.probes, 0);
+  for (const auto& q : f->params) {
+    if (q.kind != minilang::ParamKind::Pointer) continue;
+    analysis::ArrayInfo info;
+    info.name = q.name;
+    info.elem = q.elem;
+    info.liveness = live.classes.at(q.name);
+    try {
+      auto d = analysis::detect_dims(p.prog, *f, q.name, fn.int_params, probe, max_rank);
+      info.has_dims = true;
+      info.dims = d.dims;
+    } catch (const analysis::NoDimsFound&) {
+      info.has_dims = false;
+    }
+    fn.arrays.push_back(std::move(info));
+  }
+  return fn;
+}
+
+int cmd_corpus(atc_ctx* ctx) {
+  auto specs = default_specs();
+  std::vector<std::pair<classifier::FeatureVector, std::string>> ex;
+  for (const auto& [k, v] : embedded_files()) {  // tools/liftc.cpp:92-106 over the whole corpus
+    if (k.rfind("corpus/", 0) != 0 || k.substr(k.size() - 3) != ".ml") continue;
+    auto side = embedded_files().find(k.substr(0, k.size() - 3) + ".json");
+    if (side == embedded_files().end()) continue;
+    auto meta = pipeline::parse_fixture_meta(side->second);
+    if (meta.function.empty() || meta.label.empty()) continue;
+    auto prog = minilang::parse_program(v);
+    if (const auto* fn = prog.find(meta.function)) ex.emplace_back(classifier::extract_features(prog, *fn), meta.label);
+  }
+  auto model = classifier::train_classifier(ex);
+  pipeline::PipelineConfig cfg;
+  cfg.specs = specs;
+  cfg.classifier = &model;
+  cfg.workers = 1;
+  int mismatches = 0;
+  for (const auto& p : corpus()) {
+    auto t0 = std::chrono::steady_clock::now();
+    auto rep = pipeline::lift_program(p.prog, p.tag, p.meta, cfg, nullptr);
+    const double ref_ms = ms_since(t0);
+    const pipeline::FunctionReport* fr = nullptr;
+    for (const auto& f : rep.functions)
+      if (f.function == p.function) fr = &f;
+    json j = {{"stem", p.stem}, {"reference_status", pipeline::status_name(fr->status)}, {"reference_ms", ref_ms}};
+    if (fr->status == pipeline::FunctionStatus::Misclassified) {
+      std::cout << j.dump() << std::endl;
+      continue;
+    }
+    const uint64_t fseed = Rng::mix(cfg.seed, p.tag + ":" + p.function);  // pipeline.cpp:131
+    std::vector<const api::ApiSpec*> lspecs;
+    for (const auto& s : specs)
+      if (s.semantics == fr->class_label) lspecs.push_back(&s);
+    auto fn = analyze(p, fseed, lspecs);
+    t0 = std::chrono::steady_clock::now();
+    std::string gpu_status = "NoMatch", gpu_api;
+    int gpu_rank = -1;
+    matching::CandidateBinding gpu_binding;
+    bool too_many = false;
+    int p1_calls = 0;
+    double gpu_ms = 0;
+    auto recorded = gpu::record_tests(p.prog, p.function, p.meta.rules, Rng::mix(fseed, "post"), cfg.verify_tests);
+    for (const auto* spec : lspecs) {  // pipeline.cpp:227-312 control flow
+      auto ranked = matching::rank_candidates(matching::find_matchings(fn, *spec), cfg.max_candidates);
+      if (ranked.truncated) {
+        too_many = true;
+        continue;
+      }
+      auto lr = gpu::first_accepted(ctx, p.prog, fn, p.function, *spec, ranked.ranked, p.meta.rules, fseed,
+                                    cfg.tests, cfg.verify_tests, &recorded);
+      p1_calls += lr.p1_calls;
+      gpu_ms += lr.gpu_ms;
+      if (lr.winner) {
+        gpu_status = "Lifted";
+        gpu_api = spec->name;
+        gpu_rank = (int)*lr.winner;
+        gpu_binding = ranked.ranked[*lr.winner];
+        break;
+      }
+      if (too_many) break;
+    }
+    if (gpu_status != "Lifted" && too_many) gpu_status = "TooManyCandidates";
+    const double ours_ms = ms_since(t0);
+    bool same = gpu_status == pipeline::status_name(fr->status);
+    if (same && gpu_status == "Lifted")
+      same = gpu_api == fr->winning_api && gpu_rank == fr->manifest.winner_rank &&
+             gpu_binding.arrays == fr->manifest.arrays && gpu_binding.sizes == fr->manifest.sizes;
+    if (!same) ++mismatches;
+    j["gpu_status"] = gpu_status;
+    j["gpu_api"] = gpu_api;
+    j["gpu_rank"] = gpu_rank;
+    j["same_outcome"] = same;
+    j["p1_calls"] = p1_calls;
+    j["candidate_loop_ms"] = ours_ms;
+    j["gpu_p2_ms"] = gpu_ms;
+    std::cout << j.dump() << std::endl;
+  }
+  std::cout << json({{"mismatches", mismatches}}).dump() << std::endl;
+  return mismatches == 0 ? 0 : 1;
+}
+
+int cmd_unpruned(atc_ctx* ctx, const std::string& stem, const std::string& spec_name, int tests) {
+  auto specs = default_specs();
+  const api::ApiSpec* spec = nullptr;
+  for (const auto& s : specs)
+    if (s.name == spec_name) spec = &s;
+  for (const auto& p : corpus()) {
+    if (p.stem != stem) continue;
+    const uint64_t fseed = Rng::mix(0, p.tag + ":" + p.function);
+    auto fn = analyze(p, fseed, {spec});
+    // Appendix C order: array k-permutations (odometer) x size maps (digit 0 fastest)
+    std::vector<matching::CandidateBinding> space;
+    std::vector<std::string> ptrs, ints = fn.int_params;
+    for (const auto& a : fn.arrays) ptrs.push_back(a.name);
+    auto arrays = spec->arrays();
+    auto sizes = spec->size_params();
+    std::vector<int> sel(arrays.size());
+    std::vector<bool> used(ptrs.size(), false);
+    std::vector<std::vector<int>> perms;
+    std::function<void(size_t)> rec = [&](size_t i) {
+      if (i == arrays.size()) {
+        perms.push_back(sel);
+        return;
+      }
+      for (size_t j = 0; j < ptrs.size(); ++j)
+        if (!used[j]) {
+          used[j] = true;
+          sel[i] = (int)j;
+          rec(i + 1);
+          used[j] = false;
+        }
+    };
+    rec(0);
+    size_t maps = 1;
+    for (size_t q = 0; q < sizes.size(); ++q) maps *= ints.size();
+    for (const auto& perm : perms)
+      for (size_t s = 0; s < maps; ++s) {
+        matching::CandidateBinding b;
+        for (size_t a = 0; a < arrays.size(); ++a) b.arrays[arrays[a]->name] = ptrs[perm[a]];
+        size_t x = s;
+        for (size_t q = 0; q < sizes.size(); ++q) {
+          b.sizes[sizes[q]->name] = ints[x % ints.size()];
+          x /= ints.size();
+        }
+        space.push_back(std::move(b));
+      }
+    auto t0 = std::chrono::steady_clock::now();
+    auto lr = gpu::first_accepted(ctx, p.prog, fn, p.function, *spec, space, p.meta.rules, fseed, 30, tests);
+    const double total = ms_since(t0);
+    int64_t passed = 0;
+    for (auto r : lr.p2_reason) passed += r == ATC_PASS;
+    std::cout << json({{"stem", stem}, {"spec", spec_name}, {"bindings", space.size()}, {"tests", tests},
+                       {"p2_passed", passed}, {"winner", lr.winner ? (int64_t)*lr.winner : -1},
+                       {"p1_calls", lr.p1_calls}, {"record_ms", lr.record_ms}, {"gpu_p2_ms", lr.gpu_ms},
+                       {"p1_ms", lr.p1_ms}, {"total_ms", total}})
+                     .dump()
+              << std::endl;
+    return 0;
+  }
+  return 1;
+}
+
+int cmd_dispatch(atc_ctx* ctx) {
+  auto specs = default_specs();
+  int bad = 0;
+  for (const auto& p : corpus()) {
+    if (!p.meta.expect_lift) continue;
+    const api::ApiSpec* spec = nullptr;
+    for (const auto& s : specs)
+      if (s.name == p.meta.api) spec = &s;
+    if (!spec) continue;
+    matching::CandidateBinding b;
+    for (const auto& [k, v] : p.meta.binding_truth) {
+      const auto* ap = spec->find(k);
+      if (ap && ap->kind == api::ApiParamKind::Array) b.arrays[k] = v;
+      if (ap && ap->kind == api::ApiParamKind::IntSize) b.sizes[k] = v;
+    }
+    auto rr = rewriter::rewrite(p.prog, p.function, b, *spec);
+    const uint64_t fseed = Rng::mix(0, p.tag + ":" + p.function);
+    Rng rng(Rng::mix(fseed, "dispatch-check"));
+    std::vector<std::string> int_params;
+    for (const auto& q : p.prog.find(p.function)->params)
+      if (q.kind == minilang::ParamKind::IntScalar) int_params.push_back(q.name);
+    std::map<std::string, long long> sizes;
+    while (!analysis::draw_sizes(int_params, p.meta.rules, rng, sizes)) {
+    }
+    auto img = analysis::build_probe_image(*p.prog.find(p.function), sizes, rng);
+    auto oracle = rewriter::make_oracle_dispatch(*spec);
+    auto gpu_ctx = gpu::make_gpu_dispatch(*spec, ctx);
+    interp::InstrumentationPolicy po, pg;
+    po.dispatch = &oracle;
+    pg.dispatch = &gpu_ctx;
+    auto a = interp::execute(rr.program, p.function, img, po);
+    auto g = interp::execute(rr.program, p.function, img, pg);
+    bool same = a.status == g.status;
+    for (const auto& [name, reg] : a.final.regions) same = same && reg.data == g.final.regions.at(name).data;
+    bad += !same;
+    std::cout << json({{"stem", p.stem}, {"api", spec->name}, {"bit_identical", same}}).dump() << std::endl;
+  }
+  std::cout << json({{"mismatches", bad}}).dump() << std::endl;
+  return bad == 0 ? 0 : 1;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  atc_ctx* ctx = atc_create(0);
+  if (!ctx || atc_last_error(ctx)[0]) {
+    std::fprintf(stderr, "adapter_check: %s\n", ctx ? atc_last_error(ctx) : "no context");
+    return 2;
+  }
+  int rc = 1;
+  try {
+    std::string cmd = argc > 1 ? argv[1] : "corpus";
+    if (cmd == "corpus") rc = cmd_corpus(ctx);
+    if (cmd == "unpruned" && argc >= 4) rc = cmd_unpruned(ctx, argv[2], argv[3], argc > 4 ? std::atoi(argv[4]) : 10);
+    if (cmd == "dispatch") rc = cmd_dispatch(ctx);
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "adapter_check: %s\n", e.what());
+    rc = 1;
+  }
+  atc_destroy(ctx);
+  return rc;
+}

@@ -1,0 +1,66 @@
+// atc_liftc_adapter — the reference-side glue a liftc maintainer adds to use
+// libatc_b200 (include/atc_b200.h).  It is written against the reference's own
+// headers (/root/reference/proj/include/liftc/*.hpp) and replaces exactly two
+// things:
+//
+//   1. the per-candidate loop body of pipeline::lift_function
+//      (src/pipeline.cpp:248-310) — first_accepted() runs P2 for every ranked
+//      candidate of a spec in ONE GPU launch and P1 (check_equivalence) only on
+//      the P2 survivors, in rank order;
+//   2. the oracle DispatchContext (rewriter.cpp:176-181) — make_gpu_dispatch()
+//      returns a handler with the same checks and messages that computes on the
+//      GPU (FP64, bit-exact).
+//
+// Nothing in the reference changes otherwise; the binding-independent half of
+// verify_rewrite (draw_sizes, build_probe_image, the original run) is recorded
+// with the reference's own functions.
+#pragma once
+
+#include <cstdint>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "atc_b200.h"
+#include "liftc/analysis.hpp"
+#include "liftc/api_spec.hpp"
+#include "liftc/interp.hpp"
+#include "liftc/matching.hpp"
+#include "liftc/minilang.hpp"
+
+namespace liftc::gpu {
+
+// atc_spec_desc for a validated ApiSpec (canonical dims, api_spec.cpp:116-119).
+atc_spec_desc encode_spec(const api::ApiSpec& spec);
+
+// The binding-independent half of verify_rewrite (rewriter.cpp:235-251) for
+// tests t = 0..tests-1, kept alive for the upload.
+struct RecordedTests {
+  std::vector<std::string> int_params, ptr_params;
+  std::vector<int64_t> ints;                  // [T][nI]
+  std::vector<int32_t> is_f32, test_ok;       // [nP], [T]
+  std::vector<int64_t> region_len;            // [nP]
+  std::vector<std::vector<double>> init, fin;  // [T*nP]
+  int T = 0;
+};
+RecordedTests record_tests(const minilang::Program& prog, const std::string& function,
+                           const api::SizeRules& rules, uint64_t p2seed, int tests);
+
+struct LoopResult {
+  std::optional<size_t> winner;  // rank of the accepted candidate
+  std::vector<int8_t> p2_fail_t, p2_reason;
+  int p1_calls = 0;
+  double gpu_ms = 0.0, record_ms = 0.0, p1_ms = 0.0;
+};
+
+// Replacement of pipeline.cpp:248-310 for one spec: P2 (GPU, batched) for all
+// ranked candidates, then P1 (host) on the survivors in rank order.
+LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const analysis::AnalyzedFunction& fn,
+                          const std::string& function, const api::ApiSpec& spec,
+                          const std::vector<matching::CandidateBinding>& ranked, const api::SizeRules& rules,
+                          uint64_t fseed, int p1_tests, int verify_tests, const RecordedTests* recorded = nullptr);
+
+// DispatchContext whose handler is run_dispatch on the GPU (atc_dispatch).
+interp::DispatchContext make_gpu_dispatch(const api::ApiSpec& spec, atc_ctx* ctx);
+
+}  // namespace liftc::gpu
