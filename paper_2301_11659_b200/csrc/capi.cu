@@ -19,20 +19,21 @@ __global__ void k_build_dirty(TestsetView ts, int32_t* dirty_pos, int32_t* dirty
 __global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, int budget,
                          int32_t* keys, uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                          unsigned long long* reason_hist);
-constexpr int kMaxPos0Roles = 5;
-struct Pos0Table {
-  int R;
-  int q[kMaxPos0Roles];
-  uint64_t per_perm;
-  const uint8_t* table;
-};
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out);
 __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
                               uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                               unsigned long long* reason_hist);
+template <int SEM, int NS, bool I32, uint32_t Q0MASK>
+__global__ void k_screen_rows(TestsetView ts, SpecView sp, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
+                              uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
+                              unsigned long long* surv_cnt, unsigned long long* reason_hist);
 __global__ void k_confirm(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
-                          const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys);
+                          const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
+                          const uint32_t* sel, const unsigned long long* sel_cnt, int t_begin);
+__global__ void k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
+                             const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
+                             uint32_t* next, unsigned long long* next_cnt);
 __global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
                              const int32_t* surv_keys, int32_t* keys);
 __global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason);
@@ -392,7 +393,8 @@ int screen_budget(const SpecView& sp) { return sp.sem == ATC_SEM_GEMM ? 16 : 2; 
 // Runs K1 + K2 over `n` bindings; survivors/keys live in ctx scratch.
 int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, const BindingSource& src,
              uint64_t n, int32_t* keys, uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
-             int32_t* surv_keys, unsigned long long* hist, cudaStream_t st, const Pos0Table* pt = nullptr) {
+             int32_t* surv_keys, unsigned long long* hist, cudaStream_t st, const Pos0Table* pt = nullptr,
+             const RowPlan* plan = nullptr) {
   if (n == 0) return ATC_OK;
   const uint64_t blocks_needed = (n + kScreenThreads - 1) / kScreenThreads;
   const unsigned grid = (unsigned)std::min<uint64_t>(blocks_needed, (uint64_t)ctx->sm_count * 32);
@@ -409,7 +411,51 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     cudaEventRecord(e1.first, st);
     ctx->prof_bindings += (long long)n;
   }
-  if (pt) {
+  if (plan) {
+    const uint64_t rows = n / ts->nI + 2;
+    const unsigned g2 = (unsigned)std::min<uint64_t>((rows + kScreenThreads - 1) / kScreenThreads,
+                                                     (uint64_t)ctx->sm_count * 16);
+    const uint64_t b = src.begin, e = src.begin + n;
+    // 32-bit index arithmetic when every t=0 size is <= 200 (any product of 4 sizes < 2^31)
+    int64_t umax = 0;
+    for (int i = 0; i < ts->nI; ++i) umax = std::max<int64_t>(umax, std::llabs(ts->h_ints[i]));
+    const bool i32 = umax <= 200;
+    uint32_t q0mask = 0;  // roles bound to digit 0 (after fallbacks)
+    for (int rr = 0; rr < ATC_SZ_COUNT; ++rr)
+      if (plan->role_q[rr] == 0) q0mask |= 1u << rr;
+    constexpr uint32_t kDyn = 0xFFFFFFFFu;
+#define ATC_LAUNCH_ROWS(SEM, NS, MASK)                                                                               \
+  do {                                                                                                              \
+    if (i32)                                                                                                        \
+      k_screen_rows<SEM, NS, true, MASK><<<g2, kScreenThreads, 0, st>>>(ts->view, sp, src.perms, src.size_maps, b, \
+                                                                        e, *plan, surv, surv_cap, surv_cnt, hist); \
+    else                                                                                                            \
+      k_screen_rows<SEM, NS, false, MASK><<<g2, kScreenThreads, 0, st>>>(ts->view, sp, src.perms, src.size_maps,  \
+                                                                         b, e, *plan, surv, surv_cap, surv_cnt,    \
+                                                                         hist);                                    \
+  } while (0)
+    constexpr uint32_t kM = 1u << ATC_SZ_M, kMcol = (1u << ATC_SZ_M) | (1u << ATC_SZ_LDA) | (1u << ATC_SZ_LDC);
+    constexpr uint32_t kCN = 1u << ATC_SZ_CN;
+    if (sp.sem == ATC_SEM_GEMM && sp.nS == 3) {
+      if (q0mask == kM)
+        ATC_LAUNCH_ROWS(ATC_SEM_GEMM, 3, kM);
+      else if (q0mask == kMcol)
+        ATC_LAUNCH_ROWS(ATC_SEM_GEMM, 3, kMcol);
+      else
+        ATC_LAUNCH_ROWS(ATC_SEM_GEMM, 3, kDyn);
+    } else if (sp.sem == ATC_SEM_GEMM && sp.nS == 6) {
+      if (q0mask == kM)
+        ATC_LAUNCH_ROWS(ATC_SEM_GEMM, 6, kM);
+      else
+        ATC_LAUNCH_ROWS(ATC_SEM_GEMM, 6, kDyn);
+    } else {
+      if (q0mask == kCN)
+        ATC_LAUNCH_ROWS(ATC_SEM_CONV2D, 9, kCN);
+      else
+        ATC_LAUNCH_ROWS(ATC_SEM_CONV2D, 9, kDyn);
+    }
+#undef ATC_LAUNCH_ROWS
+  } else if (pt) {
     const uint64_t runs = (n + 15) / 16;
     const unsigned g2 = (unsigned)std::min<uint64_t>((runs + kScreenThreads - 1) / kScreenThreads,
                                                      (uint64_t)ctx->sm_count * 16);
@@ -428,7 +474,18 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     e2 = ev_pair();
     cudaEventRecord(e2.first, st);
   }
-  k_confirm<<<(unsigned)ctx->sm_count * 8, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys);
+  // K2a: warp per survivor at t = 0; K2b: CTA per (t = 0 passer, t >= 1)
+  uint32_t* next = (uint32_t*)atc_ctx_scratch(ctx, 18, surv_cap * 4 + 16);
+  unsigned long long* next_cnt = (unsigned long long*)atc_ctx_scratch(ctx, 19, 64);
+  if (!next || !next_cnt) {
+    atc_set_error(ctx, "scratch allocation failed (K2)");
+    return ATC_ERR_CUDA;
+  }
+  cudaMemsetAsync(next_cnt, 0, 8, st);
+  k_confirm_t0<<<(unsigned)ctx->sm_count * 8, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys,
+                                                            next, next_cnt);
+  k_confirm<<<(unsigned)ctx->sm_count * 8, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, next,
+                                                         next_cnt, 1);
   if (ctx->prof) {
     cudaEventRecord(e2.second, st);
     ctx->prof_confirm.push_back(e2);
@@ -572,6 +629,32 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
   }
   const uint64_t table_bytes = pt.per_perm * (uint64_t)n_perms;
   if (table_bytes > (256ull << 20)) use_table = false;
+  // row-hoisted screen (k_screen_rows) for the bundled spec shapes
+  RowPlan plan{};
+  bool use_rows = use_table && ((sp.sem == ATC_SEM_GEMM && (sp.nS == 3 || sp.nS == 6)) ||
+                                (sp.sem == ATC_SEM_CONV2D && sp.nS == 9));
+  if (use_rows) {
+    for (int a = 0; a < sp.nA; ++a) {
+      plan.dim_mask[a] = 0;
+      for (int d = 0; d < sp.ndims[a]; ++d) {
+        if (plan.dim_mask[a] & (1u << sp.dims[a][d])) use_rows = false;  // repeated dim: not expressible
+        plan.dim_mask[a] |= 1u << sp.dims[a][d];
+      }
+    }
+    for (int r = 0; r < ATC_SZ_COUNT; ++r) plan.role_q[r] = sp.role_size[r];
+    if (sp.sem == ATC_SEM_GEMM) {  // equivalence.cpp:46-48 fallbacks
+      const bool row = sp.layout == ATC_LAYOUT_ROW;
+      if (plan.role_q[ATC_SZ_LDA] < 0) plan.role_q[ATC_SZ_LDA] = row ? sp.role_size[ATC_SZ_K] : sp.role_size[ATC_SZ_M];
+      if (plan.role_q[ATC_SZ_LDB] < 0) plan.role_q[ATC_SZ_LDB] = row ? sp.role_size[ATC_SZ_N] : sp.role_size[ATC_SZ_K];
+      if (plan.role_q[ATC_SZ_LDC] < 0) plan.role_q[ATC_SZ_LDC] = row ? sp.role_size[ATC_SZ_N] : sp.role_size[ATC_SZ_M];
+    }
+    uint64_t mul = 1;
+    for (int q = 0; q < ATC_MAX_SIZES; ++q) plan.key_stride[q] = 0;
+    for (int k = 0; k < pt.R; ++k) {
+      plan.key_stride[pt.q[k]] += mul;
+      mul *= (uint64_t)ts->nI;
+    }
+  }
   if (use_table) {
     uint8_t* tab = (uint8_t*)atc_ctx_scratch(ctx, 17, table_bytes + 16);
     if (!tab) {
@@ -579,6 +662,7 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
       return ATC_ERR_CUDA;
     }
     pt.table = tab;
+    plan.pt = pt;
     k_pos0_table<<<(unsigned)std::min<uint64_t>((table_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16), 256, 0,
                    st>>>(ts->view, sp, d_perms, n_perms, pt, tab);
   }
@@ -591,7 +675,7 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
     const uint64_t hi = std::min(end, lo + chunk);
     BindingSource src{nullptr, nullptr, d_perms, size_maps, lo, 1};
     int rc = run_eval(ctx, sp, ts, src, hi - lo, nullptr, surv, chunk_cap, cnt, skeys, hist, st,
-                      use_table ? &pt : nullptr);
+                      use_table ? &pt : nullptr, use_rows ? &plan : nullptr);
     if (rc) return rc;
     unsigned long long c = 0;
     if (!atc_cuda_ok(ctx, cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, st), "D2H") ||

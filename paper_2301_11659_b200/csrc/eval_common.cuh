@@ -65,6 +65,23 @@ struct BindingSource {
   int enumerated;
 };
 
+// Position-0 verdict table of an enumerated space (k_pos0_table).
+constexpr int kMaxPos0Roles = 5;
+struct Pos0Table {
+  int R;                 // number of roles the position-0 value depends on
+  int q[kMaxPos0Roles];  // size-param index of each role
+  uint64_t per_perm;     // nI^R
+  const uint8_t* table;  // [n_perms][nI^R]: 0 match, 1 mismatch, 2 not tabulated
+};
+
+// Per-launch plan of the row-hoisted screen (k_screen_rows).
+struct RowPlan {
+  uint32_t dim_mask[ATC_MAX_ARRAYS];   // per API array: bitmask of its dims over size params
+  int32_t role_q[ATC_SZ_COUNT];        // per role: size-param index (fallbacks resolved), -1 absent
+  Pos0Table pt;
+  uint64_t key_stride[ATC_MAX_SIZES];  // table-key contribution of each size-param digit
+};
+
 enum : int32_t { kUndecided = -2 };
 
 // Encoded per-binding result: t * 8 + reason; kPassKey when every test passed.

@@ -212,14 +212,6 @@ __global__ void __launch_bounds__(256) k_screen(TestsetView ts, SpecView sp, Bin
 // The per-binding screen is then integer-only: run_dispatch extent checks,
 // access bounds, the dirty-set (write-set) check, one table lookup.  Bindings
 // that pass all of it go to K2, which re-checks every test completely.
-constexpr int kMaxPos0Roles = 5;
-
-struct Pos0Table {
-  int R;                       // number of roles the position-0 value depends on
-  int q[kMaxPos0Roles];        // size-param index of each role
-  uint64_t per_perm;           // nI^R
-  const uint8_t* table;        // [n_perms][nI^R]: 0 match, 1 mismatch, 2 not tabulated (read outside region)
-};
 
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out) {
@@ -366,7 +358,8 @@ __global__ void __launch_bounds__(256) k_screen_enum(TestsetView ts, SpecView sp
         }
       }
       if (r > 0) {
-        cnt[r]++;
+#pragma unroll
+        for (int rr = 1; rr < ATC_REASON_COUNT; ++rr) cnt[rr] += (r == rr);
       } else {
         const unsigned long long slot = atomicAdd(surv_cnt, 1ull);
         if (slot < surv_cap) surv[slot] = lo + j;
@@ -391,25 +384,131 @@ __global__ void __launch_bounds__(256) k_screen_enum(TestsetView ts, SpecView sp
     atomicAdd(&reason_hist[threadIdx.x], (unsigned long long)s_hist[threadIdx.x]);
 }
 
+
 // ------------------------------------------------------------------ K2 -------
 constexpr int kConfirmThreads = 256;
 constexpr int kStageDoubles = 6080;  // ~47.5 KB of operand staging per CTA (static smem cap 48 KB)
 
+// K2a: one WARP per survivor, test t = 0 only.  Most K1 survivors agree with the
+// user program at output position 0 but not elsewhere; a warp checks 32 output
+// positions per step (lanes split the write set, __any_sync early exit) and the
+// dirty set in parallel.  Survivors of t = 0 are appended to `next` for K2b.
+__global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src,
+                                                    const uint64_t* surv, const unsigned long long* surv_cnt,
+                                                    uint64_t surv_cap, int32_t* surv_keys, uint32_t* next,
+                                                    unsigned long long* next_cnt) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long cnt = *surv_cnt;
+  if (cnt > surv_cap) cnt = surv_cap;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t si = (uint64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; si < cnt; si += warps) {
+    int ptr_of[ATC_MAX_ARRAYS], int_of[ATC_MAX_SIZES];
+    decode_binding(src, sp, ts.nI, surv[si], ptr_of, int_of);
+    int64_t sz[ATC_MAX_SIZES];
+    for (int q = 0; q < sp.nS; ++q) sz[q] = ts.ints[int_of[q]];
+    int r = 0;
+    if (!ts.test_ok[0]) r = ATC_FAIL_TESTSET;
+    if (!r) r = extent_check(sp, sz, ptr_of, ts.region_len);
+    Dims d;
+    resolve_dims(sp, sz, d);
+    if (!r) r = ub_check(sp, d, ptr_of, ts.region_len);
+    if (!r) {
+      const int pA = ptr_of[sp.arr_of_role[0]], pB = ptr_of[sp.arr_of_role[1]], pC = ptr_of[sp.arr_of_role[2]];
+      const double* __restrict__ A = ts.init + ts.region_off[pA];
+      const double* __restrict__ B = ts.init + ts.region_off[pB];
+      const double* __restrict__ F = ts.fin + ts.region_off[pC];
+      const bool f32 = ts.is_f32[pC] != 0;
+      const int ndirty = ts.dirty_cnt[pC];
+      const int32_t* dirty = ts.dirty_pos + ts.dirty_off[pC];
+      bool bad = false;
+      if (sp.sem == ATC_SEM_GEMM) {
+        const bool row = sp.layout == ATC_LAYOUT_ROW;
+        const int m = (int)d.m, n = (int)d.n, k = (int)d.k, lda = (int)d.lda, ldb = (int)d.ldb, ldc = (int)d.ldc;
+        if (m < 1 || n < 1) {
+          bad = ndirty > 0;
+        } else {
+          for (int e = lane; e < ndirty && !bad; e += 32) bad = !gemm_written(row, __ldg(dirty + e), m, n, ldc);
+          bad = __any_sync(0xffffffffu, bad);
+          const bool overlap = row ? (ldc < n && m > 1) : (ldc < m && n > 1);
+          const int outs = m * n;
+          for (int o0 = 0; o0 < outs && !bad; o0 += 32) {
+            const int o = o0 + lane;
+            bool mm = false;
+            if (o < outs) {
+              const int i = o / n, j = o - (o / n) * n;
+              if (!overlap || gemm_last_writer(row, i, j, m, ldc)) {
+                double acc = 0.0;
+                if (row)
+                  for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(__ldg(A + i * lda + p), __ldg(B + p * ldb + j)));
+                else
+                  for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(__ldg(A + p * lda + i), __ldg(B + j * ldb + p)));
+                mm = mismatch(round_region(acc, f32), __ldg(F + (row ? i * ldc + j : j * ldc + i)), f32);
+              }
+            }
+            bad = __any_sync(0xffffffffu, mm);
+          }
+        }
+      } else {
+        const int N = (int)d.cn, C = (int)d.cc, H = (int)d.ch, W = (int)d.cw, K = (int)d.ck, R = (int)d.cr,
+                  S = (int)d.cs, OH = (int)d.coh, OW = (int)d.cow;
+        const int64_t wext = (int64_t)N * K * OH * OW;
+        bad = ts.dirty_max[pC] >= wext;
+        for (int o0 = 0; o0 < (int)wext && !bad; o0 += 32) {
+          const int o = o0 + lane;
+          bool mm = false;
+          if (o < wext) {
+            int rem = o;
+            const int x = rem % OW; rem /= OW;
+            const int y = rem % OH; rem /= OH;
+            const int q = rem % K;
+            const int b = rem / K;
+            double acc = 0.0;
+            for (int z = 0; z < C; ++z)
+              for (int u = 0; u < R; ++u) {
+                const double* in = A + ((b * C + z) * H + y + u) * W + x;
+                const double* wt = B + ((q * C + z) * R + u) * S;
+                for (int v = 0; v < S; ++v) acc = dadd(acc, dmul(__ldg(in + v), __ldg(wt + v)));
+              }
+            mm = mismatch(round_region(acc, f32), __ldg(F + o), f32);
+          }
+          bad = __any_sync(0xffffffffu, mm);
+        }
+      }
+      if (bad) r = ATC_FAIL_MISMATCH;
+    }
+    if (lane == 0) {
+      if (r) {
+        surv_keys[si] = fail_key(0, r);
+      } else {
+        surv_keys[si] = kPassKey;
+        const unsigned long long slot = atomicAdd(next_cnt, 1ull);
+        next[slot] = (uint32_t)si;
+      }
+    }
+  }
+}
+
+// K2b (and the explicit-list confirm): one CTA per (survivor, t) for t >= t_begin.
+// With `sel`, the survivors are surv[sel[0..*sel_cnt)] (the t = 0 passers of K2a).
 __global__ void __launch_bounds__(kConfirmThreads) k_confirm(TestsetView ts, SpecView sp, BindingSource src,
                                                              const uint64_t* surv,
                                                              const unsigned long long* surv_cnt,
-                                                             uint64_t surv_cap, int32_t* surv_keys) {
+                                                             uint64_t surv_cap, int32_t* surv_keys,
+                                                             const uint32_t* sel,
+                                                             const unsigned long long* sel_cnt, int t_begin) {
   __shared__ double s_stage[kStageDoubles];
   __shared__ int s_fail;
   __shared__ int s_ptr[ATC_MAX_ARRAYS];
   __shared__ int64_t s_sz[ATC_MAX_SIZES];
   __shared__ int s_pre;  // result of the per-(b,t) scalar prologue
-  unsigned long long cnt = *surv_cnt;
+  unsigned long long cnt = sel ? *sel_cnt : *surv_cnt;
   if (cnt > surv_cap) cnt = surv_cap;
-  const uint64_t work = cnt * (uint64_t)ts.T;
+  const int nt = ts.T - t_begin;
+  const uint64_t work = nt > 0 ? cnt * (uint64_t)nt : 0;
   for (uint64_t w = blockIdx.x; w < work; w += gridDim.x) {
-    const uint64_t si = w / ts.T;
-    const int t = (int)(w - si * ts.T);
+    const uint64_t wi = w / nt;
+    const uint64_t si = sel ? sel[wi] : wi;
+    const int t = t_begin + (int)(w - wi * nt);
     const uint64_t idx = surv[si];
     if (threadIdx.x == 0) {
       int ptr_of[ATC_MAX_ARRAYS], int_of[ATC_MAX_SIZES];

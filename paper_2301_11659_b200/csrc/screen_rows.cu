@@ -1,0 +1,214 @@
+// K1 for enumerated spaces: the row-hoisted integer screen (k_screen_rows).
+//
+// Predicate: the t = 0 part of eval_common.cuh (run_dispatch extent checks,
+// access bounds, write-set/dirty check) plus the tabulated position-0 verdict
+// of k_pos0_table (eval_kernels.cu); bindings that pass go to K2, which
+// re-checks every output of every test.  Equivalent to k_screen_enum, which it
+// replaces for the bundled spec shapes (gemm with 3 or 6 size params, conv2d
+// with 9).
+//
+// Organisation (SURVEY.md Appendix C order): a thread owns one "row" — a fixed
+// array permutation and fixed size-map digits 1..NS-1 — and walks the nI values
+// of digit 0, the fastest-varying size param.  Everything independent of digit
+// 0 is computed once per row: the row decode (NS-1 divisions), the role values,
+// extents of arrays that do not use it, the table key, the dirty maximum.  NS
+// and the semantics are template parameters so the per-size arrays unroll into
+// registers, and I32 selects 32-bit index arithmetic when the host has proven
+// every product fits (max t=0 size <= 215, so any product of 4 sizes < 2^31).
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "eval_common.cuh"
+
+namespace atc {
+
+template <int NS>
+__device__ __forceinline__ int64_t pick(const int64_t (&u)[NS], int q) {
+  int64_t v = 0;
+#pragma unroll
+  for (int i = 0; i < NS; ++i)
+    if (q == i) v = u[i];
+  return v;
+}
+
+// Q0MASK: compile-time set of roles bound to digit 0 (bit per ATC_SZ_* role), so
+// that every quantity not depending on digit 0 is loop-invariant and hoisted by
+// the compiler; kQ0Dynamic takes the set from the plan at run time.
+constexpr uint32_t kQ0Dynamic = 0xFFFFFFFFu;
+
+template <int SEM, int NS, bool I32, uint32_t Q0MASK>
+__global__ void __launch_bounds__(256) k_screen_rows(TestsetView ts, SpecView sp, const uint8_t* perms,
+                                                      uint64_t size_maps, uint64_t begin, uint64_t end, RowPlan plan,
+                                                      uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
+                                                      unsigned long long* reason_hist) {
+  using I = typename std::conditional<I32, int32_t, int64_t>::type;
+  __shared__ int64_t s_u0[kMaxInts];
+  __shared__ unsigned int s_hist[ATC_REASON_COUNT];
+  if (threadIdx.x < ts.nI) s_u0[threadIdx.x] = ts.ints[threadIdx.x];
+  if (threadIdx.x < ATC_REASON_COUNT) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int nI = ts.nI;
+  const bool test_ok0 = ts.test_ok[0] != 0;
+  const bool row_major = sp.layout == ATC_LAYOUT_ROW;
+  unsigned int cnt1 = 0, cnt2 = 0, cnt3 = 0, cnt4 = 0;
+  const uint64_t row_lo = begin / nI, row_hi = (end + nI - 1) / nI;
+  for (uint64_t row = row_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; row < row_hi;
+       row += (uint64_t)gridDim.x * blockDim.x) {
+    // ---------------- per-row setup ----------------
+    const uint64_t g0 = row * nI;
+    const uint64_t perm = g0 / size_maps;
+    uint64_t s = (g0 - perm * size_maps) / nI;
+    int digit[NS];
+    int64_t u[NS];
+    digit[0] = 0;
+    u[0] = 0;
+#pragma unroll
+    for (int q = 1; q < NS; ++q) {
+      const uint64_t dq = s / (uint64_t)nI;
+      digit[q] = (int)(s - dq * (uint64_t)nI);
+      s = dq;
+      u[q] = s_u0[digit[q]];
+    }
+    int ptr_of[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ptr_of[a] = perms[perm * 3 + a];
+    const I len_a0 = (I)ts.region_len[ptr_of[0]], len_a1 = (I)ts.region_len[ptr_of[1]],
+            len_a2 = (I)ts.region_len[ptr_of[2]];
+    const int pC = ptr_of[sp.arr_of_role[2]];
+    const I lenA = (I)ts.region_len[ptr_of[sp.arr_of_role[0]]];
+    const I lenB = (I)ts.region_len[ptr_of[sp.arr_of_role[1]]];
+    const I lenC = (I)ts.region_len[pC];
+    // extents without digit 0; any non-digit-0 dim < 1 fails every binding of the row
+    I ext_rest[3];
+    bool bad_rest = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      I e = 1;
+#pragma unroll
+      for (int q = 1; q < NS; ++q)
+        if (plan.dim_mask[a] & (1u << q)) {
+          e *= (I)u[q];
+          bad_rest |= u[q] < 1;
+        }
+      ext_rest[a] = e;
+    }
+    const bool use0_a0 = plan.dim_mask[0] & 1u, use0_a1 = plan.dim_mask[1] & 1u, use0_a2 = plan.dim_mask[2] & 1u;
+    const bool use0_any = use0_a0 || use0_a1 || use0_a2;
+    // role values not bound to digit 0
+    I rv[ATC_SZ_COUNT];
+    bool r0[ATC_SZ_COUNT];
+#pragma unroll
+    for (int rr = 0; rr < ATC_SZ_COUNT; ++rr) {
+      const int q = plan.role_q[rr];
+      r0[rr] = q == 0;
+      rv[rr] = q <= 0 ? 0 : (I)pick<NS>(u, q);
+    }
+    uint64_t key_rest = perm * plan.pt.per_perm;
+#pragma unroll
+    for (int q = 1; q < NS; ++q) key_rest += (uint64_t)digit[q] * plan.key_stride[q];
+    const uint64_t key0 = plan.key_stride[0];
+    const int row_tab = key0 == 0 ? __ldg(plan.pt.table + key_rest) : -1;
+    const I dmaxC = (I)ts.dirty_max[pC];
+    const int ndirty = ts.dirty_cnt[pC];
+    const int32_t* dirty = ts.dirty_pos + ts.dirty_off[pC];
+
+    const int v_lo = g0 < begin ? (int)(begin - g0) : 0;
+    const int v_hi = g0 + nI > end ? (int)(end - g0) : nI;
+    // ---------------- digit-0 loop ----------------
+    for (int v = v_lo; v < v_hi; ++v) {
+      const I uv = (I)s_u0[v];
+      auto role = [&](int rr) -> I {
+        if (Q0MASK == kQ0Dynamic) return r0[rr] ? uv : rv[rr];
+        return ((Q0MASK >> rr) & 1u) ? uv : rv[rr];
+      };
+      int r = test_ok0 ? 0 : ATC_FAIL_TESTSET;
+      if (!r) {  // run_dispatch extent checks (rewriter.cpp:136-148)
+        const I e0 = use0_a0 ? ext_rest[0] * uv : ext_rest[0];
+        const I e1 = use0_a1 ? ext_rest[1] * uv : ext_rest[1];
+        const I e2 = use0_a2 ? ext_rest[2] * uv : ext_rest[2];
+        if (bad_rest || (use0_any && uv < 1) || e0 > len_a0 || e1 > len_a1 || e2 > len_a2) r = ATC_FAIL_DISPATCH;
+      }
+      if (!r) {
+        int tv = -1;  // position-0 table verdict, when position 0 is written
+        if (SEM == ATC_SEM_GEMM) {
+          const I m = role(ATC_SZ_M), n = role(ATC_SZ_N), k = role(ATC_SZ_K);
+          const I lda = role(ATC_SZ_LDA), ldb = role(ATC_SZ_LDB), ldc = role(ATC_SZ_LDC);
+          if (m >= 1 && n >= 1 && k >= 1) {
+            if (lda < 0 || ldb < 0 || ldc < 0) {
+              r = ATC_FAIL_UB;
+            } else {
+              const I amax = row_major ? (m - 1) * lda + (k - 1) : (k - 1) * lda + (m - 1);
+              const I bmax = row_major ? (k - 1) * ldb + (n - 1) : (n - 1) * ldb + (k - 1);
+              const I cmax = row_major ? (m - 1) * ldc + (n - 1) : (n - 1) * ldc + (m - 1);
+              if (amax >= lenA || bmax >= lenB || cmax >= lenC) r = ATC_FAIL_UB;
+            }
+          }
+          if (!r) {
+            if (m < 1 || n < 1) {
+              if (ndirty) r = ATC_FAIL_MISMATCH;
+            } else {
+              for (int e = 0; e < ndirty; ++e)
+                if (!gemm_written(row_major, __ldg(dirty + e), (int)m, (int)n, (int)ldc)) {
+                  r = ATC_FAIL_MISMATCH;
+                  break;
+                }
+              if (!r) tv = row_tab >= 0 ? row_tab : __ldg(plan.pt.table + key_rest + (uint64_t)v * key0);
+            }
+          }
+        } else {
+          const I cn = role(ATC_SZ_CN), cc = role(ATC_SZ_CC), ch = role(ATC_SZ_CH), cw = role(ATC_SZ_CW);
+          const I ck = role(ATC_SZ_CK), cr = role(ATC_SZ_CR), cs = role(ATC_SZ_CS);
+          const I coh = plan.role_q[ATC_SZ_COH] >= 0 ? role(ATC_SZ_COH) : ch - cr + 1;
+          const I cow = plan.role_q[ATC_SZ_COW] >= 0 ? role(ATC_SZ_COW) : cw - cs + 1;
+          // grouped so that, with tc_n on digit 0, the n-free factors are loop-invariant
+          const I wext = cn * (ck * (coh * cow));
+          if (cn >= 1 && ck >= 1 && coh >= 1 && cow >= 1 && cc >= 1 && cr >= 1 && cs >= 1) {
+            // = (((cn-1)*cc + (cc-1))*ch + (coh-1) + (cr-1))*cw + (cow-1) + (cs-1), expanded
+            const I imax = cn * (cc * (ch * cw)) - ch * cw + (coh + cr - 2) * cw + (cow + cs - 2);
+            const I wmax = ck * cc * cr * cs - 1;
+            if (imax >= lenA || imax < 0 || wmax >= lenB || wext - 1 >= lenC) r = ATC_FAIL_UB;
+          }
+          if (!r && dmaxC >= wext) r = ATC_FAIL_MISMATCH;
+          if (!r && wext > 0) tv = row_tab >= 0 ? row_tab : __ldg(plan.pt.table + key_rest + (uint64_t)v * key0);
+        }
+        if (tv == 1) r = ATC_FAIL_MISMATCH;
+      }
+      cnt1 += r == ATC_FAIL_MISMATCH;
+      cnt2 += r == ATC_FAIL_DISPATCH;
+      cnt3 += r == ATC_FAIL_TESTSET;
+      cnt4 += r == ATC_FAIL_UB;
+      if (r == 0) {
+        const unsigned long long slot = atomicAdd(surv_cnt, 1ull);
+        if (slot < surv_cap) surv[slot] = g0 + v - begin;
+      }
+    }
+  }
+  // per-reason reduction: warp shuffle, one shared atomic per warp, one global per block
+  unsigned int cnt[ATC_REASON_COUNT] = {0, cnt1, cnt2, cnt3, cnt4};
+#pragma unroll
+  for (int r = 1; r < ATC_REASON_COUNT; ++r) {
+    unsigned int v = cnt[r];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_hist[r], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < ATC_REASON_COUNT && s_hist[threadIdx.x])
+    atomicAdd(&reason_hist[threadIdx.x], (unsigned long long)s_hist[threadIdx.x]);
+}
+
+#define ATC_ROWS_INST(SEM, NS, I32, MASK)                                                                        \
+  template __global__ void k_screen_rows<SEM, NS, I32, MASK>(TestsetView, SpecView, const uint8_t*, uint64_t,    \
+                                                             uint64_t, uint64_t, RowPlan, uint64_t*, uint64_t,   \
+                                                             unsigned long long*, unsigned long long*);
+#define ATC_ROWS_INST2(SEM, NS, MASK) ATC_ROWS_INST(SEM, NS, true, MASK) ATC_ROWS_INST(SEM, NS, false, MASK)
+ATC_ROWS_INST2(ATC_SEM_GEMM, 3, kQ0Dynamic)
+ATC_ROWS_INST2(ATC_SEM_GEMM, 6, kQ0Dynamic)
+ATC_ROWS_INST2(ATC_SEM_CONV2D, 9, kQ0Dynamic)
+// the bundled specs: conv2d digit 0 = tc_n; gemm digit 0 = tc_m (col-major: lda/ldc fall back to m)
+ATC_ROWS_INST2(ATC_SEM_CONV2D, 9, 1u << ATC_SZ_CN)
+ATC_ROWS_INST2(ATC_SEM_GEMM, 3, 1u << ATC_SZ_M)
+ATC_ROWS_INST2(ATC_SEM_GEMM, 3, (1u << ATC_SZ_M) | (1u << ATC_SZ_LDA) | (1u << ATC_SZ_LDC))
+ATC_ROWS_INST2(ATC_SEM_GEMM, 6, 1u << ATC_SZ_M)
+
+}  // namespace atc
