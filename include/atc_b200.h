@@ -128,6 +128,7 @@ typedef struct {
   int64_t confirm_launches;
   int64_t survivors;       /* bindings handed from K1 to K2                   */
   int64_t bindings;        /* bindings screened                               */
+  int64_t kernels;         /* libatc kernels launched                          */
 } atc_profile;
 int atc_profile_start(atc_ctx* ctx);
 int atc_profile_read(atc_ctx* ctx, atc_profile* out);

@@ -79,6 +79,7 @@ class Profile(C.Structure):
         ("confirm_launches", C.c_int64),
         ("survivors", C.c_int64),
         ("bindings", C.c_int64),
+        ("kernels", C.c_int64),
     ]
 
 

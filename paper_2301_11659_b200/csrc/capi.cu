@@ -81,6 +81,38 @@ void* atc_ctx_scratch(atc_ctx* ctx, int slot, size_t bytes) {
   return ctx->scratch[slot];
 }
 
+// Device-memory pool for test-set uploads: freed blocks are kept per context and
+// reused (best fit), so a per-function upload costs no cudaMalloc/cudaFree.
+void* atc_pool_alloc(atc_ctx* ctx, size_t bytes) {
+  bytes = (bytes + 255) / 256 * 256;
+  size_t best = SIZE_MAX, bi = 0;
+  for (size_t i = 0; i < ctx->pool_free.size(); ++i)
+    if (ctx->pool_free[i].second >= bytes && ctx->pool_free[i].second < best) {
+      best = ctx->pool_free[i].second;
+      bi = i;
+    }
+  if (best != SIZE_MAX) {
+    auto blk = ctx->pool_free[bi];
+    ctx->pool_free.erase(ctx->pool_free.begin() + bi);
+    ctx->pool_used[blk.first] = blk.second;
+    return blk.first;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  ctx->pool_used[p] = bytes;
+  return p;
+}
+
+void atc_pool_free(atc_ctx* ctx, void* p) {
+  auto it = ctx->pool_used.find(p);
+  if (it == ctx->pool_used.end()) {
+    cudaFree(p);
+    return;
+  }
+  ctx->pool_free.emplace_back(p, it->second);
+  ctx->pool_used.erase(it);
+}
+
 namespace {
 
 bool build_spec_view(atc_ctx* ctx, const atc_spec_desc* s, SpecView& v) {
@@ -196,6 +228,8 @@ void atc_destroy(atc_ctx* ctx) {
     cudaSetDevice(ctx->device);
     for (auto& p : ctx->scratch)
       if (p) cudaFree(p);
+    for (auto& b : ctx->pool_free) cudaFree(b.first);
+    for (auto& b : ctx->pool_used) cudaFree(b.first);
     for (auto& p : ctx->pinned)
       if (p) cudaFreeHost(p);
     for (auto& e : ctx->prof_screen) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
@@ -218,7 +252,7 @@ static void prof_clear(atc_ctx* ctx) {
   for (auto& e : ctx->prof_confirm) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
   ctx->prof_screen.clear();
   ctx->prof_confirm.clear();
-  ctx->prof_survivors = ctx->prof_bindings = 0;
+  ctx->prof_survivors = ctx->prof_bindings = ctx->prof_kernels = 0;
 }
 
 int atc_profile_start(atc_ctx* ctx) {
@@ -252,6 +286,7 @@ int atc_profile_read(atc_ctx* ctx, atc_profile* out) {
   }
   out->survivors = ctx->prof_survivors;
   out->bindings = ctx->prof_bindings;
+  out->kernels = ctx->prof_kernels;
   prof_clear(ctx);
   ctx->prof = false;
   return ATC_OK;
@@ -288,9 +323,8 @@ int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle
       dtotal += len;
     }
   auto dmalloc = [&](size_t bytes) -> void* {
-    void* p = nullptr;
-    if (cudaMalloc(&p, std::max(bytes, (size_t)256)) != cudaSuccess) return nullptr;
-    h->allocations.push_back(p);
+    void* p = atc_pool_alloc(ctx, std::max(bytes, (size_t)256));
+    if (p) h->allocations.push_back(p);
     return p;
   };
   double* init = (double*)dmalloc(total * 8);
@@ -377,7 +411,12 @@ int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle
 int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h) {
   if (!h) return ATC_OK;
   if (ctx && !ctx->broken) cudaSetDevice(ctx->device);
-  for (void* p : h->allocations) cudaFree(p);
+  for (void* p : h->allocations) {
+    if (ctx && !ctx->broken)
+      atc_pool_free(ctx, p);
+    else
+      cudaFree(p);
+  }
   delete h;
   return ATC_OK;
 }
@@ -491,6 +530,7 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     ctx->prof_confirm.push_back(e2);
   }
   if (keys) k_merge_keys<<<64, 256, 0, st>>>(surv, surv_cnt, surv_cap, surv_keys, keys);
+  if (ctx->prof) ctx->prof_kernels += keys ? 5 : 4;  /* fill, K1, K2a, K2b (+ merge) */
   if (!atc_cuda_ok(ctx, cudaGetLastError(), "evaluator launch")) return ATC_ERR_CUDA;
   return ATC_OK;
 }
@@ -665,6 +705,7 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
     plan.pt = pt;
     k_pos0_table<<<(unsigned)std::min<uint64_t>((table_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16), 256, 0,
                    st>>>(ts->view, sp, d_perms, n_perms, pt, tab);
+    if (ctx->prof) ctx->prof_kernels += 1;
   }
   std::vector<uint64_t> h_surv;
   std::vector<int32_t> h_keys;

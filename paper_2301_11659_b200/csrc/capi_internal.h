@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
 #include <string>
 #include <utility>
 #include <vector>
@@ -22,8 +23,14 @@ struct atc_ctx {
   // instrumentation (atc_profile_*)
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_screen, prof_confirm;
-  long long prof_survivors = 0, prof_bindings = 0;
+  long long prof_survivors = 0, prof_bindings = 0, prof_kernels = 0;
+  // device-memory pool for test-set uploads (atc_pool_alloc / atc_pool_free)
+  std::vector<std::pair<void*, size_t>> pool_free;
+  std::map<void*, size_t> pool_used;
 };
+
+void* atc_pool_alloc(atc_ctx* ctx, size_t bytes);
+void atc_pool_free(atc_ctx* ctx, void* p);
 
 void atc_set_error(atc_ctx* ctx, const char* fmt, ...);
 bool atc_cuda_ok(atc_ctx* ctx, cudaError_t e, const char* what);
