@@ -18,7 +18,7 @@ __global__ void k_build_dirty(TestsetView ts, int32_t* dirty_pos, int32_t* dirty
 
 __global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, int budget,
                          int32_t* keys, uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
-                         unsigned long long* reason_hist);
+                         unsigned long long* reason_hist, int mode);
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out);
 __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
@@ -30,10 +30,10 @@ __global__ void k_screen_rows(TestsetView ts, SpecView sp, const uint8_t* perms,
                               unsigned long long* surv_cnt, unsigned long long* reason_hist);
 __global__ void k_confirm(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                           const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
-                          const uint32_t* sel, const unsigned long long* sel_cnt, int t_begin);
+                          const uint32_t* sel, const unsigned long long* sel_cnt, int t_begin, int mode);
 __global__ void k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                              const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
-                             uint32_t* next, unsigned long long* next_cnt);
+                             uint32_t* next, unsigned long long* next_cnt, int mode);
 __global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
                              const int32_t* surv_keys, int32_t* keys);
 __global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason);
@@ -501,7 +501,7 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     k_screen_enum<<<g2, kScreenThreads, 0, st>>>(ts->view, sp, src, n, *pt, surv, surv_cap, surv_cnt, hist);
   } else {
     k_screen<<<grid, kScreenThreads, 0, st>>>(ts->view, sp, src, n, screen_budget(sp), keys, surv, surv_cap,
-                                              surv_cnt, hist);
+                                              surv_cnt, hist, ctx->mode);
   }
   if (ctx->prof) {
     cudaEventRecord(e1.second, st);
@@ -522,9 +522,9 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
   }
   cudaMemsetAsync(next_cnt, 0, 8, st);
   k_confirm_t0<<<(unsigned)ctx->sm_count * 8, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys,
-                                                            next, next_cnt);
+                                                            next, next_cnt, ctx->mode);
   k_confirm<<<(unsigned)ctx->sm_count * 8, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, next,
-                                                         next_cnt, 1);
+                                                         next_cnt, 1, ctx->mode);
   if (ctx->prof) {
     cudaEventRecord(e2.second, st);
     ctx->prof_confirm.push_back(e2);
@@ -553,6 +553,7 @@ int atc_eval_bindings_device(atc_ctx* ctx, const atc_spec_desc* spec, const atc_
   cudaSetDevice(ctx->device);
   cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
   const uint64_t n = (uint64_t)n_bindings;
+  ctx->mode = mode;
   int32_t* keys = (int32_t*)atc_ctx_scratch(ctx, 0, n * 4);
   uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, n * 8);
   int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, n * 4);
@@ -635,6 +636,7 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
   }
   cudaSetDevice(ctx->device);
   cudaStream_t st = ctx->stream;
+  ctx->mode = mode;
   const uint64_t chunk_cap = 1ull << 22;  // survivors per chunk
   uint8_t* d_perms = (uint8_t*)atc_ctx_scratch(ctx, 6, (size_t)n_perms * sp.nA + 16);
   uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);

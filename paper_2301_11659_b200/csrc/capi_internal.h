@@ -20,6 +20,7 @@ struct atc_ctx {
   void* pinned[4] = {};
   size_t pinned_bytes[4] = {};
   cudaStream_t own_stream = nullptr;
+  int mode = 0;  // ATC_MODE_* of the evaluation in flight
   // instrumentation (atc_profile_*)
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_screen, prof_confirm;

@@ -104,6 +104,78 @@ __device__ __forceinline__ double round_region(double v, bool f32) {
   return f32 ? (double)__double2float_rn(v) : v;  // rewriter.cpp:156-157
 }
 
+// Verdict of one output position (does the value the API call writes there
+// mismatch the recorded `want`?).
+//   ATC_MODE_FP64:        the reference arithmetic (dot64: FP64, non-fused).
+//   ATC_MODE_FP32_SCREEN: first an FP32 FMA dot product (dot32) with a running
+//     sum S = sum |a'b'| of the float-rounded operands; the reference result
+//     acc64 is then known to lie in [acc32 - E, acc32 + E] with
+//       E = 1.01 (n + 4) u S + 1e-30,   u = 2^-24, n = dot length (< 4096),
+//     covering operand rounding to float (2u|ab| per term), FMA accumulation
+//     (gamma_n = n u / (1 - n u)), the reference's own FP64 rounding (2^-53 n) and
+//     subnormal slack.  If every value in that interval (after the f32
+//     write-back rounding, widened by u|acc| for f32 regions) is beyond the
+//     tolerance the position is a mismatch; if every value is within it, a match;
+//     otherwise the FP64 reference arithmetic decides.  Verdicts are therefore
+//     identical in both modes; FP32 only makes clear cases cheaper.
+template <class Dot64, class Dot32>
+__device__ __forceinline__ bool position_mismatch(int mode, int n, double want, bool f32, Dot64 dot64, Dot32 dot32) {
+  if (mode == ATC_MODE_FP32_SCREEN && n < 4096) {
+    float S = 0.0f;
+    const float acc32 = dot32(S);
+    const double u = 5.9604644775390625e-08;  // 2^-24
+    double E = 1.01 * (n + 4) * u * (double)S + 1e-30;
+    if (f32) E += u * (fabs((double)acc32) + E);
+    const double rel = f32 ? 1e-4 : 1e-9;
+    const double abs_ = f32 ? 1e-6 : 1e-12;
+    const double tol = abs_ + rel * fabs(want);
+    const double d = fabs((double)acc32 - want);
+    if (d - E > tol * (1.0 + 1e-12)) return true;    // every candidate value mismatches
+    if (d + E < tol * (1.0 - 1e-12)) return false;   // every candidate value matches
+  }
+  return mismatch(round_region(dot64(), f32), want, f32);
+}
+
+// reference_gemm's inner loop (equivalence.cpp:55-58) over strided operands (generic
+// loads: operands may be staged in shared memory)
+__device__ __forceinline__ double gemm_dot64(const double* a, int sa, const double* b, int sb, int k) {
+  double acc = 0.0;
+  for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(a[p * sa], b[p * sb]));
+  return acc;
+}
+__device__ __forceinline__ float gemm_dot32(const double* a, int sa, const double* b, int sb, int k, float& S) {
+  float acc = 0.0f;
+  for (int p = 0; p < k; ++p) {
+    const float x = __double2float_rn(a[p * sa]), y = __double2float_rn(b[p * sb]);
+    acc = fmaf(x, y, acc);
+    S = fmaf(fabsf(x), fabsf(y), S);
+  }
+  return acc;
+}
+// reference_conv2d's inner loops (equivalence.cpp:85-90); `in` points at
+// in[b][0][y][x], `wt` at wt[q][0][0][0]
+__device__ __forceinline__ double conv_dot64(const double* in, const double* wt, int C, int R, int S, int H, int W) {
+  double acc = 0.0;
+  for (int z = 0; z < C; ++z)
+    for (int u = 0; u < R; ++u)
+      for (int v = 0; v < S; ++v)
+        acc = dadd(acc, dmul(in[(z * H + u) * W + v], wt[(z * R + u) * S + v]));
+  return acc;
+}
+__device__ __forceinline__ float conv_dot32(const double* in, const double* wt, int C, int R, int S, int H, int W,
+                                            float& Sabs) {
+  float acc = 0.0f;
+  for (int z = 0; z < C; ++z)
+    for (int u = 0; u < R; ++u)
+      for (int v = 0; v < S; ++v) {
+        const float x = __double2float_rn(in[(z * H + u) * W + v]);
+        const float y = __double2float_rn(wt[(z * R + u) * S + v]);
+        acc = fmaf(x, y, acc);
+        Sabs = fmaf(fabsf(x), fabsf(y), Sabs);
+      }
+  return acc;
+}
+
 // Resolved sizes of one (binding, t), reference roles with their fallbacks.
 struct Dims {
   // gemm (equivalence.cpp:42-48)

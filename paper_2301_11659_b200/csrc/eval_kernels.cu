@@ -82,7 +82,7 @@ __device__ __forceinline__ void decode_binding(const BindingSource& src, const S
 // looked at), a reason code, or kUndecided when `budget` output positions were
 // checked without reaching the end.
 __device__ int thread_check(const TestsetView& ts, const SpecView& sp, const int* ptr_of,
-                            const int64_t* sz, int t, int budget, bool* complete) {
+                            const int64_t* sz, int t, int budget, bool* complete, int mode) {
   *complete = false;
   if (!ts.test_ok[t]) return ATC_FAIL_TESTSET;
   if (int r = extent_check(sp, sz, ptr_of, ts.region_len)) return r;
@@ -117,18 +117,14 @@ __device__ int thread_check(const TestsetView& ts, const SpecView& sp, const int
         if (overlap && !gemm_last_writer(row, i, j, m, ldc)) continue;
         if (checked == budget) return kUndecided;
         ++checked;
-        double acc = 0.0;
-        if (row) {
-          const double* a = A + i * lda;
-          const double* b = B + j;
-          for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(__ldg(a + p), __ldg(b + p * ldb)));
-        } else {
-          const double* a = A + i;
-          const double* b = B + j * ldb;
-          for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(__ldg(a + p * lda), __ldg(b + p)));
-        }
+        const double* a = row ? A + i * lda : A + i;
+        const double* b = row ? B + j : B + j * ldb;
+        const int sa = row ? 1 : lda, sb = row ? ldb : 1;
         const int pos = row ? i * ldc + j : j * ldc + i;
-        if (mismatch(round_region(acc, f32), __ldg(F + pos), f32)) return ATC_FAIL_MISMATCH;
+        if (position_mismatch(
+                mode, k, __ldg(F + pos), f32, [&] { return gemm_dot64(a, sa, b, sb, k); },
+                [&](float& S) { return gemm_dot32(a, sa, b, sb, k, S); }))
+          return ATC_FAIL_MISMATCH;
       }
     *complete = true;
     return 0;
@@ -145,15 +141,13 @@ __device__ int thread_check(const TestsetView& ts, const SpecView& sp, const int
         for (int x = 0; x < OW; ++x) {
           if (checked == budget) return kUndecided;
           ++checked;
-          double acc = 0.0;
-          for (int z = 0; z < C; ++z)
-            for (int u = 0; u < R; ++u) {
-              const double* in = A + ((b * C + z) * H + y + u) * W + x;
-              const double* wt = B + ((q * C + z) * R + u) * S;
-              for (int v = 0; v < S; ++v) acc = dadd(acc, dmul(__ldg(in + v), __ldg(wt + v)));
-            }
+          const double* in = A + ((b * C) * H + y) * W + x;
+          const double* wt = B + (q * C) * R * S;
           const int pos = ((b * K + q) * OH + y) * OW + x;
-          if (mismatch(round_region(acc, f32), __ldg(F + pos), f32)) return ATC_FAIL_MISMATCH;
+          if (position_mismatch(
+                  mode, C * R * S, __ldg(F + pos), f32, [&] { return conv_dot64(in, wt, C, R, S, H, W); },
+                  [&](float& Sa) { return conv_dot32(in, wt, C, R, S, H, W, Sa); }))
+            return ATC_FAIL_MISMATCH;
         }
   *complete = true;
   return 0;
@@ -167,7 +161,7 @@ __global__ void __launch_bounds__(256) k_screen(TestsetView ts, SpecView sp, Bin
                                                  uint64_t n, int budget, int32_t* keys,
                                                  uint64_t* surv, uint64_t surv_cap,
                                                  unsigned long long* surv_cnt,
-                                                 unsigned long long* reason_hist) {
+                                                 unsigned long long* reason_hist, int mode) {
   __shared__ int64_t s_ints0[kMaxInts];
   __shared__ unsigned long long s_hist[ATC_REASON_COUNT];
   if (threadIdx.x < ts.nI) s_ints0[threadIdx.x] = ts.ints[threadIdx.x];
@@ -180,7 +174,7 @@ __global__ void __launch_bounds__(256) k_screen(TestsetView ts, SpecView sp, Bin
     int64_t sz[ATC_MAX_SIZES];
     for (int q = 0; q < sp.nS; ++q) sz[q] = s_ints0[int_of[q]];
     bool complete;
-    int r = thread_check(ts, sp, ptr_of, sz, 0, budget, &complete);
+    int r = thread_check(ts, sp, ptr_of, sz, 0, budget, &complete, mode);
     if (r > 0) {
       if (keys) keys[idx] = fail_key(0, r);
       if (reason_hist) atomicAdd(&s_hist[r], 1ull);
@@ -396,7 +390,7 @@ constexpr int kStageDoubles = 6080;  // ~47.5 KB of operand staging per CTA (sta
 __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src,
                                                     const uint64_t* surv, const unsigned long long* surv_cnt,
                                                     uint64_t surv_cap, int32_t* surv_keys, uint32_t* next,
-                                                    unsigned long long* next_cnt) {
+                                                    unsigned long long* next_cnt, int mode) {
   const int lane = threadIdx.x & 31;
   unsigned long long cnt = *surv_cnt;
   if (cnt > surv_cap) cnt = surv_cap;
@@ -437,12 +431,12 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
             if (o < outs) {
               const int i = o / n, j = o - (o / n) * n;
               if (!overlap || gemm_last_writer(row, i, j, m, ldc)) {
-                double acc = 0.0;
-                if (row)
-                  for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(__ldg(A + i * lda + p), __ldg(B + p * ldb + j)));
-                else
-                  for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(__ldg(A + p * lda + i), __ldg(B + j * ldb + p)));
-                mm = mismatch(round_region(acc, f32), __ldg(F + (row ? i * ldc + j : j * ldc + i)), f32);
+                const double* a = row ? A + i * lda : A + i;
+                const double* b = row ? B + j : B + j * ldb;
+                const int sa = row ? 1 : lda, sb = row ? ldb : 1;
+                mm = position_mismatch(
+                    mode, k, __ldg(F + (row ? i * ldc + j : j * ldc + i)), f32,
+                    [&] { return gemm_dot64(a, sa, b, sb, k); }, [&](float& S) { return gemm_dot32(a, sa, b, sb, k, S); });
               }
             }
             bad = __any_sync(0xffffffffu, mm);
@@ -462,14 +456,11 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
             const int y = rem % OH; rem /= OH;
             const int q = rem % K;
             const int b = rem / K;
-            double acc = 0.0;
-            for (int z = 0; z < C; ++z)
-              for (int u = 0; u < R; ++u) {
-                const double* in = A + ((b * C + z) * H + y + u) * W + x;
-                const double* wt = B + ((q * C + z) * R + u) * S;
-                for (int v = 0; v < S; ++v) acc = dadd(acc, dmul(__ldg(in + v), __ldg(wt + v)));
-              }
-            mm = mismatch(round_region(acc, f32), __ldg(F + o), f32);
+            const double* in = A + ((b * C) * H + y) * W + x;
+            const double* wt = B + (q * C) * R * S;
+            mm = position_mismatch(
+                mode, C * R * S, __ldg(F + o), f32, [&] { return conv_dot64(in, wt, C, R, S, H, W); },
+                [&](float& Sa) { return conv_dot32(in, wt, C, R, S, H, W, Sa); });
           }
           bad = __any_sync(0xffffffffu, mm);
         }
@@ -495,7 +486,8 @@ __global__ void __launch_bounds__(kConfirmThreads) k_confirm(TestsetView ts, Spe
                                                              const unsigned long long* surv_cnt,
                                                              uint64_t surv_cap, int32_t* surv_keys,
                                                              const uint32_t* sel,
-                                                             const unsigned long long* sel_cnt, int t_begin) {
+                                                             const unsigned long long* sel_cnt, int t_begin,
+                                                             int mode) {
   __shared__ double s_stage[kStageDoubles];
   __shared__ int s_fail;
   __shared__ int s_ptr[ATC_MAX_ARRAYS];
@@ -591,14 +583,14 @@ __global__ void __launch_bounds__(kConfirmThreads) k_confirm(TestsetView ts, Spe
             if (o < outs) {
               const int i = o / n, j = o - (o / n) * n;
               if (!overlap || gemm_last_writer(row, i, j, m, ldc)) {
-                double acc = 0.0;
-                if (row) {
-                  for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(A[i * lda + p], B[p * ldb + j]));
-                } else {
-                  for (int p = 0; p < k; ++p) acc = dadd(acc, dmul(A[p * lda + i], B[j * ldb + p]));
-                }
+                const double* a = row ? A + i * lda : A + i;
+                const double* b = row ? B + j : B + j * ldb;
+                const int sa = row ? 1 : lda, sb = row ? ldb : 1;
                 const int pos = row ? i * ldc + j : j * ldc + i;
-                if (mismatch(round_region(acc, f32), __ldg(F + pos), f32)) s_fail = ATC_FAIL_MISMATCH;
+                if (position_mismatch(
+                        mode, k, __ldg(F + pos), f32, [&] { return gemm_dot64(a, sa, b, sb, k); },
+                        [&](float& Sa) { return gemm_dot32(a, sa, b, sb, k, Sa); }))
+                  s_fail = ATC_FAIL_MISMATCH;
               }
             }
             // block-wide early exit on the first mismatching chunk
@@ -631,14 +623,12 @@ __global__ void __launch_bounds__(kConfirmThreads) k_confirm(TestsetView ts, Spe
               const int y = rem % OH; rem /= OH;
               const int q = rem % K;
               const int b = rem / K;
-              double acc = 0.0;
-              for (int z = 0; z < C; ++z)
-                for (int u = 0; u < R; ++u) {
-                  const double* in = gA + ((b * C + z) * H + y + u) * W + x;
-                  const double* wt = Wt + ((q * C + z) * R + u) * S;
-                  for (int v = 0; v < S; ++v) acc = dadd(acc, dmul(__ldg(in + v), wt[v]));
-                }
-              if (mismatch(round_region(acc, f32), __ldg(F + o), f32)) s_fail = ATC_FAIL_MISMATCH;
+              const double* in = gA + ((b * C) * H + y) * W + x;
+              const double* wt = Wt + (q * C) * R * S;
+              if (position_mismatch(
+                      mode, C * R * S, __ldg(F + o), f32, [&] { return conv_dot64(in, wt, C, R, S, H, W); },
+                      [&](float& Sa) { return conv_dot32(in, wt, C, R, S, H, W, Sa); }))
+                s_fail = ATC_FAIL_MISMATCH;
             }
             if (__syncthreads_or(s_fail != 0)) break;
           }

@@ -148,3 +148,28 @@ def test_malformed_spec_rejected(ev):
                                    am.ctypes.data, am.ctypes.data, None)
     assert rc == L.ATC_ERR_ARG
     assert b"output" in L.lib().atc_last_error(ev.ctx.handle)
+
+
+@pytest.mark.parametrize("stem", STEMS)
+def test_fp32_screen_mode_identical_verdicts(ev, stem):
+    """ATC_MODE_FP32_SCREEN (FP32 FMA with the stated error bound, FP64 only for
+    undecided positions) gives exactly the reference's verdicts."""
+    p = fixtures.load(stem)
+    for sname in p.spec_names():
+        v = p.verdicts(sname)
+        am, sm = p.space(sname).decode(v["idx"])
+        got = ev.eval_bindings(fixtures.spec(sname), p.testsets(16), am, sm, mode=L.MODE_FP32_SCREEN)
+        np.testing.assert_array_equal(got.fail_t, v["fail_t"])
+        np.testing.assert_array_equal(got.reason, v["reason"])
+
+
+@pytest.mark.parametrize("stem", ["naive_f32", "naive_rowmajor"])
+def test_fp32_screen_mode_64cubed(ev, stem):
+    for sname in ("gemm_rowmajor", "gemm_colmajor"):
+        p = fixtures.load(stem)
+        v = p.verdicts(sname, "p2_64")
+        am, sm = p.space(sname).decode(v["idx"])
+        got = ev.eval_bindings(fixtures.spec(sname), p.testsets(16, variant="testsets64"), am, sm,
+                               mode=L.MODE_FP32_SCREEN)
+        np.testing.assert_array_equal(got.fail_t, v["fail_t"])
+        np.testing.assert_array_equal(got.reason, v["reason"])
