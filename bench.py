@@ -141,6 +141,30 @@ def run_reference_arm(args, jobs, rank):
     print(json.dumps(line))
 
 
+def _backend_cpu_baseline() -> dict:
+    """The reference's backend loop nests on the host: profitability::xpu_gemm (all
+    host threads) on a 512-row M-slice of the 8192^3 sgemm, and run_reference's
+    f64 conv2d on one image of the conv2_x 3x3 layer."""
+    tool = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
+    out = {}
+    if not os.path.exists(tool):
+        return out
+    try:
+        r = subprocess.run([tool, "time-xpu-gemm", "512", "8192", "8192"], capture_output=True, text=True, timeout=300)
+        j = json.loads(r.stdout.strip().splitlines()[-1])
+        out["xpu_gemm_gflops"] = j["gflops"]
+        out["xpu_gemm_threads"] = j["threads"]
+        out["xpu_gemm_sample"] = "512 x 8192 x 8192 M-slice of the 8192^3 workload"
+        r = subprocess.run([tool, "time-conv", "1", "64", "58", "58", "64", "3", "3"], capture_output=True, text=True,
+                           timeout=300)
+        j = json.loads(r.stdout.strip().splitlines()[-1])
+        out["run_reference_conv_gflops"] = j["gflops"]
+        out["run_reference_conv_sample"] = "N=1, 64->64, 3x3, 58x58 (one image of conv2_x.b), f64, 1 thread"
+    except Exception as e:  # the baseline is reported, not required
+        out["error"] = str(e)
+    return out
+
+
 def _ncu_summary():
     """The newest committed ncu summary (profiles/<round>_ncu_summary.json)."""
     d = os.path.join(ROOT, "profiles")
@@ -290,10 +314,13 @@ def main():
                              "SURVEY 8d's 8 B x (extA+extB+extC) per binding, which the factorisation never streams"},
         "k2_confirm": {"ms_per_step": prof.confirm_ms / args.steps, "survivors_per_step": prof.survivors / args.steps},
     }
+    if not args.no_sgemm:
+        # replaced-call backends: sgemm split along M, conv along batch, no collective
+        # on the data path; the time of the slowest rank is the job time
+        line["replaced_gemm"] = _sgemm_bench(ctx, stream, torch, dist, world)
+        line["replaced_conv"] = _conv_bench(ctx, stream, torch, dist, world)
     if rank == 0:
         line["clocks"] = clocks.summary()
-        if not args.no_sgemm:
-            line["replaced_gemm"] = _sgemm_bench(ctx, stream, torch)
         if not args.no_cpu_baseline and world == 1:
             rates = reference_rates(6.0, os.cpu_count() or 1)
             if rates:
@@ -302,7 +329,8 @@ def main():
                     "kind": "reference",
                     "sample": "rewriter::verify_rewrite T=16, random bindings of conv_direct x conv2d and naive_ld x "
                               "gemm_rowmajor_ld, 6 s each, weighted by this workload's binding counts",
-                    "rates": {k: r["bindings_per_s"] for k, r in rates.items()}}
+                    "rates": {k: r["bindings_per_s"] for k, r in rates.items()},
+                    "backends": _backend_cpu_baseline()}
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
@@ -378,12 +406,76 @@ def _e2e(args, ctx, jobs, shards, stream, torch, dist):
     return ms, h2d, d2h
 
 
-def _sgemm_bench(ctx, stream, torch):
-    """Replaced-call backend: row-major FP32 sgemm 8192^3 (cpu_gemm contract) on tcgen05."""
+# ResNet-50 conv layers expressible as valid, unit-stride NCHW (SURVEY.md §8d
+# config 5; 3x3 layers on host-padded inputs): (name, C, K, R, H_in)
+RESNET_LAYERS = [("conv2_x.a 1x1", 64, 64, 1, 56), ("conv2_x.b 3x3", 64, 64, 3, 58),
+                 ("conv2_x.c 1x1", 64, 256, 1, 56), ("conv3_x.b 3x3", 128, 128, 3, 30),
+                 ("conv3_x.a 1x1", 512, 128, 1, 28), ("conv4_x.b 3x3", 256, 256, 3, 16),
+                 ("conv5_x.b 3x3", 512, 512, 3, 9)]
+
+
+def _max_over_ranks(ms, dist, torch):
+    if dist is None:
+        return ms
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _conv_bench(ctx, stream, torch, dist=None, world=1, batch=256):
+    """Replaced-call conv2d backend on tcgen05 (TF32): global batch `batch`,
+    split across ranks (batch // world images each)."""
     from paper_2301_11659_b200 import _lib
 
     L = _lib.lib()
-    m = n = k = 8192
+    out = {"batch": batch, "per_rank_batch": batch // world, "precision": "tf32", "layers": []}
+    tot_flops = tot_ms = 0.0
+    gb = batch
+    batch = gb // world
+    for name, c, k, r, h in RESNET_LAYERS:
+        oh = h - r + 1
+        x = torch.empty(batch, c, h, h, device="cuda").uniform_(-1, 1)
+        w = torch.empty(k, c, r, r, device="cuda").uniform_(-1, 1)
+        y = torch.empty(batch, k, oh, oh, device="cuda")
+
+        def run():
+            _lib.check(ctx.handle, L.atc_conv2d_nchw_device(ctx.handle, x.data_ptr(), w.data_ptr(), y.data_ptr(),
+                                                            batch, c, h, h, k, r, r, _lib.PREC_TF32,
+                                                            C.c_void_p(stream.cuda_stream)))
+
+        for _ in range(3):
+            run()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = _max_over_ranks(float(np.median(ts)), dist, torch)
+        flops = 2.0 * gb * k * oh * oh * c * r * r
+        ref = torch.nn.functional.conv2d(x[:1].double(), w.double())
+        err = ((y[:1].double() - ref).abs() / (1 + ref.abs())).max().item()
+        out["layers"].append({"layer": name, "C": c, "K": k, "RxS": f"{r}x{r}", "H": h, "ms": ms,
+                              "tflops": flops / (ms / 1e3) / 1e12, "max_rel_err_vs_fp64": err})
+        tot_flops += flops
+        tot_ms += ms
+        del x, w, y
+    out["total_tflops"] = tot_flops / (tot_ms / 1e3) / 1e12
+    out["note"] = "includes the per-call NCHW->NHWC input transpose and KCRS->KRSC weight reorder"
+    return out
+
+
+def _sgemm_bench(ctx, stream, torch, dist=None, world=1):
+    """Replaced-call backend: row-major FP32 sgemm 8192^3 (cpu_gemm contract) on
+    tcgen05, split along M across ranks (8192/world rows each, B replicated)."""
+    from paper_2301_11659_b200 import _lib
+
+    L = _lib.lib()
+    M = n = k = 8192
+    m = M // world
     g = torch.Generator(device="cuda").manual_seed(0)
     a = torch.empty(m, k, device="cuda").uniform_(-1, 1, generator=g)
     b = torch.empty(k, n, device="cuda").uniform_(-1, 1, generator=g)
@@ -405,14 +497,15 @@ def _sgemm_bench(ctx, stream, torch):
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
-        ms = float(np.median(times))
-        tflops = 2.0 * m * n * k / (ms / 1e3) / 1e12
+        ms = _max_over_ranks(float(np.median(times)), dist, torch)
+        tflops = 2.0 * M * n * k / (ms / 1e3) / 1e12
         ref = (a[:256].double() @ b.double())
         err = ((c[:256].double() - ref).abs() / (1 + ref.abs())).max().item()
         out[prec_name] = {"ms": ms, "tflops": tflops, "max_rel_err_vs_fp64": err}
     _, bf16, kind = _peaks()
     tf32_peak = bf16 / 2
-    out["shape"] = [m, n, k]
+    out["shape"] = [M, n, k]
+    out["per_rank_rows"] = m
     g = next((d for d in _ncu_summary() if d["kernel"].startswith("k_tc_gemm")), {})
     out["roofline"] = {"bound": "tensor", "achieved": out["tf32"]["tflops"], "peak": tf32_peak, "unit": "TFLOP/s",
                        "frac": out["tf32"]["tflops"] / tf32_peak,

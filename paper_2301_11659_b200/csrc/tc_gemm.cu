@@ -187,8 +187,14 @@ __device__ __forceinline__ void kblock_coords(const Problem& p, int kb, int kblo
     const int r = rs / p.S, s = rs - (rs / p.S) * p.S;
     a_c0 = rs * p.K + c0;             // column in W_krsc [Kf][R*S*C]
     a_c1 = tm * BM;                   // filter row
-    b_c0 = c0;                        // channel block of the NHWC input [N*H*W][C]
-    b_c1 = ti * p.H * p.W + tn * BN + r * p.W + s;  // pixel row: affine shift on the input grid
+    if (p.conv == 1) {
+      b_c0 = c0;                      // channel block of the NHWC input [N*H*W][C]
+      b_c1 = ti * p.H * p.W + tn * BN + r * p.W + s;  // pixel row: affine shift on the input grid
+    } else {
+      // 1x1 on NCHW directly: [N*C][H*W] view, MN-major, pixel offset 0 (aligned)
+      b_c0 = tn * BN;
+      b_c1 = ti * p.Cin + c0;
+    }
   }
 }
 
@@ -244,7 +250,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           uint8_t* sB = sA + A_BYTES;
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           tma_load_2d(sA, &maps.a[sa], &full[stage], a0, a1);
-          if (p.conv) {
+          if (p.conv == 1) {
             // K-major: 256 pixel rows x 32 channels (128 B) in one box
             tma_load_2d(sB, &maps.b[sb], &full[stage], b0, b1);
           } else {
@@ -283,9 +289,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
             // B (sgemm): MN-major SW128 with 32 B atoms: chunks of 32 N at LBO = 32 rows *
             // 128 B, 4-row K groups at SBO = 512 B; +8 rows (1 KB) per K step.
             // B (conv): K-major SW128 like A.
-            const uint64_t bd = p.conv ? make_desc(b_addr + kk * 32, 16, 1024, kSw128)
-                                       : make_desc(b_addr + kk * 1024, BK * 128, 512, kSw128Base32);
-            mma_tf32(d_tmem, ad, bd, p.conv ? idesc_tf32(0) : idesc_tf32(1), (kb > 0 || kk > 0) ? 1u : 0u);
+            const uint64_t bd = p.conv == 1 ? make_desc(b_addr + kk * 32, 16, 1024, kSw128)
+                                            : make_desc(b_addr + kk * 1024, BK * 128, 512, kSw128Base32);
+            mma_tf32(d_tmem, ad, bd, p.conv == 1 ? idesc_tf32(0) : idesc_tf32(1), (kb > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&empty[stage]);  // smem stage free once these MMAs complete
           if (++stage == STAGES) {
@@ -333,11 +339,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           } else {
             // pixel p = y*W + x on the input grid; keep y < OH, x < OW
             float* dst = p.C + ((int64_t)ti * p.M + row) * ((int64_t)p.OH * p.OW);
+            if (p.R == 1 && p.S == 1) {  // every pixel is an output: contiguous, vectorised
+              const int npix = p.OH * p.OW;
+              if (col0 + 32 <= npix && (npix & 3) == 0) {
 #pragma unroll
-            for (int v = 0; v < 32; ++v) {
-              const int pix = col0 + v;
-              const int y = pix / p.W, x = pix - (pix / p.W) * p.W;
-              if (y < p.OH && x < p.OW) dst[y * p.OW + x] = __uint_as_float(r[v]);
+                for (int v = 0; v < 32; v += 4)
+                  *reinterpret_cast<float4*>(dst + col0 + v) =
+                      make_float4(__uint_as_float(r[v]), __uint_as_float(r[v + 1]), __uint_as_float(r[v + 2]),
+                                  __uint_as_float(r[v + 3]));
+              } else {
+                for (int v = 0; v < 32; ++v)
+                  if (col0 + v < npix) dst[col0 + v] = __uint_as_float(r[v]);
+              }
+            } else {
+              int y = col0 / p.W, x = col0 - y * p.W;
+#pragma unroll
+              for (int v = 0; v < 32; ++v) {
+                if (y < p.OH && x < p.OW) dst[y * p.OW + x] = __uint_as_float(r[v]);
+                if (++x == p.W) {
+                  x = 0;
+                  ++y;
+                }
+              }
             }
           }
         }
@@ -602,13 +625,24 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
   // operand K-major, so the (r, s) pixel shift is a row offset of a 2-D TMA box
   // (any offset is legal) instead of a sub-16-byte column offset (illegal for
   // swizzled TMA boxes).
+  // 1x1 filters need no pixel shift: the NCHW input is used as is ([N*C][H*W]
+  // view, MN-major B, like the sgemm), no transpose (conv mode 2)
   const int64_t in_elems = n * c * hw;
-  float* ih = (float*)atc_ctx_scratch(ctx, 16, (size_t)in_elems * 4 * (splits == 3 ? 2 : 1));
-  if (!ih) return ATC_ERR_CUDA;
-  float* il = splits == 3 ? ih + in_elems : nullptr;
-  {
-    dim3 grid((unsigned)((hw + 31) / 32), (unsigned)(c / 32), (unsigned)n);
-    k_nchw_to_nhwc<<<grid, dim3(32, 8), 0, st>>>(d_in, ih, il, (int)c, hw);
+  const bool direct = r == 1 && s == 1 && hw % 4 == 0;
+  const float* ih = d_in;
+  const float* il = nullptr;
+  if (!direct || splits == 3) {
+    float* buf = (float*)atc_ctx_scratch(ctx, 16, (size_t)in_elems * 4 * (splits == 3 ? 2 : 1));
+    if (!buf) return ATC_ERR_CUDA;
+    float* lo = splits == 3 ? buf + in_elems : nullptr;
+    if (direct) {
+      k_split_tf32<<<grid_for(in_elems), 256, 0, st>>>(d_in, buf, lo, in_elems);
+    } else {
+      dim3 grid((unsigned)((hw + 31) / 32), (unsigned)(c / 32), (unsigned)n);
+      k_nchw_to_nhwc<<<grid, dim3(32, 8), 0, st>>>(d_in, buf, lo, (int)c, hw);
+    }
+    ih = buf;
+    il = lo;
   }
   const int64_t wn = k * c * r * s;
   float* wh = (float*)atc_ctx_scratch(ctx, 15, (size_t)wn * 4 * 2);
@@ -617,16 +651,18 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
   k_weights_krsc<<<grid_for(wn), 256, 0, st>>>(d_w, wh, wl, (int)k, (int)c, (int)r, (int)s);
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
-  if (!make_map(ctx, &maps.a[0], wh, k, r * s * c, r * s * c, BK, BM, false) ||
-      !make_map(ctx, &maps.b[0], ih, n * hw, c, c, BK, BN, false))
+  auto bmap = [&](CUtensorMap* m, const float* base) {
+    return direct ? make_map(ctx, m, base, n * c, hw, hw, 32, BK, true)   // [N*C][H*W], MN-major chunks
+                  : make_map(ctx, m, base, n * hw, c, c, BK, BN, false);  // NHWC [N*H*W][C], K-major
+  };
+  if (!make_map(ctx, &maps.a[0], wh, k, r * s * c, r * s * c, BK, BM, false) || !bmap(&maps.b[0], ih))
     return ATC_ERR_CUDA;
   maps.a[1] = maps.a[0];
   maps.b[1] = maps.b[0];
-  if (splits == 3 && (!make_map(ctx, &maps.a[1], wl, k, r * s * c, r * s * c, BK, BM, false) ||
-                      !make_map(ctx, &maps.b[1], il, n * hw, c, c, BK, BN, false)))
+  if (splits == 3 && (!make_map(ctx, &maps.a[1], wl, k, r * s * c, r * s * c, BK, BM, false) || !bmap(&maps.b[1], il)))
     return ATC_ERR_CUDA;
   Problem p{};
-  p.conv = 1;
+  p.conv = direct ? 2 : 1;
   p.M = (int)k;
   p.N = (int)hw;
   p.K = (int)c;
