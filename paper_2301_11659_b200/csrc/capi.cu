@@ -38,6 +38,9 @@ __global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* sur
                              const int32_t* surv_keys, int32_t* keys);
 __global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason);
 __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v);
+__global__ void k_finalize(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
+                           const int32_t* surv_keys, uint64_t base, uint64_t* res, unsigned long long* hist);
+constexpr uint64_t kResultPrefix = 4096;  // passing indices returned with the first D2H
 }  // namespace atc
 
 using namespace atc;
@@ -79,6 +82,17 @@ void* atc_ctx_scratch(atc_ctx* ctx, int slot, size_t bytes) {
   if (cudaMalloc(&ctx->scratch[slot], want) != cudaSuccess) return nullptr;
   ctx->scratch_bytes[slot] = want;
   return ctx->scratch[slot];
+}
+
+void* atc_ctx_pinned(atc_ctx* ctx, int slot, size_t bytes) {
+  if (slot < 0 || slot >= 4) return nullptr;
+  if (ctx->pinned_bytes[slot] >= bytes) return ctx->pinned[slot];
+  if (ctx->pinned[slot]) cudaFreeHost(ctx->pinned[slot]);
+  ctx->pinned[slot] = nullptr;
+  ctx->pinned_bytes[slot] = 0;
+  if (cudaMallocHost(&ctx->pinned[slot], bytes) != cudaSuccess) return nullptr;
+  ctx->pinned_bytes[slot] = bytes;
+  return ctx->pinned[slot];
 }
 
 // Device-memory pool for test-set uploads: freed blocks are kept per context and
@@ -709,64 +723,67 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
                    st>>>(ts->view, sp, d_perms, n_perms, pt, tab);
     if (ctx->prof) ctx->prof_kernels += 1;
   }
-  std::vector<uint64_t> h_surv;
-  std::vector<int32_t> h_keys;
+  // result block on the device: [0] survivor count (copied from cnt), [1] passing
+  // count, [2..2+cap) passing global indices; reasons accumulate in `hist`
+  uint64_t* res = (uint64_t*)atc_ctx_scratch(ctx, 20, (chunk_cap + 2) * 8);
+  uint64_t* h_res = (uint64_t*)atc_ctx_pinned(ctx, 0, (kResultPrefix + 2 + ATC_REASON_COUNT) * 8);
+  if (!res || !h_res) {
+    atc_set_error(ctx, "result buffer allocation failed");
+    return ATC_ERR_CUDA;
+  }
+  std::vector<uint64_t> pass_all;
   int64_t passed = 0;
-  int64_t k2_hist[ATC_REASON_COUNT] = {0};
-  uint64_t chunk = 1ull << 30;
+  uint64_t chunk = 1ull << 34;  // one chunk covers every corpus space
   for (uint64_t lo = begin; lo < end;) {
     const uint64_t hi = std::min(end, lo + chunk);
     BindingSource src{nullptr, nullptr, d_perms, size_maps, lo, 1};
     int rc = run_eval(ctx, sp, ts, src, hi - lo, nullptr, surv, chunk_cap, cnt, skeys, hist, st,
                       use_table ? &pt : nullptr, use_rows ? &plan : nullptr);
     if (rc) return rc;
-    unsigned long long c = 0;
-    if (!atc_cuda_ok(ctx, cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, st), "D2H") ||
+    // K2 outcomes -> passing list + reason histogram, on the device (one sync per chunk)
+    cudaMemsetAsync(res + 1, 0, 8, st);
+    k_finalize<<<64, 256, 0, st>>>(surv, cnt, chunk_cap, skeys, lo, res, hist);
+    if (ctx->prof) ctx->prof_kernels += 1;
+    const uint64_t pre = std::min<uint64_t>(kResultPrefix, cap > 0 ? (uint64_t)cap : 0);
+    if (!atc_cuda_ok(ctx, cudaMemcpyAsync(h_res, res, (2 + pre) * 8, cudaMemcpyDeviceToHost, st), "D2H result") ||
+        !atc_cuda_ok(ctx, cudaMemcpyAsync(h_res + 2 + kResultPrefix, hist, ATC_REASON_COUNT * 8,
+                                          cudaMemcpyDeviceToHost, st), "D2H hist") ||
         !atc_cuda_ok(ctx, cudaStreamSynchronize(st), "enumerate sync"))
       return ATC_ERR_CUDA;
-    if (c > chunk_cap) {  // too many survivors for this chunk: split it and redo
+    const uint64_t c = h_res[0], npass = h_res[1];
+    if (c > chunk_cap) {  // too many survivors for this chunk: restart with smaller chunks
       if (chunk == 1) {
         atc_set_error(ctx, "survivor overflow");
         return ATC_ERR_CUDA;
       }
-      // the screen already counted this chunk's rejections; undo by recounting
-      // from scratch is not possible, so histogram is rebuilt per chunk below
-      chunk = std::max<uint64_t>(1, chunk / 8);
+      chunk = std::max<uint64_t>(1, std::min(chunk, hi - lo) / 8);
       cudaMemsetAsync(hist, 0, 64, st);
       lo = begin;
-      h_surv.clear();
+      pass_all.clear();
       passed = 0;
-      std::fill(k2_hist, k2_hist + ATC_REASON_COUNT, 0);
       continue;
     }
     if (ctx->prof) ctx->prof_survivors += (long long)c;
-    h_surv.resize(c);
-    h_keys.resize(c);
-    if (c) {
-      cudaMemcpyAsync(h_surv.data(), surv, c * 8, cudaMemcpyDeviceToHost, st);
-      cudaMemcpyAsync(h_keys.data(), skeys, c * 4, cudaMemcpyDeviceToHost, st);
-      if (!atc_cuda_ok(ctx, cudaStreamSynchronize(st), "survivor D2H")) return ATC_ERR_CUDA;
+    const uint64_t want = std::min<uint64_t>(npass, cap > 0 ? (uint64_t)cap : 0);
+    std::vector<uint64_t> chunk_pass(h_res + 2, h_res + 2 + std::min(want, pre));
+    if (want > pre) {  // rare: more passing bindings than the pinned prefix
+      chunk_pass.resize(want);
+      if (!atc_cuda_ok(ctx, cudaMemcpyAsync(chunk_pass.data(), res + 2, want * 8, cudaMemcpyDeviceToHost, st),
+                       "D2H passing") ||
+          !atc_cuda_ok(ctx, cudaStreamSynchronize(st), "passing sync"))
+        return ATC_ERR_CUDA;
     }
-    std::vector<uint64_t> pass_idx;
-    for (uint64_t i = 0; i < c; ++i) {
-      if (h_keys[i] == kPassKey)
-        pass_idx.push_back(lo + h_surv[i]);
-      else
-        k2_hist[h_keys[i] & 7]++;
-    }
-    std::sort(pass_idx.begin(), pass_idx.end());
-    for (uint64_t g : pass_idx) {
-      if (survivors && passed < cap) survivors[passed] = g;
-      ++passed;
-    }
+    std::sort(chunk_pass.begin(), chunk_pass.end());
+    pass_all.insert(pass_all.end(), chunk_pass.begin(), chunk_pass.end());
+    passed += (int64_t)npass;
     lo = hi;
   }
-  unsigned long long h_hist[ATC_REASON_COUNT] = {0};
-  cudaMemcpyAsync(h_hist, hist, sizeof h_hist, cudaMemcpyDeviceToHost, st);
-  if (!atc_cuda_ok(ctx, cudaStreamSynchronize(st), "hist D2H")) return ATC_ERR_CUDA;
+  for (size_t i = 0; i < pass_all.size() && (int64_t)i < cap; ++i)
+    if (survivors) survivors[i] = pass_all[i];
   if (n_survivors) *n_survivors = passed;
   if (reason_counts) {
-    for (int r = 0; r < ATC_REASON_COUNT; ++r) reason_counts[r] = (int64_t)h_hist[r] + k2_hist[r];
+    const uint64_t* h_hist = h_res + 2 + kResultPrefix;
+    for (int r = 0; r < ATC_REASON_COUNT; ++r) reason_counts[r] = (int64_t)h_hist[r];
     reason_counts[ATC_PASS] = passed;
   }
   return ATC_OK;

@@ -36,3 +36,4 @@ void atc_pool_free(atc_ctx* ctx, void* p);
 void atc_set_error(atc_ctx* ctx, const char* fmt, ...);
 bool atc_cuda_ok(atc_ctx* ctx, cudaError_t e, const char* what);
 void* atc_ctx_scratch(atc_ctx* ctx, int slot, size_t bytes);
+void* atc_ctx_pinned(atc_ctx* ctx, int slot, size_t bytes);

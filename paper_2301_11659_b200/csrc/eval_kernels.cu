@@ -665,3 +665,23 @@ __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
 }
 
 }  // namespace atc
+
+namespace atc {
+// Enumerated spaces: fold the K2 outcome of every survivor into the passing list
+// (global indices) and the reason histogram, so the host reads one small block.
+__global__ void k_finalize(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
+                           const int32_t* surv_keys, uint64_t base, uint64_t* res, unsigned long long* hist) {
+  unsigned long long cnt = *surv_cnt;
+  if (blockIdx.x == 0 && threadIdx.x == 0) res[0] = cnt;
+  if (cnt > cap) return;  // overflow: the host retries with smaller chunks
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
+    const int32_t k = surv_keys[i];
+    if (k == kPassKey) {
+      const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(res + 1), 1ull);
+      res[2 + slot] = base + surv[i];
+    } else {
+      atomicAdd(&hist[k & 7], 1ull);
+    }
+  }
+}
+}  // namespace atc

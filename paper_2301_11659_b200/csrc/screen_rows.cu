@@ -53,23 +53,55 @@ __global__ void __launch_bounds__(256) k_screen_rows(TestsetView ts, SpecView sp
   const bool row_major = sp.layout == ATC_LAYOUT_ROW;
   unsigned int cnt1 = 0, cnt2 = 0, cnt3 = 0, cnt4 = 0;
   const uint64_t row_lo = begin / nI, row_hi = (end + nI - 1) / nI;
-  for (uint64_t row = row_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; row < row_hi;
-       row += (uint64_t)gridDim.x * blockDim.x) {
+  // each thread owns kRowBlock consecutive rows: one full decode, then an
+  // odometer step (digit 1 upwards, carrying into the permutation) per row
+  constexpr int kRowBlock = 4;
+  const uint64_t blocks = (row_hi - row_lo + kRowBlock - 1) / kRowBlock;
+  for (uint64_t rb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; rb < blocks;
+       rb += (uint64_t)gridDim.x * blockDim.x) {
+  const uint64_t row0 = row_lo + rb * kRowBlock;
+  uint64_t perm = (row0 * nI) / size_maps;
+  int digit[NS];
+  digit[0] = 0;
+  {
+    uint64_t s = (row0 * nI - perm * size_maps) / nI;
+    if (s < (1ull << 32)) {
+      uint32_t s32 = (uint32_t)s;
+#pragma unroll
+      for (int q = 1; q < NS; ++q) {
+        const uint32_t dq = s32 / (uint32_t)nI;
+        digit[q] = (int)(s32 - dq * (uint32_t)nI);
+        s32 = dq;
+      }
+    } else {
+#pragma unroll
+      for (int q = 1; q < NS; ++q) {
+        const uint64_t dq = s / (uint64_t)nI;
+        digit[q] = (int)(s - dq * (uint64_t)nI);
+        s = dq;
+      }
+    }
+  }
+  for (int rbi = 0; rbi < kRowBlock; ++rbi) {
+    const uint64_t row = row0 + rbi;
+    if (row >= row_hi) break;
+    if (rbi > 0) {  // odometer: next row = next value of digits 1..NS-1
+      bool carry = true;
+#pragma unroll
+      for (int q = 1; q < NS; ++q) {
+        if (carry) {
+          carry = ++digit[q] == nI;
+          if (carry) digit[q] = 0;
+        }
+      }
+      if (carry) ++perm;
+    }
     // ---------------- per-row setup ----------------
     const uint64_t g0 = row * nI;
-    const uint64_t perm = g0 / size_maps;
-    uint64_t s = (g0 - perm * size_maps) / nI;
-    int digit[NS];
     int64_t u[NS];
-    digit[0] = 0;
     u[0] = 0;
 #pragma unroll
-    for (int q = 1; q < NS; ++q) {
-      const uint64_t dq = s / (uint64_t)nI;
-      digit[q] = (int)(s - dq * (uint64_t)nI);
-      s = dq;
-      u[q] = s_u0[digit[q]];
-    }
+    for (int q = 1; q < NS; ++q) u[q] = s_u0[digit[q]];
     int ptr_of[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) ptr_of[a] = perms[perm * 3 + a];
@@ -98,8 +130,14 @@ __global__ void __launch_bounds__(256) k_screen_rows(TestsetView ts, SpecView sp
     // role values not bound to digit 0
     I rv[ATC_SZ_COUNT];
     bool r0[ATC_SZ_COUNT];
+    // only the roles of this semantics (gemm m..ldc, conv n..ow)
+    constexpr int kRoleLo = SEM == ATC_SEM_GEMM ? ATC_SZ_M : ATC_SZ_CN;
+    constexpr int kRoleHi = SEM == ATC_SEM_GEMM ? ATC_SZ_LDC + 1 : ATC_SZ_COUNT;
 #pragma unroll
     for (int rr = 0; rr < ATC_SZ_COUNT; ++rr) {
+      r0[rr] = false;
+      rv[rr] = 0;
+      if (rr < kRoleLo || rr >= kRoleHi) continue;
       const int q = plan.role_q[rr];
       r0[rr] = q == 0;
       rv[rr] = q <= 0 ? 0 : (I)pick<NS>(u, q);
@@ -184,6 +222,7 @@ __global__ void __launch_bounds__(256) k_screen_rows(TestsetView ts, SpecView sp
       }
     }
   }
+  }  // row block
   // per-reason reduction: warp shuffle, one shared atomic per warp, one global per block
   unsigned int cnt[ATC_REASON_COUNT] = {0, cnt1, cnt2, cnt3, cnt4};
 #pragma unroll
