@@ -144,6 +144,12 @@ int cmd_corpus(atc_ctx* ctx) {
     matching::CandidateBinding gpu_binding;
     bool too_many = false;
     int p1_calls = 0;
+    struct Ev {
+      std::string api;
+      int rank;
+      std::string verdict;
+    };
+    std::vector<Ev> evaluated;
     double gpu_ms = 0;
     auto recorded = gpu::record_tests(p.prog, p.function, p.meta.rules, Rng::mix(fseed, "post"), cfg.verify_tests);
     for (const auto* spec : lspecs) {  // pipeline.cpp:227-312 control flow
@@ -153,7 +159,8 @@ int cmd_corpus(atc_ctx* ctx) {
         continue;
       }
       auto lr = gpu::first_accepted(ctx, p.prog, fn, p.function, *spec, ranked.ranked, p.meta.rules, fseed,
-                                    cfg.tests, cfg.verify_tests, &recorded);
+                                    cfg.tests, cfg.verify_tests, &recorded, /*report_parity=*/true);
+      for (size_t i = 0; i < lr.verdicts.size(); ++i) evaluated.push_back({spec->name, (int)i, lr.verdicts[i]});
       p1_calls += lr.p1_calls;
       gpu_ms += lr.gpu_ms;
       if (lr.winner) {
@@ -171,6 +178,13 @@ int cmd_corpus(atc_ctx* ctx) {
     if (same && gpu_status == "Lifted")
       same = gpu_api == fr->winning_api && gpu_rank == fr->manifest.winner_rank &&
              gpu_binding.arrays == fr->manifest.arrays && gpu_binding.sizes == fr->manifest.sizes;
+    // report-level parity: the evaluated[] entries (pipeline.cpp:262-309)
+    bool same_report = evaluated.size() == fr->evaluated.size();
+    for (size_t i = 0; same_report && i < evaluated.size(); ++i)
+      same_report = evaluated[i].api == fr->evaluated[i].api && evaluated[i].rank == fr->evaluated[i].rank &&
+                    evaluated[i].verdict == fr->evaluated[i].verdict;
+    j["same_evaluated"] = same_report;
+    same = same && same_report;
     if (!same) ++mismatches;
     j["gpu_status"] = gpu_status;
     j["gpu_api"] = gpu_api;

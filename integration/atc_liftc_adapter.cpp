@@ -1,10 +1,13 @@
 // See atc_liftc_adapter.hpp.  Reference anchors are cited per function.
 #include "atc_liftc_adapter.hpp"
 
+#include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstring>
 #include <map>
 #include <stdexcept>
+#include <thread>
 
 #include "liftc/equivalence.hpp"
 #include "liftc/rng.hpp"
@@ -76,33 +79,48 @@ RecordedTests record_tests(const minilang::Program& prog, const std::string& fun
   r.region_len.assign(nP, 65536);
   r.init.resize((size_t)tests * nP);
   r.fin.resize((size_t)tests * nP);
-  for (int t = 0; t < tests; ++t) {
+  // the T tests are independent streams (rewriter.cpp:236) and interp::execute is
+  // re-entrant, so they are recorded on parallel host threads
+  auto record_one = [&](int t) {
     Rng rng(Rng::mix(p2seed, "verify:" + function + ":" + std::to_string(t)));
     std::map<std::string, long long> sizes;
     bool drawn = false;
     for (int tries = 0; tries < 20 && !drawn; ++tries) drawn = analysis::draw_sizes(r.int_params, rules, rng, sizes);
     if (!drawn) {
       for (size_t p = 0; p < nP; ++p) r.init[t * nP + p].assign(65536, 0.0);
-      continue;
+      return;
     }
     interp::MemoryImage img = analysis::build_probe_image(*f, sizes, rng);
     for (size_t i = 0; i < nI; ++i) r.ints[t * nI + i] = sizes.at(r.int_params[i]);
     interp::InstrumentationPolicy plain;
     auto ref = interp::execute(prog, function, img, plain);
     for (size_t p = 0; p < nP; ++p) {
-      r.region_len[p] = (int64_t)img.regions.at(r.ptr_params[p]).data.size();
       r.init[t * nP + p] = img.regions.at(r.ptr_params[p]).data;
       if (ref.status == interp::ExecStatus::Normal) r.fin[t * nP + p] = ref.final.regions.at(r.ptr_params[p]).data;
     }
     r.test_ok[t] = ref.status == interp::ExecStatus::Normal;
-  }
+  };
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int workers = (int)std::min<unsigned>(hw, (unsigned)tests);
+  std::atomic<int> next{0};
+  std::vector<std::thread> pool;
+  for (int w = 0; w < workers; ++w)
+    pool.emplace_back([&] {
+      for (int t = next.fetch_add(1); t < tests; t = next.fetch_add(1)) record_one(t);
+    });
+  for (auto& th : pool) th.join();
+  // probe regions are kProbeRegionLen (analysis.cpp:23) long for every pointer
+  for (size_t p = 0; p < nP; ++p)
+    for (int t = 0; t < tests; ++t)
+      if (!r.init[t * nP + p].empty()) r.region_len[p] = (int64_t)r.init[t * nP + p].size();
   return r;
 }
 
 LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const analysis::AnalyzedFunction& fn,
                           const std::string& function, const api::ApiSpec& spec,
                           const std::vector<matching::CandidateBinding>& ranked, const api::SizeRules& rules,
-                          uint64_t fseed, int p1_tests, int verify_tests, const RecordedTests* recorded) {
+                          uint64_t fseed, int p1_tests, int verify_tests, const RecordedTests* recorded,
+                          bool report_parity) {
   LoopResult out;
   if (ranked.empty()) return out;
   auto t0 = std::chrono::steady_clock::now();
@@ -148,16 +166,25 @@ LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const ana
   if (rc != ATC_OK) throw std::runtime_error(atc_last_error(ctx));
   out.gpu_ms = ms_since(t0);
 
-  // P1 on P2 survivors in rank order (pipeline.cpp:257-261 + :271-307)
+  // P1 on P2 survivors in rank order (pipeline.cpp:257-261 + :271-307).  With
+  // report_parity, P1 also runs on the P2-rejected candidates that precede the
+  // winner, so `verdicts` reproduces the reference's evaluated[] entries exactly:
+  // the P1 verdict name, or "VerificationFailed" when P1 said Equivalent but P2
+  // failed (pipeline.cpp:279-283).
   t0 = std::chrono::steady_clock::now();
   for (size_t b = 0; b < ranked.size(); ++b) {
-    if (out.p2_reason[b] != ATC_PASS) continue;
+    const bool p2_ok = out.p2_reason[b] == ATC_PASS;
+    if (!p2_ok && !report_parity) continue;
     equivalence::EquivalenceConfig ec;
     ec.tests = p1_tests;
     ec.seed = fseed;
     ++out.p1_calls;
     auto er = equivalence::check_equivalence(prog, fn, ranked[b], spec, rules, ec);
-    if (er.verdict == equivalence::Verdict::Equivalent) {
+    const bool eq = er.verdict == equivalence::Verdict::Equivalent;
+    if (report_parity)
+      out.verdicts.push_back(eq && !p2_ok ? std::string("VerificationFailed")
+                                          : std::string(equivalence::verdict_name(er.verdict)));
+    if (eq && p2_ok) {
       out.winner = b;
       break;
     }

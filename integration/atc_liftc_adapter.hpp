@@ -51,6 +51,7 @@ struct LoopResult {
   std::vector<int8_t> p2_fail_t, p2_reason;
   int p1_calls = 0;
   double gpu_ms = 0.0, record_ms = 0.0, p1_ms = 0.0;
+  std::vector<std::string> verdicts;  // report_parity: evaluated[] verdicts in rank order
 };
 
 // Replacement of pipeline.cpp:248-310 for one spec: P2 (GPU, batched) for all
@@ -58,7 +59,8 @@ struct LoopResult {
 LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const analysis::AnalyzedFunction& fn,
                           const std::string& function, const api::ApiSpec& spec,
                           const std::vector<matching::CandidateBinding>& ranked, const api::SizeRules& rules,
-                          uint64_t fseed, int p1_tests, int verify_tests, const RecordedTests* recorded = nullptr);
+                          uint64_t fseed, int p1_tests, int verify_tests, const RecordedTests* recorded = nullptr,
+                          bool report_parity = false);
 
 // DispatchContext whose handler is run_dispatch on the GPU (atc_dispatch).
 interp::DispatchContext make_gpu_dispatch(const api::ApiSpec& spec, atc_ctx* ctx);
