@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "atc_b200.h"
@@ -81,6 +82,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -118,6 +130,13 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -146,6 +165,7 @@ struct Problem {
   // conv geometry
   int img, Cin, H, W, R, S, OH, OW;
   int tiles_m, tiles_n, tiles_img;
+  int pair;  // 1: CTA pairs (cluster of 2) on adjacent M tiles share the B tile via TMA multicast
 };
 
 struct Maps {
@@ -154,14 +174,16 @@ struct Maps {
 };
 
 __device__ __forceinline__ void tile_coords(const Problem& p, int tile, int& tm, int& tn, int& ti) {
-  // grouped raster: 16 m-tiles x all n-tiles per group, for L2 reuse of A/B panels
-  const int per_img = p.tiles_m * p.tiles_n;
+  // grouped raster: 16 m-tiles x all n-tiles per group, for L2 reuse of A/B panels.
+  // With p.pair the unit is an M-tile pair: the caller maps tm -> 2*tm + rank.
+  const int tiles_m = p.pair ? (p.tiles_m + 1) / 2 : p.tiles_m;
+  const int per_img = tiles_m * p.tiles_n;
   ti = tile / per_img;
   int t = tile - ti * per_img;
-  const int G = 16;
+  const int G = p.pair ? 8 : 16;
   const int group = t / (G * p.tiles_n);
   const int first_m = group * G;
-  const int gm = min(G, p.tiles_m - first_m);
+  const int gm = min(G, tiles_m - first_m);
   const int in_group = t - group * G * p.tiles_n;
   tm = first_m + in_group % gm;
   tn = in_group / gm;
@@ -210,12 +232,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kblocks = (p.conv ? p.R * p.S * (p.K / BK) : (p.K + BK - 1) / BK);
   const int total_kb = kblocks * p.splits;
-  const int num_tiles = p.tiles_m * p.tiles_n * p.tiles_img;
+  // work units: single tiles, or M-tile pairs processed by a 2-CTA cluster
+  uint32_t rank = 0;
+  if (p.pair) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int num_units = (p.pair ? (p.tiles_m + 1) / 2 : p.tiles_m) * p.tiles_n * p.tiles_img;
+  const int unit0 = p.pair ? (int)(blockIdx.x / 2) : (int)blockIdx.x;
+  const int unit_step = p.pair ? (int)(gridDim.x / 2) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], p.pair ? 2 : 1);  // pair: both CTAs' MMAs release the stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
@@ -231,6 +258,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
   }
   tc_fence_before();
   __syncthreads();
+  if (p.pair) cluster_sync();  // peer barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
 
@@ -239,9 +267,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       // ================= TMA producer =================
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int unit = unit0; unit < num_units; unit += unit_step) {
         int tm, tn, ti;
-        tile_coords(p, tile, tm, tn, ti);
+        tile_coords(p, unit, tm, tn, ti);
+        if (p.pair) tm = 2 * tm + (int)rank;
         for (int kb = 0; kb < total_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           int sa, sb, a0, a1, b0, b1;
@@ -253,12 +282,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           if (p.conv == 1) {
             // K-major: 256 pixel rows x 32 channels (128 B) in one box
             tma_load_2d(sB, &maps.b[sb], &full[stage], b0, b1);
+          } else if (p.pair) {
+            // MN-major B shared by the pair: this CTA loads half of the 8 chunks and
+            // multicasts them into both CTAs' smem (each CTA's full barrier expects
+            // its A plus all of B)
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) {
+              const int jj = (int)rank * (BN / 64) + j;
+              tma_load_2d_mc(sB + jj * (BK * 128), &maps.b[sb], &full[stage], b0 + 32 * jj, b1, 0x3);
+            }
           } else {
             // MN-major: 8 chunks of [32 K rows x 32 N]
 #pragma unroll
             for (int j = 0; j < BN / 32; ++j)
               tma_load_2d(sB + j * (BK * 128), &maps.b[sb], &full[stage], b0 + 32 * j, b1);
           }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (p.pair) {
+        // tail: wait until both CTAs' MMAs released every stage, so no remote
+        // arrive is still in flight towards this CTA's barriers at exit
+        for (int i = 0; i < STAGES; ++i) {
+          mbar_wait(&empty[stage], phase ^ 1);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -273,7 +322,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int unit = unit0; unit < num_units; unit += unit_step) {
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -293,7 +342,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
                                             : make_desc(b_addr + kk * 1024, BK * 128, 512, kSw128Base32);
             mma_tf32(d_tmem, ad, bd, p.conv == 1 ? idesc_tf32(0) : idesc_tf32(1), (kb > 0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&empty[stage]);  // smem stage free once these MMAs complete
+          // smem stage free once these MMAs complete (pair: in both CTAs)
+          if (p.pair)
+            mma_commit_mc(&empty[stage], 0x3);
+          else
+            mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -311,9 +364,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
     const int q = warp - 4;  // TMEM lanes 32q .. 32q+31
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int unit = unit0; unit < num_units; unit += unit_step) {
       int tm, tn, ti;
-      tile_coords(p, tile, tm, tn, ti);
+      tile_coords(p, unit, tm, tn, ti);
+      if (p.pair) tm = 2 * tm + (int)rank;
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const int row = tm * BM + q * 32 + lane;  // output row (gemm M / conv filter)
@@ -376,6 +430,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
   }
   tc_fence_before();
   __syncthreads();
+  if (p.pair) cluster_sync();  // no multicast or remote arrive may still target this CTA
   tc_fence_after();
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
@@ -497,6 +552,16 @@ bool make_map(atc_ctx* ctx, CUtensorMap* m, const float* base, uint64_t rows, ui
   return true;
 }
 
+// CTA pairs need an MN-major B (loaded as chunks, half by each CTA) and >= 2
+// M tiles; ATC_TC_PAIR=0 disables them (A/B measurement)
+int use_pair(const Problem& p) {
+  static const int enabled = [] {
+    const char* e = std::getenv("ATC_TC_PAIR");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return enabled && p.conv != 1 && p.tiles_m >= 2 ? 1 : 0;
+}
+
 bool launch(atc_ctx* ctx, const Maps& maps, const Problem& p, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
@@ -504,6 +569,23 @@ bool launch(atc_ctx* ctx, const Maps& maps, const Problem& p, cudaStream_t st) {
                      "cudaFuncSetAttribute"))
       return false;
     configured = true;
+  }
+  if (p.pair) {
+    // 2-CTA clusters: one M-tile pair per cluster iteration, persistent over pairs
+    const int units = (p.tiles_m + 1) / 2 * p.tiles_n * p.tiles_img;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(2 * std::min(units, ctx->sm_count / 2)));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return atc_cuda_ok(ctx, cudaLaunchKernelEx(&cfg, k_tc_gemm, maps, p), "k_tc_gemm cluster launch");
   }
   const int tiles = p.tiles_m * p.tiles_n * p.tiles_img;
   const int grid = std::min(tiles, ctx->sm_count);
@@ -555,6 +637,7 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
   p.tiles_m = (int)((m + BM - 1) / BM);
   p.tiles_n = (int)((n + BN - 1) / BN);
   p.tiles_img = 1;
+  p.pair = use_pair(p);
   p.splits = precision == ATC_PREC_3XTF32 ? 3 : 1;
   if (p.splits == 3) {
     float* ah = (float*)atc_ctx_scratch(ctx, 13, (size_t)m * kp * 4 * 2);
@@ -680,6 +763,7 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
   // only pixels p < OH*W can be valid outputs (rows y < OH)
   p.tiles_n = (int)((oh * w_ + BN - 1) / BN);
   p.tiles_img = (int)n;
+  p.pair = use_pair(p);
   return launch(ctx, maps, p, st) ? ATC_OK : ATC_ERR_CUDA;
 }
 
