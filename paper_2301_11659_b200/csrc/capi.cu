@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -24,6 +25,9 @@ __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, 
 __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
                               uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                               unsigned long long* reason_hist);
+__global__ void k_screen_conv_rows(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
+                                   uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
+                                   unsigned long long* surv_cnt, unsigned long long* reason_hist);
 template <int SEM, int NS, bool I32, uint32_t Q0MASK>
 __global__ void k_screen_rows(TestsetView ts, SpecView sp, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
                               uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
@@ -443,6 +447,24 @@ constexpr int kScreenThreads = 256;
 
 int screen_budget(const SpecView& sp) { return sp.sem == ATC_SEM_GEMM ? 16 : 2; }
 
+// Preconditions of k_screen_conv_rows (screen_rows.cu): the bundled conv2d
+// shape — roles tc_n..tc_ow on size params 0..8, dims in=(n,c,h,w),
+// weights=(c,k,r,s), out=(n,k,oh,ow) in any order, in/weights/out = arrays
+// 0/1/2, a table key free of digit 0, nI <= 32.  ATC_SCREEN_GENERIC=1 forces
+// the generic k_screen_rows (A/B checks).
+bool conv_thresholds_ok(const SpecView& sp, const RowPlan& plan, int nI) {
+  static const bool generic = [] {
+    const char* e = std::getenv("ATC_SCREEN_GENERIC");
+    return e && e[0] == '1';
+  }();
+  if (generic || sp.sem != ATC_SEM_CONV2D || sp.nS != 9 || sp.nA != 3 || nI > kMaxInts) return false;
+  for (int i = 0; i < 9; ++i)
+    if (plan.role_q[ATC_SZ_CN + i] != i) return false;
+  if (plan.dim_mask[0] != 0xFu || plan.dim_mask[1] != 0x72u || plan.dim_mask[2] != 0x191u) return false;
+  if (sp.arr_of_role[0] != 0 || sp.arr_of_role[1] != 1 || sp.arr_of_role[2] != 2) return false;
+  return plan.key_stride[0] == 0;
+}
+
 // Runs K1 + K2 over `n` bindings; survivors/keys live in ctx scratch.
 int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, const BindingSource& src,
              uint64_t n, int32_t* keys, uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
@@ -501,6 +523,9 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
         ATC_LAUNCH_ROWS(ATC_SEM_GEMM, 6, kM);
       else
         ATC_LAUNCH_ROWS(ATC_SEM_GEMM, 6, kDyn);
+    } else if (i32 && conv_thresholds_ok(sp, *plan, ts->nI)) {
+      k_screen_conv_rows<<<g2, kScreenThreads, 0, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
+                                                        surv_cap, surv_cnt, hist);
     } else {
       if (q0mask == kCN)
         ATC_LAUNCH_ROWS(ATC_SEM_CONV2D, 9, kCN);

@@ -173,3 +173,66 @@ def test_fp32_screen_mode_64cubed(ev, stem):
                                mode=L.MODE_FP32_SCREEN)
         np.testing.assert_array_equal(got.fail_t, v["fail_t"])
         np.testing.assert_array_equal(got.reason, v["reason"])
+
+
+def _shrunk(ts, lens):
+    """The same tests with region p cut to lens[p] elements (None: unchanged)."""
+    from paper_2301_11659_b200.evaluator import RecordedTestsets
+
+    cut = lambda a, L: a if (a is None or L is None) else a[:L].copy()
+    init = [[cut(a, lens[p]) for p, a in enumerate(row)] for row in ts.init]
+    final = [None if row is None else [cut(a, lens[p]) for p, a in enumerate(row)] for row in ts.final]
+    return RecordedTestsets(ts.params, ts.ints.copy(), init, final, ts.test_ok.copy())
+
+
+CONV_VARIANTS = {
+    "recorded": lambda ts: ts,
+    # small regions: dispatch failures (extent > region) and access-bound (UB) failures
+    "in_3000": lambda ts: _shrunk(ts, [3000, None, None, None]),
+    "in_700_out_900": lambda ts: _shrunk(ts, [700, None, 900, None]),
+    "wt_200": lambda ts: _shrunk(ts, [None, 200, None, None]),
+    # digit values < 1 (dispatch "size #q is not positive")
+    "zero_int": lambda ts: _with_int(ts, 1, 0),
+    "neg_int": lambda ts: _with_int(ts, 0, -3),
+    "test0_failed": lambda ts: _with_ok(ts, 0),
+}
+
+
+def _with_int(ts, i, v):
+    ts = _shrunk(ts, [None] * 4)
+    ts.ints[0, i] = v
+    return ts
+
+
+def _with_ok(ts, t):
+    ts = _shrunk(ts, [None] * 4)
+    ts.test_ok[t] = 0
+    return ts
+
+
+@pytest.mark.parametrize("variant", sorted(CONV_VARIANTS))
+@pytest.mark.parametrize("stem", ["conv_direct", "im2col_buffered", "conv_permuted_sig"])
+def test_enumerated_conv_matches_explicit(ev, stem, variant):
+    """The enumerated conv screen (k_screen_conv_rows: digit-0 verdicts by
+    thresholds) returns exactly the passing set and reason histogram of the
+    explicit per-binding path (k_screen/k_confirm, itself pinned to the reference
+    dumps) on whole row-unaligned ranges, including test sets that make the
+    dispatch, access-bound and test-set reasons occur."""
+    p = fixtures.load(stem)
+    space = p.space("conv2d")
+    spec = fixtures.spec("conv2d")
+    ts = CONV_VARIANTS[variant](p.testsets(16))
+    rng = np.random.default_rng(11)
+    ranges = [(0, 1 << 19), (int(rng.integers(1, space.count - (1 << 20))), 654_321),
+              (space.count - 100_003, space.count), (381367040, 381367049)]
+    for b, e in ranges:
+        e = b + e if e < b else e
+        passing, n, hist = ev.eval_enumerated(spec, ts, space, b, e)
+        idx = np.arange(b, e, dtype=np.uint64)
+        am, sm = space.decode(idx)
+        got = ev.eval_bindings(spec, ts, am, sm)
+        want = idx[got.reason == 0]
+        np.testing.assert_array_equal(passing, want, err_msg=f"{stem}/{variant} [{b},{e})")
+        assert n == len(want)
+        assert hist.tolist() == np.bincount(got.reason, minlength=5).tolist(), (stem, variant, b, e)
+        print(stem, variant, b, e, hist.tolist())
