@@ -25,7 +25,7 @@ __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, 
 __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
                               uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                               unsigned long long* reason_hist);
-__global__ void k_screen_conv_rows(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
+__global__ void k_screen_conv_planes(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
                                    uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
                                    unsigned long long* surv_cnt, unsigned long long* reason_hist);
 template <int SEM, int NS, bool I32, uint32_t Q0MASK>
@@ -447,7 +447,7 @@ constexpr int kScreenThreads = 256;
 
 int screen_budget(const SpecView& sp) { return sp.sem == ATC_SEM_GEMM ? 16 : 2; }
 
-// Preconditions of k_screen_conv_rows (screen_rows.cu): the bundled conv2d
+// Preconditions of k_screen_conv_planes (screen_rows.cu): the bundled conv2d
 // shape — roles tc_n..tc_ow on size params 0..8, dims in=(n,c,h,w),
 // weights=(c,k,r,s), out=(n,k,oh,ow) in any order, in/weights/out = arrays
 // 0/1/2, a table key free of digit 0, nI <= 32.  ATC_SCREEN_GENERIC=1 forces
@@ -524,7 +524,7 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
       else
         ATC_LAUNCH_ROWS(ATC_SEM_GEMM, 6, kDyn);
     } else if (i32 && conv_thresholds_ok(sp, *plan, ts->nI)) {
-      k_screen_conv_rows<<<g2, kScreenThreads, 0, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
+      k_screen_conv_planes<<<g2, kScreenThreads, 0, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
                                                         surv_cap, surv_cnt, hist);
     } else {
       if (q0mask == kCN)

@@ -237,28 +237,32 @@ __global__ void __launch_bounds__(256) k_screen_rows(TestsetView ts, SpecView sp
 }
 
 // ----------------------------------------------------------------------------
-// k_screen_conv_rows: k_screen_rows for the bundled conv2d spec shape, with the
-// digit-0 loop replaced by thresholds.
+// k_screen_conv_planes: k_screen_rows for the bundled conv2d spec shape, with
+// the loops over digits 0 and 1 (tc_n, tc_c) replaced by thresholds.
 //
-// Preconditions (checked by the host, capi.cu): roles tc_n .. tc_ow bound to
-// size params 0 .. 8 in order, array dims in = (n,c,h,w), weights = (c,k,r,s),
-// out = (n,k,oh,ow), roles in/weights/out = API arrays 0/1/2, every digit value
-// |u| <= 200 (so every product below is exact in 32 bits) and nI <= 32.
+// Preconditions (checked by the host, capi.cu conv_thresholds_ok): roles
+// tc_n .. tc_ow bound to size params 0 .. 8 in order, array dims in = (n,c,h,w),
+// weights = (c,k,r,s), out = (n,k,oh,ow) in any order, in/weights/out = API
+// arrays 0/1/2, every digit value |u| <= 200 (every product below is exact in
+// 32 bits), nI <= 32, a position-0 table key free of digit 0.
 //
-// With the row (array permutation + digits 1..8) fixed, each check of the
-// screen is a threshold on x = tc_n (digit 0):
-//   dispatch (rewriter.cpp:136-148)  fails iff x < 1, x*c*h*w > len(in) or
-//                                    x*k*oh*ow > len(out) (the weights extent
-//                                    c*k*r*s is row-constant)
-//   access bound (UB)                fails iff x*c*h*w + Q >= len(in), Q = the
-//                                    digit-0-free part of the last input index;
-//                                    the weights/out bounds coincide with the
-//                                    extents already checked
+// A thread owns a "plane": the nI x nI bindings sharing the permutation and
+// digits 2..8 (contiguous in Appendix C order).  With x = tc_n and c = tc_c,
+// every t = 0 check of the screen is a threshold on x whose bound depends on
+// the plane and on c only through one small division:
+//   dispatch (rewriter.cpp:136-148)  fails iff x < 1, c < 1, a digit 2..8 < 1,
+//                                    c > len(wt)/(k*r*s), x > (len(in)/(h*w))/c
+//                                    or x > len(out)/(k*oh*ow)   [floors]
+//   access bound (UB)                fails iff x*c*h*w + Q >= len(in), i.e.
+//                                    x > ((len(in) - Q - 1)/(h*w))/c, Q = the
+//                                    x-free part of the last input index; the
+//                                    weights/out bounds equal the extents above
 //   written set                      fails iff x*k*oh*ow <= dirty_max(out)
-//   position 0                       the row's tabulated verdict (k_pos0_table)
-// so the row's verdicts over its nI bindings are bit masks: gt[T] = the digits
-// whose value exceeds T, tabulated once per CTA for T in [0, 255].  Verdicts and
-// reason counts are identical to k_screen_rows (tests/test_gpu_eval.py).
+//   position 0                       the tabulated verdict of (perm, c,h,w,r,s)
+// (floor(floor(a/b)/c) = floor(a/(b*c)) for positive integers).  A row's
+// verdicts over its nI values of x are then bit masks: gt[T] = the digits whose
+// value exceeds T, tabulated once per CTA for T in [0, 255].  Verdicts, reason
+// counts and survivors are identical to k_screen_rows (tests/test_gpu_eval.py).
 constexpr int kGtCap = 255;  // > every digit value in 32-bit mode (<= 200)
 
 // min(floor(a / b), kGtCap) for a >= 0, b >= 1, rb ~= 1/b: float estimate, exact fix-up
@@ -270,16 +274,22 @@ __device__ __forceinline__ int div_cap(int64_t a, int64_t b, float rb) {
   return q;
 }
 
-__global__ void __launch_bounds__(256) k_screen_conv_rows(TestsetView ts, const uint8_t* perms, uint64_t size_maps,
-                                                           uint64_t begin, uint64_t end, RowPlan plan, uint64_t* surv,
-                                                           uint64_t surv_cap, unsigned long long* surv_cnt,
-                                                           unsigned long long* reason_hist) {
+__global__ void __launch_bounds__(256) k_screen_conv_planes(TestsetView ts, const uint8_t* perms,
+                                                             uint64_t size_maps, uint64_t begin, uint64_t end,
+                                                             RowPlan plan, uint64_t* surv, uint64_t surv_cap,
+                                                             unsigned long long* surv_cnt,
+                                                             unsigned long long* reason_hist) {
   constexpr int NS = 9;
   __shared__ int32_t s_u[kMaxInts];
+  __shared__ float s_rcp[kMaxInts];
   __shared__ uint32_t s_gt[kGtCap + 1];
   __shared__ unsigned int s_hist[ATC_REASON_COUNT];
   const int nI = ts.nI;
-  if (threadIdx.x < nI) s_u[threadIdx.x] = (int32_t)ts.ints[threadIdx.x];
+  if (threadIdx.x < nI) {
+    const int32_t u = (int32_t)ts.ints[threadIdx.x];
+    s_u[threadIdx.x] = u;
+    s_rcp[threadIdx.x] = __frcp_rn((float)(u > 0 ? u : 1));
+  }
   if (threadIdx.x < ATC_REASON_COUNT) s_hist[threadIdx.x] = 0;
   for (int t = threadIdx.x; t <= kGtCap; t += blockDim.x) {
     uint32_t m = 0;
@@ -289,81 +299,84 @@ __global__ void __launch_bounds__(256) k_screen_conv_rows(TestsetView ts, const 
   __syncthreads();
   const bool test_ok0 = ts.test_ok[0] != 0;
   const uint32_t per_perm = (uint32_t)plan.pt.per_perm;  // table < 256 MB: 32-bit keys
+  const uint32_t ks1 = (uint32_t)plan.key_stride[1];
+  const uint32_t gt0 = s_gt[0];
+  const uint64_t nI2 = (uint64_t)nI * nI;
+  const uint64_t planes_per_perm = size_maps / nI2;
   unsigned int cnt1 = 0, cnt2 = 0, cnt3 = 0, cnt4 = 0;
-  const uint64_t row_lo = begin / nI, row_hi = (end + nI - 1) / nI;
-  constexpr int kRowBlock = 8;
-  const uint64_t blocks = (row_hi - row_lo + kRowBlock - 1) / kRowBlock;
-  for (uint64_t rb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; rb < blocks;
-       rb += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t row0 = row_lo + rb * kRowBlock;
-    uint64_t perm = (row0 * nI) / size_maps;
+  const uint64_t plane_lo = begin / nI2, plane_hi = (end + nI2 - 1) / nI2;
+  for (uint64_t pl = plane_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; pl < plane_hi;
+       pl += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p0 = pl * nI2;
+    const uint64_t lo = p0 < begin ? begin : p0, hi = p0 + nI2 > end ? end : p0 + nI2;
+    const unsigned int n_here = (unsigned int)(hi - lo);
+    if (!test_ok0) {
+      cnt3 += n_here;
+      continue;
+    }
+    const uint64_t perm = pl / planes_per_perm;
     int digit[NS];
     {
-      uint64_t s = (row0 * nI - perm * size_maps) / nI;
+      uint64_t s = pl - perm * planes_per_perm;  // digits 2..8
       if (s < (1ull << 32)) {
         uint32_t s32 = (uint32_t)s;
 #pragma unroll
-        for (int q = 1; q < NS; ++q) {
+        for (int q = 2; q < NS; ++q) {
           const uint32_t dq = s32 / (uint32_t)nI;
           digit[q] = (int)(s32 - dq * (uint32_t)nI);
           s32 = dq;
         }
       } else {
 #pragma unroll
-        for (int q = 1; q < NS; ++q) {
+        for (int q = 2; q < NS; ++q) {
           const uint64_t dq = s / (uint64_t)nI;
           digit[q] = (int)(s - dq * (uint64_t)nI);
           s = dq;
         }
       }
     }
-    for (int rbi = 0; rbi < kRowBlock; ++rbi) {
-      const uint64_t row = row0 + rbi;
-      if (row >= row_hi) break;
-      if (rbi > 0) {  // odometer over digits 1..8, carrying into the permutation
-        bool carry = true;
+    const int32_t ch = s_u[digit[2]], cw = s_u[digit[3]], ck = s_u[digit[4]], cr = s_u[digit[5]];
+    const int32_t cs = s_u[digit[6]], coh = s_u[digit[7]], cow = s_u[digit[8]];
+    if (min(min(min(ch, cw), min(ck, cr)), min(min(cs, coh), cow)) < 1) {
+      cnt2 += n_here;  // a dim of the plane < 1: "size is not positive" for every binding
+      continue;
+    }
+    const int p_in = perms[perm * 3 + 0], p_w = perms[perm * 3 + 1], p_out = perms[perm * 3 + 2];
+    const int64_t len_in = ts.region_len[p_in], len_w = ts.region_len[p_w], len_out = ts.region_len[p_out];
+    const int32_t hw = ch * cw, krs = ck * cr * cs, ext_out = ck * coh * cow;
+    const float r_out = __frcp_rn((float)ext_out);
+    // plane-level bounds (exact floors)
+    const int64_t c_max = len_w / krs;    // weights extent: c*k*r*s <= len(wt)
+    const int64_t a_in = len_in / hw;     // in extent: x*c <= a_in
+    const int32_t q_in = -hw + (coh + cr - 2) * cw + (cow + cs - 2);
+    const int64_t alim = len_in - q_in;   // UB iff x*c*h*w >= alim
+    const int64_t b_in = alim > 0 ? (alim - 1) / hw : -1;
+    const uint32_t out_fail = s_gt[div_cap(len_out, ext_out, r_out)];
+    const int dmax = ts.dirty_max[p_out];
+    const uint32_t dirty_fail = ~s_gt[dmax < 0 ? 0 : div_cap(dmax, ext_out, r_out)];
+    uint32_t key = (uint32_t)perm * per_perm;
 #pragma unroll
-        for (int q = 1; q < NS; ++q) {
-          if (carry) {
-            carry = ++digit[q] == nI;
-            if (carry) digit[q] = 0;
-          }
-        }
-        if (carry) ++perm;
-      }
-      const uint64_t g0 = row * nI;
+    for (int q = 2; q < NS; ++q) key += (uint32_t)digit[q] * (uint32_t)plan.key_stride[q];
+    for (int j = 0; j < nI; ++j) {  // digit 1: tc_c
+      const uint64_t g0 = p0 + (uint64_t)j * nI;
+      if (g0 + nI <= begin || g0 >= end) continue;
       const int v_lo = g0 < begin ? (int)(begin - g0) : 0;
       const int v_hi = g0 + nI > end ? (int)(end - g0) : nI;
       const uint32_t range = (v_hi >= 32 ? 0xFFFFFFFFu : ((1u << v_hi) - 1u)) & ~((1u << v_lo) - 1u);
-      if (!test_ok0) {
-        cnt3 += __popc(range);
+      const int32_t c = s_u[j];
+      if (c < 1 || c > c_max) {
+        cnt2 += __popc(range);
         continue;
       }
-      const int32_t cc = s_u[digit[1]], ch = s_u[digit[2]], cw = s_u[digit[3]], ck = s_u[digit[4]];
-      const int32_t cr = s_u[digit[5]], cs = s_u[digit[6]], coh = s_u[digit[7]], cow = s_u[digit[8]];
-      const int p_in = perms[perm * 3 + 0], p_w = perms[perm * 3 + 1], p_out = perms[perm * 3 + 2];
-      const int64_t len_in = ts.region_len[p_in], len_w = ts.region_len[p_w], len_out = ts.region_len[p_out];
-      const int32_t ext_in = cc * ch * cw, ext_w = cc * ck * cr * cs, ext_out = ck * coh * cow;
-      if (min(min(min(cc, ch), min(cw, ck)), min(min(cr, cs), min(coh, cow))) < 1 || ext_w > len_w) {
-        cnt2 += __popc(range);  // a non-digit-0 dim < 1, or the weights extent: every binding of the row
-        continue;
-      }
-      const float r_in = __frcp_rn((float)ext_in), r_out = __frcp_rn((float)ext_out);
-      const uint32_t dm =
-          range & (~s_gt[0] | s_gt[div_cap(len_in, ext_in, r_in)] | s_gt[div_cap(len_out, ext_out, r_out)]);
+      const float rc = s_rcp[j];
+      const uint32_t dm = range & (~gt0 | out_fail | s_gt[div_cap(a_in, c, rc)]);
       uint32_t ok = range & ~dm, um = 0, mm = 0;
       if (ok) {
-        const int32_t q_in = -ch * cw + (coh + cr - 2) * cw + (cow + cs - 2);
-        const int64_t alim = len_in - q_in;
-        um = alim <= 0 ? ok : (ok & s_gt[div_cap(alim - 1, ext_in, r_in)]);
+        um = b_in < 0 ? ok : (ok & s_gt[div_cap(b_in, c, rc)]);
         ok &= ~um;
         if (ok) {
-          uint32_t key = (uint32_t)perm * per_perm;
-#pragma unroll
-          for (int q = 1; q < NS; ++q) key += (uint32_t)digit[q] * (uint32_t)plan.key_stride[q];
-          const int dmax = ts.dirty_max[p_out];
-          const bool tab_fail = __ldg(plan.pt.table + key) == 1;
-          mm = tab_fail ? ok : (ok & ~s_gt[dmax < 0 ? 0 : div_cap(dmax, ext_out, r_out)]);
+          const bool tab_fail = __ldg(plan.pt.table + key + (uint32_t)j * ks1) == 1;
+          mm = tab_fail ? ok : (ok & dirty_fail);
           ok &= ~mm;
         }
       }

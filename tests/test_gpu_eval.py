@@ -213,7 +213,7 @@ def _with_ok(ts, t):
 @pytest.mark.parametrize("variant", sorted(CONV_VARIANTS))
 @pytest.mark.parametrize("stem", ["conv_direct", "im2col_buffered", "conv_permuted_sig"])
 def test_enumerated_conv_matches_explicit(ev, stem, variant):
-    """The enumerated conv screen (k_screen_conv_rows: digit-0 verdicts by
+    """The enumerated conv screen (k_screen_conv_planes: digit-0 verdicts by
     thresholds) returns exactly the passing set and reason histogram of the
     explicit per-binding path (k_screen/k_confirm, itself pinned to the reference
     dumps) on whole row-unaligned ranges, including test sets that make the
