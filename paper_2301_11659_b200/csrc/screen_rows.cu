@@ -274,6 +274,21 @@ __device__ __forceinline__ int div_cap(int64_t a, int64_t b, float rb) {
   return q;
 }
 
+// min(floor(a / c), kGtCap) for 0 <= a <= kDivClamp, 1 <= c <= 200, rc ~= 1/c (exact)
+constexpr int32_t kDivClamp = kGtCap * 200;  // a >= this gives kGtCap for every c <= 200
+__device__ __forceinline__ int div_small(int32_t a, int32_t c, float rc) {
+  int q = __float2int_rz(__int2float_rn(a) * rc);  // a < 2^24: |error| < 1
+  q -= q * c > a;
+  q += (q + 1) * c <= a;
+  return min(q, kGtCap);
+}
+
+// min(floor(a / b), kDivClamp) for a >= 0, b >= 1
+__device__ __forceinline__ int32_t clamp_div(int64_t a, int32_t b) {
+  if (a >= (int64_t)b * kDivClamp) return kDivClamp;
+  return (int32_t)((uint32_t)a / (uint32_t)b);  // a < 200 * 255 * b < 2^32 here (b <= 200^2)
+}
+
 __global__ void __launch_bounds__(256) k_screen_conv_planes(TestsetView ts, const uint8_t* perms,
                                                              uint64_t size_maps, uint64_t begin, uint64_t end,
                                                              RowPlan plan, uint64_t* surv, uint64_t surv_cap,
@@ -303,6 +318,8 @@ __global__ void __launch_bounds__(256) k_screen_conv_planes(TestsetView ts, cons
   const uint32_t gt0 = s_gt[0];
   const uint64_t nI2 = (uint64_t)nI * nI;
   const uint64_t planes_per_perm = size_maps / nI2;
+  const uint32_t all_rows = nI >= 32 ? 0xFFFFFFFFu : ((1u << nI) - 1u);
+  const uint32_t magic = (uint32_t)(0xFFFFFFFFull / (uint32_t)nI) + 1u;  // n / nI = umulhi(n, magic), n < 2^27
   unsigned int cnt1 = 0, cnt2 = 0, cnt3 = 0, cnt4 = 0;
   const uint64_t plane_lo = begin / nI2, plane_hi = (end + nI2 - 1) / nI2;
   for (uint64_t pl = plane_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; pl < plane_hi;
@@ -318,7 +335,15 @@ __global__ void __launch_bounds__(256) k_screen_conv_planes(TestsetView ts, cons
     int digit[NS];
     {
       uint64_t s = pl - perm * planes_per_perm;  // digits 2..8
-      if (s < (1ull << 32)) {
+      if (s < (1ull << 27)) {
+        uint32_t s32 = (uint32_t)s;
+#pragma unroll
+        for (int q = 2; q < NS; ++q) {
+          const uint32_t dq = __umulhi(s32, magic);
+          digit[q] = (int)(s32 - dq * (uint32_t)nI);
+          s32 = dq;
+        }
+      } else if (s < (1ull << 32)) {
         uint32_t s32 = (uint32_t)s;
 #pragma unroll
         for (int q = 2; q < NS; ++q) {
@@ -347,10 +372,12 @@ __global__ void __launch_bounds__(256) k_screen_conv_planes(TestsetView ts, cons
     const float r_out = __frcp_rn((float)ext_out);
     // plane-level bounds (exact floors)
     const int64_t c_max = len_w / krs;    // weights extent: c*k*r*s <= len(wt)
-    const int64_t a_in = len_in / hw;     // in extent: x*c <= a_in
+    // in extent: x*c <= a_in; clamped where every quotient saturates anyway
+    const int32_t a_in = clamp_div(len_in, hw);
     const int32_t q_in = -hw + (coh + cr - 2) * cw + (cow + cs - 2);
     const int64_t alim = len_in - q_in;   // UB iff x*c*h*w >= alim
-    const int64_t b_in = alim > 0 ? (alim - 1) / hw : -1;
+    const int32_t b_in = alim > 0 ? clamp_div(alim - 1, hw) : -1;
+    const bool full = lo == p0 && hi == p0 + nI2;
     const uint32_t out_fail = s_gt[div_cap(len_out, ext_out, r_out)];
     const int dmax = ts.dirty_max[p_out];
     const uint32_t dirty_fail = ~s_gt[dmax < 0 ? 0 : div_cap(dmax, ext_out, r_out)];
@@ -358,21 +385,24 @@ __global__ void __launch_bounds__(256) k_screen_conv_planes(TestsetView ts, cons
 #pragma unroll
     for (int q = 2; q < NS; ++q) key += (uint32_t)digit[q] * (uint32_t)plan.key_stride[q];
     for (int j = 0; j < nI; ++j) {  // digit 1: tc_c
-      const uint64_t g0 = p0 + (uint64_t)j * nI;
-      if (g0 + nI <= begin || g0 >= end) continue;
-      const int v_lo = g0 < begin ? (int)(begin - g0) : 0;
-      const int v_hi = g0 + nI > end ? (int)(end - g0) : nI;
-      const uint32_t range = (v_hi >= 32 ? 0xFFFFFFFFu : ((1u << v_hi) - 1u)) & ~((1u << v_lo) - 1u);
+      uint32_t range = all_rows;
+      if (!full) {
+        const uint64_t g0 = p0 + (uint64_t)j * nI;
+        if (g0 + nI <= begin || g0 >= end) continue;
+        const int v_lo = g0 < begin ? (int)(begin - g0) : 0;
+        const int v_hi = g0 + nI > end ? (int)(end - g0) : nI;
+        range = (v_hi >= 32 ? 0xFFFFFFFFu : ((1u << v_hi) - 1u)) & ~((1u << v_lo) - 1u);
+      }
       const int32_t c = s_u[j];
       if (c < 1 || c > c_max) {
         cnt2 += __popc(range);
         continue;
       }
       const float rc = s_rcp[j];
-      const uint32_t dm = range & (~gt0 | out_fail | s_gt[div_cap(a_in, c, rc)]);
+      const uint32_t dm = range & (~gt0 | out_fail | s_gt[div_small(a_in, c, rc)]);
       uint32_t ok = range & ~dm, um = 0, mm = 0;
       if (ok) {
-        um = b_in < 0 ? ok : (ok & s_gt[div_cap(b_in, c, rc)]);
+        um = b_in < 0 ? ok : (ok & s_gt[div_small(b_in, c, rc)]);
         ok &= ~um;
         if (ok) {
           const bool tab_fail = __ldg(plan.pt.table + key + (uint32_t)j * ks1) == 1;
@@ -386,7 +416,7 @@ __global__ void __launch_bounds__(256) k_screen_conv_planes(TestsetView ts, cons
       if (ok) {
         unsigned long long slot = atomicAdd(surv_cnt, (unsigned long long)__popc(ok));
         for (; ok; ok &= ok - 1, ++slot)
-          if (slot < surv_cap) surv[slot] = g0 + (__ffs(ok) - 1) - begin;
+          if (slot < surv_cap) surv[slot] = p0 + (uint64_t)j * nI + (__ffs(ok) - 1) - begin;
       }
     }
   }
