@@ -25,6 +25,7 @@ __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, 
 __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
                               uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                               unsigned long long* reason_hist);
+__global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need);
 __global__ void k_screen_conv_planes(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
                                    uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
                                    unsigned long long* surv_cnt, unsigned long long* reason_hist);
@@ -735,6 +736,17 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
       plan.key_stride[pt.q[k]] += mul;
       mul *= (uint64_t)ts->nI;
     }
+  }
+  if (use_rows && sp.sem == ATC_SEM_GEMM) {  // written-set check by lookup (k_gemm_need)
+    const unsigned cells = (unsigned)(ts->nP * ts->nI * ts->nI);
+    int32_t* need = (int32_t*)atc_ctx_scratch(ctx, 21, (size_t)cells * 4 + 16);
+    if (!need) {
+      atc_set_error(ctx, "scratch allocation failed (gemm_need)");
+      return ATC_ERR_CUDA;
+    }
+    k_gemm_need<<<cells, 128, 0, st>>>(ts->view, sp.layout == ATC_LAYOUT_ROW ? 1 : 0, need);
+    plan.gemm_need = need;
+    if (ctx->prof) ctx->prof_kernels += 1;
   }
   if (use_table) {
     uint8_t* tab = (uint8_t*)atc_ctx_scratch(ctx, 17, table_bytes + 16);

@@ -80,6 +80,10 @@ struct RowPlan {
   int32_t role_q[ATC_SZ_COUNT];        // per role: size-param index (fallbacks resolved), -1 absent
   Pos0Table pt;
   uint64_t key_stride[ATC_MAX_SIZES];  // table-key contribution of each size-param digit
+  // gemm: the written-set check as one lookup — need[(p*nI + ldc digit)*nI + m digit]
+  // = the smallest n writing every dirty position of region p at t = 0 (k_gemm_need;
+  // INT32_MAX: none does, -1: not tabulated, use the dirty list)
+  const int32_t* gemm_need;
 };
 
 enum : int32_t { kUndecided = -2 };

@@ -207,6 +207,46 @@ __global__ void __launch_bounds__(256) k_screen(TestsetView ts, SpecView sp, Bin
 // access bounds, the dirty-set (write-set) check, one table lookup.  Bindings
 // that pass all of it go to K2, which re-checks every test completely.
 
+// Written-set table for the gemm screen (RowPlan::gemm_need).  For a region p,
+// an ldc value L and an m value, position q of the dirty list is written by a
+// binding iff n >= n_min(q) (gemm_written is monotone in n):
+//   row-major: i = min(q / L, m - 1),  n_min = q - i*L + 1
+//   col-major: hi = min(q, m - 1), r = q % L; never if r > hi, else
+//              i = r + L*((hi - r) / L),  n_min = (q - i)/L + 1
+// need = max over the dirty list.  One CTA per (p, L digit, m digit).
+__global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need) {
+  const int nI = ts.nI;
+  const int e = blockIdx.x;
+  const int dm = e % nI, dl = (e / nI) % nI, p = e / (nI * nI);
+  const int64_t m = ts.ints[dm], L = ts.ints[dl];  // t = 0 values
+  __shared__ int32_t s_max;
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
+  if (m < 1 || L < 1) {
+    if (threadIdx.x == 0) need[e] = -1;
+    return;
+  }
+  const int32_t* dirty = ts.dirty_pos + ts.dirty_off[p];
+  const int cnt = ts.dirty_cnt[p];
+  int32_t local = 0;
+  for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+    const int64_t q = dirty[k];
+    int64_t nmin;
+    if (row_major) {
+      const int64_t i = min(q / L, m - 1);
+      nmin = q - i * L + 1;
+    } else {
+      const int64_t hi = min(q, m - 1), r = q % L;
+      nmin = r > hi ? (int64_t)INT32_MAX : (q - (r + L * ((hi - r) / L))) / L + 1;
+    }
+    local = max(local, (int32_t)(nmin < INT32_MAX ? nmin : INT32_MAX));
+  }
+  for (int o = 16; o > 0; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&s_max, local);
+  __syncthreads();
+  if (threadIdx.x == 0) need[e] = s_max;
+}
+
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out) {
   const uint64_t total = (uint64_t)n_perms * pt.per_perm;

@@ -32,6 +32,15 @@ __device__ __forceinline__ int64_t pick(const int64_t (&u)[NS], int q) {
   return v;
 }
 
+template <int NS>
+__device__ __forceinline__ int pick_digit(const int (&d)[NS], int q) {
+  int v = 0;
+#pragma unroll
+  for (int i = 1; i < NS; ++i)
+    if (q == i) v = d[i];
+  return v;
+}
+
 // Q0MASK: compile-time set of roles bound to digit 0 (bit per ATC_SZ_* role), so
 // that every quantity not depending on digit 0 is loop-invariant and hoisted by
 // the compiler; kQ0Dynamic takes the set from the plan at run time.
@@ -186,11 +195,22 @@ __global__ void __launch_bounds__(256) k_screen_rows(TestsetView ts, SpecView sp
             if (m < 1 || n < 1) {
               if (ndirty) r = ATC_FAIL_MISMATCH;
             } else {
-              for (int e = 0; e < ndirty; ++e)
-                if (!gemm_written(row_major, __ldg(dirty + e), (int)m, (int)n, (int)ldc)) {
-                  r = ATC_FAIL_MISMATCH;
-                  break;
-                }
+              int need = -1;
+              if (plan.gemm_need) {  // digits of m and ldc -> tabulated minimum n
+                const int qm = plan.role_q[ATC_SZ_M], ql = plan.role_q[ATC_SZ_LDC];
+                const int dm = qm == 0 ? v : pick_digit<NS>(digit, qm);
+                const int dl = ql == 0 ? v : pick_digit<NS>(digit, ql);
+                need = __ldg(plan.gemm_need + ((size_t)pC * nI + dl) * nI + dm);
+              }
+              if (need >= 0) {
+                if ((int64_t)n < need) r = ATC_FAIL_MISMATCH;
+              } else {
+                for (int e = 0; e < ndirty; ++e)
+                  if (!gemm_written(row_major, __ldg(dirty + e), (int)m, (int)n, (int)ldc)) {
+                    r = ATC_FAIL_MISMATCH;
+                    break;
+                  }
+              }
               if (!r) tv = row_tab >= 0 ? row_tab : __ldg(plan.pt.table + key_rest + (uint64_t)v * key0);
             }
           }

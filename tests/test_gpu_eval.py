@@ -236,3 +236,32 @@ def test_enumerated_conv_matches_explicit(ev, stem, variant):
         assert n == len(want)
         assert hist.tolist() == np.bincount(got.reason, minlength=5).tolist(), (stem, variant, b, e)
         print(stem, variant, b, e, hist.tolist())
+
+
+GEMM_VARIANTS = {
+    "recorded": lambda ts: ts,
+    "int1_is_1": lambda ts: _with_int(ts, 1, 1),
+    "int0_is_2": lambda ts: _with_int(ts, 0, 2),
+    "int2_is_0": lambda ts: _with_int(ts, 2, 0),
+    "c_300": lambda ts: _shrunk(ts, [None, None, 300, None]),
+}
+
+
+@pytest.mark.parametrize("variant", sorted(GEMM_VARIANTS))
+@pytest.mark.parametrize("stem", ["naive_ld", "kernel_dot", "blocked_copy_local", "naive_colmajor", "strassen_staged"])
+def test_enumerated_gemm_matches_explicit(ev, stem, variant):
+    """The enumerated gemm screen (k_screen_rows with the k_gemm_need written-set
+    lookup) agrees with the explicit per-binding path on whole spaces, with test
+    sets whose t = 0 sizes make partial, overlapping (ldc < n) and empty writes."""
+    p = fixtures.load(stem)
+    for sname in p.spec_names():
+        space = p.space(sname)
+        spec = fixtures.spec(sname)
+        ts = GEMM_VARIANTS[variant](p.testsets(16))
+        passing, n, hist = ev.eval_enumerated(spec, ts, space, 0, space.count)
+        idx = np.arange(space.count, dtype=np.uint64)
+        got = ev.eval_bindings(spec, ts, *space.decode(idx))
+        want = idx[got.reason == 0]
+        np.testing.assert_array_equal(passing, want, err_msg=f"{stem}/{sname}/{variant}")
+        assert n == len(want)
+        assert hist.tolist() == np.bincount(got.reason, minlength=5).tolist(), (stem, sname, variant)
