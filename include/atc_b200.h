@@ -163,6 +163,26 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
                         int32_t mode, uint64_t* survivors, int64_t cap, int64_t* n_survivors,
                         int64_t* reason_counts);
 
+/* Many enumerated spaces in one stream pass (a corpus sweep: every function x
+ * spec the pipeline would try).  No reference counterpart — it batches what
+ * pipeline.cpp:248-310 does one spec at a time; each job's outputs equal
+ * atc_eval_enumerated on that job alone.  All jobs' kernels are queued back to
+ * back and the results come back in one copy; a job whose survivors or passing
+ * list overflow the batched buffers is re-run through atc_eval_enumerated. */
+typedef struct atc_enum_job {
+  const atc_spec_desc* spec;
+  const atc_testset_handle* ts;
+  const uint8_t* perms;
+  int32_t n_perms;
+  uint64_t begin, end;
+  uint64_t* survivors; /* out: ascending passing indices, at most cap */
+  int64_t cap;
+  int64_t n_survivors;                      /* out */
+  int64_t reason_counts[ATC_REASON_COUNT];  /* out */
+  int32_t status;                           /* out: ATC_OK or the job's error */
+} atc_enum_job;
+int atc_eval_enumerated_many(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, int32_t mode);
+
 /* FP64 reference semantics on the GPU (equivalence::run_reference).  sizes[q] per
  * spec size param; buffers[a] (host, length buffer_len[a]) per spec array;
  * non-LiveIn arrays are rewritten in place. */

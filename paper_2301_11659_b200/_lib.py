@@ -83,6 +83,24 @@ class Profile(C.Structure):
     ]
 
 
+class EnumJob(C.Structure):
+    """atc_enum_job (include/atc_b200.h)."""
+
+    _fields_ = [
+        ("spec", C.c_void_p),
+        ("ts", C.c_void_p),
+        ("perms", C.c_void_p),
+        ("n_perms", C.c_int32),
+        ("begin", C.c_uint64),
+        ("end", C.c_uint64),
+        ("survivors", C.c_void_p),
+        ("cap", C.c_int64),
+        ("n_survivors", C.c_int64),
+        ("reason_counts", C.c_int64 * 5),
+        ("status", C.c_int32),
+    ]
+
+
 # (name, restype, argtypes) for every function declared in include/atc_b200.h
 _P = C.c_void_p
 _SIGS = [
@@ -100,6 +118,7 @@ _SIGS = [
     ("atc_eval_bindings_device", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, C.c_int64, C.c_int32, _P, _P, _P]),
     ("atc_eval_enumerated", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, C.c_int32, C.c_uint64, C.c_uint64, C.c_int32,
                                       _P, C.c_int64, C.POINTER(C.c_int64), _P]),
+    ("atc_eval_enumerated_many", C.c_int, [_P, C.POINTER(EnumJob), C.c_int32, C.c_int32]),
     ("atc_run_reference", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P]),
     ("atc_dispatch", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, _P]),
     ("atc_sgemm_rm", C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int32]),

@@ -44,7 +44,8 @@ __global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* sur
 __global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason);
 __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v);
 __global__ void k_finalize(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
-                           const int32_t* surv_keys, uint64_t base, uint64_t* res, unsigned long long* hist);
+                           const int32_t* surv_keys, uint64_t base, uint64_t* res, uint64_t res_cap,
+                           unsigned long long* hist);
 constexpr uint64_t kResultPrefix = 4096;  // passing indices returned with the first D2H
 }  // namespace atc
 
@@ -651,12 +652,24 @@ int atc_eval_bindings(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset
   return ATC_OK;
 }
 
-int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_handle* ts,
-                        const uint8_t* perms, int32_t n_perms, uint64_t begin, uint64_t end, int32_t mode,
-                        uint64_t* survivors, int64_t cap, int64_t* n_survivors, int64_t* reason_counts) {
-  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+}  // extern "C"
+
+namespace {
+
+// ---- enumerated spaces --------------------------------------------------------
+// Per-space plan: the decode, the position-0 table shape and the row plan.
+struct EnumPlan {
   SpecView sp;
-  if (!build_spec_view(ctx, spec, sp)) return ATC_ERR_ARG;
+  Pos0Table pt;
+  RowPlan plan;
+  bool use_table = false, use_rows = false;
+  uint64_t size_maps = 1, table_bytes = 0;
+};
+
+int plan_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_handle* ts, const uint8_t* perms,
+                    int32_t n_perms, uint64_t begin, uint64_t end, int32_t mode, EnumPlan& e) {
+  if (!build_spec_view(ctx, spec, e.sp)) return ATC_ERR_ARG;
+  const SpecView& sp = e.sp;
   if (!ts || n_perms < 0 || !perms || end < begin || (mode != ATC_MODE_FP64 && mode != ATC_MODE_FP32_SCREEN)) {
     atc_set_error(ctx, "bad arguments to atc_eval_enumerated");
     return ATC_ERR_ARG;
@@ -667,31 +680,17 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
         atc_set_error(ctx, "perm %d maps array %d to pointer %d of %d", p, a, perms[p * sp.nA + a], ts->nP);
         return ATC_ERR_ARG;
       }
-  uint64_t size_maps = 1;
-  for (int q = 0; q < sp.nS; ++q) size_maps *= (uint64_t)ts->nI;
-  if (end > (uint64_t)n_perms * size_maps) {
+  e.size_maps = 1;
+  for (int q = 0; q < sp.nS; ++q) e.size_maps *= (uint64_t)ts->nI;
+  if (end > (uint64_t)n_perms * e.size_maps) {
     atc_set_error(ctx, "range end %llu beyond the space (%llu)", (unsigned long long)end,
-                  (unsigned long long)((uint64_t)n_perms * size_maps));
+                  (unsigned long long)((uint64_t)n_perms * e.size_maps));
     return ATC_ERR_ARG;
   }
-  cudaSetDevice(ctx->device);
-  cudaStream_t st = ctx->stream;
-  ctx->mode = mode;
-  const uint64_t chunk_cap = 1ull << 22;  // survivors per chunk
-  uint8_t* d_perms = (uint8_t*)atc_ctx_scratch(ctx, 6, (size_t)n_perms * sp.nA + 16);
-  uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
-  int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, chunk_cap * 4);
-  unsigned long long* cnt = (unsigned long long*)atc_ctx_scratch(ctx, 3, 64);
-  unsigned long long* hist = (unsigned long long*)atc_ctx_scratch(ctx, 7, 64);
-  if (!d_perms || !surv || !skeys || !cnt || !hist) {
-    atc_set_error(ctx, "scratch allocation failed");
-    return ATC_ERR_CUDA;
-  }
-  cudaMemcpyAsync(d_perms, perms, (size_t)n_perms * sp.nA, cudaMemcpyHostToDevice, st);
-  cudaMemsetAsync(hist, 0, 64, st);
   // position-0 table (k_pos0_table): roles the first output element depends on
-  Pos0Table pt{};
-  bool use_table = true;
+  Pos0Table& pt = e.pt;
+  pt = Pos0Table{};
+  e.use_table = true;
   if (sp.sem == ATC_SEM_GEMM) {
     const bool row = sp.layout == ATC_LAYOUT_ROW;
     const int ld = row ? (sp.role_size[ATC_SZ_LDB] >= 0 ? sp.role_size[ATC_SZ_LDB] : sp.role_size[ATC_SZ_N])
@@ -706,20 +705,21 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
   }
   pt.per_perm = 1;
   for (int r = 0; r < pt.R; ++r) {
-    if (pt.q[r] < 0) use_table = false;
+    if (pt.q[r] < 0) e.use_table = false;
     pt.per_perm *= (uint64_t)ts->nI;
   }
-  const uint64_t table_bytes = pt.per_perm * (uint64_t)n_perms;
-  if (table_bytes > (256ull << 20)) use_table = false;
+  e.table_bytes = pt.per_perm * (uint64_t)n_perms;
+  if (e.table_bytes > (256ull << 20)) e.use_table = false;
   // row-hoisted screen (k_screen_rows) for the bundled spec shapes
-  RowPlan plan{};
-  bool use_rows = use_table && ((sp.sem == ATC_SEM_GEMM && (sp.nS == 3 || sp.nS == 6)) ||
-                                (sp.sem == ATC_SEM_CONV2D && sp.nS == 9));
-  if (use_rows) {
+  RowPlan& plan = e.plan;
+  plan = RowPlan{};
+  e.use_rows = e.use_table && ((sp.sem == ATC_SEM_GEMM && (sp.nS == 3 || sp.nS == 6)) ||
+                               (sp.sem == ATC_SEM_CONV2D && sp.nS == 9));
+  if (e.use_rows) {
     for (int a = 0; a < sp.nA; ++a) {
       plan.dim_mask[a] = 0;
       for (int d = 0; d < sp.ndims[a]; ++d) {
-        if (plan.dim_mask[a] & (1u << sp.dims[a][d])) use_rows = false;  // repeated dim: not expressible
+        if (plan.dim_mask[a] & (1u << sp.dims[a][d])) e.use_rows = false;  // repeated dim: not expressible
         plan.dim_mask[a] |= 1u << sp.dims[a][d];
       }
     }
@@ -737,7 +737,22 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
       mul *= (uint64_t)ts->nI;
     }
   }
-  if (use_rows && sp.sem == ATC_SEM_GEMM) {  // written-set check by lookup (k_gemm_need)
+  return ATC_OK;
+}
+
+// Uploads the permutations and builds the per-space tables (k_gemm_need,
+// k_pos0_table) on the stream; scratch slots 6/17/21 are reused in stream order.
+int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, const uint8_t* perms, int32_t n_perms,
+                   uint8_t** d_perms_out, cudaStream_t st) {
+  const SpecView& sp = e.sp;
+  uint8_t* d_perms = (uint8_t*)atc_ctx_scratch(ctx, 6, (size_t)n_perms * sp.nA + 16);
+  if (!d_perms) {
+    atc_set_error(ctx, "scratch allocation failed");
+    return ATC_ERR_CUDA;
+  }
+  cudaMemcpyAsync(d_perms, perms, (size_t)n_perms * sp.nA, cudaMemcpyHostToDevice, st);
+  *d_perms_out = d_perms;
+  if (e.use_rows && sp.sem == ATC_SEM_GEMM) {  // written-set check by lookup (k_gemm_need)
     const unsigned cells = (unsigned)(ts->nP * ts->nI * ts->nI);
     int32_t* need = (int32_t*)atc_ctx_scratch(ctx, 21, (size_t)cells * 4 + 16);
     if (!need) {
@@ -745,21 +760,53 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
       return ATC_ERR_CUDA;
     }
     k_gemm_need<<<cells, 128, 0, st>>>(ts->view, sp.layout == ATC_LAYOUT_ROW ? 1 : 0, need);
-    plan.gemm_need = need;
+    e.plan.gemm_need = need;
     if (ctx->prof) ctx->prof_kernels += 1;
   }
-  if (use_table) {
-    uint8_t* tab = (uint8_t*)atc_ctx_scratch(ctx, 17, table_bytes + 16);
+  if (e.use_table) {
+    uint8_t* tab = (uint8_t*)atc_ctx_scratch(ctx, 17, e.table_bytes + 16);
     if (!tab) {
       atc_set_error(ctx, "scratch allocation failed (table)");
       return ATC_ERR_CUDA;
     }
-    pt.table = tab;
-    plan.pt = pt;
-    k_pos0_table<<<(unsigned)std::min<uint64_t>((table_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16), 256, 0,
-                   st>>>(ts->view, sp, d_perms, n_perms, pt, tab);
+    e.pt.table = tab;
+    e.plan.pt = e.pt;
+    k_pos0_table<<<(unsigned)std::min<uint64_t>((e.table_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16), 256, 0,
+                   st>>>(ts->view, sp, d_perms, n_perms, e.pt, tab);
     if (ctx->prof) ctx->prof_kernels += 1;
   }
+  return ATC_OK;
+}
+
+constexpr uint64_t kEnumChunkCap = 1ull << 22;  // survivors per K1 launch
+
+}  // namespace
+
+extern "C" {
+
+int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_handle* ts,
+                        const uint8_t* perms, int32_t n_perms, uint64_t begin, uint64_t end, int32_t mode,
+                        uint64_t* survivors, int64_t cap, int64_t* n_survivors, int64_t* reason_counts) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  EnumPlan e;
+  int rc = plan_enumerated(ctx, spec, ts, perms, n_perms, begin, end, mode, e);
+  if (rc) return rc;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  ctx->mode = mode;
+  const uint64_t chunk_cap = kEnumChunkCap;
+  uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
+  int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, chunk_cap * 4);
+  unsigned long long* cnt = (unsigned long long*)atc_ctx_scratch(ctx, 3, 64);
+  unsigned long long* hist = (unsigned long long*)atc_ctx_scratch(ctx, 7, 64);
+  if (!surv || !skeys || !cnt || !hist) {
+    atc_set_error(ctx, "scratch allocation failed");
+    return ATC_ERR_CUDA;
+  }
+  cudaMemsetAsync(hist, 0, 64, st);
+  uint8_t* d_perms = nullptr;
+  rc = enqueue_tables(ctx, e, ts, perms, n_perms, &d_perms, st);
+  if (rc) return rc;
   // result block on the device: [0] survivor count (copied from cnt), [1] passing
   // count, [2..2+cap) passing global indices; reasons accumulate in `hist`
   uint64_t* res = (uint64_t*)atc_ctx_scratch(ctx, 20, (chunk_cap + 2) * 8);
@@ -773,15 +820,16 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
   uint64_t chunk = 1ull << 34;  // one chunk covers every corpus space
   for (uint64_t lo = begin; lo < end;) {
     const uint64_t hi = std::min(end, lo + chunk);
-    BindingSource src{nullptr, nullptr, d_perms, size_maps, lo, 1};
-    int rc = run_eval(ctx, sp, ts, src, hi - lo, nullptr, surv, chunk_cap, cnt, skeys, hist, st,
-                      use_table ? &pt : nullptr, use_rows ? &plan : nullptr);
+    BindingSource src{nullptr, nullptr, d_perms, e.size_maps, lo, 1};
+    rc = run_eval(ctx, e.sp, ts, src, hi - lo, nullptr, surv, chunk_cap, cnt, skeys, hist, st,
+                  e.use_table ? &e.pt : nullptr, e.use_rows ? &e.plan : nullptr);
     if (rc) return rc;
     // K2 outcomes -> passing list + reason histogram, on the device (one sync per chunk)
     cudaMemsetAsync(res + 1, 0, 8, st);
-    k_finalize<<<64, 256, 0, st>>>(surv, cnt, chunk_cap, skeys, lo, res, hist);
+    k_finalize<<<64, 256, 0, st>>>(surv, cnt, chunk_cap, skeys, lo, res, chunk_cap, hist);
     if (ctx->prof) ctx->prof_kernels += 1;
-    const uint64_t pre = std::min<uint64_t>(kResultPrefix, cap > 0 ? (uint64_t)cap : 0);
+    // the passing list is unordered on the device: the smallest `cap` need all of it
+    const uint64_t pre = cap > 0 ? kResultPrefix : 0;
     if (!atc_cuda_ok(ctx, cudaMemcpyAsync(h_res, res, (2 + pre) * 8, cudaMemcpyDeviceToHost, st), "D2H result") ||
         !atc_cuda_ok(ctx, cudaMemcpyAsync(h_res + 2 + kResultPrefix, hist, ATC_REASON_COUNT * 8,
                                           cudaMemcpyDeviceToHost, st), "D2H hist") ||
@@ -801,7 +849,7 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
       continue;
     }
     if (ctx->prof) ctx->prof_survivors += (long long)c;
-    const uint64_t want = std::min<uint64_t>(npass, cap > 0 ? (uint64_t)cap : 0);
+    const uint64_t want = cap > 0 ? npass : 0;
     std::vector<uint64_t> chunk_pass(h_res + 2, h_res + 2 + std::min(want, pre));
     if (want > pre) {  // rare: more passing bindings than the pinned prefix
       chunk_pass.resize(want);
@@ -820,8 +868,87 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
   if (n_survivors) *n_survivors = passed;
   if (reason_counts) {
     const uint64_t* h_hist = h_res + 2 + kResultPrefix;
-    for (int r = 0; r < ATC_REASON_COUNT; ++r) reason_counts[r] = (int64_t)h_hist[r];
+    for (int r = 0; r < ATC_REASON_COUNT; ++r) reason_counts[r] = end > begin ? (int64_t)h_hist[r] : 0;
     reason_counts[ATC_PASS] = passed;
+  }
+  return ATC_OK;
+}
+
+int atc_eval_enumerated_many(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, int32_t mode) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs)) {
+    atc_set_error(ctx, "bad arguments to atc_eval_enumerated_many");
+    return ATC_ERR_ARG;
+  }
+  if (n_jobs == 0) return ATC_OK;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  ctx->mode = mode;
+  const uint64_t chunk_cap = kEnumChunkCap;
+  const uint64_t stride = 2 + kResultPrefix;  // per-job result block: count, passing count, passing prefix
+  uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
+  int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, chunk_cap * 4);
+  unsigned long long* cnt = (unsigned long long*)atc_ctx_scratch(ctx, 3, 64);
+  uint64_t* res = (uint64_t*)atc_ctx_scratch(ctx, 22, (size_t)n_jobs * (stride + 8) * 8);
+  uint64_t* h_res = (uint64_t*)atc_ctx_pinned(ctx, 1, (size_t)n_jobs * (stride + 8) * 8);
+  if (!surv || !skeys || !cnt || !res || !h_res) {
+    atc_set_error(ctx, "scratch allocation failed");
+    return ATC_ERR_CUDA;
+  }
+  // job j: result block res + j*stride; histogram hist + 8*j after all blocks
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(res + (size_t)n_jobs * stride);
+  cudaMemsetAsync(res, 0, (size_t)n_jobs * (stride + 8) * 8, st);
+  std::vector<char> batched(n_jobs, 0);
+  for (int j = 0; j < n_jobs; ++j) {
+    atc_enum_job& job = jobs[j];
+    job.status = ATC_OK;
+    job.n_survivors = 0;
+    for (int r = 0; r < ATC_REASON_COUNT; ++r) job.reason_counts[r] = 0;
+    EnumPlan e;
+    int rc = plan_enumerated(ctx, job.spec, job.ts, job.perms, job.n_perms, job.begin, job.end, mode, e);
+    if (rc) {
+      job.status = rc;
+      continue;
+    }
+    if (job.end - job.begin > (1ull << 34)) continue;  // chunked: single-space path below
+    uint8_t* d_perms = nullptr;
+    rc = enqueue_tables(ctx, e, job.ts, job.perms, job.n_perms, &d_perms, st);
+    if (rc) return rc;
+    uint64_t* rj = res + (size_t)j * stride;
+    if (job.end > job.begin) {
+      BindingSource src{nullptr, nullptr, d_perms, e.size_maps, job.begin, 1};
+      rc = run_eval(ctx, e.sp, job.ts, src, job.end - job.begin, nullptr, surv, chunk_cap, cnt, skeys, hist + 8 * j,
+                    st, e.use_table ? &e.pt : nullptr, e.use_rows ? &e.plan : nullptr);
+      if (rc) return rc;
+      k_finalize<<<64, 256, 0, st>>>(surv, cnt, chunk_cap, skeys, job.begin, rj, kResultPrefix, hist + 8 * j);
+      if (ctx->prof) ctx->prof_kernels += 1;
+    }
+    batched[j] = 1;
+  }
+  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(h_res, res, (size_t)n_jobs * (stride + 8) * 8, cudaMemcpyDeviceToHost, st),
+                   "D2H results") ||
+      !atc_cuda_ok(ctx, cudaStreamSynchronize(st), "enumerate-many sync"))
+    return ATC_ERR_CUDA;
+  const uint64_t* h_hist = h_res + (size_t)n_jobs * stride;
+  for (int j = 0; j < n_jobs; ++j) {
+    atc_enum_job& job = jobs[j];
+    if (job.status != ATC_OK) continue;
+    const uint64_t* rj = h_res + (size_t)j * stride;
+    const uint64_t c = rj[0], npass = rj[1];
+    if (!batched[j] || c > chunk_cap || npass > kResultPrefix) {
+      // overflow (or a very large range): the single-space path with its own chunking
+      job.status = atc_eval_enumerated(ctx, job.spec, job.ts, job.perms, job.n_perms, job.begin, job.end, mode,
+                                       job.survivors, job.cap, &job.n_survivors, job.reason_counts);
+      continue;
+    }
+    if (ctx->prof) ctx->prof_survivors += (long long)c;
+    std::vector<uint64_t> pass(rj + 2, rj + 2 + npass);
+    std::sort(pass.begin(), pass.end());
+    for (size_t i = 0; i < pass.size() && (int64_t)i < job.cap; ++i)
+      if (job.survivors) job.survivors[i] = pass[i];
+    job.n_survivors = (int64_t)npass;
+    for (int r = 0; r < ATC_REASON_COUNT; ++r) job.reason_counts[r] = (int64_t)h_hist[8 * j + r];
+    job.reason_counts[ATC_PASS] = (int64_t)npass;
   }
   return ATC_OK;
 }

@@ -710,18 +710,33 @@ namespace atc {
 // Enumerated spaces: fold the K2 outcome of every survivor into the passing list
 // (global indices) and the reason histogram, so the host reads one small block.
 __global__ void k_finalize(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
-                           const int32_t* surv_keys, uint64_t base, uint64_t* res, unsigned long long* hist) {
+                           const int32_t* surv_keys, uint64_t base, uint64_t* res, uint64_t res_cap,
+                           unsigned long long* hist) {
+  __shared__ unsigned int s_hist[ATC_REASON_COUNT];
+  if (threadIdx.x < ATC_REASON_COUNT) s_hist[threadIdx.x] = 0;
+  __syncthreads();
   unsigned long long cnt = *surv_cnt;
   if (blockIdx.x == 0 && threadIdx.x == 0) res[0] = cnt;
   if (cnt > cap) return;  // overflow: the host retries with smaller chunks
+  unsigned int local[ATC_REASON_COUNT] = {0, 0, 0, 0, 0};
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
     const int32_t k = surv_keys[i];
     if (k == kPassKey) {
       const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(res + 1), 1ull);
-      res[2 + slot] = base + surv[i];
+      if (slot < res_cap) res[2 + slot] = base + surv[i];
     } else {
-      atomicAdd(&hist[k & 7], 1ull);
+#pragma unroll
+      for (int r = 1; r < ATC_REASON_COUNT; ++r) local[r] += (k & 7) == r;
     }
   }
+#pragma unroll
+  for (int r = 1; r < ATC_REASON_COUNT; ++r) {
+    unsigned int v = local[r];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_hist[r], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < ATC_REASON_COUNT && s_hist[threadIdx.x])
+    atomicAdd(&hist[threadIdx.x], (unsigned long long)s_hist[threadIdx.x]);
 }
 }  // namespace atc

@@ -272,6 +272,36 @@ class Evaluator:
         n = int(nsurv.value)
         return surv[:min(n, cap)].copy(), n, hist
 
+    def eval_enumerated_many(self, items: list, cap: int = 1 << 16, mode: int = _lib.MODE_FP64) -> list:
+        """eval_enumerated for many (spec, ts, space, begin, end) at once
+        (atc_eval_enumerated_many: one stream pass, one result copy)."""
+        n = len(items)
+        jobs = (_lib.EnumJob * max(n, 1))()
+        keep = []
+        for j, (spec, ts, space, begin, end) in enumerate(items):
+            h = ts.upload(self.ctx)
+            desc = spec.to_desc()
+            perms = np.ascontiguousarray(space.perms, dtype=np.uint8)
+            surv = np.zeros(max(cap, 1), dtype=np.uint64)
+            keep.append((desc, perms, surv))
+            jb = jobs[j]
+            jb.spec = C.cast(C.pointer(desc), C.c_void_p)
+            jb.ts = h.value
+            jb.perms = perms.ctypes.data
+            jb.n_perms = int(perms.shape[0])
+            jb.begin, jb.end = int(begin), int(space.count if end is None else end)
+            jb.survivors = surv.ctypes.data
+            jb.cap = cap
+        _lib.check(self.ctx.handle, _lib.lib().atc_eval_enumerated_many(self.ctx.handle, jobs, n, mode))
+        out = []
+        for j in range(n):
+            jb = jobs[j]
+            if jb.status != _lib.ATC_OK:
+                raise _lib.AtcError(jb.status, f"job {j}: atc error {jb.status}")
+            k = int(jb.n_survivors)
+            out.append((keep[j][2][:min(k, cap)].copy(), k, np.array(list(jb.reason_counts), dtype=np.int64)))
+        return out
+
 
 @dataclass
 class VerifyResult:

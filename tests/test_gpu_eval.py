@@ -265,3 +265,23 @@ def test_enumerated_gemm_matches_explicit(ev, stem, variant):
         np.testing.assert_array_equal(passing, want, err_msg=f"{stem}/{sname}/{variant}")
         assert n == len(want)
         assert hist.tolist() == np.bincount(got.reason, minlength=5).tolist(), (stem, sname, variant)
+
+
+def test_enumerated_many_matches_single(ev):
+    """atc_eval_enumerated_many (all corpus spaces in one stream pass) returns per
+    job exactly what atc_eval_enumerated returns for that job alone, including
+    partial ranges, an empty range and a job with more passing bindings than cap."""
+    from paper_2301_11659_b200 import workloads
+
+    jobs = workloads.corpus_jobs()
+    items = [(j.spec, j.ts, j.space, 0, j.count) for j in jobs]
+    j0 = next(j for j in jobs if j.stem == "conv_direct")
+    items += [(j0.spec, j0.ts, j0.space, 381367040, 381367049), (j0.spec, j0.ts, j0.space, 5, 5)]
+    g = next(j for j in jobs if j.stem == "naive_rowmajor" and j.spec_name == "gemm_rowmajor")
+    ts64 = fixtures.load("naive_rowmajor").testsets(16, variant="testsets64")
+    items.append((g.spec, ts64, g.space, 0, g.count))  # 27 passing bindings, cap 8 below
+    many = ev.eval_enumerated_many(items, cap=8)
+    for (spec, ts, space, b, e), (pm, nm, hm) in zip(items, many):
+        ps, ns, hs = ev.eval_enumerated(spec, ts, space, b, e, cap=8)
+        np.testing.assert_array_equal(pm, ps)
+        assert nm == ns and hm.tolist() == hs.tolist()
