@@ -183,6 +183,16 @@ typedef struct atc_enum_job {
 } atc_enum_job;
 int atc_eval_enumerated_many(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, int32_t mode);
 
+/* The same sweep prepared once and run many times: create plans every job and
+ * keeps its permutations on the device (jobs[] and the test-set handles must
+ * outlive the batch); run evaluates every job and fills its outputs — eagerly on
+ * the first run (and while profiling), afterwards as one CUDA-graph launch.
+ * create returns NULL on error (atc_last_error). */
+typedef struct atc_enum_batch atc_enum_batch;
+atc_enum_batch* atc_enum_batch_create(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, int32_t mode);
+int atc_enum_batch_run(atc_ctx* ctx, atc_enum_batch* batch);
+void atc_enum_batch_destroy(atc_ctx* ctx, atc_enum_batch* batch);
+
 /* FP64 reference semantics on the GPU (equivalence::run_reference).  sizes[q] per
  * spec size param; buffers[a] (host, length buffer_len[a]) per spec array;
  * non-LiveIn arrays are rewritten in place. */

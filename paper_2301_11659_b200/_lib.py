@@ -119,6 +119,9 @@ _SIGS = [
     ("atc_eval_enumerated", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, C.c_int32, C.c_uint64, C.c_uint64, C.c_int32,
                                       _P, C.c_int64, C.POINTER(C.c_int64), _P]),
     ("atc_eval_enumerated_many", C.c_int, [_P, C.POINTER(EnumJob), C.c_int32, C.c_int32]),
+    ("atc_enum_batch_create", _P, [_P, C.POINTER(EnumJob), C.c_int32, C.c_int32]),
+    ("atc_enum_batch_run", C.c_int, [_P, _P]),
+    ("atc_enum_batch_destroy", None, [_P, _P]),
     ("atc_run_reference", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P]),
     ("atc_dispatch", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, _P]),
     ("atc_sgemm_rm", C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int32]),

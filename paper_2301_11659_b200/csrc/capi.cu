@@ -548,8 +548,7 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     cudaEventRecord(e1.second, st);
     ctx->prof_screen.push_back(e1);
   }
-  k_fill_i32<<<(unsigned)std::min<uint64_t>((surv_cap + 255) / 256, 1024), 256, 0, st>>>(surv_keys, (int64_t)surv_cap,
-                                                                                        kPassKey);
+  // (no key initialisation: K2a writes the key of every survivor it reads)
   if (ctx->prof) {
     e2 = ev_pair();
     cudaEventRecord(e2.first, st);
@@ -571,7 +570,7 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     ctx->prof_confirm.push_back(e2);
   }
   if (keys) k_merge_keys<<<64, 256, 0, st>>>(surv, surv_cnt, surv_cap, surv_keys, keys);
-  if (ctx->prof) ctx->prof_kernels += keys ? 5 : 4;  /* fill, K1, K2a, K2b (+ merge) */
+  if (ctx->prof) ctx->prof_kernels += keys ? 4 : 3;  /* K1, K2a, K2b (+ merge) */
   if (!atc_cuda_ok(ctx, cudaGetLastError(), "evaluator launch")) return ATC_ERR_CUDA;
   return ATC_OK;
 }
@@ -745,13 +744,16 @@ int plan_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_h
 int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, const uint8_t* perms, int32_t n_perms,
                    uint8_t** d_perms_out, cudaStream_t st) {
   const SpecView& sp = e.sp;
-  uint8_t* d_perms = (uint8_t*)atc_ctx_scratch(ctx, 6, (size_t)n_perms * sp.nA + 16);
+  uint8_t* d_perms = *d_perms_out;  // device-resident already (batches), else staged here
   if (!d_perms) {
-    atc_set_error(ctx, "scratch allocation failed");
-    return ATC_ERR_CUDA;
+    d_perms = (uint8_t*)atc_ctx_scratch(ctx, 6, (size_t)n_perms * sp.nA + 16);
+    if (!d_perms) {
+      atc_set_error(ctx, "scratch allocation failed");
+      return ATC_ERR_CUDA;
+    }
+    cudaMemcpyAsync(d_perms, perms, (size_t)n_perms * sp.nA, cudaMemcpyHostToDevice, st);
+    *d_perms_out = d_perms;
   }
-  cudaMemcpyAsync(d_perms, perms, (size_t)n_perms * sp.nA, cudaMemcpyHostToDevice, st);
-  *d_perms_out = d_perms;
   if (e.use_rows && sp.sem == ATC_SEM_GEMM) {  // written-set check by lookup (k_gemm_need)
     const unsigned cells = (unsigned)(ts->nP * ts->nI * ts->nI);
     int32_t* need = (int32_t*)atc_ctx_scratch(ctx, 21, (size_t)cells * 4 + 16);
@@ -874,70 +876,203 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
   return ATC_OK;
 }
 
-int atc_eval_enumerated_many(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, int32_t mode) {
-  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
-  if (n_jobs < 0 || (n_jobs > 0 && !jobs)) {
-    atc_set_error(ctx, "bad arguments to atc_eval_enumerated_many");
-    return ATC_ERR_ARG;
-  }
-  if (n_jobs == 0) return ATC_OK;
-  cudaSetDevice(ctx->device);
-  cudaStream_t st = ctx->stream;
-  ctx->mode = mode;
+}  // extern "C"
+
+// A prepared sweep (atc_enum_batch_*): per-job plans, device-resident
+// permutations, a result block per job; replayed as one CUDA graph after the
+// first (eager) run has sized every scratch buffer.
+struct atc_enum_batch {
+  atc_enum_job* jobs = nullptr;
+  int n = 0, mode = 0, runs = 0;
+  std::vector<EnumPlan> plans;
+  std::vector<uint8_t*> d_perms;
+  std::vector<char> batched;
+  uint64_t* res = nullptr;    // device: n blocks of kBatchStride, then n x 8 histogram words
+  uint64_t* h_res = nullptr;  // pinned mirror
+  cudaGraphExec_t exec = nullptr;
+  bool graph_failed = false;
+  bool transient = false;  // one-shot (atc_eval_enumerated_many): buffers borrowed from the context
+  uint8_t* perm_block = nullptr;  // owned permutation buffer (reusable batches)
+};
+
+namespace {
+
+constexpr uint64_t kBatchStride = 2 + kResultPrefix;  // count, passing count, passing prefix
+
+size_t batch_res_words(int n) { return (size_t)n * (kBatchStride + 8); }
+
+int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st) {
   const uint64_t chunk_cap = kEnumChunkCap;
-  const uint64_t stride = 2 + kResultPrefix;  // per-job result block: count, passing count, passing prefix
   uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
   int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, chunk_cap * 4);
   unsigned long long* cnt = (unsigned long long*)atc_ctx_scratch(ctx, 3, 64);
-  uint64_t* res = (uint64_t*)atc_ctx_scratch(ctx, 22, (size_t)n_jobs * (stride + 8) * 8);
-  uint64_t* h_res = (uint64_t*)atc_ctx_pinned(ctx, 1, (size_t)n_jobs * (stride + 8) * 8);
-  if (!surv || !skeys || !cnt || !res || !h_res) {
+  if (!surv || !skeys || !cnt) {
     atc_set_error(ctx, "scratch allocation failed");
     return ATC_ERR_CUDA;
   }
-  // job j: result block res + j*stride; histogram hist + 8*j after all blocks
-  unsigned long long* hist = reinterpret_cast<unsigned long long*>(res + (size_t)n_jobs * stride);
-  cudaMemsetAsync(res, 0, (size_t)n_jobs * (stride + 8) * 8, st);
-  std::vector<char> batched(n_jobs, 0);
-  for (int j = 0; j < n_jobs; ++j) {
-    atc_enum_job& job = jobs[j];
-    job.status = ATC_OK;
-    job.n_survivors = 0;
-    for (int r = 0; r < ATC_REASON_COUNT; ++r) job.reason_counts[r] = 0;
-    EnumPlan e;
-    int rc = plan_enumerated(ctx, job.spec, job.ts, job.perms, job.n_perms, job.begin, job.end, mode, e);
-    if (rc) {
-      job.status = rc;
-      continue;
-    }
-    if (job.end - job.begin > (1ull << 34)) continue;  // chunked: single-space path below
-    uint8_t* d_perms = nullptr;
-    rc = enqueue_tables(ctx, e, job.ts, job.perms, job.n_perms, &d_perms, st);
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(b->res + (size_t)b->n * kBatchStride);
+  cudaMemsetAsync(b->res, 0, batch_res_words(b->n) * 8, st);
+  for (int j = 0; j < b->n; ++j) {
+    if (!b->batched[j]) continue;
+    atc_enum_job& job = b->jobs[j];
+    EnumPlan& e = b->plans[j];
+    int rc = enqueue_tables(ctx, e, job.ts, job.perms, job.n_perms, &b->d_perms[j], st);
     if (rc) return rc;
-    uint64_t* rj = res + (size_t)j * stride;
     if (job.end > job.begin) {
-      BindingSource src{nullptr, nullptr, d_perms, e.size_maps, job.begin, 1};
-      rc = run_eval(ctx, e.sp, job.ts, src, job.end - job.begin, nullptr, surv, chunk_cap, cnt, skeys, hist + 8 * j,
-                    st, e.use_table ? &e.pt : nullptr, e.use_rows ? &e.plan : nullptr);
+      BindingSource src{nullptr, nullptr, b->d_perms[j], e.size_maps, job.begin, 1};
+      rc = run_eval(ctx, e.sp, job.ts, src, job.end - job.begin, nullptr, surv, chunk_cap, cnt, skeys,
+                    hist + 8 * j, st, e.use_table ? &e.pt : nullptr, e.use_rows ? &e.plan : nullptr);
       if (rc) return rc;
-      k_finalize<<<64, 256, 0, st>>>(surv, cnt, chunk_cap, skeys, job.begin, rj, kResultPrefix, hist + 8 * j);
+      k_finalize<<<64, 256, 0, st>>>(surv, cnt, chunk_cap, skeys, job.begin, b->res + (size_t)j * kBatchStride,
+                                     kResultPrefix, hist + 8 * j);
       if (ctx->prof) ctx->prof_kernels += 1;
     }
-    batched[j] = 1;
   }
-  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(h_res, res, (size_t)n_jobs * (stride + 8) * 8, cudaMemcpyDeviceToHost, st),
-                   "D2H results") ||
-      !atc_cuda_ok(ctx, cudaStreamSynchronize(st), "enumerate-many sync"))
+  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(b->h_res, b->res, batch_res_words(b->n) * 8, cudaMemcpyDeviceToHost, st),
+                   "D2H results"))
     return ATC_ERR_CUDA;
-  const uint64_t* h_hist = h_res + (size_t)n_jobs * stride;
+  return atc_cuda_ok(ctx, cudaGetLastError(), "batch launch") ? ATC_OK : ATC_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+}  // extern "C"
+
+namespace {
+
+atc_enum_batch* batch_create(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, int32_t mode, bool transient) {
+  if (!ctx || ctx->broken) return nullptr;
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs) || (mode != ATC_MODE_FP64 && mode != ATC_MODE_FP32_SCREEN)) {
+    atc_set_error(ctx, "bad arguments to atc_enum_batch_create");
+    return nullptr;
+  }
+  cudaSetDevice(ctx->device);
+  auto* b = new atc_enum_batch;
+  b->jobs = jobs;
+  b->n = n_jobs;
+  b->mode = mode;
+  b->transient = transient;
+  b->plans.resize(n_jobs);
+  b->d_perms.assign(n_jobs, nullptr);
+  b->batched.assign(n_jobs, 0);
+  std::vector<size_t> off(n_jobs, 0);
+  size_t total = 0;
   for (int j = 0; j < n_jobs; ++j) {
     atc_enum_job& job = jobs[j];
+    job.status = plan_enumerated(ctx, job.spec, job.ts, job.perms, job.n_perms, job.begin, job.end, mode,
+                                 b->plans[j]);
+    if (job.status != ATC_OK || job.end - job.begin > (1ull << 34)) continue;  // errors / chunked: not batched
+    off[j] = total;
+    total += ((size_t)job.n_perms * b->plans[j].sp.nA + 15) / 16 * 16;
+    b->batched[j] = 1;
+  }
+  // every job's permutations in one device buffer (the context's slot 6 for a
+  // one-shot batch, an owned allocation for a reusable one)
+  uint8_t* perms = nullptr;
+  const size_t words = batch_res_words(n_jobs > 0 ? n_jobs : 1);
+  bool ok = true;
+  if (transient) {
+    perms = (uint8_t*)atc_ctx_scratch(ctx, 6, total + 16);
+    b->res = (uint64_t*)atc_ctx_scratch(ctx, 22, words * 8);
+    b->h_res = (uint64_t*)atc_ctx_pinned(ctx, 1, words * 8);
+    ok = perms && b->res && b->h_res;
+  } else {
+    ok = cudaMalloc(&perms, total + 16) == cudaSuccess && cudaMalloc(&b->res, words * 8) == cudaSuccess &&
+         cudaMallocHost(&b->h_res, words * 8) == cudaSuccess;
+    b->perm_block = perms;
+  }
+  if (!ok) {
+    atc_set_error(ctx, "batch allocation failed");
+    atc_enum_batch_destroy(ctx, b);
+    return nullptr;
+  }
+  for (int j = 0; j < n_jobs; ++j) {
+    if (!b->batched[j]) continue;
+    b->d_perms[j] = perms + off[j];
+    cudaMemcpyAsync(b->d_perms[j], jobs[j].perms, (size_t)jobs[j].n_perms * b->plans[j].sp.nA,
+                    cudaMemcpyHostToDevice, ctx->stream);
+  }
+  return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+atc_enum_batch* atc_enum_batch_create(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, int32_t mode) {
+  atc_enum_batch* b = batch_create(ctx, jobs, n_jobs, mode, false);
+  if (b && !atc_cuda_ok(ctx, cudaStreamSynchronize(ctx->stream), "batch upload")) {
+    atc_enum_batch_destroy(ctx, b);
+    return nullptr;
+  }
+  return b;
+}
+
+void atc_enum_batch_destroy(atc_ctx* ctx, atc_enum_batch* b) {
+  if (!b) return;
+  if (ctx) cudaSetDevice(ctx->device);
+  if (b->exec) cudaGraphExecDestroy(b->exec);
+  if (!b->transient) {
+    if (b->perm_block) cudaFree(b->perm_block);
+    if (b->res) cudaFree(b->res);
+    if (b->h_res) cudaFreeHost(b->h_res);
+  }
+  delete b;
+}
+
+int atc_enum_batch_run(atc_ctx* ctx, atc_enum_batch* b) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (!b) {
+    atc_set_error(ctx, "null batch");
+    return ATC_ERR_ARG;
+  }
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  ctx->mode = b->mode;
+  for (int j = 0; j < b->n; ++j) {
+    atc_enum_job& job = b->jobs[j];
+    if (job.status != ATC_OK && b->batched[j]) job.status = ATC_OK;
+    job.n_survivors = 0;
+    for (int r = 0; r < ATC_REASON_COUNT; ++r) job.reason_counts[r] = 0;
+  }
+  // eager on the first run (sizes the scratch) and whenever profiling; a graph
+  // replay afterwards (one launch for the whole sweep)
+  int rc = ATC_OK;
+  if (b->runs == 0 || ctx->prof || b->graph_failed) {
+    rc = enqueue_batch(ctx, b, st);
+  } else {
+    if (!b->exec) {
+      cudaGraph_t g = nullptr;
+      bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+      if (ok) {
+        const int erc = enqueue_batch(ctx, b, st);
+        ok = cudaStreamEndCapture(st, &g) == cudaSuccess && erc == ATC_OK;
+        ok = ok && cudaGraphInstantiate(&b->exec, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+      }
+      if (!ok) {
+        cudaGetLastError();
+        b->exec = nullptr;
+        b->graph_failed = true;
+      }
+    }
+    rc = b->exec ? (atc_cuda_ok(ctx, cudaGraphLaunch(b->exec, st), "batch graph launch") ? ATC_OK : ATC_ERR_CUDA)
+                 : enqueue_batch(ctx, b, st);
+  }
+  if (rc) return rc;
+  if (!atc_cuda_ok(ctx, cudaStreamSynchronize(st), "batch sync")) return ATC_ERR_CUDA;
+  ++b->runs;
+  const uint64_t* h_hist = b->h_res + (size_t)b->n * kBatchStride;
+  for (int j = 0; j < b->n; ++j) {
+    atc_enum_job& job = b->jobs[j];
     if (job.status != ATC_OK) continue;
-    const uint64_t* rj = h_res + (size_t)j * stride;
+    const uint64_t* rj = b->h_res + (size_t)j * kBatchStride;
     const uint64_t c = rj[0], npass = rj[1];
-    if (!batched[j] || c > chunk_cap || npass > kResultPrefix) {
+    if (!b->batched[j] || c > kEnumChunkCap || npass > kResultPrefix) {
       // overflow (or a very large range): the single-space path with its own chunking
-      job.status = atc_eval_enumerated(ctx, job.spec, job.ts, job.perms, job.n_perms, job.begin, job.end, mode,
+      job.status = atc_eval_enumerated(ctx, job.spec, job.ts, job.perms, job.n_perms, job.begin, job.end, b->mode,
                                        job.survivors, job.cap, &job.n_survivors, job.reason_counts);
       continue;
     }
@@ -947,10 +1082,20 @@ int atc_eval_enumerated_many(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, i
     for (size_t i = 0; i < pass.size() && (int64_t)i < job.cap; ++i)
       if (job.survivors) job.survivors[i] = pass[i];
     job.n_survivors = (int64_t)npass;
-    for (int r = 0; r < ATC_REASON_COUNT; ++r) job.reason_counts[r] = (int64_t)h_hist[8 * j + r];
+    for (int r = 0; r < ATC_REASON_COUNT; ++r) job.reason_counts[r] = job.end > job.begin ? (int64_t)h_hist[8 * j + r] : 0;
     job.reason_counts[ATC_PASS] = (int64_t)npass;
   }
   return ATC_OK;
+}
+
+int atc_eval_enumerated_many(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, int32_t mode) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (n_jobs == 0) return ATC_OK;
+  atc_enum_batch* b = batch_create(ctx, jobs, n_jobs, mode, true);
+  if (!b) return ATC_ERR_ARG;
+  const int rc = atc_enum_batch_run(ctx, b);
+  atc_enum_batch_destroy(ctx, b);
+  return rc;
 }
 
 }  // extern "C"

@@ -275,16 +275,26 @@ class Evaluator:
     def eval_enumerated_many(self, items: list, cap: int = 1 << 16, mode: int = _lib.MODE_FP64) -> list:
         """eval_enumerated for many (spec, ts, space, begin, end) at once
         (atc_eval_enumerated_many: one stream pass, one result copy)."""
-        n = len(items)
-        jobs = (_lib.EnumJob * max(n, 1))()
-        keep = []
+        return EnumSweep(self, items, cap, mode, prepared=False).run()
+
+    def sweep(self, items: list, cap: int = 1 << 16, mode: int = _lib.MODE_FP64) -> "EnumSweep":
+        """A prepared, reusable sweep (atc_enum_batch_*): run() repeatedly replays
+        one CUDA graph of every job after the first eager run."""
+        return EnumSweep(self, items, cap, mode, prepared=True)
+
+
+class EnumSweep:
+    def __init__(self, ev: Evaluator, items: list, cap: int, mode: int, prepared: bool):
+        self.ev, self.cap, self.mode, self.n = ev, cap, mode, len(items)
+        self.jobs = (_lib.EnumJob * max(self.n, 1))()
+        self._keep = []
         for j, (spec, ts, space, begin, end) in enumerate(items):
-            h = ts.upload(self.ctx)
+            h = ts.upload(ev.ctx)
             desc = spec.to_desc()
             perms = np.ascontiguousarray(space.perms, dtype=np.uint8)
             surv = np.zeros(max(cap, 1), dtype=np.uint64)
-            keep.append((desc, perms, surv))
-            jb = jobs[j]
+            self._keep.append((desc, perms, surv, ts))
+            jb = self.jobs[j]
             jb.spec = C.cast(C.pointer(desc), C.c_void_p)
             jb.ts = h.value
             jb.perms = perms.ctypes.data
@@ -292,15 +302,40 @@ class Evaluator:
             jb.begin, jb.end = int(begin), int(space.count if end is None else end)
             jb.survivors = surv.ctypes.data
             jb.cap = cap
-        _lib.check(self.ctx.handle, _lib.lib().atc_eval_enumerated_many(self.ctx.handle, jobs, n, mode))
+        self.handle = None
+        if prepared:
+            L = _lib.lib()
+            self.handle = L.atc_enum_batch_create(ev.ctx.handle, self.jobs, self.n, mode)
+            if not self.handle:
+                raise _lib.AtcError(_lib.ATC_ERR_ARG, L.atc_last_error(ev.ctx.handle).decode())
+
+    def run(self) -> list:
+        """[(passing indices ascending (<= cap), passing count, reason histogram)] per item."""
+        L = _lib.lib()
+        if self.handle:
+            _lib.check(self.ev.ctx.handle, L.atc_enum_batch_run(self.ev.ctx.handle, self.handle))
+        else:
+            _lib.check(self.ev.ctx.handle, L.atc_eval_enumerated_many(self.ev.ctx.handle, self.jobs, self.n,
+                                                                      self.mode))
         out = []
-        for j in range(n):
-            jb = jobs[j]
+        for j in range(self.n):
+            jb = self.jobs[j]
             if jb.status != _lib.ATC_OK:
                 raise _lib.AtcError(jb.status, f"job {j}: atc error {jb.status}")
             k = int(jb.n_survivors)
-            out.append((keep[j][2][:min(k, cap)].copy(), k, np.array(list(jb.reason_counts), dtype=np.int64)))
+            out.append((self._keep[j][2][:min(k, self.cap)].copy(), k, np.array(list(jb.reason_counts), dtype=np.int64)))
         return out
+
+    def close(self):
+        if self.handle:
+            _lib.lib().atc_enum_batch_destroy(self.ev.ctx.handle, self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 @dataclass

@@ -280,8 +280,11 @@ def test_enumerated_many_matches_single(ev):
     g = next(j for j in jobs if j.stem == "naive_rowmajor" and j.spec_name == "gemm_rowmajor")
     ts64 = fixtures.load("naive_rowmajor").testsets(16, variant="testsets64")
     items.append((g.spec, ts64, g.space, 0, g.count))  # 27 passing bindings, cap 8 below
-    many = ev.eval_enumerated_many(items, cap=8)
-    for (spec, ts, space, b, e), (pm, nm, hm) in zip(items, many):
-        ps, ns, hs = ev.eval_enumerated(spec, ts, space, b, e, cap=8)
-        np.testing.assert_array_equal(pm, ps)
-        assert nm == ns and hm.tolist() == hs.tolist()
+    single = [ev.eval_enumerated(spec, ts, space, b, e, cap=8) for spec, ts, space, b, e in items]
+    sweep = ev.sweep(items, cap=8)
+    runs = [ev.eval_enumerated_many(items, cap=8)] + [sweep.run() for _ in range(3)]  # eager, then graph replays
+    for many in runs:
+        for (ps, ns, hs), (pm, nm, hm) in zip(single, many):
+            np.testing.assert_array_equal(pm, ps)
+            assert nm == ns and hm.tolist() == hs.tolist()
+    sweep.close()
