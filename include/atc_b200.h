@@ -139,6 +139,13 @@ int atc_profile_read(atc_ctx* ctx, atc_profile* out);
 int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out);
 int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h);
 
+/* atc_testsets_upload without the final wait: the copies and the dirty-list
+ * kernel run on the context's copy stream, and every evaluation that uses the
+ * handle waits for them on the device, so uploads overlap evaluations of
+ * earlier handles.  Host buffers must stay valid and unmodified until an
+ * evaluation using the handle has returned (or the handle is freed). */
+int atc_testsets_upload_async(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out);
+
 /* Explicit candidate list (ranked order).  arr_map[b*n_arrays + a] = user pointer
  * index bound to API array a; size_map[b*n_sizes + q] = user int index bound to
  * API size param q.  Outputs (host): fail_t[b] = first failing test or -1,

@@ -113,6 +113,7 @@ _SIGS = [
     ("atc_profile_read", C.c_int, [_P, C.POINTER(Profile)]),
     ("atc_testsets_upload", C.c_int, [_P, C.POINTER(Testsets), C.POINTER(_P)]),
     ("atc_testsets_free", C.c_int, [_P, _P]),
+    ("atc_testsets_upload_async", C.c_int, [_P, C.POINTER(Testsets), C.POINTER(_P)]),
     ("atc_eval_bindings", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, C.c_int64, C.c_int32, _P, _P,
                                     C.POINTER(C.c_int64)]),
     ("atc_eval_bindings_device", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, C.c_int64, C.c_int32, _P, _P, _P]),

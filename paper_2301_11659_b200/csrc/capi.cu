@@ -56,7 +56,13 @@ struct atc_testset_handle {
   int32_t T = 0, nI = 0, nP = 0;
   std::vector<int64_t> h_ints;  // host copy of the int values
   std::vector<void*> allocations;
+  cudaEvent_t ready = nullptr;  // uploads + dirty lists complete (recorded on the copy stream)
 };
+
+// Makes `st` wait for the upload of `ts` (no-op once it has completed).
+static void ts_wait(const atc_testset_handle* ts, cudaStream_t st) {
+  if (ts && ts->ready) cudaStreamWaitEvent(st, ts->ready, 0);
+}
 
 // ------------------------------------------------------------ ctx helpers -----
 void atc_set_error(atc_ctx* ctx, const char* fmt, ...) {
@@ -236,7 +242,9 @@ atc_ctx* atc_create(int device) {
     return ctx;
   }
   cudaSetDevice(device);
-  if (!atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate"))
+  if (!atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
+      !atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
+      !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->free_ev, cudaEventDisableTiming), "cudaEventCreate"))
     ctx->broken = true;
   ctx->own_stream = ctx->stream;
   return ctx;
@@ -255,6 +263,8 @@ void atc_destroy(atc_ctx* ctx) {
     for (auto& e : ctx->prof_screen) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
     for (auto& e : ctx->prof_confirm) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->free_ev) cudaEventDestroy(ctx->free_ev);
   }
   delete ctx;
 }
@@ -312,7 +322,9 @@ int atc_profile_read(atc_ctx* ctx, atc_profile* out) {
   return ATC_OK;
 }
 
-int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out) {
+}  // extern "C"
+
+static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out, bool sync) {
   if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
   if (!ts || !out || ts->n_tests < 1 || ts->n_tests > kMaxT || ts->n_ints < 1 || ts->n_ints > kMaxInts ||
       ts->n_ptrs < 1 || ts->n_ptrs > kMaxPtrs) {
@@ -363,8 +375,35 @@ int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle
     atc_testsets_free(ctx, h);
     return ATC_ERR_CUDA;
   }
-  cudaStream_t st = ctx->stream;
+  // copies and the dirty-list kernel go to the copy stream, after any pool
+  // memory freed by earlier handles is no longer read by the compute stream
+  cudaStream_t st = ctx->copy_stream;
+  if (ctx->free_pending) {
+    cudaStreamWaitEvent(st, ctx->free_ev, 0);
+    ctx->free_pending = false;
+  }
   bool ok = true;
+  // host regions that lie back to back in the same order as the device pool are
+  // copied as one run (one DMA instead of T*n_ptrs)
+  struct Run {
+    const double* src = nullptr;
+    size_t dst = 0, bytes = 0;
+  };
+  Run run_i, run_f;
+  auto flush = [&](Run& r, double* base, const char* what) {
+    if (r.bytes) ok = ok && atc_cuda_ok(ctx, cudaMemcpyAsync(base + r.dst, r.src, r.bytes, cudaMemcpyHostToDevice, st), what);
+    r = Run{};
+  };
+  auto add = [&](Run& r, double* base, const double* src, size_t dst, size_t bytes, const char* what) {
+    if (r.bytes && r.src + r.bytes / 8 == src && r.dst + r.bytes / 8 == dst && r.bytes % 256 == 0) {
+      r.bytes += bytes;
+      return;
+    }
+    flush(r, base, what);
+    r.src = src;
+    r.dst = dst;
+    r.bytes = bytes;
+  };
   for (int t = 0; t < T && ok; ++t)
     for (int p = 0; p < nP && ok; ++p) {
       const size_t i = (size_t)t * nP + p;
@@ -382,9 +421,11 @@ int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle
              atc_cuda_ok(ctx, cudaMemsetAsync(fin + off[i], 0, bytes, st), "memset");
         continue;
       }
-      ok = atc_cuda_ok(ctx, cudaMemcpyAsync(init + off[i], hi, bytes, cudaMemcpyHostToDevice, st), "H2D init") &&
-           atc_cuda_ok(ctx, cudaMemcpyAsync(fin + off[i], hf, bytes, cudaMemcpyHostToDevice, st), "H2D final");
+      add(run_i, init, hi, (size_t)off[i], bytes, "H2D init");
+      add(run_f, fin, hf, (size_t)off[i], bytes, "H2D final");
     }
+  flush(run_i, init, "H2D init");
+  flush(run_f, fin, "H2D final");
   std::vector<int32_t> tok_h(T, 1);
   if (ts->test_ok)
     for (int t = 0; t < T; ++t) tok_h[t] = ts->test_ok[t] ? 1 : 0;
@@ -418,7 +459,9 @@ int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle
     dim3 grid((unsigned)std::min<int64_t>((maxlen + 255) / 256, 64), (unsigned)(T * nP));
     k_build_dirty<<<grid, 256, 0, st>>>(v, dpos, dcnt, dmax);
     ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_build_dirty") &&
-         atc_cuda_ok(ctx, cudaStreamSynchronize(st), "upload sync");
+         atc_cuda_ok(ctx, cudaEventCreateWithFlags(&h->ready, cudaEventDisableTiming), "cudaEventCreate") &&
+         atc_cuda_ok(ctx, cudaEventRecord(h->ready, st), "cudaEventRecord") &&
+         (!sync || atc_cuda_ok(ctx, cudaEventSynchronize(h->ready), "upload sync"));
   }
   if (!ok) {
     atc_testsets_free(ctx, h);
@@ -428,9 +471,27 @@ int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle
   return ATC_OK;
 }
 
+extern "C" {
+
+int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out) {
+  return testsets_upload(ctx, ts, out, true);
+}
+
+int atc_testsets_upload_async(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out) {
+  return testsets_upload(ctx, ts, out, false);
+}
+
 int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h) {
   if (!h) return ATC_OK;
-  if (ctx && !ctx->broken) cudaSetDevice(ctx->device);
+  if (ctx && !ctx->broken) {
+    cudaSetDevice(ctx->device);
+    // the memory returns to the pool: later uploads wait until the compute
+    // stream has passed this point (and this handle's own copies are done)
+    ts_wait(h, ctx->stream);
+    cudaEventRecord(ctx->free_ev, ctx->stream);
+    ctx->free_pending = true;
+  }
+  if (h->ready) cudaEventDestroy(h->ready);
   for (void* p : h->allocations) {
     if (ctx && !ctx->broken)
       atc_pool_free(ctx, p);
@@ -592,6 +653,7 @@ int atc_eval_bindings_device(atc_ctx* ctx, const atc_spec_desc* spec, const atc_
   if (n_bindings == 0) return ATC_OK;
   cudaSetDevice(ctx->device);
   cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  ts_wait(ts, st);
   const uint64_t n = (uint64_t)n_bindings;
   ctx->mode = mode;
   int32_t* keys = (int32_t*)atc_ctx_scratch(ctx, 0, n * 4);
@@ -795,6 +857,7 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
   if (rc) return rc;
   cudaSetDevice(ctx->device);
   cudaStream_t st = ctx->stream;
+  ts_wait(ts, st);
   ctx->mode = mode;
   const uint64_t chunk_cap = kEnumChunkCap;
   uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
@@ -901,7 +964,7 @@ constexpr uint64_t kBatchStride = 2 + kResultPrefix;  // count, passing count, p
 
 size_t batch_res_words(int n) { return (size_t)n * (kBatchStride + 8); }
 
-int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st) {
+int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_uploads) {
   const uint64_t chunk_cap = kEnumChunkCap;
   uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
   int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, chunk_cap * 4);
@@ -916,6 +979,7 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st) {
     if (!b->batched[j]) continue;
     atc_enum_job& job = b->jobs[j];
     EnumPlan& e = b->plans[j];
+    if (wait_uploads) ts_wait(job.ts, st);  // job j starts as soon as its own test sets are resident
     int rc = enqueue_tables(ctx, e, job.ts, job.perms, job.n_perms, &b->d_perms[j], st);
     if (rc) return rc;
     if (job.end > job.begin) {
@@ -1003,6 +1067,8 @@ extern "C" {
 
 atc_enum_batch* atc_enum_batch_create(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, int32_t mode) {
   atc_enum_batch* b = batch_create(ctx, jobs, n_jobs, mode, false);
+  if (b)
+    for (int j = 0; j < n_jobs; ++j) ts_wait(jobs[j].ts, ctx->stream);
   if (b && !atc_cuda_ok(ctx, cudaStreamSynchronize(ctx->stream), "batch upload")) {
     atc_enum_batch_destroy(ctx, b);
     return nullptr;
@@ -1041,13 +1107,13 @@ int atc_enum_batch_run(atc_ctx* ctx, atc_enum_batch* b) {
   // replay afterwards (one launch for the whole sweep)
   int rc = ATC_OK;
   if (b->runs == 0 || ctx->prof || b->graph_failed) {
-    rc = enqueue_batch(ctx, b, st);
+    rc = enqueue_batch(ctx, b, st, true);
   } else {
     if (!b->exec) {
       cudaGraph_t g = nullptr;
       bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) == cudaSuccess;
       if (ok) {
-        const int erc = enqueue_batch(ctx, b, st);
+        const int erc = enqueue_batch(ctx, b, st, false);  // uploads completed at create
         ok = cudaStreamEndCapture(st, &g) == cudaSuccess && erc == ATC_OK;
         ok = ok && cudaGraphInstantiate(&b->exec, g, 0) == cudaSuccess;
         if (g) cudaGraphDestroy(g);
@@ -1059,7 +1125,7 @@ int atc_enum_batch_run(atc_ctx* ctx, atc_enum_batch* b) {
       }
     }
     rc = b->exec ? (atc_cuda_ok(ctx, cudaGraphLaunch(b->exec, st), "batch graph launch") ? ATC_OK : ATC_ERR_CUDA)
-                 : enqueue_batch(ctx, b, st);
+                 : enqueue_batch(ctx, b, st, true);
   }
   if (rc) return rc;
   if (!atc_cuda_ok(ctx, cudaStreamSynchronize(st), "batch sync")) return ATC_ERR_CUDA;

@@ -20,6 +20,12 @@ struct atc_ctx {
   void* pinned[4] = {};
   size_t pinned_bytes[4] = {};
   cudaStream_t own_stream = nullptr;
+  // test-set uploads run on their own stream (copy engine) and publish a ready
+  // event per handle; frees record free_ev on the compute stream, which the
+  // next upload waits on before reusing pool memory
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t free_ev = nullptr;
+  bool free_pending = false;
   int mode = 0;  // ATC_MODE_* of the evaluation in flight
   // instrumentation (atc_profile_*)
   bool prof = false;
