@@ -26,6 +26,10 @@ __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, ui
                               uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                               unsigned long long* reason_hist);
 __global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need);
+__global__ void k_cmask(const uint8_t* table, uint64_t n_words, int nI, uint32_t* cmask);
+__global__ void k_screen_conv_pairs(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
+                                    uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
+                                    unsigned long long* surv_cnt, unsigned long long* reason_hist);
 __global__ void k_screen_conv_planes(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
                                    uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
                                    unsigned long long* surv_cnt, unsigned long long* reason_hist);
@@ -515,6 +519,22 @@ int screen_budget(const SpecView& sp) { return sp.sem == ATC_SEM_GEMM ? 16 : 2; 
 // weights=(c,k,r,s), out=(n,k,oh,ow) in any order, in/weights/out = arrays
 // 0/1/2, a table key free of digit 0, nI <= 32.  ATC_SCREEN_GENERIC=1 forces
 // the generic k_screen_rows (A/B checks).
+// ATC_SCREEN_PLANES=1: k_screen_conv_planes instead of k_screen_conv_pairs (A/B checks)
+bool pairs_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("ATC_SCREEN_PLANES");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
+// 32-bit index arithmetic when every t=0 size is <= 200 (any product of 4 sizes < 2^31)
+bool ts_i32(const atc_testset_handle* ts) {
+  int64_t umax = 0;
+  for (int i = 0; i < ts->nI; ++i) umax = std::max<int64_t>(umax, std::llabs(ts->h_ints[i]));
+  return umax <= 200;
+}
+
 bool conv_thresholds_ok(const SpecView& sp, const RowPlan& plan, int nI) {
   static const bool generic = [] {
     const char* e = std::getenv("ATC_SCREEN_GENERIC");
@@ -586,6 +606,9 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
         ATC_LAUNCH_ROWS(ATC_SEM_GEMM, 6, kM);
       else
         ATC_LAUNCH_ROWS(ATC_SEM_GEMM, 6, kDyn);
+    } else if (plan->cmask) {  // conv_pairs_ok at table time
+      k_screen_conv_pairs<<<g2, kScreenThreads, (size_t)16 << ts->nI, st>>>(
+          ts->view, src.perms, src.size_maps, b, e, *plan, surv, surv_cap, surv_cnt, hist);
     } else if (i32 && conv_thresholds_ok(sp, *plan, ts->nI)) {
       k_screen_conv_planes<<<g2, kScreenThreads, 0, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
                                                         surv_cap, surv_cnt, hist);
@@ -838,6 +861,23 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
     k_pos0_table<<<(unsigned)std::min<uint64_t>((e.table_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16), 256, 0,
                    st>>>(ts->view, sp, d_perms, n_perms, e.pt, tab);
     if (ctx->prof) ctx->prof_kernels += 1;
+    // conv with nI <= 11: the pair screen reads the table as one bit word per
+    // (perm, h, w, r, s) over the values of tc_c (key stride 1)
+    if (e.use_rows && ts_i32(ts) && conv_thresholds_ok(sp, e.plan, ts->nI) && ts->nI <= 11 &&
+        e.plan.key_stride[1] == 1 && !pairs_disabled()) {
+      const uint64_t words = e.table_bytes / (uint64_t)ts->nI;
+      uint32_t* cm = (uint32_t*)atc_ctx_scratch(ctx, 23, words * 4 + 16);
+      if (!cm) {
+        atc_set_error(ctx, "scratch allocation failed (cmask)");
+        return ATC_ERR_CUDA;
+      }
+      k_cmask<<<(unsigned)std::min<uint64_t>((words + 255) / 256, (uint64_t)ctx->sm_count * 16), 256, 0, st>>>(
+          tab, words, ts->nI, cm);
+      e.plan.cmask = cm;
+      if (ctx->prof) ctx->prof_kernels += 1;
+    } else {
+      e.plan.cmask = nullptr;
+    }
   }
   return ATC_OK;
 }

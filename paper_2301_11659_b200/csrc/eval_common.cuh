@@ -84,6 +84,9 @@ struct RowPlan {
   // = the smallest n writing every dirty position of region p at t = 0 (k_gemm_need;
   // INT32_MAX: none does, -1: not tabulated, use the dirty list)
   const int32_t* gemm_need;
+  // conv (k_screen_conv_pairs): position-0 verdict bits over the nI values of tc_c
+  // per (perm, h, w, r, s) key (k_cmask)
+  const uint32_t* cmask;
 };
 
 enum : int32_t { kUndecided = -2 };

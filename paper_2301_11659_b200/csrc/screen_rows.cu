@@ -452,6 +452,215 @@ __global__ void __launch_bounds__(256) k_screen_conv_planes(TestsetView ts, cons
     atomicAdd(&reason_hist[threadIdx.x], (unsigned long long)s_hist[threadIdx.x]);
 }
 
+// ----------------------------------------------------------------------------
+// k_cmask: position-0 verdict bits of the nI values of tc_c (the first table
+// role, key stride 1): cmask[i] bit j = table[i*nI + j] == 1.
+__global__ void k_cmask(const uint8_t* table, uint64_t n_words, int nI, uint32_t* cmask) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_words; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t m = 0;
+    for (int j = 0; j < nI; ++j) m |= (table[i * nI + j] == 1 ? 1u : 0u) << j;
+    cmask[i] = m;
+  }
+}
+
+// k_screen_conv_pairs: k_screen_conv_planes with the loop over tc_c removed too
+// (nI <= 11, so a plane's nI x nI bindings fit one 128-bit mask; bit
+// c_index*nI + x_index = the binding's offset in the plane, Appendix C order).
+//
+// The plane's checks as masks over (x, c) pairs, from CTA-wide tables:
+//   gtx[T] / gtc[T]   pairs whose x (tc_n) / c (tc_c) value exceeds T, T in [0, 255]
+//   gt_prod(T)        pairs whose product x*c exceeds T (sorted products + suffix masks)
+//   dispatch  = x < 1 | c < 1 | c > len(wt)/(k*r*s) | x*c > len(in)/(h*w) | x > len(out)/(k*oh*ow)
+//   UB        = x*c > (len(in) - Q - 1)/(h*w)               (all, if len(in) <= Q)
+//   mismatch  = x <= dirty_max(out)/(k*oh*ow) | position-0 verdict of (perm, c, h, w, r, s)
+// (floors; the same thresholds as k_screen_conv_planes, now applied to all nI
+// values of c at once).  Verdicts, reason counts and survivors are identical.
+struct M128 {
+  uint64_t lo, hi;
+};
+__device__ __forceinline__ M128 operator|(M128 a, M128 b) { return {a.lo | b.lo, a.hi | b.hi}; }
+__device__ __forceinline__ M128 operator&(M128 a, M128 b) { return {a.lo & b.lo, a.hi & b.hi}; }
+__device__ __forceinline__ M128 operator~(M128 a) { return {~a.lo, ~a.hi}; }
+__device__ __forceinline__ bool any(M128 a) { return (a.lo | a.hi) != 0; }
+__device__ __forceinline__ unsigned popc(M128 a) { return __popcll(a.lo) + __popcll(a.hi); }
+__device__ __forceinline__ M128 bit_range(int lo, int hi) {  // bits [lo, hi), 0 <= lo <= hi <= 128
+  auto upto = [](int n) -> M128 {
+    if (n <= 0) return {0, 0};
+    if (n < 64) return {(1ull << n) - 1, 0};
+    if (n == 64) return {~0ull, 0};
+    if (n < 128) return {~0ull, (1ull << (n - 64)) - 1};
+    return {~0ull, ~0ull};
+  };
+  return upto(hi) & ~upto(lo);
+}
+__device__ __forceinline__ void set_bit(M128& m, int b) {
+  if (b < 64) m.lo |= 1ull << b;
+  else m.hi |= 1ull << (b - 64);
+}
+
+constexpr int kPairMaxInts = 11;  // nI^2 <= 121 bits
+
+__global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const uint8_t* perms, uint64_t size_maps,
+                                                            uint64_t begin, uint64_t end, RowPlan plan,
+                                                            uint64_t* surv, uint64_t surv_cap,
+                                                            unsigned long long* surv_cnt,
+                                                            unsigned long long* reason_hist) {
+  constexpr int NS = 9;
+  extern __shared__ M128 s_rowx[];  // [2^nI]: rows j of the plane for every bit j of the index
+  __shared__ int32_t s_u[kMaxInts];
+  __shared__ M128 s_gtx[kGtCap + 1], s_gtc[kGtCap + 1];
+  __shared__ int32_t s_prod[128];  // products x*c ascending, padded with INT32_MAX
+  __shared__ int s_pidx[128];
+  __shared__ M128 s_pgt[129];      // s_pgt[r] = pairs of product rank >= r
+  __shared__ unsigned int s_hist[ATC_REASON_COUNT];
+  const int nI = ts.nI, nI2 = nI * nI;
+  if (threadIdx.x < nI) s_u[threadIdx.x] = (int32_t)ts.ints[threadIdx.x];
+  if (threadIdx.x < ATC_REASON_COUNT) s_hist[threadIdx.x] = 0;
+  if (threadIdx.x < 128) s_prod[threadIdx.x] = INT32_MAX;
+  for (int m = threadIdx.x; m < (1 << nI); m += blockDim.x) {
+    M128 r{0, 0};
+    for (int j = 0; j < nI; ++j)
+      if (m >> j & 1) r = r | bit_range(j * nI, j * nI + nI);
+    s_rowx[m] = r;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t <= kGtCap; t += blockDim.x) {
+    uint32_t xm = 0;  // digit indices whose value exceeds t
+    for (int i = 0; i < nI; ++i) xm |= (s_u[i] > t ? 1u : 0u) << i;
+    M128 gx{0, 0};    // the same x bits in every row
+    for (int j = 0; j < nI; ++j) {
+      const int b0 = j * nI;
+      if (b0 < 64) gx.lo |= (uint64_t)xm << b0;
+      if (b0 + nI > 64) gx.hi |= b0 >= 64 ? (uint64_t)xm << (b0 - 64) : (uint64_t)xm >> (64 - b0);
+    }
+    s_gtx[t] = gx;
+    s_gtc[t] = s_rowx[xm];
+  }
+  if (threadIdx.x < nI2) {  // stable rank of the pair's product
+    const int b = threadIdx.x;
+    const int32_t pr = s_u[b % nI] * s_u[b / nI];
+    int rank = 0;
+    for (int i = 0; i < nI2; ++i) {
+      const int32_t q = s_u[i % nI] * s_u[i / nI];
+      rank += q < pr || (q == pr && i < b);
+    }
+    s_prod[rank] = pr;
+    s_pidx[rank] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x <= 128) {
+    M128 m{0, 0};
+    for (int r = threadIdx.x; r < nI2; ++r) set_bit(m, s_pidx[r]);
+    s_pgt[threadIdx.x] = m;
+  }
+  __syncthreads();
+  int p2 = 1;  // power of two > nI2: branch-free search over the padded products
+  while (p2 <= nI2) p2 <<= 1;
+  auto gt_prod = [&](int64_t t) -> M128 {
+    const int32_t tc = (int32_t)(t > INT32_MAX - 1 ? INT32_MAX - 1 : (t < INT32_MIN ? INT32_MIN : t));
+    int lo = 0;
+    for (int step = p2 >> 1; step > 0; step >>= 1)
+      if (s_prod[lo + step - 1] <= tc) lo += step;
+    return s_pgt[lo];
+  };
+  const bool test_ok0 = ts.test_ok[0] != 0;
+  // position-0 verdicts of a plane's nI values of c: one word of plan.cmask at
+  // (table key without c) / nI — the key strides of the other roles are multiples of nI
+  const uint32_t cperm = (uint32_t)(plan.pt.per_perm / (uint64_t)nI);
+  const M128 all = bit_range(0, nI2);
+  const M128 x_lt1 = ~s_gtx[0], c_lt1 = ~s_gtc[0];
+  const uint64_t planes_per_perm = size_maps / (uint64_t)nI2;
+  const uint32_t magic = (uint32_t)(0xFFFFFFFFull / (uint32_t)nI) + 1u;  // n / nI = umulhi(n, magic), n < 2^27
+  unsigned int cnt1 = 0, cnt2 = 0, cnt3 = 0, cnt4 = 0;
+  const uint64_t plane_lo = begin / nI2, plane_hi = (end + nI2 - 1) / nI2;
+  for (uint64_t pl = plane_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; pl < plane_hi;
+       pl += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p0 = pl * nI2;
+    const uint64_t lo = p0 < begin ? begin : p0, hi = p0 + nI2 > end ? end : p0 + nI2;
+    const unsigned int n_here = (unsigned int)(hi - lo);
+    if (!test_ok0) {
+      cnt3 += n_here;
+      continue;
+    }
+    const uint64_t perm = (pl >> 32) == 0 && (planes_per_perm >> 32) == 0
+                              ? (uint64_t)((uint32_t)pl / (uint32_t)planes_per_perm)
+                              : pl / planes_per_perm;
+    int digit[NS];
+    {
+      uint64_t s = pl - perm * planes_per_perm;  // digits 2..8
+      if (s < (1ull << 27)) {
+        uint32_t s32 = (uint32_t)s;
+#pragma unroll
+        for (int q = 2; q < NS; ++q) {
+          const uint32_t dq = __umulhi(s32, magic);
+          digit[q] = (int)(s32 - dq * (uint32_t)nI);
+          s32 = dq;
+        }
+      } else {
+#pragma unroll
+        for (int q = 2; q < NS; ++q) {
+          const uint64_t dq = s / (uint64_t)nI;
+          digit[q] = (int)(s - dq * (uint64_t)nI);
+          s = dq;
+        }
+      }
+    }
+    const int32_t ch = s_u[digit[2]], cw = s_u[digit[3]], ck = s_u[digit[4]], cr = s_u[digit[5]];
+    const int32_t cs = s_u[digit[6]], coh = s_u[digit[7]], cow = s_u[digit[8]];
+    if (min(min(min(ch, cw), min(ck, cr)), min(min(cs, coh), cow)) < 1) {
+      cnt2 += n_here;  // a dim of the plane < 1: "size is not positive" for every binding
+      continue;
+    }
+    const M128 range = (lo == p0 && hi == p0 + nI2) ? all : bit_range((int)(lo - p0), (int)(hi - p0));
+    const int p_in = perms[perm * 3 + 0], p_w = perms[perm * 3 + 1], p_out = perms[perm * 3 + 2];
+    // region lengths are < 2^31 (atc_testsets_upload): 32-bit divisions
+    const uint32_t len_in = (uint32_t)ts.region_len[p_in], len_w = (uint32_t)ts.region_len[p_w];
+    const uint32_t len_out = (uint32_t)ts.region_len[p_out];
+    const int32_t hw = ch * cw, krs = ck * cr * cs, ext_out = ck * coh * cow;
+    const float r_out = __frcp_rn((float)ext_out);
+    const uint32_t c_max = len_w / (uint32_t)krs;
+    const int d_out = div_cap(len_out, ext_out, r_out);
+    const M128 dm = range & (x_lt1 | c_lt1 | s_gtc[c_max < kGtCap ? (int)c_max : kGtCap] | s_gtx[d_out] |
+                             gt_prod(len_in / (uint32_t)hw));
+    M128 ok = range & ~dm, um{0, 0}, mm{0, 0};
+    if (any(ok)) {
+      const int32_t q_in = -hw + (coh + cr - 2) * cw + (cow + cs - 2);
+      const int64_t alim = (int64_t)len_in - q_in;  // UB iff x*c*h*w >= alim (< 2^32)
+      um = alim <= 0 ? ok : (ok & gt_prod((uint32_t)(alim - 1) / (uint32_t)hw));
+      ok = ok & ~um;
+      if (any(ok)) {
+        uint32_t ckey = (uint32_t)perm * cperm;
+#pragma unroll
+        for (int q = 2; q < NS; ++q) ckey += (uint32_t)digit[q] * (uint32_t)(plan.key_stride[q] / (uint64_t)nI);
+        const M128 tab = s_rowx[__ldg(plan.cmask + ckey)];
+        const int dmax = ts.dirty_max[p_out];
+        mm = ok & (~s_gtx[dmax < 0 ? 0 : div_cap(dmax, ext_out, r_out)] | tab);
+        ok = ok & ~mm;
+      }
+    }
+    cnt2 += popc(dm);
+    cnt4 += popc(um);
+    cnt1 += popc(mm);
+    if (any(ok)) {
+      unsigned long long slot = atomicAdd(surv_cnt, (unsigned long long)popc(ok));
+      for (uint64_t w = ok.lo; w; w &= w - 1, ++slot)
+        if (slot < surv_cap) surv[slot] = p0 + (uint64_t)(__ffsll((long long)w) - 1) - begin;
+      for (uint64_t w = ok.hi; w; w &= w - 1, ++slot)
+        if (slot < surv_cap) surv[slot] = p0 + 64 + (uint64_t)(__ffsll((long long)w) - 1) - begin;
+    }
+  }
+  unsigned int cnt[ATC_REASON_COUNT] = {0, cnt1, cnt2, cnt3, cnt4};
+#pragma unroll
+  for (int r = 1; r < ATC_REASON_COUNT; ++r) {
+    unsigned int v = cnt[r];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_hist[r], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < ATC_REASON_COUNT && s_hist[threadIdx.x])
+    atomicAdd(&reason_hist[threadIdx.x], (unsigned long long)s_hist[threadIdx.x]);
+}
+
 #define ATC_ROWS_INST(SEM, NS, I32, MASK)                                                                        \
   template __global__ void k_screen_rows<SEM, NS, I32, MASK>(TestsetView, SpecView, const uint8_t*, uint64_t,    \
                                                              uint64_t, uint64_t, RowPlan, uint64_t*, uint64_t,   \

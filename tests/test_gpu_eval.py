@@ -288,3 +288,23 @@ def test_enumerated_many_matches_single(ev):
             np.testing.assert_array_equal(pm, ps)
             assert nm == ns and hm.tolist() == hs.tolist()
     sweep.close()
+
+
+def test_conv_screen_kernels_agree():
+    """k_screen_conv_pairs (default), k_screen_conv_planes (ATC_SCREEN_PLANES=1) and
+    the generic k_screen_rows (ATC_SCREEN_GENERIC=1) give identical passing sets and
+    reason histograms (each run in its own process: the switches are read once)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    script = os.path.join(os.path.dirname(__file__), "screen_variant_run.py")
+    res = {}
+    for name, env in (("pairs", {}), ("planes", {"ATC_SCREEN_PLANES": "1"}), ("generic", {"ATC_SCREEN_GENERIC": "1"})):
+        out = subprocess.run([sys.executable, script], env={**os.environ, **env}, capture_output=True, text=True,
+                             timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[name] = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["pairs"] == res["planes"] == res["generic"]
+    assert any(r["hist"][4] for r in res["pairs"]) and any(r["hist"][2] for r in res["pairs"])
