@@ -29,7 +29,7 @@ __global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need);
 __global__ void k_cmask(const uint8_t* table, uint64_t n_words, int nI, uint32_t* cmask);
 __global__ void k_screen_conv_pairs(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
                                     uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
-                                    unsigned long long* surv_cnt, unsigned long long* reason_hist);
+                                    unsigned long long* surv_cnt, unsigned long long* reason_hist, int lut_n);
 __global__ void k_screen_conv_planes(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
                                    uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
                                    unsigned long long* surv_cnt, unsigned long long* reason_hist);
@@ -607,8 +607,14 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
       else
         ATC_LAUNCH_ROWS(ATC_SEM_GEMM, 6, kDyn);
     } else if (plan->cmask) {  // conv_pairs_ok at table time
-      k_screen_conv_pairs<<<g2, kScreenThreads, (size_t)16 << ts->nI, st>>>(
-          ts->view, src.perms, src.size_maps, b, e, *plan, surv, surv_cap, surv_cnt, hist);
+      // rank table of pair products when they are small (<= 4095)
+      int64_t pmax = 0;
+      for (int i = 0; i < ts->nI; ++i)
+        for (int k = 0; k < ts->nI; ++k) pmax = std::max<int64_t>(pmax, ts->h_ints[i] * ts->h_ints[k]);
+      const int lut_n = pmax < 4096 ? (int)pmax + 1 : 0;
+      const size_t smem = ((size_t)16 << ts->nI) + (size_t)(lut_n + 15) / 16 * 16;
+      k_screen_conv_pairs<<<g2, kScreenThreads, smem, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
+                                                            surv_cap, surv_cnt, hist, lut_n);
     } else if (i32 && conv_thresholds_ok(sp, *plan, ts->nI)) {
       k_screen_conv_planes<<<g2, kScreenThreads, 0, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
                                                         surv_cap, surv_cnt, hist);

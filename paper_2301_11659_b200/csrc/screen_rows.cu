@@ -500,11 +500,22 @@ __device__ __forceinline__ void set_bit(M128& m, int b) {
 
 constexpr int kPairMaxInts = 11;  // nI^2 <= 121 bits
 
+// min(floor(a / b), cap) for 0 <= a < 2^32, 1 <= b, cap <= 65536, rb ~= 1/b (exact)
+__device__ __forceinline__ int div_capn(uint32_t a, uint32_t b, float rb, int cap) {
+  if ((uint64_t)a >= (uint64_t)b * (uint32_t)cap) return cap;
+  int q = (int)((float)a * rb);  // q < cap: |error| < 1
+  if ((uint64_t)q * b > a) --q;
+  else if ((uint64_t)(q + 1) * b <= a) ++q;
+  return q;
+}
+
+// lut_n > 0: products are in [.., lut_n - 1] and the dynamic shared memory holds a
+// rank table (count of pair products <= T, T in [0, lut_n)) after the row table
 __global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const uint8_t* perms, uint64_t size_maps,
                                                             uint64_t begin, uint64_t end, RowPlan plan,
                                                             uint64_t* surv, uint64_t surv_cap,
                                                             unsigned long long* surv_cnt,
-                                                            unsigned long long* reason_hist) {
+                                                            unsigned long long* reason_hist, int lut_n) {
   constexpr int NS = 9;
   extern __shared__ M128 s_rowx[];  // [2^nI]: rows j of the plane for every bit j of the index
   __shared__ int32_t s_u[kMaxInts];
@@ -548,25 +559,37 @@ __global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const
     s_pidx[rank] = b;
   }
   __syncthreads();
+  uint8_t* s_rank = reinterpret_cast<uint8_t*>(s_rowx + (1 << nI));
   if (threadIdx.x <= 128) {
     M128 m{0, 0};
     for (int r = threadIdx.x; r < nI2; ++r) set_bit(m, s_pidx[r]);
     s_pgt[threadIdx.x] = m;
   }
+  for (int t = threadIdx.x; t < lut_n; t += blockDim.x) {  // rank = number of products <= t
+    int lo = 0;
+    while (lo < nI2 && s_prod[lo] <= t) ++lo;
+    s_rank[t] = (uint8_t)lo;
+  }
   __syncthreads();
   int p2 = 1;  // power of two > nI2: branch-free search over the padded products
   while (p2 <= nI2) p2 <<= 1;
+  // pairs whose product x*c exceeds t (t >= 0; t >= lut_n: none when lut_n > 0)
   auto gt_prod = [&](int64_t t) -> M128 {
-    const int32_t tc = (int32_t)(t > INT32_MAX - 1 ? INT32_MAX - 1 : (t < INT32_MIN ? INT32_MIN : t));
+    if (lut_n) return s_pgt[t >= lut_n ? nI2 : s_rank[t]];
+    const int32_t tc = (int32_t)(t > INT32_MAX - 1 ? INT32_MAX - 1 : t);
     int lo = 0;
     for (int step = p2 >> 1; step > 0; step >>= 1)
       if (s_prod[lo + step - 1] <= tc) lo += step;
     return s_pgt[lo];
   };
+  const int qcap = lut_n ? lut_n : INT32_MAX;  // quotients at or above it select no pair
   const bool test_ok0 = ts.test_ok[0] != 0;
   // position-0 verdicts of a plane's nI values of c: one word of plan.cmask at
   // (table key without c) / nI — the key strides of the other roles are multiples of nI
   const uint32_t cperm = (uint32_t)(plan.pt.per_perm / (uint64_t)nI);
+  uint32_t cks[NS];
+#pragma unroll
+  for (int q = 2; q < NS; ++q) cks[q] = (uint32_t)(plan.key_stride[q] / (uint64_t)nI);
   const M128 all = bit_range(0, nI2);
   const M128 x_lt1 = ~s_gtx[0], c_lt1 = ~s_gtc[0];
   const uint64_t planes_per_perm = size_maps / (uint64_t)nI2;
@@ -617,21 +640,22 @@ __global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const
     const uint32_t len_in = (uint32_t)ts.region_len[p_in], len_w = (uint32_t)ts.region_len[p_w];
     const uint32_t len_out = (uint32_t)ts.region_len[p_out];
     const int32_t hw = ch * cw, krs = ck * cr * cs, ext_out = ck * coh * cow;
-    const float r_out = __frcp_rn((float)ext_out);
-    const uint32_t c_max = len_w / (uint32_t)krs;
+    const float r_out = __frcp_rn((float)ext_out), r_hw = __frcp_rn((float)hw);
+    const int c_max = div_cap(len_w, krs, __frcp_rn((float)krs));
     const int d_out = div_cap(len_out, ext_out, r_out);
-    const M128 dm = range & (x_lt1 | c_lt1 | s_gtc[c_max < kGtCap ? (int)c_max : kGtCap] | s_gtx[d_out] |
-                             gt_prod(len_in / (uint32_t)hw));
+    const int a_in = lut_n ? div_capn(len_in, hw, r_hw, qcap) : (int)(len_in / (uint32_t)hw);
+    const M128 dm = range & (x_lt1 | c_lt1 | s_gtc[c_max] | s_gtx[d_out] | gt_prod(a_in));
     M128 ok = range & ~dm, um{0, 0}, mm{0, 0};
     if (any(ok)) {
       const int32_t q_in = -hw + (coh + cr - 2) * cw + (cow + cs - 2);
       const int64_t alim = (int64_t)len_in - q_in;  // UB iff x*c*h*w >= alim (< 2^32)
-      um = alim <= 0 ? ok : (ok & gt_prod((uint32_t)(alim - 1) / (uint32_t)hw));
+      const uint32_t am1 = (uint32_t)(alim - 1);
+      um = alim <= 0 ? ok : (ok & gt_prod(lut_n ? div_capn(am1, hw, r_hw, qcap) : (int)(am1 / (uint32_t)hw)));
       ok = ok & ~um;
       if (any(ok)) {
         uint32_t ckey = (uint32_t)perm * cperm;
 #pragma unroll
-        for (int q = 2; q < NS; ++q) ckey += (uint32_t)digit[q] * (uint32_t)(plan.key_stride[q] / (uint64_t)nI);
+        for (int q = 2; q < NS; ++q) ckey += (uint32_t)digit[q] * cks[q];
         const M128 tab = s_rowx[__ldg(plan.cmask + ckey)];
         const int dmax = ts.dirty_max[p_out];
         mm = ok & (~s_gtx[dmax < 0 ? 0 : div_cap(dmax, ext_out, r_out)] | tab);
