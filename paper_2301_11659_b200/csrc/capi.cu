@@ -21,7 +21,7 @@ __global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_
                          int32_t* keys, uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                          unsigned long long* reason_hist, int mode);
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
-                             uint8_t* out);
+                             uint8_t* out, uint8_t* out1);
 __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
                               uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                               unsigned long long* reason_hist);
@@ -857,32 +857,37 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
     if (ctx->prof) ctx->prof_kernels += 1;
   }
   if (e.use_table) {
-    uint8_t* tab = (uint8_t*)atc_ctx_scratch(ctx, 17, e.table_bytes + 16);
+    // conv with nI <= 11: the pair screen reads the table as one bit word per
+    // (perm, h, w, r, s) over the values of tc_c (key stride 1), for output
+    // positions 0 and 1
+    const bool pairs = e.use_rows && ts_i32(ts) && conv_thresholds_ok(sp, e.plan, ts->nI) && ts->nI <= 11 &&
+                       e.plan.key_stride[1] == 1 && !pairs_disabled();
+    uint8_t* tab = (uint8_t*)atc_ctx_scratch(ctx, 17, e.table_bytes * (pairs ? 2 : 1) + 32);
     if (!tab) {
       atc_set_error(ctx, "scratch allocation failed (table)");
       return ATC_ERR_CUDA;
     }
+    uint8_t* tab1 = pairs ? tab + (e.table_bytes + 15) / 16 * 16 : nullptr;
     e.pt.table = tab;
     e.plan.pt = e.pt;
     k_pos0_table<<<(unsigned)std::min<uint64_t>((e.table_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16), 256, 0,
-                   st>>>(ts->view, sp, d_perms, n_perms, e.pt, tab);
+                   st>>>(ts->view, sp, d_perms, n_perms, e.pt, tab, tab1);
     if (ctx->prof) ctx->prof_kernels += 1;
-    // conv with nI <= 11: the pair screen reads the table as one bit word per
-    // (perm, h, w, r, s) over the values of tc_c (key stride 1)
-    if (e.use_rows && ts_i32(ts) && conv_thresholds_ok(sp, e.plan, ts->nI) && ts->nI <= 11 &&
-        e.plan.key_stride[1] == 1 && !pairs_disabled()) {
+    e.plan.cmask = e.plan.cmask1 = nullptr;
+    if (pairs) {
       const uint64_t words = e.table_bytes / (uint64_t)ts->nI;
-      uint32_t* cm = (uint32_t*)atc_ctx_scratch(ctx, 23, words * 4 + 16);
+      uint32_t* cm = (uint32_t*)atc_ctx_scratch(ctx, 23, words * 8 + 32);
       if (!cm) {
         atc_set_error(ctx, "scratch allocation failed (cmask)");
         return ATC_ERR_CUDA;
       }
-      k_cmask<<<(unsigned)std::min<uint64_t>((words + 255) / 256, (uint64_t)ctx->sm_count * 16), 256, 0, st>>>(
-          tab, words, ts->nI, cm);
+      uint32_t* cm1 = cm + (words + 3) / 4 * 4;
+      const unsigned g = (unsigned)std::min<uint64_t>((words + 255) / 256, (uint64_t)ctx->sm_count * 16);
+      k_cmask<<<g, 256, 0, st>>>(tab, words, ts->nI, cm);
+      k_cmask<<<g, 256, 0, st>>>(tab1, words, ts->nI, cm1);
       e.plan.cmask = cm;
-      if (ctx->prof) ctx->prof_kernels += 1;
-    } else {
-      e.plan.cmask = nullptr;
+      e.plan.cmask1 = cm1;
+      if (ctx->prof) ctx->prof_kernels += 2;
     }
   }
   return ATC_OK;

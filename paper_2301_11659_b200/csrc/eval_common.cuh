@@ -87,6 +87,7 @@ struct RowPlan {
   // conv (k_screen_conv_pairs): position-0 verdict bits over the nI values of tc_c
   // per (perm, h, w, r, s) key (k_cmask)
   const uint32_t* cmask;
+  const uint32_t* cmask1;  // the same at output position 1 (tc_ow >= 2), or null
 };
 
 enum : int32_t { kUndecided = -2 };

@@ -247,8 +247,10 @@ __global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need) {
   if (threadIdx.x == 0) need[e] = s_max;
 }
 
+// out1 (conv, optional): the same verdict at output position 1 for bindings with
+// tc_ow >= 2, i.e. output (b, q, y, x) = (0, 0, 0, 1): the input window shifted by one.
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
-                             uint8_t* out) {
+                             uint8_t* out, uint8_t* out1) {
   const uint64_t total = (uint64_t)n_perms * pt.per_perm;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t perm = e / pt.per_perm;
@@ -282,6 +284,7 @@ __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, 
       }
     } else {
       const int64_t c = v[0], h = v[1], w = v[2], r = v[3], s = v[4];
+      uint8_t res1 = 2;
       if (c >= 1 && r >= 1 && s >= 1 && h >= 0 && w >= 0) {
         const int64_t imax = ((c - 1) * h + (r - 1)) * w + (s - 1), wmax = c * r * s - 1;
         if (imax >= 0 && imax < lenA && wmax < lenB) {
@@ -291,9 +294,18 @@ __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, 
                 acc = dadd(acc, dmul(A[(z * h + u) * w + t], B[(z * r + u) * s + t]));
           res = mismatch(round_region(acc, f32), want, f32) ? 1 : 0;
         }
+        if (out1 && imax >= 0 && imax + 1 < lenA && wmax < lenB && ts.region_len[pC] > 1) {
+          double acc1 = 0.0;
+          for (int64_t z = 0; z < c; ++z)
+            for (int64_t u = 0; u < r; ++u)
+              for (int64_t t = 0; t < s; ++t)
+                acc1 = dadd(acc1, dmul(A[(z * h + u) * w + t + 1], B[(z * r + u) * s + t]));
+          res1 = mismatch(round_region(acc1, f32), ts.fin[ts.region_off[pC] + 1], f32) ? 1 : 0;
+        }
       } else {
         res = mismatch(round_region(0.0, f32), want, f32) ? 1 : 0;
       }
+      if (out1) out1[e] = res1;
     }
     out[e] = res;
   }

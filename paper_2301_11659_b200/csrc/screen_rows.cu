@@ -656,7 +656,9 @@ __global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const
         uint32_t ckey = (uint32_t)perm * cperm;
 #pragma unroll
         for (int q = 2; q < NS; ++q) ckey += (uint32_t)digit[q] * cks[q];
-        const M128 tab = s_rowx[__ldg(plan.cmask + ckey)];
+        M128 tab = s_rowx[__ldg(plan.cmask + ckey)];
+        // output position 1 is (0, 0, 0, 1) when ow >= 2: its tabulated verdict too
+        if (plan.cmask1 && cow >= 2) tab = tab | s_rowx[__ldg(plan.cmask1 + ckey)];
         const int dmax = ts.dirty_max[p_out];
         mm = ok & (~s_gtx[dmax < 0 ? 0 : div_cap(dmax, ext_out, r_out)] | tab);
         ok = ok & ~mm;
