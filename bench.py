@@ -284,21 +284,21 @@ def main():
     # ---- e2e through the C ABI with host buffers (pinned), uploads inside the region
     e2e_ms, h2d, d2h = _e2e(args, ctx, jobs, shards, stream, torch, dist)
 
-    # ---- roofline of the dominant kernel (K1: k_screen_conv_planes on the conv
+    # ---- roofline of the dominant kernel (K1: k_screen_conv_pairs on the conv
     # spaces, k_screen_rows on the gemm spaces), from the profiled step
     hbm, _, peak_kind = _peaks()
     ncu = _ncu_summary()
-    k1 = next((d for d in ncu if d["kernel"].startswith("k_screen_conv_planes")), {})
+    k1 = next((d for d in ncu if d["kernel"].startswith("k_screen_conv_pairs")), {})
     screen_s = prof.screen_ms / 1e3
     # algorithmic bytes: the recorded data the factorised screen must read.  Per
     # conv plane (permutation + digits 2..8; nI x nI bindings): the permutation
-    # (3 B), three region lengths (24 B), the output's dirty maximum (4 B) and nI
-    # position-0 verdict bytes.  Per gemm row (nI bindings): 3 + 24 + 4 + 1 B.
+    # (3 B), three region lengths (24 B), the output's dirty maximum (4 B) and the
+    # position-0/1 verdict words (8 B).  Per gemm row (nI bindings): 3 + 24 + 4 + 1 B.
     alg_bytes = 0.0
     for j, (b, e) in zip(jobs, shards):
         nI = len(j.ts.int_params)
         if j.spec.semantics == "conv2d":
-            alg_bytes += (e - b) / (nI * nI) * (31.0 + nI)
+            alg_bytes += (e - b) / (nI * nI) * 39.0
         else:
             alg_bytes += (e - b) / nI * 32.0
     achieved = alg_bytes / screen_s / 1e9 if screen_s > 0 else None
@@ -319,7 +319,7 @@ def main():
                      "traffic": k1.get("dram_read", 0) + k1.get("dram_write", 0) if k1 else None,
                      "traffic_launch": "ncu --set full of the conv_direct x conv2d launch (2.3e9 bindings; "
                                        "profiles/r1_ncu_summary.json)",
-                     "peak_kind": peak_kind, "kernel": "K1 screen (k_screen_conv_planes + k_screen_rows)",
+                     "peak_kind": peak_kind, "kernel": "K1 screen (k_screen_conv_pairs + k_screen_rows)",
                      "kernel_ms_per_step": prof.screen_ms,
                      "limiter": "instruction issue (integer ALU); operands are L1/L2 resident",
                      "issue_slots_busy_pct": k1.get("issue_slots_busy_pct"), "ipc_per_sm": k1.get("ipc_per_sm"),
