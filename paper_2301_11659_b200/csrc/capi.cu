@@ -651,10 +651,16 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     return ATC_ERR_CUDA;
   }
   cudaMemsetAsync(next_cnt, 0, 8, st);
-  k_confirm_t0<<<(unsigned)ctx->sm_count * 8, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys,
-                                                            next, next_cnt, ctx->mode);
-  k_confirm<<<(unsigned)ctx->sm_count * 8, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, next,
-                                                         next_cnt, 1, ctx->mode);
+  // grids bounded by the most work there can be (survivors <= bindings screened):
+  // small spaces launch a few CTAs instead of 8 per SM
+  const uint64_t max_surv = std::min<uint64_t>(n, surv_cap);
+  const unsigned g_t0 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 7) / 8, ctx->sm_count * 8));
+  const unsigned g_t1 = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>(max_surv * (uint64_t)std::max(ts->T - 1, 0), ctx->sm_count * 8));
+  k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, next, next_cnt,
+                                     ctx->mode);
+  k_confirm<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, next, next_cnt, 1,
+                                  ctx->mode);
   if (ctx->prof) {
     cudaEventRecord(e2.second, st);
     ctx->prof_confirm.push_back(e2);

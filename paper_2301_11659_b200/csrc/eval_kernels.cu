@@ -252,7 +252,19 @@ __global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need) {
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out, uint8_t* out1) {
   const uint64_t total = (uint64_t)n_perms * pt.per_perm;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+  // conv: thread i takes the entry whose (c, r, s) digits are its slowest-varying
+  // part, so the lanes of a warp share the dot-product trip counts c*r*s and
+  // differ in (h, w, permutation) only (no divergence in the loops below)
+  const uint64_t nI = (uint64_t)ts.nI, nI2 = nI * nI;
+  const uint64_t inner = nI2 * (uint64_t)n_perms;  // (h, w, perm) combinations
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t e = i;
+    if (sp.sem == ATC_SEM_CONV2D && pt.R == 5) {
+      const uint64_t crs = i / inner, hwp = i - crs * inner;  // crs = c + nI*(r + nI*s)
+      const uint64_t perm_i = hwp / nI2, hw = hwp - perm_i * nI2;
+      const uint64_t c = crs % nI, rs = crs / nI;               // rs = r + nI*s
+      e = perm_i * pt.per_perm + c + nI * hw + nI2 * nI * rs;   // key: c + nI*(h + nI*(w + nI*(r + nI*s)))
+    }
     const uint64_t perm = e / pt.per_perm;
     uint64_t rem = e - perm * pt.per_perm;
     int64_t v[kMaxPos0Roles];
@@ -287,20 +299,25 @@ __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, 
       uint8_t res1 = 2;
       if (c >= 1 && r >= 1 && s >= 1 && h >= 0 && w >= 0) {
         const int64_t imax = ((c - 1) * h + (r - 1)) * w + (s - 1), wmax = c * r * s - 1;
-        if (imax >= 0 && imax < lenA && wmax < lenB) {
-          for (int64_t z = 0; z < c; ++z)
-            for (int64_t u = 0; u < r; ++u)
-              for (int64_t t = 0; t < s; ++t)
-                acc = dadd(acc, dmul(A[(z * h + u) * w + t], B[(z * r + u) * s + t]));
-          res = mismatch(round_region(acc, f32), want, f32) ? 1 : 0;
-        }
-        if (out1 && imax >= 0 && imax + 1 < lenA && wmax < lenB && ts.region_len[pC] > 1) {
+        const bool ok0 = imax >= 0 && imax < lenA && wmax < lenB;
+        const bool ok1 = out1 && imax >= 0 && imax + 1 < lenA && wmax < lenB && ts.region_len[pC] > 1;
+        if (ok0 || ok1) {
+          // positions 0 and 1 in one pass (each its own reference-order sum); the
+          // indices are < len(region) < 2^31
           double acc1 = 0.0;
-          for (int64_t z = 0; z < c; ++z)
-            for (int64_t u = 0; u < r; ++u)
-              for (int64_t t = 0; t < s; ++t)
-                acc1 = dadd(acc1, dmul(A[(z * h + u) * w + t + 1], B[(z * r + u) * s + t]));
-          res1 = mismatch(round_region(acc1, f32), ts.fin[ts.region_off[pC] + 1], f32) ? 1 : 0;
+          const int ci = (int)c, hi = (int)h, wi = (int)w, ri = (int)r, si = (int)s;
+          for (int z = 0; z < ci; ++z)
+            for (int u = 0; u < ri; ++u) {
+              const double* a = A + (z * hi + u) * wi;
+              const double* b = B + (z * ri + u) * si;
+              for (int t = 0; t < si; ++t) {
+                const double bv = b[t];
+                if (ok0) acc = dadd(acc, dmul(a[t], bv));
+                if (ok1) acc1 = dadd(acc1, dmul(a[t + 1], bv));
+              }
+            }
+          if (ok0) res = mismatch(round_region(acc, f32), want, f32) ? 1 : 0;
+          if (ok1) res1 = mismatch(round_region(acc1, f32), ts.fin[ts.region_off[pC] + 1], f32) ? 1 : 0;
         }
       } else {
         res = mismatch(round_region(0.0, f32), want, f32) ? 1 : 0;
