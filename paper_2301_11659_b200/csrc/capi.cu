@@ -37,9 +37,9 @@ template <int SEM, int NS, bool I32, uint32_t Q0MASK>
 __global__ void k_screen_rows(TestsetView ts, SpecView sp, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
                               uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
                               unsigned long long* surv_cnt, unsigned long long* reason_hist);
-__global__ void k_confirm(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
-                          const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
-                          const uint32_t* sel, const unsigned long long* sel_cnt, int t_begin, int mode);
+__global__ void k_confirm_warp(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
+                               uint64_t surv_cap, int32_t* surv_keys, const uint32_t* sel,
+                               const unsigned long long* sel_cnt, int mode);
 __global__ void k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                              const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
                              uint32_t* next, unsigned long long* next_cnt, int mode);
@@ -656,11 +656,10 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
   const uint64_t max_surv = std::min<uint64_t>(n, surv_cap);
   const unsigned g_t0 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 7) / 8, ctx->sm_count * 8));
   const unsigned g_t1 = (unsigned)std::max<uint64_t>(
-      1, std::min<uint64_t>(max_surv * (uint64_t)std::max(ts->T - 1, 0), ctx->sm_count * 8));
+      1, std::min<uint64_t>((max_surv * (uint64_t)std::max(ts->T - 1, 0) + 7) / 8, ctx->sm_count * 8));
   k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, next, next_cnt,
                                      ctx->mode);
-  k_confirm<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, next, next_cnt, 1,
-                                  ctx->mode);
+  k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, next, next_cnt, ctx->mode);
   if (ctx->prof) {
     cudaEventRecord(e2.second, st);
     ctx->prof_confirm.push_back(e2);

@@ -449,13 +449,88 @@ __global__ void __launch_bounds__(256) k_screen_enum(TestsetView ts, SpecView sp
 
 
 // ------------------------------------------------------------------ K2 -------
-constexpr int kConfirmThreads = 256;
-constexpr int kStageDoubles = 6080;  // ~47.5 KB of operand staging per CTA (static smem cap 48 KB)
+
+// The verdict of binding `idx` at test t computed by one warp (every lane returns
+// it): the scalar checks of run_dispatch / bounds, then the dirty set and the
+// written outputs 32 at a time (lanes split the write set, __any_sync early exit).
+__device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const BindingSource& src, uint64_t idx, int t,
+                            int mode, int lane) {
+  int ptr_of[ATC_MAX_ARRAYS], int_of[ATC_MAX_SIZES];
+  decode_binding(src, sp, ts.nI, idx, ptr_of, int_of);
+  int64_t sz[ATC_MAX_SIZES];
+  for (int q = 0; q < sp.nS; ++q) sz[q] = ts.ints[t * ts.nI + int_of[q]];
+  int r = 0;
+  if (!ts.test_ok[t]) r = ATC_FAIL_TESTSET;
+  if (!r) r = extent_check(sp, sz, ptr_of, ts.region_len);
+  Dims d;
+  resolve_dims(sp, sz, d);
+  if (!r) r = ub_check(sp, d, ptr_of, ts.region_len);
+  if (r) return r;
+  const int pA = ptr_of[sp.arr_of_role[0]], pB = ptr_of[sp.arr_of_role[1]], pC = ptr_of[sp.arr_of_role[2]];
+  const int tpA = t * ts.nP + pA, tpB = t * ts.nP + pB, tpC = t * ts.nP + pC;
+  const double* __restrict__ A = ts.init + ts.region_off[tpA];
+  const double* __restrict__ B = ts.init + ts.region_off[tpB];
+  const double* __restrict__ F = ts.fin + ts.region_off[tpC];
+  const bool f32 = ts.is_f32[pC] != 0;
+  const int ndirty = ts.dirty_cnt[tpC];
+  const int32_t* dirty = ts.dirty_pos + ts.dirty_off[tpC];
+  bool bad = false;
+  if (sp.sem == ATC_SEM_GEMM) {
+    const bool row = sp.layout == ATC_LAYOUT_ROW;
+    const int m = (int)d.m, n = (int)d.n, k = (int)d.k, lda = (int)d.lda, ldb = (int)d.ldb, ldc = (int)d.ldc;
+    if (m < 1 || n < 1) {
+      bad = ndirty > 0;
+    } else {
+      for (int e = lane; e < ndirty && !bad; e += 32) bad = !gemm_written(row, __ldg(dirty + e), m, n, ldc);
+      bad = __any_sync(0xffffffffu, bad);
+      const bool overlap = row ? (ldc < n && m > 1) : (ldc < m && n > 1);
+      const int outs = m * n;
+      for (int o0 = 0; o0 < outs && !bad; o0 += 32) {
+        const int o = o0 + lane;
+        bool mm = false;
+        if (o < outs) {
+          const int i = o / n, j = o - (o / n) * n;
+          if (!overlap || gemm_last_writer(row, i, j, m, ldc)) {
+            const double* a = row ? A + i * lda : A + i;
+            const double* b = row ? B + j : B + j * ldb;
+            const int sa = row ? 1 : lda, sb = row ? ldb : 1;
+            mm = position_mismatch(
+                mode, k, __ldg(F + (row ? i * ldc + j : j * ldc + i)), f32,
+                [&] { return gemm_dot64(a, sa, b, sb, k); }, [&](float& S) { return gemm_dot32(a, sa, b, sb, k, S); });
+          }
+        }
+        bad = __any_sync(0xffffffffu, mm);
+      }
+    }
+  } else {
+    const int N = (int)d.cn, C = (int)d.cc, H = (int)d.ch, W = (int)d.cw, K = (int)d.ck, R = (int)d.cr,
+              S = (int)d.cs, OH = (int)d.coh, OW = (int)d.cow;
+    const int64_t wext = (int64_t)N * K * OH * OW;
+    bad = ts.dirty_max[tpC] >= wext;
+    for (int o0 = 0; o0 < (int)wext && !bad; o0 += 32) {
+      const int o = o0 + lane;
+      bool mm = false;
+      if (o < wext) {
+        int rem = o;
+        const int x = rem % OW; rem /= OW;
+        const int y = rem % OH; rem /= OH;
+        const int q = rem % K;
+        const int b = rem / K;
+        const double* in = A + ((b * C) * H + y) * W + x;
+        const double* wt = B + (q * C) * R * S;
+        mm = position_mismatch(
+            mode, C * R * S, __ldg(F + o), f32, [&] { return conv_dot64(in, wt, C, R, S, H, W); },
+            [&](float& Sa) { return conv_dot32(in, wt, C, R, S, H, W, Sa); });
+      }
+      bad = __any_sync(0xffffffffu, mm);
+    }
+  }
+  return bad ? ATC_FAIL_MISMATCH : 0;
+}
 
 // K2a: one WARP per survivor, test t = 0 only.  Most K1 survivors agree with the
-// user program at output position 0 but not elsewhere; a warp checks 32 output
-// positions per step (lanes split the write set, __any_sync early exit) and the
-// dirty set in parallel.  Survivors of t = 0 are appended to `next` for K2b.
+// user program at output positions 0 and 1 but not elsewhere.  Survivors of t = 0
+// are appended to `next` for K2b.
 __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src,
                                                     const uint64_t* surv, const unsigned long long* surv_cnt,
                                                     uint64_t surv_cap, int32_t* surv_keys, uint32_t* next,
@@ -465,77 +540,7 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
   if (cnt > surv_cap) cnt = surv_cap;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
   for (uint64_t si = (uint64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; si < cnt; si += warps) {
-    int ptr_of[ATC_MAX_ARRAYS], int_of[ATC_MAX_SIZES];
-    decode_binding(src, sp, ts.nI, surv[si], ptr_of, int_of);
-    int64_t sz[ATC_MAX_SIZES];
-    for (int q = 0; q < sp.nS; ++q) sz[q] = ts.ints[int_of[q]];
-    int r = 0;
-    if (!ts.test_ok[0]) r = ATC_FAIL_TESTSET;
-    if (!r) r = extent_check(sp, sz, ptr_of, ts.region_len);
-    Dims d;
-    resolve_dims(sp, sz, d);
-    if (!r) r = ub_check(sp, d, ptr_of, ts.region_len);
-    if (!r) {
-      const int pA = ptr_of[sp.arr_of_role[0]], pB = ptr_of[sp.arr_of_role[1]], pC = ptr_of[sp.arr_of_role[2]];
-      const double* __restrict__ A = ts.init + ts.region_off[pA];
-      const double* __restrict__ B = ts.init + ts.region_off[pB];
-      const double* __restrict__ F = ts.fin + ts.region_off[pC];
-      const bool f32 = ts.is_f32[pC] != 0;
-      const int ndirty = ts.dirty_cnt[pC];
-      const int32_t* dirty = ts.dirty_pos + ts.dirty_off[pC];
-      bool bad = false;
-      if (sp.sem == ATC_SEM_GEMM) {
-        const bool row = sp.layout == ATC_LAYOUT_ROW;
-        const int m = (int)d.m, n = (int)d.n, k = (int)d.k, lda = (int)d.lda, ldb = (int)d.ldb, ldc = (int)d.ldc;
-        if (m < 1 || n < 1) {
-          bad = ndirty > 0;
-        } else {
-          for (int e = lane; e < ndirty && !bad; e += 32) bad = !gemm_written(row, __ldg(dirty + e), m, n, ldc);
-          bad = __any_sync(0xffffffffu, bad);
-          const bool overlap = row ? (ldc < n && m > 1) : (ldc < m && n > 1);
-          const int outs = m * n;
-          for (int o0 = 0; o0 < outs && !bad; o0 += 32) {
-            const int o = o0 + lane;
-            bool mm = false;
-            if (o < outs) {
-              const int i = o / n, j = o - (o / n) * n;
-              if (!overlap || gemm_last_writer(row, i, j, m, ldc)) {
-                const double* a = row ? A + i * lda : A + i;
-                const double* b = row ? B + j : B + j * ldb;
-                const int sa = row ? 1 : lda, sb = row ? ldb : 1;
-                mm = position_mismatch(
-                    mode, k, __ldg(F + (row ? i * ldc + j : j * ldc + i)), f32,
-                    [&] { return gemm_dot64(a, sa, b, sb, k); }, [&](float& S) { return gemm_dot32(a, sa, b, sb, k, S); });
-              }
-            }
-            bad = __any_sync(0xffffffffu, mm);
-          }
-        }
-      } else {
-        const int N = (int)d.cn, C = (int)d.cc, H = (int)d.ch, W = (int)d.cw, K = (int)d.ck, R = (int)d.cr,
-                  S = (int)d.cs, OH = (int)d.coh, OW = (int)d.cow;
-        const int64_t wext = (int64_t)N * K * OH * OW;
-        bad = ts.dirty_max[pC] >= wext;
-        for (int o0 = 0; o0 < (int)wext && !bad; o0 += 32) {
-          const int o = o0 + lane;
-          bool mm = false;
-          if (o < wext) {
-            int rem = o;
-            const int x = rem % OW; rem /= OW;
-            const int y = rem % OH; rem /= OH;
-            const int q = rem % K;
-            const int b = rem / K;
-            const double* in = A + ((b * C) * H + y) * W + x;
-            const double* wt = B + (q * C) * R * S;
-            mm = position_mismatch(
-                mode, C * R * S, __ldg(F + o), f32, [&] { return conv_dot64(in, wt, C, R, S, H, W); },
-                [&](float& Sa) { return conv_dot32(in, wt, C, R, S, H, W, Sa); });
-          }
-          bad = __any_sync(0xffffffffu, mm);
-        }
-      }
-      if (bad) r = ATC_FAIL_MISMATCH;
-    }
+    const int r = warp_verdict(ts, sp, src, surv[si], 0, mode, lane);
     if (lane == 0) {
       if (r) {
         surv_keys[si] = fail_key(0, r);
@@ -548,166 +553,27 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
   }
 }
 
-// K2b (and the explicit-list confirm): one CTA per (survivor, t) for t >= t_begin.
-// With `sel`, the survivors are surv[sel[0..*sel_cnt)] (the t = 0 passers of K2a).
-__global__ void __launch_bounds__(kConfirmThreads) k_confirm(TestsetView ts, SpecView sp, BindingSource src,
-                                                             const uint64_t* surv,
-                                                             const unsigned long long* surv_cnt,
-                                                             uint64_t surv_cap, int32_t* surv_keys,
-                                                             const uint32_t* sel,
-                                                             const unsigned long long* sel_cnt, int t_begin,
-                                                             int mode) {
-  __shared__ double s_stage[kStageDoubles];
-  __shared__ int s_fail;
-  __shared__ int s_ptr[ATC_MAX_ARRAYS];
-  __shared__ int64_t s_sz[ATC_MAX_SIZES];
-  __shared__ int s_pre;  // result of the per-(b,t) scalar prologue
-  unsigned long long cnt = sel ? *sel_cnt : *surv_cnt;
+// K2b: one WARP per (t = 0 passer, t >= 1) — many (binding, t) items in flight
+// per SM, each with its own scalar prologue; an item is skipped once a lower t of
+// the same binding has failed (the atomicMin result is unchanged by the skip).
+__global__ void __launch_bounds__(256) k_confirm_warp(TestsetView ts, SpecView sp, BindingSource src,
+                                                      const uint64_t* surv, uint64_t surv_cap, int32_t* surv_keys,
+                                                      const uint32_t* sel, const unsigned long long* sel_cnt,
+                                                      int mode) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long cnt = *sel_cnt;
   if (cnt > surv_cap) cnt = surv_cap;
-  const int nt = ts.T - t_begin;
-  const uint64_t work = nt > 0 ? cnt * (uint64_t)nt : 0;
-  for (uint64_t w = blockIdx.x; w < work; w += gridDim.x) {
+  const int nt = ts.T - 1;
+  if (nt <= 0) return;
+  const uint64_t work = cnt * (uint64_t)nt;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t w = (uint64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; w < work; w += warps) {
     const uint64_t wi = w / nt;
-    const uint64_t si = sel ? sel[wi] : wi;
-    const int t = t_begin + (int)(w - wi * nt);
-    const uint64_t idx = surv[si];
-    if (threadIdx.x == 0) {
-      int ptr_of[ATC_MAX_ARRAYS], int_of[ATC_MAX_SIZES];
-      decode_binding(src, sp, ts.nI, idx, ptr_of, int_of);
-      for (int a = 0; a < sp.nA; ++a) s_ptr[a] = ptr_of[a];
-      for (int q = 0; q < sp.nS; ++q) s_sz[q] = ts.ints[t * ts.nI + int_of[q]];
-      int r = 0;
-      if (!ts.test_ok[t]) r = ATC_FAIL_TESTSET;
-      if (!r) r = extent_check(sp, s_sz, ptr_of, ts.region_len);
-      if (!r) {
-        Dims d;
-        resolve_dims(sp, s_sz, d);
-        r = ub_check(sp, d, ptr_of, ts.region_len);
-      }
-      s_pre = r;
-      s_fail = 0;
-    }
-    __syncthreads();
-    int fail = s_pre;
-    if (!fail) {
-      Dims d;
-      resolve_dims(sp, s_sz, d);
-      const int pA = s_ptr[sp.arr_of_role[0]], pB = s_ptr[sp.arr_of_role[1]], pC = s_ptr[sp.arr_of_role[2]];
-      const int tpA = t * ts.nP + pA, tpB = t * ts.nP + pB, tpC = t * ts.nP + pC;
-      const double* gA = ts.init + ts.region_off[tpA];
-      const double* gB = ts.init + ts.region_off[tpB];
-      const double* F = ts.fin + ts.region_off[tpC];
-      const bool f32 = ts.is_f32[pC] != 0;
-      const int ndirty = ts.dirty_cnt[tpC];
-      const int32_t* dirty = ts.dirty_pos + ts.dirty_off[tpC];
-      if (sp.sem == ATC_SEM_GEMM) {
-        const bool row = sp.layout == ATC_LAYOUT_ROW;
-        const int m = (int)d.m, n = (int)d.n, k = (int)d.k;
-        const int lda = (int)d.lda, ldb = (int)d.ldb, ldc = (int)d.ldc;
-        // operand footprints (prefix lengths) for shared-memory staging
-        int alen = 0, blen = 0;
-        if (m >= 1 && n >= 1 && k >= 1) {
-          alen = (row ? (m - 1) * lda + k : (k - 1) * lda + m);
-          blen = (row ? (k - 1) * ldb + n : (n - 1) * ldb + k);
-        }
-        const bool staged = alen + blen <= kStageDoubles;
-        const double* A = gA;
-        const double* B = gB;
-        if (staged) {
-          // coalesced 16-byte loads when aligned (regions are 256-B aligned)
-          for (int e = threadIdx.x * 2; e < alen; e += kConfirmThreads * 2) {
-            if (e + 1 < alen) {
-              double2 v = __ldg(reinterpret_cast<const double2*>(gA + e));
-              s_stage[e] = v.x;
-              s_stage[e + 1] = v.y;
-            } else {
-              s_stage[e] = __ldg(gA + e);
-            }
-          }
-          for (int e = threadIdx.x * 2; e < blen; e += kConfirmThreads * 2) {
-            if (e + 1 < blen) {
-              double2 v = __ldg(reinterpret_cast<const double2*>(gB + e));
-              s_stage[alen + e] = v.x;
-              s_stage[alen + e + 1] = v.y;
-            } else {
-              s_stage[alen + e] = __ldg(gB + e);
-            }
-          }
-          A = s_stage;
-          B = s_stage + alen;
-        }
-        // dirty subset check, split across the CTA
-        if (m < 1 || n < 1) {
-          if (ndirty && threadIdx.x == 0) s_fail = ATC_FAIL_MISMATCH;
-        } else {
-          for (int e = threadIdx.x; e < ndirty; e += kConfirmThreads)
-            if (!gemm_written(row, __ldg(dirty + e), m, n, ldc)) s_fail = ATC_FAIL_MISMATCH;
-        }
-        __syncthreads();
-        if (!s_fail && m >= 1 && n >= 1) {
-          const bool overlap = row ? (ldc < n && m > 1) : (ldc < m && n > 1);
-          const int outs = m * n;
-          for (int o0 = 0; o0 < outs; o0 += kConfirmThreads) {
-            const int o = o0 + threadIdx.x;
-            if (o < outs) {
-              const int i = o / n, j = o - (o / n) * n;
-              if (!overlap || gemm_last_writer(row, i, j, m, ldc)) {
-                const double* a = row ? A + i * lda : A + i;
-                const double* b = row ? B + j : B + j * ldb;
-                const int sa = row ? 1 : lda, sb = row ? ldb : 1;
-                const int pos = row ? i * ldc + j : j * ldc + i;
-                if (position_mismatch(
-                        mode, k, __ldg(F + pos), f32, [&] { return gemm_dot64(a, sa, b, sb, k); },
-                        [&](float& Sa) { return gemm_dot32(a, sa, b, sb, k, Sa); }))
-                  s_fail = ATC_FAIL_MISMATCH;
-              }
-            }
-            // block-wide early exit on the first mismatching chunk
-            if (__syncthreads_or(s_fail != 0)) break;
-          }
-        }
-      } else {
-        const int N = (int)d.cn, C = (int)d.cc, H = (int)d.ch, W = (int)d.cw, K = (int)d.ck,
-                  R = (int)d.cr, S = (int)d.cs, OH = (int)d.coh, OW = (int)d.cow;
-        const int64_t wext = (int64_t)N * K * OH * OW;
-        if (ts.dirty_max[tpC] >= wext) {
-          if (threadIdx.x == 0) s_fail = ATC_FAIL_MISMATCH;
-        }
-        __syncthreads();
-        if (!s_fail) {
-          const int wlen = K * C * R * S;
-          const bool staged = wlen <= kStageDoubles;
-          const double* Wt = gB;
-          if (staged) {
-            for (int e = threadIdx.x; e < wlen; e += kConfirmThreads) s_stage[e] = __ldg(gB + e);
-            __syncthreads();
-            Wt = s_stage;
-          }
-          const int outs = (int)wext;
-          for (int o0 = 0; o0 < outs; o0 += kConfirmThreads) {
-            const int o = o0 + threadIdx.x;
-            if (o < outs) {
-              int rem = o;
-              const int x = rem % OW; rem /= OW;
-              const int y = rem % OH; rem /= OH;
-              const int q = rem % K;
-              const int b = rem / K;
-              const double* in = gA + ((b * C) * H + y) * W + x;
-              const double* wt = Wt + (q * C) * R * S;
-              if (position_mismatch(
-                      mode, C * R * S, __ldg(F + o), f32, [&] { return conv_dot64(in, wt, C, R, S, H, W); },
-                      [&](float& Sa) { return conv_dot32(in, wt, C, R, S, H, W, Sa); }))
-                s_fail = ATC_FAIL_MISMATCH;
-            }
-            if (__syncthreads_or(s_fail != 0)) break;
-          }
-        }
-      }
-      __syncthreads();
-      fail = s_fail;
-    }
-    if (threadIdx.x == 0 && fail) atomicMin(&surv_keys[si], fail_key(t, fail));
-    __syncthreads();
+    const uint32_t si = sel[wi];
+    const int t = 1 + (int)(w - wi * nt);
+    if (*(volatile int32_t*)(surv_keys + si) < fail_key(t, 0)) continue;  // failed at a lower t already
+    const int r = warp_verdict(ts, sp, src, surv[si], t, mode, lane);
+    if (lane == 0 && r) atomicMin(&surv_keys[si], fail_key(t, r));
   }
 }
 
