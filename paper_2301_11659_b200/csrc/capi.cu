@@ -86,6 +86,7 @@ bool atc_cuda_ok(atc_ctx* ctx, cudaError_t e, const char* what) {
 }
 
 void* atc_ctx_scratch(atc_ctx* ctx, int slot, size_t bytes) {
+  slot += ctx->slot_base;
   if (slot < 0 || slot >= atc_ctx::kSlots) {
     atc_set_error(ctx, "internal: scratch slot %d out of range", slot);
     return nullptr;
@@ -248,7 +249,10 @@ atc_ctx* atc_create(int device) {
   cudaSetDevice(device);
   if (!atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
       !atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
-      !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->free_ev, cudaEventDisableTiming), "cudaEventCreate"))
+      !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->free_ev, cudaEventDisableTiming), "cudaEventCreate") ||
+      !atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
+      !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming), "cudaEventCreate") ||
+      !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming), "cudaEventCreate"))
     ctx->broken = true;
   ctx->own_stream = ctx->stream;
   return ctx;
@@ -269,6 +273,9 @@ void atc_destroy(atc_ctx* ctx) {
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->free_ev) cudaEventDestroy(ctx->free_ev);
+    if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   }
   delete ctx;
 }
@@ -1020,34 +1027,57 @@ constexpr uint64_t kBatchStride = 2 + kResultPrefix;  // count, passing count, p
 
 size_t batch_res_words(int n) { return (size_t)n * (kBatchStride + 8); }
 
+// Two concurrent branches: conv spaces (large K1 launches) on the caller's
+// stream, gemm spaces (chains of small latency-bound kernels) on the side stream
+// with their own scratch (slot + 32); they fork from and join back into `st`, so
+// a captured graph has the same two branches.
 int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_uploads) {
   const uint64_t chunk_cap = kEnumChunkCap;
-  uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
-  int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, chunk_cap * 4);
-  unsigned long long* cnt = (unsigned long long*)atc_ctx_scratch(ctx, 3, 64);
-  if (!surv || !skeys || !cnt) {
-    atc_set_error(ctx, "scratch allocation failed");
-    return ATC_ERR_CUDA;
-  }
   unsigned long long* hist = reinterpret_cast<unsigned long long*>(b->res + (size_t)b->n * kBatchStride);
   cudaMemsetAsync(b->res, 0, batch_res_words(b->n) * 8, st);
-  for (int j = 0; j < b->n; ++j) {
+  bool has_main = false, has_side = false;
+  for (int j = 0; j < b->n; ++j)
+    if (b->batched[j]) (b->plans[j].sp.sem == ATC_SEM_CONV2D ? has_main : has_side) = true;
+  const bool split = has_main && has_side;
+  if (split) {
+    cudaEventRecord(ctx->fork_ev, st);
+    cudaStreamWaitEvent(ctx->side_stream, ctx->fork_ev, 0);
+  }
+  int rc = ATC_OK;
+  for (int j = 0; j < b->n && rc == ATC_OK; ++j) {
     if (!b->batched[j]) continue;
     atc_enum_job& job = b->jobs[j];
     EnumPlan& e = b->plans[j];
-    if (wait_uploads) ts_wait(job.ts, st);  // job j starts as soon as its own test sets are resident
-    int rc = enqueue_tables(ctx, e, job.ts, job.perms, job.n_perms, &b->d_perms[j], st);
-    if (rc) return rc;
+    const bool side = split && e.sp.sem != ATC_SEM_CONV2D;
+    cudaStream_t js = side ? ctx->side_stream : st;
+    ctx->slot_base = side ? 32 : 0;
+    uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
+    int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, chunk_cap * 4);
+    unsigned long long* cnt = (unsigned long long*)atc_ctx_scratch(ctx, 3, 64);
+    if (!surv || !skeys || !cnt) {
+      atc_set_error(ctx, "scratch allocation failed");
+      rc = ATC_ERR_CUDA;
+      break;
+    }
+    if (wait_uploads) ts_wait(job.ts, js);  // job j starts as soon as its own test sets are resident
+    rc = enqueue_tables(ctx, e, job.ts, job.perms, job.n_perms, &b->d_perms[j], js);
+    if (rc) break;
     if (job.end > job.begin) {
       BindingSource src{nullptr, nullptr, b->d_perms[j], e.size_maps, job.begin, 1};
       rc = run_eval(ctx, e.sp, job.ts, src, job.end - job.begin, nullptr, surv, chunk_cap, cnt, skeys,
-                    hist + 8 * j, st, e.use_table ? &e.pt : nullptr, e.use_rows ? &e.plan : nullptr);
-      if (rc) return rc;
-      k_finalize<<<64, 256, 0, st>>>(surv, cnt, chunk_cap, skeys, job.begin, b->res + (size_t)j * kBatchStride,
+                    hist + 8 * j, js, e.use_table ? &e.pt : nullptr, e.use_rows ? &e.plan : nullptr);
+      if (rc) break;
+      k_finalize<<<64, 256, 0, js>>>(surv, cnt, chunk_cap, skeys, job.begin, b->res + (size_t)j * kBatchStride,
                                      kResultPrefix, hist + 8 * j);
       if (ctx->prof) ctx->prof_kernels += 1;
     }
   }
+  ctx->slot_base = 0;
+  if (split) {
+    cudaEventRecord(ctx->join_ev, ctx->side_stream);
+    cudaStreamWaitEvent(st, ctx->join_ev, 0);
+  }
+  if (rc) return rc;
   if (!atc_cuda_ok(ctx, cudaMemcpyAsync(b->h_res, b->res, batch_res_words(b->n) * 8, cudaMemcpyDeviceToHost, st),
                    "D2H results"))
     return ATC_ERR_CUDA;

@@ -14,7 +14,12 @@ struct atc_ctx {
   std::string err;
   cudaStream_t stream = nullptr;
   // reusable device scratch, grown on demand (slot ids are per call site)
-  static constexpr int kSlots = 32;
+  static constexpr int kSlots = 64;
+  // sweeps run gemm and conv spaces on two concurrent branches; the second
+  // branch's evaluator scratch lives at slot + 32 (set while enqueueing it)
+  int slot_base = 0;
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   void* scratch[kSlots] = {};
   size_t scratch_bytes[kSlots] = {};
   void* pinned[4] = {};
