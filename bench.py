@@ -282,7 +282,8 @@ def main():
             summary[f"{j.stem}x{j.spec_name}"] = pl[:4]
 
     # ---- e2e through the C ABI with host buffers (pinned), uploads inside the region
-    e2e_ms, h2d, d2h = _e2e(args, ctx, jobs, shards, stream, torch, dist)
+    e2e_ms, h2d, d2h = _e2e(args, ctx, jobs, shards, stream, torch, dist, seeded=True)
+    e2e_full_ms, h2d_full, _ = _e2e(args, ctx, jobs, shards, stream, torch, dist, seeded=False)
 
     # ---- roofline of the dominant kernel (K1: k_screen_conv_pairs on the conv
     # spaces, k_screen_rows on the gemm spaces), from the profiled step
@@ -310,7 +311,13 @@ def main():
         "config": _config(args, jobs),
         "correct": correct, "passing_sample": summary,
         "e2e": {"value": bindings / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "inputs": "per program: the P2 tests' Rng seeds + region stream positions + int values + the "
+                          "original runs' final-minus-init entries (atc_testsets_upload_seeded; probe images "
+                          "generated on the GPU)",
+                "full_regions": {"value": bindings / (e2e_full_ms / 1e3), "ms_per_step": e2e_full_ms,
+                                 "h2d_bytes_per_step": h2d_full,
+                                 "inputs": "every 65,536-element init and final region (atc_testsets_upload_async)"}},
         # every library kernel of one step (counted by the profiled step) x timed steps;
         # the timed steps replay them as one CUDA graph per step
         "gpu_launches": int(prof.kernels) * args.steps,
@@ -352,44 +359,57 @@ def main():
         dist.destroy_process_group()
 
 
-def _e2e(args, ctx, jobs, shards, stream, torch, dist):
-    """Same metric through atc_testsets_upload_async + atc_eval_enumerated_many from pinned
-    host buffers, one upload per program per step (copies inside the region)."""
+def _e2e(args, ctx, jobs, shards, stream, torch, dist, seeded=True):
+    """Same metric through the C ABI from pinned host buffers, every program's test
+    sets uploaded every step (copies inside the timed region), then
+    atc_eval_enumerated_many.  seeded: atc_testsets_upload_seeded (the tests' Rng
+    seeds + stream positions + the original runs' final-minus-init entries; the
+    probe images are generated on the GPU); else atc_testsets_upload_async with the
+    full 65,536-element regions."""
     from paper_2301_11659_b200 import _lib
 
     L = _lib.lib()
-    progs = {}
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    progs, h2d = {}, 0
     for j in jobs:
-        if j.stem not in progs:
-            ts = j.ts
-            # one pinned block per program for the initial regions and one for the
-            # final regions, (t, pointer) back to back: one DMA each
-            nP = len(ts.ptrs)
-            lens = [len(ts.init[0][p]) for p in range(nP)]
-            total = ts.n_tests * sum(lens)
-            blk_i = torch.empty(total, dtype=torch.float64, pin_memory=True).numpy()
-            blk_f = torch.zeros(total, dtype=torch.float64, pin_memory=True).numpy()
-            pinned, o = [], 0
-            for t in range(ts.n_tests):
-                row_i, row_f = [], []
-                for p in range(nP):
-                    a, f = blk_i[o:o + lens[p]], blk_f[o:o + lens[p]]
-                    a[:] = ts.init[t][p]
-                    row_i.append(a)
-                    if ts.final[t] is not None:
-                        f[:] = ts.final[t][p]
-                        row_f.append(f)
-                    else:
-                        row_f.append(None)
-                    o += lens[p]
-                pinned.append((row_i, row_f))
-            from paper_2301_11659_b200.evaluator import RecordedTestsets
+        if j.stem in progs:
+            continue
+        ts = j.ts
+        if seeded:
+            s, keep = ts.seeded_struct()
+            keep = [pin(a) for a in keep]  # same order as the struct's fields below
+            (s.int_values, s.ptr_is_f32, s.region_len, s.test_ok, s.stream_seed, s.stream_skip, s.diff_off,
+             s.diff_pos, s.diff_val) = [a.ctypes.data for a in keep]
+            progs[j.stem] = (s, keep, L.atc_testsets_upload_seeded)
+            h2d += sum(a.nbytes for a in keep)
+            continue
+        # one pinned block per program for the initial regions and one for the
+        # final regions, (t, pointer) back to back: one DMA each
+        nP = len(ts.ptrs)
+        lens = [len(ts.init[0][p]) for p in range(nP)]
+        total = ts.n_tests * sum(lens)
+        blk_i = torch.empty(total, dtype=torch.float64, pin_memory=True).numpy()
+        blk_f = torch.zeros(total, dtype=torch.float64, pin_memory=True).numpy()
+        pinned, o = [], 0
+        for t in range(ts.n_tests):
+            row_i, row_f = [], []
+            for p in range(nP):
+                a, f = blk_i[o:o + lens[p]], blk_f[o:o + lens[p]]
+                a[:] = ts.init[t][p]
+                row_i.append(a)
+                if ts.final[t] is not None:
+                    f[:] = ts.final[t][p]
+                    row_f.append(f)
+                else:
+                    row_f.append(None)
+                o += lens[p]
+            pinned.append((row_i, row_f))
+        from paper_2301_11659_b200.evaluator import RecordedTestsets
 
-            pts = RecordedTestsets(ts.params, ts.ints, [r[0] for r in pinned],
-                                   [None if any(x is None for x in r[1]) else r[1] for r in pinned], ts.test_ok)
-            progs[j.stem] = pts.c_struct()
-    h2d = 0
-    for s, _ in progs.values():
+        pts = RecordedTestsets(ts.params, ts.ints, [r[0] for r in pinned],
+                               [None if any(x is None for x in r[1]) else r[1] for r in pinned], ts.test_ok)
+        s, keep = pts.c_struct()
+        progs[j.stem] = (s, keep, L.atc_testsets_upload_async)
         h2d += 2 * s.n_tests * s.n_ptrs * 65536 * 8
     d2h = 0
     static = [(j.spec.to_desc(), np.ascontiguousarray(j.space.perms, dtype=np.uint8), np.zeros(1 << 16, np.uint64))
@@ -399,10 +419,10 @@ def _e2e(args, ctx, jobs, shards, stream, torch, dist):
         nonlocal d2h
         d2h = 0
         handles = {}
-        for stem, (s, _) in progs.items():
+        for stem, (s, _, upload) in progs.items():
             out = C.c_void_p()
             # copy stream; each space's kernels wait only for their own program's upload
-            _lib.check(ctx.handle, L.atc_testsets_upload_async(ctx.handle, C.byref(s), C.byref(out)))
+            _lib.check(ctx.handle, upload(ctx.handle, C.byref(s), C.byref(out)))
             handles[stem] = out.value
         arr = (_lib.EnumJob * len(jobs))()
         for i, (j, (b, e)) in enumerate(zip(jobs, shards)):

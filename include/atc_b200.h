@@ -146,6 +146,31 @@ int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h);
  * evaluation using the handle has returned (or the handle is freed). */
 int atc_testsets_upload_async(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out);
 
+/* The same test sets described the way verify_rewrite builds them: test t's
+ * probe image comes from one liftc::Rng stream (rewriter.cpp:236-245; Rng =
+ * std::mt19937_64, rng.hpp:13-48) — region p holds uniform_real(-1, 1) draws
+ * (f32-rounded for *f32 pointers) starting at stream position stream_skip[t][p]
+ * (analysis.cpp:73-98) — and the original run's final images differ from it only
+ * at the listed positions.  The regions are generated on the GPU (no region
+ * crosses PCIe); otherwise equivalent to atc_testsets_upload_async. */
+typedef struct {
+  int32_t n_tests, n_ints, n_ptrs;
+  const int64_t* int_values;   /* [T][n_ints]                                         */
+  const int32_t* ptr_is_f32;   /* [n_ptrs]                                            */
+  const int64_t* region_len;   /* [n_ptrs]                                            */
+  const int32_t* test_ok;      /* [T]                                                 */
+  const uint64_t* stream_seed; /* [T]: Rng seed of test t                             */
+  const uint64_t* stream_skip; /* [T][n_ptrs]: draws before region p's first element  */
+  const int64_t* diff_off;     /* [T*n_ptrs + 1]: entries of (t, p) = [off[i], off[i+1]) */
+  const int32_t* diff_pos;     /* final-minus-init positions                           */
+  const double* diff_val;      /* final values there                                  */
+} atc_seeded_testsets;
+int atc_testsets_upload_seeded(atc_ctx* ctx, const atc_seeded_testsets* ts, atc_testset_handle** out);
+
+/* Copies a handle's regions back ((t, pointer) regions back to back, unpadded;
+ * either pointer may be NULL) — for checks and debugging. */
+int atc_testsets_download(atc_ctx* ctx, const atc_testset_handle* h, double* init, double* final_);
+
 /* Explicit candidate list (ranked order).  arr_map[b*n_arrays + a] = user pointer
  * index bound to API array a; size_map[b*n_sizes + q] = user int index bound to
  * API size param q.  Outputs (host): fail_t[b] = first failing test or -1,

@@ -71,6 +71,25 @@ class Testsets(C.Structure):
     ]
 
 
+class SeededTestsets(C.Structure):
+    """atc_seeded_testsets (include/atc_b200.h)."""
+
+    _fields_ = [
+        ("n_tests", C.c_int32),
+        ("n_ints", C.c_int32),
+        ("n_ptrs", C.c_int32),
+        ("int_values", C.c_void_p),
+        ("ptr_is_f32", C.c_void_p),
+        ("region_len", C.c_void_p),
+        ("test_ok", C.c_void_p),
+        ("stream_seed", C.c_void_p),
+        ("stream_skip", C.c_void_p),
+        ("diff_off", C.c_void_p),
+        ("diff_pos", C.c_void_p),
+        ("diff_val", C.c_void_p),
+    ]
+
+
 class Profile(C.Structure):
     _fields_ = [
         ("screen_ms", C.c_double),
@@ -114,6 +133,8 @@ _SIGS = [
     ("atc_testsets_upload", C.c_int, [_P, C.POINTER(Testsets), C.POINTER(_P)]),
     ("atc_testsets_free", C.c_int, [_P, _P]),
     ("atc_testsets_upload_async", C.c_int, [_P, C.POINTER(Testsets), C.POINTER(_P)]),
+    ("atc_testsets_upload_seeded", C.c_int, [_P, C.POINTER(SeededTestsets), C.POINTER(_P)]),
+    ("atc_testsets_download", C.c_int, [_P, _P, _P, _P]),
     ("atc_eval_bindings", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, C.c_int64, C.c_int32, _P, _P,
                                     C.POINTER(C.c_int64)]),
     ("atc_eval_bindings_device", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, C.c_int64, C.c_int32, _P, _P, _P]),

@@ -15,6 +15,10 @@
 #include "eval_common.cuh"
 
 namespace atc {
+__global__ void k_probe_regions(int T, int nP, const uint64_t* seeds, const uint64_t* skips, const int64_t* region_len,
+                                const int32_t* is_f32, const int64_t* region_off, double* init, double* fin);
+__global__ void k_apply_diffs(int nP, const int64_t* region_len, const int64_t* region_off, const int64_t* diff_off,
+                              const int32_t* diff_pos, const double* diff_val, double* fin);
 __global__ void k_build_dirty(TestsetView ts, int32_t* dirty_pos, int32_t* dirty_cnt, int32_t* dirty_max);
 
 __global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, int budget,
@@ -248,12 +252,15 @@ atc_ctx* atc_create(int device) {
   }
   cudaSetDevice(device);
   if (!atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
-      !atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
+
       !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->free_ev, cudaEventDisableTiming), "cudaEventCreate") ||
       !atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
       !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming), "cudaEventCreate") ||
       !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming), "cudaEventCreate"))
     ctx->broken = true;
+  for (auto& cs : ctx->copy_stream)
+    if (!ctx->broken && !atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate"))
+      ctx->broken = true;
   ctx->own_stream = ctx->stream;
   return ctx;
 }
@@ -271,7 +278,8 @@ void atc_destroy(atc_ctx* ctx) {
     for (auto& e : ctx->prof_screen) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
     for (auto& e : ctx->prof_confirm) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
-    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    for (auto& cs : ctx->copy_stream)
+      if (cs) cudaStreamDestroy(cs);
     if (ctx->free_ev) cudaEventDestroy(ctx->free_ev);
     if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
@@ -335,10 +343,26 @@ int atc_profile_read(atc_ctx* ctx, atc_profile* out) {
 
 }  // extern "C"
 
-static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out, bool sync) {
+// Both upload forms: full host regions (`ts`) or seeds + final-minus-init entries
+// (`sd`, regions generated on the device); the common header fields are equal.
+static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_seeded_testsets* sd,
+                           atc_testset_handle** out, bool sync) {
   if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
-  if (!ts || !out || ts->n_tests < 1 || ts->n_tests > kMaxT || ts->n_ints < 1 || ts->n_ints > kMaxInts ||
-      ts->n_ptrs < 1 || ts->n_ptrs > kMaxPtrs) {
+  atc_testsets hdr{};
+  if (ts_full) hdr = *ts_full;
+  if (sd) {
+    hdr.n_tests = sd->n_tests;
+    hdr.n_ints = sd->n_ints;
+    hdr.n_ptrs = sd->n_ptrs;
+    hdr.int_values = sd->int_values;
+    hdr.ptr_is_f32 = sd->ptr_is_f32;
+    hdr.region_len = sd->region_len;
+    hdr.test_ok = sd->test_ok;
+  }
+  const atc_testsets* ts = &hdr;
+  if ((!ts_full && !sd) || !out || ts->n_tests < 1 || ts->n_tests > kMaxT || ts->n_ints < 1 ||
+      ts->n_ints > kMaxInts || ts->n_ptrs < 1 || ts->n_ptrs > kMaxPtrs || !ts->int_values || !ts->region_len ||
+      !ts->ptr_is_f32 || (sd && (!sd->stream_seed || !sd->stream_skip || !sd->diff_off))) {
     atc_set_error(ctx, "malformed test sets");
     return ATC_ERR_ARG;
   }
@@ -388,10 +412,12 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_han
   }
   // copies and the dirty-list kernel go to the copy stream, after any pool
   // memory freed by earlier handles is no longer read by the compute stream
-  cudaStream_t st = ctx->copy_stream;
-  if (ctx->free_pending) {
+  const int cs = ctx->copy_next;
+  ctx->copy_next = (cs + 1) % atc_ctx::kCopyStreams;
+  cudaStream_t st = ctx->copy_stream[cs];
+  if (ctx->free_pending & (1u << cs)) {
     cudaStreamWaitEvent(st, ctx->free_ev, 0);
-    ctx->free_pending = false;
+    ctx->free_pending &= ~(1u << cs);
   }
   bool ok = true;
   // host regions that lie back to back in the same order as the device pool are
@@ -415,7 +441,7 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_han
     r.dst = dst;
     r.bytes = bytes;
   };
-  for (int t = 0; t < T && ok; ++t)
+  for (int t = 0; t < T && ok && ts_full; ++t)
     for (int p = 0; p < nP && ok; ++p) {
       const size_t i = (size_t)t * nP + p;
       const size_t bytes = (size_t)ts->region_len[p] * 8;
@@ -437,6 +463,36 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_han
     }
   flush(run_i, init, "H2D init");
   flush(run_f, fin, "H2D final");
+  if (sd && ok) {
+    // regions from the tests' mt19937_64 streams (k_probe_regions), then the
+    // final-minus-init entries scattered into the final images (k_apply_diffs)
+    const int64_t nd = sd->diff_off[(size_t)T * nP];
+    uint64_t* seeds = (uint64_t*)dmalloc((size_t)T * 8);
+    uint64_t* skips = (uint64_t*)dmalloc((size_t)T * nP * 8);
+    int64_t* doffs = (int64_t*)dmalloc(((size_t)T * nP + 1) * 8);
+    int32_t* dps = (int32_t*)dmalloc((size_t)std::max<int64_t>(nd, 1) * 4);
+    double* dvs = (double*)dmalloc((size_t)std::max<int64_t>(nd, 1) * 8);
+    ok = seeds && skips && doffs && dps && dvs;
+    if (!ok) atc_set_error(ctx, "device allocation failed (seeded test sets)");
+    for (int64_t i = 0; ok && i < nd; ++i)
+      if (sd->diff_pos[i] < 0) {
+        atc_set_error(ctx, "negative final-minus-init position");
+        ok = false;
+      }
+    ok = ok && atc_cuda_ok(ctx, cudaMemcpyAsync(seeds, sd->stream_seed, (size_t)T * 8, cudaMemcpyHostToDevice, st), "H2D") &&
+         atc_cuda_ok(ctx, cudaMemcpyAsync(skips, sd->stream_skip, (size_t)T * nP * 8, cudaMemcpyHostToDevice, st), "H2D") &&
+         atc_cuda_ok(ctx, cudaMemcpyAsync(doffs, sd->diff_off, ((size_t)T * nP + 1) * 8, cudaMemcpyHostToDevice, st), "H2D") &&
+         (nd == 0 || (atc_cuda_ok(ctx, cudaMemcpyAsync(dps, sd->diff_pos, (size_t)nd * 4, cudaMemcpyHostToDevice, st), "H2D") &&
+                      atc_cuda_ok(ctx, cudaMemcpyAsync(dvs, sd->diff_val, (size_t)nd * 8, cudaMemcpyHostToDevice, st), "H2D")));
+    if (ok) {
+      ok = atc_cuda_ok(ctx, cudaMemcpyAsync(rlen, ts->region_len, nP * 8, cudaMemcpyHostToDevice, st), "H2D") &&
+           atc_cuda_ok(ctx, cudaMemcpyAsync(isf, ts->ptr_is_f32, nP * 4, cudaMemcpyHostToDevice, st), "H2D") &&
+           atc_cuda_ok(ctx, cudaMemcpyAsync(roff, off.data(), (size_t)T * nP * 8, cudaMemcpyHostToDevice, st), "H2D");
+      k_probe_regions<<<T, 320, 0, st>>>(T, nP, seeds, skips, rlen, isf, roff, init, fin);
+      k_apply_diffs<<<(unsigned)(T * nP), 256, 0, st>>>(nP, rlen, roff, doffs, dps, dvs, fin);
+      ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_probe_regions");
+    }
+  }
   std::vector<int32_t> tok_h(T, 1);
   if (ts->test_ok)
     for (int t = 0; t < T; ++t) tok_h[t] = ts->test_ok[t] ? 1 : 0;
@@ -485,11 +541,39 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_han
 extern "C" {
 
 int atc_testsets_upload(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out) {
-  return testsets_upload(ctx, ts, out, true);
+  return testsets_upload(ctx, ts, nullptr, out, true);
 }
 
 int atc_testsets_upload_async(atc_ctx* ctx, const atc_testsets* ts, atc_testset_handle** out) {
-  return testsets_upload(ctx, ts, out, false);
+  return testsets_upload(ctx, ts, nullptr, out, false);
+}
+
+int atc_testsets_upload_seeded(atc_ctx* ctx, const atc_seeded_testsets* ts, atc_testset_handle** out) {
+  return testsets_upload(ctx, nullptr, ts, out, false);
+}
+
+int atc_testsets_download(atc_ctx* ctx, const atc_testset_handle* h, double* init, double* final_) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (!h || (!init && !final_)) {
+    atc_set_error(ctx, "bad arguments to atc_testsets_download");
+    return ATC_ERR_ARG;
+  }
+  cudaSetDevice(ctx->device);
+  if (h->ready && !atc_cuda_ok(ctx, cudaEventSynchronize(h->ready), "upload wait")) return ATC_ERR_CUDA;
+  std::vector<int64_t> off((size_t)h->T * h->nP), len(h->nP);
+  if (!atc_cuda_ok(ctx, cudaMemcpy(off.data(), h->view.region_off, off.size() * 8, cudaMemcpyDeviceToHost), "D2H") ||
+      !atc_cuda_ok(ctx, cudaMemcpy(len.data(), h->view.region_len, len.size() * 8, cudaMemcpyDeviceToHost), "D2H"))
+    return ATC_ERR_CUDA;
+  size_t o = 0;  // host layout: (t, p) regions back to back, unpadded
+  for (int t = 0; t < h->T; ++t)
+    for (int p = 0; p < h->nP; ++p) {
+      const size_t i = (size_t)t * h->nP + p, bytes = (size_t)len[p] * 8;
+      if ((init && !atc_cuda_ok(ctx, cudaMemcpy(init + o, h->view.init + off[i], bytes, cudaMemcpyDeviceToHost), "D2H")) ||
+          (final_ && !atc_cuda_ok(ctx, cudaMemcpy(final_ + o, h->view.fin + off[i], bytes, cudaMemcpyDeviceToHost), "D2H")))
+        return ATC_ERR_CUDA;
+      o += (size_t)len[p];
+    }
+  return ATC_OK;
 }
 
 int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h) {
@@ -500,7 +584,7 @@ int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h) {
     // stream has passed this point (and this handle's own copies are done)
     ts_wait(h, ctx->stream);
     cudaEventRecord(ctx->free_ev, ctx->stream);
-    ctx->free_pending = true;
+    ctx->free_pending = (1u << atc_ctx::kCopyStreams) - 1;
   }
   if (h->ready) cudaEventDestroy(h->ready);
   for (void* p : h->allocations) {

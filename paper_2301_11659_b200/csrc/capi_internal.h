@@ -28,9 +28,11 @@ struct atc_ctx {
   // test-set uploads run on their own stream (copy engine) and publish a ready
   // event per handle; frees record free_ev on the compute stream, which the
   // next upload waits on before reusing pool memory
-  cudaStream_t copy_stream = nullptr;
+  static constexpr int kCopyStreams = 16;  // uploads round-robin over these (concurrent generators)
+  cudaStream_t copy_stream[kCopyStreams] = {};
+  int copy_next = 0;
   cudaEvent_t free_ev = nullptr;
-  bool free_pending = false;
+  unsigned free_pending = 0;  // copy streams that have not waited on the latest free
   int mode = 0;  // ATC_MODE_* of the evaluation in flight
   // instrumentation (atc_profile_*)
   bool prof = false;

@@ -42,6 +42,10 @@ class RecordedTestsets:
     final: list  # [T][nP] float64 arrays (None when not test_ok)
     test_ok: np.ndarray  # int32 [T]
     _handles: dict = field(default_factory=dict, repr=False)
+    # how verify_rewrite drew the initial regions (when known): test t's Rng seed and
+    # the stream position of each region's first draw — atc_testsets_upload_seeded
+    seeds: Optional[np.ndarray] = None  # uint64 [T]
+    skips: Optional[np.ndarray] = None  # uint64 [T, nP]
 
     @property
     def ptrs(self) -> list:
@@ -58,7 +62,57 @@ class RecordedTestsets:
     def head(self, T: int) -> "RecordedTestsets":
         """The first T tests (t-indexed streams are independent: prefix = fewer tests)."""
         return RecordedTestsets(self.params, self.ints[:T].copy(), self.init[:T], self.final[:T],
-                                self.test_ok[:T].copy())
+                                self.test_ok[:T].copy(),
+                                seeds=None if self.seeds is None else self.seeds[:T].copy(),
+                                skips=None if self.skips is None else self.skips[:T].copy())
+
+    def seeded_struct(self):
+        """atc_seeded_testsets: seeds + stream positions + the final-minus-init
+        entries (positions where the original run's final image differs)."""
+        if self.seeds is None or self.skips is None:
+            raise ValueError("these test sets carry no stream seeds")
+        ptrs = self.ptrs
+        T, nP = self.n_tests, len(ptrs)
+        pos, val, off = [], [], [0]
+        for t in range(T):
+            for p in range(nP):
+                if self.final[t] is not None:
+                    d = np.nonzero(self.final[t][p] != self.init[t][p])[0]
+                    pos.append(d.astype(np.int32))
+                    val.append(np.asarray(self.final[t][p])[d].astype(np.float64))
+                    off.append(off[-1] + len(d))
+                else:
+                    off.append(off[-1])
+        dpos = np.ascontiguousarray(np.concatenate(pos) if pos else np.zeros(0, np.int32), dtype=np.int32)
+        dval = np.ascontiguousarray(np.concatenate(val) if val else np.zeros(0), dtype=np.float64)
+        doff = np.array(off, dtype=np.int64)
+        ints = np.ascontiguousarray(self.ints, dtype=np.int64)
+        is_f32 = np.array([1 if p.elem == "f32" else 0 for p in ptrs], dtype=np.int32)
+        lens = np.array([len(self.init[0][p]) for p in range(nP)], dtype=np.int64)
+        ok = np.ascontiguousarray(self.test_ok, dtype=np.int32)
+        seeds = np.ascontiguousarray(self.seeds, dtype=np.uint64)
+        skips = np.ascontiguousarray(self.skips, dtype=np.uint64)
+        s = _lib.SeededTestsets()
+        s.n_tests, s.n_ints, s.n_ptrs = T, ints.shape[1], nP
+        s.int_values = ints.ctypes.data
+        s.ptr_is_f32 = is_f32.ctypes.data
+        s.region_len = lens.ctypes.data
+        s.test_ok = ok.ctypes.data
+        s.stream_seed = seeds.ctypes.data
+        s.stream_skip = skips.ctypes.data
+        s.diff_off = doff.ctypes.data
+        s.diff_pos = dpos.ctypes.data
+        s.diff_val = dval.ctypes.data
+        return s, [ints, is_f32, lens, ok, seeds, skips, doff, dpos, dval]
+
+    def upload_seeded(self, ctx: "_lib.Context"):
+        """atc_testsets_upload_seeded: regions generated on the GPU from the seeds."""
+        s, keep = self.seeded_struct()
+        out = C.c_void_p()
+        _lib.check(ctx.handle, _lib.lib().atc_testsets_upload_seeded(ctx.handle, C.byref(s), C.byref(out)))
+        h = _TestsetHandle(ctx, out.value)
+        h.keep = keep  # host buffers stay valid until the handle is used (async upload)
+        return h
 
     def c_struct(self):
         ptrs = self.ptrs
@@ -134,6 +188,7 @@ def record_testsets(function: str, params: list, rules: SizeRules, p2seed: int, 
     T = tests
     ints = np.zeros((T, len(int_names)), dtype=np.int64)
     init, final, ok = [], [], np.zeros(T, dtype=np.int32)
+    seeds, skips = np.zeros(T, dtype=np.uint64), np.zeros((T, len(ptrs)), dtype=np.uint64)
     for t in range(T):
         pt = p2_test_inputs(function, params, rules, p2seed, t)
         if not pt.ok:
@@ -141,6 +196,8 @@ def record_testsets(function: str, params: list, rules: SizeRules, p2seed: int, 
             final.append(None)
             continue
         ints[t] = [pt.sizes[n] for n in int_names]
+        seeds[t] = pt.seed
+        skips[t] = [pt.streams[p.name] for p in ptrs]
         init.append([pt.regions[p.name] for p in ptrs])
         fin = run_original(t, pt.sizes, pt.regions, pt.floats)
         if fin is None:
@@ -148,7 +205,7 @@ def record_testsets(function: str, params: list, rules: SizeRules, p2seed: int, 
             continue
         final.append([fin[p.name] for p in ptrs])
         ok[t] = 1
-    return RecordedTestsets(params, ints, init, final, ok)
+    return RecordedTestsets(params, ints, init, final, ok, seeds=seeds, skips=skips)
 
 
 # ------------------------------------------------------------- binding spaces --

@@ -102,6 +102,7 @@ class Program:
         ptrs = [p for p in params if p.kind == "ptr"]
         ints = np.zeros((T, len(self.user_ints)), dtype=np.int64)
         init, final, ok = [], [], np.zeros(T, dtype=np.int32)
+        seeds, skips = np.zeros(T, dtype=np.uint64), np.zeros((T, len(ptrs)), dtype=np.uint64)
         for rec in self.meta[variant][:T]:
             t = rec["t"]
             pt = p2_test_inputs(self.function, params, rules, self.p2seed, t)
@@ -112,6 +113,8 @@ class Program:
                 continue
             assert {k: int(v) for k, v in rec["sizes"].items()} == pt.sizes, f"{self.stem} t={t}: sizes differ"
             ints[t] = [pt.sizes[u] for u in self.user_ints]
+            seeds[t] = pt.seed
+            skips[t] = [pt.streams[p.name] for p in ptrs]
             init.append([pt.regions[p.name] for p in ptrs])
             if check is not None:
                 for p in ptrs:
@@ -127,7 +130,7 @@ class Program:
                 fin.append(f)
             final.append(fin)
             ok[t] = 1
-        return RecordedTestsets(params, ints, init, final, ok)
+        return RecordedTestsets(params, ints, init, final, ok, seeds=seeds, skips=skips)
 
 
 @lru_cache(maxsize=None)

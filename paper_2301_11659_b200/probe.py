@@ -176,13 +176,17 @@ class Param:
     elem: str  # "f32" | "f64" | "i64"
 
 
-def build_probe_image(params: list, sizes: dict, rng: Rng, region_len: int = PROBE_REGION_LEN):
-    """analysis::build_probe_image (analysis.cpp:73-98): params in signature order."""
+def build_probe_image(params: list, sizes: dict, rng: Rng, region_len: int = PROBE_REGION_LEN,
+                      streams: dict | None = None):
+    """analysis::build_probe_image (analysis.cpp:73-98): params in signature order.
+    `streams`, when given, receives each region's first stream position."""
     regions, floats = {}, {}
     for p in params:
         if p.kind == "float":
             floats[p.name] = rng.uniform_real(-1.0, 1.0)
         elif p.kind == "ptr":
+            if streams is not None:
+                streams[p.name] = rng.pos
             regions[p.name] = rng.fill_uniform(region_len, -1.0, 1.0, p.elem == "f32")
     return regions, floats
 
@@ -194,6 +198,8 @@ class ProbeTest:
     sizes: dict
     regions: dict  # name -> np.float64[65536] (initial contents)
     floats: dict
+    seed: int = 0  # the test's Rng seed
+    streams: dict = field(default_factory=dict)  # name -> stream position of the region's first draw
 
 
 def p2_test_inputs(function: str, params: list, rules: SizeRules, p2seed: int, t: int) -> ProbeTest:
@@ -207,8 +213,9 @@ def p2_test_inputs(function: str, params: list, rules: SizeRules, p2seed: int, t
             break
     if sizes is None:
         return ProbeTest(t, False, {}, {}, {})
-    regions, floats = build_probe_image(params, sizes, rng)
-    return ProbeTest(t, True, sizes, regions, floats)
+    streams: dict = {}
+    regions, floats = build_probe_image(params, sizes, rng, streams=streams)
+    return ProbeTest(t, True, sizes, regions, floats, rng.seed, streams)
 
 
 def fnv1a_bytes(a: np.ndarray) -> int:

@@ -308,3 +308,39 @@ def test_conv_screen_kernels_agree():
         res[name] = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["pairs"] == res["planes"] == res["generic"]
     assert any(r["hist"][4] for r in res["pairs"]) and any(r["hist"][2] for r in res["pairs"])
+
+
+@pytest.mark.parametrize("stem", ["naive_f32", "conv_direct", "naive_ld", "im2col_buffered", "strassen_staged"])
+def test_seeded_upload_regenerates_regions(ev, stem):
+    """atc_testsets_upload_seeded rebuilds every probe image on the GPU from the
+    tests' mt19937_64 streams (std::mt19937_64, uniform_real(-1,1), f32 rounding)
+    bit-identically to the host regions, and the final images from the
+    final-minus-init entries."""
+    import ctypes as C
+
+    p = fixtures.load(stem)
+    ts = p.testsets(16)
+    h = ts.upload_seeded(ev.ctx)
+    nP, T, lens = len(ts.ptrs), ts.n_tests, [len(ts.init[0][q]) for q in range(len(ts.ptrs))]
+    tot = T * sum(lens)
+    ini, fin = np.empty(tot), np.empty(tot)
+    L.check(ev.ctx.handle, L.lib().atc_testsets_download(ev.ctx.handle, C.c_void_p(h.value), ini.ctypes.data,
+                                                         fin.ctypes.data))
+    o = 0
+    for t in range(T):
+        for q in range(nP):
+            if ts.test_ok[t]:
+                assert np.array_equal(ini[o:o + lens[q]].view(np.uint64), np.asarray(ts.init[t][q]).view(np.uint64))
+                assert np.array_equal(fin[o:o + lens[q]].view(np.uint64), np.asarray(ts.final[t][q]).view(np.uint64))
+            o += lens[q]
+    # the same verdicts through the seeded handle
+    for sname in p.spec_names():
+        space = p.space(sname)
+        end = min(space.count, 1 << 22)
+        want = ev.eval_enumerated(fixtures.spec(sname), ts, space, 0, end)
+        ts2 = p.testsets(16)
+        ts2._handles[id(ev.ctx)] = h
+        got = ev.eval_enumerated(fixtures.spec(sname), ts2, space, 0, end)
+        np.testing.assert_array_equal(got[0], want[0])
+        assert got[1] == want[1] and got[2].tolist() == want[2].tolist()
+    ts2._handles.clear()
