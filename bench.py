@@ -475,6 +475,28 @@ def _max_over_ranks(ms, dist, torch):
     return float(t.item())
 
 
+def _time_ms(fn, stream, torch, reps=5):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
+def _library_tf32(torch):
+    """A library comparison point (not on the product path): cuBLAS / cuDNN with TF32."""
+    torch.backends.cuda.matmul.allow_tf32 = True
+    torch.backends.cudnn.allow_tf32 = True
+    torch.backends.cudnn.benchmark = True
+
+
 def _conv_bench(ctx, stream, torch, dist=None, world=1, batch=256):
     """Replaced-call conv2d backend on tcgen05 (TF32): global batch `batch`,
     split across ranks (batch // world images each)."""
@@ -511,13 +533,18 @@ def _conv_bench(ctx, stream, torch, dist=None, world=1, batch=256):
         flops = 2.0 * gb * k * oh * oh * c * r * r
         ref = torch.nn.functional.conv2d(x[:1].double(), w.double())
         err = ((y[:1].double() - ref).abs() / (1 + ref.abs())).max().item()
+        _library_tf32(torch)
+        lib_ms = _max_over_ranks(_time_ms(lambda: torch.nn.functional.conv2d(x, w), stream, torch), dist, torch)
         out["layers"].append({"layer": name, "C": c, "K": k, "RxS": f"{r}x{r}", "H": h, "ms": ms,
-                              "tflops": flops / (ms / 1e3) / 1e12, "max_rel_err_vs_fp64": err})
+                              "tflops": flops / (ms / 1e3) / 1e12, "max_rel_err_vs_fp64": err,
+                              "cudnn_tf32_tflops": flops / (lib_ms / 1e3) / 1e12})
         tot_flops += flops
         tot_ms += ms
         del x, w, y
     out["total_tflops"] = tot_flops / (tot_ms / 1e3) / 1e12
-    out["note"] = "includes the per-call NCHW->NHWC input transpose and KCRS->KRSC weight reorder"
+    out["note"] = ("includes the per-call NCHW->NHWC input transpose and KCRS->KRSC weight reorder; "
+                   "cudnn_tf32_tflops = torch conv2d (cuDNN, TF32, benchmark mode) on the same tensors, "
+                   "a library comparison point only")
     return out
 
 
@@ -555,6 +582,9 @@ def _sgemm_bench(ctx, stream, torch, dist=None, world=1):
         ref = (a[:256].double() @ b.double())
         err = ((c[:256].double() - ref).abs() / (1 + ref.abs())).max().item()
         out[prec_name] = {"ms": ms, "tflops": tflops, "max_rel_err_vs_fp64": err}
+    _library_tf32(torch)
+    cublas_ms = _max_over_ranks(_time_ms(lambda: torch.matmul(a, b, out=c), stream, torch), dist, torch)
+    out["cublas_tf32_tflops"] = 2.0 * M * n * k / (cublas_ms / 1e3) / 1e12
     _, bf16, kind = _peaks()
     tf32_peak = bf16 / 2
     out["shape"] = [M, n, k]
@@ -565,7 +595,8 @@ def _sgemm_bench(ctx, stream, torch, dist=None, world=1):
                        "traffic": (g.get("dram_read", 0) + g.get("dram_write", 0)) if g else None,
                        "algorithmic_bytes": 3 * m * n * 4,
                        "tensor_pipe_active_pct": g.get("tensor_pipe_active_pct"),
-                       "peak_kind": f"TF32 dense = 1/2 of the {kind} cuBLAS bf16 peak (not separately measured)"}
+                       "peak_kind": f"TF32 dense = 1/2 of the {kind} cuBLAS bf16 peak; cuBLAS TF32 on the same "
+                                    f"operands measured {out['cublas_tf32_tflops']:.0f} TFLOP/s in this run"}
     return out
 
 

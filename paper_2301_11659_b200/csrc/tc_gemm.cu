@@ -50,7 +50,8 @@ constexpr int B_BYTES = BN * BK * 4;        // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int NUM_THREADS = 256;
 constexpr int TMEM_COLS = 512;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int EPI_BYTES = 4 * 32 * 33 * 4;  // epilogue transpose staging, one 32x33 tile per warp
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_BYTES;
 
 // ------------------------------------------------------------ PTX helpers ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -197,11 +198,16 @@ __device__ __forceinline__ void kblock_coords(const Problem& p, int kb, int kblo
   // 3xTF32 order: lo*hi, hi*lo, hi*hi (small terms first)
   sel_a = split == 0 && p.splits == 3 ? 1 : 0;
   sel_b = split == 1 ? 1 : 0;
-  if (!p.conv) {
+  if (p.conv == 0) {
     a_c0 = k * BK;        // K
     a_c1 = tm * BM;       // M
     b_c0 = tn * BN;       // N (chunk offset added by caller)
     b_c1 = k * BK;        // K
+  } else if (p.conv == 3) {  // sgemm with B transposed to [N][K]: K-major like A
+    a_c0 = k * BK;
+    a_c1 = tm * BM;
+    b_c0 = k * BK;        // K
+    b_c1 = tn * BN;       // N row (half offset added by caller)
   } else {
     const int cblocks = p.K / BK;     // C / 32
     const int rs = k / cblocks;       // r*S + s
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kblocks = (p.conv ? p.R * p.S * (p.K / BK) : (p.K + BK - 1) / BK);
+  const int kblocks = (p.conv == 1 || p.conv == 2 ? p.R * p.S * (p.K / BK) : (p.K + BK - 1) / BK);
   const int total_kb = kblocks * p.splits;
   // work units: single tiles, or M-tile pairs processed by a 2-CTA cluster
   uint32_t rank = 0;
@@ -282,6 +288,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
           if (p.conv == 1) {
             // K-major: 256 pixel rows x 32 channels (128 B) in one box
             tma_load_2d(sB, &maps.b[sb], &full[stage], b0, b1);
+          } else if (p.conv == 3) {
+            // K-major B in two boxes of 128 rows; a pair multicasts one half each
+            if (p.pair)
+              tma_load_2d_mc(sB + rank * (BN / 2) * 128, &maps.b[sb], &full[stage], b0, b1 + (int)rank * (BN / 2),
+                             0x3);
+            else
+              for (int h = 0; h < 2; ++h)
+                tma_load_2d(sB + h * (BN / 2) * 128, &maps.b[sb], &full[stage], b0, b1 + h * (BN / 2));
           } else if (p.pair) {
             // MN-major B shared by the pair: this CTA loads half of the 8 chunks and
             // multicasts them into both CTAs' smem (each CTA's full barrier expects
@@ -338,9 +352,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
             // B (sgemm): MN-major SW128 with 32 B atoms: chunks of 32 N at LBO = 32 rows *
             // 128 B, 4-row K groups at SBO = 512 B; +8 rows (1 KB) per K step.
             // B (conv): K-major SW128 like A.
-            const uint64_t bd = p.conv == 1 ? make_desc(b_addr + kk * 32, 16, 1024, kSw128)
+            const bool b_kmajor = p.conv == 1 || p.conv == 3;
+            const uint64_t bd = b_kmajor ? make_desc(b_addr + kk * 32, 16, 1024, kSw128)
                                             : make_desc(b_addr + kk * 1024, BK * 128, 512, kSw128Base32);
-            mma_tf32(d_tmem, ad, bd, p.conv == 1 ? idesc_tf32(0) : idesc_tf32(1), (kb > 0 || kk > 0) ? 1u : 0u);
+            mma_tf32(d_tmem, ad, bd, b_kmajor ? idesc_tf32(0) : idesc_tf32(1), (kb > 0 || kk > 0) ? 1u : 0u);
           }
           // smem stage free once these MMAs complete (pair: in both CTAs)
           if (p.pair)
@@ -362,6 +377,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
   } else if (warp >= 4) {
     // ================= epilogue =================
     const int q = warp - 4;  // TMEM lanes 32q .. 32q+31
+    float* stg = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + q * (32 * 33);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int unit = unit0; unit < num_units; unit += unit_step) {
@@ -370,54 +386,64 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       if (p.pair) tm = 2 * tm + (int)rank;
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
-      const int row = tm * BM + q * 32 + lane;  // output row (gemm M / conv filter)
+      // gemm / 1x1: each lane stores its row's 32 contiguous columns as float4s.
+      // conv on the input grid (gaps at x >= OW): each 32x32 sub-tile goes TMEM ->
+      // registers (lane = row) -> shared memory -> registers (lane = column), so a
+      // store instruction writes consecutive pixels of one output row
+      const int row0 = tm * BM + q * 32;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         const uint32_t taddr = tmem_base + acc * BN + c0 + ((uint32_t)(q * 32) << 16);
         TMEM_LD_32x32b_x32(taddr, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        const int col0 = tn * BN + c0;
-        if (row < p.M) {
-          if (!p.conv) {
-            float* dst = p.C + (int64_t)row * p.ldc + col0;
-            if (col0 + 32 <= p.N && (p.ldc & 3) == 0) {
+        if (p.conv != 1) {
+          // gemm rows / 1x1 image rows: 128 contiguous bytes per lane, float4 stores
+          const int row = row0 + lane;
+          const int col0 = tn * BN + c0;
+          const int64_t ncols = (p.conv == 2) ? (int64_t)p.OH * p.OW : p.N;
+          const int64_t pitch = (p.conv == 2) ? ncols : p.ldc;
+          float* dst = p.C + ((p.conv == 2) ? ((int64_t)ti * p.M + row) * ncols : (int64_t)row * pitch) + col0;
+          if (row < p.M) {
+            if (col0 + 32 <= ncols && (pitch & 3) == 0) {
 #pragma unroll
               for (int v = 0; v < 32; v += 4)
                 *reinterpret_cast<float4*>(dst + v) = make_float4(__uint_as_float(r[v]), __uint_as_float(r[v + 1]),
                                                                   __uint_as_float(r[v + 2]), __uint_as_float(r[v + 3]));
             } else {
               for (int v = 0; v < 32; ++v)
-                if (col0 + v < p.N) dst[v] = __uint_as_float(r[v]);
-            }
-          } else {
-            // pixel p = y*W + x on the input grid; keep y < OH, x < OW
-            float* dst = p.C + ((int64_t)ti * p.M + row) * ((int64_t)p.OH * p.OW);
-            if (p.R == 1 && p.S == 1) {  // every pixel is an output: contiguous, vectorised
-              const int npix = p.OH * p.OW;
-              if (col0 + 32 <= npix && (npix & 3) == 0) {
-#pragma unroll
-                for (int v = 0; v < 32; v += 4)
-                  *reinterpret_cast<float4*>(dst + col0 + v) =
-                      make_float4(__uint_as_float(r[v]), __uint_as_float(r[v + 1]), __uint_as_float(r[v + 2]),
-                                  __uint_as_float(r[v + 3]));
-              } else {
-                for (int v = 0; v < 32; ++v)
-                  if (col0 + v < npix) dst[col0 + v] = __uint_as_float(r[v]);
-              }
-            } else {
-              int y = col0 / p.W, x = col0 - y * p.W;
-#pragma unroll
-              for (int v = 0; v < 32; ++v) {
-                if (y < p.OH && x < p.OW) dst[y * p.OW + x] = __uint_as_float(r[v]);
-                if (++x == p.W) {
-                  x = 0;
-                  ++y;
-                }
-              }
+                if (col0 + v < ncols) dst[v] = __uint_as_float(r[v]);
             }
           }
+          continue;
         }
+#pragma unroll
+        for (int v = 0; v < 32; ++v) stg[lane * 33 + v] = __uint_as_float(r[v]);
+        __syncwarp();
+        const int col = tn * BN + c0 + lane;  // this lane's output column
+        bool ok;
+        int64_t off, rstride;  // element of (row0, col), distance between rows
+        if (p.conv == 0 || p.conv == 3) {
+          ok = col < p.N;
+          off = (int64_t)row0 * p.ldc + col;
+          rstride = p.ldc;
+        } else if (p.conv == 1) {
+          // pixels of the whole batch back to back (P = img*H*W + y*W + x) on the input grid
+          const int hw = p.H * p.W;
+          const int img = col / hw, rem = col - img * hw, y = rem / p.W, x = rem - (rem / p.W) * p.W;
+          rstride = (int64_t)p.OH * p.OW;
+          ok = img < p.img && y < p.OH && x < p.OW;
+          off = ((int64_t)img * p.M + row0) * rstride + (int64_t)y * p.OW + x;
+        } else {
+          // 1x1 on one image: every pixel is an output
+          rstride = (int64_t)p.OH * p.OW;
+          ok = col < rstride;
+          off = ((int64_t)ti * p.M + row0) * rstride + col;
+        }
+        const int rows = min(32, p.M - row0);
+        if (ok)
+          for (int i = 0; i < rows; ++i) p.C[off + (int64_t)i * rstride] = stg[i * 33 + lane];
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
@@ -625,10 +651,16 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
     k_pitch_copy<<<grid_for(k * np), 256, 0, st>>>(dB, t, k, n, np);
     B = t;
   }
+  // ATC_TC_BKMAJOR=1: B transposed once to [N][K] (K-major, like A) — A/B experiment
+  static const bool bk = [] {
+    const char* e = std::getenv("ATC_TC_BKMAJOR");
+    return e && e[0] == '1';
+  }();
+  const bool b_kmajor = bk && k % 32 == 0 && n % 32 == 0;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   Problem p{};
-  p.conv = 0;
+  p.conv = b_kmajor ? 3 : 0;
   p.M = (int)m;
   p.N = (int)n;
   p.K = (int)k;
@@ -639,7 +671,30 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
   p.tiles_img = 1;
   p.pair = use_pair(p);
   p.splits = precision == ATC_PREC_3XTF32 ? 3 : 1;
-  if (p.splits == 3) {
+  if (b_kmajor) {
+    float* bt = (float*)atc_ctx_scratch(ctx, 14, (size_t)k * n * 4 * (p.splits == 3 ? 2 : 1));
+    if (!bt) return ATC_ERR_CUDA;
+    float* btl = p.splits == 3 ? bt + k * n : nullptr;
+    dim3 grid((unsigned)((n + 31) / 32), (unsigned)(k / 32), 1u);
+    k_nchw_to_nhwc<<<grid, dim3(32, 8), 0, st>>>(B, bt, btl, (int)k, n);  // [K][N] -> [N][K] (+ hi/lo)
+    float* a_lo = nullptr;
+    const float* a_hi = A;
+    if (p.splits == 3) {
+      float* ah = (float*)atc_ctx_scratch(ctx, 13, (size_t)m * kp * 4 * 2);
+      if (!ah) return ATC_ERR_CUDA;
+      a_lo = ah + m * kp;
+      k_split_tf32<<<grid_for(m * kp), 256, 0, st>>>(A, ah, a_lo, m * kp);
+      a_hi = ah;
+    }
+    if (!make_map(ctx, &maps.a[0], a_hi, m, k, kp, BK, BM, false) ||
+        !make_map(ctx, &maps.b[0], bt, n, k, k, BK, BN / 2, false))
+      return ATC_ERR_CUDA;
+    maps.a[1] = maps.a[0];
+    maps.b[1] = maps.b[0];
+    if (p.splits == 3 && (!make_map(ctx, &maps.a[1], a_lo, m, k, kp, BK, BM, false) ||
+                          !make_map(ctx, &maps.b[1], btl, n, k, k, BK, BN / 2, false)))
+      return ATC_ERR_CUDA;
+  } else if (p.splits == 3) {
     float* ah = (float*)atc_ctx_scratch(ctx, 13, (size_t)m * kp * 4 * 2);
     float* bh = (float*)atc_ctx_scratch(ctx, 14, (size_t)k * np * 4 * 2);
     if (!ah || !bh) return ATC_ERR_CUDA;
@@ -695,7 +750,7 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
     atc_set_error(ctx, "bad arguments to atc_conv2d_nchw");
     return ATC_ERR_ARG;
   }
-  if (c % BK != 0 || n * c >= (1LL << 31) || h * w_ >= (1LL << 31)) {
+  if (c % BK != 0 || n * c >= (1LL << 31) || n * h * w_ >= (1LL << 31) - (1LL << 20)) {
     atc_set_error(ctx, "atc_conv2d_nchw: C must be a multiple of %d (got %lld)", BK, (long long)c);
     return ATC_ERR_ARG;
   }
@@ -760,9 +815,17 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
   p.OH = (int)oh;
   p.OW = (int)ow;
   p.tiles_m = (int)((k + BM - 1) / BM);
-  // only pixels p < OH*W can be valid outputs (rows y < OH)
-  p.tiles_n = (int)((oh * w_ + BN - 1) / BN);
-  p.tiles_img = (int)n;
+  if (direct) {
+    // per image ([N*C][H*W] view); only pixels p < OH*W can be valid outputs
+    p.tiles_n = (int)((oh * w_ + BN - 1) / BN);
+    p.tiles_img = (int)n;
+  } else {
+    // the batch's pixels back to back on the NHWC input: tiles run across image
+    // boundaries (shifted rows of a valid output never leave its image)
+    const int64_t last = (n - 1) * hw + (oh - 1) * w_ + (ow - 1);
+    p.tiles_n = (int)((last + BN) / BN);
+    p.tiles_img = 1;
+  }
   p.pair = use_pair(p);
   return launch(ctx, maps, p, st) ? ATC_OK : ATC_ERR_CUDA;
 }
