@@ -48,10 +48,11 @@ constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK * 4;        // 16 KB
 constexpr int B_BYTES = BN * BK * 4;        // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARPS = 4;  // one per TMEM lane quadrant (8 = two per quadrant, each half of the columns)
+constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int TMEM_COLS = 512;
-constexpr int EPI_BYTES = 4 * 32 * 33 * 4;  // epilogue transpose staging, one 32x33 tile per warp
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_BYTES;
+constexpr int kEpiStride = 1280;  // floats per epilogue warp: a 32x33 tile, rounded to 1 KB (TMA swizzle alignment)
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + EPI_WARPS * kEpiStride * 4;
 
 // ------------------------------------------------------------ PTX helpers ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -90,6 +91,12 @@ __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -167,11 +174,13 @@ struct Problem {
   int img, Cin, H, W, R, S, OH, OW;
   int tiles_m, tiles_n, tiles_img;
   int pair;  // 1: CTA pairs (cluster of 2) on adjacent M tiles share the B tile via TMA multicast
+  int tma_store;  // 1: epilogue writes 32x32 sub-tiles with TMA bulk stores (modes 0, 2, 3)
 };
 
 struct Maps {
   CUtensorMap a[2];  // hi, lo
   CUtensorMap b[2];
+  CUtensorMap c;     // output [rows][cols] fp32, 32x32 boxes, 128B swizzle (p.tma_store)
 };
 
 __device__ __forceinline__ void tile_coords(const Problem& p, int tile, int& tm, int& tn, int& ti) {
@@ -252,7 +261,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tmem_empty[a], EPI_WARPS);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -376,8 +385,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
     }
   } else if (warp >= 4) {
     // ================= epilogue =================
-    const int q = warp - 4;  // TMEM lanes 32q .. 32q+31
-    float* stg = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + q * (32 * 33);
+    const int q = (warp - 4) % 4;        // TMEM lanes 32q .. 32q+31 (a warp reaches quadrant warp % 4)
+    const int half = (warp - 4) / 4;     // columns [half * BN/2, (half + 1) * BN/2)
+    // 1024-aligned per-warp staging (the TMA store buffer needs the 128B-swizzle alignment)
+    float* stg = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024) + (warp - 4) * kEpiStride;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int unit = unit0; unit < num_units; unit += unit_step) {
@@ -392,11 +403,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       // store instruction writes consecutive pixels of one output row
       const int row0 = tm * BM + q * 32;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      constexpr int kColSpan = BN / (EPI_WARPS / 4);  // columns per epilogue warp
+      for (int c0 = half * kColSpan; c0 < (half + 1) * kColSpan; c0 += 32) {
         uint32_t r[32];
         const uint32_t taddr = tmem_base + acc * BN + c0 + ((uint32_t)(q * 32) << 16);
         TMEM_LD_32x32b_x32(taddr, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (p.tma_store) {
+          // registers -> this warp's 4 KB buffer in the TMA 128B-swizzle layout (16 B
+          // chunk j of row `lane` at chunk j ^ (lane & 7): conflict-free STS.128) ->
+          // one bulk tensor store of the 32x32 sub-tile (full-line writes; edges clipped)
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(stg + lane * 32 + ((j ^ (lane & 7)) * 4)) =
+                make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                            __uint_as_float(r[4 * j + 3]));
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            tma_store_2d(&maps.c, stg, tn * BN + c0, (p.conv == 2 ? ti * p.M : 0) + row0);
+          continue;
+        }
         if (p.conv != 1) {
           // gemm rows / 1x1 image rows: 128 contiguous bytes per lane, float4 stores
           const int row = row0 + lane;
@@ -454,6 +483,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       }
     }
   }
+  if (p.tma_store && warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   if (p.pair) cluster_sync();  // no multicast or remote arrive may still target this CTA
@@ -578,6 +608,15 @@ bool make_map(atc_ctx* ctx, CUtensorMap* m, const float* base, uint64_t rows, ui
   return true;
 }
 
+// ATC_TC_TMA_STORE=0 disables the TMA-store epilogue (A/B measurement)
+int tma_store_enabled() {
+  static const int enabled = [] {
+    const char* e = std::getenv("ATC_TC_TMA_STORE");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return enabled;
+}
+
 // CTA pairs need an MN-major B (loaded as chunks, half by each CTA) and >= 2
 // M tiles; ATC_TC_PAIR=0 disables them (A/B measurement)
 int use_pair(const Problem& p) {
@@ -671,6 +710,9 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
   p.tiles_img = 1;
   p.pair = use_pair(p);
   p.splits = precision == ATC_PREC_3XTF32 ? 3 : 1;
+  // TMA-store epilogue when C's row pitch is a multiple of 16 bytes
+  p.tma_store = tma_store_enabled() && (n % 4) == 0 ? 1 : 0;
+  if (p.tma_store && !make_map(ctx, &maps.c, dC, m, n, n, 32, 32, false)) return ATC_ERR_CUDA;
   if (b_kmajor) {
     float* bt = (float*)atc_ctx_scratch(ctx, 14, (size_t)k * n * 4 * (p.splits == 3 ? 2 : 1));
     if (!bt) return ATC_ERR_CUDA;
@@ -827,6 +869,9 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
     p.tiles_img = 1;
   }
   p.pair = use_pair(p);
+  // 1x1 direct: the output is a [N*K][OH*OW] matrix (hw % 4 == 0): TMA-store epilogue
+  p.tma_store = direct && tma_store_enabled() ? 1 : 0;
+  if (p.tma_store && !make_map(ctx, &maps.c, d_out, n * k, oh * ow, oh * ow, 32, 32, false)) return ATC_ERR_CUDA;
   return launch(ctx, maps, p, st) ? ATC_OK : ATC_ERR_CUDA;
 }
 
