@@ -175,6 +175,7 @@ struct Problem {
   int tiles_m, tiles_n, tiles_img;
   int pair;  // 1: CTA pairs (cluster of 2) on adjacent M tiles share the B tile via TMA multicast
   int tma_store;  // 1: epilogue writes 32x32 sub-tiles with TMA bulk stores (modes 0, 2, 3)
+  int umma2;      // 1: sgemm on k_tc_gemm2 (cta_group::2, M = 256 per CTA pair)
 };
 
 struct Maps {
@@ -492,6 +493,236 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
 }
 
+// ---------------------------------------------------------------------------
+// k_tc_gemm2: the sgemm on CTA pairs with tcgen05.mma.cta_group::2 (M = 256 per
+// pair, N = 256).  Each CTA of the pair holds its 128 rows of A and its 128
+// columns of B per stage (32 KB, 6 stages); the leader (rank 0) issues the MMAs,
+// which read A from each CTA's own shared memory and B from both; each CTA's TMEM
+// holds its 128 rows x 256 columns of the accumulator.  Both CTAs' TMA loads
+// signal the leader's `full` barrier (.cta_group::2); MMA commits arrive on both
+// CTAs' `empty` / `tmem_full` barriers (multicast); both CTAs' epilogue warps
+// arrive on the leader's `tmem_empty`.
+constexpr int STAGES2 = 6;
+constexpr int B2_BYTES = (BN / 2) * BK * 4;  // 16 KB: this CTA's half of the B tile
+constexpr int STAGE2_BYTES = A_BYTES + B2_BYTES;
+constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + EPI_WARPS * kEpiStride * 4;
+
+__device__ __forceinline__ uint32_t peer_addr(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+__host__ __device__ constexpr uint32_t idesc_tf32_m256() {  // M = 256 (cta_group::2), N = 256, B MN-major
+  return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(256 >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_constant__ Maps maps, const Problem p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tmem_full = empty + STAGES2;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kblocks = (p.K + BK - 1) / BK;
+  const int total_kb = kblocks * p.splits;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int tiles_m2 = (p.tiles_m + 1) / 2;  // 256-row tiles
+  const int num_units = tiles_m2 * p.tiles_n;
+  const int unit0 = (int)(blockIdx.x / 2), unit_step = (int)(gridDim.x / 2);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);   // leader: its producer's arrive + both CTAs' bytes
+      mbar_init(&empty[s], 1);  // the leader's MMA commit (multicast)
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 2 * EPI_WARPS);  // leader: both CTAs' epilogue warps
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer (both CTAs) =================
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int unit = unit0; unit < num_units; unit += unit_step) {
+        int tm2, tn, ti;
+        {
+          Problem q = p;
+          q.tiles_m = tiles_m2;
+          q.pair = 0;
+          tile_coords(q, unit, tm2, tn, ti);
+        }
+        const int tm = 2 * tm2 + (int)rank;  // this CTA's 128 rows
+        for (int kb = 0; kb < total_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          int sa, sb, a0, a1, b0, b1;
+          kblock_coords(p, kb, kblocks, tm, tn, 0, sa, sb, a0, a1, b0, b1);
+          uint8_t* sA = smem + stage * STAGE2_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          const uint32_t bar = peer_addr(smem_u32(&full[stage]), 0);  // the leader's barrier
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE2_BYTES);
+          tma_load_2d_2sm(sA, &maps.a[sa], bar, a0, a1);
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j)  // this CTA's 4 chunks of 32 columns
+            tma_load_2d_2sm(sB + j * (BK * 128), &maps.b[sb], bar, b0 + (int)rank * (BN / 2) + 32 * j, b1);
+          if (++stage == STAGES2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      // tail: every stage released by the MMAs before exit
+      for (int i = 0; i < STAGES2; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == STAGES2) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ================= MMA issuer (leader) =================
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int unit = unit0; unit < num_units; unit += unit_step) {
+        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < total_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * STAGE2_BYTES);
+          const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t ad = make_desc(a_addr + kk * 32, 16, 1024, kSw128);
+            const uint64_t bd = make_desc(b_addr + kk * 1024, BK * 128, 512, kSw128Base32);
+            mma_tf32_2sm(d_tmem, ad, bd, idesc_tf32_m256(), (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit_2sm(&empty[stage]);  // both CTAs' stage buffers free once these complete
+          if (++stage == STAGES2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_2sm(&tmem_full[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue (both CTAs: own 128 rows) =================
+    const int q = (warp - 4) % 4;
+    float* stg = reinterpret_cast<float*>(smem + STAGES2 * STAGE2_BYTES + 1024) + (warp - 4) * kEpiStride;
+    const uint32_t empty_leader = peer_addr(smem_u32(&tmem_empty[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int unit = unit0; unit < num_units; unit += unit_step) {
+      int tm2, tn, ti;
+      {
+        Problem q2 = p;
+        q2.tiles_m = tiles_m2;
+        q2.pair = 0;
+        tile_coords(q2, unit, tm2, tn, ti);
+      }
+      const int tm = 2 * tm2 + (int)rank;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const int row0 = tm * BM + q * 32;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem_base + acc * BN + c0 + ((uint32_t)(q * 32) << 16);
+        TMEM_LD_32x32b_x32(taddr, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (p.tma_store) {
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(stg + lane * 32 + ((j ^ (lane & 7)) * 4)) =
+                make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                            __uint_as_float(r[4 * j + 3]));
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) tma_store_2d(&maps.c, stg, tn * BN + c0, row0);
+        } else {
+          const int row = row0 + lane, col0 = tn * BN + c0;
+          if (row < p.M) {
+            float* dst = p.C + (int64_t)row * p.ldc + col0;
+            for (int v = 0; v < 32; ++v)
+              if (col0 + v < p.N) dst[v] = __uint_as_float(r[v]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(empty_leader + acc * 8);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  if (p.tma_store && warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+}
+
 // hi/lo split for 3xTF32: hi = x with the 13 low mantissa bits cleared (exactly
 // representable in TF32), lo = x - hi (exact in FP32).
 __global__ void k_split_tf32(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo, int64_t n) {
@@ -631,9 +862,27 @@ bool launch(atc_ctx* ctx, const Maps& maps, const Problem& p, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     if (!atc_cuda_ok(ctx, cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
+                     "cudaFuncSetAttribute") ||
+        !atc_cuda_ok(ctx, cudaFuncSetAttribute(k_tc_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES),
                      "cudaFuncSetAttribute"))
       return false;
     configured = true;
+  }
+  if (p.umma2) {
+    const int units = (p.tiles_m + 1) / 2 * p.tiles_n;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(2 * std::min(units, ctx->sm_count / 2)));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = SMEM2_BYTES;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return atc_cuda_ok(ctx, cudaLaunchKernelEx(&cfg, k_tc_gemm2, maps, p), "k_tc_gemm2 cluster launch");
   }
   if (p.pair) {
     // 2-CTA clusters: one M-tile pair per cluster iteration, persistent over pairs
@@ -712,6 +961,12 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
   p.splits = precision == ATC_PREC_3XTF32 ? 3 : 1;
   // TMA-store epilogue when C's row pitch is a multiple of 16 bytes
   p.tma_store = tma_store_enabled() && (n % 4) == 0 ? 1 : 0;
+  // cta_group::2 (M = 256 per CTA pair) for the MN-major sgemm; ATC_TC_2SM=0 disables
+  static const int umma2_on = [] {
+    const char* e = std::getenv("ATC_TC_2SM");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  p.umma2 = umma2_on && p.conv == 0 && p.tiles_m >= 2 ? 1 : 0;
   if (p.tma_store && !make_map(ctx, &maps.c, dC, m, n, n, 32, 32, false)) return ATC_ERR_CUDA;
   if (b_kmajor) {
     float* bt = (float*)atc_ctx_scratch(ctx, 14, (size_t)k * n * 4 * (p.splits == 3 ? 2 : 1));
