@@ -493,6 +493,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
 }
 
+// One 32x32 accumulator sub-tile (lane = row row0 + lane, columns c0..c0+31 of
+// tile column tn) from registers to global: TMA bulk store (p.tma_store), the
+// smem-transposed path for conv on the input grid, or per-row stores.
+__device__ __forceinline__ void epilogue_chunk(const Problem& p, const Maps& maps, const uint32_t (&r)[32], float* stg,
+                                               int lane, int row0, int tn, int ti, int c0) {
+  if (p.tma_store) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<float4*>(stg + lane * 32 + ((j ^ (lane & 7)) * 4)) =
+          make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                      __uint_as_float(r[4 * j + 3]));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) tma_store_2d(&maps.c, stg, tn * BN + c0, (p.conv == 2 ? ti * p.M : 0) + row0);
+    return;
+  }
+  if (p.conv == 1) {
+#pragma unroll
+    for (int v = 0; v < 32; ++v) stg[lane * 33 + v] = __uint_as_float(r[v]);
+    __syncwarp();
+    const int col = tn * BN + c0 + lane;
+    const int hw = p.H * p.W;
+    const int img = col / hw, rem = col - img * hw, y = rem / p.W, x = rem - (rem / p.W) * p.W;
+    const int64_t rstride = (int64_t)p.OH * p.OW;
+    const bool ok = img < p.img && y < p.OH && x < p.OW;
+    const int64_t off = ((int64_t)img * p.M + row0) * rstride + (int64_t)y * p.OW + x;
+    const int rows = min(32, p.M - row0);
+    if (ok)
+      for (int i = 0; i < rows; ++i) p.C[off + (int64_t)i * rstride] = stg[i * 33 + lane];
+    __syncwarp();
+    return;
+  }
+  const int row = row0 + lane, col0 = tn * BN + c0;
+  const int64_t ncols = (p.conv == 2) ? (int64_t)p.OH * p.OW : p.N;
+  const int64_t pitch = (p.conv == 2) ? ncols : p.ldc;
+  if (row < p.M) {
+    float* dst = p.C + ((p.conv == 2) ? ((int64_t)ti * p.M + row) * ncols : (int64_t)row * pitch) + col0;
+    for (int v = 0; v < 32; ++v)
+      if (col0 + v < ncols) dst[v] = __uint_as_float(r[v]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // k_tc_gemm2: the sgemm on CTA pairs with tcgen05.mma.cta_group::2 (M = 256 per
 // pair, N = 256).  Each CTA of the pair holds its 128 rows of A and its 128
@@ -538,8 +582,8 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
-__host__ __device__ constexpr uint32_t idesc_tf32_m256() {  // M = 256 (cta_group::2), N = 256, B MN-major
-  return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
+__host__ __device__ constexpr uint32_t idesc_tf32_m256(uint32_t b_mn_major) {  // M = 256 (cta_group::2), N = 256
+  return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (b_mn_major << 16) | ((uint32_t)(BN >> 3) << 17) |
          ((uint32_t)(256 >> 4) << 24);
 }
 
@@ -553,12 +597,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kblocks = (p.K + BK - 1) / BK;
+  const int kblocks = (p.conv == 1 || p.conv == 2 ? p.R * p.S * (p.K / BK) : (p.K + BK - 1) / BK);
   const int total_kb = kblocks * p.splits;
   uint32_t rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int tiles_m2 = (p.tiles_m + 1) / 2;  // 256-row tiles
-  const int num_units = tiles_m2 * p.tiles_n;
+  const int num_units = tiles_m2 * p.tiles_n * p.tiles_img;
   const int unit0 = (int)(blockIdx.x / 2), unit_step = (int)(gridDim.x / 2);
 
   if (warp == 0 && lane == 0) {
@@ -601,15 +645,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
         for (int kb = 0; kb < total_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           int sa, sb, a0, a1, b0, b1;
-          kblock_coords(p, kb, kblocks, tm, tn, 0, sa, sb, a0, a1, b0, b1);
+          kblock_coords(p, kb, kblocks, tm, tn, ti, sa, sb, a0, a1, b0, b1);
           uint8_t* sA = smem + stage * STAGE2_BYTES;
           uint8_t* sB = sA + A_BYTES;
           const uint32_t bar = peer_addr(smem_u32(&full[stage]), 0);  // the leader's barrier
           if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE2_BYTES);
           tma_load_2d_2sm(sA, &maps.a[sa], bar, a0, a1);
+          if (p.conv == 1) {
+            // K-major: this CTA's 128 pixel rows x 32 channels in one box
+            tma_load_2d_2sm(sB, &maps.b[sb], bar, b0, b1 + (int)rank * (BN / 2));
+          } else {
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j)  // this CTA's 4 chunks of 32 columns
-            tma_load_2d_2sm(sB + j * (BK * 128), &maps.b[sb], bar, b0 + (int)rank * (BN / 2) + 32 * j, b1);
+            for (int j = 0; j < BN / 64; ++j)  // MN-major: this CTA's 4 chunks of 32 columns
+              tma_load_2d_2sm(sB + j * (BK * 128), &maps.b[sb], bar, b0 + (int)rank * (BN / 2) + 32 * j, b1);
+          }
           if (++stage == STAGES2) {
             stage = 0;
             phase ^= 1;
@@ -641,11 +690,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * STAGE2_BYTES);
           const uint32_t b_addr = a_addr + A_BYTES;
+          const bool b_kmajor = p.conv == 1;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint64_t ad = make_desc(a_addr + kk * 32, 16, 1024, kSw128);
-            const uint64_t bd = make_desc(b_addr + kk * 1024, BK * 128, 512, kSw128Base32);
-            mma_tf32_2sm(d_tmem, ad, bd, idesc_tf32_m256(), (kb > 0 || kk > 0) ? 1u : 0u);
+            const uint64_t bd = b_kmajor ? make_desc(b_addr + kk * 32, 16, 1024, kSw128)
+                                         : make_desc(b_addr + kk * 1024, BK * 128, 512, kSw128Base32);
+            mma_tf32_2sm(d_tmem, ad, bd, idesc_tf32_m256(b_kmajor ? 0u : 1u), (kb > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit_2sm(&empty[stage]);  // both CTAs' stage buffers free once these complete
           if (++stage == STAGES2) {
@@ -685,25 +736,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
         const uint32_t taddr = tmem_base + acc * BN + c0 + ((uint32_t)(q * 32) << 16);
         TMEM_LD_32x32b_x32(taddr, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (p.tma_store) {
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(stg + lane * 32 + ((j ^ (lane & 7)) * 4)) =
-                make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
-                            __uint_as_float(r[4 * j + 3]));
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) tma_store_2d(&maps.c, stg, tn * BN + c0, row0);
-        } else {
-          const int row = row0 + lane, col0 = tn * BN + c0;
-          if (row < p.M) {
-            float* dst = p.C + (int64_t)row * p.ldc + col0;
-            for (int v = 0; v < 32; ++v)
-              if (col0 + v < p.N) dst[v] = __uint_as_float(r[v]);
-          }
-        }
+        epilogue_chunk(p, maps, r, stg, lane, row0, tn, ti, c0);
       }
       tc_fence_before();
       __syncwarp();
@@ -839,6 +872,15 @@ bool make_map(atc_ctx* ctx, CUtensorMap* m, const float* base, uint64_t rows, ui
   return true;
 }
 
+// ATC_TC_2SM=0 disables the cta_group::2 kernel (A/B measurement)
+int umma2_enabled() {
+  static const int on = [] {
+    const char* e = std::getenv("ATC_TC_2SM");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return on;
+}
+
 // ATC_TC_TMA_STORE=0 disables the TMA-store epilogue (A/B measurement)
 int tma_store_enabled() {
   static const int enabled = [] {
@@ -961,12 +1003,8 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
   p.splits = precision == ATC_PREC_3XTF32 ? 3 : 1;
   // TMA-store epilogue when C's row pitch is a multiple of 16 bytes
   p.tma_store = tma_store_enabled() && (n % 4) == 0 ? 1 : 0;
-  // cta_group::2 (M = 256 per CTA pair) for the MN-major sgemm; ATC_TC_2SM=0 disables
-  static const int umma2_on = [] {
-    const char* e = std::getenv("ATC_TC_2SM");
-    return e && e[0] == '0' ? 0 : 1;
-  }();
-  p.umma2 = umma2_on && p.conv == 0 && p.tiles_m >= 2 ? 1 : 0;
+  // cta_group::2 (M = 256 per CTA pair) for the MN-major sgemm
+  p.umma2 = umma2_enabled() && p.conv == 0 && p.tiles_m >= 2 ? 1 : 0;
   if (p.tma_store && !make_map(ctx, &maps.c, dC, m, n, n, 32, 32, false)) return ATC_ERR_CUDA;
   if (b_kmajor) {
     float* bt = (float*)atc_ctx_scratch(ctx, 14, (size_t)k * n * 4 * (p.splits == 3 ? 2 : 1));
@@ -1086,9 +1124,12 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
   k_weights_krsc<<<grid_for(wn), 256, 0, st>>>(d_w, wh, wl, (int)k, (int)c, (int)r, (int)s);
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
+  // cta_group::2 (M = 256 filters per CTA pair) when there are >= 2 filter tiles;
+  // each CTA then loads half of the pixel rows (K-major box of BN/2 rows)
+  const bool umma2 = umma2_enabled() && k > BM && !direct;  // (1x1 direct: slower on the pair kernel)
   auto bmap = [&](CUtensorMap* m, const float* base) {
     return direct ? make_map(ctx, m, base, n * c, hw, hw, 32, BK, true)   // [N*C][H*W], MN-major chunks
-                  : make_map(ctx, m, base, n * hw, c, c, BK, BN, false);  // NHWC [N*H*W][C], K-major
+                  : make_map(ctx, m, base, n * hw, c, c, BK, umma2 ? BN / 2 : BN, false);  // NHWC, K-major
   };
   if (!make_map(ctx, &maps.a[0], wh, k, r * s * c, r * s * c, BK, BM, false) || !bmap(&maps.b[0], ih))
     return ATC_ERR_CUDA;
@@ -1124,6 +1165,7 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
     p.tiles_img = 1;
   }
   p.pair = use_pair(p);
+  p.umma2 = umma2 ? 1 : 0;
   // 1x1 direct: the output is a [N*K][OH*OW] matrix (hw % 4 == 0): TMA-store epilogue
   p.tma_store = direct && tma_store_enabled() ? 1 : 0;
   if (p.tma_store && !make_map(ctx, &maps.c, d_out, n * k, oh * ow, oh * ow, 32, 32, false)) return ATC_ERR_CUDA;
