@@ -328,6 +328,9 @@ def main():
                                        "profiles/r1_ncu_summary.json)",
                      "peak_kind": peak_kind, "kernel": "K1 screen (k_screen_conv_pairs + k_screen_rows)",
                      "kernel_ms_per_step": prof.screen_ms,
+                     "kernel_ms_note": "sum of the K1 launch durations of one profiled step (CUDA events); the "
+                                       "gemm and conv branches of a sweep run concurrently, so this exceeds their "
+                                       "wall-clock share",
                      "limiter": "instruction issue (integer ALU); operands are L1/L2 resident",
                      "issue_slots_busy_pct": k1.get("issue_slots_busy_pct"), "ipc_per_sm": k1.get("ipc_per_sm"),
                      "survey_operand_GBps": survey_bytes / screen_s / 1e9 if screen_s > 0 else None,
