@@ -44,9 +44,13 @@ __global__ void k_screen_rows(TestsetView ts, SpecView sp, const uint8_t* perms,
 __global__ void k_confirm_warp(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                                uint64_t surv_cap, int32_t* surv_keys, const uint32_t* sel,
                                const unsigned long long* sel_cnt, int mode);
+__global__ void k_confirm_pre(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
+                              const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
+                              uint32_t* pend, unsigned long long* pend_cnt, int mode);
 __global__ void k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                              const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
-                             uint32_t* next, unsigned long long* next_cnt, int mode);
+                             const uint32_t* pend, const unsigned long long* pend_cnt, uint32_t* next,
+                             unsigned long long* next_cnt, int mode);
 __global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
                              const int32_t* surv_keys, int32_t* keys);
 __global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason);
@@ -741,22 +745,32 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     atc_set_error(ctx, "scratch allocation failed (K2)");
     return ATC_ERR_CUDA;
   }
-  cudaMemsetAsync(next_cnt, 0, 8, st);
+  cudaMemsetAsync(next_cnt, 0, 16, st);  // next_cnt[0]: t=0 passers, next_cnt[1]: K2-pre pending
+  uint32_t* pend = (uint32_t*)atc_ctx_scratch(ctx, 24, surv_cap * 4 + 16);
+  if (!pend) {
+    atc_set_error(ctx, "scratch allocation failed (K2)");
+    return ATC_ERR_CUDA;
+  }
   // grids bounded by the most work there can be (survivors <= bindings screened):
   // small spaces launch a few CTAs instead of 8 per SM
   const uint64_t max_surv = std::min<uint64_t>(n, surv_cap);
   const unsigned g_t0 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 7) / 8, ctx->sm_count * 8));
   const unsigned g_t1 = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>((max_surv * (uint64_t)std::max(ts->T - 1, 0) + 7) / 8, ctx->sm_count * 8));
-  k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, next, next_cnt,
-                                     ctx->mode);
+  const bool pre = sp.sem == ATC_SEM_CONV2D;
+  if (pre)
+    k_confirm_pre<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 255) / 256, ctx->sm_count * 8)),
+                    256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pend, next_cnt + 1,
+                                  ctx->mode);
+  k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pre ? pend : nullptr,
+                                     next_cnt + 1, next, next_cnt, ctx->mode);
   k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, next, next_cnt, ctx->mode);
   if (ctx->prof) {
     cudaEventRecord(e2.second, st);
     ctx->prof_confirm.push_back(e2);
   }
   if (keys) k_merge_keys<<<64, 256, 0, st>>>(surv, surv_cnt, surv_cap, surv_keys, keys);
-  if (ctx->prof) ctx->prof_kernels += keys ? 4 : 3;  /* K1, K2a, K2b (+ merge) */
+  if (ctx->prof) ctx->prof_kernels += (keys ? 4 : 3) + (pre ? 1 : 0); /* K1, (K2-pre), K2a, K2b (+ merge) */
   if (!atc_cuda_ok(ctx, cudaGetLastError(), "evaluator launch")) return ATC_ERR_CUDA;
   return ATC_OK;
 }

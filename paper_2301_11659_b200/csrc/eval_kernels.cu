@@ -531,15 +531,87 @@ __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const Bin
 // K2a: one WARP per survivor, test t = 0 only.  Most K1 survivors agree with the
 // user program at output positions 0 and 1 but not elsewhere.  Survivors of t = 0
 // are appended to `next` for K2b.
-__global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src,
-                                                    const uint64_t* surv, const unsigned long long* surv_cnt,
-                                                    uint64_t surv_cap, int32_t* surv_keys, uint32_t* next,
-                                                    unsigned long long* next_cnt, int mode) {
-  const int lane = threadIdx.x & 31;
+// K2-pre (conv): one THREAD per survivor, test t = 0, a few probe outputs — where
+// wrong bindings that agree at positions 0 and 1 first differ: position 2, the
+// first output of row 1 / filter 1 / image 1, the one after the original's last
+// write.  A mismatch there decides the binding (reason 1 at t = 0, as the full
+// check would); the rest go to K2a through `pend`.  Gemm spaces pass everything.
+__global__ void __launch_bounds__(256) k_confirm_pre(TestsetView ts, SpecView sp, BindingSource src,
+                                                     const uint64_t* surv, const unsigned long long* surv_cnt,
+                                                     uint64_t surv_cap, int32_t* surv_keys, uint32_t* pend,
+                                                     unsigned long long* pend_cnt, int mode) {
   unsigned long long cnt = *surv_cnt;
   if (cnt > surv_cap) cnt = surv_cap;
+  for (uint64_t si = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; si < cnt;
+       si += (uint64_t)gridDim.x * blockDim.x) {
+    bool decided = false;
+    if (sp.sem == ATC_SEM_CONV2D) {
+      int ptr_of[ATC_MAX_ARRAYS], int_of[ATC_MAX_SIZES];
+      decode_binding(src, sp, ts.nI, surv[si], ptr_of, int_of);
+      int64_t sz[ATC_MAX_SIZES];
+      for (int q = 0; q < sp.nS; ++q) sz[q] = ts.ints[int_of[q]];
+      int r = 0;
+      if (!ts.test_ok[0]) r = ATC_FAIL_TESTSET;
+      if (!r) r = extent_check(sp, sz, ptr_of, ts.region_len);
+      Dims d;
+      resolve_dims(sp, sz, d);
+      if (!r) r = ub_check(sp, d, ptr_of, ts.region_len);
+      if (r) {
+        surv_keys[si] = fail_key(0, r);
+        decided = true;
+      } else {
+        const int pA = ptr_of[sp.arr_of_role[0]], pB = ptr_of[sp.arr_of_role[1]], pC = ptr_of[sp.arr_of_role[2]];
+        const double* __restrict__ A = ts.init + ts.region_off[pA];
+        const double* __restrict__ B = ts.init + ts.region_off[pB];
+        const double* __restrict__ F = ts.fin + ts.region_off[pC];
+        const bool f32 = ts.is_f32[pC] != 0;
+        const int N = (int)d.cn, C = (int)d.cc, H = (int)d.ch, W = (int)d.cw, K = (int)d.ck, R = (int)d.cr,
+                  S = (int)d.cs, OH = (int)d.coh, OW = (int)d.cow;
+        const int64_t wext = (int64_t)N * K * OH * OW;
+        const int dmax = ts.dirty_max[pC];
+        if (dmax >= wext) {
+          surv_keys[si] = fail_key(0, ATC_FAIL_MISMATCH);
+          decided = true;
+        } else {
+          const int64_t probes[6] = {2, OW, (int64_t)OW * OH, (int64_t)OW * OH * K, (int64_t)dmax + 1, 3};
+          for (int i = 0; i < 6 && !decided; ++i) {
+            const int64_t o = probes[i];
+            if (o < 2 || o >= wext) continue;
+            int rem = (int)o;
+            const int x = rem % OW; rem /= OW;
+            const int y = rem % OH; rem /= OH;
+            const int q = rem % K;
+            const int b = rem / K;
+            const double* in = A + ((b * C) * H + y) * W + x;
+            const double* wt = B + (q * C) * R * S;
+            if (position_mismatch(
+                    mode, C * R * S, __ldg(F + o), f32, [&] { return conv_dot64(in, wt, C, R, S, H, W); },
+                    [&](float& Sa) { return conv_dot32(in, wt, C, R, S, H, W, Sa); })) {
+              surv_keys[si] = fail_key(0, ATC_FAIL_MISMATCH);
+              decided = true;
+            }
+          }
+        }
+      }
+    }
+    if (!decided) pend[atomicAdd(pend_cnt, 1ull)] = (uint32_t)si;
+  }
+}
+
+// K2a: one WARP per pending survivor (all survivors without K2-pre), test t = 0
+// only: every written output, 32 per step.  Survivors of t = 0 are appended to
+// `next` for K2b.
+__global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src,
+                                                    const uint64_t* surv, const unsigned long long* surv_cnt,
+                                                    uint64_t surv_cap, int32_t* surv_keys, const uint32_t* pend,
+                                                    const unsigned long long* pend_cnt, uint32_t* next,
+                                                    unsigned long long* next_cnt, int mode) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long cnt = pend ? *pend_cnt : *surv_cnt;
+  if (cnt > surv_cap) cnt = surv_cap;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
-  for (uint64_t si = (uint64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; si < cnt; si += warps) {
+  for (uint64_t wi = (uint64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; wi < cnt; wi += warps) {
+    const uint64_t si = pend ? pend[wi] : wi;
     const int r = warp_verdict(ts, sp, src, surv[si], 0, mode, lane);
     if (lane == 0) {
       if (r) {
