@@ -26,6 +26,8 @@ __global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_
                          unsigned long long* reason_hist, int mode);
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out, uint8_t* out1);
+__global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
+                                  uint8_t* out, uint8_t* out1);
 __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
                               uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                               unsigned long long* reason_hist);
@@ -980,8 +982,15 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
     uint8_t* tab1 = pairs ? tab + (e.table_bytes + 15) / 16 * 16 : nullptr;
     e.pt.table = tab;
     e.plan.pt = e.pt;
-    k_pos0_table<<<(unsigned)std::min<uint64_t>((e.table_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16), 256, 0,
-                   st>>>(ts->view, sp, d_perms, n_perms, e.pt, tab, tab1);
+    // conv with the canonical key (c first): one running sum per (perm, h, w, r, s)
+    if (sp.sem == ATC_SEM_CONV2D && e.pt.R == 5 && e.plan.key_stride[1] == 1 && e.use_rows &&
+        conv_thresholds_ok(sp, e.plan, ts->nI))
+      k_pos0_table_conv<<<(unsigned)std::min<uint64_t>((e.table_bytes / ts->nI + 255) / 256,
+                                                       (uint64_t)ctx->sm_count * 16),
+                          256, 0, st>>>(ts->view, sp, d_perms, n_perms, e.pt, tab, tab1);
+    else
+      k_pos0_table<<<(unsigned)std::min<uint64_t>((e.table_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16), 256,
+                     0, st>>>(ts->view, sp, d_perms, n_perms, e.pt, tab, tab1);
     if (ctx->prof) ctx->prof_kernels += 1;
     e.plan.cmask = e.plan.cmask1 = nullptr;
     if (pairs) {

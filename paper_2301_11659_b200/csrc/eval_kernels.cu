@@ -249,6 +249,68 @@ __global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need) {
 
 // out1 (conv, optional): the same verdict at output position 1 for bindings with
 // tc_ow >= 2, i.e. output (b, q, y, x) = (0, 0, 0, 1): the input window shifted by one.
+// Conv position-0/1 tables with one accumulation per (perm, h, w, r, s): the
+// reference sums z (channel) outermost, so the sum for c channels is the running
+// sum after z = c - 1 — every value of tc_c is read off one pass (same order, same
+// bits as k_pos0_table's per-entry loops).  Lanes of a warp share (r, s).
+__global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
+                                  uint8_t* out, uint8_t* out1) {
+  const uint64_t nI = (uint64_t)ts.nI, nI2 = nI * nI;
+  const uint64_t inner = nI2 * (uint64_t)n_perms;  // (h, w, perm) combinations
+  const uint64_t total = inner * nI2;              // x (r, s)
+  int64_t cmax_all = 0;
+  for (int j = 0; j < ts.nI; ++j) cmax_all = max(cmax_all, ts.ints[j]);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t rs_d = i / inner, hwp = i - rs_d * inner;
+    const uint64_t perm = hwp / nI2, hw_d = hwp - perm * nI2;
+    const uint64_t r_d = rs_d % nI, s_d = rs_d / nI, h_d = hw_d % nI, w_d = hw_d / nI;
+    const int64_t h = ts.ints[h_d], w = ts.ints[w_d], r = ts.ints[r_d], s = ts.ints[s_d];
+    const uint64_t base = perm * pt.per_perm + nI * (h_d + nI * (w_d + nI * (r_d + nI * s_d)));  // + c digit
+    const int pA = perms[perm * sp.nA + sp.arr_of_role[0]];
+    const int pB = perms[perm * sp.nA + sp.arr_of_role[1]];
+    const int pC = perms[perm * sp.nA + sp.arr_of_role[2]];
+    const double* A = ts.init + ts.region_off[pA];
+    const double* B = ts.init + ts.region_off[pB];
+    const double want = ts.fin[ts.region_off[pC]];
+    const bool f32 = ts.is_f32[pC] != 0;
+    const int64_t lenA = ts.region_len[pA], lenB = ts.region_len[pB];
+    const bool pos1 = out1 && ts.region_len[pC] > 1;
+    const double want1 = pos1 ? ts.fin[ts.region_off[pC] + 1] : 0.0;
+    const uint8_t empty_res = mismatch(round_region(0.0, f32), want, f32) ? 1 : 0;
+    const bool shape_ok = r >= 1 && s >= 1 && h >= 0 && w >= 0;
+    // entries whose c digit is < 1 (or a bad shape): the empty sum; others: 2 until computed
+    for (uint64_t j = 0; j < nI; ++j) {
+      const bool empty_sum = !shape_ok || ts.ints[j] < 1;
+      out[base + j] = empty_sum ? empty_res : 2;
+      if (out1) out1[base + j] = 2;
+    }
+    if (!shape_ok) continue;
+    double acc = 0.0, acc1 = 0.0;
+    bool v1_live = pos1;
+    for (int64_t z = 0; z < cmax_all; ++z) {
+      const int64_t c = z + 1;
+      const int64_t imax = ((c - 1) * h + (r - 1)) * w + (s - 1), wmax = c * r * s - 1;
+      const bool v0 = imax < lenA && wmax < lenB;  // imax >= 0 here
+      v1_live = v1_live && imax + 1 < lenA && wmax < lenB;
+      if (!v0) break;  // monotone in c: no larger c is tabulated either
+      for (int64_t u = 0; u < r; ++u) {
+        const double* a = A + (z * h + u) * w;
+        const double* b = B + (z * r + u) * s;
+        for (int64_t t = 0; t < s; ++t) {
+          const double bv = b[t];
+          acc = dadd(acc, dmul(a[t], bv));
+          if (v1_live) acc1 = dadd(acc1, dmul(a[t + 1], bv));
+        }
+      }
+      for (uint64_t j = 0; j < nI; ++j)
+        if (ts.ints[j] == c) {
+          out[base + j] = mismatch(round_region(acc, f32), want, f32) ? 1 : 0;
+          if (out1 && v1_live) out1[base + j] = mismatch(round_region(acc1, f32), want1, f32) ? 1 : 0;
+        }
+    }
+  }
+}
+
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out, uint8_t* out1) {
   const uint64_t total = (uint64_t)n_perms * pt.per_perm;
