@@ -595,84 +595,104 @@ __global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const
   const uint64_t planes_per_perm = size_maps / (uint64_t)nI2;
   const uint32_t magic = (uint32_t)(0xFFFFFFFFull / (uint32_t)nI) + 1u;  // n / nI = umulhi(n, magic), n < 2^27
   unsigned int cnt1 = 0, cnt2 = 0, cnt3 = 0, cnt4 = 0;
-  const uint64_t plane_lo = begin / nI2, plane_hi = (end + nI2 - 1) / nI2;
-  for (uint64_t pl = plane_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; pl < plane_hi;
-       pl += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t p0 = pl * nI2;
-    const uint64_t lo = p0 < begin ? begin : p0, hi = p0 + nI2 > end ? end : p0 + nI2;
-    const unsigned int n_here = (unsigned int)(hi - lo);
+  // a thread owns a "cube": the nI planes sharing the permutation and digits 3..8
+  // (all values of tc_h, digit 2); everything free of h is computed once per cube
+  const uint64_t nI3 = (uint64_t)nI2 * nI;
+  const uint64_t cubes_per_perm = planes_per_perm / (uint64_t)nI;
+  const uint64_t cube_lo = begin / nI3, cube_hi = (end + nI3 - 1) / nI3;
+  for (uint64_t cb = cube_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; cb < cube_hi;
+       cb += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c0b = cb * nI3;
     if (!test_ok0) {
-      cnt3 += n_here;
+      const uint64_t lo = c0b < begin ? begin : c0b, hi = c0b + nI3 > end ? end : c0b + nI3;
+      cnt3 += (unsigned int)(hi - lo);
       continue;
     }
-    const uint64_t perm = (pl >> 32) == 0 && (planes_per_perm >> 32) == 0
-                              ? (uint64_t)((uint32_t)pl / (uint32_t)planes_per_perm)
-                              : pl / planes_per_perm;
+    const uint64_t perm = (cb >> 32) == 0 && (cubes_per_perm >> 32) == 0
+                              ? (uint64_t)((uint32_t)cb / (uint32_t)cubes_per_perm)
+                              : cb / cubes_per_perm;
     int digit[NS];
     {
-      uint64_t s = pl - perm * planes_per_perm;  // digits 2..8
+      uint64_t s = cb - perm * cubes_per_perm;  // digits 3..8
       if (s < (1ull << 27)) {
         uint32_t s32 = (uint32_t)s;
 #pragma unroll
-        for (int q = 2; q < NS; ++q) {
+        for (int q = 3; q < NS; ++q) {
           const uint32_t dq = __umulhi(s32, magic);
           digit[q] = (int)(s32 - dq * (uint32_t)nI);
           s32 = dq;
         }
       } else {
 #pragma unroll
-        for (int q = 2; q < NS; ++q) {
+        for (int q = 3; q < NS; ++q) {
           const uint64_t dq = s / (uint64_t)nI;
           digit[q] = (int)(s - dq * (uint64_t)nI);
           s = dq;
         }
       }
     }
-    const int32_t ch = s_u[digit[2]], cw = s_u[digit[3]], ck = s_u[digit[4]], cr = s_u[digit[5]];
+    const int32_t cw = s_u[digit[3]], ck = s_u[digit[4]], cr = s_u[digit[5]];
     const int32_t cs = s_u[digit[6]], coh = s_u[digit[7]], cow = s_u[digit[8]];
-    if (min(min(min(ch, cw), min(ck, cr)), min(min(cs, coh), cow)) < 1) {
-      cnt2 += n_here;  // a dim of the plane < 1: "size is not positive" for every binding
-      continue;
-    }
-    const M128 range = (lo == p0 && hi == p0 + nI2) ? all : bit_range((int)(lo - p0), (int)(hi - p0));
+    const bool cube_bad = min(min(min(cw, ck), min(cr, cs)), min(coh, cow)) < 1;
     const int p_in = perms[perm * 3 + 0], p_w = perms[perm * 3 + 1], p_out = perms[perm * 3 + 2];
     // region lengths are < 2^31 (atc_testsets_upload): 32-bit divisions
     const uint32_t len_in = (uint32_t)ts.region_len[p_in], len_w = (uint32_t)ts.region_len[p_w];
     const uint32_t len_out = (uint32_t)ts.region_len[p_out];
-    const int32_t hw = ch * cw, krs = ck * cr * cs, ext_out = ck * coh * cow;
-    const float r_out = __frcp_rn((float)ext_out), r_hw = __frcp_rn((float)hw);
-    const int c_max = div_cap(len_w, krs, __frcp_rn((float)krs));
-    const int d_out = div_cap(len_out, ext_out, r_out);
-    const int a_in = lut_n ? div_capn(len_in, hw, r_hw, qcap) : (int)(len_in / (uint32_t)hw);
-    const M128 dm = range & (x_lt1 | c_lt1 | s_gtc[c_max] | s_gtx[d_out] | gt_prod(a_in));
-    M128 ok = range & ~dm, um{0, 0}, mm{0, 0};
-    if (any(ok)) {
-      const int32_t q_in = -hw + (coh + cr - 2) * cw + (cow + cs - 2);
-      const int64_t alim = (int64_t)len_in - q_in;  // UB iff x*c*h*w >= alim (< 2^32)
-      const uint32_t am1 = (uint32_t)(alim - 1);
-      um = alim <= 0 ? ok : (ok & gt_prod(lut_n ? div_capn(am1, hw, r_hw, qcap) : (int)(am1 / (uint32_t)hw)));
-      ok = ok & ~um;
-      if (any(ok)) {
-        uint32_t ckey = (uint32_t)perm * cperm;
-#pragma unroll
-        for (int q = 2; q < NS; ++q) ckey += (uint32_t)digit[q] * cks[q];
-        M128 tab = s_rowx[__ldg(plan.cmask + ckey)];
-        // output position 1 is (0, 0, 0, 1) when ow >= 2: its tabulated verdict too
-        if (plan.cmask1 && cow >= 2) tab = tab | s_rowx[__ldg(plan.cmask1 + ckey)];
-        const int dmax = ts.dirty_max[p_out];
-        mm = ok & (~s_gtx[dmax < 0 ? 0 : div_cap(dmax, ext_out, r_out)] | tab);
-        ok = ok & ~mm;
-      }
+    const int32_t krs = ck * cr * cs, ext_out = ck * coh * cow;
+    const float r_out = __frcp_rn((float)ext_out);
+    int c_max = 0, d_out = 0, mth = 0;
+    if (!cube_bad) {
+      c_max = div_cap(len_w, krs, __frcp_rn((float)krs));
+      d_out = div_cap(len_out, ext_out, r_out);
+      const int dmax = ts.dirty_max[p_out];
+      mth = dmax < 0 ? 0 : div_cap(dmax, ext_out, r_out);
     }
-    cnt2 += popc(dm);
-    cnt4 += popc(um);
-    cnt1 += popc(mm);
-    if (any(ok)) {
-      unsigned long long slot = atomicAdd(surv_cnt, (unsigned long long)popc(ok));
-      for (uint64_t w = ok.lo; w; w &= w - 1, ++slot)
-        if (slot < surv_cap) surv[slot] = p0 + (uint64_t)(__ffsll((long long)w) - 1) - begin;
-      for (uint64_t w = ok.hi; w; w &= w - 1, ++slot)
-        if (slot < surv_cap) surv[slot] = p0 + 64 + (uint64_t)(__ffsll((long long)w) - 1) - begin;
+    const M128 cube_dm = x_lt1 | c_lt1 | s_gtc[c_max] | s_gtx[d_out];  // h-free dispatch failures
+    const M128 dirty_fail = ~s_gtx[mth];
+    const int32_t q_rest = (coh + cr - 2) * cw + (cow + cs - 2);   // Q = -h*w + q_rest
+    uint32_t ckey0 = (uint32_t)perm * cperm;
+#pragma unroll
+    for (int q = 3; q < NS; ++q) ckey0 += (uint32_t)digit[q] * cks[q];
+    for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
+      const uint64_t p0 = c0b + (uint64_t)hd * nI2;
+      if (p0 + nI2 <= begin || p0 >= end) continue;
+      const uint64_t lo = p0 < begin ? begin : p0, hi = p0 + nI2 > end ? end : p0 + nI2;
+      const int32_t ch = s_u[hd];
+      if (cube_bad || ch < 1) {
+        cnt2 += (unsigned int)(hi - lo);  // a dim of the plane < 1: "size is not positive" for every binding
+        continue;
+      }
+      const M128 range = (lo == p0 && hi == p0 + nI2) ? all : bit_range((int)(lo - p0), (int)(hi - p0));
+      const int32_t hw = ch * cw;
+      const float r_hw = __frcp_rn((float)hw);
+      const int a_in = lut_n ? div_capn(len_in, hw, r_hw, qcap) : (int)(len_in / (uint32_t)hw);
+      const M128 dm = range & (cube_dm | gt_prod(a_in));
+      M128 ok = range & ~dm, um{0, 0}, mm{0, 0};
+      if (any(ok)) {
+        const int32_t q_in = -hw + q_rest;
+        const int64_t alim = (int64_t)len_in - q_in;  // UB iff x*c*h*w >= alim (< 2^32)
+        const uint32_t am1 = (uint32_t)(alim - 1);
+        um = alim <= 0 ? ok : (ok & gt_prod(lut_n ? div_capn(am1, hw, r_hw, qcap) : (int)(am1 / (uint32_t)hw)));
+        ok = ok & ~um;
+        if (any(ok)) {
+          const uint32_t ckey = ckey0 + (uint32_t)hd * cks[2];
+          M128 tab = s_rowx[__ldg(plan.cmask + ckey)];
+          // output position 1 is (0, 0, 0, 1) when ow >= 2: its tabulated verdict too
+          if (plan.cmask1 && cow >= 2) tab = tab | s_rowx[__ldg(plan.cmask1 + ckey)];
+          mm = ok & (dirty_fail | tab);
+          ok = ok & ~mm;
+        }
+      }
+      cnt2 += popc(dm);
+      cnt4 += popc(um);
+      cnt1 += popc(mm);
+      if (any(ok)) {
+        unsigned long long slot = atomicAdd(surv_cnt, (unsigned long long)popc(ok));
+        for (uint64_t w = ok.lo; w; w &= w - 1, ++slot)
+          if (slot < surv_cap) surv[slot] = p0 + (uint64_t)(__ffsll((long long)w) - 1) - begin;
+        for (uint64_t w = ok.hi; w; w &= w - 1, ++slot)
+          if (slot < surv_cap) surv[slot] = p0 + 64 + (uint64_t)(__ffsll((long long)w) - 1) - begin;
+      }
     }
   }
   unsigned int cnt[ATC_REASON_COUNT] = {0, cnt1, cnt2, cnt3, cnt4};
