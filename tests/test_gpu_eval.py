@@ -195,6 +195,8 @@ CONV_VARIANTS = {
     "zero_int": lambda ts: _with_int(ts, 1, 0),
     "neg_int": lambda ts: _with_int(ts, 0, -3),
     "test0_failed": lambda ts: _with_ok(ts, 0),
+    # a size above 200: 64-bit index arithmetic (the generic row screen)
+    "big_int": lambda ts: _with_int(ts, 2, 300),
 }
 
 
@@ -244,6 +246,7 @@ GEMM_VARIANTS = {
     "int0_is_2": lambda ts: _with_int(ts, 0, 2),
     "int2_is_0": lambda ts: _with_int(ts, 2, 0),
     "c_300": lambda ts: _shrunk(ts, [None, None, 300, None]),
+    "big_int": lambda ts: _with_int(ts, 1, 250),
 }
 
 
