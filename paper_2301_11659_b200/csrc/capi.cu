@@ -710,7 +710,9 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
         for (int k = 0; k < ts->nI; ++k) pmax = std::max<int64_t>(pmax, ts->h_ints[i] * ts->h_ints[k]);
       const int lut_n = pmax < 4096 ? (int)pmax + 1 : 0;
       const size_t smem = ((size_t)16 << ts->nI) + (size_t)(lut_n + 15) / 16 * 16;
-      k_screen_conv_pairs<<<g2, kScreenThreads, smem, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
+      // one wave (3 CTAs per SM at 80 registers): each CTA builds its tables once
+      const unsigned g3 = std::min<unsigned>(g2, (unsigned)ctx->sm_count * 3);
+      k_screen_conv_pairs<<<g3, kScreenThreads, smem, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
                                                             surv_cap, surv_cnt, hist, lut_n);
     } else if (i32 && conv_thresholds_ok(sp, *plan, ts->nI)) {
       k_screen_conv_planes<<<g2, kScreenThreads, 0, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
