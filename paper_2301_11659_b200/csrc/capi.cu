@@ -260,10 +260,12 @@ atc_ctx* atc_create(int device) {
   if (!atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
 
       !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->free_ev, cudaEventDisableTiming), "cudaEventCreate") ||
-      !atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
-      !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming), "cudaEventCreate") ||
-      !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming), "cudaEventCreate"))
+      !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming), "cudaEventCreate"))
     ctx->broken = true;
+  for (int k = 0; k < atc_ctx::kSideStreams && !ctx->broken; ++k)
+    if (!atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->side_stream[k], cudaStreamNonBlocking), "cudaStreamCreate") ||
+        !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->join_ev[k], cudaEventDisableTiming), "cudaEventCreate"))
+      ctx->broken = true;
   for (auto& cs : ctx->copy_stream)
     if (!ctx->broken && !atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate"))
       ctx->broken = true;
@@ -287,9 +289,11 @@ void atc_destroy(atc_ctx* ctx) {
     for (auto& cs : ctx->copy_stream)
       if (cs) cudaStreamDestroy(cs);
     if (ctx->free_ev) cudaEventDestroy(ctx->free_ev);
-    if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
+    for (int k = 0; k < atc_ctx::kSideStreams; ++k) {
+      if (ctx->side_stream[k]) cudaStreamDestroy(ctx->side_stream[k]);
+      if (ctx->join_ev[k]) cudaEventDestroy(ctx->join_ev[k]);
+    }
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
-    if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   }
   delete ctx;
 }
@@ -1136,30 +1140,32 @@ constexpr uint64_t kBatchStride = 2 + kResultPrefix;  // count, passing count, p
 
 size_t batch_res_words(int n) { return (size_t)n * (kBatchStride + 8); }
 
-// Two concurrent branches: conv spaces (large K1 launches) on the caller's
-// stream, gemm spaces (chains of small latency-bound kernels) on the side stream
-// with their own scratch (slot + 32); they fork from and join back into `st`, so
-// a captured graph has the same two branches.
+// Concurrent branches: conv spaces (large K1 launches) on the caller's stream,
+// gemm spaces (chains of small latency-bound kernels) round-robin on the side
+// streams with their own scratch (slot + 32 * (k + 1)); they fork from and join
+// back into `st`, so a captured graph has the same branches.
 int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_uploads) {
   const uint64_t chunk_cap = kEnumChunkCap;
   unsigned long long* hist = reinterpret_cast<unsigned long long*>(b->res + (size_t)b->n * kBatchStride);
   cudaMemsetAsync(b->res, 0, batch_res_words(b->n) * 8, st);
-  bool has_main = false, has_side = false;
-  for (int j = 0; j < b->n; ++j)
-    if (b->batched[j]) (b->plans[j].sp.sem == ATC_SEM_CONV2D ? has_main : has_side) = true;
-  const bool split = has_main && has_side;
+  int n_side = 0;
+  for (int j = 0; j < b->n; ++j) n_side += b->batched[j] && b->plans[j].sp.sem != ATC_SEM_CONV2D;
+  const bool split = n_side > 1 || (n_side == 1 && n_side < b->n);
   if (split) {
     cudaEventRecord(ctx->fork_ev, st);
-    cudaStreamWaitEvent(ctx->side_stream, ctx->fork_ev, 0);
+    for (int k = 0; k < atc_ctx::kSideStreams; ++k) cudaStreamWaitEvent(ctx->side_stream[k], ctx->fork_ev, 0);
   }
+  int side_next = 0;
   int rc = ATC_OK;
   for (int j = 0; j < b->n && rc == ATC_OK; ++j) {
     if (!b->batched[j]) continue;
     atc_enum_job& job = b->jobs[j];
     EnumPlan& e = b->plans[j];
     const bool side = split && e.sp.sem != ATC_SEM_CONV2D;
-    cudaStream_t js = side ? ctx->side_stream : st;
-    ctx->slot_base = side ? 32 : 0;
+    const int sk = side ? side_next : -1;
+    if (side) side_next = (side_next + 1) % atc_ctx::kSideStreams;
+    cudaStream_t js = side ? ctx->side_stream[sk] : st;
+    ctx->slot_base = side ? 32 * (sk + 1) : 0;
     uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
     int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, chunk_cap * 4);
     unsigned long long* cnt = (unsigned long long*)atc_ctx_scratch(ctx, 3, 64);
@@ -1182,10 +1188,11 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
     }
   }
   ctx->slot_base = 0;
-  if (split) {
-    cudaEventRecord(ctx->join_ev, ctx->side_stream);
-    cudaStreamWaitEvent(st, ctx->join_ev, 0);
-  }
+  if (split)
+    for (int k = 0; k < atc_ctx::kSideStreams; ++k) {
+      cudaEventRecord(ctx->join_ev[k], ctx->side_stream[k]);
+      cudaStreamWaitEvent(st, ctx->join_ev[k], 0);
+    }
   if (rc) return rc;
   if (!atc_cuda_ok(ctx, cudaMemcpyAsync(b->h_res, b->res, batch_res_words(b->n) * 8, cudaMemcpyDeviceToHost, st),
                    "D2H results"))

@@ -14,12 +14,14 @@ struct atc_ctx {
   std::string err;
   cudaStream_t stream = nullptr;
   // reusable device scratch, grown on demand (slot ids are per call site)
-  static constexpr int kSlots = 64;
-  // sweeps run gemm and conv spaces on two concurrent branches; the second
-  // branch's evaluator scratch lives at slot + 32 (set while enqueueing it)
+  // sweeps run conv spaces on the caller's stream and gemm spaces round-robin on
+  // kSideStreams concurrent side streams; side stream k's evaluator scratch lives
+  // at slot + 32 * (k + 1) (set while enqueueing it)
+  static constexpr int kSideStreams = 4;
+  static constexpr int kSlots = 32 * (kSideStreams + 1);
   int slot_base = 0;
-  cudaStream_t side_stream = nullptr;
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaStream_t side_stream[kSideStreams] = {};
+  cudaEvent_t fork_ev = nullptr, join_ev[kSideStreams] = {};
   void* scratch[kSlots] = {};
   size_t scratch_bytes[kSlots] = {};
   void* pinned[4] = {};
