@@ -338,7 +338,8 @@ def main():
                              "row, see bench.py); survey_operand_GBps is SURVEY 8d's 8 B x (extA+extB+extC) per "
                              "binding at t=0 — operand bytes the factorisation never streams, so it is not an HBM "
                              "utilisation.  The kernel is issue bound: see issue_slots_busy_pct (ncu)."},
-        "k2_confirm": {"ms_per_step": prof.confirm_ms, "survivors_per_step": prof.survivors},
+        "k2_confirm": {"ms_per_step": prof.confirm_ms, "survivors_per_step": prof.survivors,
+                       "note": "sum of K2 launch durations over the concurrent sweep streams (overlapping)"},
     }
     if not args.no_sgemm:
         # replaced-call backends: sgemm split along M, conv along batch, no collective
