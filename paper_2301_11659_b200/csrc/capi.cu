@@ -406,22 +406,68 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_
   };
   double* init = (double*)dmalloc(total * 8);
   double* fin = (double*)dmalloc(total * 8);
-  int64_t* ints = (int64_t*)dmalloc((size_t)T * nI * 8);
-  int32_t* isf = (int32_t*)dmalloc(nP * 4);
-  int64_t* rlen = (int64_t*)dmalloc(nP * 8);
-  int32_t* tok = (int32_t*)dmalloc(T * 4);
-  int64_t* roff = (int64_t*)dmalloc((size_t)T * nP * 8);
   int32_t* dpos = (int32_t*)dmalloc(dtotal * 4);
-  int64_t* dof = (int64_t*)dmalloc((size_t)T * nP * 8);
-  int32_t* dcnt = (int32_t*)dmalloc((size_t)T * nP * 4);
-  int32_t* dmax = (int32_t*)dmalloc((size_t)T * nP * 4);
-  if (!init || !fin || !ints || !isf || !rlen || !tok || !roff || !dpos || !dof || !dcnt || !dmax) {
+  // every small array in one block, built on the host and copied once:
+  // 8-byte arrays first, then the 4-byte ones
+  const size_t TP = (size_t)T * nP;
+  const int64_t nd = sd ? sd->diff_off[TP] : 0;
+  if (nd < 0) {
+    atc_set_error(ctx, "malformed final-minus-init offsets");
+    atc_testsets_free(ctx, h);
+    return ATC_ERR_ARG;
+  }
+  size_t mo = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = mo;
+    mo += (bytes + 15) / 16 * 16;
+    return o;
+  };
+  const size_t o_ints = take((size_t)T * nI * 8), o_rlen = take(nP * 8), o_roff = take(TP * 8),
+               o_dof = take(TP * 8);
+  const size_t o_seeds = sd ? take((size_t)T * 8) : 0, o_skips = sd ? take(TP * 8) : 0,
+               o_doffs = sd ? take((TP + 1) * 8) : 0, o_dvs = sd ? take((size_t)nd * 8) : 0;
+  const size_t o_isf = take(nP * 4), o_tok = take(T * 4), o_dcnt = take(TP * 4), o_dmax = take(TP * 4);
+  const size_t o_dps = sd ? take((size_t)nd * 4) : 0;
+  std::vector<uint8_t> meta(mo, 0);
+  auto put = [&](size_t o, const void* src, size_t bytes) {
+    if (bytes) std::memcpy(meta.data() + o, src, bytes);
+  };
+  put(o_ints, ts->int_values, (size_t)T * nI * 8);
+  put(o_rlen, ts->region_len, nP * 8);
+  put(o_roff, off.data(), TP * 8);
+  put(o_dof, doff.data(), TP * 8);
+  put(o_isf, ts->ptr_is_f32, nP * 4);
+  for (int t = 0; t < T; ++t) {
+    const int32_t ok_t = ts->test_ok ? (ts->test_ok[t] ? 1 : 0) : 1;
+    put(o_tok + t * 4, &ok_t, 4);
+  }
+  for (size_t i = 0; i < TP; ++i) {
+    const int32_t neg = -1;
+    put(o_dmax + i * 4, &neg, 4);  // dcnt stays 0
+  }
+  if (sd) {
+    put(o_seeds, sd->stream_seed, (size_t)T * 8);
+    put(o_skips, sd->stream_skip, TP * 8);
+    put(o_doffs, sd->diff_off, (TP + 1) * 8);
+    put(o_dvs, sd->diff_val, (size_t)nd * 8);
+    put(o_dps, sd->diff_pos, (size_t)nd * 4);
+  }
+  uint8_t* dmeta = (uint8_t*)dmalloc(mo);
+  if (!init || !fin || !dpos || !dmeta) {
     atc_set_error(ctx, "cudaMalloc failed for %lld region doubles", (long long)total);
     atc_testsets_free(ctx, h);
     return ATC_ERR_CUDA;
   }
-  // copies and the dirty-list kernel go to the copy stream, after any pool
-  // memory freed by earlier handles is no longer read by the compute stream
+  int64_t* ints = (int64_t*)(dmeta + o_ints);
+  int64_t* rlen = (int64_t*)(dmeta + o_rlen);
+  int64_t* roff = (int64_t*)(dmeta + o_roff);
+  int64_t* dof = (int64_t*)(dmeta + o_dof);
+  int32_t* isf = (int32_t*)(dmeta + o_isf);
+  int32_t* tok = (int32_t*)(dmeta + o_tok);
+  int32_t* dcnt = (int32_t*)(dmeta + o_dcnt);
+  int32_t* dmax = (int32_t*)(dmeta + o_dmax);
+  // copies and kernels go to a copy stream (round-robin), after any pool memory
+  // freed by earlier handles is no longer read by the compute stream
   const int cs = ctx->copy_next;
   ctx->copy_next = (cs + 1) % atc_ctx::kCopyStreams;
   cudaStream_t st = ctx->copy_stream[cs];
@@ -429,7 +475,7 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_
     cudaStreamWaitEvent(st, ctx->free_ev, 0);
     ctx->free_pending &= ~(1u << cs);
   }
-  bool ok = true;
+  bool ok = atc_cuda_ok(ctx, cudaMemcpyAsync(dmeta, meta.data(), mo, cudaMemcpyHostToDevice, st), "H2D metadata");
   // host regions that lie back to back in the same order as the device pool are
   // copied as one run (one DMA instead of T*n_ptrs)
   struct Run {
@@ -476,45 +522,20 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_
   if (sd && ok) {
     // regions from the tests' mt19937_64 streams (k_probe_regions), then the
     // final-minus-init entries scattered into the final images (k_apply_diffs)
-    const int64_t nd = sd->diff_off[(size_t)T * nP];
-    uint64_t* seeds = (uint64_t*)dmalloc((size_t)T * 8);
-    uint64_t* skips = (uint64_t*)dmalloc((size_t)T * nP * 8);
-    int64_t* doffs = (int64_t*)dmalloc(((size_t)T * nP + 1) * 8);
-    int32_t* dps = (int32_t*)dmalloc((size_t)std::max<int64_t>(nd, 1) * 4);
-    double* dvs = (double*)dmalloc((size_t)std::max<int64_t>(nd, 1) * 8);
-    ok = seeds && skips && doffs && dps && dvs;
-    if (!ok) atc_set_error(ctx, "device allocation failed (seeded test sets)");
     for (int64_t i = 0; ok && i < nd; ++i)
       if (sd->diff_pos[i] < 0) {
         atc_set_error(ctx, "negative final-minus-init position");
         ok = false;
       }
-    ok = ok && atc_cuda_ok(ctx, cudaMemcpyAsync(seeds, sd->stream_seed, (size_t)T * 8, cudaMemcpyHostToDevice, st), "H2D") &&
-         atc_cuda_ok(ctx, cudaMemcpyAsync(skips, sd->stream_skip, (size_t)T * nP * 8, cudaMemcpyHostToDevice, st), "H2D") &&
-         atc_cuda_ok(ctx, cudaMemcpyAsync(doffs, sd->diff_off, ((size_t)T * nP + 1) * 8, cudaMemcpyHostToDevice, st), "H2D") &&
-         (nd == 0 || (atc_cuda_ok(ctx, cudaMemcpyAsync(dps, sd->diff_pos, (size_t)nd * 4, cudaMemcpyHostToDevice, st), "H2D") &&
-                      atc_cuda_ok(ctx, cudaMemcpyAsync(dvs, sd->diff_val, (size_t)nd * 8, cudaMemcpyHostToDevice, st), "H2D")));
     if (ok) {
-      ok = atc_cuda_ok(ctx, cudaMemcpyAsync(rlen, ts->region_len, nP * 8, cudaMemcpyHostToDevice, st), "H2D") &&
-           atc_cuda_ok(ctx, cudaMemcpyAsync(isf, ts->ptr_is_f32, nP * 4, cudaMemcpyHostToDevice, st), "H2D") &&
-           atc_cuda_ok(ctx, cudaMemcpyAsync(roff, off.data(), (size_t)T * nP * 8, cudaMemcpyHostToDevice, st), "H2D");
-      k_probe_regions<<<T, 320, 0, st>>>(T, nP, seeds, skips, rlen, isf, roff, init, fin);
-      k_apply_diffs<<<(unsigned)(T * nP), 256, 0, st>>>(nP, rlen, roff, doffs, dps, dvs, fin);
+      k_probe_regions<<<T, 320, 0, st>>>(T, nP, (const uint64_t*)(dmeta + o_seeds),
+                                         (const uint64_t*)(dmeta + o_skips), rlen, isf, roff, init, fin);
+      k_apply_diffs<<<(unsigned)TP, 256, 0, st>>>(nP, rlen, roff, (const int64_t*)(dmeta + o_doffs),
+                                                  (const int32_t*)(dmeta + o_dps), (const double*)(dmeta + o_dvs),
+                                                  fin);
       ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_probe_regions");
     }
   }
-  std::vector<int32_t> tok_h(T, 1);
-  if (ts->test_ok)
-    for (int t = 0; t < T; ++t) tok_h[t] = ts->test_ok[t] ? 1 : 0;
-  std::vector<int32_t> zero((size_t)T * nP, 0), neg((size_t)T * nP, -1);
-  ok = ok && atc_cuda_ok(ctx, cudaMemcpyAsync(ints, ts->int_values, (size_t)T * nI * 8, cudaMemcpyHostToDevice, st), "H2D") &&
-       atc_cuda_ok(ctx, cudaMemcpyAsync(isf, ts->ptr_is_f32, nP * 4, cudaMemcpyHostToDevice, st), "H2D") &&
-       atc_cuda_ok(ctx, cudaMemcpyAsync(rlen, ts->region_len, nP * 8, cudaMemcpyHostToDevice, st), "H2D") &&
-       atc_cuda_ok(ctx, cudaMemcpyAsync(tok, tok_h.data(), T * 4, cudaMemcpyHostToDevice, st), "H2D") &&
-       atc_cuda_ok(ctx, cudaMemcpyAsync(roff, off.data(), (size_t)T * nP * 8, cudaMemcpyHostToDevice, st), "H2D") &&
-       atc_cuda_ok(ctx, cudaMemcpyAsync(dof, doff.data(), (size_t)T * nP * 8, cudaMemcpyHostToDevice, st), "H2D") &&
-       atc_cuda_ok(ctx, cudaMemcpyAsync(dcnt, zero.data(), (size_t)T * nP * 4, cudaMemcpyHostToDevice, st), "H2D") &&
-       atc_cuda_ok(ctx, cudaMemcpyAsync(dmax, neg.data(), (size_t)T * nP * 4, cudaMemcpyHostToDevice, st), "H2D");
   TestsetView& v = h->view;
   v.T = T;
   v.nI = nI;
