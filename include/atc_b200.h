@@ -167,6 +167,12 @@ typedef struct {
 } atc_seeded_testsets;
 int atc_testsets_upload_seeded(atc_ctx* ctx, const atc_seeded_testsets* ts, atc_testset_handle** out);
 
+/* New seeded contents for an existing handle (same n_tests, n_ints, n_ptrs,
+ * region lengths and element types), written in place after every evaluation
+ * already queued on the context's stream: prepared batches (atc_enum_batch_*)
+ * over the handle stay valid and pick the new contents up on their next run. */
+int atc_testsets_update_seeded(atc_ctx* ctx, atc_testset_handle* h, const atc_seeded_testsets* ts);
+
 /* Copies a handle's regions back ((t, pointer) regions back to back, unpadded;
  * either pointer may be NULL) — for checks and debugging. */
 int atc_testsets_download(atc_ctx* ctx, const atc_testset_handle* h, double* init, double* final_);

@@ -71,6 +71,16 @@ struct atc_testset_handle {
   std::vector<int64_t> h_ints;  // host copy of the int values
   std::vector<void*> allocations;
   cudaEvent_t ready = nullptr;  // uploads + dirty lists complete (recorded on the copy stream)
+  // layout, kept for in-place updates (atc_testsets_update_seeded)
+  int cs = 0;                   // the copy stream all of this handle's uploads use
+  std::vector<int64_t> lens, off, doff;
+  std::vector<int32_t> is_f32;
+  uint8_t* meta = nullptr;      // the small arrays (TestsetView points into it)
+  size_t meta_bytes = 0, o_ints = 0, o_rlen = 0, o_roff = 0, o_dof = 0, o_isf = 0, o_tok = 0, o_dcnt = 0,
+         o_dmax = 0;
+  uint8_t* seeded = nullptr;    // seeds, stream positions, final-minus-init entries
+  size_t seeded_cap = 0;
+  cudaEvent_t reuse = nullptr;  // readers of the previous contents are done (compute stream)
 };
 
 // Makes `st` wait for the upload of `ts` (no-op once it has completed).
@@ -353,6 +363,153 @@ int atc_profile_read(atc_ctx* ctx, atc_profile* out) {
 
 }  // extern "C"
 
+// Fills an allocated handle from full host regions (`ts_full`) or from seeds +
+// final-minus-init entries (`sd`, regions generated on the device), on the
+// handle's copy stream, and records its ready event.
+static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets* ts_full,
+                         const atc_seeded_testsets* sd, bool sync) {
+  const int T = h->T, nI = h->nI, nP = h->nP;
+  const size_t TP = (size_t)T * nP;
+  const int64_t* int_values = ts_full ? ts_full->int_values : sd->int_values;
+  const int32_t* test_ok = ts_full ? ts_full->test_ok : sd->test_ok;
+  h->h_ints.assign(int_values, int_values + (size_t)T * nI);
+  // every small array in one block, built on the host and copied once
+  std::vector<uint8_t> meta(h->meta_bytes, 0);
+  auto put = [&](size_t o, const void* src, size_t bytes) {
+    if (bytes) std::memcpy(meta.data() + o, src, bytes);
+  };
+  put(h->o_ints, int_values, (size_t)T * nI * 8);
+  put(h->o_rlen, h->lens.data(), nP * 8);
+  put(h->o_roff, h->off.data(), TP * 8);
+  put(h->o_dof, h->doff.data(), TP * 8);
+  put(h->o_isf, h->is_f32.data(), nP * 4);
+  for (int t = 0; t < T; ++t) {
+    const int32_t ok_t = test_ok ? (test_ok[t] ? 1 : 0) : 1;
+    put(h->o_tok + t * 4, &ok_t, 4);
+  }
+  for (size_t i = 0; i < TP; ++i) {
+    const int32_t neg = -1;
+    put(h->o_dmax + i * 4, &neg, 4);  // dirty counts stay 0
+  }
+  cudaStream_t st = ctx->copy_stream[h->cs];
+  if (ctx->free_pending & (1u << h->cs)) {  // pool memory freed by earlier handles
+    cudaStreamWaitEvent(st, ctx->free_ev, 0);
+    ctx->free_pending &= ~(1u << h->cs);
+  }
+  if (h->reuse) cudaStreamWaitEvent(st, h->reuse, 0);  // in-place update: earlier readers first
+  bool ok = atc_cuda_ok(ctx, cudaMemcpyAsync(h->meta, meta.data(), h->meta_bytes, cudaMemcpyHostToDevice, st),
+                        "H2D metadata");
+  double* init = const_cast<double*>(h->view.init);
+  double* fin = const_cast<double*>(h->view.fin);
+  if (ts_full) {
+    // host regions that lie back to back in the same order as the device pool are
+    // copied as one run (one DMA instead of T*n_ptrs)
+    struct Run {
+      const double* src = nullptr;
+      size_t dst = 0, bytes = 0;
+    };
+    Run run_i, run_f;
+    auto flush = [&](Run& r, double* base, const char* what) {
+      if (r.bytes)
+        ok = ok && atc_cuda_ok(ctx, cudaMemcpyAsync(base + r.dst, r.src, r.bytes, cudaMemcpyHostToDevice, st), what);
+      r = Run{};
+    };
+    auto add = [&](Run& r, double* base, const double* src, size_t dst, size_t bytes, const char* what) {
+      if (r.bytes && r.src + r.bytes / 8 == src && r.dst + r.bytes / 8 == dst && r.bytes % 256 == 0) {
+        r.bytes += bytes;
+        return;
+      }
+      flush(r, base, what);
+      r.src = src;
+      r.dst = dst;
+      r.bytes = bytes;
+    };
+    for (int t = 0; t < T && ok; ++t)
+      for (int p = 0; p < nP && ok; ++p) {
+        const size_t i = (size_t)t * nP + p;
+        const size_t bytes = (size_t)h->lens[p] * 8;
+        const double* hi = ts_full->init[i];
+        const double* hf = ts_full->final_[i];
+        if (!hi || !hf) {
+          // a test whose original run failed has no final image; the region stays
+          // unused because every binding fails at t (test_ok[t] == 0)
+          if (test_ok && test_ok[t]) {
+            atc_set_error(ctx, "test %d pointer %d: missing region", t, p);
+            ok = false;
+          }
+          ok = ok && atc_cuda_ok(ctx, cudaMemsetAsync(init + h->off[i], 0, bytes, st), "memset") &&
+               atc_cuda_ok(ctx, cudaMemsetAsync(fin + h->off[i], 0, bytes, st), "memset");
+          continue;
+        }
+        add(run_i, init, hi, (size_t)h->off[i], bytes, "H2D init");
+        add(run_f, fin, hf, (size_t)h->off[i], bytes, "H2D final");
+      }
+    flush(run_i, init, "H2D init");
+    flush(run_f, fin, "H2D final");
+  } else if (ok) {
+    // regions from the tests' mt19937_64 streams (k_probe_regions), then the
+    // final-minus-init entries scattered into the final images (k_apply_diffs)
+    const int64_t nd = sd->diff_off[TP];
+    for (int64_t i = 0; ok && i < nd; ++i)
+      if (sd->diff_pos[i] < 0) {
+        atc_set_error(ctx, "negative final-minus-init position");
+        ok = false;
+      }
+    size_t so = 0;
+    auto take = [&](size_t bytes) {
+      const size_t o = so;
+      so += (bytes + 15) / 16 * 16;
+      return o;
+    };
+    const size_t o_seeds = take((size_t)T * 8), o_skips = take(TP * 8), o_doffs = take((TP + 1) * 8),
+                 o_dvs = take((size_t)nd * 8), o_dps = take((size_t)nd * 4);
+    if (ok && so > h->seeded_cap) {  // grow (the old block stays owned by the handle)
+      h->seeded = (uint8_t*)atc_pool_alloc(ctx, std::max(so, (size_t)256));
+      if (h->seeded) h->allocations.push_back(h->seeded);
+      h->seeded_cap = h->seeded ? so : 0;
+      if (!h->seeded) {
+        atc_set_error(ctx, "device allocation failed (seeded test sets)");
+        ok = false;
+      }
+    }
+    if (ok) {
+      std::vector<uint8_t> sb(so, 0);
+      std::memcpy(sb.data() + o_seeds, sd->stream_seed, (size_t)T * 8);
+      std::memcpy(sb.data() + o_skips, sd->stream_skip, TP * 8);
+      std::memcpy(sb.data() + o_doffs, sd->diff_off, (TP + 1) * 8);
+      if (nd) {
+        std::memcpy(sb.data() + o_dvs, sd->diff_val, (size_t)nd * 8);
+        std::memcpy(sb.data() + o_dps, sd->diff_pos, (size_t)nd * 4);
+      }
+      ok = atc_cuda_ok(ctx, cudaMemcpyAsync(h->seeded, sb.data(), so, cudaMemcpyHostToDevice, st), "H2D seeds");
+    }
+    if (ok) {
+      const TestsetView& v = h->view;
+      k_probe_regions<<<T, 320, 0, st>>>(T, nP, (const uint64_t*)(h->seeded + o_seeds),
+                                         (const uint64_t*)(h->seeded + o_skips), v.region_len, v.is_f32,
+                                         v.region_off, init, fin);
+      k_apply_diffs<<<(unsigned)TP, 256, 0, st>>>(nP, v.region_len, v.region_off,
+                                                  (const int64_t*)(h->seeded + o_doffs),
+                                                  (const int32_t*)(h->seeded + o_dps),
+                                                  (const double*)(h->seeded + o_dvs), fin);
+      ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_probe_regions");
+    }
+  }
+  if (ok) {
+    int64_t maxlen = 0;
+    for (int p = 0; p < nP; ++p) maxlen = std::max<int64_t>(maxlen, h->lens[p]);
+    dim3 grid((unsigned)std::min<int64_t>((maxlen + 255) / 256, 64), (unsigned)(T * nP));
+    k_build_dirty<<<grid, 256, 0, st>>>(h->view, const_cast<int32_t*>(h->view.dirty_pos),
+                                        const_cast<int32_t*>(h->view.dirty_cnt),
+                                        const_cast<int32_t*>(h->view.dirty_max));
+    ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_build_dirty") &&
+         (h->ready || atc_cuda_ok(ctx, cudaEventCreateWithFlags(&h->ready, cudaEventDisableTiming), "cudaEventCreate")) &&
+         atc_cuda_ok(ctx, cudaEventRecord(h->ready, st), "cudaEventRecord") &&
+         (!sync || atc_cuda_ok(ctx, cudaEventSynchronize(h->ready), "upload sync"));
+  }
+  return ok ? ATC_OK : ATC_ERR_CUDA;
+}
+
 // Both upload forms: full host regions (`ts`) or seeds + final-minus-init entries
 // (`sd`, regions generated on the device); the common header fields are equal.
 static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_seeded_testsets* sd,
@@ -372,19 +529,22 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_
   const atc_testsets* ts = &hdr;
   if ((!ts_full && !sd) || !out || ts->n_tests < 1 || ts->n_tests > kMaxT || ts->n_ints < 1 ||
       ts->n_ints > kMaxInts || ts->n_ptrs < 1 || ts->n_ptrs > kMaxPtrs || !ts->int_values || !ts->region_len ||
-      !ts->ptr_is_f32 || (sd && (!sd->stream_seed || !sd->stream_skip || !sd->diff_off))) {
+      !ts->ptr_is_f32 || (sd && (!sd->stream_seed || !sd->stream_skip || !sd->diff_off || sd->diff_off[0] != 0))) {
     atc_set_error(ctx, "malformed test sets");
     return ATC_ERR_ARG;
   }
   cudaSetDevice(ctx->device);
   const int T = ts->n_tests, nI = ts->n_ints, nP = ts->n_ptrs;
+  const size_t TP = (size_t)T * nP;
   auto* h = new atc_testset_handle();
   h->T = T;
   h->nI = nI;
   h->nP = nP;
-  h->h_ints.assign(ts->int_values, ts->int_values + (size_t)T * nI);
+  h->lens.assign(ts->region_len, ts->region_len + nP);
+  h->is_f32.assign(ts->ptr_is_f32, ts->ptr_is_f32 + nP);
   // region pool layout: (t, p) regions back to back, each 32-element aligned
-  std::vector<int64_t> off((size_t)T * nP), doff((size_t)T * nP);
+  h->off.resize(TP);
+  h->doff.resize(TP);
   int64_t total = 0, dtotal = 0;
   for (int t = 0; t < T; ++t)
     for (int p = 0; p < nP; ++p) {
@@ -394,11 +554,26 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_
         delete h;
         return ATC_ERR_ARG;
       }
-      off[(size_t)t * nP + p] = total;
-      doff[(size_t)t * nP + p] = dtotal;
+      h->off[(size_t)t * nP + p] = total;
+      h->doff[(size_t)t * nP + p] = dtotal;
       total += (len + 31) / 32 * 32;
       dtotal += len;
     }
+  size_t mo = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = mo;
+    mo += (bytes + 15) / 16 * 16;
+    return o;
+  };
+  h->o_ints = take((size_t)T * nI * 8);
+  h->o_rlen = take(nP * 8);
+  h->o_roff = take(TP * 8);
+  h->o_dof = take(TP * 8);
+  h->o_isf = take(nP * 4);
+  h->o_tok = take(T * 4);
+  h->o_dcnt = take(TP * 4);
+  h->o_dmax = take(TP * 4);
+  h->meta_bytes = mo;
   auto dmalloc = [&](size_t bytes) -> void* {
     void* p = atc_pool_alloc(ctx, std::max(bytes, (size_t)256));
     if (p) h->allocations.push_back(p);
@@ -407,163 +582,33 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_
   double* init = (double*)dmalloc(total * 8);
   double* fin = (double*)dmalloc(total * 8);
   int32_t* dpos = (int32_t*)dmalloc(dtotal * 4);
-  // every small array in one block, built on the host and copied once:
-  // 8-byte arrays first, then the 4-byte ones
-  const size_t TP = (size_t)T * nP;
-  const int64_t nd = sd ? sd->diff_off[TP] : 0;
-  if (nd < 0) {
-    atc_set_error(ctx, "malformed final-minus-init offsets");
-    atc_testsets_free(ctx, h);
-    return ATC_ERR_ARG;
-  }
-  size_t mo = 0;
-  auto take = [&](size_t bytes) {
-    const size_t o = mo;
-    mo += (bytes + 15) / 16 * 16;
-    return o;
-  };
-  const size_t o_ints = take((size_t)T * nI * 8), o_rlen = take(nP * 8), o_roff = take(TP * 8),
-               o_dof = take(TP * 8);
-  const size_t o_seeds = sd ? take((size_t)T * 8) : 0, o_skips = sd ? take(TP * 8) : 0,
-               o_doffs = sd ? take((TP + 1) * 8) : 0, o_dvs = sd ? take((size_t)nd * 8) : 0;
-  const size_t o_isf = take(nP * 4), o_tok = take(T * 4), o_dcnt = take(TP * 4), o_dmax = take(TP * 4);
-  const size_t o_dps = sd ? take((size_t)nd * 4) : 0;
-  std::vector<uint8_t> meta(mo, 0);
-  auto put = [&](size_t o, const void* src, size_t bytes) {
-    if (bytes) std::memcpy(meta.data() + o, src, bytes);
-  };
-  put(o_ints, ts->int_values, (size_t)T * nI * 8);
-  put(o_rlen, ts->region_len, nP * 8);
-  put(o_roff, off.data(), TP * 8);
-  put(o_dof, doff.data(), TP * 8);
-  put(o_isf, ts->ptr_is_f32, nP * 4);
-  for (int t = 0; t < T; ++t) {
-    const int32_t ok_t = ts->test_ok ? (ts->test_ok[t] ? 1 : 0) : 1;
-    put(o_tok + t * 4, &ok_t, 4);
-  }
-  for (size_t i = 0; i < TP; ++i) {
-    const int32_t neg = -1;
-    put(o_dmax + i * 4, &neg, 4);  // dcnt stays 0
-  }
-  if (sd) {
-    put(o_seeds, sd->stream_seed, (size_t)T * 8);
-    put(o_skips, sd->stream_skip, TP * 8);
-    put(o_doffs, sd->diff_off, (TP + 1) * 8);
-    put(o_dvs, sd->diff_val, (size_t)nd * 8);
-    put(o_dps, sd->diff_pos, (size_t)nd * 4);
-  }
-  uint8_t* dmeta = (uint8_t*)dmalloc(mo);
-  if (!init || !fin || !dpos || !dmeta) {
+  h->meta = (uint8_t*)dmalloc(mo);
+  if (!init || !fin || !dpos || !h->meta) {
     atc_set_error(ctx, "cudaMalloc failed for %lld region doubles", (long long)total);
     atc_testsets_free(ctx, h);
     return ATC_ERR_CUDA;
-  }
-  int64_t* ints = (int64_t*)(dmeta + o_ints);
-  int64_t* rlen = (int64_t*)(dmeta + o_rlen);
-  int64_t* roff = (int64_t*)(dmeta + o_roff);
-  int64_t* dof = (int64_t*)(dmeta + o_dof);
-  int32_t* isf = (int32_t*)(dmeta + o_isf);
-  int32_t* tok = (int32_t*)(dmeta + o_tok);
-  int32_t* dcnt = (int32_t*)(dmeta + o_dcnt);
-  int32_t* dmax = (int32_t*)(dmeta + o_dmax);
-  // copies and kernels go to a copy stream (round-robin), after any pool memory
-  // freed by earlier handles is no longer read by the compute stream
-  const int cs = ctx->copy_next;
-  ctx->copy_next = (cs + 1) % atc_ctx::kCopyStreams;
-  cudaStream_t st = ctx->copy_stream[cs];
-  if (ctx->free_pending & (1u << cs)) {
-    cudaStreamWaitEvent(st, ctx->free_ev, 0);
-    ctx->free_pending &= ~(1u << cs);
-  }
-  bool ok = atc_cuda_ok(ctx, cudaMemcpyAsync(dmeta, meta.data(), mo, cudaMemcpyHostToDevice, st), "H2D metadata");
-  // host regions that lie back to back in the same order as the device pool are
-  // copied as one run (one DMA instead of T*n_ptrs)
-  struct Run {
-    const double* src = nullptr;
-    size_t dst = 0, bytes = 0;
-  };
-  Run run_i, run_f;
-  auto flush = [&](Run& r, double* base, const char* what) {
-    if (r.bytes) ok = ok && atc_cuda_ok(ctx, cudaMemcpyAsync(base + r.dst, r.src, r.bytes, cudaMemcpyHostToDevice, st), what);
-    r = Run{};
-  };
-  auto add = [&](Run& r, double* base, const double* src, size_t dst, size_t bytes, const char* what) {
-    if (r.bytes && r.src + r.bytes / 8 == src && r.dst + r.bytes / 8 == dst && r.bytes % 256 == 0) {
-      r.bytes += bytes;
-      return;
-    }
-    flush(r, base, what);
-    r.src = src;
-    r.dst = dst;
-    r.bytes = bytes;
-  };
-  for (int t = 0; t < T && ok && ts_full; ++t)
-    for (int p = 0; p < nP && ok; ++p) {
-      const size_t i = (size_t)t * nP + p;
-      const size_t bytes = (size_t)ts->region_len[p] * 8;
-      const double* hi = ts->init[i];
-      const double* hf = ts->final_[i];
-      if (!hi || !hf) {
-        // a test whose original run failed has no final image; the region stays
-        // unused because every binding fails at t (test_ok[t] == 0)
-        if (ts->test_ok && ts->test_ok[t]) {
-          atc_set_error(ctx, "test %d pointer %d: missing region", t, p);
-          ok = false;
-        }
-        ok = ok && atc_cuda_ok(ctx, cudaMemsetAsync(init + off[i], 0, bytes, st), "memset") &&
-             atc_cuda_ok(ctx, cudaMemsetAsync(fin + off[i], 0, bytes, st), "memset");
-        continue;
-      }
-      add(run_i, init, hi, (size_t)off[i], bytes, "H2D init");
-      add(run_f, fin, hf, (size_t)off[i], bytes, "H2D final");
-    }
-  flush(run_i, init, "H2D init");
-  flush(run_f, fin, "H2D final");
-  if (sd && ok) {
-    // regions from the tests' mt19937_64 streams (k_probe_regions), then the
-    // final-minus-init entries scattered into the final images (k_apply_diffs)
-    for (int64_t i = 0; ok && i < nd; ++i)
-      if (sd->diff_pos[i] < 0) {
-        atc_set_error(ctx, "negative final-minus-init position");
-        ok = false;
-      }
-    if (ok) {
-      k_probe_regions<<<T, 320, 0, st>>>(T, nP, (const uint64_t*)(dmeta + o_seeds),
-                                         (const uint64_t*)(dmeta + o_skips), rlen, isf, roff, init, fin);
-      k_apply_diffs<<<(unsigned)TP, 256, 0, st>>>(nP, rlen, roff, (const int64_t*)(dmeta + o_doffs),
-                                                  (const int32_t*)(dmeta + o_dps), (const double*)(dmeta + o_dvs),
-                                                  fin);
-      ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_probe_regions");
-    }
   }
   TestsetView& v = h->view;
   v.T = T;
   v.nI = nI;
   v.nP = nP;
-  v.ints = ints;
-  v.is_f32 = isf;
-  v.region_len = rlen;
-  v.test_ok = tok;
+  v.ints = (const int64_t*)(h->meta + h->o_ints);
+  v.is_f32 = (const int32_t*)(h->meta + h->o_isf);
+  v.region_len = (const int64_t*)(h->meta + h->o_rlen);
+  v.test_ok = (const int32_t*)(h->meta + h->o_tok);
   v.init = init;
   v.fin = fin;
-  v.region_off = roff;
+  v.region_off = (const int64_t*)(h->meta + h->o_roff);
   v.dirty_pos = dpos;
-  v.dirty_off = dof;
-  v.dirty_cnt = dcnt;
-  v.dirty_max = dmax;
-  if (ok) {
-    int64_t maxlen = 0;
-    for (int p = 0; p < nP; ++p) maxlen = std::max<int64_t>(maxlen, ts->region_len[p]);
-    dim3 grid((unsigned)std::min<int64_t>((maxlen + 255) / 256, 64), (unsigned)(T * nP));
-    k_build_dirty<<<grid, 256, 0, st>>>(v, dpos, dcnt, dmax);
-    ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_build_dirty") &&
-         atc_cuda_ok(ctx, cudaEventCreateWithFlags(&h->ready, cudaEventDisableTiming), "cudaEventCreate") &&
-         atc_cuda_ok(ctx, cudaEventRecord(h->ready, st), "cudaEventRecord") &&
-         (!sync || atc_cuda_ok(ctx, cudaEventSynchronize(h->ready), "upload sync"));
-  }
-  if (!ok) {
+  v.dirty_off = (const int64_t*)(h->meta + h->o_dof);
+  v.dirty_cnt = (const int32_t*)(h->meta + h->o_dcnt);
+  v.dirty_max = (const int32_t*)(h->meta + h->o_dmax);
+  h->cs = ctx->copy_next;  // round-robin over the copy streams
+  ctx->copy_next = (h->cs + 1) % atc_ctx::kCopyStreams;
+  const int rc = testsets_fill(ctx, h, ts_full, sd, sync);
+  if (rc) {
     atc_testsets_free(ctx, h);
-    return ATC_ERR_CUDA;
+    return rc;
   }
   *out = h;
   return ATC_OK;
@@ -581,6 +626,28 @@ int atc_testsets_upload_async(atc_ctx* ctx, const atc_testsets* ts, atc_testset_
 
 int atc_testsets_upload_seeded(atc_ctx* ctx, const atc_seeded_testsets* ts, atc_testset_handle** out) {
   return testsets_upload(ctx, nullptr, ts, out, false);
+}
+
+int atc_testsets_update_seeded(atc_ctx* ctx, atc_testset_handle* h, const atc_seeded_testsets* ts) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (!h || !ts || ts->n_tests != h->T || ts->n_ints != h->nI || ts->n_ptrs != h->nP || !ts->int_values ||
+      !ts->region_len || !ts->ptr_is_f32 || !ts->stream_seed || !ts->stream_skip || !ts->diff_off ||
+      ts->diff_off[0] != 0) {
+    atc_set_error(ctx, "atc_testsets_update_seeded: test sets do not match the handle");
+    return ATC_ERR_ARG;
+  }
+  for (int p = 0; p < h->nP; ++p)
+    if (ts->region_len[p] != h->lens[p] || (ts->ptr_is_f32[p] != 0) != (h->is_f32[p] != 0)) {
+      atc_set_error(ctx, "atc_testsets_update_seeded: pointer %d differs from the handle's", p);
+      return ATC_ERR_ARG;
+    }
+  cudaSetDevice(ctx->device);
+  // the new contents are written after everything queued so far on the compute
+  // stream (evaluations of every sweep branch join it) has read the old ones
+  if (!h->reuse && !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&h->reuse, cudaEventDisableTiming), "cudaEventCreate"))
+    return ATC_ERR_CUDA;
+  if (!atc_cuda_ok(ctx, cudaEventRecord(h->reuse, ctx->stream), "cudaEventRecord")) return ATC_ERR_CUDA;
+  return testsets_fill(ctx, h, nullptr, ts, false);
 }
 
 int atc_testsets_download(atc_ctx* ctx, const atc_testset_handle* h, double* init, double* final_) {
@@ -618,6 +685,7 @@ int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h) {
     ctx->free_pending = (1u << atc_ctx::kCopyStreams) - 1;
   }
   if (h->ready) cudaEventDestroy(h->ready);
+  if (h->reuse) cudaEventDestroy(h->reuse);
   for (void* p : h->allocations) {
     if (ctx && !ctx->broken)
       atc_pool_free(ctx, p);
@@ -1151,6 +1219,7 @@ struct atc_enum_batch {
   uint64_t* h_res = nullptr;  // pinned mirror
   cudaGraphExec_t exec = nullptr;
   bool graph_failed = false;
+  std::vector<std::vector<int64_t>> captured_ints;  // per job: its test sets' ints when the graph was captured
   bool transient = false;  // one-shot (atc_eval_enumerated_many): buffers borrowed from the context
   uint8_t* perm_block = nullptr;  // owned permutation buffer (reusable batches)
 };
@@ -1332,7 +1401,21 @@ int atc_enum_batch_run(atc_ctx* ctx, atc_enum_batch* b) {
   if (b->runs == 0 || ctx->prof || b->graph_failed) {
     rc = enqueue_batch(ctx, b, st, true);
   } else {
+    // the graph bakes in choices made from the test sets' ints (index width, tables,
+    // kernels): re-capture if an in-place update changed any of them
+    bool stale = false;
+    for (int j = 0; j < b->n && b->exec && !stale; ++j)
+      stale = b->batched[j] && (size_t)j < b->captured_ints.size() && b->captured_ints[j] != b->jobs[j].ts->h_ints;
+    if (stale) {
+      cudaGraphExecDestroy(b->exec);
+      b->exec = nullptr;
+    }
+    for (int j = 0; j < b->n; ++j)
+      if (b->batched[j]) ts_wait(b->jobs[j].ts, st);  // updated test sets resident before the replay
     if (!b->exec) {
+      b->captured_ints.assign(b->n, {});
+      for (int j = 0; j < b->n; ++j)
+        if (b->batched[j]) b->captured_ints[j] = b->jobs[j].ts->h_ints;
       cudaGraph_t g = nullptr;
       bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) == cudaSuccess;
       if (ok) {

@@ -182,7 +182,7 @@ def _shrunk(ts, lens):
     cut = lambda a, L: a if (a is None or L is None) else a[:L].copy()
     init = [[cut(a, lens[p]) for p, a in enumerate(row)] for row in ts.init]
     final = [None if row is None else [cut(a, lens[p]) for p, a in enumerate(row)] for row in ts.final]
-    return RecordedTestsets(ts.params, ts.ints.copy(), init, final, ts.test_ok.copy())
+    return RecordedTestsets(ts.params, ts.ints.copy(), init, final, ts.test_ok.copy(), seeds=ts.seeds, skips=ts.skips)
 
 
 CONV_VARIANTS = {
@@ -347,3 +347,34 @@ def test_seeded_upload_regenerates_regions(ev, stem):
         np.testing.assert_array_equal(got[0], want[0])
         assert got[1] == want[1] and got[2].tolist() == want[2].tolist()
     ts2._handles.clear()
+
+
+def test_seeded_update_in_place_with_prepared_sweep(ev):
+    """atc_testsets_update_seeded rewrites a handle's test sets in place; a
+    prepared (graph-replayed) sweep over it then evaluates the new contents —
+    re-captured when the new int values change the plan — exactly like a fresh
+    one-shot evaluation of the same test sets."""
+    import ctypes as C
+
+    from paper_2301_11659_b200.evaluator import _TestsetHandle
+
+    p = fixtures.load("conv_direct")
+    base = p.testsets(16)
+    h = base.upload_seeded(ev.ctx)
+    space, spec = p.space("conv2d"), fixtures.spec("conv2d")
+    ranges = [(0, 1 << 22), (381367000, 381367100)]
+    holder = p.testsets(16)
+    holder._handles[id(ev.ctx)] = h  # the sweep reads this handle
+    sweep = ev.sweep([(spec, holder, space, b, e) for b, e in ranges])
+    variants = [base, _with_int(base, 2, 5), _with_int(base, 4, 3), base]
+    for ts in variants:
+        s, keep = ts.seeded_struct()
+        L.check(ev.ctx.handle, L.lib().atc_testsets_update_seeded(ev.ctx.handle, C.c_void_p(h.value), C.byref(s)))
+        for _ in range(2):  # eager/capture, then replay
+            got = sweep.run()
+            for (b, e), (pg, ng, hg) in zip(ranges, got):
+                pw, nw, hw = ev.eval_enumerated(spec, ts, space, b, e)
+                np.testing.assert_array_equal(pg, pw)
+                assert ng == nw and hg.tolist() == hw.tolist()
+    sweep.close()
+    holder._handles.clear()
