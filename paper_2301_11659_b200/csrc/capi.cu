@@ -81,6 +81,8 @@ struct atc_testset_handle {
   uint8_t* seeded = nullptr;    // seeds, stream positions, final-minus-init entries
   size_t seeded_cap = 0;
   cudaEvent_t reuse = nullptr;  // readers of the previous contents are done (compute stream)
+  uint8_t* pin = nullptr;       // pinned staging of the metadata + seeded blocks (async DMA)
+  size_t pin_bytes = 0;
 };
 
 // Makes `st` wait for the upload of `ts` (no-op once it has completed).
@@ -373,10 +375,26 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
   const int64_t* int_values = ts_full ? ts_full->int_values : sd->int_values;
   const int32_t* test_ok = ts_full ? ts_full->test_ok : sd->test_ok;
   h->h_ints.assign(int_values, int_values + (size_t)T * nI);
-  // every small array in one block, built on the host and copied once
-  std::vector<uint8_t> meta(h->meta_bytes, 0);
+  // every small array in one block, built in pinned staging and copied once; the
+  // seeded block follows it in the same staging buffer
+  const int64_t nd_s = sd ? sd->diff_off[TP] : 0;
+  const size_t seeded_need =
+      sd ? ((size_t)T * 8 + 15) / 16 * 16 + (TP * 8 + 15) / 16 * 16 + ((TP + 1) * 8 + 15) / 16 * 16 +
+               ((size_t)nd_s * 8 + 15) / 16 * 16 + ((size_t)nd_s * 4 + 15) / 16 * 16
+         : 0;
+  if (h->ready && !atc_cuda_ok(ctx, cudaEventSynchronize(h->ready), "staging reuse"))  // previous DMA done
+    return ATC_ERR_CUDA;
+  if (h->pin_bytes < h->meta_bytes + seeded_need) {
+    if (h->pin) cudaFreeHost(h->pin);
+    h->pin = nullptr;
+    h->pin_bytes = 0;
+    if (!atc_cuda_ok(ctx, cudaMallocHost(&h->pin, h->meta_bytes + seeded_need), "cudaMallocHost")) return ATC_ERR_CUDA;
+    h->pin_bytes = h->meta_bytes + seeded_need;
+  }
+  uint8_t* meta = h->pin;
+  std::memset(meta, 0, h->meta_bytes);
   auto put = [&](size_t o, const void* src, size_t bytes) {
-    if (bytes) std::memcpy(meta.data() + o, src, bytes);
+    if (bytes) std::memcpy(meta + o, src, bytes);
   };
   put(h->o_ints, int_values, (size_t)T * nI * 8);
   put(h->o_rlen, h->lens.data(), nP * 8);
@@ -397,7 +415,7 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
     ctx->free_pending &= ~(1u << h->cs);
   }
   if (h->reuse) cudaStreamWaitEvent(st, h->reuse, 0);  // in-place update: earlier readers first
-  bool ok = atc_cuda_ok(ctx, cudaMemcpyAsync(h->meta, meta.data(), h->meta_bytes, cudaMemcpyHostToDevice, st),
+  bool ok = atc_cuda_ok(ctx, cudaMemcpyAsync(h->meta, meta, h->meta_bytes, cudaMemcpyHostToDevice, st),
                         "H2D metadata");
   double* init = const_cast<double*>(h->view.init);
   double* fin = const_cast<double*>(h->view.fin);
@@ -473,15 +491,15 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
       }
     }
     if (ok) {
-      std::vector<uint8_t> sb(so, 0);
-      std::memcpy(sb.data() + o_seeds, sd->stream_seed, (size_t)T * 8);
-      std::memcpy(sb.data() + o_skips, sd->stream_skip, TP * 8);
-      std::memcpy(sb.data() + o_doffs, sd->diff_off, (TP + 1) * 8);
+      uint8_t* sb = h->pin + h->meta_bytes;  // so == seeded_need
+      std::memcpy(sb + o_seeds, sd->stream_seed, (size_t)T * 8);
+      std::memcpy(sb + o_skips, sd->stream_skip, TP * 8);
+      std::memcpy(sb + o_doffs, sd->diff_off, (TP + 1) * 8);
       if (nd) {
-        std::memcpy(sb.data() + o_dvs, sd->diff_val, (size_t)nd * 8);
-        std::memcpy(sb.data() + o_dps, sd->diff_pos, (size_t)nd * 4);
+        std::memcpy(sb + o_dvs, sd->diff_val, (size_t)nd * 8);
+        std::memcpy(sb + o_dps, sd->diff_pos, (size_t)nd * 4);
       }
-      ok = atc_cuda_ok(ctx, cudaMemcpyAsync(h->seeded, sb.data(), so, cudaMemcpyHostToDevice, st), "H2D seeds");
+      ok = atc_cuda_ok(ctx, cudaMemcpyAsync(h->seeded, sb, so, cudaMemcpyHostToDevice, st), "H2D seeds");
     }
     if (ok) {
       const TestsetView& v = h->view;
@@ -684,8 +702,12 @@ int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h) {
     cudaEventRecord(ctx->free_ev, ctx->stream);
     ctx->free_pending = (1u << atc_ctx::kCopyStreams) - 1;
   }
-  if (h->ready) cudaEventDestroy(h->ready);
+  if (h->ready) {
+    cudaEventSynchronize(h->ready);  // the staging buffer may still be read by its DMA
+    cudaEventDestroy(h->ready);
+  }
   if (h->reuse) cudaEventDestroy(h->reuse);
+  if (h->pin) cudaFreeHost(h->pin);
   for (void* p : h->allocations) {
     if (ctx && !ctx->broken)
       atc_pool_free(ctx, p);
@@ -1264,7 +1286,13 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
       rc = ATC_ERR_CUDA;
       break;
     }
-    if (wait_uploads) ts_wait(job.ts, js);  // job j starts as soon as its own test sets are resident
+    // job j starts as soon as its own test sets are resident; in a captured graph the
+    // wait is an external event node on the handle's ready event, so a replay after
+    // an in-place update (atc_testsets_update_seeded) waits for that update only
+    if (wait_uploads)
+      ts_wait(job.ts, js);
+    else if (job.ts->ready)
+      cudaStreamWaitEvent(js, job.ts->ready, cudaEventWaitExternal);
     rc = enqueue_tables(ctx, e, job.ts, job.perms, job.n_perms, &b->d_perms[j], js);
     if (rc) break;
     if (job.end > job.begin) {
@@ -1410,8 +1438,6 @@ int atc_enum_batch_run(atc_ctx* ctx, atc_enum_batch* b) {
       cudaGraphExecDestroy(b->exec);
       b->exec = nullptr;
     }
-    for (int j = 0; j < b->n; ++j)
-      if (b->batched[j]) ts_wait(b->jobs[j].ts, st);  // updated test sets resident before the replay
     if (!b->exec) {
       b->captured_ints.assign(b->n, {});
       for (int j = 0; j < b->n; ++j)
