@@ -224,7 +224,7 @@ def main():
     torch.cuda.set_stream(stream)
     _lib.check(ctx.handle, _lib.lib().atc_set_stream(ctx.handle, C.c_void_p(stream.cuda_stream)))
     ev = Evaluator(ctx)
-    shards = [workloads.shard(j.count, rank, world) for j in jobs]
+    shards = workloads.plan_shards(jobs, rank, world)
     for j in jobs:
         j.ts.upload(ctx)  # device-resident recorded test sets for the kernel-level number
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")

@@ -1062,8 +1062,13 @@ int plan_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_h
 // Uploads the permutations and builds the per-space tables (k_gemm_need,
 // k_pos0_table) on the stream; scratch slots 6/17/21 are reused in stream order.
 int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, const uint8_t* perms, int32_t n_perms,
-                   uint8_t** d_perms_out, cudaStream_t st) {
+                   uint8_t** d_perms_out, cudaStream_t st, uint64_t begin, uint64_t end) {
   const SpecView& sp = e.sp;
+  // only the permutations [p_lo, p_hi] the range [begin, end) touches are tabulated
+  // (a rank of a multi-GPU sweep owns a block of the space)
+  const uint64_t p_lo = end > begin ? begin / e.size_maps : 0;
+  const uint64_t p_hi = end > begin ? (end - 1) / e.size_maps : 0;
+  const uint64_t np_local = std::min<uint64_t>(p_hi - p_lo + 1, (uint64_t)n_perms - p_lo);
   uint8_t* d_perms = *d_perms_out;  // device-resident already (batches), else staged here
   if (!d_perms) {
     d_perms = (uint8_t*)atc_ctx_scratch(ctx, 6, (size_t)n_perms * sp.nA + 16);
@@ -1100,14 +1105,19 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
     e.pt.table = tab;
     e.plan.pt = e.pt;
     // conv with the canonical key (c first): one running sum per (perm, h, w, r, s)
+    const uint64_t t_off = p_lo * e.pt.per_perm, t_bytes = np_local * e.pt.per_perm;
+    const uint8_t* perms_local = d_perms + p_lo * sp.nA;
     if (sp.sem == ATC_SEM_CONV2D && e.pt.R == 5 && e.plan.key_stride[1] == 1 && e.use_rows &&
         conv_thresholds_ok(sp, e.plan, ts->nI))
-      k_pos0_table_conv<<<(unsigned)std::min<uint64_t>((e.table_bytes / ts->nI + 255) / 256,
-                                                       (uint64_t)ctx->sm_count * 16),
-                          256, 0, st>>>(ts->view, sp, d_perms, n_perms, e.pt, tab, tab1);
+      k_pos0_table_conv<<<(unsigned)std::max<uint64_t>(
+                              1, std::min<uint64_t>((t_bytes / ts->nI + 255) / 256, (uint64_t)ctx->sm_count * 16)),
+                          256, 0, st>>>(ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off,
+                                        tab1 ? tab1 + t_off : nullptr);
     else
-      k_pos0_table<<<(unsigned)std::min<uint64_t>((e.table_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16), 256,
-                     0, st>>>(ts->view, sp, d_perms, n_perms, e.pt, tab, tab1);
+      k_pos0_table<<<(unsigned)std::max<uint64_t>(
+                         1, std::min<uint64_t>((t_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16)),
+                     256, 0, st>>>(ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off,
+                                   tab1 ? tab1 + t_off : nullptr);
     if (ctx->prof) ctx->prof_kernels += 1;
     e.plan.cmask = e.plan.cmask1 = nullptr;
     if (pairs) {
@@ -1118,9 +1128,11 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
         return ATC_ERR_CUDA;
       }
       uint32_t* cm1 = cm + (words + 3) / 4 * 4;
-      const unsigned g = (unsigned)std::min<uint64_t>((words + 255) / 256, (uint64_t)ctx->sm_count * 16);
-      k_cmask<<<g, 256, 0, st>>>(tab, words, ts->nI, cm);
-      k_cmask<<<g, 256, 0, st>>>(tab1, words, ts->nI, cm1);
+      const uint64_t w_off = t_off / (uint64_t)ts->nI, w_local = t_bytes / (uint64_t)ts->nI;
+      const unsigned g =
+          (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((w_local + 255) / 256, (uint64_t)ctx->sm_count * 16));
+      k_cmask<<<g, 256, 0, st>>>(tab + t_off, w_local, ts->nI, cm + w_off);
+      k_cmask<<<g, 256, 0, st>>>(tab1 + t_off, w_local, ts->nI, cm1 + w_off);
       e.plan.cmask = cm;
       e.plan.cmask1 = cm1;
       if (ctx->prof) ctx->prof_kernels += 2;
@@ -1157,7 +1169,7 @@ int atc_eval_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_tests
   }
   cudaMemsetAsync(hist, 0, 64, st);
   uint8_t* d_perms = nullptr;
-  rc = enqueue_tables(ctx, e, ts, perms, n_perms, &d_perms, st);
+  rc = enqueue_tables(ctx, e, ts, perms, n_perms, &d_perms, st, begin, end);
   if (rc) return rc;
   // result block on the device: [0] survivor count (copied from cnt), [1] passing
   // count, [2..2+cap) passing global indices; reasons accumulate in `hist`
@@ -1293,7 +1305,8 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
       ts_wait(job.ts, js);
     else if (job.ts->ready)
       cudaStreamWaitEvent(js, job.ts->ready, cudaEventWaitExternal);
-    rc = enqueue_tables(ctx, e, job.ts, job.perms, job.n_perms, &b->d_perms[j], js);
+    if (job.end <= job.begin) continue;  // nothing of this space on this rank
+    rc = enqueue_tables(ctx, e, job.ts, job.perms, job.n_perms, &b->d_perms[j], js, job.begin, job.end);
     if (rc) break;
     if (job.end > job.begin) {
       BindingSource src{nullptr, nullptr, b->d_perms[j], e.size_maps, job.begin, 1};

@@ -102,3 +102,22 @@ def stress_jobs(T: int = 16) -> list:
 def shard(count: int, rank: int, world: int) -> tuple:
     """Contiguous block partition of [0, count)."""
     return count * rank // world, count * (rank + 1) // world
+
+
+BIG_SPACE = 1 << 24  # spaces at least this large are block-partitioned across ranks
+
+
+def plan_shards(jobs: list, rank: int, world: int) -> list:
+    """This rank's [begin, end) of every job.  Large spaces are block-partitioned
+    across all ranks (their screens dominate); small spaces — chains of a few
+    latency-bound kernels — go whole to one rank each, dealt round-robin, so every
+    rank runs ~1/world of them instead of a sliver of each.  Ranks without a space
+    get an empty range (and contribute nothing to its reduction)."""
+    out, k = [], 0
+    for j in jobs:
+        if world == 1 or j.count >= BIG_SPACE:
+            out.append(shard(j.count, rank, world))
+        else:
+            out.append((0, j.count) if k % world == rank else (0, 0))
+            k += 1
+    return out

@@ -75,3 +75,27 @@ def test_block_range_partition():
             assert ranges[0][0] == 0 and ranges[-1][1] == count
             assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
             assert max(h - l for l, h in ranges) - min(h - l for l, h in ranges) <= 1
+
+
+def test_plan_shards_cover_every_space_once():
+    """workloads.plan_shards: across ranks every binding of every corpus space is
+    assigned exactly once; large spaces are split over all ranks, small spaces go
+    whole to one rank and are dealt evenly."""
+    from paper_2301_11659_b200 import workloads
+
+    jobs = workloads.corpus_jobs()
+    for world in (1, 2, 4, 8):
+        plans = [workloads.plan_shards(jobs, r, world) for r in range(world)]
+        for i, j in enumerate(jobs):
+            rs = sorted((plans[r][i] for r in range(world)), key=lambda x: x[0])
+            covered = sum(e - b for b, e in rs)
+            assert covered == j.count, (j.stem, world)
+            nonempty = [(b, e) for b, e in rs if e > b]
+            assert all(a[1] == c[0] for a, c in zip(nonempty, nonempty[1:]))
+            if j.count >= workloads.BIG_SPACE:
+                assert len(nonempty) == min(world, j.count)
+            else:
+                assert len(nonempty) == 1
+        small = [sum(1 for i, j in enumerate(jobs) if j.count < workloads.BIG_SPACE and plans[r][i][1] > 0)
+                 for r in range(world)]
+        assert max(small) - min(small) <= 1
