@@ -1279,15 +1279,26 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
     cudaEventRecord(ctx->fork_ev, st);
     for (int k = 0; k < atc_ctx::kSideStreams; ++k) cudaStreamWaitEvent(ctx->side_stream[k], ctx->fork_ev, 0);
   }
-  int side_next = 0;
+  int side_next = 0, conv_next = 0;
   int rc = ATC_OK;
   for (int j = 0; j < b->n && rc == ATC_OK; ++j) {
     if (!b->batched[j]) continue;
     atc_enum_job& job = b->jobs[j];
     EnumPlan& e = b->plans[j];
-    const bool side = split && e.sp.sem != ATC_SEM_CONV2D;
-    const int sk = side ? side_next : -1;
-    if (side) side_next = (side_next + 1) % atc_ctx::kSideStreams;
+    // conv spaces on the caller's stream and side stream 0 alternately when they
+    // are small (a multi-GPU rank's share: chains of short kernels), else the
+    // caller's stream; gemm spaces round-robin over the side streams
+    int sk = -1;
+    if (split && e.sp.sem == ATC_SEM_CONV2D) {
+      if (job.end - job.begin < (1ull << 30)) {
+        sk = conv_next ? 0 : -1;
+        conv_next ^= 1;
+      }
+    } else if (split) {
+      sk = side_next;
+      side_next = (side_next + 1) % atc_ctx::kSideStreams;
+    }
+    const bool side = sk >= 0;
     cudaStream_t js = side ? ctx->side_stream[sk] : st;
     ctx->slot_base = side ? 32 * (sk + 1) : 0;
     uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
