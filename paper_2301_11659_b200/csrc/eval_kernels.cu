@@ -258,8 +258,11 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
   const uint64_t nI = (uint64_t)ts.nI, nI2 = nI * nI;
   const uint64_t inner = nI2 * (uint64_t)n_perms;  // (h, w, perm) combinations
   const uint64_t total = inner * nI2;              // x (r, s)
+  __shared__ int64_t s_ints[kMaxInts];
+  if (threadIdx.x < ts.nI) s_ints[threadIdx.x] = ts.ints[threadIdx.x];
+  __syncthreads();
   int64_t cmax_all = 0;
-  for (int j = 0; j < ts.nI; ++j) cmax_all = max(cmax_all, ts.ints[j]);
+  for (int j = 0; j < ts.nI; ++j) cmax_all = max(cmax_all, s_ints[j]);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t rs_d = i / inner, hwp = i - rs_d * inner;
     const uint64_t perm = hwp / nI2, hw_d = hwp - perm * nI2;
@@ -293,17 +296,29 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
       const bool v0 = imax < lenA && wmax < lenB;  // imax >= 0 here
       v1_live = v1_live && imax + 1 < lenA && wmax < lenB;
       if (!v0) break;  // monotone in c: no larger c is tabulated either
-      for (int64_t u = 0; u < r; ++u) {
-        const double* a = A + (z * h + u) * w;
-        const double* b = B + (z * r + u) * s;
-        for (int64_t t = 0; t < s; ++t) {
-          const double bv = b[t];
-          acc = dadd(acc, dmul(a[t], bv));
-          if (v1_live) acc1 = dadd(acc1, dmul(a[t + 1], bv));
+      // indices below are < len(region) < 2^31 here: 32-bit
+      const int hi = (int)h, wi = (int)w, ri = (int)r, si = (int)s, zi = (int)z;
+      if (v1_live) {
+        for (int u = 0; u < ri; ++u) {
+          const double* __restrict__ a = A + (zi * hi + u) * wi;
+          const double* __restrict__ b = B + (zi * ri + u) * si;
+          double a0 = a[0];
+          for (int t = 0; t < si; ++t) {
+            const double bv = b[t], a1 = a[t + 1];
+            acc = dadd(acc, dmul(a0, bv));
+            acc1 = dadd(acc1, dmul(a1, bv));
+            a0 = a1;
+          }
+        }
+      } else {
+        for (int u = 0; u < ri; ++u) {
+          const double* __restrict__ a = A + (zi * hi + u) * wi;
+          const double* __restrict__ b = B + (zi * ri + u) * si;
+          for (int t = 0; t < si; ++t) acc = dadd(acc, dmul(a[t], b[t]));
         }
       }
       for (uint64_t j = 0; j < nI; ++j)
-        if (ts.ints[j] == c) {
+        if (s_ints[j] == c) {
           out[base + j] = mismatch(round_region(acc, f32), want, f32) ? 1 : 0;
           if (out1 && v1_live) out1[base + j] = mismatch(round_region(acc1, f32), want1, f32) ? 1 : 0;
         }
