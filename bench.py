@@ -372,6 +372,10 @@ def _e2e(args, ctx, jobs, shards, stream, torch, dist, seeded=True):
     full 65,536-element regions."""
     from paper_2301_11659_b200 import _lib
 
+    # only the spaces (and so the programs) this rank has work in
+    active = [(j, sh) for j, sh in zip(jobs, shards) if sh[1] > sh[0]]
+    jobs, shards = [a[0] for a in active], [a[1] for a in active]
+
     L = _lib.lib()
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
     progs, h2d = {}, 0
