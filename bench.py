@@ -176,6 +176,22 @@ def _ncu_summary():
         return []
 
 
+def _fp64_pipe(ctx, ncu):
+    """K2's FP64-pipe utilisation (ncu) against a DFMA peak measured on
+    this box (atc_measure_dfma_peak)."""
+    from paper_2301_11659_b200 import _lib
+
+    peak = C.c_double(0)
+    rc = _lib.lib().atc_measure_dfma_peak(ctx.handle, C.byref(peak))
+    get = lambda name: next((d for d in ncu if d["kernel"].startswith(name)), {})
+    k2a, k2b = get("k_confirm_t0"), get("k_confirm_warp")
+    return {"dfma_peak_gflops_measured": peak.value if rc == 0 else None,
+            "k2a_fp64_pipe_pct": k2a.get("fp64_pipe_pct"), "k2b_fp64_pipe_pct": k2b.get("fp64_pipe_pct"),
+            "note": "ncu sm__inst_executed_pipe_fp64 (% of peak, active cycles) of the K2 launches in "
+                    "profiles/<round>_ncu_summary.json; K2 is latency bound (short dependent FP64 chains "
+                    "per output), not FP64-throughput bound"}
+
+
 def _config(args, jobs):
     return {"workload": args.workload, "programs": len({j.stem for j in jobs}), "spaces": len(jobs),
             "bindings_per_step": int(sum(j.count for j in jobs)), "tests_per_binding": 16,
@@ -333,13 +349,15 @@ def main():
                                        "wall-clock share",
                      "limiter": "instruction issue (integer ALU); operands are L1/L2 resident",
                      "issue_slots_busy_pct": k1.get("issue_slots_busy_pct"), "ipc_per_sm": k1.get("ipc_per_sm"),
+                     "alu_pipe_pct": k1.get("alu_pipe_pct"),
                      "survey_operand_GBps": survey_bytes / screen_s / 1e9 if screen_s > 0 else None,
                      "note": "achieved counts the recorded data the factorised screen reads (per conv plane / gemm "
                              "row, see bench.py); survey_operand_GBps is SURVEY 8d's 8 B x (extA+extB+extC) per "
                              "binding at t=0 — operand bytes the factorisation never streams, so it is not an HBM "
                              "utilisation.  The kernel is issue bound: see issue_slots_busy_pct (ncu)."},
         "k2_confirm": {"ms_per_step": prof.confirm_ms, "survivors_per_step": prof.survivors,
-                       "note": "sum of K2 launch durations over the concurrent sweep streams (overlapping)"},
+                       "note": "sum of K2 launch durations over the concurrent sweep streams (overlapping)",
+                       "fp64_pipe": _fp64_pipe(ctx, ncu)},
     }
     if not args.no_sgemm:
         # replaced-call backends: sgemm split along M, conv along batch, no collective

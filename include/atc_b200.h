@@ -133,6 +133,11 @@ typedef struct {
 int atc_profile_start(atc_ctx* ctx);
 int atc_profile_read(atc_ctx* ctx, atc_profile* out);
 
+/* Measurement support: the FP64 CUDA-core (DFMA) peak of this device in GFLOP/s,
+ * from independent FMA chains on every SM — the denominator SURVEY.md §8d asks
+ * the K2 FP64-pipe utilisation to be reported against. */
+int atc_measure_dfma_peak(atc_ctx* ctx, double* gflops);
+
 /* Uploads the T recorded test sets to HBM once per user function and builds the
  * per-(t, pointer) dirty lists {i : |init_i - final_i| > abs + rel*|final_i|}.
  * Host buffers are not retained. */

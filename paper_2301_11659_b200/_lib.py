@@ -130,6 +130,7 @@ _SIGS = [
     ("atc_set_stream", C.c_int, [_P, _P]),
     ("atc_profile_start", C.c_int, [_P]),
     ("atc_profile_read", C.c_int, [_P, C.POINTER(Profile)]),
+    ("atc_measure_dfma_peak", C.c_int, [_P, C.POINTER(C.c_double)]),
     ("atc_testsets_upload", C.c_int, [_P, C.POINTER(Testsets), C.POINTER(_P)]),
     ("atc_testsets_free", C.c_int, [_P, _P]),
     ("atc_testsets_upload_async", C.c_int, [_P, C.POINTER(Testsets), C.POINTER(_P)]),
