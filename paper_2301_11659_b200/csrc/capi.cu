@@ -369,7 +369,7 @@ int atc_profile_read(atc_ctx* ctx, atc_profile* out) {
 // final-minus-init entries (`sd`, regions generated on the device), on the
 // handle's copy stream, and records its ready event.
 static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets* ts_full,
-                         const atc_seeded_testsets* sd, bool sync) {
+                         const atc_seeded_testsets* sd, bool sync, bool pinned_staging = false) {
   const int T = h->T, nI = h->nI, nP = h->nP;
   const size_t TP = (size_t)T * nP;
   const int64_t* int_values = ts_full ? ts_full->int_values : sd->int_values;
@@ -382,16 +382,27 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
       sd ? ((size_t)T * 8 + 15) / 16 * 16 + (TP * 8 + 15) / 16 * 16 + ((TP + 1) * 8 + 15) / 16 * 16 +
                ((size_t)nd_s * 8 + 15) / 16 * 16 + ((size_t)nd_s * 4 + 15) / 16 * 16
          : 0;
-  if (h->ready && !atc_cuda_ok(ctx, cudaEventSynchronize(h->ready), "staging reuse"))  // previous DMA done
-    return ATC_ERR_CUDA;
-  if (h->pin_bytes < h->meta_bytes + seeded_need) {
-    if (h->pin) cudaFreeHost(h->pin);
-    h->pin = nullptr;
-    h->pin_bytes = 0;
-    if (!atc_cuda_ok(ctx, cudaMallocHost(&h->pin, h->meta_bytes + seeded_need), "cudaMallocHost")) return ATC_ERR_CUDA;
-    h->pin_bytes = h->meta_bytes + seeded_need;
+  // in-place updates stage through the handle's pinned buffer (true async DMA,
+  // allocated once); a first upload stages through pageable memory (the driver
+  // copies it before returning) and avoids a pinned allocation per handle
+  std::vector<uint8_t> pageable;
+  uint8_t* meta = nullptr;
+  if (pinned_staging) {
+    if (h->ready && !atc_cuda_ok(ctx, cudaEventSynchronize(h->ready), "staging reuse"))  // previous DMA done
+      return ATC_ERR_CUDA;
+    if (h->pin_bytes < h->meta_bytes + seeded_need) {
+      if (h->pin) cudaFreeHost(h->pin);
+      h->pin = nullptr;
+      h->pin_bytes = 0;
+      if (!atc_cuda_ok(ctx, cudaMallocHost(&h->pin, h->meta_bytes + seeded_need), "cudaMallocHost"))
+        return ATC_ERR_CUDA;
+      h->pin_bytes = h->meta_bytes + seeded_need;
+    }
+    meta = h->pin;
+  } else {
+    pageable.resize(h->meta_bytes + seeded_need);
+    meta = pageable.data();
   }
-  uint8_t* meta = h->pin;
   std::memset(meta, 0, h->meta_bytes);
   auto put = [&](size_t o, const void* src, size_t bytes) {
     if (bytes) std::memcpy(meta + o, src, bytes);
@@ -410,9 +421,9 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
     put(h->o_dmax + i * 4, &neg, 4);  // dirty counts stay 0
   }
   cudaStream_t st = ctx->copy_stream[h->cs];
-  if (ctx->free_pending & (1u << h->cs)) {  // pool memory freed by earlier handles
+  if (ctx->free_pending & (1ull << h->cs)) {  // pool memory freed by earlier handles
     cudaStreamWaitEvent(st, ctx->free_ev, 0);
-    ctx->free_pending &= ~(1u << h->cs);
+    ctx->free_pending &= ~(1ull << h->cs);
   }
   if (h->reuse) cudaStreamWaitEvent(st, h->reuse, 0);  // in-place update: earlier readers first
   bool ok = atc_cuda_ok(ctx, cudaMemcpyAsync(h->meta, meta, h->meta_bytes, cudaMemcpyHostToDevice, st),
@@ -491,7 +502,7 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
       }
     }
     if (ok) {
-      uint8_t* sb = h->pin + h->meta_bytes;  // so == seeded_need
+      uint8_t* sb = meta + h->meta_bytes;  // so == seeded_need
       std::memcpy(sb + o_seeds, sd->stream_seed, (size_t)T * 8);
       std::memcpy(sb + o_skips, sd->stream_skip, TP * 8);
       std::memcpy(sb + o_doffs, sd->diff_off, (TP + 1) * 8);
@@ -665,7 +676,7 @@ int atc_testsets_update_seeded(atc_ctx* ctx, atc_testset_handle* h, const atc_se
   if (!h->reuse && !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&h->reuse, cudaEventDisableTiming), "cudaEventCreate"))
     return ATC_ERR_CUDA;
   if (!atc_cuda_ok(ctx, cudaEventRecord(h->reuse, ctx->stream), "cudaEventRecord")) return ATC_ERR_CUDA;
-  return testsets_fill(ctx, h, nullptr, ts, false);
+  return testsets_fill(ctx, h, nullptr, ts, false, true);
 }
 
 int atc_testsets_download(atc_ctx* ctx, const atc_testset_handle* h, double* init, double* final_) {
@@ -700,7 +711,7 @@ int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h) {
     // stream has passed this point (and this handle's own copies are done)
     ts_wait(h, ctx->stream);
     cudaEventRecord(ctx->free_ev, ctx->stream);
-    ctx->free_pending = (1u << atc_ctx::kCopyStreams) - 1;
+    ctx->free_pending = (atc_ctx::kCopyStreams >= 64) ? ~0ull : (1ull << atc_ctx::kCopyStreams) - 1;
   }
   if (h->ready) {
     cudaEventSynchronize(h->ready);  // the staging buffer may still be read by its DMA

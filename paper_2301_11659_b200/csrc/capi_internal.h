@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include <map>
 #include <string>
 #include <utility>
@@ -30,11 +32,11 @@ struct atc_ctx {
   // test-set uploads run on their own stream (copy engine) and publish a ready
   // event per handle; frees record free_ev on the compute stream, which the
   // next upload waits on before reusing pool memory
-  static constexpr int kCopyStreams = 16;  // uploads round-robin over these (concurrent generators)
+  static constexpr int kCopyStreams = 48;  // uploads round-robin over these (concurrent generators)
   cudaStream_t copy_stream[kCopyStreams] = {};
   int copy_next = 0;
   cudaEvent_t free_ev = nullptr;
-  unsigned free_pending = 0;  // copy streams that have not waited on the latest free
+  uint64_t free_pending = 0;  // copy streams that have not waited on the latest free (bit per stream)
   int mode = 0;  // ATC_MODE_* of the evaluation in flight
   // instrumentation (atc_profile_*)
   bool prof = false;
