@@ -110,7 +110,7 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 // SWIZZLE_128B_BASE32B (32 B granules ^= row % 4).  32-bit MN-major operands
 // need the BASE32B form (TMA: CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B); a plain
 // 128B swizzle on an MN-major tf32 operand makes the MMA produce zeros
-// (measured with .gpu_scripts/tc_probe2).
+// (measured with tools/tc_probe_mn_major.cu).
 constexpr uint32_t kSw128 = 2, kSw128Base32 = 1;
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
