@@ -27,7 +27,7 @@ __global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out, uint8_t* out1);
 __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
-                                  uint8_t* out, uint8_t* out1);
+                                  uint8_t* out, uint8_t* out1, uint32_t* cm, uint32_t* cm1);
 __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
                               uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                               unsigned long long* reason_hist);
@@ -1118,35 +1118,45 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
     // conv with the canonical key (c first): one running sum per (perm, h, w, r, s)
     const uint64_t t_off = p_lo * e.pt.per_perm, t_bytes = np_local * e.pt.per_perm;
     const uint8_t* perms_local = d_perms + p_lo * sp.nA;
-    if (sp.sem == ATC_SEM_CONV2D && e.pt.R == 5 && e.plan.key_stride[1] == 1 && e.use_rows &&
-        conv_thresholds_ok(sp, e.plan, ts->nI))
-      k_pos0_table_conv<<<(unsigned)std::max<uint64_t>(
-                              1, std::min<uint64_t>((t_bytes / ts->nI + 255) / 256, (uint64_t)ctx->sm_count * 16)),
-                          256, 0, st>>>(ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off,
-                                        tab1 ? tab1 + t_off : nullptr);
-    else
-      k_pos0_table<<<(unsigned)std::max<uint64_t>(
-                         1, std::min<uint64_t>((t_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16)),
-                     256, 0, st>>>(ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off,
-                                   tab1 ? tab1 + t_off : nullptr);
-    if (ctx->prof) ctx->prof_kernels += 1;
     e.plan.cmask = e.plan.cmask1 = nullptr;
+    uint32_t* cm = nullptr;
+    uint32_t* cm1 = nullptr;
+    const uint64_t words = e.table_bytes / (uint64_t)ts->nI;
     if (pairs) {
-      const uint64_t words = e.table_bytes / (uint64_t)ts->nI;
-      uint32_t* cm = (uint32_t*)atc_ctx_scratch(ctx, 23, words * 8 + 32);
+      cm = (uint32_t*)atc_ctx_scratch(ctx, 23, words * 8 + 32);
       if (!cm) {
         atc_set_error(ctx, "scratch allocation failed (cmask)");
         return ATC_ERR_CUDA;
       }
-      uint32_t* cm1 = cm + (words + 3) / 4 * 4;
-      const uint64_t w_off = t_off / (uint64_t)ts->nI, w_local = t_bytes / (uint64_t)ts->nI;
-      const unsigned g =
-          (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((w_local + 255) / 256, (uint64_t)ctx->sm_count * 16));
-      k_cmask<<<g, 256, 0, st>>>(tab + t_off, w_local, ts->nI, cm + w_off);
-      k_cmask<<<g, 256, 0, st>>>(tab1 + t_off, w_local, ts->nI, cm1 + w_off);
+      cm1 = cm + (words + 3) / 4 * 4;
       e.plan.cmask = cm;
       e.plan.cmask1 = cm1;
-      if (ctx->prof) ctx->prof_kernels += 2;
+    }
+    const uint64_t w_off = t_off / (uint64_t)ts->nI;
+    if (sp.sem == ATC_SEM_CONV2D && e.pt.R == 5 && e.plan.key_stride[1] == 1 && e.use_rows &&
+        conv_thresholds_ok(sp, e.plan, ts->nI)) {
+      // one running sum per (perm, h, w, r, s); the pair screen's bit words come out
+      // of the same pass
+      k_pos0_table_conv<<<(unsigned)std::max<uint64_t>(
+                              1, std::min<uint64_t>((t_bytes / ts->nI + 255) / 256, (uint64_t)ctx->sm_count * 16)),
+                          256, 0, st>>>(ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off,
+                                        tab1 ? tab1 + t_off : nullptr, cm ? cm + w_off : nullptr,
+                                        cm1 ? cm1 + w_off : nullptr);
+      if (ctx->prof) ctx->prof_kernels += 1;
+    } else {
+      k_pos0_table<<<(unsigned)std::max<uint64_t>(
+                         1, std::min<uint64_t>((t_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16)),
+                     256, 0, st>>>(ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off,
+                                   tab1 ? tab1 + t_off : nullptr);
+      if (ctx->prof) ctx->prof_kernels += 1;
+      if (pairs) {
+        const uint64_t w_local = t_bytes / (uint64_t)ts->nI;
+        const unsigned g =
+            (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((w_local + 255) / 256, (uint64_t)ctx->sm_count * 16));
+        k_cmask<<<g, 256, 0, st>>>(tab + t_off, w_local, ts->nI, cm + w_off);
+        k_cmask<<<g, 256, 0, st>>>(tab1 + t_off, w_local, ts->nI, cm1 + w_off);
+        if (ctx->prof) ctx->prof_kernels += 2;
+      }
     }
   }
   return ATC_OK;

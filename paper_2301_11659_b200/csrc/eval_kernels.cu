@@ -253,8 +253,11 @@ __global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need) {
 // reference sums z (channel) outermost, so the sum for c channels is the running
 // sum after z = c - 1 — every value of tc_c is read off one pass (same order, same
 // bits as k_pos0_table's per-entry loops).  Lanes of a warp share (r, s).
+// cm / cm1 (optional): the same verdicts as bit words over the c digits — word
+// (perm, h, w, r, s) bit j = table entry (perm, c digit j, h, w, r, s) == 1 — which
+// is what k_screen_conv_pairs reads (one thread owns exactly one word).
 __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
-                                  uint8_t* out, uint8_t* out1) {
+                                  uint8_t* out, uint8_t* out1, uint32_t* cm, uint32_t* cm1) {
   const uint64_t nI = (uint64_t)ts.nI, nI2 = nI * nI;
   const uint64_t inner = nI2 * (uint64_t)n_perms;  // (h, w, perm) combinations
   const uint64_t total = inner * nI2;              // x (r, s)
@@ -281,13 +284,26 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
     const double want1 = pos1 ? ts.fin[ts.region_off[pC] + 1] : 0.0;
     const uint8_t empty_res = mismatch(round_region(0.0, f32), want, f32) ? 1 : 0;
     const bool shape_ok = r >= 1 && s >= 1 && h >= 0 && w >= 0;
+    auto words = [&]() {  // this thread's entries as bit words (it wrote them itself)
+      if (!cm) return;
+      uint32_t m0 = 0, m1 = 0;
+      for (uint64_t j = 0; j < nI; ++j) {
+        m0 |= (out[base + j] == 1 ? 1u : 0u) << j;
+        if (out1) m1 |= (out1[base + j] == 1 ? 1u : 0u) << j;
+      }
+      cm[base / nI] = m0;
+      if (cm1) cm1[base / nI] = m1;
+    };
     // entries whose c digit is < 1 (or a bad shape): the empty sum; others: 2 until computed
     for (uint64_t j = 0; j < nI; ++j) {
       const bool empty_sum = !shape_ok || ts.ints[j] < 1;
       out[base + j] = empty_sum ? empty_res : 2;
       if (out1) out1[base + j] = 2;
     }
-    if (!shape_ok) continue;
+    if (!shape_ok) {
+      words();
+      continue;
+    }
     double acc = 0.0, acc1 = 0.0;
     bool v1_live = pos1;
     for (int64_t z = 0; z < cmax_all; ++z) {
@@ -323,6 +339,7 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
           if (out1 && v1_live) out1[base + j] = mismatch(round_region(acc1, f32), want1, f32) ? 1 : 0;
         }
     }
+    words();
   }
 }
 
