@@ -511,6 +511,22 @@ __device__ __forceinline__ void epilogue_chunk(const Problem& p, const Maps& map
     if (lane == 0) tma_store_2d(&maps.c, stg, tn * BN + c0, (p.conv == 2 ? ti * p.M : 0) + row0);
     return;
   }
+  if (p.conv == 4) {
+    // compact output pixels q = n*OH*OW + oh*OW + ow: contiguous within an image
+#pragma unroll
+    for (int v = 0; v < 32; ++v) stg[lane * 33 + v] = __uint_as_float(r[v]);
+    __syncwarp();
+    const int q = tn * BN + c0 + lane;
+    const int64_t ohw = (int64_t)p.OH * p.OW;
+    const int n = (int)(q / ohw);
+    const bool ok = n < p.img;
+    const int64_t off = ((int64_t)n * p.M + row0) * ohw + (q - n * ohw);
+    const int rows = min(32, p.M - row0);
+    if (ok)
+      for (int i = 0; i < rows; ++i) p.C[off + (int64_t)i * ohw] = stg[i * 33 + lane];
+    __syncwarp();
+    return;
+  }
   if (p.conv == 1) {
 #pragma unroll
     for (int v = 0; v < 32; ++v) stg[lane * 33 + v] = __uint_as_float(r[v]);
@@ -564,6 +580,17 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
       "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1)
       : "memory");
 }
+// im2col-mode TMA (conv, mode 4): pixelsPerColumn consecutive OUTPUT pixels starting
+// at (n, oh, ow) — traversal clipped to the valid-output box of the map — each
+// shifted by the filter tap (s, r), x 32 channels from c, into K-major rows.
+__device__ __forceinline__ void tma_load_im2col_2sm(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c,
+                                                    int w, int h, int n, uint16_t off_w, uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w), "h"(off_h)
+      : "memory");
+}
 __device__ __forceinline__ void mma_tf32_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                              uint32_t accumulate) {
   asm volatile(
@@ -597,7 +624,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kblocks = (p.conv == 1 || p.conv == 2 ? p.R * p.S * (p.K / BK) : (p.K + BK - 1) / BK);
+  const int kblocks = (p.conv == 1 || p.conv == 2 || p.conv == 4 ? p.R * p.S * (p.K / BK) : (p.K + BK - 1) / BK);
   const int total_kb = kblocks * p.splits;
   uint32_t rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
@@ -651,7 +678,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
           const uint32_t bar = peer_addr(smem_u32(&full[stage]), 0);  // the leader's barrier
           if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE2_BYTES);
           tma_load_2d_2sm(sA, &maps.a[sa], bar, a0, a1);
-          if (p.conv == 1) {
+          if (p.conv == 4) {
+            // im2col: this CTA's 128 output pixels (compact, across images) at tap (r, s)
+            const int cblocks = p.K / BK, kk = kb % kblocks, rs = kk / cblocks, c0 = (kk - rs * cblocks) * BK;
+            const int rr = rs / p.S, ss = rs - rr * p.S;
+            const int ohw = p.OH * p.OW, q0 = tn * BN + (int)rank * (BN / 2);
+            const int n0 = q0 / ohw, rem = q0 - n0 * ohw, oh0 = rem / p.OW, ow0 = rem - (rem / p.OW) * p.OW;
+            tma_load_im2col_2sm(sB, &maps.b[sb], bar, c0, ow0, oh0, n0, (uint16_t)ss, (uint16_t)rr);
+          } else if (p.conv == 1) {
             // K-major: this CTA's 128 pixel rows x 32 channels in one box
             tma_load_2d_2sm(sB, &maps.b[sb], bar, b0, b1 + (int)rank * (BN / 2));
           } else {
@@ -690,7 +724,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * STAGE2_BYTES);
           const uint32_t b_addr = a_addr + A_BYTES;
-          const bool b_kmajor = p.conv == 1;
+          const bool b_kmajor = p.conv == 1 || p.conv == 4;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint64_t ad = make_desc(a_addr + kk * 32, 16, 1024, kSw128);
@@ -848,6 +882,37 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode(atc_ctx* ctx) {
   }
   fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   return fn;
+}
+
+// im2col map over an NHWC fp32 tensor [n][h][w][c]: boxes of `pixels` consecutive
+// valid-output pixels (the traversal box excludes the last r-1 rows and s-1
+// columns of each image) x 32 channels, 128B swizzle (K-major rows like make_map).
+bool make_im2col_map(atc_ctx* ctx, CUtensorMap* m, const float* base, int64_t n, int64_t h, int64_t w, int64_t c,
+                     int r, int s, uint32_t pixels) {
+  static PFN_cuTensorMapEncodeIm2col_v12000 enc = nullptr;
+  if (!enc) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p) {
+      atc_set_error(ctx, "cuTensorMapEncodeIm2col is unavailable");
+      return false;
+    }
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)c * 4, (cuuint64_t)(w * c) * 4, (cuuint64_t)(h * w * c) * 4};
+  int lower[2] = {0, 0};
+  int upper[2] = {-(s - 1), -(r - 1)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult res = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, lower, upper,
+                     (cuuint32_t)BK, pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (res != CUDA_SUCCESS) {
+    atc_set_error(ctx, "cuTensorMapEncodeIm2col failed (%d)", (int)res);
+    return false;
+  }
+  return true;
 }
 
 // 2-D fp32 tensor map over [rows][cols] with row pitch `pitch` elements.
@@ -1127,7 +1192,15 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
   // cta_group::2 (M = 256 filters per CTA pair) when there are >= 2 filter tiles;
   // each CTA then loads half of the pixel rows (K-major box of BN/2 rows)
   const bool umma2 = umma2_enabled() && k > BM && !direct;  // (1x1 direct: slower on the pair kernel)
+  // im2col-mode TMA on the pair kernel: tiles of compact output pixels (no input-grid
+  // waste); ATC_TC_IM2COL=0 keeps the input-grid formulation
+  static const bool im2col_on = [] {
+    const char* e = std::getenv("ATC_TC_IM2COL");
+    return !(e && e[0] == '0');
+  }();
+  const bool im2col = umma2 && im2col_on && r <= 128 && s <= 128;
   auto bmap = [&](CUtensorMap* m, const float* base) {
+    if (im2col) return make_im2col_map(ctx, m, base, n, h, w_, c, (int)r, (int)s, BN / 2);
     return direct ? make_map(ctx, m, base, n * c, hw, hw, 32, BK, true)   // [N*C][H*W], MN-major chunks
                   : make_map(ctx, m, base, n * hw, c, c, BK, umma2 ? BN / 2 : BN, false);  // NHWC, K-major
   };
@@ -1138,7 +1211,7 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
   if (splits == 3 && (!make_map(ctx, &maps.a[1], wl, k, r * s * c, r * s * c, BK, BM, false) || !bmap(&maps.b[1], il)))
     return ATC_ERR_CUDA;
   Problem p{};
-  p.conv = direct ? 2 : 1;
+  p.conv = direct ? 2 : (im2col ? 4 : 1);
   p.M = (int)k;
   p.N = (int)hw;
   p.K = (int)c;
@@ -1157,6 +1230,10 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
     // per image ([N*C][H*W] view); only pixels p < OH*W can be valid outputs
     p.tiles_n = (int)((oh * w_ + BN - 1) / BN);
     p.tiles_img = (int)n;
+  } else if (im2col) {
+    // compact output pixels of the whole batch
+    p.tiles_n = (int)((n * oh * ow + BN - 1) / BN);
+    p.tiles_img = 1;
   } else {
     // the batch's pixels back to back on the NHWC input: tiles run across image
     // boundaries (shifted rows of a valid output never leave its image)
