@@ -195,7 +195,8 @@ def _fp64_pipe(ctx, ncu):
 def _config(args, jobs):
     return {"workload": args.workload, "programs": len({j.stem for j in jobs}), "spaces": len(jobs),
             "bindings_per_step": int(sum(j.count for j in jobs)), "tests_per_binding": 16,
-            "parallelism": f"bindings block-partitioned dp{args.gpus}", "l2": "flushed (256 MB write) between steps"}
+            "parallelism": f"dp{args.gpus}: large spaces block-partitioned over ranks, small spaces dealt whole",
+            "l2": "flushed (256 MB write) between steps"}
 
 
 # ------------------------------------------------------------------ ours -------
