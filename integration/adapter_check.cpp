@@ -15,7 +15,16 @@
 //       ranked list: GPU P2 over all of it + host P1 on survivors, timed.
 //   adapter_check dispatch
 //       the lifted program run with make_gpu_dispatch vs make_oracle_dispatch.
+//   adapter_check routed
+//       make_gpu_routed_dispatch vs rewriter::make_routed_dispatch: the same
+//       cpu/xpu labels on every lifted corpus function (model trained by the
+//       reference's train_svm on rewriter_test.cpp's volume-labelled set),
+//       bit-identical results on the exact route; then f32 GEMM/conv calls
+//       routed "xpu" onto the tcgen05 backends, within 3xTF32 / TF32 tolerance
+//       of the reference's FP64 dispatch.
+#include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <functional>
 #include <iostream>
@@ -25,6 +34,7 @@
 #include "liftc/classifier.hpp"
 #include "liftc/equivalence.hpp"
 #include "liftc/pipeline.hpp"
+#include "liftc/profitability.hpp"
 #include "liftc/rewriter.hpp"
 #include "liftc/rng.hpp"
 
@@ -301,6 +311,161 @@ int cmd_dispatch(atc_ctx* ctx) {
   return bad == 0 ? 0 : 1;
 }
 
+
+// rewriter_test.cpp:109-118's volume-thresholded training set.
+profitability::SvmModel volume_model() {
+  std::vector<profitability::TimingSample> data;
+  for (long long m = 2; m <= 10; m += 2)
+    for (long long n = 2; n <= 10; n += 2)
+      for (long long k = 2; k <= 10; k += 2) {
+        const long long v = m * n * k;
+        if (v > 150 && v < 600) continue;
+        profitability::TimingSample t;
+        t.sizes = {m, n, k};
+        t.t_cpu = 1.0;
+        t.t_xpu = v >= 600 ? 0.5 : 2.0;
+        t.label = v >= 600 ? 1 : 0;
+        data.push_back(t);
+      }
+  return profitability::train_svm(data);
+}
+
+// A model whose decision value is the constant b (no support vectors).
+profitability::SvmModel constant_model(double b) {
+  profitability::SvmModel m;
+  m.feature_dim = 3;
+  m.feat_min = {0, 0, 0};
+  m.feat_max = {1, 1, 1};
+  m.b = b;
+  return m;
+}
+
+double max_rel_err(const std::vector<double>& got, const std::vector<double>& ref) {
+  double e = 0;
+  for (size_t i = 0; i < ref.size(); ++i) e = std::max(e, std::abs(got[i] - ref[i]) / (1.0 + std::abs(ref[i])));
+  return e;
+}
+
+int cmd_routed(atc_ctx* ctx) {
+  auto specs = default_specs();
+  const auto model = volume_model();
+  int bad = 0;
+  for (const auto& p : corpus()) {
+    if (!p.meta.expect_lift) continue;
+    const api::ApiSpec* spec = nullptr;
+    for (const auto& s : specs)
+      if (s.name == p.meta.api) spec = &s;
+    if (!spec) continue;
+    matching::CandidateBinding b;
+    for (const auto& [k, v] : p.meta.binding_truth) {
+      const auto* ap = spec->find(k);
+      if (ap && ap->kind == api::ApiParamKind::Array) b.arrays[k] = v;
+      if (ap && ap->kind == api::ApiParamKind::IntSize) b.sizes[k] = v;
+    }
+    auto rr = rewriter::rewrite(p.prog, p.function, b, *spec);
+    Rng rng(Rng::mix(Rng::mix(0, p.tag + ":" + p.function), "routed-check"));
+    std::vector<std::string> int_params;
+    for (const auto& q : p.prog.find(p.function)->params)
+      if (q.kind == minilang::ParamKind::IntScalar) int_params.push_back(q.name);
+    std::map<std::string, long long> sizes;
+    while (!analysis::draw_sizes(int_params, p.meta.rules, rng, sizes)) {
+    }
+    auto img = analysis::build_probe_image(*p.prog.find(p.function), sizes, rng);
+    std::vector<std::string> rc_, ge_, gt_;
+    auto ref = rewriter::make_routed_dispatch(*spec, &model, &rc_);
+    auto exact = gpu::make_gpu_routed_dispatch(*spec, ctx, &model, &ge_, gpu::kRouteExact);
+    auto tens = gpu::make_gpu_routed_dispatch(*spec, ctx, &model, &gt_, ATC_PREC_3XTF32);
+    interp::InstrumentationPolicy pr, pe, pt;
+    pr.dispatch = &ref;
+    pe.dispatch = &exact;
+    pt.dispatch = &tens;
+    auto a = interp::execute(rr.program, p.function, img, pr);
+    auto e = interp::execute(rr.program, p.function, img, pe);
+    auto t = interp::execute(rr.program, p.function, img, pt);
+    bool same = a.status == e.status && rc_ == ge_ && rc_ == gt_ && a.status == t.status;
+    double err = 0;
+    for (const auto& [name, reg] : a.final.regions) {
+      same = same && reg.data == e.final.regions.at(name).data;
+      err = std::max(err, max_rel_err(t.final.regions.at(name).data, reg.data));
+    }
+    same = same && err <= 1e-3;
+    bad += !same;
+    std::cout << json({{"stem", p.stem}, {"api", spec->name}, {"choices", rc_}, {"ok", same}, {"tensor_err", err}})
+                     .dump()
+              << std::endl;
+  }
+
+  // f32 calls the predictor routes "xpu", straight through the handler
+  const auto xpu = constant_model(1.0), cpu = constant_model(-1.0);
+  auto call = [&](const api::ApiSpec& spec, const std::map<std::string, long long>& ints,
+                  const std::map<std::string, size_t>& lens, const profitability::SvmModel& m, int32_t prec,
+                  uint64_t seed, std::string& label, double& err) {
+    Rng rng(seed);
+    interp::MemoryImage mem;
+    std::vector<interp::DispatchArg> args;
+    for (const auto& ap : spec.params) {
+      interp::DispatchArg a;
+      if (ap.kind == api::ApiParamKind::Array) {
+        interp::Region r;
+        r.elem = minilang::ScalarType::F32;
+        r.data.resize(lens.at(ap.role));
+        for (auto& x : r.data) x = (double)(float)rng.uniform_real(-1.0, 1.0);
+        mem.regions[ap.name] = r;
+        a.kind = interp::DispatchArg::Kind::Ptr;
+        a.region = ap.name;
+      } else {
+        a.kind = interp::DispatchArg::Kind::Int;
+        a.i = ints.at(ap.role);
+      }
+      args.push_back(a);
+    }
+    auto mem_ref = mem;
+    std::vector<std::string> ch, rch;
+    gpu::make_gpu_routed_dispatch(spec, ctx, &m, &ch, prec).handler("atc_dispatch_" + spec.semantics, args, mem);
+    rewriter::make_routed_dispatch(spec, &m, &rch).handler("atc_dispatch_" + spec.semantics, args, mem_ref);
+    label = ch.at(0) == rch.at(0) ? ch.at(0) : "label-mismatch";
+    err = 0;
+    for (const auto& [name, reg] : mem_ref.regions) err = std::max(err, max_rel_err(mem.regions.at(name).data, reg.data));
+  };
+  struct Case {
+    const char* spec;
+    std::map<std::string, long long> ints;
+    std::map<std::string, size_t> lens;
+    double depth;  // reduction length (k, or c*r*s)
+  };
+  const std::vector<Case> cases = {
+      {"gemm_rowmajor", {{"m", 256}, {"n", 192}, {"k", 320}}, {{"a", 256 * 320}, {"b", 320 * 192}, {"c", 256 * 192}}, 320},
+      {"gemm_colmajor", {{"m", 130}, {"n", 70}, {"k", 200}}, {{"a", 130 * 200}, {"b", 200 * 70}, {"c", 130 * 70}}, 200},
+      {"gemm_rowmajor_ld",
+       {{"m", 200}, {"n", 96}, {"k", 160}, {"lda", 170}, {"ldb", 100}, {"ldc", 101}},
+       {{"a", 200 * 170}, {"b", 160 * 100}, {"c", 200 * 101}}, 160},
+      {"conv2d",
+       {{"n", 2}, {"c", 64}, {"h", 12}, {"w", 11}, {"k", 48}, {"r", 3}, {"s", 3}, {"oh", 10}, {"ow", 9}},
+       {{"in", 2 * 64 * 12 * 11}, {"weights", 48 * 64 * 9}, {"out", 2 * 48 * 10 * 9}}, 576},
+  };
+  for (const auto& c : cases) {
+    const api::ApiSpec* spec = nullptr;
+    for (const auto& s : specs)
+      if (s.name == c.spec) spec = &s;
+    for (int32_t prec : {ATC_PREC_3XTF32, ATC_PREC_TF32}) {
+      std::string lx, lc;
+      double ex, ec;
+      call(*spec, c.ints, c.lens, xpu, prec, 7 + prec, lx, ex);
+      call(*spec, c.ints, c.lens, cpu, prec, 7 + prec, lc, ec);
+      // the backends' stated bounds (tests/test_gpu_backends.py TOLS): TOL * sqrt(depth)
+      const double tol = (prec == ATC_PREC_3XTF32 ? 2e-5 : 5e-4) * std::sqrt(c.depth);
+      const bool ok = lx == "xpu" && lc == "cpu" && ex > 0 && ex <= tol && ec == 0;
+      bad += !ok;
+      std::cout << json({{"direct", c.spec}, {"precision", prec == ATC_PREC_TF32 ? "tf32" : "3xtf32"},
+                         {"xpu_err", ex}, {"cpu_err", ec}, {"labels", {lx, lc}}, {"ok", ok}})
+                       .dump()
+                << std::endl;
+    }
+  }
+  std::cout << json({{"mismatches", bad}}).dump() << std::endl;
+  return bad == 0 ? 0 : 1;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -315,6 +480,7 @@ int main(int argc, char** argv) {
     if (cmd == "corpus") rc = cmd_corpus(ctx);
     if (cmd == "unpruned" && argc >= 4) rc = cmd_unpruned(ctx, argv[2], argv[3], argc > 4 ? std::atoi(argv[4]) : 10);
     if (cmd == "dispatch") rc = cmd_dispatch(ctx);
+    if (cmd == "routed") rc = cmd_routed(ctx);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "adapter_check: %s\n", e.what());
     rc = 1;

@@ -193,53 +193,200 @@ LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const ana
   return out;
 }
 
+namespace {
+
+// One decoded dispatch call: rewriter.cpp:101-134's name/arity/kind checks and
+// positional decode (messages verbatim).
+struct DecodedCall {
+  std::vector<int64_t> sizes;                 // spec.size_params() order
+  std::map<std::string, long long> by_name;  // size name -> value
+  std::vector<std::string> regions;           // spec.arrays() order
+};
+
+DecodedCall decode_call(const api::ApiSpec& spec, const std::string& name,
+                        const std::vector<interp::DispatchArg>& args, const interp::MemoryImage& mem) {
+  if (name != "atc_dispatch_" + spec.semantics)
+    throw std::runtime_error("dispatch name '" + name + "' does not match api semantics '" + spec.semantics + "'");
+  if (args.size() != spec.params.size())
+    throw std::runtime_error("dispatch arity " + std::to_string(args.size()) + ", api expects " +
+                             std::to_string(spec.params.size()));
+  DecodedCall d;
+  for (size_t i = 0; i < spec.params.size(); ++i) {
+    const auto& ap = spec.params[i];
+    const auto& a = args[i];
+    if (ap.kind == api::ApiParamKind::Array) {
+      if (a.kind != interp::DispatchArg::Kind::Ptr)
+        throw std::runtime_error("dispatch arg for array '" + ap.name + "' is not a pointer");
+      if (!mem.regions.count(a.region)) throw std::runtime_error("dispatch region '" + a.region + "' missing");
+      d.regions.push_back(a.region);
+    } else if (ap.kind == api::ApiParamKind::IntSize) {
+      if (a.kind != interp::DispatchArg::Kind::Int)
+        throw std::runtime_error("dispatch arg for size '" + ap.name + "' is not an int");
+      d.sizes.push_back(a.i);
+      d.by_name[ap.name] = a.i;
+    }
+  }
+  return d;
+}
+
+// run_dispatch (rewriter.cpp:136-161) on the GPU in FP64: atc_dispatch does the
+// extent checks, the reference arithmetic and the f32 write-back rounding.
+void exact_dispatch(const api::ApiSpec& spec, const atc_spec_desc& desc, atc_ctx* ctx, const DecodedCall& d,
+                    interp::MemoryImage& mem) {
+  // full-region copies (rewriter.cpp:121), computed and written back on the GPU
+  std::vector<std::vector<double>> bufs;
+  std::vector<double*> ptrs;
+  std::vector<int64_t> lens;
+  std::vector<int32_t> f32;
+  for (const auto& rname : d.regions) bufs.push_back(mem.regions.at(rname).data);
+  for (size_t a = 0; a < d.regions.size(); ++a) {
+    ptrs.push_back(bufs[a].data());
+    lens.push_back((int64_t)bufs[a].size());
+    f32.push_back(mem.regions.at(d.regions[a]).elem == minilang::ScalarType::F32);
+  }
+  int rc = atc_dispatch(ctx, &desc, d.sizes.data(), ptrs.data(), lens.data(), f32.data());
+  if (rc == ATC_ERR_DISPATCH) {
+    // same wording as rewriter.cpp:141,145-147 ("... is not positive", "... elements ...")
+    throw std::runtime_error(std::string("dispatch: ") + atc_last_error(ctx));
+  }
+  if (rc != ATC_OK) throw std::runtime_error(atc_last_error(ctx));
+  const auto arrays = spec.arrays();
+  for (size_t a = 0; a < arrays.size(); ++a)
+    if (arrays[a]->liveness != api::Liveness::LiveIn) mem.regions.at(d.regions[a]).data = bufs[a];
+}
+
+// rewriter.cpp:164-172: the value of the size parameter with `role`, else 1.
+long long role_size(const api::ApiSpec& spec, const std::map<std::string, long long>& sizes, const std::string& role,
+                    long long dflt = 1) {
+  for (const auto& p : spec.params)
+    if (p.kind == api::ApiParamKind::IntSize && p.role == role) {
+      auto it = sizes.find(p.name);
+      if (it != sizes.end()) return it->second;
+    }
+  return dflt;
+}
+
+// The array of `spec` with semantic `role` and its region index in d.regions.
+int array_slot(const api::ApiSpec& spec, const std::string& role) {
+  const auto arrays = spec.arrays();
+  for (size_t a = 0; a < arrays.size(); ++a)
+    if (arrays[a]->role == role) return (int)a;
+  return -1;
+}
+
+// The "xpu" leg: the same call on the tcgen05 FP32 backends (atc_sgemm_rm /
+// atc_conv2d_nchw) when every region is f32 and the call is one those backends
+// express; returns false (caller runs the exact path) otherwise.  The checks
+// mirror run_dispatch's (rewriter.cpp:136-148) so the exact path is left to
+// raise the reference's errors.
+bool tensor_dispatch(const api::ApiSpec& spec, atc_ctx* ctx, int32_t precision, const DecodedCall& d,
+                     interp::MemoryImage& mem) {
+  for (const auto& r : d.regions)
+    if (mem.regions.at(r).elem != minilang::ScalarType::F32) return false;
+  for (const auto* ap : spec.arrays()) {
+    long double extent = 1;
+    for (const auto& dim : ap->dims) {
+      auto it = d.by_name.find(dim);
+      if (it == d.by_name.end() || it->second < 1) return false;
+      extent *= (long double)it->second;
+    }
+    if ((long double)mem.regions.at(d.regions[array_slot(spec, ap->role)]).data.size() < extent) return false;
+  }
+  const auto& S = d.by_name;
+  if (spec.semantics == "gemm") {
+    // equivalence.cpp:40-64 with lda/ldb/ldc; operands packed dense row-major
+    const long long m = role_size(spec, S, "m", 0), n = role_size(spec, S, "n", 0), k = role_size(spec, S, "k", 0);
+    const bool row = spec.layout == api::Layout::RowMajor;
+    const long long lda = role_size(spec, S, "lda", row ? k : m), ldb = role_size(spec, S, "ldb", row ? n : k),
+                    ldc = role_size(spec, S, "ldc", row ? n : m);
+    if (m < 1 || n < 1 || k < 1 || lda < (row ? k : m) || ldb < (row ? n : k) || ldc < (row ? n : m)) return false;
+    const int sa = array_slot(spec, "a"), sb = array_slot(spec, "b"), sc = array_slot(spec, "c");
+    if (sa < 0 || sb < 0 || sc < 0) return false;
+    const auto& A = mem.regions.at(d.regions[sa]).data;
+    const auto& B = mem.regions.at(d.regions[sb]).data;
+    auto& Cr = mem.regions.at(d.regions[sc]).data;
+    // last element each operand touches (row: i*lda+p; col: p*lda+i)
+    if ((size_t)((m - 1) * (row ? lda : 1) + (k - 1) * (row ? 1 : lda)) >= A.size() ||
+        (size_t)((k - 1) * (row ? ldb : 1) + (n - 1) * (row ? 1 : ldb)) >= B.size() ||
+        (size_t)((m - 1) * (row ? ldc : 1) + (n - 1) * (row ? 1 : ldc)) >= Cr.size())
+      return false;
+    std::vector<float> a((size_t)(m * k)), b((size_t)(k * n)), c((size_t)(m * n));
+    for (long long i = 0; i < m; ++i)
+      for (long long p = 0; p < k; ++p) a[(size_t)(i * k + p)] = (float)A[(size_t)(row ? i * lda + p : p * lda + i)];
+    for (long long p = 0; p < k; ++p)
+      for (long long j = 0; j < n; ++j) b[(size_t)(p * n + j)] = (float)B[(size_t)(row ? p * ldb + j : j * ldb + p)];
+    if (atc_sgemm_rm(ctx, a.data(), b.data(), c.data(), m, n, k, precision) != ATC_OK)
+      throw std::runtime_error(atc_last_error(ctx));
+    for (long long i = 0; i < m; ++i)
+      for (long long j = 0; j < n; ++j) Cr[(size_t)(row ? i * ldc + j : j * ldc + i)] = (double)c[(size_t)(i * n + j)];
+    return true;
+  }
+  // equivalence.cpp:66-93; the backend takes valid padding, unit stride, C % 32 == 0
+  const long long n = role_size(spec, S, "n", 0), c = role_size(spec, S, "c", 0), h = role_size(spec, S, "h", 0),
+                  w = role_size(spec, S, "w", 0), k = role_size(spec, S, "k", 0), r = role_size(spec, S, "r", 0),
+                  s = role_size(spec, S, "s", 0);
+  const long long oh = role_size(spec, S, "oh", h - r + 1), ow = role_size(spec, S, "ow", w - s + 1);
+  if (n < 1 || c < 1 || k < 1 || r < 1 || s < 1 || oh != h - r + 1 || ow != w - s + 1 || oh < 1 || ow < 1 ||
+      c % 32 != 0)
+    return false;
+  const int si = array_slot(spec, "in"), sw = array_slot(spec, "weights"), so = array_slot(spec, "out");
+  if (si < 0 || sw < 0 || so < 0) return false;
+  const auto& In = mem.regions.at(d.regions[si]).data;
+  const auto& Wt = mem.regions.at(d.regions[sw]).data;
+  auto& Out = mem.regions.at(d.regions[so]).data;
+  const size_t nin = (size_t)(n * c * h * w), nw = (size_t)(k * c * r * s), nout = (size_t)(n * k * oh * ow);
+  if (In.size() < nin || Wt.size() < nw || Out.size() < nout) return false;
+  std::vector<float> x(In.begin(), In.begin() + nin), wt(Wt.begin(), Wt.begin() + nw), out(nout);
+  if (atc_conv2d_nchw(ctx, x.data(), wt.data(), out.data(), n, c, h, w, k, r, s, precision) != ATC_OK)
+    throw std::runtime_error(atc_last_error(ctx));
+  for (size_t i = 0; i < nout; ++i) Out[i] = (double)out[i];
+  return true;
+}
+
+}  // namespace
+
 interp::DispatchContext make_gpu_dispatch(const api::ApiSpec& spec, atc_ctx* ctx) {
   interp::DispatchContext dc;
   const atc_spec_desc desc = encode_spec(spec);
   dc.handler = [spec, desc, ctx](const std::string& name, const std::vector<interp::DispatchArg>& args,
                                  interp::MemoryImage& mem) {
-    // rewriter.cpp:101-134: name, arity and kinds, positional decode
-    if (name != "atc_dispatch_" + spec.semantics)
-      throw std::runtime_error("dispatch name '" + name + "' does not match api semantics '" + spec.semantics + "'");
-    if (args.size() != spec.params.size())
-      throw std::runtime_error("dispatch arity " + std::to_string(args.size()) + ", api expects " +
-                               std::to_string(spec.params.size()));
-    std::vector<int64_t> sizes;
-    std::vector<std::string> regions;
-    for (size_t i = 0; i < spec.params.size(); ++i) {
-      const auto& ap = spec.params[i];
-      const auto& a = args[i];
-      if (ap.kind == api::ApiParamKind::Array) {
-        if (a.kind != interp::DispatchArg::Kind::Ptr)
-          throw std::runtime_error("dispatch arg for array '" + ap.name + "' is not a pointer");
-        if (!mem.regions.count(a.region)) throw std::runtime_error("dispatch region '" + a.region + "' missing");
-        regions.push_back(a.region);
-      } else if (ap.kind == api::ApiParamKind::IntSize) {
-        if (a.kind != interp::DispatchArg::Kind::Int)
-          throw std::runtime_error("dispatch arg for size '" + ap.name + "' is not an int");
-        sizes.push_back(a.i);
-      }
+    exact_dispatch(spec, desc, ctx, decode_call(spec, name, args, mem), mem);
+  };
+  return dc;
+}
+
+std::vector<long long> routed_sizes(const api::ApiSpec& spec, const std::map<std::string, long long>& sizes) {
+  // rewriter.cpp:194-205: conv as its im2col GEMM (filters x batch*out positions, depth c*r*s)
+  if (spec.semantics == "conv2d")
+    return {role_size(spec, sizes, "k"),
+            role_size(spec, sizes, "n") * role_size(spec, sizes, "oh") * role_size(spec, sizes, "ow"),
+            role_size(spec, sizes, "c") * role_size(spec, sizes, "r") * role_size(spec, sizes, "s")};
+  return {role_size(spec, sizes, "m"), role_size(spec, sizes, "n"), role_size(spec, sizes, "k")};
+}
+
+interp::DispatchContext make_gpu_routed_dispatch(const api::ApiSpec& spec, atc_ctx* ctx,
+                                                 const profitability::SvmModel* model,
+                                                 std::vector<std::string>* choices, int32_t precision) {
+  interp::DispatchContext dc;
+  const atc_spec_desc desc = encode_spec(spec);
+  dc.handler = [spec, desc, ctx, model, choices, precision](const std::string& name,
+                                                             const std::vector<interp::DispatchArg>& args,
+                                                             interp::MemoryImage& mem) {
+    // rewriter.cpp:190-209: the label comes first, from an arity-clipped decode of
+    // the size slots (so a call run_dispatch then rejects is still labelled)
+    bool xpu = false;
+    if (model && choices) {
+      std::map<std::string, long long> sizes;
+      for (size_t i = 0; i < spec.params.size() && i < args.size(); ++i)
+        if (spec.params[i].kind == api::ApiParamKind::IntSize) sizes[spec.params[i].name] = args[i].i;
+      xpu = profitability::predict_backend(*model, routed_sizes(spec, sizes)) == 1;
+      choices->push_back(xpu ? "xpu" : "cpu");
+    } else if (choices) {
+      choices->push_back("cpu");
     }
-    // full-region copies (rewriter.cpp:121), computed and written back on the GPU
-    std::vector<std::vector<double>> bufs;
-    std::vector<double*> ptrs;
-    std::vector<int64_t> lens;
-    std::vector<int32_t> f32;
-    for (const auto& rname : regions) bufs.push_back(mem.regions.at(rname).data);
-    for (size_t a = 0; a < regions.size(); ++a) {
-      ptrs.push_back(bufs[a].data());
-      lens.push_back((int64_t)bufs[a].size());
-      f32.push_back(mem.regions.at(regions[a]).elem == minilang::ScalarType::F32);
-    }
-    int rc = atc_dispatch(ctx, &desc, sizes.data(), ptrs.data(), lens.data(), f32.data());
-    if (rc == ATC_ERR_DISPATCH) {
-      // same wording as rewriter.cpp:141,145-147 ("... is not positive", "... elements ...")
-      throw std::runtime_error(std::string("dispatch: ") + atc_last_error(ctx));
-    }
-    if (rc != ATC_OK) throw std::runtime_error(atc_last_error(ctx));
-    const auto arrays = spec.arrays();
-    for (size_t a = 0; a < arrays.size(); ++a)
-      if (arrays[a]->liveness != api::Liveness::LiveIn) mem.regions.at(regions[a]).data = bufs[a];
+    const DecodedCall d = decode_call(spec, name, args, mem);
+    if (xpu && precision != kRouteExact && tensor_dispatch(spec, ctx, precision, d, mem)) return;
+    exact_dispatch(spec, desc, ctx, d, mem);
   };
   return dc;
 }

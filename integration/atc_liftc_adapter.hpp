@@ -9,7 +9,8 @@
 //      the P2 survivors, in rank order;
 //   2. the oracle DispatchContext (rewriter.cpp:176-181) — make_gpu_dispatch()
 //      returns a handler with the same checks and messages that computes on the
-//      GPU (FP64, bit-exact).
+//      GPU (FP64, bit-exact); make_gpu_routed_dispatch() is the routed one
+//      (rewriter.cpp:183-213), with "xpu" f32 calls on the tcgen05 backends.
 //
 // Nothing in the reference changes otherwise; the binding-independent half of
 // verify_rewrite (draw_sizes, build_probe_image, the original run) is recorded
@@ -17,6 +18,7 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <optional>
 #include <string>
 #include <vector>
@@ -27,6 +29,7 @@
 #include "liftc/interp.hpp"
 #include "liftc/matching.hpp"
 #include "liftc/minilang.hpp"
+#include "liftc/profitability.hpp"
 
 namespace liftc::gpu {
 
@@ -64,5 +67,23 @@ LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const ana
 
 // DispatchContext whose handler is run_dispatch on the GPU (atc_dispatch).
 interp::DispatchContext make_gpu_dispatch(const api::ApiSpec& spec, atc_ctx* ctx);
+
+// rewriter::make_routed_dispatch (rewriter.hpp, rewriter.cpp:183-213) on the GPU.
+// Labels each call "cpu"/"xpu" with profitability::predict_backend on the same
+// (m, n, k) features the reference uses and records it in *choices.  "cpu"
+// calls, f64 regions, and calls the FP32 backends cannot express run the exact
+// FP64 path (== make_gpu_dispatch, bit-identical to the reference).  "xpu" calls
+// on f32 regions run on atc_sgemm_rm / atc_conv2d_nchw at `precision`
+// (ATC_PREC_TF32 / ATC_PREC_3XTF32).  kRouteExact keeps every call on the exact
+// path, which makes the handler a drop-in for the reference's routed dispatch
+// (labels recorded, results unchanged).
+constexpr int32_t kRouteExact = -1;
+interp::DispatchContext make_gpu_routed_dispatch(const api::ApiSpec& spec, atc_ctx* ctx,
+                                                 const profitability::SvmModel* model,
+                                                 std::vector<std::string>* choices,
+                                                 int32_t precision = ATC_PREC_3XTF32);
+
+// The predictor features of one call (rewriter.cpp:194-205).
+std::vector<long long> routed_sizes(const api::ApiSpec& spec, const std::map<std::string, long long>& sizes);
 
 }  // namespace liftc::gpu

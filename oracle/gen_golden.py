@@ -1,6 +1,7 @@
 """Generate tests/golden/ from the compiled reference (TEST INFRASTRUCTURE).
 
     make -C oracle ref && python oracle/gen_golden.py
+    python oracle/gen_golden.py --svm     (tests/golden/svm_volume.json only)
 
 Runs `oracle/_ref/ref_tool golden <tmp>` (the unmodified reference: liftc_core
 built from /root/reference/proj/src) and converts its raw dump into small
@@ -12,6 +13,9 @@ committed fixtures:
                                   analysis, P2 test-set metadata (sizes, init-region
                                   FNV-1a + head values), pruned candidates with P1/P2
                                   verdicts, unpruned-space metadata
+  tests/golden/svm_volume.json    ref_tool svm-golden: the reference's train_svm model on
+                                  rewriter_test.cpp's volume set (save_svm JSON) and its
+                                  decision_value / predict_backend over a feature grid
   tests/golden/<stem>.npz         final-minus-init diffs of the original runs and the
                                   per-binding verdict arrays (P2 first failing test +
                                   reason at T=16, P1 verdict at 30 tests)
@@ -74,6 +78,9 @@ def convert(raw: str) -> None:
 
 def main() -> None:
     tool = os.path.join(HERE, "_ref", "ref_tool")
+    if len(sys.argv) > 1 and sys.argv[1] == "--svm":
+        subprocess.run([tool, "svm-golden", os.path.join(OUT, "svm_volume.json")], check=True)
+        return
     if len(sys.argv) > 1:
         convert(sys.argv[1])
         return

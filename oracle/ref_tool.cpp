@@ -8,6 +8,9 @@
 //                                   P1/P2 verdicts for every GEMM/conv corpus program
 //   time-p2  <stem> <spec> <T> <budget_s> <threads> [rules64]
 //   time-acc <stem> <spec> <T> <budget_s> <threads> [rules64]
+//   svm-golden <out.json>           profitability::train_svm on rewriter_test.cpp:109-118's
+//                                   volume-labelled set, save_svm's JSON, and
+//                                   decision_value / predict_backend over a feature grid
 //   time-xpu-gemm <m> <n> <k>       profitability::xpu_gemm (hardware_concurrency threads)
 //   time-cpu-gemm <m> <n> <k> <rows> profitability::cpu_gemm over a `rows`-row M slice
 //   time-conv <n> <c> <h> <w> <k> <r> <s>   equivalence::run_reference (conv2d, f64)
@@ -725,6 +728,43 @@ int cmd_time_conv(long long n, long long c, long long h, long long w, long long 
   return 0;
 }
 
+
+int cmd_svm_golden(const std::string& out) {
+  std::vector<profitability::TimingSample> data;
+  for (long long m = 2; m <= 10; m += 2)
+    for (long long n = 2; n <= 10; n += 2)
+      for (long long k = 2; k <= 10; k += 2) {
+        const long long v = m * n * k;
+        if (v > 150 && v < 600) continue;
+        profitability::TimingSample t;
+        t.sizes = {m, n, k};
+        t.t_cpu = 1.0;
+        t.t_xpu = v >= 600 ? 0.5 : 2.0;
+        t.label = v >= 600 ? 1 : 0;
+        data.push_back(t);
+      }
+  const auto model = profitability::train_svm(data);
+  profitability::save_svm(model, out + ".model");
+  std::ifstream in(out + ".model");
+  json j = {{"model", json::parse(in)}};
+  std::remove((out + ".model").c_str());
+  json cases = json::array();
+  std::vector<std::vector<long long>> grid;
+  for (long long m = 1; m <= 12; ++m)
+    for (long long n = 1; n <= 12; n += 1)
+      for (long long k = 1; k <= 12; k += 1) grid.push_back({m, n, k});
+  for (long long v : {16LL, 64LL, 256LL, 1024LL, 8192LL}) grid.push_back({v, v, v});
+  grid.push_back({48, 180, 576});  // a conv im2col feature (k, n*oh*ow, c*r*s)
+  grid.push_back({1, 1000, 3});
+  for (const auto& g : grid)
+    cases.push_back({{"mnk", g},
+                     {"decision", profitability::decision_value(model, g)},
+                     {"backend", profitability::predict_backend(model, g)}});
+  j["cases"] = cases;
+  std::ofstream(out) << j.dump(1) << "\n";
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -732,6 +772,7 @@ int main(int argc, char** argv) {
     if (argc < 2) throw std::runtime_error("usage: ref_tool <cmd> ...");
     std::string cmd = argv[1];
     if (cmd == "golden" && argc == 3) return cmd_golden(argv[2]);
+    if (cmd == "svm-golden" && argc == 3) return cmd_svm_golden(argv[2]);
     if ((cmd == "time-p2" || cmd == "time-acc") && argc >= 7)
       return cmd_time(cmd == "time-p2" ? "p2" : "acc", argv[2], argv[3], std::atoi(argv[4]),
                       std::atof(argv[5]), std::atoi(argv[6]),

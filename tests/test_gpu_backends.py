@@ -128,3 +128,81 @@ def test_conv2d_matches_reference_semantics_small():
 def test_bad_arguments_raise():
     with pytest.raises(AtcError):
         backends.conv2d_nchw(np.ones((1, 3, 5, 5), np.float32), np.ones((2, 3, 3, 3), np.float32))
+
+
+def _svm_model():
+    import json
+    import os
+
+    return json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "svm_volume.json")))["model"]
+
+
+def _routed_call(spec, ints, lens, elem, seed):
+    D, R = backends.DispatchArg, backends.Region
+    rng = np.random.default_rng(seed)
+    regions, args = {}, []
+    for p in spec.params:
+        if p.kind == "array":
+            regions[p.name] = R(rng.uniform(-1, 1, lens[p.role]).astype(np.float32).astype(np.float64), elem)
+            args.append(D("ptr", p.name))
+        else:
+            args.append(D("int", i=ints[p.role]))
+    return args, regions
+
+
+ROUTED = [("gemm_rowmajor", {"m": 256, "n": 192, "k": 320}, {"a": 256 * 320, "b": 320 * 192, "c": 256 * 192}, 320),
+          ("gemm_colmajor", {"m": 130, "n": 70, "k": 200}, {"a": 130 * 200, "b": 200 * 70, "c": 130 * 70}, 200),
+          ("gemm_rowmajor_ld", {"m": 200, "n": 96, "k": 160, "lda": 170, "ldb": 100, "ldc": 101},
+           {"a": 200 * 170, "b": 160 * 100, "c": 200 * 101}, 160),
+          ("conv2d", {"n": 2, "c": 64, "h": 12, "w": 11, "k": 48, "r": 3, "s": 3, "oh": 10, "ow": 9},
+           {"in": 2 * 64 * 12 * 11, "weights": 48 * 64 * 9, "out": 2 * 48 * 10 * 9}, 576)]
+
+
+@pytest.mark.parametrize("case", ROUTED, ids=[c[0] for c in ROUTED])
+@pytest.mark.parametrize("prec", ["tf32", "3xtf32"])
+def test_routed_dispatch_xpu(case, prec):
+    """make_routed_dispatch with the reference's trained model: these shapes label
+    "xpu"; f32 calls run on the tcgen05 backends within the stated bound of the exact
+    dispatch (untouched elements — ld gaps — stay bit-identical); f64 regions and
+    precision="exact" stay bit-identical to make_gpu_dispatch."""
+    name, ints, lens, depth = case
+    spec = fixtures.spec(name)
+    predict = backends.svm_predictor(_svm_model())
+    for elem in ("f32", "f64"):
+        args, regions = _routed_call(spec, ints, lens, elem, 5)
+        exact = {k: backends.Region(v.data.copy(), v.elem) for k, v in regions.items()}
+        backends.make_gpu_dispatch(spec)("atc_dispatch_" + spec.semantics, args, exact)
+        for mode in (prec, "exact"):
+            got = {k: backends.Region(v.data.copy(), v.elem) for k, v in regions.items()}
+            choices = []
+            backends.make_routed_dispatch(spec, predict, choices, mode)("atc_dispatch_" + spec.semantics, args, got)
+            assert choices == ["xpu"]
+            for k in regions:
+                a, b = got[k].data, exact[k].data
+                if elem == "f64" or mode == "exact":
+                    assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (k, elem, mode)
+                else:
+                    err = np.abs(a - b) / (1 + np.abs(b))
+                    assert err.max() <= TOLS[prec][0] * np.sqrt(depth), (k, err.max())
+                    moved = np.flatnonzero(a != b)
+                    if k.endswith(("C", "out")):
+                        assert len(moved) > 0  # the tensor path ran (results differ in low bits)
+                    else:
+                        assert len(moved) == 0, k
+
+
+def test_routed_dispatch_cpu_label():
+    """rewriter_test.cpp:106-140 on the GPU handler: 2x2x2 labels "cpu" and computes C=2.0."""
+    spec = fixtures.spec("gemm_rowmajor")
+    D, R = backends.DispatchArg, backends.Region
+    regions = {r: R(np.ones(16)) for r in "abc"}
+    args = [D("ptr", "a"), D("ptr", "b"), D("ptr", "c"), D("int", i=2), D("int", i=2), D("int", i=2)]
+    choices = []
+    backends.make_routed_dispatch(spec, backends.svm_predictor(_svm_model()), choices)("atc_dispatch_gemm", args,
+                                                                                        regions)
+    assert choices == ["cpu"] and regions["c"].data[:4].tolist() == [2.0] * 4
+    with pytest.raises(RuntimeError, match="elements"):
+        bad = [D("ptr", "a"), D("ptr", "b"), D("ptr", "c"), D("int", i=10), D("int", i=10), D("int", i=10)]
+        backends.make_routed_dispatch(spec, backends.svm_predictor(_svm_model()), choices)("atc_dispatch_gemm", bad,
+                                                                                            regions)
+    assert choices == ["cpu", "xpu"]  # labelled before run_dispatch's checks

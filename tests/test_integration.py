@@ -44,3 +44,15 @@ def test_adapter_unpruned_stress_space():
     assert rc == 0, err
     j = lines[-1]
     assert j["bindings"] == 279936 and j["p2_passed"] == 1 and j["winner"] == 44790 and j["p1_calls"] == 1
+
+
+def test_adapter_routed_dispatch():
+    """make_gpu_routed_dispatch vs rewriter::make_routed_dispatch (rewriter.cpp:183-213):
+    identical cpu/xpu labels on every lifted corpus function, bit-identical results on
+    the exact route; f32 GEMM (row/col/ld) and conv calls labelled "xpu" run on the
+    tcgen05 backends within their stated TF32 / 3xTF32 bounds; "cpu" stays exact."""
+    rc, lines, err = _run("routed")
+    assert rc == 0, err + json.dumps([x for x in lines if not x.get("ok", True)][:3])
+    assert lines[-1]["mismatches"] == 0
+    direct = [x for x in lines if "direct" in x]
+    assert len(direct) == 8 and all(x["ok"] for x in direct)
