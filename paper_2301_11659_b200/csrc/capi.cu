@@ -27,12 +27,12 @@ __global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out, uint8_t* out1);
 __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
-                                  uint8_t* out, uint8_t* out1, uint32_t* cm, uint32_t* cm1);
+                                  uint8_t* out, uint8_t* out1, uint32_t* cm);
 __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
                               uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                               unsigned long long* reason_hist);
 __global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need);
-__global__ void k_cmask(const uint8_t* table, uint64_t n_words, int nI, uint32_t* cmask);
+__global__ void k_cmask(const uint8_t* table, uint64_t n_words, int nI, uint32_t* cmask, int shift);
 __global__ void k_screen_conv_pairs(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
                                     uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
                                     unsigned long long* surv_cnt, unsigned long long* reason_hist, int lut_n);
@@ -269,6 +269,8 @@ atc_ctx* atc_create(int device) {
     return ctx;
   }
   cudaSetDevice(device);
+  // k_screen_conv_pairs: up to 2^11 row masks + rank / in-extent tables (~40 KB dynamic)
+  cudaFuncSetAttribute(k_screen_conv_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   if (!atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
 
       !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->free_ev, cudaEventDisableTiming), "cudaEventCreate") ||
@@ -835,7 +837,9 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
       for (int i = 0; i < ts->nI; ++i)
         for (int k = 0; k < ts->nI; ++k) pmax = std::max<int64_t>(pmax, ts->h_ints[i] * ts->h_ints[k]);
       const int lut_n = pmax < 4096 ? (int)pmax + 1 : 0;
-      const size_t smem = ((size_t)16 << ts->nI) + (size_t)(lut_n + 15) / 16 * 16;
+      const size_t nI2 = (size_t)ts->nI * ts->nI;
+      const size_t smem = ((size_t)16 << ts->nI) + (size_t)(lut_n + 15) / 16 * 16 +
+                          ((size_t)ts->nP * nI2 + 15) / 16 * 16 + nI2 * sizeof(float);
       // one wave (3 CTAs per SM at 80 registers): each CTA builds its tables once
       const unsigned g3 = std::min<unsigned>(g2, (unsigned)ctx->sm_count * 3);
       k_screen_conv_pairs<<<g3, kScreenThreads, smem, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
@@ -1118,19 +1122,16 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
     // conv with the canonical key (c first): one running sum per (perm, h, w, r, s)
     const uint64_t t_off = p_lo * e.pt.per_perm, t_bytes = np_local * e.pt.per_perm;
     const uint8_t* perms_local = d_perms + p_lo * sp.nA;
-    e.plan.cmask = e.plan.cmask1 = nullptr;
+    e.plan.cmask = nullptr;
     uint32_t* cm = nullptr;
-    uint32_t* cm1 = nullptr;
     const uint64_t words = e.table_bytes / (uint64_t)ts->nI;
     if (pairs) {
-      cm = (uint32_t*)atc_ctx_scratch(ctx, 23, words * 8 + 32);
+      cm = (uint32_t*)atc_ctx_scratch(ctx, 23, words * 4 + 32);
       if (!cm) {
         atc_set_error(ctx, "scratch allocation failed (cmask)");
         return ATC_ERR_CUDA;
       }
-      cm1 = cm + (words + 3) / 4 * 4;
       e.plan.cmask = cm;
-      e.plan.cmask1 = cm1;
     }
     const uint64_t w_off = t_off / (uint64_t)ts->nI;
     if (sp.sem == ATC_SEM_CONV2D && e.pt.R == 5 && e.plan.key_stride[1] == 1 && e.use_rows &&
@@ -1140,8 +1141,7 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
       k_pos0_table_conv<<<(unsigned)std::max<uint64_t>(
                               1, std::min<uint64_t>((t_bytes / ts->nI + 255) / 256, (uint64_t)ctx->sm_count * 16)),
                           256, 0, st>>>(ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off,
-                                        tab1 ? tab1 + t_off : nullptr, cm ? cm + w_off : nullptr,
-                                        cm1 ? cm1 + w_off : nullptr);
+                                        tab1 ? tab1 + t_off : nullptr, cm ? cm + w_off : nullptr);
       if (ctx->prof) ctx->prof_kernels += 1;
     } else {
       k_pos0_table<<<(unsigned)std::max<uint64_t>(
@@ -1153,8 +1153,8 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
         const uint64_t w_local = t_bytes / (uint64_t)ts->nI;
         const unsigned g =
             (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((w_local + 255) / 256, (uint64_t)ctx->sm_count * 16));
-        k_cmask<<<g, 256, 0, st>>>(tab + t_off, w_local, ts->nI, cm + w_off);
-        k_cmask<<<g, 256, 0, st>>>(tab1 + t_off, w_local, ts->nI, cm1 + w_off);
+        k_cmask<<<g, 256, 0, st>>>(tab + t_off, w_local, ts->nI, cm + w_off, 0);
+        k_cmask<<<g, 256, 0, st>>>(tab1 + t_off, w_local, ts->nI, cm + w_off, 16);
         if (ctx->prof) ctx->prof_kernels += 2;
       }
     }

@@ -84,10 +84,10 @@ struct RowPlan {
   // = the smallest n writing every dirty position of region p at t = 0 (k_gemm_need;
   // INT32_MAX: none does, -1: not tabulated, use the dirty list)
   const int32_t* gemm_need;
-  // conv (k_screen_conv_pairs): position-0 verdict bits over the nI values of tc_c
-  // per (perm, h, w, r, s) key (k_cmask)
+  // conv (k_screen_conv_pairs): verdict bits over the nI values of tc_c per
+  // (perm, h, w, r, s) key — output position 0 in bits 0..15, position 1 (used when
+  // tc_ow >= 2) in bits 16..31 (k_pos0_table_conv / k_cmask)
   const uint32_t* cmask;
-  const uint32_t* cmask1;  // the same at output position 1 (tc_ow >= 2), or null
 };
 
 enum : int32_t { kUndecided = -2 };

@@ -253,11 +253,12 @@ __global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need) {
 // reference sums z (channel) outermost, so the sum for c channels is the running
 // sum after z = c - 1 — every value of tc_c is read off one pass (same order, same
 // bits as k_pos0_table's per-entry loops).  Lanes of a warp share (r, s).
-// cm / cm1 (optional): the same verdicts as bit words over the c digits — word
-// (perm, h, w, r, s) bit j = table entry (perm, c digit j, h, w, r, s) == 1 — which
-// is what k_screen_conv_pairs reads (one thread owns exactly one word).
+// cm (optional): the same verdicts as bit words over the c digits — word
+// (perm, h, w, r, s) bit j = table entry (perm, c digit j, h, w, r, s) == 1 for
+// output position 0, bit 16 + j the same for position 1 — which is what
+// k_screen_conv_pairs reads (one thread owns exactly one word).
 __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
-                                  uint8_t* out, uint8_t* out1, uint32_t* cm, uint32_t* cm1) {
+                                  uint8_t* out, uint8_t* out1, uint32_t* cm) {
   const uint64_t nI = (uint64_t)ts.nI, nI2 = nI * nI;
   const uint64_t inner = nI2 * (uint64_t)n_perms;  // (h, w, perm) combinations
   const uint64_t total = inner * nI2;              // x (r, s)
@@ -291,8 +292,7 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
         m0 |= (out[base + j] == 1 ? 1u : 0u) << j;
         if (out1) m1 |= (out1[base + j] == 1 ? 1u : 0u) << j;
       }
-      cm[base / nI] = m0;
-      if (cm1) cm1[base / nI] = m1;
+      cm[base / nI] = m0 | m1 << 16;  // position 0 in bits 0..15, position 1 in bits 16..31
     };
     // entries whose c digit is < 1 (or a bad shape): the empty sum; others: 2 until computed
     for (uint64_t j = 0; j < nI; ++j) {

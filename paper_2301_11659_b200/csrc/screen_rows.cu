@@ -453,13 +453,14 @@ __global__ void __launch_bounds__(256) k_screen_conv_planes(TestsetView ts, cons
 }
 
 // ----------------------------------------------------------------------------
-// k_cmask: position-0 verdict bits of the nI values of tc_c (the first table
-// role, key stride 1): cmask[i] bit j = table[i*nI + j] == 1.
-__global__ void k_cmask(const uint8_t* table, uint64_t n_words, int nI, uint32_t* cmask) {
+// k_cmask: verdict bits of the nI values of tc_c (the first table role, key
+// stride 1): cmask[i] bit (shift + j) = table[i*nI + j] == 1.
+// shift 16: OR the bits into the upper half (the position-1 verdicts).
+__global__ void k_cmask(const uint8_t* table, uint64_t n_words, int nI, uint32_t* cmask, int shift) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_words; i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t m = 0;
     for (int j = 0; j < nI; ++j) m |= (table[i * nI + j] == 1 ? 1u : 0u) << j;
-    cmask[i] = m;
+    cmask[i] = shift ? (cmask[i] | m << shift) : m;
   }
 }
 
@@ -573,6 +574,28 @@ __global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const
   __syncthreads();
   int p2 = 1;  // power of two > nI2: branch-free search over the padded products
   while (p2 <= nI2) p2 <<= 1;
+  // per (in region, w digit, h digit): the number of pair products <= len(in)/(h*w)
+  // (the s_pgt index of the in-extent dispatch check), and 1/(h*w) for the UB bound
+  const int nP = ts.nP;
+  uint8_t* s_ainr = s_rank + (lut_n + 15) / 16 * 16;
+  float* s_rhw = reinterpret_cast<float*>(s_ainr + (nP * nI2 + 15) / 16 * 16);
+  for (int i = threadIdx.x; i < nP * nI2; i += blockDim.x) {
+    const int p = i / nI2, wh = i - p * nI2, wd = wh / nI, hd = wh - wd * nI;
+    const int64_t hw = (int64_t)s_u[hd] * s_u[wd];
+    int lo = 0;
+    if (hw >= 1) {
+      const int64_t a = ts.region_len[p] / hw;
+      const int32_t tc = (int32_t)(a > INT32_MAX - 1 ? INT32_MAX - 1 : a);
+      for (int step = p2 >> 1; step > 0; step >>= 1)
+        if (s_prod[lo + step - 1] <= tc) lo += step;
+    }
+    s_ainr[i] = (uint8_t)lo;
+  }
+  for (int i = threadIdx.x; i < nI2; i += blockDim.x) {
+    const int64_t hw = (int64_t)s_u[i % nI] * s_u[i / nI];
+    s_rhw[i] = hw >= 1 ? __frcp_rn((float)hw) : 0.f;
+  }
+  __syncthreads();
   // pairs whose product x*c exceeds t (t >= 0; t >= lut_n: none when lut_n > 0)
   auto gt_prod = [&](int64_t t) -> M128 {
     if (lut_n) return s_pgt[t >= lut_n ? nI2 : s_rank[t]];
@@ -591,10 +614,12 @@ __global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const
 #pragma unroll
   for (int q = 2; q < NS; ++q) cks[q] = (uint32_t)(plan.key_stride[q] / (uint64_t)nI);
   const M128 all = bit_range(0, nI2);
-  const M128 x_lt1 = ~s_gtx[0], c_lt1 = ~s_gtc[0];
+  const M128 x_lt1 = ~s_gtx[0] & all, c_lt1 = ~s_gtc[0] & all;
   const uint64_t planes_per_perm = size_maps / (uint64_t)nI2;
   const uint32_t magic = (uint32_t)(0xFFFFFFFFull / (uint32_t)nI) + 1u;  // n / nI = umulhi(n, magic), n < 2^27
   unsigned int cnt1 = 0, cnt2 = 0, cnt3 = 0, cnt4 = 0;
+  // whole cubes inside [begin, end): mismatches are counted as the remainder
+  unsigned int f_bind = 0, f2 = 0, f4 = 0, f_surv = 0;
   // a thread owns a "cube": the nI planes sharing the permutation and digits 3..8
   // (all values of tc_h, digit 2); everything free of h is computed once per cube
   const uint64_t nI3 = (uint64_t)nI2 * nI;
@@ -653,6 +678,52 @@ __global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const
     uint32_t ckey0 = (uint32_t)perm * cperm;
 #pragma unroll
     for (int q = 3; q < NS; ++q) ckey0 += (uint32_t)digit[q] * cks[q];
+    // position-1 verdicts (bits 16..) apply when ow >= 2: output position 1 is (0, 0, 0, 1)
+    const uint32_t sel = cow >= 2 ? 0xFFFFFFFFu : 0xFFFFu;
+    if (c0b >= begin && c0b + nI3 <= end) {  // the whole cube: no range masks
+      f_bind += (unsigned int)nI3;
+      if (cube_bad) {
+        f2 += (unsigned int)nI3;
+        continue;
+      }
+      const uint8_t* ainr = s_ainr + ((uint32_t)p_in * nI + digit[3]) * nI;
+      const float* rhw = s_rhw + digit[3] * nI;
+      for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
+        const int32_t ch = s_u[hd];
+        if (ch < 1) {
+          f2 += (unsigned int)nI2;
+          continue;
+        }
+        const M128 dm = cube_dm | s_pgt[ainr[hd]];
+        M128 ok = all & ~dm;
+        f2 += popc(dm);
+        if (!any(ok)) continue;
+        const int32_t hw = ch * cw;
+        // UB needs (x*c - 1)*h*w + Q' >= len(in) with x*c*h*w <= len(in): only if Q' >= h*w
+        if (q_rest >= hw) {
+          const int64_t alim = (int64_t)len_in + hw - q_rest;
+          const uint32_t am1 = (uint32_t)(alim - 1);
+          const M128 um =
+              alim <= 0 ? ok : (ok & gt_prod(lut_n ? div_capn(am1, hw, rhw[hd], qcap) : (int)(am1 / (uint32_t)hw)));
+          f4 += popc(um);
+          ok = ok & ~um;
+          if (!any(ok)) continue;
+        }
+        const uint32_t cw2 = __ldg(plan.cmask + ckey0 + (uint32_t)hd * cks[2]) & sel;
+        ok = ok & ~(dirty_fail | s_rowx[(cw2 | cw2 >> 16) & 0xFFFFu]);
+        if (any(ok)) {
+          const unsigned int k = popc(ok);
+          f_surv += k;
+          const uint64_t p0 = c0b + (uint64_t)hd * nI2;
+          unsigned long long slot = atomicAdd(surv_cnt, (unsigned long long)k);
+          for (uint64_t w = ok.lo; w; w &= w - 1, ++slot)
+            if (slot < surv_cap) surv[slot] = p0 + (uint64_t)(__ffsll((long long)w) - 1) - begin;
+          for (uint64_t w = ok.hi; w; w &= w - 1, ++slot)
+            if (slot < surv_cap) surv[slot] = p0 + 64 + (uint64_t)(__ffsll((long long)w) - 1) - begin;
+        }
+      }
+      continue;
+    }
     for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
       const uint64_t p0 = c0b + (uint64_t)hd * nI2;
       if (p0 + nI2 <= begin || p0 >= end) continue;
@@ -675,11 +746,8 @@ __global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const
         um = alim <= 0 ? ok : (ok & gt_prod(lut_n ? div_capn(am1, hw, r_hw, qcap) : (int)(am1 / (uint32_t)hw)));
         ok = ok & ~um;
         if (any(ok)) {
-          const uint32_t ckey = ckey0 + (uint32_t)hd * cks[2];
-          M128 tab = s_rowx[__ldg(plan.cmask + ckey)];
-          // output position 1 is (0, 0, 0, 1) when ow >= 2: its tabulated verdict too
-          if (plan.cmask1 && cow >= 2) tab = tab | s_rowx[__ldg(plan.cmask1 + ckey)];
-          mm = ok & (dirty_fail | tab);
+          const uint32_t cw2 = __ldg(plan.cmask + ckey0 + (uint32_t)hd * cks[2]) & sel;
+          mm = ok & (dirty_fail | s_rowx[(cw2 | cw2 >> 16) & 0xFFFFu]);
           ok = ok & ~mm;
         }
       }
@@ -695,6 +763,10 @@ __global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const
       }
     }
   }
+  // whole cubes: every binding not counted as dispatch / UB / survivor is a mismatch
+  cnt1 += f_bind - f2 - f4 - f_surv;
+  cnt2 += f2;
+  cnt4 += f4;
   unsigned int cnt[ATC_REASON_COUNT] = {0, cnt1, cnt2, cnt3, cnt4};
 #pragma unroll
   for (int r = 1; r < ATC_REASON_COUNT; ++r) {
