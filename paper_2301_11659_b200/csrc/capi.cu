@@ -27,7 +27,7 @@ __global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out, uint8_t* out1);
 __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
-                                  uint8_t* out, uint8_t* out1, uint32_t* cm);
+                                  uint8_t* out, uint8_t* out1, uint32_t* cm, int stage_a, int stage_b);
 __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
                               uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                               unsigned long long* reason_hist);
@@ -52,7 +52,7 @@ __global__ void k_confirm_pre(TestsetView ts, SpecView sp, BindingSource src, co
 __global__ void k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                              const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
                              const uint32_t* pend, const unsigned long long* pend_cnt, uint32_t* next,
-                             unsigned long long* next_cnt, int mode);
+                             unsigned long long* next_cnt, int mode, int lazy);
 __global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
                              const int32_t* surv_keys, int32_t* keys);
 __global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason);
@@ -896,9 +896,18 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     k_confirm_pre<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 255) / 256, ctx->sm_count * 8)),
                     256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pend, next_cnt + 1,
                                   ctx->mode);
-  k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pre ? pend : nullptr,
-                                     next_cnt + 1, next, next_cnt, ctx->mode);
-  k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, next, next_cnt, ctx->mode);
+  if (pre && !keys) {
+    // enumerated ranges report reasons, not failing tests: t >= 1 first over every
+    // pending survivor, then t = 0 only where it can change the reason (k_confirm_t0)
+    k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, pend, next_cnt + 1,
+                                         ctx->mode);
+    k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pend, next_cnt + 1,
+                                       next, next_cnt, ctx->mode, 1);
+  } else {
+    k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys,
+                                       pre ? pend : nullptr, next_cnt + 1, next, next_cnt, ctx->mode, 0);
+    k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, next, next_cnt, ctx->mode);
+  }
   if (ctx->prof) {
     cudaEventRecord(e2.second, st);
     ctx->prof_confirm.push_back(e2);
@@ -1138,10 +1147,19 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
         conv_thresholds_ok(sp, e.plan, ts->nI)) {
       // one running sum per (perm, h, w, r, s); the pair screen's bit words come out
       // of the same pass
-      k_pos0_table_conv<<<(unsigned)std::max<uint64_t>(
-                              1, std::min<uint64_t>((t_bytes / ts->nI + 255) / 256, (uint64_t)ctx->sm_count * 16)),
-                          256, 0, st>>>(ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off,
-                                        tab1 ? tab1 + t_off : nullptr, cm ? cm + w_off : nullptr);
+      // every element a sum reads: in < (cmax*hmax + rmax)*wmax + smax + 1 (position 1
+      // included), weights < cmax*rmax*smax; staged in shared memory when <= 48 KB
+      int64_t umax = 0;
+      for (int q = 0; q < ts->nI; ++q) umax = std::max<int64_t>(umax, ts->h_ints[q]);
+      const int64_t need_a = (umax * umax + umax) * umax + umax + 1, need_b = umax * umax * umax;
+      const bool stage = umax >= 1 && need_a + need_b <= 6144;
+      const int sa = stage ? (int)need_a : 0, sb = stage ? (int)need_b : 0;
+      const uint64_t per = (uint64_t)ts->nI * ts->nI * ts->nI * ts->nI;
+      const dim3 grid((unsigned)std::max<uint64_t>(1, std::min<uint64_t>((per + 255) / 256, 65535)),
+                      (unsigned)np_local);
+      k_pos0_table_conv<<<grid, 256, (size_t)(sa + sb) * sizeof(double), st>>>(
+          ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off, tab1 ? tab1 + t_off : nullptr,
+          cm ? cm + w_off : nullptr, sa, sb);
       if (ctx->prof) ctx->prof_kernels += 1;
     } else {
       k_pos0_table<<<(unsigned)std::max<uint64_t>(

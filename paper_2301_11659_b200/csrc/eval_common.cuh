@@ -162,13 +162,55 @@ __device__ __forceinline__ float gemm_dot32(const double* a, int sa, const doubl
 }
 // reference_conv2d's inner loops (equivalence.cpp:85-90); `in` points at
 // in[b][0][y][x], `wt` at wt[q][0][0][0]
+// Taps of a row are loaded four at a time ahead of their (in-order) additions: the
+// loads do not depend on the running sum, so a row's loads are in flight together.
 __device__ __forceinline__ double conv_dot64(const double* in, const double* wt, int C, int R, int S, int H, int W) {
   double acc = 0.0;
   for (int z = 0; z < C; ++z)
-    for (int u = 0; u < R; ++u)
-      for (int v = 0; v < S; ++v)
-        acc = dadd(acc, dmul(in[(z * H + u) * W + v], wt[(z * R + u) * S + v]));
+    for (int u = 0; u < R; ++u) {
+      const double* a = in + (z * H + u) * W;
+      const double* b = wt + (z * R + u) * S;
+      for (int v0 = 0; v0 < S; v0 += 4) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          av[i] = v0 + i < S ? a[v0 + i] : 0.0;
+          bv[i] = v0 + i < S ? b[v0 + i] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (v0 + i < S) acc = dadd(acc, dmul(av[i], bv[i]));
+      }
+    }
   return acc;
+}
+
+// conv_dot64 for MO outputs at once (independent chains, each in conv_dot64's order).
+template <int MO>
+__device__ __forceinline__ void conv_dot64_multi(const double* const* in, const double* const* wt, int C, int R, int S,
+                                                 int H, int W, double* acc) {
+#pragma unroll
+  for (int m = 0; m < MO; ++m) acc[m] = 0.0;
+  for (int z = 0; z < C; ++z)
+    for (int u = 0; u < R; ++u) {
+      const int ia = (z * H + u) * W, iw = (z * R + u) * S;
+      for (int v0 = 0; v0 < S; v0 += 4) {
+        double av[4][MO], bv[4][MO];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int m = 0; m < MO; ++m) {
+            av[i][m] = v0 + i < S ? in[m][ia + v0 + i] : 0.0;
+            bv[i][m] = v0 + i < S ? wt[m][iw + v0 + i] : 0.0;
+          }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (v0 + i < S) {
+#pragma unroll
+            for (int m = 0; m < MO; ++m) acc[m] = dadd(acc[m], dmul(av[i][m], bv[i][m]));
+          }
+      }
+    }
 }
 __device__ __forceinline__ float conv_dot32(const double* in, const double* wt, int C, int R, int S, int H, int W,
                                             float& Sabs) {

@@ -258,32 +258,42 @@ __global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need) {
 // output position 0, bit 16 + j the same for position 1 — which is what
 // k_screen_conv_pairs reads (one thread owns exactly one word).
 __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
-                                  uint8_t* out, uint8_t* out1, uint32_t* cm) {
+                                  uint8_t* out, uint8_t* out1, uint32_t* cm, int stage_a, int stage_b) {
+  // blockIdx.y = permutation; blockIdx.x strides over its (h, w, r, s) entries.
+  // stage_a / stage_b > 0: the first stage_a / stage_b elements of the in / weights
+  // regions (every element a tabulated sum can read) are staged in shared memory.
+  extern __shared__ double s_stage[];
   const uint64_t nI = (uint64_t)ts.nI, nI2 = nI * nI;
-  const uint64_t inner = nI2 * (uint64_t)n_perms;  // (h, w, perm) combinations
-  const uint64_t total = inner * nI2;              // x (r, s)
+  const uint64_t per = nI2 * nI2;  // (h, w) x (r, s)
   __shared__ int64_t s_ints[kMaxInts];
   if (threadIdx.x < ts.nI) s_ints[threadIdx.x] = ts.ints[threadIdx.x];
+  const uint64_t perm = blockIdx.y;
+  const int pA = perms[perm * sp.nA + sp.arr_of_role[0]];
+  const int pB = perms[perm * sp.nA + sp.arr_of_role[1]];
+  const int pC = perms[perm * sp.nA + sp.arr_of_role[2]];
+  const int64_t lenA = ts.region_len[pA], lenB = ts.region_len[pB];
+  const double* A = ts.init + ts.region_off[pA];
+  const double* B = ts.init + ts.region_off[pB];
+  if (stage_a > 0) {
+    const int na = (int)(lenA < stage_a ? lenA : stage_a), nb = (int)(lenB < stage_b ? lenB : stage_b);
+    for (int k = threadIdx.x; k < na; k += blockDim.x) s_stage[k] = A[k];
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) s_stage[stage_a + k] = B[k];
+    A = s_stage;
+    B = s_stage + stage_a;
+  }
   __syncthreads();
   int64_t cmax_all = 0;
   for (int j = 0; j < ts.nI; ++j) cmax_all = max(cmax_all, s_ints[j]);
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t rs_d = i / inner, hwp = i - rs_d * inner;
-    const uint64_t perm = hwp / nI2, hw_d = hwp - perm * nI2;
+  const double want = ts.fin[ts.region_off[pC]];
+  const bool f32 = ts.is_f32[pC] != 0;
+  const bool pos1 = out1 && ts.region_len[pC] > 1;
+  const double want1 = pos1 ? ts.fin[ts.region_off[pC] + 1] : 0.0;
+  const uint8_t empty_res = mismatch(round_region(0.0, f32), want, f32) ? 1 : 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t rs_d = i / nI2, hw_d = i - rs_d * nI2;
     const uint64_t r_d = rs_d % nI, s_d = rs_d / nI, h_d = hw_d % nI, w_d = hw_d / nI;
-    const int64_t h = ts.ints[h_d], w = ts.ints[w_d], r = ts.ints[r_d], s = ts.ints[s_d];
+    const int64_t h = s_ints[h_d], w = s_ints[w_d], r = s_ints[r_d], s = s_ints[s_d];
     const uint64_t base = perm * pt.per_perm + nI * (h_d + nI * (w_d + nI * (r_d + nI * s_d)));  // + c digit
-    const int pA = perms[perm * sp.nA + sp.arr_of_role[0]];
-    const int pB = perms[perm * sp.nA + sp.arr_of_role[1]];
-    const int pC = perms[perm * sp.nA + sp.arr_of_role[2]];
-    const double* A = ts.init + ts.region_off[pA];
-    const double* B = ts.init + ts.region_off[pB];
-    const double want = ts.fin[ts.region_off[pC]];
-    const bool f32 = ts.is_f32[pC] != 0;
-    const int64_t lenA = ts.region_len[pA], lenB = ts.region_len[pB];
-    const bool pos1 = out1 && ts.region_len[pC] > 1;
-    const double want1 = pos1 ? ts.fin[ts.region_off[pC] + 1] : 0.0;
-    const uint8_t empty_res = mismatch(round_region(0.0, f32), want, f32) ? 1 : 0;
     const bool shape_ok = r >= 1 && s >= 1 && h >= 0 && w >= 0;
     auto words = [&]() {  // this thread's entries as bit words (it wrote them itself)
       if (!cm) return;
@@ -296,7 +306,7 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
     };
     // entries whose c digit is < 1 (or a bad shape): the empty sum; others: 2 until computed
     for (uint64_t j = 0; j < nI; ++j) {
-      const bool empty_sum = !shape_ok || ts.ints[j] < 1;
+      const bool empty_sum = !shape_ok || s_ints[j] < 1;
       out[base + j] = empty_sum ? empty_res : 2;
       if (out1) out1[base + j] = 2;
     }
@@ -312,7 +322,7 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
       const bool v0 = imax < lenA && wmax < lenB;  // imax >= 0 here
       v1_live = v1_live && imax + 1 < lenA && wmax < lenB;
       if (!v0) break;  // monotone in c: no larger c is tabulated either
-      // indices below are < len(region) < 2^31 here: 32-bit
+      // indices below are < len(region) < 2^31 here (and < stage_a / stage_b when staged)
       const int hi = (int)h, wi = (int)w, ri = (int)r, si = (int)s, zi = (int)z;
       if (v1_live) {
         for (int u = 0; u < ri; ++u) {
@@ -601,6 +611,36 @@ __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const Bin
               S = (int)d.cs, OH = (int)d.coh, OW = (int)d.cow;
     const int64_t wext = (int64_t)N * K * OH * OW;
     bad = ts.dirty_max[tpC] >= wext;
+    if (mode == ATC_MODE_FP64) {
+      // four outputs per lane per step: four independent accumulation chains (each in
+      // the reference's order) hide the dependent-add latency of long checks
+      constexpr int MO = 4;
+      for (int o0 = 0; o0 < (int)wext && !bad; o0 += 32 * MO) {
+        const double* inp[MO];
+        const double* wtp[MO];
+        int oo[MO];
+#pragma unroll
+        for (int m = 0; m < MO; ++m) {
+          const int o = o0 + m * 32 + lane;
+          oo[m] = o < wext ? o : -1;
+          int rem = o < wext ? o : 0;
+          const int x = rem % OW; rem /= OW;
+          const int y = rem % OH; rem /= OH;
+          const int q = rem % K;
+          const int b = rem / K;
+          inp[m] = A + ((b * C) * H + y) * W + x;
+          wtp[m] = B + (q * C) * R * S;
+        }
+        double acc[MO];
+        conv_dot64_multi<MO>(inp, wtp, C, R, S, H, W, acc);
+        bool mm = false;
+#pragma unroll
+        for (int m = 0; m < MO; ++m)
+          if (oo[m] >= 0) mm = mm || mismatch(round_region(acc[m], f32), __ldg(F + oo[m]), f32);
+        bad = __any_sync(0xffffffffu, mm);
+      }
+      return bad ? ATC_FAIL_MISMATCH : 0;
+    }
     for (int o0 = 0; o0 < (int)wext && !bad; o0 += 32) {
       const int o = o0 + lane;
       bool mm = false;
@@ -688,29 +728,42 @@ __global__ void __launch_bounds__(256) k_confirm_pre(TestsetView ts, SpecView sp
         }
       }
     }
-    if (!decided) pend[atomicAdd(pend_cnt, 1ull)] = (uint32_t)si;
+    if (!decided) {
+      surv_keys[si] = kPassKey;  // lazy K2a / K2b fold failures in with atomicMin
+      pend[atomicAdd(pend_cnt, 1ull)] = (uint32_t)si;
+    }
   }
 }
 
 // K2a: one WARP per pending survivor (all survivors without K2-pre), test t = 0
 // only: every written output, 32 per step.  Survivors of t = 0 are appended to
 // `next` for K2b.
+// lazy (enumerated ranges, which report reasons but not failing tests): K2b has
+// already run over the pending list, and t = 0 is checked only where it can change
+// the reason — a binding whose first failure at t >= 1 is a mismatch is a mismatch
+// whatever t = 0 gives (K2-pre has passed t = 0's scalar checks).
 __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src,
                                                     const uint64_t* surv, const unsigned long long* surv_cnt,
                                                     uint64_t surv_cap, int32_t* surv_keys, const uint32_t* pend,
                                                     const unsigned long long* pend_cnt, uint32_t* next,
-                                                    unsigned long long* next_cnt, int mode) {
+                                                    unsigned long long* next_cnt, int mode, int lazy) {
   const int lane = threadIdx.x & 31;
   unsigned long long cnt = pend ? *pend_cnt : *surv_cnt;
   if (cnt > surv_cap) cnt = surv_cap;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
-  for (uint64_t wi = (uint64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; wi < cnt; wi += warps) {
+  // warp-major numbering: consecutive items land in different CTAs (different SMs) —
+  // the few long full-length checks do not share an SM
+  for (uint64_t wi = (uint64_t)(threadIdx.x / 32) * gridDim.x + blockIdx.x; wi < cnt; wi += warps) {
     const uint64_t si = pend ? pend[wi] : wi;
+    if (lazy) {
+      const int32_t k = surv_keys[si];
+      if (k != kPassKey && (k & 7) == ATC_FAIL_MISMATCH) continue;
+    }
     const int r = warp_verdict(ts, sp, src, surv[si], 0, mode, lane);
     if (lane == 0) {
       if (r) {
         surv_keys[si] = fail_key(0, r);
-      } else {
+      } else if (!lazy) {
         surv_keys[si] = kPassKey;
         const unsigned long long slot = atomicAdd(next_cnt, 1ull);
         next[slot] = (uint32_t)si;
@@ -733,10 +786,12 @@ __global__ void __launch_bounds__(256) k_confirm_warp(TestsetView ts, SpecView s
   if (nt <= 0) return;
   const uint64_t work = cnt * (uint64_t)nt;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  // t-major: every binding's t = 1 item is dispatched before any t = 2 item, so the
+  // later items of bindings that fail early are mostly skipped
   for (uint64_t w = (uint64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; w < work; w += warps) {
-    const uint64_t wi = w / nt;
-    const uint32_t si = sel[wi];
-    const int t = 1 + (int)(w - wi * nt);
+    const uint64_t tt = w / cnt;
+    const uint32_t si = sel[w - tt * cnt];
+    const int t = 1 + (int)tt;
     if (*(volatile int32_t*)(surv_keys + si) < fail_key(t, 0)) continue;  // failed at a lower t already
     const int r = warp_verdict(ts, sp, src, surv[si], t, mode, lane);
     if (lane == 0 && r) atomicMin(&surv_keys[si], fail_key(t, r));
