@@ -169,6 +169,15 @@ typedef struct {
   const int64_t* diff_off;     /* [T*n_ptrs + 1]: entries of (t, p) = [off[i], off[i+1]) */
   const int32_t* diff_pos;     /* final-minus-init positions                           */
   const double* diff_val;      /* final values there                                  */
+  /* nonzero: generate only the part of each region an evaluation can read.  With
+   * U = test t's largest int value, every index the gemm / conv2d semantics read
+   * for a binding that passes run_dispatch's extent check and the UB check is
+   * below U^4 + 2U^2 + 2U + 1 (conv input: (N*C - 1)*H*W + (OH + R - 2)*W + OW + S - 2;
+   * weights, outputs and every gemm operand are smaller), so region (t, p) is
+   * generated up to that bound or one past its last final-minus-init position,
+   * whichever is larger (capped at the region length).  Evaluations are unchanged;
+   * atc_testsets_download refuses such a handle. */
+  int32_t needed_only;
 } atc_seeded_testsets;
 int atc_testsets_upload_seeded(atc_ctx* ctx, const atc_seeded_testsets* ts, atc_testset_handle** out);
 

@@ -87,6 +87,7 @@ class SeededTestsets(C.Structure):
         ("diff_off", C.c_void_p),
         ("diff_pos", C.c_void_p),
         ("diff_val", C.c_void_p),
+        ("needed_only", C.c_int32),
     ]
 
 

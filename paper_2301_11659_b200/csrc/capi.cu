@@ -16,7 +16,9 @@
 
 namespace atc {
 __global__ void k_probe_regions(int T, int nP, const uint64_t* seeds, const uint64_t* skips, const int64_t* region_len,
-                                const int32_t* is_f32, const int64_t* region_off, double* init, double* fin);
+                                const int32_t* is_f32, const int64_t* region_off, const int64_t* need, double* init,
+                                double* fin, TestsetView v, const int64_t* diff_off, const int32_t* diff_pos,
+                                const double* diff_val);
 __global__ void k_apply_diffs(int nP, const int64_t* region_len, const int64_t* region_off, const int64_t* diff_off,
                               const int32_t* diff_pos, const double* diff_val, double* fin);
 __global__ void k_build_dirty(TestsetView ts, int32_t* dirty_pos, int32_t* dirty_cnt, int32_t* dirty_max);
@@ -81,6 +83,7 @@ struct atc_testset_handle {
   uint8_t* seeded = nullptr;    // seeds, stream positions, final-minus-init entries
   size_t seeded_cap = 0;
   cudaEvent_t reuse = nullptr;  // readers of the previous contents are done (compute stream)
+  bool needed_only = false;     // seeded with needed_only: region prefixes only
   uint8_t* pin = nullptr;       // pinned staging of the metadata + seeded blocks (async DMA)
   size_t pin_bytes = 0;
 };
@@ -382,7 +385,7 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
   const int64_t nd_s = sd ? sd->diff_off[TP] : 0;
   const size_t seeded_need =
       sd ? ((size_t)T * 8 + 15) / 16 * 16 + (TP * 8 + 15) / 16 * 16 + ((TP + 1) * 8 + 15) / 16 * 16 +
-               ((size_t)nd_s * 8 + 15) / 16 * 16 + ((size_t)nd_s * 4 + 15) / 16 * 16
+               ((size_t)nd_s * 8 + 15) / 16 * 16 + ((size_t)nd_s * 4 + 15) / 16 * 16 + (TP * 8 + 15) / 16 * 16
          : 0;
   // in-place updates stage through the handle's pinned buffer (true async DMA,
   // allocated once); a first upload stages through pageable memory (the driver
@@ -432,6 +435,7 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
                         "H2D metadata");
   double* init = const_cast<double*>(h->view.init);
   double* fin = const_cast<double*>(h->view.fin);
+  bool fused = false;  // dirty lists built by k_probe_regions
   if (ts_full) {
     // host regions that lie back to back in the same order as the device pool are
     // copied as one run (one DMA instead of T*n_ptrs)
@@ -493,7 +497,22 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
       return o;
     };
     const size_t o_seeds = take((size_t)T * 8), o_skips = take(TP * 8), o_doffs = take((TP + 1) * 8),
-                 o_dvs = take((size_t)nd * 8), o_dps = take((size_t)nd * 4);
+                 o_dvs = take((size_t)nd * 8), o_dps = take((size_t)nd * 4), o_need = take(TP * 8);
+    // needed_only: region (t, p) up to max(U^4 + 2U^2 + 2U + 1, last final-minus-init
+    // position + 1), U = test t's largest int (include/atc_b200.h); else whole regions
+    std::vector<int64_t> need(TP);
+    for (int t = 0; t < T; ++t) {
+      int64_t u = 1;
+      for (int q = 0; q < nI; ++q) u = std::max<int64_t>(u, sd->int_values[(size_t)t * nI + q]);
+      const int64_t bound = u > 46340 ? INT64_MAX : u * u * u * u + 2 * u * u + 2 * u + 1;
+      for (int p = 0; p < nP; ++p) {
+        const size_t i = (size_t)t * nP + p;
+        int64_t n = bound;
+        for (int64_t e = sd->diff_off[i]; e < sd->diff_off[i + 1]; ++e) n = std::max<int64_t>(n, sd->diff_pos[e] + 1);
+        need[i] = sd->needed_only ? std::min<int64_t>(n, h->lens[p]) : h->lens[p];
+      }
+    }
+    h->needed_only = sd->needed_only != 0;
     if (ok && so > h->seeded_cap) {  // grow (the old block stays owned by the handle)
       h->seeded = (uint8_t*)atc_pool_alloc(ctx, std::max(so, (size_t)256));
       if (h->seeded) h->allocations.push_back(h->seeded);
@@ -512,27 +531,36 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
         std::memcpy(sb + o_dvs, sd->diff_val, (size_t)nd * 8);
         std::memcpy(sb + o_dps, sd->diff_pos, (size_t)nd * 4);
       }
+      std::memcpy(sb + o_need, need.data(), TP * 8);
       ok = atc_cuda_ok(ctx, cudaMemcpyAsync(h->seeded, sb, so, cudaMemcpyHostToDevice, st), "H2D seeds");
     }
     if (ok) {
       const TestsetView& v = h->view;
-      k_probe_regions<<<T, 320, 0, st>>>(T, nP, (const uint64_t*)(h->seeded + o_seeds),
+      // needed_only: one kernel generates the prefixes, applies the diffs and builds
+      // the dirty lists; else whole regions, then k_apply_diffs and k_build_dirty
+      const int64_t* dn = sd->needed_only ? (const int64_t*)(h->seeded + o_need) : nullptr;
+      k_probe_regions<<<T, 160, 0, st>>>(T, nP, (const uint64_t*)(h->seeded + o_seeds),
                                          (const uint64_t*)(h->seeded + o_skips), v.region_len, v.is_f32,
-                                         v.region_off, init, fin);
-      k_apply_diffs<<<(unsigned)TP, 256, 0, st>>>(nP, v.region_len, v.region_off,
-                                                  (const int64_t*)(h->seeded + o_doffs),
-                                                  (const int32_t*)(h->seeded + o_dps),
-                                                  (const double*)(h->seeded + o_dvs), fin);
+                                         v.region_off, dn, init, fin, v, (const int64_t*)(h->seeded + o_doffs),
+                                         (const int32_t*)(h->seeded + o_dps), (const double*)(h->seeded + o_dvs));
+      if (!dn)
+        k_apply_diffs<<<(unsigned)TP, 256, 0, st>>>(nP, v.region_len, v.region_off,
+                                                    (const int64_t*)(h->seeded + o_doffs),
+                                                    (const int32_t*)(h->seeded + o_dps),
+                                                    (const double*)(h->seeded + o_dvs), fin);
+      fused = dn != nullptr;
       ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_probe_regions");
     }
   }
   if (ok) {
-    int64_t maxlen = 0;
-    for (int p = 0; p < nP; ++p) maxlen = std::max<int64_t>(maxlen, h->lens[p]);
-    dim3 grid((unsigned)std::min<int64_t>((maxlen + 255) / 256, 64), (unsigned)(T * nP));
-    k_build_dirty<<<grid, 256, 0, st>>>(h->view, const_cast<int32_t*>(h->view.dirty_pos),
-                                        const_cast<int32_t*>(h->view.dirty_cnt),
-                                        const_cast<int32_t*>(h->view.dirty_max));
+    if (!fused) {
+      int64_t maxlen = 0;
+      for (int p = 0; p < nP; ++p) maxlen = std::max<int64_t>(maxlen, h->lens[p]);
+      dim3 grid((unsigned)std::min<int64_t>((maxlen + 255) / 256, 64), (unsigned)(T * nP));
+      k_build_dirty<<<grid, 256, 0, st>>>(h->view, const_cast<int32_t*>(h->view.dirty_pos),
+                                          const_cast<int32_t*>(h->view.dirty_cnt),
+                                          const_cast<int32_t*>(h->view.dirty_max));
+    }
     ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_build_dirty") &&
          (h->ready || atc_cuda_ok(ctx, cudaEventCreateWithFlags(&h->ready, cudaEventDisableTiming), "cudaEventCreate")) &&
          atc_cuda_ok(ctx, cudaEventRecord(h->ready, st), "cudaEventRecord") &&
@@ -685,6 +713,10 @@ int atc_testsets_download(atc_ctx* ctx, const atc_testset_handle* h, double* ini
   if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
   if (!h || (!init && !final_)) {
     atc_set_error(ctx, "bad arguments to atc_testsets_download");
+    return ATC_ERR_ARG;
+  }
+  if (h->needed_only) {
+    atc_set_error(ctx, "atc_testsets_download: the handle holds only the needed region prefixes");
     return ATC_ERR_ARG;
   }
   cudaSetDevice(ctx->device);

@@ -12,6 +12,8 @@
 
 #include <cstdint>
 
+#include "eval_common.cuh"
+
 namespace atc {
 
 namespace {
@@ -19,10 +21,6 @@ constexpr int kN = 312, kM = 156;
 constexpr uint64_t kMatrixA = 0xB5026F5AA96619E9ull;
 constexpr uint64_t kUpper = 0xFFFFFFFF80000000ull, kLower = 0x000000007FFFFFFFull;
 
-__device__ __forceinline__ uint64_t twist_word(uint64_t cur, uint64_t next, uint64_t mid) {
-  const uint64_t y = (cur & kUpper) | (next & kLower);
-  return mid ^ (y >> 1) ^ ((y & 1ull) ? kMatrixA : 0ull);
-}
 __device__ __forceinline__ uint64_t temper(uint64_t y) {
   y ^= (y >> 29) & 0x5555555555555555ull;
   y ^= (y << 17) & 0x71D67FFFEDA60000ull;
@@ -32,63 +30,103 @@ __device__ __forceinline__ uint64_t temper(uint64_t y) {
 }
 }  // namespace
 
-// One CTA (320 threads) per test t.  The twist runs in two parallel phases
-// (words [0, 156) read only old words; [156, 312) read the phase-1 results at
-// k - 156 and, for k = 311, the new word 0), then 312 outputs are tempered and
-// written to whichever region's stream window holds them.
-__global__ void __launch_bounds__(320) k_probe_regions(int T, int nP, const uint64_t* seeds, const uint64_t* skips,
+// One CTA per test t.  As a sequence, std::mt19937_64 is z[0..311] = the seeded
+// state and z[n + 312] = z[n + 156] ^ f(z[n], z[n + 1]) (f: the upper/lower-bit
+// merge, shift and matrix-A step of the twist), draw i = temper(z[312 + i]) — the
+// standard's twist computes exactly these words in place.  Step j computes the 156
+// words z[312 + 156j + q] (q < 156) at once from words of earlier steps, in a
+// 624-word ring (each step overwrites only words no later step reads), so one
+// barrier per 156 draws; steps whose draws fall in no region are not tempered.
+// need (optional, [T * nP]): generate only the first need[t * nP + p] elements of
+// region (t, p) — the steps stop at the last of them — and then, in the same CTA,
+// scatter test t's final-minus-init entries (k_apply_diffs) and build its dirty
+// lists over those prefixes (k_build_dirty), diff_* and v's dirty arrays.
+__global__ void __launch_bounds__(160) k_probe_regions(int T, int nP, const uint64_t* seeds, const uint64_t* skips,
                                                        const int64_t* region_len, const int32_t* is_f32,
-                                                       const int64_t* region_off, double* init, double* fin) {
-  __shared__ uint64_t mt[kN];
+                                                       const int64_t* region_off, const int64_t* need, double* init,
+                                                       double* fin, TestsetView v, const int64_t* diff_off,
+                                                       const int32_t* diff_pos, const double* diff_val) {
+  constexpr int kRing = 2 * kN;
+  __shared__ uint64_t z[kRing];
   const int t = blockIdx.x;
   if (t >= T) return;
-  const int k = threadIdx.x;
-  if (k == 0) {  // seeding: mt[i] = f * (mt[i-1] ^ (mt[i-1] >> 62)) + i
+  const int q = threadIdx.x;
+  if (q == 0) {  // seeding: mt[i] = f * (mt[i-1] ^ (mt[i-1] >> 62)) + i
     uint64_t x = seeds[t];
-    mt[0] = x;
+    z[0] = x;
     for (int i = 1; i < kN; ++i) {
       x = 6364136223846793005ull * (x ^ (x >> 62)) + (uint64_t)i;
-      mt[i] = x;
+      z[i] = x;
     }
   }
   uint64_t lo[8], hi[8];
   uint64_t end = 0;
-  for (int p = 0; p < nP && p < 8; ++p) {
+  const int np = nP < 8 ? nP : 8;
+  for (int p = 0; p < np; ++p) {
     lo[p] = skips[(size_t)t * nP + p];
-    hi[p] = lo[p] + (uint64_t)region_len[p];
+    hi[p] = lo[p] + (uint64_t)(need ? need[(size_t)t * nP + p] : region_len[p]);
     end = hi[p] > end ? hi[p] : end;
   }
   __syncthreads();
-  // each twist: phase 1 (read, sync, write, sync), phase 2 (read, sync, write,
-  // sync); the new word is tempered from the register it was just computed in
-  auto emit = [&](uint64_t base, uint64_t word) {
-    const uint64_t pos = base + (uint64_t)k;  // stream position of this output
-    const uint64_t y = temper(word);
-    for (int p = 0; p < nP && p < 8; ++p)
-      if (pos >= lo[p] && pos < hi[p]) {
-        const double u = (double)(y >> 11) * 0x1.0p-53;
-        double x = __dadd_rn(-1.0, __dmul_rn(u, 2.0));  // lo + u * (hi - lo), not contracted
-        if (is_f32[p]) x = (double)__double2float_rn(x);
-        const int64_t o = region_off[(size_t)t * nP + p] + (int64_t)(pos - lo[p]);
-        init[o] = x;
-        fin[o] = x;
-      }
-  };
-  for (uint64_t base = 0; base < end; base += kN) {
-    uint64_t v = 0;
-    if (k < kM) v = twist_word(mt[k], mt[k + 1], mt[k + kM]);
-    __syncthreads();
-    if (k < kM) mt[k] = v;
-    __syncthreads();
-    if (k < kM) emit(base, v);
+  auto wrap = [](int i) { return i >= kRing ? i - kRing : i; };  // i < 2 * kRing
+  int r = 0;  // base % kRing
+  for (uint64_t base = 0; base < end; base += kM, r = wrap(r + kM)) {  // step: draws [base, base + 156)
     uint64_t w = 0;
-    if (k >= kM && k < kN) w = twist_word(mt[k], mt[(k + 1) % kN], mt[k - kM]);
-    __syncthreads();
-    if (k >= kM && k < kN) {
-      mt[k] = w;
-      emit(base, w);
+    if (q < kM) {
+      const int n = r + q;  // z[n + 312] from z[n], z[n + 1], z[n + 156] (ring slots)
+      const uint64_t y = (z[wrap(n)] & kUpper) | (z[wrap(n + 1)] & kLower);
+      w = z[wrap(n + kM)] ^ (y >> 1) ^ ((y & 1ull) ? kMatrixA : 0ull);
+      // the slot of z[n + 312] held z[n - 312]: no read of this step or the next
+      z[wrap(n + kN)] = w;
     }
-    __syncthreads();
+    bool any = false;  // block-uniform: does this step's window meet a region?
+    for (int p = 0; p < np; ++p) any = any || (base < hi[p] && base + kM > lo[p]);
+    if (any && q < kM) {
+      const uint64_t pos = base + (uint64_t)q;
+      const uint64_t y = temper(w);
+      const double u = (double)(y >> 11) * 0x1.0p-53;
+      const double x0 = __dadd_rn(-1.0, __dmul_rn(u, 2.0));  // lo + u * (hi - lo), not contracted
+      for (int p = 0; p < np; ++p)
+        if (pos >= lo[p] && pos < hi[p]) {
+          const double x = is_f32[p] ? (double)__double2float_rn(x0) : x0;
+          const int64_t o = region_off[(size_t)t * nP + p] + (int64_t)(pos - lo[p]);
+          init[o] = x;
+          fin[o] = x;
+        }
+    }
+    __syncthreads();  // this step's words visible to the next step
+  }
+  if (!need) return;
+  for (int p = 0; p < nP; ++p) {  // final = init + the original run's writes
+    const size_t i = (size_t)t * nP + p;
+    double* f = fin + region_off[i];
+    for (int64_t e = diff_off[i] + q; e < diff_off[i + 1]; e += blockDim.x) {
+      const int32_t pos = diff_pos[e];
+      if (pos < region_len[p]) f[pos] = diff_val[e];
+    }
+  }
+  __syncthreads();
+  const int lane = q & 31;
+  for (int p = 0; p < nP; ++p) {  // dirty lists over the generated prefixes
+    const size_t i = (size_t)t * nP + p;
+    const int64_t len = need[i];
+    const bool f32 = is_f32[p] != 0;
+    const double* a = init + region_off[i];
+    const double* f = fin + region_off[i];
+    int32_t* out = const_cast<int32_t*>(v.dirty_pos) + v.dirty_off[i];
+    for (int64_t b = 0; b < len; b += blockDim.x) {
+      const int64_t e = b + q;
+      const bool dirty = e < len && mismatch(a[e], f[e], f32);
+      const unsigned ball = __ballot_sync(0xffffffffu, dirty);
+      if (ball == 0) continue;
+      int slot = 0;
+      if (lane == 0) slot = atomicAdd(const_cast<int32_t*>(v.dirty_cnt) + i, __popc(ball));
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      if (dirty) {
+        out[slot + __popc(ball & ((1u << lane) - 1))] = (int32_t)e;
+        atomicMax(const_cast<int32_t*>(v.dirty_max) + i, (int32_t)e);
+      }
+    }
   }
 }
 

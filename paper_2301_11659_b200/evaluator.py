@@ -66,9 +66,11 @@ class RecordedTestsets:
                                 seeds=None if self.seeds is None else self.seeds[:T].copy(),
                                 skips=None if self.skips is None else self.skips[:T].copy())
 
-    def seeded_struct(self):
+    def seeded_struct(self, needed_only: bool = False):
         """atc_seeded_testsets: seeds + stream positions + the final-minus-init
-        entries (positions where the original run's final image differs)."""
+        entries (positions where the original run's final image differs).
+        needed_only: the device generates only the region prefixes an evaluation
+        can read (include/atc_b200.h)."""
         if self.seeds is None or self.skips is None:
             raise ValueError("these test sets carry no stream seeds")
         ptrs = self.ptrs
@@ -103,11 +105,12 @@ class RecordedTestsets:
         s.diff_off = doff.ctypes.data
         s.diff_pos = dpos.ctypes.data
         s.diff_val = dval.ctypes.data
+        s.needed_only = 1 if needed_only else 0
         return s, [ints, is_f32, lens, ok, seeds, skips, doff, dpos, dval]
 
-    def upload_seeded(self, ctx: "_lib.Context"):
+    def upload_seeded(self, ctx: "_lib.Context", needed_only: bool = False):
         """atc_testsets_upload_seeded: regions generated on the GPU from the seeds."""
-        s, keep = self.seeded_struct()
+        s, keep = self.seeded_struct(needed_only)
         out = C.c_void_p()
         _lib.check(ctx.handle, _lib.lib().atc_testsets_upload_seeded(ctx.handle, C.byref(s), C.byref(out)))
         h = _TestsetHandle(ctx, out.value)

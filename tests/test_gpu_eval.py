@@ -378,3 +378,35 @@ def test_seeded_update_in_place_with_prepared_sweep(ev):
                 assert ng == nw and hg.tolist() == hw.tolist()
     sweep.close()
     holder._handles.clear()
+
+
+@pytest.mark.parametrize("stem", ["conv_direct", "im2col_virtual", "naive_ld", "strassen_staged", "naive_f32"])
+def test_seeded_needed_only_regions(ev, stem):
+    """needed_only seeded handles (only the region prefixes an evaluation can read
+    are generated) give the same verdicts as whole regions: full spaces (or their
+    first 2^22 bindings) and an explicit list with every reason code; downloading
+    such a handle is refused."""
+    import ctypes as C
+
+    p = fixtures.load(stem)
+    ts = p.testsets(16)
+    h = ts.upload_seeded(ev.ctx, needed_only=True)
+    holder = p.testsets(16)
+    holder._handles[id(ev.ctx)] = h
+    for sname in p.spec_names():
+        space, spec = p.space(sname), fixtures.spec(sname)
+        end = min(space.count, 1 << 22)
+        want = ev.eval_enumerated(spec, ts, space, 0, end)
+        got = ev.eval_enumerated(spec, holder, space, 0, end)
+        np.testing.assert_array_equal(got[0], want[0])
+        assert got[1] == want[1] and got[2].tolist() == want[2].tolist()
+        idx = np.arange(0, end, max(1, end // 4096), dtype=np.uint64)
+        am, sm = space.decode(idx)
+        a, b = ev.eval_bindings(spec, ts, am, sm), ev.eval_bindings(spec, holder, am, sm)
+        np.testing.assert_array_equal(a.fail_t, b.fail_t)
+        np.testing.assert_array_equal(a.reason, b.reason)
+    buf = np.empty(ts.n_tests * sum(len(ts.init[0][q]) for q in range(len(ts.ptrs))))
+    with pytest.raises(L.AtcError, match="prefixes"):
+        L.check(ev.ctx.handle, L.lib().atc_testsets_download(ev.ctx.handle, C.c_void_p(h.value), buf.ctypes.data,
+                                                             None))
+    holder._handles.clear()
