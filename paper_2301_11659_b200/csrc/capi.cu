@@ -1344,8 +1344,15 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
   unsigned long long* hist = reinterpret_cast<unsigned long long*>(b->res + (size_t)b->n * kBatchStride);
   cudaMemsetAsync(b->res, 0, batch_res_words(b->n) * 8, st);
   int n_side = 0;
-  for (int j = 0; j < b->n; ++j) n_side += b->batched[j] && b->plans[j].sp.sem != ATC_SEM_CONV2D;
-  const bool split = n_side > 1 || (n_side == 1 && n_side < b->n);
+  // jobs with an empty range (a multi-GPU rank's share of nothing) take no stream,
+  // event wait or graph node at all
+  auto active = [&](int j) { return b->batched[j] && b->jobs[j].end > b->jobs[j].begin; };
+  int n_active = 0;
+  for (int j = 0; j < b->n; ++j) {
+    n_active += active(j);
+    n_side += active(j) && b->plans[j].sp.sem != ATC_SEM_CONV2D;
+  }
+  const bool split = n_side > 1 || (n_side == 1 && n_side < n_active);
   if (split) {
     cudaEventRecord(ctx->fork_ev, st);
     for (int k = 0; k < atc_ctx::kSideStreams; ++k) cudaStreamWaitEvent(ctx->side_stream[k], ctx->fork_ev, 0);
@@ -1353,7 +1360,7 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
   int side_next = 0, conv_next = 0;
   int rc = ATC_OK;
   for (int j = 0; j < b->n && rc == ATC_OK; ++j) {
-    if (!b->batched[j]) continue;
+    if (!active(j)) continue;
     atc_enum_job& job = b->jobs[j];
     EnumPlan& e = b->plans[j];
     // conv spaces on the caller's stream and side stream 0 alternately when they
@@ -1387,7 +1394,6 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
       ts_wait(job.ts, js);
     else if (job.ts->ready)
       cudaStreamWaitEvent(js, job.ts->ready, cudaEventWaitExternal);
-    if (job.end <= job.begin) continue;  // nothing of this space on this rank
     rc = enqueue_tables(ctx, e, job.ts, job.perms, job.n_perms, &b->d_perms[j], js, job.begin, job.end);
     if (rc) break;
     if (job.end > job.begin) {

@@ -104,19 +104,60 @@ def shard(count: int, rank: int, world: int) -> tuple:
     return count * rank // world, count * (rank + 1) // world
 
 
-BIG_SPACE = 1 << 24  # spaces at least this large are block-partitioned across ranks
+BIG_SPACE = 1 << 24  # spaces at least this large are split by the cost model below
+
+# Per-space cost model of a large (conv) space on one B200, from the measured chain
+# (tools/prof_sweep.py, tools/one_conv_space.py): a fixed part (position tables, K2,
+# finalize: ~0.14 ms) plus the K1 screen (~0.19 ms per 2.32e9 bindings).
+SPACE_FIXED_MS = 0.14
+SPACE_MS_PER_BINDING = 0.19 / 2324522934
+
+
+def space_cost_ms(n: int) -> float:
+    return SPACE_FIXED_MS + n * SPACE_MS_PER_BINDING if n > 0 else 0.0
 
 
 def plan_shards(jobs: list, rank: int, world: int) -> list:
-    """This rank's [begin, end) of every job.  Large spaces are block-partitioned
-    across all ranks (their screens dominate); small spaces — chains of a few
-    latency-bound kernels — go whole to one rank each, dealt round-robin, so every
-    rank runs ~1/world of them instead of a sliver of each.  Ranks without a space
-    get an empty range (and contribute nothing to its reduction)."""
+    """This rank's [begin, end) of every job.
+
+    Large spaces are balanced with the cost model, largest first: the target per
+    rank is their total cost / world; a space goes whole to the least-loaded rank
+    if that stays within the target (+15%), else it is cut into the fewest k ~equal
+    contiguous pieces (k <= world, one per least-loaded rank) that do, else into the
+    k with the lowest resulting maximum — a rank pays the fixed part of every piece
+    it takes, so a space is split only when that buys balance.  Small spaces — chains of a few latency-bound kernels — go whole to one
+    rank each, dealt round-robin.  Ranks without a piece of a space get an empty
+    range (and contribute nothing to its reduction).  Deterministic: every rank
+    computes the same plan."""
+    if world == 1:
+        return [(0, j.count) for j in jobs]
+    big = [i for i, j in enumerate(jobs) if j.count >= BIG_SPACE]
+    target = sum(space_cost_ms(jobs[i].count) for i in big) / world
+    load = [0.0] * world
+    pieces = {}
+    for i in sorted(big, key=lambda i: (-jobs[i].count, i)):
+        n = jobs[i].count
+        order = sorted(range(world), key=lambda r: (load[r], r))
+        # the fewest pieces that keep every receiving rank within the target (+15%),
+        # else the piece count with the lowest resulting maximum
+        fits, best = None, None
+        for k in range(1, world + 1):
+            peak = load[order[k - 1]] + space_cost_ms(-(-n // k))
+            if fits is None and peak <= 1.15 * target:
+                fits = k
+            if best is None or peak < best[0] - 1e-12:
+                best = (peak, k)
+        k = fits or best[1]
+        ranks = sorted(order[:k])
+        pieces[i] = {}
+        for idx, r in enumerate(ranks):
+            b, e = shard(n, idx, k)
+            pieces[i][r] = (b, e)
+            load[r] += space_cost_ms(e - b)
     out, k = [], 0
-    for j in jobs:
-        if world == 1 or j.count >= BIG_SPACE:
-            out.append(shard(j.count, rank, world))
+    for i, j in enumerate(jobs):
+        if i in pieces:
+            out.append(pieces[i].get(rank, (0, 0)))
         else:
             out.append((0, j.count) if k % world == rank else (0, 0))
             k += 1

@@ -79,8 +79,9 @@ def test_block_range_partition():
 
 def test_plan_shards_cover_every_space_once():
     """workloads.plan_shards: across ranks every binding of every corpus space is
-    assigned exactly once; large spaces are split over all ranks, small spaces go
-    whole to one rank and are dealt evenly."""
+    assigned exactly once in contiguous pieces; small spaces go whole to one rank
+    and are dealt evenly; the large spaces' modelled cost is balanced (no rank above
+    the per-rank target by more than one space's fixed part plus one piece)."""
     from paper_2301_11659_b200 import workloads
 
     jobs = workloads.corpus_jobs()
@@ -91,11 +92,16 @@ def test_plan_shards_cover_every_space_once():
             covered = sum(e - b for b, e in rs)
             assert covered == j.count, (j.stem, world)
             nonempty = [(b, e) for b, e in rs if e > b]
-            assert all(a[1] == c[0] for a, c in zip(nonempty, nonempty[1:]))
-            if j.count >= workloads.BIG_SPACE:
-                assert len(nonempty) == min(world, j.count)
-            else:
+            assert nonempty[0][0] == 0 and all(a[1] == c[0] for a, c in zip(nonempty, nonempty[1:]))
+            if j.count < workloads.BIG_SPACE:
                 assert len(nonempty) == 1
+        big = [i for i, j in enumerate(jobs) if j.count >= workloads.BIG_SPACE]
+        loads = [sum(workloads.space_cost_ms(plans[r][i][1] - plans[r][i][0]) for i in big) for r in range(world)]
+        target = sum(workloads.space_cost_ms(jobs[i].count) for i in big) / world
+        biggest = max(workloads.space_cost_ms(jobs[i].count) for i in big)
+        assert max(loads) <= target + biggest, (world, loads)
+        if world > 1:
+            assert max(loads) < sum(loads) / 2 or world == 2
         small = [sum(1 for i, j in enumerate(jobs) if j.count < workloads.BIG_SPACE and plans[r][i][1] > 0)
                  for r in range(world)]
         assert max(small) - min(small) <= 1

@@ -1,4 +1,4 @@
-"""Corpus sweep split by class: conv-only and gemm-only sweeps timed alone (CUDA
+"""Corpus sweep split by class (--fp32: ATC_MODE_FP32_SCREEN): conv-only and gemm-only sweeps timed alone (CUDA
 events, graph replay), then one conv-only sweep per job for the per-space cost.
 Under ncu (`--metrics gpu__time_duration.sum`) the last eager run of each sweep
 gives the per-kernel launch list."""
@@ -19,8 +19,11 @@ ev = Evaluator(ctx)
 jobs = workloads.corpus_jobs()
 
 
+MODE = _lib.MODE_FP32_SCREEN if "--fp32" in sys.argv else _lib.MODE_FP64
+
+
 def timed(items, reps=5):
-    sw = ev.sweep(items)
+    sw = ev.sweep(items, mode=MODE)
     for _ in range(3):
         sw.run()
     torch.cuda.synchronize()
