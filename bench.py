@@ -422,9 +422,12 @@ def _e2e_prepared(args, ctx, ev, jobs, shards, stream, torch, dist, want):
     sweep = ev.sweep([(j.spec, progs[j.stem][3], j.space, b, e) for _, j, (b, e) in active], cap=1 << 16)
     d2h = len(active) * (2 + 4096 + 8) * 8  # the batch's result block (atc_enum_batch_run)
 
-    def one():
-        for s, _, h, _ in progs.values():
-            _lib.check(ctx.handle, L.atc_testsets_update_seeded(ctx.handle, C.c_void_p(h.value), C.byref(s)))
+    vals = list(progs.values())
+    structs = (_lib.SeededTestsets * len(vals))(*[v[0] for v in vals])
+    hptrs = (C.c_void_p * len(vals))(*[v[2].value for v in vals])
+
+    def one():  # one C call rewrites every program's handle, then the graph replay
+        _lib.check(ctx.handle, L.atc_testsets_update_seeded_many(ctx.handle, hptrs, structs, len(vals)))
         return sweep.run()
 
     for _ in range(2):  # eager + capture

@@ -186,6 +186,10 @@ int atc_testsets_upload_seeded(atc_ctx* ctx, const atc_seeded_testsets* ts, atc_
  * already queued on the context's stream: prepared batches (atc_enum_batch_*)
  * over the handle stay valid and pick the new contents up on their next run. */
 int atc_testsets_update_seeded(atc_ctx* ctx, atc_testset_handle* h, const atc_seeded_testsets* ts);
+/* The same for n handles at once (handles[i] gets ts[i]); one ordering event for
+ * all of them. */
+int atc_testsets_update_seeded_many(atc_ctx* ctx, atc_testset_handle* const* handles,
+                                    const atc_seeded_testsets* ts, int32_t n);
 
 /* Copies a handle's regions back ((t, pointer) regions back to back, unpadded;
  * either pointer may be NULL) — for checks and debugging. */

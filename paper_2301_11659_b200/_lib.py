@@ -137,6 +137,7 @@ _SIGS = [
     ("atc_testsets_upload_async", C.c_int, [_P, C.POINTER(Testsets), C.POINTER(_P)]),
     ("atc_testsets_upload_seeded", C.c_int, [_P, C.POINTER(SeededTestsets), C.POINTER(_P)]),
     ("atc_testsets_update_seeded", C.c_int, [_P, _P, C.POINTER(SeededTestsets)]),
+    ("atc_testsets_update_seeded_many", C.c_int, [_P, _P, C.POINTER(SeededTestsets), C.c_int32]),
     ("atc_testsets_download", C.c_int, [_P, _P, _P, _P]),
     ("atc_eval_bindings", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, C.c_int64, C.c_int32, _P, _P,
                                     C.POINTER(C.c_int64)]),

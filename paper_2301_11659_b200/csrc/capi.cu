@@ -82,7 +82,6 @@ struct atc_testset_handle {
          o_dmax = 0;
   uint8_t* seeded = nullptr;    // seeds, stream positions, final-minus-init entries
   size_t seeded_cap = 0;
-  cudaEvent_t reuse = nullptr;  // readers of the previous contents are done (compute stream)
   bool needed_only = false;     // seeded with needed_only: region prefixes only
   uint8_t* pin = nullptr;       // pinned staging of the metadata + seeded blocks (async DMA)
   size_t pin_bytes = 0;
@@ -306,6 +305,7 @@ void atc_destroy(atc_ctx* ctx) {
     for (auto& cs : ctx->copy_stream)
       if (cs) cudaStreamDestroy(cs);
     if (ctx->free_ev) cudaEventDestroy(ctx->free_ev);
+    if (ctx->update_ev) cudaEventDestroy(ctx->update_ev);
     for (int k = 0; k < atc_ctx::kSideStreams; ++k) {
       if (ctx->side_stream[k]) cudaStreamDestroy(ctx->side_stream[k]);
       if (ctx->join_ev[k]) cudaEventDestroy(ctx->join_ev[k]);
@@ -374,7 +374,8 @@ int atc_profile_read(atc_ctx* ctx, atc_profile* out) {
 // final-minus-init entries (`sd`, regions generated on the device), on the
 // handle's copy stream, and records its ready event.
 static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets* ts_full,
-                         const atc_seeded_testsets* sd, bool sync, bool pinned_staging = false) {
+                         const atc_seeded_testsets* sd, bool sync, bool pinned_staging = false,
+                         cudaEvent_t reuse = nullptr) {
   const int T = h->T, nI = h->nI, nP = h->nP;
   const size_t TP = (size_t)T * nP;
   const int64_t* int_values = ts_full ? ts_full->int_values : sd->int_values;
@@ -430,7 +431,7 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
     cudaStreamWaitEvent(st, ctx->free_ev, 0);
     ctx->free_pending &= ~(1ull << h->cs);
   }
-  if (h->reuse) cudaStreamWaitEvent(st, h->reuse, 0);  // in-place update: earlier readers first
+  if (reuse) cudaStreamWaitEvent(st, reuse, 0);  // in-place update: earlier readers first
   bool ok = atc_cuda_ok(ctx, cudaMemcpyAsync(h->meta, meta, h->meta_bytes, cudaMemcpyHostToDevice, st),
                         "H2D metadata");
   double* init = const_cast<double*>(h->view.init);
@@ -687,26 +688,48 @@ int atc_testsets_upload_seeded(atc_ctx* ctx, const atc_seeded_testsets* ts, atc_
   return testsets_upload(ctx, nullptr, ts, out, false);
 }
 
-int atc_testsets_update_seeded(atc_ctx* ctx, atc_testset_handle* h, const atc_seeded_testsets* ts) {
-  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+static bool update_matches(atc_ctx* ctx, const atc_testset_handle* h, const atc_seeded_testsets* ts) {
   if (!h || !ts || ts->n_tests != h->T || ts->n_ints != h->nI || ts->n_ptrs != h->nP || !ts->int_values ||
       !ts->region_len || !ts->ptr_is_f32 || !ts->stream_seed || !ts->stream_skip || !ts->diff_off ||
       ts->diff_off[0] != 0) {
     atc_set_error(ctx, "atc_testsets_update_seeded: test sets do not match the handle");
-    return ATC_ERR_ARG;
+    return false;
   }
   for (int p = 0; p < h->nP; ++p)
     if (ts->region_len[p] != h->lens[p] || (ts->ptr_is_f32[p] != 0) != (h->is_f32[p] != 0)) {
       atc_set_error(ctx, "atc_testsets_update_seeded: pointer %d differs from the handle's", p);
-      return ATC_ERR_ARG;
+      return false;
     }
+  return true;
+}
+
+int atc_testsets_update_seeded(atc_ctx* ctx, atc_testset_handle* h, const atc_seeded_testsets* ts) {
+  return atc_testsets_update_seeded_many(ctx, &h, ts, 1);
+}
+
+int atc_testsets_update_seeded_many(atc_ctx* ctx, atc_testset_handle* const* handles, const atc_seeded_testsets* ts,
+                                    int32_t n) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (n < 0 || (n > 0 && (!handles || !ts))) {
+    atc_set_error(ctx, "bad arguments to atc_testsets_update_seeded_many");
+    return ATC_ERR_ARG;
+  }
+  for (int i = 0; i < n; ++i)
+    if (!update_matches(ctx, handles[i], ts + i)) return ATC_ERR_ARG;
+  if (n == 0) return ATC_OK;
   cudaSetDevice(ctx->device);
   // the new contents are written after everything queued so far on the compute
-  // stream (evaluations of every sweep branch join it) has read the old ones
-  if (!h->reuse && !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&h->reuse, cudaEventDisableTiming), "cudaEventCreate"))
+  // stream (evaluations of every sweep branch join it) has read the old ones: one
+  // event for the whole set of updates
+  if (!ctx->update_ev &&
+      !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->update_ev, cudaEventDisableTiming), "cudaEventCreate"))
     return ATC_ERR_CUDA;
-  if (!atc_cuda_ok(ctx, cudaEventRecord(h->reuse, ctx->stream), "cudaEventRecord")) return ATC_ERR_CUDA;
-  return testsets_fill(ctx, h, nullptr, ts, false, true);
+  if (!atc_cuda_ok(ctx, cudaEventRecord(ctx->update_ev, ctx->stream), "cudaEventRecord")) return ATC_ERR_CUDA;
+  for (int i = 0; i < n; ++i) {
+    const int rc = testsets_fill(ctx, handles[i], nullptr, ts + i, false, true, ctx->update_ev);
+    if (rc) return rc;
+  }
+  return ATC_OK;
 }
 
 int atc_testsets_download(atc_ctx* ctx, const atc_testset_handle* h, double* init, double* final_) {
@@ -751,7 +774,6 @@ int atc_testsets_free(atc_ctx* ctx, atc_testset_handle* h) {
     cudaEventSynchronize(h->ready);  // the staging buffer may still be read by its DMA
     cudaEventDestroy(h->ready);
   }
-  if (h->reuse) cudaEventDestroy(h->reuse);
   if (h->pin) cudaFreeHost(h->pin);
   for (void* p : h->allocations) {
     if (ctx && !ctx->broken)

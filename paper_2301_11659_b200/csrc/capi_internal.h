@@ -36,6 +36,7 @@ struct atc_ctx {
   cudaStream_t copy_stream[kCopyStreams] = {};
   int copy_next = 0;
   cudaEvent_t free_ev = nullptr;
+  cudaEvent_t update_ev = nullptr;  // in-place updates wait for earlier readers (compute stream)
   uint64_t free_pending = 0;  // copy streams that have not waited on the latest free (bit per stream)
   int mode = 0;  // ATC_MODE_* of the evaluation in flight
   // instrumentation (atc_profile_*)

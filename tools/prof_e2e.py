@@ -37,9 +37,13 @@ for j in jobs:
 sweep = ev.sweep([(j.spec, progs[j.stem][3], j.space, 0, j.space.count) for j in jobs])
 
 
+vals = list(progs.values())
+structs = (_lib.SeededTestsets * len(vals))(*[v[0] for v in vals])
+hptrs = (C.c_void_p * len(vals))(*[v[2].value for v in vals])
+
+
 def updates():
-    for s, _, h, _ in progs.values():
-        _lib.check(ctx.handle, L.atc_testsets_update_seeded(ctx.handle, C.c_void_p(h.value), C.byref(s)))
+    _lib.check(ctx.handle, L.atc_testsets_update_seeded_many(ctx.handle, hptrs, structs, len(vals)))
 
 
 def timed(fn, reps=5):
