@@ -512,7 +512,7 @@ __device__ __forceinline__ int div_capn(uint32_t a, uint32_t b, float rb, int ca
 
 // lut_n > 0: products are in [.., lut_n - 1] and the dynamic shared memory holds a
 // rank table (count of pair products <= T, T in [0, lut_n)) after the row table
-__global__ void __launch_bounds__(256) k_screen_conv_pairs(TestsetView ts, const uint8_t* perms, uint64_t size_maps,
+__global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, const uint8_t* perms, uint64_t size_maps,
                                                             uint64_t begin, uint64_t end, RowPlan plan,
                                                             uint64_t* surv, uint64_t surv_cap,
                                                             unsigned long long* surv_cnt,
