@@ -184,14 +184,14 @@ struct Maps {
   CUtensorMap c;     // output [rows][cols] fp32, 32x32 boxes, 128B swizzle (p.tma_store)
 };
 
-__device__ __forceinline__ void tile_coords(const Problem& p, int tile, int& tm, int& tn, int& ti) {
-  // grouped raster: 16 m-tiles x all n-tiles per group, for L2 reuse of A/B panels.
+__device__ __forceinline__ void tile_coords(const Problem& p, int tile, int& tm, int& tn, int& ti, int G = 0) {
+  // grouped raster: G m-tiles x all n-tiles per group, for L2 reuse of A/B panels.
   // With p.pair the unit is an M-tile pair: the caller maps tm -> 2*tm + rank.
   const int tiles_m = p.pair ? (p.tiles_m + 1) / 2 : p.tiles_m;
   const int per_img = tiles_m * p.tiles_n;
   ti = tile / per_img;
   int t = tile - ti * per_img;
-  const int G = p.pair ? 8 : 16;
+  if (G == 0) G = p.pair ? 8 : 16;
   const int group = t / (G * p.tiles_n);
   const int first_m = group * G;
   const int gm = min(G, tiles_m - first_m);
@@ -614,6 +614,10 @@ __host__ __device__ constexpr uint32_t idesc_tf32_m256(uint32_t b_mn_major) {  /
          ((uint32_t)(256 >> 4) << 24);
 }
 
+// 256-row units: 8 per raster group (~sqrt of the units in flight: the fewest
+// distinct A + B panels per wave)
+constexpr int kGroup2 = 8;
+
 __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_constant__ Maps maps, const Problem p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -666,7 +670,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
           Problem q = p;
           q.tiles_m = tiles_m2;
           q.pair = 0;
-          tile_coords(q, unit, tm2, tn, ti);
+          tile_coords(q, unit, tm2, tn, ti, kGroup2);
         }
         const int tm = 2 * tm2 + (int)rank;  // this CTA's 128 rows
         for (int kb = 0; kb < total_kb; ++kb) {
@@ -758,7 +762,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
         Problem q2 = p;
         q2.tiles_m = tiles_m2;
         q2.pair = 0;
-        tile_coords(q2, unit, tm2, tn, ti);
+        tile_coords(q2, unit, tm2, tn, ti, kGroup2);
       }
       const int tm = 2 * tm2 + (int)rank;
       mbar_wait(&tmem_full[acc], acc_phase);
