@@ -50,7 +50,7 @@ __global__ void k_confirm_warp(TestsetView ts, SpecView sp, BindingSource src, c
                                const unsigned long long* sel_cnt, int mode);
 __global__ void k_confirm_pre(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                               const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
-                              uint32_t* pend, unsigned long long* pend_cnt, int mode);
+                              uint32_t* pend, unsigned long long* pend_cnt, int mode, int screened);
 __global__ void k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                              const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
                              const uint32_t* pend, const unsigned long long* pend_cnt, uint32_t* next,
@@ -949,7 +949,7 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
   if (pre)
     k_confirm_pre<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 255) / 256, ctx->sm_count * 8)),
                     256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pend, next_cnt + 1,
-                                  ctx->mode);
+                                  ctx->mode, plan && plan->cmask && src.enumerated ? 1 : 0);
   if (pre && !keys) {
     // enumerated ranges report reasons, not failing tests: t >= 1 first over every
     // pending survivor, then t = 0 only where it can change the reason (k_confirm_t0)
