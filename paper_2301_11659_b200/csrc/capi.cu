@@ -285,6 +285,13 @@ atc_ctx* atc_create(int device) {
   for (auto& cs : ctx->copy_stream)
     if (!ctx->broken && !atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate"))
       ctx->broken = true;
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (!ctx->broken &&
+      (!atc_cuda_ok(ctx, cudaStreamCreateWithPriority(&ctx->conv_stream, cudaStreamNonBlocking, prio_hi),
+                    "cudaStreamCreate") ||
+       !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->conv_join_ev, cudaEventDisableTiming), "cudaEventCreate")))
+    ctx->broken = true;
   ctx->own_stream = ctx->stream;
   return ctx;
 }
@@ -310,6 +317,8 @@ void atc_destroy(atc_ctx* ctx) {
       if (ctx->side_stream[k]) cudaStreamDestroy(ctx->side_stream[k]);
       if (ctx->join_ev[k]) cudaEventDestroy(ctx->join_ev[k]);
     }
+    if (ctx->conv_stream) cudaStreamDestroy(ctx->conv_stream);
+    if (ctx->conv_join_ev) cudaEventDestroy(ctx->conv_join_ev);
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   }
   delete ctx;
@@ -1378,6 +1387,7 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
   if (split) {
     cudaEventRecord(ctx->fork_ev, st);
     for (int k = 0; k < atc_ctx::kSideStreams; ++k) cudaStreamWaitEvent(ctx->side_stream[k], ctx->fork_ev, 0);
+    cudaStreamWaitEvent(ctx->conv_stream, ctx->fork_ev, 0);
   }
   int side_next = 0, conv_next = 0;
   int rc = ATC_OK;
@@ -1399,7 +1409,7 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
       side_next = (side_next + 1) % atc_ctx::kSideStreams;
     }
     const bool side = sk >= 0;
-    cudaStream_t js = side ? ctx->side_stream[sk] : st;
+    cudaStream_t js = side ? ctx->side_stream[sk] : split ? ctx->conv_stream : st;
     ctx->slot_base = side ? 32 * (sk + 1) : 0;
     uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
     int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, chunk_cap * 4);
@@ -1429,11 +1439,14 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
     }
   }
   ctx->slot_base = 0;
-  if (split)
+  if (split) {
     for (int k = 0; k < atc_ctx::kSideStreams; ++k) {
       cudaEventRecord(ctx->join_ev[k], ctx->side_stream[k]);
       cudaStreamWaitEvent(st, ctx->join_ev[k], 0);
     }
+    cudaEventRecord(ctx->conv_join_ev, ctx->conv_stream);
+    cudaStreamWaitEvent(st, ctx->conv_join_ev, 0);
+  }
   if (rc) return rc;
   if (!atc_cuda_ok(ctx, cudaMemcpyAsync(b->h_res, b->res, batch_res_words(b->n) * 8, cudaMemcpyDeviceToHost, st),
                    "D2H results"))

@@ -24,6 +24,10 @@ struct atc_ctx {
   int slot_base = 0;
   cudaStream_t side_stream[kSideStreams] = {};
   cudaEvent_t fork_ev = nullptr, join_ev[kSideStreams] = {};
+  // conv spaces of a split batch (the critical path) run on a highest-priority
+  // stream, so their CTAs are dispatched ahead of the gemm branches'
+  cudaStream_t conv_stream = nullptr;
+  cudaEvent_t conv_join_ev = nullptr;
   void* scratch[kSlots] = {};
   size_t scratch_bytes[kSlots] = {};
   void* pinned[4] = {};
