@@ -951,9 +951,12 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
   // grids bounded by the most work there can be (survivors <= bindings screened):
   // small spaces launch a few CTAs instead of 8 per SM
   const uint64_t max_surv = std::min<uint64_t>(n, surv_cap);
-  const unsigned g_t0 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 7) / 8, ctx->sm_count * 8));
+  // gemm spaces keep few survivors (grid-stride loops cover them): a small cap keeps
+  // their mostly-empty K2 grids from taking SM slots from the concurrent conv chain
+  const uint64_t k2_cap = sp.sem == ATC_SEM_GEMM ? 64 : (uint64_t)ctx->sm_count * 8;
+  const unsigned g_t0 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 7) / 8, k2_cap));
   const unsigned g_t1 = (unsigned)std::max<uint64_t>(
-      1, std::min<uint64_t>((max_surv * (uint64_t)std::max(ts->T - 1, 0) + 7) / 8, ctx->sm_count * 8));
+      1, std::min<uint64_t>((max_surv * (uint64_t)std::max(ts->T - 1, 0) + 7) / 8, k2_cap));
   const bool pre = sp.sem == ATC_SEM_CONV2D;
   if (pre)
     k_confirm_pre<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 255) / 256, ctx->sm_count * 8)),
