@@ -420,7 +420,7 @@ def _e2e_prepared(args, ctx, ev, jobs, shards, stream, torch, dist, want):
         progs[j.stem] = (s, keep, h, holder)
         h2d += sum(a.nbytes for a in keep)
     sweep = ev.sweep([(j.spec, progs[j.stem][3], j.space, b, e) for _, j, (b, e) in active], cap=1 << 16)
-    d2h = len(active) * (2 + 4096 + 8) * 8  # the batch's result block (atc_enum_batch_run)
+    d2h = len(active) * (2 + 256 + 8) * 8  # the batch's result block (atc_enum_batch_run)
 
     vals = list(progs.values())
     structs = (_lib.SeededTestsets * len(vals))(*[v[0] for v in vals])

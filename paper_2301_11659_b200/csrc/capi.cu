@@ -1365,7 +1365,11 @@ struct atc_enum_batch {
 
 namespace {
 
-constexpr uint64_t kBatchStride = 2 + kResultPrefix;  // count, passing count, passing prefix
+// per job of a batch: count, passing count, passing prefix (a job with more passing
+// bindings than the prefix is redone alone by atc_eval_enumerated); small, because
+// the whole block comes back every run
+constexpr uint64_t kBatchPrefix = 256;
+constexpr uint64_t kBatchStride = 2 + kBatchPrefix;
 
 size_t batch_res_words(int n) { return (size_t)n * (kBatchStride + 8); }
 
@@ -1437,7 +1441,7 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
                     hist + 8 * j, js, e.use_table ? &e.pt : nullptr, e.use_rows ? &e.plan : nullptr);
       if (rc) break;
       k_finalize<<<64, 256, 0, js>>>(surv, cnt, chunk_cap, skeys, job.begin, b->res + (size_t)j * kBatchStride,
-                                     kResultPrefix, hist + 8 * j);
+                                     kBatchPrefix, hist + 8 * j);
       if (ctx->prof) ctx->prof_kernels += 1;
     }
   }
@@ -1607,7 +1611,7 @@ int atc_enum_batch_run(atc_ctx* ctx, atc_enum_batch* b) {
     if (job.status != ATC_OK) continue;
     const uint64_t* rj = b->h_res + (size_t)j * kBatchStride;
     const uint64_t c = rj[0], npass = rj[1];
-    if (!b->batched[j] || c > kEnumChunkCap || npass > kResultPrefix) {
+    if (!b->batched[j] || c > kEnumChunkCap || npass > kBatchPrefix) {
       // overflow (or a very large range): the single-space path with its own chunking
       job.status = atc_eval_enumerated(ctx, job.spec, job.ts, job.perms, job.n_perms, job.begin, job.end, b->mode,
                                        job.survivors, job.cap, &job.n_survivors, job.reason_counts);
