@@ -7,6 +7,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -734,11 +736,50 @@ int atc_testsets_update_seeded_many(atc_ctx* ctx, atc_testset_handle* const* han
       !atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->update_ev, cudaEventDisableTiming), "cudaEventCreate"))
     return ATC_ERR_CUDA;
   if (!atc_cuda_ok(ctx, cudaEventRecord(ctx->update_ev, ctx->stream), "cudaEventRecord")) return ATC_ERR_CUDA;
-  for (int i = 0; i < n; ++i) {
-    const int rc = testsets_fill(ctx, handles[i], nullptr, ts + i, false, true, ctx->update_ev);
-    if (rc) return rc;
+  // shared context state first, serially: pool growth of the seeded blocks and the
+  // copy streams' waits on earlier frees; then the per-handle work (staging, H2D,
+  // generator launch) on up to four host threads when the handles are distinct
+  bool distinct = true;
+  for (int i = 0; i < n && distinct; ++i) {
+    atc_testset_handle* h = handles[i];
+    for (int k = 0; k < i; ++k) distinct = distinct && handles[k] != h;
+    const size_t TP = (size_t)h->T * h->nP;
+    const int64_t nd = ts[i].diff_off[TP];
+    const size_t so = ((size_t)h->T * 8 + 15) / 16 * 16 + (TP * 8 + 15) / 16 * 16 + ((TP + 1) * 8 + 15) / 16 * 16 +
+                      ((size_t)nd * 8 + 15) / 16 * 16 + ((size_t)nd * 4 + 15) / 16 * 16 + (TP * 8 + 15) / 16 * 16;
+    if (so > h->seeded_cap) {
+      h->seeded = (uint8_t*)atc_pool_alloc(ctx, std::max(so, (size_t)256));
+      if (!h->seeded) {
+        h->seeded_cap = 0;
+        atc_set_error(ctx, "device allocation failed (seeded test sets)");
+        return ATC_ERR_CUDA;
+      }
+      h->allocations.push_back(h->seeded);
+      h->seeded_cap = so;
+    }
+    if (ctx->free_pending & (1ull << h->cs)) {
+      cudaStreamWaitEvent(ctx->copy_stream[h->cs], ctx->free_ev, 0);
+      ctx->free_pending &= ~(1ull << h->cs);
+    }
   }
-  return ATC_OK;
+  const int workers = distinct ? std::min(n, 4) : 1;
+  std::atomic<int> first_rc{ATC_OK};
+  auto work = [&](int w) {
+    cudaSetDevice(ctx->device);
+    for (int i = w; i < n; i += workers) {
+      const int rc = testsets_fill(ctx, handles[i], nullptr, ts + i, false, true, ctx->update_ev);
+      if (rc) {
+        int expected = ATC_OK;
+        first_rc.compare_exchange_strong(expected, rc);
+        return;
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int w = 1; w < workers; ++w) pool.emplace_back(work, w);
+  work(0);
+  for (auto& th : pool) th.join();
+  return first_rc.load();
 }
 
 int atc_testsets_download(atc_ctx* ctx, const atc_testset_handle* h, double* init, double* final_) {
