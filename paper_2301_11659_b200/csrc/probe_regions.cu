@@ -114,17 +114,28 @@ __global__ void __launch_bounds__(160) k_probe_regions(int T, int nP, const uint
     const double* a = init + region_off[i];
     const double* f = fin + region_off[i];
     int32_t* out = const_cast<int32_t*>(v.dirty_pos) + v.dirty_off[i];
-    for (int64_t b = 0; b < len; b += blockDim.x) {
-      const int64_t e = b + q;
-      const bool dirty = e < len && mismatch(a[e], f[e], f32);
-      const unsigned ball = __ballot_sync(0xffffffffu, dirty);
-      if (ball == 0) continue;
-      int slot = 0;
-      if (lane == 0) slot = atomicAdd(const_cast<int32_t*>(v.dirty_cnt) + i, __popc(ball));
-      slot = __shfl_sync(0xffffffffu, slot, 0);
-      if (dirty) {
-        out[slot + __popc(ball & ((1u << lane) - 1))] = (int32_t)e;
-        atomicMax(const_cast<int32_t*>(v.dirty_max) + i, (int32_t)e);
+    constexpr int U = 4;  // four elements per thread in flight: the loads do not wait on the ballots
+    for (int64_t b = 0; b < len; b += (int64_t)U * blockDim.x) {
+      double av[U], fv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = b + (int64_t)u * blockDim.x + q;
+        av[u] = e < len ? a[e] : 0.0;
+        fv[u] = e < len ? f[e] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = b + (int64_t)u * blockDim.x + q;
+        const bool dirty = e < len && mismatch(av[u], fv[u], f32);
+        const unsigned ball = __ballot_sync(0xffffffffu, dirty);
+        if (ball == 0) continue;
+        int slot = 0;
+        if (lane == 0) slot = atomicAdd(const_cast<int32_t*>(v.dirty_cnt) + i, __popc(ball));
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (dirty) {
+          out[slot + __popc(ball & ((1u << lane) - 1))] = (int32_t)e;
+          atomicMax(const_cast<int32_t*>(v.dirty_max) + i, (int32_t)e);
+        }
       }
     }
   }
