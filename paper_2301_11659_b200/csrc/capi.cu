@@ -49,14 +49,14 @@ __global__ void k_screen_rows(TestsetView ts, SpecView sp, const uint8_t* perms,
                               unsigned long long* surv_cnt, unsigned long long* reason_hist);
 __global__ void k_confirm_warp(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                                uint64_t surv_cap, int32_t* surv_keys, const uint32_t* sel,
-                               const unsigned long long* sel_cnt, int mode);
+                               const unsigned long long* sel_cnt, int mode, int screened);
 __global__ void k_confirm_pre(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                               const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
                               uint32_t* pend, unsigned long long* pend_cnt, int mode, int screened);
 __global__ void k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                              const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
                              const uint32_t* pend, const unsigned long long* pend_cnt, uint32_t* next,
-                             unsigned long long* next_cnt, int mode, int lazy);
+                             unsigned long long* next_cnt, int mode, int lazy, int screened);
 __global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
                              const int32_t* surv_keys, int32_t* keys);
 __global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason);
@@ -999,21 +999,23 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
   const unsigned g_t1 = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>((max_surv * (uint64_t)std::max(ts->T - 1, 0) + 7) / 8, k2_cap));
   const bool pre = sp.sem == ATC_SEM_CONV2D;
+  const int screened = plan && plan->cmask && src.enumerated ? 1 : 0;  // pair-screened conv space
   if (pre)
     k_confirm_pre<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 255) / 256, ctx->sm_count * 8)),
                     256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pend, next_cnt + 1,
-                                  ctx->mode, plan && plan->cmask && src.enumerated ? 1 : 0);
+                                  ctx->mode, screened);
   if (pre && !keys) {
     // enumerated ranges report reasons, not failing tests: t >= 1 first over every
     // pending survivor, then t = 0 only where it can change the reason (k_confirm_t0)
     k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, pend, next_cnt + 1,
-                                         ctx->mode);
+                                         ctx->mode, screened);
     k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pend, next_cnt + 1,
-                                       next, next_cnt, ctx->mode, 1);
+                                       next, next_cnt, ctx->mode, 1, screened);
   } else {
     k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys,
-                                       pre ? pend : nullptr, next_cnt + 1, next, next_cnt, ctx->mode, 0);
-    k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, next, next_cnt, ctx->mode);
+                                       pre ? pend : nullptr, next_cnt + 1, next, next_cnt, ctx->mode, 0, screened);
+    k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, next, next_cnt, ctx->mode,
+                                         screened);
   }
   if (ctx->prof) {
     cudaEventRecord(e2.second, st);

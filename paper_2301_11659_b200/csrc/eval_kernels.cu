@@ -557,17 +557,59 @@ __global__ void __launch_bounds__(256) k_screen_enum(TestsetView ts, SpecView sp
 // The verdict of binding `idx` at test t computed by one warp (every lane returns
 // it): the scalar checks of run_dispatch / bounds, then the dirty set and the
 // written outputs 32 at a time (lanes split the write set, __any_sync early exit).
+// screened: an enumerated conv space of the bundled conv2d layout (the pair
+// screen's precondition: size params 0..8 = n, c, h, w, k, r, s, oh, ow; arrays
+// in, weights, out = 0, 1, 2) — the same checks on sizes read straight off the
+// nine digits, without the generic decode.
 __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const BindingSource& src, uint64_t idx, int t,
-                            int mode, int lane) {
-  int ptr_of[ATC_MAX_ARRAYS], int_of[ATC_MAX_SIZES];
-  decode_binding(src, sp, ts.nI, idx, ptr_of, int_of);
-  int64_t sz[ATC_MAX_SIZES];
-  for (int q = 0; q < sp.nS; ++q) sz[q] = ts.ints[t * ts.nI + int_of[q]];
+                            int mode, int lane, bool screened = false) {
+  int ptr_of[ATC_MAX_ARRAYS];
   int r = 0;
-  if (!ts.test_ok[t]) r = ATC_FAIL_TESTSET;
-  if (!r) r = extent_check(sp, sz, ptr_of, ts.region_len);
   Dims d;
-  resolve_dims(sp, sz, d);
+  if (screened) {
+    const uint64_t g = src.begin + idx;
+    const uint64_t perm = g / src.size_maps;
+    uint64_t s = g - perm * src.size_maps;
+    int64_t v[9];
+    const int64_t* tints = ts.ints + (size_t)t * ts.nI;
+    if (s < (1ull << 32)) {
+      uint32_t s32 = (uint32_t)s;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        const uint32_t dq = s32 / (uint32_t)ts.nI;
+        v[q] = tints[s32 - dq * (uint32_t)ts.nI];
+        s32 = dq;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        const uint64_t dq = s / (uint64_t)ts.nI;
+        v[q] = tints[s - dq * (uint64_t)ts.nI];
+        s = dq;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ptr_of[a] = src.perms[perm * 3 + a];
+    d.cn = v[0], d.cc = v[1], d.ch = v[2], d.cw = v[3], d.ck = v[4], d.cr = v[5], d.cs = v[6], d.coh = v[7],
+    d.cow = v[8];
+    if (!ts.test_ok[t]) r = ATC_FAIL_TESTSET;
+    if (!r) {  // extent_check over in (n,c,h,w), weights (k,c,r,s), out (n,k,oh,ow)
+      bool pos = true;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) pos = pos && v[q] >= 1;
+      if (!pos || ts.region_len[ptr_of[0]] < v[0] * v[1] * v[2] * v[3] ||
+          ts.region_len[ptr_of[1]] < v[4] * v[1] * v[5] * v[6] || ts.region_len[ptr_of[2]] < v[0] * v[4] * v[7] * v[8])
+        r = ATC_FAIL_DISPATCH;
+    }
+  } else {
+    int int_of[ATC_MAX_SIZES];
+    decode_binding(src, sp, ts.nI, idx, ptr_of, int_of);
+    int64_t sz[ATC_MAX_SIZES];
+    for (int q = 0; q < sp.nS; ++q) sz[q] = ts.ints[t * ts.nI + int_of[q]];
+    if (!ts.test_ok[t]) r = ATC_FAIL_TESTSET;
+    if (!r) r = extent_check(sp, sz, ptr_of, ts.region_len);
+    resolve_dims(sp, sz, d);
+  }
   if (!r) r = ub_check(sp, d, ptr_of, ts.region_len);
   if (r) return r;
   const int pA = ptr_of[sp.arr_of_role[0]], pB = ptr_of[sp.arr_of_role[1]], pC = ptr_of[sp.arr_of_role[2]];
@@ -795,7 +837,7 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
                                                     const uint64_t* surv, const unsigned long long* surv_cnt,
                                                     uint64_t surv_cap, int32_t* surv_keys, const uint32_t* pend,
                                                     const unsigned long long* pend_cnt, uint32_t* next,
-                                                    unsigned long long* next_cnt, int mode, int lazy) {
+                                                    unsigned long long* next_cnt, int mode, int lazy, int screened) {
   const int lane = threadIdx.x & 31;
   unsigned long long cnt = pend ? *pend_cnt : *surv_cnt;
   if (cnt > surv_cap) cnt = surv_cap;
@@ -808,7 +850,7 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
       const int32_t k = surv_keys[si];
       if (k != kPassKey && (k & 7) == ATC_FAIL_MISMATCH) continue;
     }
-    const int r = warp_verdict(ts, sp, src, surv[si], 0, mode, lane);
+    const int r = warp_verdict(ts, sp, src, surv[si], 0, mode, lane, screened != 0);
     if (lane == 0) {
       if (r) {
         surv_keys[si] = fail_key(0, r);
@@ -827,7 +869,7 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
 __global__ void __launch_bounds__(256) k_confirm_warp(TestsetView ts, SpecView sp, BindingSource src,
                                                       const uint64_t* surv, uint64_t surv_cap, int32_t* surv_keys,
                                                       const uint32_t* sel, const unsigned long long* sel_cnt,
-                                                      int mode) {
+                                                      int mode, int screened) {
   const int lane = threadIdx.x & 31;
   unsigned long long cnt = *sel_cnt;
   if (cnt > surv_cap) cnt = surv_cap;
@@ -842,7 +884,7 @@ __global__ void __launch_bounds__(256) k_confirm_warp(TestsetView ts, SpecView s
     const uint32_t si = sel[w - tt * cnt];
     const int t = 1 + (int)tt;
     if (*(volatile int32_t*)(surv_keys + si) < fail_key(t, 0)) continue;  // failed at a lower t already
-    const int r = warp_verdict(ts, sp, src, surv[si], t, mode, lane);
+    const int r = warp_verdict(ts, sp, src, surv[si], t, mode, lane, screened != 0);
     if (lane == 0 && r) atomicMin(&surv_keys[si], fail_key(t, r));
   }
 }
