@@ -176,6 +176,9 @@ struct Problem {
   int pair;  // 1: CTA pairs (cluster of 2) on adjacent M tiles share the B tile via TMA multicast
   int tma_store;  // 1: epilogue writes 32x32 sub-tiles with TMA bulk stores (modes 0, 2, 3)
   int umma2;      // 1: sgemm on k_tc_gemm2 (cta_group::2, M = 256 per CTA pair)
+  int ksplit;     // k_tc_gemm2, conv mode 4: 2 = each tile's k-blocks in two halves on two
+                  // pairs, both added into the zeroed output (two partial sums: the same
+                  // result in either order)
 };
 
 struct Maps {
@@ -522,7 +525,9 @@ __device__ __forceinline__ void epilogue_chunk(const Problem& p, const Maps& map
     const bool ok = n < p.img;
     const int64_t off = ((int64_t)n * p.M + row0) * ohw + (q - n * ohw);
     const int rows = min(32, p.M - row0);
-    if (ok)
+    if (ok && p.ksplit > 1)
+      for (int i = 0; i < rows; ++i) atomicAdd(p.C + off + (int64_t)i * ohw, stg[i * 33 + lane]);
+    else if (ok)
       for (int i = 0; i < rows; ++i) p.C[off + (int64_t)i * ohw] = stg[i * 33 + lane];
     __syncwarp();
     return;
@@ -633,7 +638,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
   uint32_t rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int tiles_m2 = (p.tiles_m + 1) / 2;  // 256-row tiles
-  const int num_units = tiles_m2 * p.tiles_n * p.tiles_img;
+  const int ks_n = p.ksplit > 1 ? p.ksplit : 1;  // unit = tile * ks_n + k-part
+  const int kb_per = total_kb / ks_n;
+  const int num_units = tiles_m2 * p.tiles_n * p.tiles_img * ks_n;
   const int unit0 = (int)(blockIdx.x / 2), unit_step = (int)(gridDim.x / 2);
 
   if (warp == 0 && lane == 0) {
@@ -670,10 +677,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
           Problem q = p;
           q.tiles_m = tiles_m2;
           q.pair = 0;
-          tile_coords(q, unit, tm2, tn, ti, kGroup2);
+          tile_coords(q, unit / ks_n, tm2, tn, ti, kGroup2);
         }
         const int tm = 2 * tm2 + (int)rank;  // this CTA's 128 rows
-        for (int kb = 0; kb < total_kb; ++kb) {
+        const int kb0 = (unit % ks_n) * kb_per;
+        for (int kb = kb0; kb < kb0 + kb_per; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           int sa, sb, a0, a1, b0, b1;
           kblock_coords(p, kb, kblocks, tm, tn, ti, sa, sb, a0, a1, b0, b1);
@@ -723,7 +731,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < total_kb; ++kb) {
+        const int kb0 = (unit % ks_n) * kb_per;
+        for (int kb = kb0; kb < kb0 + kb_per; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * STAGE2_BYTES);
@@ -734,7 +743,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
             const uint64_t ad = make_desc(a_addr + kk * 32, 16, 1024, kSw128);
             const uint64_t bd = b_kmajor ? make_desc(b_addr + kk * 32, 16, 1024, kSw128)
                                          : make_desc(b_addr + kk * 1024, BK * 128, 512, kSw128Base32);
-            mma_tf32_2sm(d_tmem, ad, bd, idesc_tf32_m256(b_kmajor ? 0u : 1u), (kb > 0 || kk > 0) ? 1u : 0u);
+            mma_tf32_2sm(d_tmem, ad, bd, idesc_tf32_m256(b_kmajor ? 0u : 1u), (kb > kb0 || kk > 0) ? 1u : 0u);
           }
           mma_commit_2sm(&empty[stage]);  // both CTAs' stage buffers free once these complete
           if (++stage == STAGES2) {
@@ -762,7 +771,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
         Problem q2 = p;
         q2.tiles_m = tiles_m2;
         q2.pair = 0;
-        tile_coords(q2, unit, tm2, tn, ti, kGroup2);
+        tile_coords(q2, unit / ks_n, tm2, tn, ti, kGroup2);
       }
       const int tm = 2 * tm2 + (int)rank;
       mbar_wait(&tmem_full[acc], acc_phase);
@@ -942,6 +951,14 @@ bool make_map(atc_ctx* ctx, CUtensorMap* m, const float* base, uint64_t rows, ui
 }
 
 // ATC_TC_2SM=0 disables the cta_group::2 kernel (A/B measurement)
+bool ksplit_enabled() {  // ATC_TC_KSPLIT=0: never split K (A/B checks)
+  static const bool on = [] {
+    const char* e = std::getenv("ATC_TC_KSPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int umma2_enabled() {
   static const int on = [] {
     const char* e = std::getenv("ATC_TC_2SM");
@@ -980,7 +997,7 @@ bool launch(atc_ctx* ctx, const Maps& maps, const Problem& p, cudaStream_t st) {
     configured = true;
   }
   if (p.umma2) {
-    const int units = (p.tiles_m + 1) / 2 * p.tiles_n;
+    const int units = (p.tiles_m + 1) / 2 * p.tiles_n * (p.ksplit > 1 ? p.ksplit : 1);
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1247,6 +1264,19 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
   }
   p.pair = use_pair(p);
   p.umma2 = umma2 ? 1 : 0;
+  // split-K over two CTA pairs when the pair tiles leave most of a second wave idle
+  // (conv5: 98 tiles on 74 pair slots); the output is zeroed and both halves added
+  if (im2col && splits == 1 && ksplit_enabled()) {
+    const int pairs = std::max(1, ctx->sm_count / 2);
+    const int units = (p.tiles_m + 1) / 2 * p.tiles_n;
+    const int kb = (int)(r * s * (c / BK));
+    auto eff = [&](int u) { return (double)u / (double)(((u + pairs - 1) / pairs) * pairs); };
+    if (kb % 2 == 0 && eff(2 * units) > eff(units) + 0.1) {
+      p.ksplit = 2;
+      if (!atc_cuda_ok(ctx, cudaMemsetAsync(d_out, 0, (size_t)(n * k * oh * ow) * 4, st), "memset out"))
+        return ATC_ERR_CUDA;
+    }
+  }
   // 1x1 direct: the output is a [N*K][OH*OW] matrix (hw % 4 == 0): TMA-store epilogue
   p.tma_store = direct && tma_store_enabled() ? 1 : 0;
   if (p.tma_store && !make_map(ctx, &maps.c, d_out, n * k, oh * ow, oh * ow, 32, 32, false)) return ATC_ERR_CUDA;

@@ -101,7 +101,9 @@ def test_sgemm_sample_one_pattern():
 @pytest.mark.parametrize("shape", [(2, 64, 10, 12, 64, 3, 3), (1, 32, 9, 9, 512, 3, 3), (3, 64, 8, 8, 256, 1, 1),
                                    (2, 96, 17, 13, 40, 2, 4),
                                    # > 128 filters, several images: the im2col pair kernel
-                                   (5, 64, 11, 7, 256, 3, 2), (3, 32, 6, 9, 300, 2, 3), (9, 64, 9, 9, 384, 3, 3)])
+                                   (5, 64, 11, 7, 256, 3, 2), (3, 32, 6, 9, 300, 2, 3), (9, 64, 9, 9, 384, 3, 3),
+                                   # 20 pair tiles on 74 pair slots: split-K over two pairs
+                                   (5, 64, 34, 34, 256, 3, 3)])
 @pytest.mark.parametrize("prec", ["tf32", "3xtf32"])
 def test_conv2d_accuracy(shape, prec):
     n, c, h, w, k, r, s = shape
