@@ -1009,8 +1009,9 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     // pending survivor, then t = 0 only where it can change the reason (k_confirm_t0)
     k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, pend, next_cnt + 1,
                                          ctx->mode, screened);
-    k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pend, next_cnt + 1,
-                                       next, next_cnt, ctx->mode, 1, screened);
+    const unsigned g_lazy = (unsigned)std::min<uint64_t>((uint64_t)g_t0 * 8, k2_cap);  // 8 warps per binding
+    k_confirm_t0<<<g_lazy, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pend, next_cnt + 1,
+                                         next, next_cnt, ctx->mode, 1, screened);
   } else {
     k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys,
                                        pre ? pend : nullptr, next_cnt + 1, next, next_cnt, ctx->mode, 0, screened);

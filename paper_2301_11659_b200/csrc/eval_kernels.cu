@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(256) k_screen_enum(TestsetView ts, SpecView sp
 // in, weights, out = 0, 1, 2) — the same checks on sizes read straight off the
 // nine digits, without the generic decode.
 __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const BindingSource& src, uint64_t idx, int t,
-                            int mode, int lane, bool screened = false) {
+                            int mode, int lane, bool screened = false, int part = 0, int parts = 1) {
   int ptr_of[ATC_MAX_ARRAYS];
   int r = 0;
   Dims d;
@@ -657,7 +657,8 @@ __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const Bin
       // four outputs per lane per step: four independent accumulation chains (each in
       // the reference's order) hide the dependent-add latency of long checks
       constexpr int MO = 4;
-      for (int o0 = 0; o0 < (int)wext && !bad; o0 += 32 * MO) {
+      // part / parts: this warp's share of the output steps (the others run in other warps)
+      for (int o0 = part * 32 * MO; o0 < (int)wext && !bad; o0 += parts * 32 * MO) {
         const double* inp[MO];
         const double* wtp[MO];
         int oo[MO];
@@ -844,6 +845,22 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
   // warp-major numbering: consecutive items land in different CTAs (different SMs) —
   // the few long full-length checks do not share an SM
+  // lazy conv (FP64): the few bindings still needing t = 0 are mostly full-length checks
+  // — eight warps share one binding's outputs and fold failures in with atomicMin
+  const int parts = lazy && sp.sem == ATC_SEM_CONV2D && mode == ATC_MODE_FP64 ? 8 : 1;
+  if (parts > 1) {
+    const uint64_t work = cnt * (uint64_t)parts;
+    for (uint64_t w = (uint64_t)(threadIdx.x / 32) * gridDim.x + blockIdx.x; w < work; w += warps) {
+      const uint64_t wi = w / (uint64_t)parts;
+      const int part = (int)(w - wi * (uint64_t)parts);
+      const uint64_t si = pend ? pend[wi] : wi;
+      const int32_t k = *(volatile int32_t*)(surv_keys + si);
+      if (k != kPassKey && ((k & 7) == ATC_FAIL_MISMATCH || k < fail_key(1, 0))) continue;  // decided
+      const int r = warp_verdict(ts, sp, src, surv[si], 0, mode, lane, screened != 0, part, parts);
+      if (lane == 0 && r) atomicMin(&surv_keys[si], fail_key(0, r));
+    }
+    return;
+  }
   for (uint64_t wi = (uint64_t)(threadIdx.x / 32) * gridDim.x + blockIdx.x; wi < cnt; wi += warps) {
     const uint64_t si = pend ? pend[wi] : wi;
     if (lazy) {
