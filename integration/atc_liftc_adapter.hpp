@@ -73,15 +73,15 @@ interp::DispatchContext make_gpu_dispatch(const api::ApiSpec& spec, atc_ctx* ctx
 // (m, n, k) features the reference uses and records it in *choices.  "cpu"
 // calls, f64 regions, and calls the FP32 backends cannot express run the exact
 // FP64 path (== make_gpu_dispatch, bit-identical to the reference).  "xpu" calls
-// on f32 regions run on atc_sgemm_rm / atc_conv2d_nchw at `precision`
-// (ATC_PREC_TF32 / ATC_PREC_3XTF32).  kRouteExact keeps every call on the exact
-// path, which makes the handler a drop-in for the reference's routed dispatch
-// (labels recorded, results unchanged).
+// on f32 regions run on atc_sgemm_rm / atc_conv2d_nchw only when the caller opts
+// in with `precision` = ATC_PREC_TF32 / ATC_PREC_3XTF32.  The default, kRouteExact,
+// keeps every call on the exact path, which makes the handler a drop-in for the
+// reference's routed dispatch (labels recorded, results unchanged).
 constexpr int32_t kRouteExact = -1;
 interp::DispatchContext make_gpu_routed_dispatch(const api::ApiSpec& spec, atc_ctx* ctx,
                                                  const profitability::SvmModel* model,
                                                  std::vector<std::string>* choices,
-                                                 int32_t precision = ATC_PREC_3XTF32);
+                                                 int32_t precision = kRouteExact);
 
 // The predictor features of one call (rewriter.cpp:194-205).
 std::vector<long long> routed_sizes(const api::ApiSpec& spec, const std::map<std::string, long long>& sizes);

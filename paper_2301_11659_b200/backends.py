@@ -267,15 +267,16 @@ def _tensor(spec: ApiSpec, cx, prec: int, sizes: dict, region_of: dict, regions:
     return True
 
 
-def make_routed_dispatch(spec: ApiSpec, predict=None, choices: list | None = None, precision: str = "3xtf32",
+def make_routed_dispatch(spec: ApiSpec, predict=None, choices: list | None = None, precision: str = "exact",
                          ctx=None):
     """rewriter::make_routed_dispatch (rewriter.hpp:57-66, rewriter.cpp:183-213) on the
     GPU.  predict(mnk) -> 0/1 is the backend predictor (svm_predictor(model json) for
     the reference's saved model); each call appends "xpu"/"cpu" to `choices` ("cpu"
     for every call without a predictor).  "xpu" calls on f32 regions run on the
-    tcgen05 backends at `precision` ("tf32" / "3xtf32"); everything else — and every
-    call when precision == "exact" — runs the exact FP64 path, bit-identical to the
-    reference's routed dispatch."""
+    tcgen05 backends only when the caller opts in with precision "tf32" / "3xtf32";
+    by default (precision == "exact") every call — like everything else — runs the
+    exact FP64 path, bit-identical to the reference's routed dispatch, which only
+    records the label."""
     desc = spec.to_desc()
     if precision != "exact" and precision not in _PREC:
         raise ValueError(f"precision must be 'exact', 'tf32' or '3xtf32', not {precision!r}")

@@ -302,8 +302,9 @@ class Evaluator:
         self.ctx = ctx or _lib.default_context(device)
 
     def eval_bindings(self, spec: ApiSpec, ts: RecordedTestsets, arr_map: np.ndarray, size_map: np.ndarray,
-                      mode: int = _lib.MODE_FP64) -> BatchVerdicts:
-        h = ts.upload(self.ctx)
+                      mode: int = _lib.MODE_FP64, handle=None) -> BatchVerdicts:
+        """`handle`: an already uploaded test-set handle of `ts` (e.g. upload_seeded)."""
+        h = handle or ts.upload(self.ctx)
         n = int(arr_map.shape[0])
         am = np.ascontiguousarray(arr_map, dtype=np.uint8)
         sm = np.ascontiguousarray(size_map, dtype=np.uint8)

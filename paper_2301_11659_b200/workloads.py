@@ -5,8 +5,10 @@ corpus  every GEMM and conv2d corpus program x every spec of its class, the FULL
         sets each (configs 2-4; the conv spaces are 2.3e9-9.3e9 bindings, which
         only a GPU can sweep).
 stress  naive_ld x gemm_rowmajor_ld, 279,936 bindings x 16 sets (config 4 alone).
+naive64 naive_f32 x {gemm_rowmajor, gemm_colmajor} at m = n = k = 64 (config 1:
+        the P2 sets drawn with the [64, 64] rule, 162 bindings per spec).
 pruned  the ranked (pruned) candidate list of every program (config 2 as the
-        pipeline sees it; latency-bound).
+        pipeline sees it; latency-bound): pruned_lists().
 
 Algorithmic bytes: a screened (binding, t) pair is charged
 elem_bytes * (ext_A + ext_B + ext_C) with ext_X = prod of X's API dims under
@@ -93,6 +95,72 @@ def corpus_jobs(T: int = 16, kinds=("gemm", "conv")) -> list:
                 exp = v["idx"][ok].tolist()
             jobs.append(Job(stem, sname, fixtures.spec(sname), p.space(sname), ts, exp))
     return jobs
+
+
+@dataclass
+class SpaceCount:
+    """A corpus binding space described without its test sets (pure arithmetic:
+    no probe image is regenerated, so nothing touches libatc_b200)."""
+
+    stem: str
+    spec_name: str
+    spec: ApiSpec
+    count: int
+
+
+def corpus_spaces(kinds=("gemm", "conv")) -> list:
+    """corpus_jobs()' spaces (same order), counts only."""
+    out = []
+    for stem in fixtures.stems():
+        p = fixtures.load(stem)
+        if "specs" not in p.meta or p.meta.get("corpus_dir") not in kinds:
+            continue
+        for sname in p.spec_names():
+            out.append(SpaceCount(stem, sname, fixtures.spec(sname), p.space(sname).count))
+    return out
+
+
+def naive64_jobs(T: int = 16) -> list:
+    """Config 1: naive_f32 at 64^3 (the testsets64 variant: P2 sets drawn with
+    m = n = k = [64, 64]) against both dense GEMM specs, full 162-binding spaces."""
+    p = fixtures.load("naive_f32")
+    ts = p.testsets(T, variant="testsets64")
+    jobs = []
+    for sname in ("gemm_rowmajor", "gemm_colmajor"):
+        v = p.verdicts(sname, "p2_64")
+        ok = (v["fail_t"] < 0) | (v["fail_t"] >= T)
+        jobs.append(Job("naive_f32", sname, fixtures.spec(sname), p.space(sname), ts, v["idx"][ok].tolist()))
+    return jobs
+
+
+def pruned_lists(T: int = 16) -> list:
+    """Config 2 as the pipeline sees it: per (program, spec) the ranked candidate
+    list find_matchings + rank_candidates produced (tests/golden, from the
+    reference), as (stem, spec, testsets, arr_map, size_map, reference P2 ok)."""
+    from .evaluator import encode_bindings
+
+    out = []
+    for stem in fixtures.stems():
+        p = fixtures.load(stem)
+        if "specs" not in p.meta or p.meta.get("corpus_dir") not in ("gemm", "conv"):
+            continue
+        ts = None
+        for sname, s in p.meta["specs"].items():
+            ranked = s.get("pruned") or []
+            if not ranked or s.get("truncated"):
+                continue
+            ts = ts or p.testsets(T)
+            spec = fixtures.spec(sname)
+            am, sm = encode_bindings(ranked, spec, p.user_ptrs, p.user_ints)
+            space = p.space(sname)
+            v = p.verdicts(sname)
+            pos = {int(g): i for i, g in enumerate(v["idx"])}
+            ok = []
+            for c in ranked:
+                g = pos.get(space.index_of(c))
+                ok.append(None if g is None else bool(v["fail_t"][g] < 0 or v["fail_t"][g] >= T))
+            out.append((stem, sname, spec, ts, am, sm, ok))
+    return out
 
 
 def stress_jobs(T: int = 16) -> list:
