@@ -181,6 +181,27 @@ typedef struct {
 } atc_seeded_testsets;
 int atc_testsets_upload_seeded(atc_ctx* ctx, const atc_seeded_testsets* ts, atc_testset_handle** out);
 
+/* The recorded test sets when the caller already holds the probe images (the
+ * liftc host builds them for its own original runs, rewriter.cpp:242-247): the
+ * full host regions plus the original run's final-minus-init entries, of which
+ * only what an evaluation can read crosses PCIe — region (t, p)'s prefix up to the
+ * needed_only bound of the seeded form — U^4 + 2U^2 + 2U + 1, or one past its
+ * last final-minus-init position — and the final images are rebuilt on the
+ * device.  Evaluations are unchanged; atc_testsets_download refuses such a handle.
+ * Host buffers are not retained (the prefixes are staged before returning). */
+typedef struct {
+  int32_t n_tests, n_ints, n_ptrs;
+  const int64_t* int_values;   /* [T][n_ints]                                         */
+  const int32_t* ptr_is_f32;   /* [n_ptrs]                                            */
+  const int64_t* region_len;   /* [n_ptrs]                                            */
+  const int32_t* test_ok;      /* [T]                                                 */
+  const double* const* init;   /* [T*n_ptrs]: probe regions (NULL where test_ok[t] == 0) */
+  const int64_t* diff_off;     /* [T*n_ptrs + 1]                                      */
+  const int32_t* diff_pos;
+  const double* diff_val;
+} atc_prefix_testsets;
+int atc_testsets_upload_prefix(atc_ctx* ctx, const atc_prefix_testsets* ts, atc_testset_handle** out);
+
 /* New seeded contents for an existing handle (same n_tests, n_ints, n_ptrs,
  * region lengths and element types), written in place after every evaluation
  * already queued on the context's stream: prepared batches (atc_enum_batch_*)
@@ -202,6 +223,25 @@ int atc_testsets_download(atc_ctx* ctx, const atc_testset_handle* h, double* ini
 int atc_eval_bindings(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_handle* ts,
                       const uint8_t* arr_map, const uint8_t* size_map, int64_t n_bindings,
                       int32_t mode, int8_t* fail_t, int8_t* reason, int64_t* first_pass);
+
+/* Several explicit lists at once — e.g. every spec's ranked candidates of one user
+ * function (the specs pipeline.cpp:227-312 tries in turn), each against its own
+ * test-set handle: one H2D of all maps, every list's kernels queued back to back,
+ * one D2H and one synchronisation.  Each job's outputs equal atc_eval_bindings on
+ * that job alone; status is ATC_OK or the job's own error (the call then returns
+ * the first failing status). */
+typedef struct atc_bind_job {
+  const atc_spec_desc* spec;
+  const atc_testset_handle* ts;
+  const uint8_t* arr_map;   /* [n_bindings][spec->n_arrays] */
+  const uint8_t* size_map;  /* [n_bindings][spec->n_sizes]  */
+  int64_t n_bindings;
+  int8_t* fail_t;           /* out [n_bindings] */
+  int8_t* reason;           /* out [n_bindings] */
+  int64_t first_pass;       /* out: smallest passing b, or -1 */
+  int32_t status;           /* out */
+} atc_bind_job;
+int atc_eval_bindings_many(atc_ctx* ctx, atc_bind_job* jobs, int32_t n_jobs, int32_t mode);
 
 /* Same with device-resident inputs/outputs on the caller's CUDA stream (cudaStream_t
  * passed as void*); returns without synchronising. */

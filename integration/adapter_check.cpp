@@ -7,14 +7,18 @@
 //
 //   adapter_check corpus
 //       for every GEMM/conv corpus program: the reference's own
-//       pipeline::lift_program vs. the same analysis + matching + ranking followed
-//       by liftc::gpu::first_accepted (GPU P2 batch + host P1 on survivors);
-//       prints one JSON line per program with both winners.
+//       pipeline::lift_program vs. the same analysis followed by
+//       liftc::gpu::candidate_loop (one GPU P2 batch for every spec + host P1 in
+//       rank order): byte-equal masked report_to_json, and the production
+//       setting's (P1 on P2 survivors only) winner and timings.
 //   adapter_check unpruned <stem> <spec> [tests]
 //       the full unpruned binding space of one program in Appendix C order as the
 //       ranked list: GPU P2 over all of it + host P1 on survivors, timed.
 //   adapter_check dispatch
 //       the lifted program run with make_gpu_dispatch vs make_oracle_dispatch.
+//   adapter_check details [per_space]
+//       gpu::p2_detail vs rewriter::verify_rewrite's detail on P2-rejected bindings
+//       of every corpus program x spec (report parity of VerificationFailed).
 //   adapter_check routed
 //       make_gpu_routed_dispatch vs rewriter::make_routed_dispatch: the same
 //       cpu/xpu labels on every lifted corpus function (model trained by the
@@ -148,53 +152,77 @@ int cmd_corpus(atc_ctx* ctx) {
     for (const auto& s : specs)
       if (s.semantics == fr->class_label) lspecs.push_back(&s);
     auto fn = analyze(p, fseed, lspecs);
+    gpu::LoopConfig lc;
+    lc.tests = cfg.tests;
+    lc.verify_tests = cfg.verify_tests;
+    lc.max_candidates = cfg.max_candidates;
+    lc.budget_sec = cfg.budget_sec;
+    lc.report = true;
     t0 = std::chrono::steady_clock::now();
-    std::string gpu_status = "NoMatch", gpu_api;
-    int gpu_rank = -1;
-    matching::CandidateBinding gpu_binding;
-    bool too_many = false;
-    int p1_calls = 0;
-    struct Ev {
-      std::string api;
-      int rank;
-      std::string verdict;
-    };
-    std::vector<Ev> evaluated;
-    double gpu_ms = 0;
-    auto recorded = gpu::record_tests(p.prog, p.function, p.meta.rules, Rng::mix(fseed, "post"), cfg.verify_tests);
-    for (const auto* spec : lspecs) {  // pipeline.cpp:227-312 control flow
-      auto ranked = matching::rank_candidates(matching::find_matchings(fn, *spec), cfg.max_candidates);
-      if (ranked.truncated) {
-        too_many = true;
-        continue;
-      }
-      auto lr = gpu::first_accepted(ctx, p.prog, fn, p.function, *spec, ranked.ranked, p.meta.rules, fseed,
-                                    cfg.tests, cfg.verify_tests, &recorded, /*report_parity=*/true);
-      for (size_t i = 0; i < lr.verdicts.size(); ++i) evaluated.push_back({spec->name, (int)i, lr.verdicts[i]});
-      p1_calls += lr.p1_calls;
-      gpu_ms += lr.gpu_ms;
-      if (lr.winner) {
-        gpu_status = "Lifted";
-        gpu_api = spec->name;
-        gpu_rank = (int)*lr.winner;
-        gpu_binding = ranked.ranked[*lr.winner];
-        break;
-      }
-      if (too_many) break;
-    }
-    if (gpu_status != "Lifted" && too_many) gpu_status = "TooManyCandidates";
+    auto loop = gpu::candidate_loop(ctx, p.prog, fn, p.function, lspecs, p.meta.rules, fseed, lc);
     const double ours_ms = ms_since(t0);
+    // the reference's report with every candidate-stage field replaced by ours
+    // (pipeline.cpp:223-330); everything else is the unchanged host analysis
+    pipeline::FunctionReport mine = *fr;
+    mine.status = loop.status;
+    mine.status_detail = loop.status_detail;
+    mine.by_spec = loop.by_spec;
+    mine.evaluated = loop.evaluated;
+    mine.winning_api.clear();
+    mine.manifest = rewriter::LiftManifest{};
+    if (loop.status == pipeline::FunctionStatus::Lifted) {  // pipeline.cpp:285-298
+      mine.winning_api = loop.winning_spec->name;
+      mine.manifest = loop.rewrite.manifest;
+      mine.manifest.verdict = "Equivalent";
+      mine.manifest.class_label = fr->class_label;
+      mine.manifest.class_score = fr->class_score;
+      for (const auto& b : loop.by_spec)
+        if (b.api == mine.winning_api) {
+          mine.manifest.raw_candidates = b.raw;
+          mine.manifest.pruned_candidates = b.filtered;
+        }
+      mine.manifest.winner_rank = loop.winner_rank;
+    }
+    pipeline::FileReport ref_file, our_file;
+    ref_file.file = our_file.file = p.tag;
+    ref_file.functions = {*fr};
+    our_file.functions = {mine};
+    const std::string ref_json = pipeline::mask_timings(pipeline::report_to_json(ref_file)).dump();
+    const std::string our_json = pipeline::mask_timings(pipeline::report_to_json(our_file)).dump();
+    const bool same_report = ref_json == our_json;
+    std::string gpu_status = pipeline::status_name(loop.status), gpu_api = mine.winning_api;
+    const int gpu_rank = loop.winner_rank;
     bool same = gpu_status == pipeline::status_name(fr->status);
     if (same && gpu_status == "Lifted")
       same = gpu_api == fr->winning_api && gpu_rank == fr->manifest.winner_rank &&
-             gpu_binding.arrays == fr->manifest.arrays && gpu_binding.sizes == fr->manifest.sizes;
-    // report-level parity: the evaluated[] entries (pipeline.cpp:262-309)
-    bool same_report = evaluated.size() == fr->evaluated.size();
-    for (size_t i = 0; same_report && i < evaluated.size(); ++i)
-      same_report = evaluated[i].api == fr->evaluated[i].api && evaluated[i].rank == fr->evaluated[i].rank &&
-                    evaluated[i].verdict == fr->evaluated[i].verdict;
-    j["same_evaluated"] = same_report;
+             loop.rewrite.manifest.arrays == fr->manifest.arrays && loop.rewrite.manifest.sizes == fr->manifest.sizes;
+    j["same_report_json"] = same_report;
+    if (!same_report) {
+      j["ref_report"] = json::parse(ref_json);
+      j["our_report"] = json::parse(our_json);
+    }
     same = same && same_report;
+    const int p1_calls = loop.p1_calls;
+    const double gpu_ms = loop.gpu_ms;
+    j["record_ms"] = loop.record_ms;
+    j["p1_ms"] = loop.p1_ms;
+    // the production setting (P1 only on P2 survivors) against the reference's own
+    // candidate stage (its match + equivalence + rewrite/verify phases)
+    lc.report = false;
+    t0 = std::chrono::steady_clock::now();
+    auto fast = gpu::candidate_loop(ctx, p.prog, fn, p.function, lspecs, p.meta.rules, fseed, lc);
+    j["fast_loop_ms"] = ms_since(t0);
+    j["fast_gpu_p2_ms"] = fast.gpu_ms;
+    j["fast_record_ms"] = fast.record_ms;
+    j["fast_p1_ms"] = fast.p1_ms;
+    j["fast_same_winner"] = fast.status == loop.status && fast.winner_rank == loop.winner_rank &&
+                            fast.winning_spec == loop.winning_spec;
+    same = same && fast.status == loop.status && fast.winner_rank == loop.winner_rank &&
+           fast.winning_spec == loop.winning_spec;
+    double ref_loop = 0;
+    for (const char* k : {"match_ms", "equivalence_ms", "rewrite_ms"})
+      if (fr->phase_ms.count(k)) ref_loop += fr->phase_ms.at(k);
+    j["reference_loop_ms"] = ref_loop;
     if (!same) ++mismatches;
     j["gpu_status"] = gpu_status;
     j["gpu_api"] = gpu_api;
@@ -268,6 +296,97 @@ int cmd_unpruned(atc_ctx* ctx, const std::string& stem, const std::string& spec_
     return 0;
   }
   return 1;
+}
+
+// One binding of the unpruned space in Appendix C order: array
+// k-permutations in odometer order x size maps with digit 0 fastest.
+struct UnprunedSpace {
+  std::vector<std::vector<int>> perms;
+  std::vector<std::string> ptrs, ints;
+  size_t maps = 1;
+  UnprunedSpace(const analysis::AnalyzedFunction& fn, const api::ApiSpec& spec) : ints(fn.int_params) {
+    for (const auto& a : fn.arrays) ptrs.push_back(a.name);
+    const size_t nA = spec.arrays().size();
+    std::vector<int> sel(nA);
+    std::vector<bool> used(ptrs.size(), false);
+    std::function<void(size_t)> rec = [&](size_t i) {
+      if (i == nA) {
+        perms.push_back(sel);
+        return;
+      }
+      for (size_t j = 0; j < ptrs.size(); ++j)
+        if (!used[j]) {
+          used[j] = true;
+          sel[i] = (int)j;
+          rec(i + 1);
+          used[j] = false;
+        }
+    };
+    rec(0);
+    for (size_t q = 0; q < spec.size_params().size(); ++q) maps *= ints.size();
+  }
+  size_t count() const { return perms.size() * maps; }
+  matching::CandidateBinding at(const api::ApiSpec& spec, size_t idx) const {
+    matching::CandidateBinding b;
+    const auto arrays = spec.arrays();
+    const auto sizes = spec.size_params();
+    const auto& perm = perms[idx / maps];
+    for (size_t a = 0; a < arrays.size(); ++a) b.arrays[arrays[a]->name] = ptrs[perm[a]];
+    size_t x = idx % maps;
+    for (size_t q = 0; q < sizes.size(); ++q) {
+      b.sizes[sizes[q]->name] = ints[x % ints.size()];
+      x /= ints.size();
+    }
+    return b;
+  }
+};
+
+// p2_detail vs the reference's own verify_rewrite detail (rewriter.cpp:215-284) on
+// bindings of every corpus program x spec that P2 rejects: a strided sample of
+// each unpruned space plus its first bindings (mismatch and dispatch-failure
+// details; f32 and f64 regions; every program's recorded test sets).
+int cmd_details(atc_ctx* ctx, int per_space) {
+  auto specs = default_specs();
+  int bad = 0, checked = 0;
+  std::map<std::string, int> kinds;
+  for (const auto& p : corpus()) {
+    if (p.dir != "gemm" && p.dir != "conv") continue;
+    const uint64_t fseed = Rng::mix(0, p.tag + ":" + p.function);
+    const auto* f = p.prog.find(p.function);
+    for (const auto& spec : specs) {
+      if ((spec.semantics == "conv2d") != (p.dir == "conv")) continue;
+      auto fn = analyze(p, fseed, {&spec});
+      UnprunedSpace sp(fn, spec);
+      if (sp.count() == 0) continue;
+      std::vector<matching::CandidateBinding> list;
+      const size_t stride = std::max<size_t>(1, sp.count() / (size_t)per_space);
+      for (size_t i = 0; i < sp.count() && (int)list.size() < 2 * per_space; i += (i < 16 ? 1 : stride))
+        list.push_back(sp.at(spec, i));
+      auto rec = gpu::record_tests(p.prog, p.function, p.meta.rules, Rng::mix(fseed, "post"), 10);
+      auto v = gpu::p2_verdicts(ctx, rec, {&spec}, {&list});
+      for (size_t b = 0; b < list.size(); ++b) {
+        if (v[0].reason[b] == ATC_PASS) continue;
+        auto rr = rewriter::rewrite(p.prog, p.function, list[b], spec);
+        auto vr = rewriter::verify_rewrite(p.prog, rr.program, p.function, list[b], spec, p.meta.rules,
+                                           Rng::mix(fseed, "post"), 10);
+        const std::string ours =
+            gpu::p2_detail(ctx, rec, *f, spec, list[b], v[0].fail_t[b], v[0].reason[b]);
+        ++checked;
+        ++kinds[vr.detail.rfind("mismatch", 0) == 0 ? "mismatch"
+                : vr.detail.rfind("dispatch failed", 0) == 0 ? "dispatch failed"
+                                                               : "other"];
+        if (vr.ok || ours != vr.detail) {
+          ++bad;
+          std::cout << json({{"stem", p.stem}, {"spec", spec.name}, {"reference", vr.detail}, {"ours", ours},
+                             {"reference_ok", vr.ok}})
+                           .dump()
+                    << std::endl;
+        }
+      }
+    }
+  }
+  std::cout << json({{"checked", checked}, {"mismatches", bad}, {"kinds", kinds}}).dump() << std::endl;
+  return bad == 0 ? 0 : 1;
 }
 
 int cmd_dispatch(atc_ctx* ctx) {
@@ -480,6 +599,7 @@ int main(int argc, char** argv) {
     if (cmd == "corpus") rc = cmd_corpus(ctx);
     if (cmd == "unpruned" && argc >= 4) rc = cmd_unpruned(ctx, argv[2], argv[3], argc > 4 ? std::atoi(argv[4]) : 10);
     if (cmd == "dispatch") rc = cmd_dispatch(ctx);
+    if (cmd == "details") rc = cmd_details(ctx, argc > 2 ? std::atoi(argv[2]) : 24);
     if (cmd == "routed") rc = cmd_routed(ctx);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "adapter_check: %s\n", e.what());

@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -77,10 +79,13 @@ RecordedTests record_tests(const minilang::Program& prog, const std::string& fun
   r.ints.assign((size_t)tests * nI, 0);
   r.test_ok.assign(tests, 0);
   r.region_len.assign(nP, 65536);
+  r.test_detail.assign(tests, "");
   r.init.resize((size_t)tests * nP);
   r.fin.resize((size_t)tests * nP);
   // the T tests are independent streams (rewriter.cpp:236) and interp::execute is
   // re-entrant, so they are recorded on parallel host threads
+  std::vector<std::vector<int32_t>> dpos((size_t)tests * nP);
+  std::vector<std::vector<double>> dval((size_t)tests * nP);
   auto record_one = [&](int t) {
     Rng rng(Rng::mix(p2seed, "verify:" + function + ":" + std::to_string(t)));
     std::map<std::string, long long> sizes;
@@ -88,6 +93,7 @@ RecordedTests record_tests(const minilang::Program& prog, const std::string& fun
     for (int tries = 0; tries < 20 && !drawn; ++tries) drawn = analysis::draw_sizes(r.int_params, rules, rng, sizes);
     if (!drawn) {
       for (size_t p = 0; p < nP; ++p) r.init[t * nP + p].assign(65536, 0.0);
+      r.test_detail[t] = "could not draw sizes under the declared rules";  // rewriter.cpp:240
       return;
     }
     interp::MemoryImage img = analysis::build_probe_image(*f, sizes, rng);
@@ -96,9 +102,19 @@ RecordedTests record_tests(const minilang::Program& prog, const std::string& fun
     auto ref = interp::execute(prog, function, img, plain);
     for (size_t p = 0; p < nP; ++p) {
       r.init[t * nP + p] = img.regions.at(r.ptr_params[p]).data;
-      if (ref.status == interp::ExecStatus::Normal) r.fin[t * nP + p] = ref.final.regions.at(r.ptr_params[p]).data;
+      if (ref.status == interp::ExecStatus::Normal) {
+        r.fin[t * nP + p] = ref.final.regions.at(r.ptr_params[p]).data;
+        const auto& a = r.init[t * nP + p];
+        const auto& b = r.fin[t * nP + p];
+        for (size_t i = 0; i < a.size() && i < b.size(); ++i)
+          if (std::memcmp(&a[i], &b[i], sizeof(double)) != 0) {  // bitwise: -0.0 / NaN entries travel too
+            dpos[t * nP + p].push_back((int32_t)i);
+            dval[t * nP + p].push_back(b[i]);
+          }
+      }
     }
     r.test_ok[t] = ref.status == interp::ExecStatus::Normal;
+    if (!r.test_ok[t]) r.test_detail[t] = std::string("original run ended ") + interp::status_name(ref.status);
   };
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   const int workers = (int)std::min<unsigned>(hw, (unsigned)tests);
@@ -109,6 +125,12 @@ RecordedTests record_tests(const minilang::Program& prog, const std::string& fun
       for (int t = next.fetch_add(1); t < tests; t = next.fetch_add(1)) record_one(t);
     });
   for (auto& th : pool) th.join();
+  r.diff_off.assign(1, 0);
+  for (size_t i = 0; i < dpos.size(); ++i) {
+    r.diff_pos.insert(r.diff_pos.end(), dpos[i].begin(), dpos[i].end());
+    r.diff_val.insert(r.diff_val.end(), dval[i].begin(), dval[i].end());
+    r.diff_off.push_back((int64_t)r.diff_pos.size());
+  }
   // probe regions are kProbeRegionLen (analysis.cpp:23) long for every pointer
   for (size_t p = 0; p < nP; ++p)
     for (int t = 0; t < tests; ++t)
@@ -116,11 +138,100 @@ RecordedTests record_tests(const minilang::Program& prog, const std::string& fun
   return r;
 }
 
+namespace {
+
+// Uploads r (the needed region prefixes + final-minus-init entries when the diffs
+// were recorded, else the full regions) and returns the handle.
+atc_testset_handle* upload(atc_ctx* ctx, const RecordedTests& r) {
+  const size_t nP = r.ptr_params.size();
+  atc_testset_handle* h = nullptr;
+  int rc;
+  if (!r.diff_off.empty()) {
+    std::vector<const double*> ip(r.init.size());
+    for (size_t i = 0; i < r.init.size(); ++i) ip[i] = r.test_ok[i / nP] ? r.init[i].data() : nullptr;
+    atc_prefix_testsets px{r.T,
+                           (int32_t)r.int_params.size(),
+                           (int32_t)nP,
+                           r.ints.data(),
+                           r.is_f32.data(),
+                           r.region_len.data(),
+                           r.test_ok.data(),
+                           ip.data(),
+                           r.diff_off.data(),
+                           r.diff_pos.data(),
+                           r.diff_val.data()};
+    rc = atc_testsets_upload_prefix(ctx, &px, &h);
+  } else {
+    std::vector<const double*> ip(r.init.size()), fp(r.fin.size());
+    for (size_t i = 0; i < r.init.size(); ++i) {
+      ip[i] = r.init[i].data();
+      fp[i] = r.fin[i].empty() ? nullptr : r.fin[i].data();
+    }
+    atc_testsets ts{r.T, (int32_t)r.int_params.size(), (int32_t)nP, r.ints.data(), r.is_f32.data(),
+                    r.region_len.data(), ip.data(), fp.data(), r.test_ok.data()};
+    rc = atc_testsets_upload(ctx, &ts, &h);
+  }
+  if (rc != ATC_OK) throw std::runtime_error(atc_last_error(ctx));
+  return h;
+}
+
+}  // namespace
+
+std::vector<SpecVerdicts> p2_verdicts(atc_ctx* ctx, const RecordedTests& r,
+                                      const std::vector<const api::ApiSpec*>& specs,
+                                      const std::vector<const std::vector<matching::CandidateBinding>*>& lists) {
+  std::vector<SpecVerdicts> out(specs.size());
+  std::vector<atc_spec_desc> descs(specs.size());
+  std::vector<std::vector<uint8_t>> am(specs.size()), sm(specs.size());
+  std::vector<atc_bind_job> jobs;
+  size_t total = 0;
+  for (size_t i = 0; i < specs.size(); ++i) total += lists[i]->size();
+  if (total == 0) return out;
+  atc_testset_handle* h = upload(ctx, r);
+  for (size_t i = 0; i < specs.size(); ++i) {
+    const auto& ranked = *lists[i];
+    descs[i] = encode_spec(*specs[i]);
+    const auto arrays = specs[i]->arrays();
+    const auto sizes = specs[i]->size_params();
+    am[i].resize(ranked.size() * arrays.size());
+    sm[i].resize(ranked.size() * sizes.size());
+    for (size_t b = 0; b < ranked.size(); ++b) {
+      for (size_t a = 0; a < arrays.size(); ++a) {
+        const std::string& u = ranked[b].arrays.at(arrays[a]->name);
+        am[i][b * arrays.size() + a] =
+            (uint8_t)(std::find(r.ptr_params.begin(), r.ptr_params.end(), u) - r.ptr_params.begin());
+      }
+      for (size_t q = 0; q < sizes.size(); ++q) {
+        const std::string& u = ranked[b].sizes.at(sizes[q]->name);
+        sm[i][b * sizes.size() + q] =
+            (uint8_t)(std::find(r.int_params.begin(), r.int_params.end(), u) - r.int_params.begin());
+      }
+    }
+    out[i].fail_t.resize(ranked.size());
+    out[i].reason.resize(ranked.size());
+    if (ranked.empty()) continue;
+    atc_bind_job j{};
+    j.spec = &descs[i];
+    j.ts = h;
+    j.arr_map = am[i].data();
+    j.size_map = sm[i].data();
+    j.n_bindings = (int64_t)ranked.size();
+    j.fail_t = out[i].fail_t.data();
+    j.reason = out[i].reason.data();
+    jobs.push_back(j);
+  }
+  const int rc = atc_eval_bindings_many(ctx, jobs.data(), (int32_t)jobs.size(), ATC_MODE_FP64);
+  const std::string err = rc != ATC_OK ? atc_last_error(ctx) : "";
+  atc_testsets_free(ctx, h);
+  if (rc != ATC_OK) throw std::runtime_error(err);
+  return out;
+}
+
 LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const analysis::AnalyzedFunction& fn,
                           const std::string& function, const api::ApiSpec& spec,
                           const std::vector<matching::CandidateBinding>& ranked, const api::SizeRules& rules,
                           uint64_t fseed, int p1_tests, int verify_tests, const RecordedTests* recorded,
-                          bool report_parity) {
+                          bool report_parity, const SpecVerdicts* p2) {
   LoopResult out;
   if (ranked.empty()) return out;
   auto t0 = std::chrono::steady_clock::now();
@@ -131,39 +242,16 @@ LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const ana
   }
   out.record_ms = ms_since(t0);
   const RecordedTests& r = *recorded;
-  const size_t nP = r.ptr_params.size();
 
   t0 = std::chrono::steady_clock::now();
-  std::vector<const double*> ip(r.init.size()), fp(r.fin.size());
-  for (size_t i = 0; i < r.init.size(); ++i) {
-    ip[i] = r.init[i].data();
-    fp[i] = r.fin[i].empty() ? nullptr : r.fin[i].data();
+  if (p2) {
+    out.p2_fail_t = p2->fail_t;
+    out.p2_reason = p2->reason;
+  } else {
+    auto v = p2_verdicts(ctx, r, {&spec}, {&ranked});
+    out.p2_fail_t = std::move(v[0].fail_t);
+    out.p2_reason = std::move(v[0].reason);
   }
-  atc_testsets ts{r.T, (int32_t)r.int_params.size(), (int32_t)nP, r.ints.data(), r.is_f32.data(),
-                  r.region_len.data(), ip.data(), fp.data(), r.test_ok.data()};
-  atc_testset_handle* h = nullptr;
-  if (atc_testsets_upload(ctx, &ts, &h) != ATC_OK) throw std::runtime_error(atc_last_error(ctx));
-  const atc_spec_desc desc = encode_spec(spec);
-  const auto arrays = spec.arrays();
-  const auto sizes = spec.size_params();
-  std::vector<uint8_t> am(ranked.size() * arrays.size()), sm(ranked.size() * sizes.size());
-  for (size_t b = 0; b < ranked.size(); ++b) {
-    for (size_t a = 0; a < arrays.size(); ++a) {
-      const std::string& u = ranked[b].arrays.at(arrays[a]->name);
-      am[b * arrays.size() + a] = (uint8_t)(std::find(r.ptr_params.begin(), r.ptr_params.end(), u) - r.ptr_params.begin());
-    }
-    for (size_t q = 0; q < sizes.size(); ++q) {
-      const std::string& u = ranked[b].sizes.at(sizes[q]->name);
-      sm[b * sizes.size() + q] = (uint8_t)(std::find(r.int_params.begin(), r.int_params.end(), u) - r.int_params.begin());
-    }
-  }
-  out.p2_fail_t.resize(ranked.size());
-  out.p2_reason.resize(ranked.size());
-  int64_t first = -1;
-  int rc = atc_eval_bindings(ctx, &desc, h, am.data(), sm.data(), (int64_t)ranked.size(), ATC_MODE_FP64,
-                             out.p2_fail_t.data(), out.p2_reason.data(), &first);
-  atc_testsets_free(ctx, h);
-  if (rc != ATC_OK) throw std::runtime_error(atc_last_error(ctx));
   out.gpu_ms = ms_since(t0);
 
   // P1 on P2 survivors in rank order (pipeline.cpp:257-261 + :271-307).  With
@@ -191,6 +279,23 @@ LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const ana
   }
   out.p1_ms = ms_since(t0);
   return out;
+}
+
+std::string dispatch_error_text(const api::ApiSpec& spec, const std::string& abi_msg) {
+  // atc_dispatch names params by index (the C descriptor carries no names)
+  int idx = -1;
+  long long have = 0, need = 0;
+  const auto sizes = spec.size_params();
+  const auto arrays = spec.arrays();
+  if (std::sscanf(abi_msg.c_str(), "dispatch size #%d is not positive", &idx) == 1 && idx >= 0 &&
+      (size_t)idx < sizes.size())
+    return "dispatch size '" + sizes[idx]->name + "' is not positive";  // rewriter.cpp:141
+  if (std::sscanf(abi_msg.c_str(), "region bound to array #%d holds %lld elements, call needs %lld", &idx, &have,
+                  &need) == 3 &&
+      idx >= 0 && (size_t)idx < arrays.size())
+    return "region bound to '" + arrays[idx]->name + "' holds " + std::to_string(have) +  // :145-147
+           " elements, call needs " + std::to_string(need);
+  return abi_msg;
 }
 
 namespace {
@@ -245,10 +350,7 @@ void exact_dispatch(const api::ApiSpec& spec, const atc_spec_desc& desc, atc_ctx
     f32.push_back(mem.regions.at(d.regions[a]).elem == minilang::ScalarType::F32);
   }
   int rc = atc_dispatch(ctx, &desc, d.sizes.data(), ptrs.data(), lens.data(), f32.data());
-  if (rc == ATC_ERR_DISPATCH) {
-    // same wording as rewriter.cpp:141,145-147 ("... is not positive", "... elements ...")
-    throw std::runtime_error(std::string("dispatch: ") + atc_last_error(ctx));
-  }
+  if (rc == ATC_ERR_DISPATCH) throw std::runtime_error(dispatch_error_text(spec, atc_last_error(ctx)));
   if (rc != ATC_OK) throw std::runtime_error(atc_last_error(ctx));
   const auto arrays = spec.arrays();
   for (size_t a = 0; a < arrays.size(); ++a)
@@ -344,6 +446,183 @@ bool tensor_dispatch(const api::ApiSpec& spec, atc_ctx* ctx, int32_t precision, 
 }
 
 }  // namespace
+
+std::string p2_detail(atc_ctx* ctx, const RecordedTests& r, const minilang::FunctionIR& f,
+                      const api::ApiSpec& spec, const matching::CandidateBinding& b, int t, int reason) {
+  if (reason == ATC_FAIL_TESTSET) return r.test_detail[t];
+  if (reason == ATC_FAIL_UB) return "access outside a region at test " + std::to_string(t);  // no reference text (UB)
+  const size_t nP = r.ptr_params.size(), nI = r.int_params.size();
+  auto ptr_index = [&](const std::string& u) {
+    return (size_t)(std::find(r.ptr_params.begin(), r.ptr_params.end(), u) - r.ptr_params.begin());
+  };
+  const auto arrays = spec.arrays();
+  const auto sizes = spec.size_params();
+  std::vector<int64_t> sz(sizes.size());
+  for (size_t q = 0; q < sizes.size(); ++q) {
+    const std::string& u = b.sizes.at(sizes[q]->name);
+    const size_t i = (size_t)(std::find(r.int_params.begin(), r.int_params.end(), u) - r.int_params.begin());
+    sz[q] = r.ints[(size_t)t * nI + i];
+  }
+  // the lifted run is the single dispatch call of rewriter::rewrite (rewriter.cpp:80-91)
+  // on the probe image: full-region copies, run_reference, f32 write-back
+  std::vector<std::vector<double>> bufs;
+  std::vector<double*> ptrs;
+  std::vector<int64_t> lens;
+  std::vector<int32_t> f32;
+  for (const auto* ap : arrays) bufs.push_back(r.init[(size_t)t * nP + ptr_index(b.arrays.at(ap->name))]);
+  for (size_t a = 0; a < arrays.size(); ++a) {
+    ptrs.push_back(bufs[a].data());
+    lens.push_back((int64_t)bufs[a].size());
+    f32.push_back(r.is_f32[ptr_index(b.arrays.at(arrays[a]->name))]);
+  }
+  const atc_spec_desc desc = encode_spec(spec);
+  const int rc = atc_dispatch(ctx, &desc, sz.data(), ptrs.data(), lens.data(), f32.data());
+  if (rc == ATC_ERR_DISPATCH) return "dispatch failed: " + dispatch_error_text(spec, atc_last_error(ctx));
+  if (rc != ATC_OK) throw std::runtime_error(atc_last_error(ctx));
+  // rewriter.cpp:264-279: bound arrays in binding order, LiveIn skipped, full regions
+  for (const auto& [api_arr, user_arr] : b.arrays) {
+    const api::ApiParam* ap = spec.find(api_arr);
+    if (!ap || ap->liveness == api::Liveness::LiveIn) continue;
+    size_t a = 0;
+    while (a < arrays.size() && arrays[a]->name != api_arr) ++a;
+    const auto& want = r.fin[(size_t)t * nP + ptr_index(user_arr)];
+    const auto& have = bufs[a];
+    const bool is32 = f.find_param(user_arr)->elem == minilang::ScalarType::F32;
+    const double rel = is32 ? 1e-4 : 1e-9, abs = is32 ? 1e-6 : 1e-12;
+    for (size_t i = 0; i < want.size(); ++i)
+      if (std::fabs(have[i] - want[i]) > abs + rel * std::fabs(want[i]))
+        return "mismatch on " + user_arr + "[" + std::to_string(i) + "]: original " + std::to_string(want[i]) +
+               ", lifted " + std::to_string(have[i]);
+  }
+  return "";  // the GPU and this recomputation disagree: never expected
+}
+
+CandidateLoop candidate_loop(atc_ctx* ctx, const minilang::Program& prog, const analysis::AnalyzedFunction& fn,
+                             const std::string& function, const std::vector<const api::ApiSpec*>& specs,
+                             const api::SizeRules& rules, uint64_t fseed, const LoopConfig& cfg,
+                             std::chrono::steady_clock::time_point start) {
+  CandidateLoop out;
+  const auto t_all = std::chrono::steady_clock::now();
+  const minilang::FunctionIR* f = prog.find(function);
+  if (!f) throw std::invalid_argument("no function " + function);
+  // matching + ranking per spec (pipeline.cpp:228-240), all up front: their P2
+  // verdicts come from one batched GPU evaluation
+  std::vector<matching::RankResult> ranked(specs.size());
+  std::vector<pipeline::SpecCandidates> sc(specs.size());
+  const size_t user_ptrs = fn.arrays.size();
+  for (size_t s = 0; s < specs.size(); ++s) {
+    sc[s].api = specs[s]->name;
+    sc[s].raw = matching::raw_candidate_count(user_ptrs, specs[s]->arrays().size(), fn.int_params.size(),
+                                              specs[s]->size_params().size());
+    auto found = matching::find_matchings(fn, *specs[s]);
+    sc[s].filtered = found.size();
+    ranked[s] = matching::rank_candidates(std::move(found), cfg.max_candidates);
+    sc[s].kept = ranked[s].ranked.size();
+    sc[s].truncated = ranked[s].truncated;
+    for (size_t i = 0; i < ranked[s].ranked.size() && i < 10; ++i) sc[s].top.push_back(ranked[s].ranked[i]);
+  }
+  std::vector<const api::ApiSpec*> eval_specs;
+  std::vector<const std::vector<matching::CandidateBinding>*> lists;
+  std::vector<int> slot(specs.size(), -1);
+  for (size_t s = 0; s < specs.size(); ++s)
+    if (!ranked[s].truncated && !ranked[s].ranked.empty()) {
+      slot[s] = (int)eval_specs.size();
+      eval_specs.push_back(specs[s]);
+      lists.push_back(&ranked[s].ranked);
+    }
+  RecordedTests rec;
+  std::vector<SpecVerdicts> p2;
+  if (!eval_specs.empty()) {
+    auto t0 = std::chrono::steady_clock::now();
+    rec = record_tests(prog, function, rules, Rng::mix(fseed, "post"), cfg.verify_tests);  // pipeline.cpp:277
+    out.record_ms = ms_since(t0);
+    t0 = std::chrono::steady_clock::now();
+    p2 = p2_verdicts(ctx, rec, eval_specs, lists);
+    out.gpu_ms = ms_since(t0);
+  }
+  // pipeline.cpp:241-309
+  bool too_many = false;
+  const auto t_p1 = std::chrono::steady_clock::now();
+  for (size_t s = 0; s < specs.size(); ++s) {
+    out.by_spec.push_back(sc[s]);
+    if (ranked[s].truncated) {
+      too_many = true;
+      continue;
+    }
+    const auto& list = ranked[s].ranked;
+    for (size_t i = 0; i < list.size(); ++i) {
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count() > cfg.budget_sec) {
+        too_many = true;
+        out.status_detail = "per-function budget exhausted";
+        break;
+      }
+      const auto& cand = list[i];
+      const bool p2_ok = p2[slot[s]].reason[i] == ATC_PASS;
+      if (!p2_ok && !cfg.report) continue;  // P1 cannot make it the winner
+      const auto t0 = std::chrono::steady_clock::now();
+      equivalence::EquivalenceConfig ec;
+      ec.tests = cfg.tests;
+      ec.seed = fseed;
+      auto er = equivalence::check_equivalence(prog, fn, cand, *specs[s], rules, ec);
+      ++out.p1_calls;
+      pipeline::CandidateOutcome co;
+      co.api = specs[s]->name;
+      co.rank = (int)i;
+      co.binding = cand;
+      co.verdict = equivalence::verdict_name(er.verdict);
+      co.detail = er.detail;
+      co.equiv_ms = ms_since(t0);
+      if (er.verdict == equivalence::Verdict::Equivalent) {
+        try {
+          out.rewrite = rewriter::rewrite(prog, function, cand, *specs[s]);
+        } catch (const std::exception& e) {
+          co.verdict = "VerificationFailed";
+          co.detail = std::string("rewrite: ") + e.what();
+          out.evaluated.push_back(std::move(co));
+          continue;
+        }
+        if (!out.rewrite.manifest.warnings.empty()) {
+          // rewrite skipped (already a single dispatch call, rewriter.cpp:75-79): the
+          // "lifted" program is the original, so P2 is the reference's own check of it
+          auto vr = rewriter::verify_rewrite(prog, out.rewrite.program, function, cand, *specs[s], rules,
+                                             Rng::mix(fseed, "post"), cfg.verify_tests);
+          if (!vr.ok) {
+            co.verdict = "VerificationFailed";
+            co.detail = vr.detail;
+            out.evaluated.push_back(std::move(co));
+            continue;
+          }
+        } else if (!p2_ok) {
+          co.verdict = "VerificationFailed";
+          co.detail = p2_detail(ctx, rec, *f, *specs[s], cand, p2[slot[s]].fail_t[i], p2[slot[s]].reason[i]);
+          out.evaluated.push_back(std::move(co));
+          continue;
+        }
+        out.status = pipeline::FunctionStatus::Lifted;
+        out.winning_spec = specs[s];
+        out.winner_rank = (int)i;
+        out.evaluated.push_back(std::move(co));
+        break;
+      }
+      out.evaluated.push_back(std::move(co));
+    }
+    if (out.status == pipeline::FunctionStatus::Lifted || too_many) break;
+  }
+  out.p1_ms = ms_since(t_p1);
+  // pipeline.cpp:318-329
+  if (out.status != pipeline::FunctionStatus::Lifted) {
+    if (too_many) {
+      out.status = pipeline::FunctionStatus::TooManyCandidates;
+      if (out.status_detail.empty()) out.status_detail = "candidate cap exceeded";
+    } else {
+      bool any_filtered = false;
+      for (const auto& b : out.by_spec) any_filtered |= b.filtered > 0;
+      out.status_detail = any_filtered ? "no candidate proved equivalent" : "no candidate passed the constraints";
+    }
+  }
+  out.total_ms = ms_since(t_all);
+  return out;
+}
 
 interp::DispatchContext make_gpu_dispatch(const api::ApiSpec& spec, atc_ctx* ctx) {
   interp::DispatchContext dc;

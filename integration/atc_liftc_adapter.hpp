@@ -17,6 +17,7 @@
 // with the reference's own functions.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <map>
 #include <optional>
@@ -29,7 +30,9 @@
 #include "liftc/interp.hpp"
 #include "liftc/matching.hpp"
 #include "liftc/minilang.hpp"
+#include "liftc/pipeline.hpp"
 #include "liftc/profitability.hpp"
+#include "liftc/rewriter.hpp"
 
 namespace liftc::gpu {
 
@@ -45,6 +48,15 @@ struct RecordedTests {
   std::vector<int64_t> region_len;            // [nP]
   std::vector<std::vector<double>> init, fin;  // [T*nP]
   int T = 0;
+  // The original run's final-minus-init entries per (t, p) (positions and final
+  // values): with them the upload sends only the region prefixes an evaluation
+  // can read (atc_testsets_upload_prefix) and rebuilds the finals on the device.
+  std::vector<int64_t> diff_off;  // [T*nP + 1]
+  std::vector<int32_t> diff_pos;
+  std::vector<double> diff_val;
+  // verify_rewrite's detail for a test whose draw or original run failed
+  // (rewriter.cpp:241-251); empty when test_ok[t]
+  std::vector<std::string> test_detail;  // [T]
 };
 RecordedTests record_tests(const minilang::Program& prog, const std::string& function,
                            const api::SizeRules& rules, uint64_t p2seed, int tests);
@@ -59,11 +71,67 @@ struct LoopResult {
 
 // Replacement of pipeline.cpp:248-310 for one spec: P2 (GPU, batched) for all
 // ranked candidates, then P1 (host) on the survivors in rank order.
+// The P2 verdicts of every spec's ranked list of one function from ONE test-set
+// upload (atc_testsets_upload_prefix: needed-only region prefixes) and ONE batched
+// evaluation (atc_eval_bindings_many): lists[i] are the ranked candidates of
+// specs[i].  fail_t/reason are filled per spec, in rank order.
+struct SpecVerdicts {
+  std::vector<int8_t> fail_t, reason;
+};
+std::vector<SpecVerdicts> p2_verdicts(atc_ctx* ctx, const RecordedTests& r,
+                                      const std::vector<const api::ApiSpec*>& specs,
+                                      const std::vector<const std::vector<matching::CandidateBinding>*>& lists);
+
 LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const analysis::AnalyzedFunction& fn,
                           const std::string& function, const api::ApiSpec& spec,
                           const std::vector<matching::CandidateBinding>& ranked, const api::SizeRules& rules,
                           uint64_t fseed, int p1_tests, int verify_tests, const RecordedTests* recorded = nullptr,
-                          bool report_parity = false);
+                          bool report_parity = false, const SpecVerdicts* p2 = nullptr);
+
+// run_dispatch's exception text (rewriter.cpp:141, :145-147) for an
+// ATC_ERR_DISPATCH message of atc_dispatch, which names params by index.
+std::string dispatch_error_text(const api::ApiSpec& spec, const std::string& abi_msg);
+
+// verify_rewrite's failure detail (rewriter.cpp:238-279) for binding `b` that the
+// GPU rejected at test t with `reason` (ATC_FAIL_*): the test-set failure text,
+// "dispatch failed: " + run_dispatch's message, or the first mismatching element
+// of the compared arrays in the reference's order ("mismatch on X[i]: original
+// ..., lifted ...") — recomputed for that one (binding, t) with atc_dispatch on
+// the recorded probe image.
+std::string p2_detail(atc_ctx* ctx, const RecordedTests& r, const minilang::FunctionIR& f,
+                      const api::ApiSpec& spec, const matching::CandidateBinding& b, int t, int reason);
+
+// The whole candidate stage of pipeline::lift_function (pipeline.cpp:223-330):
+// every spec's matching + ranking (host, unchanged), ONE recording of the P2 test
+// sets, ONE GPU P2 evaluation of every spec's ranked list, then the reference's
+// control flow — specs in order, truncated specs skipped (too_many), candidates
+// in rank order under the time budget, P1 (host check_equivalence) and, for an
+// Equivalent candidate, rewrite + the GPU's P2 verdict — so status, winner,
+// by_spec and evaluated[] (verdicts and details) equal the reference's.  With
+// cfg.report = false, P1 runs only on P2 survivors (same winner, fewer P1 calls,
+// evaluated[] lists only the candidates P1 ran on).
+struct LoopConfig {
+  int tests = 30;              // PipelineConfig::tests (P1)
+  int verify_tests = 10;       // PipelineConfig::verify_tests (P2)
+  size_t max_candidates = 100;
+  double budget_sec = 600.0;
+  bool report = true;
+};
+struct CandidateLoop {
+  pipeline::FunctionStatus status = pipeline::FunctionStatus::NoMatch;
+  std::string status_detail;
+  const api::ApiSpec* winning_spec = nullptr;
+  int winner_rank = -1;
+  rewriter::RewriteResult rewrite;  // the winner's (manifest: arrays/sizes/scalars)
+  std::vector<pipeline::SpecCandidates> by_spec;
+  std::vector<pipeline::CandidateOutcome> evaluated;
+  int p1_calls = 0;
+  double record_ms = 0.0, gpu_ms = 0.0, p1_ms = 0.0, total_ms = 0.0;
+};
+CandidateLoop candidate_loop(atc_ctx* ctx, const minilang::Program& prog, const analysis::AnalyzedFunction& fn,
+                             const std::string& function, const std::vector<const api::ApiSpec*>& specs,
+                             const api::SizeRules& rules, uint64_t fseed, const LoopConfig& cfg,
+                             std::chrono::steady_clock::time_point start = std::chrono::steady_clock::now());
 
 // DispatchContext whose handler is run_dispatch on the GPU (atc_dispatch).
 interp::DispatchContext make_gpu_dispatch(const api::ApiSpec& spec, atc_ctx* ctx);

@@ -91,6 +91,24 @@ class SeededTestsets(C.Structure):
     ]
 
 
+class PrefixTestsets(C.Structure):
+    """atc_prefix_testsets (include/atc_b200.h)."""
+
+    _fields_ = [
+        ("n_tests", C.c_int32),
+        ("n_ints", C.c_int32),
+        ("n_ptrs", C.c_int32),
+        ("int_values", C.c_void_p),
+        ("ptr_is_f32", C.c_void_p),
+        ("region_len", C.c_void_p),
+        ("test_ok", C.c_void_p),
+        ("init", C.c_void_p),
+        ("diff_off", C.c_void_p),
+        ("diff_pos", C.c_void_p),
+        ("diff_val", C.c_void_p),
+    ]
+
+
 class Profile(C.Structure):
     _fields_ = [
         ("screen_ms", C.c_double),
@@ -121,6 +139,22 @@ class EnumJob(C.Structure):
     ]
 
 
+class BindJob(C.Structure):
+    """atc_bind_job (include/atc_b200.h)."""
+
+    _fields_ = [
+        ("spec", C.c_void_p),
+        ("ts", C.c_void_p),
+        ("arr_map", C.c_void_p),
+        ("size_map", C.c_void_p),
+        ("n_bindings", C.c_int64),
+        ("fail_t", C.c_void_p),
+        ("reason", C.c_void_p),
+        ("first_pass", C.c_int64),
+        ("status", C.c_int32),
+    ]
+
+
 # (name, restype, argtypes) for every function declared in include/atc_b200.h
 _P = C.c_void_p
 _SIGS = [
@@ -136,11 +170,13 @@ _SIGS = [
     ("atc_testsets_free", C.c_int, [_P, _P]),
     ("atc_testsets_upload_async", C.c_int, [_P, C.POINTER(Testsets), C.POINTER(_P)]),
     ("atc_testsets_upload_seeded", C.c_int, [_P, C.POINTER(SeededTestsets), C.POINTER(_P)]),
+    ("atc_testsets_upload_prefix", C.c_int, [_P, C.POINTER(PrefixTestsets), C.POINTER(_P)]),
     ("atc_testsets_update_seeded", C.c_int, [_P, _P, C.POINTER(SeededTestsets)]),
     ("atc_testsets_update_seeded_many", C.c_int, [_P, _P, C.POINTER(SeededTestsets), C.c_int32]),
     ("atc_testsets_download", C.c_int, [_P, _P, _P, _P]),
     ("atc_eval_bindings", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, C.c_int64, C.c_int32, _P, _P,
                                     C.POINTER(C.c_int64)]),
+    ("atc_eval_bindings_many", C.c_int, [_P, C.POINTER(BindJob), C.c_int32, C.c_int32]),
     ("atc_eval_bindings_device", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, C.c_int64, C.c_int32, _P, _P, _P]),
     ("atc_eval_enumerated", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, C.c_int32, C.c_uint64, C.c_uint64, C.c_int32,
                                       _P, C.c_int64, C.POINTER(C.c_int64), _P]),

@@ -20,7 +20,7 @@ namespace atc {
 __global__ void k_probe_regions(int T, int nP, const uint64_t* seeds, const uint64_t* skips, const int64_t* region_len,
                                 const int32_t* is_f32, const int64_t* region_off, const int64_t* need, double* init,
                                 double* fin, TestsetView v, const int64_t* diff_off, const int32_t* diff_pos,
-                                const double* diff_val);
+                                const double* diff_val, const double* pre, const int64_t* pre_off);
 __global__ void k_apply_diffs(int nP, const int64_t* region_len, const int64_t* region_off, const int64_t* diff_off,
                               const int32_t* diff_pos, const double* diff_val, double* fin);
 __global__ void k_build_dirty(TestsetView ts, int32_t* dirty_pos, int32_t* dirty_cnt, int32_t* dirty_max);
@@ -384,9 +384,31 @@ int atc_profile_read(atc_ctx* ctx, atc_profile* out) {
 // Fills an allocated handle from full host regions (`ts_full`) or from seeds +
 // final-minus-init entries (`sd`, regions generated on the device), on the
 // handle's copy stream, and records its ready event.
+// needed_only bound of region (t, p): max(U^4 + 2U^2 + 2U + 1, last final-minus-init
+// position + 1), U = test t's largest int (include/atc_b200.h), capped at the region
+// length; the whole region without needed_only.
+static std::vector<int64_t> region_need(const atc_testset_handle* h, const atc_seeded_testsets* sd) {
+  const int T = h->T, nI = h->nI, nP = h->nP;
+  std::vector<int64_t> need((size_t)T * nP);
+  for (int t = 0; t < T; ++t) {
+    int64_t u = 1;
+    for (int q = 0; q < nI; ++q) u = std::max<int64_t>(u, sd->int_values[(size_t)t * nI + q]);
+    const int64_t bound = u > 46340 ? INT64_MAX : u * u * u * u + 2 * u * u + 2 * u + 1;
+    for (int p = 0; p < nP; ++p) {
+      const size_t i = (size_t)t * nP + p;
+      int64_t n = bound;
+      for (int64_t e = sd->diff_off[i]; e < sd->diff_off[i + 1]; ++e) n = std::max<int64_t>(n, sd->diff_pos[e] + 1);
+      need[i] = sd->needed_only ? std::min<int64_t>(n, h->lens[p]) : h->lens[p];
+    }
+  }
+  return need;
+}
+
+// pre (optional, with sd): the caller's own init regions [T*nP] — only their needed
+// prefixes are staged and copied, instead of generating them from the seeds.
 static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets* ts_full,
                          const atc_seeded_testsets* sd, bool sync, bool pinned_staging = false,
-                         cudaEvent_t reuse = nullptr) {
+                         cudaEvent_t reuse = nullptr, const double* const* pre = nullptr) {
   const int T = h->T, nI = h->nI, nP = h->nP;
   const size_t TP = (size_t)T * nP;
   const int64_t* int_values = ts_full ? ts_full->int_values : sd->int_values;
@@ -395,9 +417,18 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
   // every small array in one block, built in pinned staging and copied once; the
   // seeded block follows it in the same staging buffer
   const int64_t nd_s = sd ? sd->diff_off[TP] : 0;
+  std::vector<int64_t> need = sd ? region_need(h, sd) : std::vector<int64_t>();
+  if (pre)  // a failed test has no region: every binding fails there (reason 3), nothing to stage
+    for (size_t i = 0; i < TP; ++i)
+      if (!pre[i] || (test_ok && !test_ok[i / nP])) need[i] = 0;
+  std::vector<int64_t> pre_off(pre ? TP + 1 : 0, 0);
+  for (size_t i = 0; pre && i < TP; ++i)
+    pre_off[i + 1] = pre_off[i] + need[i];
+  const size_t pre_bytes = pre ? ((size_t)pre_off[TP] * 8 + 15) / 16 * 16 + ((TP + 1) * 8 + 15) / 16 * 16 : 0;
   const size_t seeded_need =
       sd ? ((size_t)T * 8 + 15) / 16 * 16 + (TP * 8 + 15) / 16 * 16 + ((TP + 1) * 8 + 15) / 16 * 16 +
-               ((size_t)nd_s * 8 + 15) / 16 * 16 + ((size_t)nd_s * 4 + 15) / 16 * 16 + (TP * 8 + 15) / 16 * 16
+               ((size_t)nd_s * 8 + 15) / 16 * 16 + ((size_t)nd_s * 4 + 15) / 16 * 16 + (TP * 8 + 15) / 16 * 16 +
+               pre_bytes
          : 0;
   // in-place updates stage through the handle's pinned buffer (true async DMA,
   // allocated once); a first upload stages through pageable memory (the driver
@@ -510,20 +541,7 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
     };
     const size_t o_seeds = take((size_t)T * 8), o_skips = take(TP * 8), o_doffs = take((TP + 1) * 8),
                  o_dvs = take((size_t)nd * 8), o_dps = take((size_t)nd * 4), o_need = take(TP * 8);
-    // needed_only: region (t, p) up to max(U^4 + 2U^2 + 2U + 1, last final-minus-init
-    // position + 1), U = test t's largest int (include/atc_b200.h); else whole regions
-    std::vector<int64_t> need(TP);
-    for (int t = 0; t < T; ++t) {
-      int64_t u = 1;
-      for (int q = 0; q < nI; ++q) u = std::max<int64_t>(u, sd->int_values[(size_t)t * nI + q]);
-      const int64_t bound = u > 46340 ? INT64_MAX : u * u * u * u + 2 * u * u + 2 * u + 1;
-      for (int p = 0; p < nP; ++p) {
-        const size_t i = (size_t)t * nP + p;
-        int64_t n = bound;
-        for (int64_t e = sd->diff_off[i]; e < sd->diff_off[i + 1]; ++e) n = std::max<int64_t>(n, sd->diff_pos[e] + 1);
-        need[i] = sd->needed_only ? std::min<int64_t>(n, h->lens[p]) : h->lens[p];
-      }
-    }
+    const size_t o_pre = pre ? take((size_t)pre_off[TP] * 8) : 0, o_preoff = pre ? take((TP + 1) * 8) : 0;
     h->needed_only = sd->needed_only != 0;
     if (ok && so > h->seeded_cap) {  // grow (the old block stays owned by the handle)
       h->seeded = (uint8_t*)atc_pool_alloc(ctx, std::max(so, (size_t)256));
@@ -544,6 +562,12 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
         std::memcpy(sb + o_dps, sd->diff_pos, (size_t)nd * 4);
       }
       std::memcpy(sb + o_need, need.data(), TP * 8);
+      if (pre) {
+        for (size_t i = 0; i < TP; ++i)
+          if (pre_off[i + 1] > pre_off[i])
+            std::memcpy(sb + o_pre + (size_t)pre_off[i] * 8, pre[i], (size_t)(pre_off[i + 1] - pre_off[i]) * 8);
+        std::memcpy(sb + o_preoff, pre_off.data(), (TP + 1) * 8);
+      }
       ok = atc_cuda_ok(ctx, cudaMemcpyAsync(h->seeded, sb, so, cudaMemcpyHostToDevice, st), "H2D seeds");
     }
     if (ok) {
@@ -554,7 +578,9 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
       k_probe_regions<<<T, 160, 0, st>>>(T, nP, (const uint64_t*)(h->seeded + o_seeds),
                                          (const uint64_t*)(h->seeded + o_skips), v.region_len, v.is_f32,
                                          v.region_off, dn, init, fin, v, (const int64_t*)(h->seeded + o_doffs),
-                                         (const int32_t*)(h->seeded + o_dps), (const double*)(h->seeded + o_dvs));
+                                         (const int32_t*)(h->seeded + o_dps), (const double*)(h->seeded + o_dvs),
+                                         pre ? (const double*)(h->seeded + o_pre) : nullptr,
+                                         pre ? (const int64_t*)(h->seeded + o_preoff) : nullptr);
       if (!dn)
         k_apply_diffs<<<(unsigned)TP, 256, 0, st>>>(nP, v.region_len, v.region_off,
                                                     (const int64_t*)(h->seeded + o_doffs),
@@ -584,7 +610,7 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
 // Both upload forms: full host regions (`ts`) or seeds + final-minus-init entries
 // (`sd`, regions generated on the device); the common header fields are equal.
 static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_seeded_testsets* sd,
-                           atc_testset_handle** out, bool sync) {
+                           atc_testset_handle** out, bool sync, const double* const* pre = nullptr) {
   if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
   atc_testsets hdr{};
   if (ts_full) hdr = *ts_full;
@@ -676,7 +702,7 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_
   v.dirty_max = (const int32_t*)(h->meta + h->o_dmax);
   h->cs = ctx->copy_next;  // round-robin over the copy streams
   ctx->copy_next = (h->cs + 1) % atc_ctx::kCopyStreams;
-  const int rc = testsets_fill(ctx, h, ts_full, sd, sync);
+  const int rc = testsets_fill(ctx, h, ts_full, sd, sync, false, nullptr, pre);
   if (rc) {
     atc_testsets_free(ctx, h);
     return rc;
@@ -697,6 +723,27 @@ int atc_testsets_upload_async(atc_ctx* ctx, const atc_testsets* ts, atc_testset_
 
 int atc_testsets_upload_seeded(atc_ctx* ctx, const atc_seeded_testsets* ts, atc_testset_handle** out) {
   return testsets_upload(ctx, nullptr, ts, out, false);
+}
+
+int atc_testsets_upload_prefix(atc_ctx* ctx, const atc_prefix_testsets* ts, atc_testset_handle** out) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (!ts || !ts->init || !ts->diff_off || ts->n_tests < 1 || ts->n_ptrs < 1 || ts->n_tests > kMaxT ||
+      ts->n_ptrs > kMaxPtrs) {
+    atc_set_error(ctx, "malformed test sets");
+    return ATC_ERR_ARG;
+  }
+  const size_t TP = (size_t)ts->n_tests * ts->n_ptrs;
+  for (size_t i = 0; i < TP; ++i)
+    if (!ts->init[i] && (!ts->test_ok || ts->test_ok[i / ts->n_ptrs])) {
+      atc_set_error(ctx, "test %d pointer %d: missing region", (int)(i / ts->n_ptrs), (int)(i % ts->n_ptrs));
+      return ATC_ERR_ARG;
+    }
+  // the seeded form's header with unused stream fields: the prefixes replace the generator
+  std::vector<uint64_t> zeros(TP, 0);
+  atc_seeded_testsets sd{ts->n_tests, ts->n_ints,   ts->n_ptrs,   ts->int_values, ts->ptr_is_f32,
+                         ts->region_len, ts->test_ok, zeros.data(), zeros.data(),  ts->diff_off,
+                         ts->diff_pos,   ts->diff_val, /*needed_only=*/1};
+  return testsets_upload(ctx, nullptr, &sd, out, false, ts->init);
 }
 
 static bool update_matches(atc_ctx* ctx, const atc_testset_handle* h, const atc_seeded_testsets* ts) {
@@ -1102,6 +1149,89 @@ int atc_eval_bindings(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset
         *first_pass = (int64_t)b;
         break;
       }
+  return ATC_OK;
+}
+
+int atc_eval_bindings_many(atc_ctx* ctx, atc_bind_job* jobs, int32_t n_jobs, int32_t mode) {
+  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs) || (mode != ATC_MODE_FP64 && mode != ATC_MODE_FP32_SCREEN)) {
+    atc_set_error(ctx, "bad arguments to atc_eval_bindings_many");
+    return ATC_ERR_ARG;
+  }
+  // validate every job and lay out one staging block: maps in, verdicts out
+  std::vector<size_t> in_off(n_jobs), out_off(n_jobs);
+  size_t in_bytes = 0, out_bytes = 0;
+  uint64_t nmax = 0;
+  int first_rc = ATC_OK;
+  for (int j = 0; j < n_jobs; ++j) {
+    atc_bind_job& jb = jobs[j];
+    jb.first_pass = -1;
+    jb.status = ATC_OK;
+    SpecView sp;
+    if (!jb.ts || jb.n_bindings < 0 ||
+        (jb.n_bindings > 0 && (!jb.arr_map || !jb.size_map || !jb.fail_t || !jb.reason))) {
+      atc_set_error(ctx, "bad arguments to atc_eval_bindings_many (job %d)", j);
+      jb.status = ATC_ERR_ARG;
+    } else if (!build_spec_view(ctx, jb.spec, sp)) {
+      jb.status = ATC_ERR_ARG;
+    }
+    if (jb.status != ATC_OK) {
+      if (first_rc == ATC_OK) first_rc = jb.status;
+      continue;
+    }
+    in_off[j] = in_bytes;
+    out_off[j] = out_bytes;
+    in_bytes += ((size_t)jb.n_bindings * (sp.nA + sp.nS) + 15) / 16 * 16;
+    out_bytes += ((size_t)jb.n_bindings * 2 + 15) / 16 * 16;
+    nmax = std::max<uint64_t>(nmax, (uint64_t)jb.n_bindings);
+  }
+  if (first_rc != ATC_OK || in_bytes == 0) return first_rc;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  // scratch sized once for the largest list (run_eval's slots), so no buffer is
+  // reallocated while an earlier list's kernels are queued
+  uint8_t* pin = (uint8_t*)atc_ctx_pinned(ctx, 2, in_bytes + out_bytes);
+  uint8_t* d_in = (uint8_t*)atc_ctx_scratch(ctx, 4, in_bytes);
+  int8_t* d_out = (int8_t*)atc_ctx_scratch(ctx, 5, out_bytes);
+  if (!pin || !d_in || !d_out || !atc_ctx_scratch(ctx, 0, nmax * 4) || !atc_ctx_scratch(ctx, 1, nmax * 8) ||
+      !atc_ctx_scratch(ctx, 2, nmax * 4) || !atc_ctx_scratch(ctx, 3, 64) ||
+      !atc_ctx_scratch(ctx, 18, nmax * 4 + 16) || !atc_ctx_scratch(ctx, 19, 64) ||
+      !atc_ctx_scratch(ctx, 24, nmax * 4 + 16)) {
+    atc_set_error(ctx, "scratch allocation failed");
+    return ATC_ERR_CUDA;
+  }
+  for (int j = 0; j < n_jobs; ++j) {
+    const atc_bind_job& jb = jobs[j];
+    const size_t n = (size_t)jb.n_bindings;
+    std::memcpy(pin + in_off[j], jb.arr_map, n * jb.spec->n_arrays);
+    std::memcpy(pin + in_off[j] + n * jb.spec->n_arrays, jb.size_map, n * jb.spec->n_sizes);
+  }
+  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(d_in, pin, in_bytes, cudaMemcpyHostToDevice, st), "H2D maps"))
+    return ATC_ERR_CUDA;
+  for (int j = 0; j < n_jobs; ++j) {
+    atc_bind_job& jb = jobs[j];
+    if (jb.n_bindings == 0) continue;
+    const size_t n = (size_t)jb.n_bindings;
+    const uint8_t* am = d_in + in_off[j];
+    jb.status = atc_eval_bindings_device(ctx, jb.spec, jb.ts, am, am + n * jb.spec->n_arrays, jb.n_bindings, mode,
+                                         d_out + out_off[j], d_out + out_off[j] + n, st);
+    if (jb.status != ATC_OK) return jb.status;
+  }
+  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(pin + in_bytes, d_out, out_bytes, cudaMemcpyDeviceToHost, st), "D2H") ||
+      !atc_cuda_ok(ctx, cudaStreamSynchronize(st), "eval sync"))
+    return ATC_ERR_CUDA;
+  for (int j = 0; j < n_jobs; ++j) {
+    atc_bind_job& jb = jobs[j];
+    const size_t n = (size_t)jb.n_bindings;
+    const int8_t* o = (const int8_t*)(pin + in_bytes + out_off[j]);
+    std::memcpy(jb.fail_t, o, n);
+    std::memcpy(jb.reason, o + n, n);
+    for (size_t b = 0; b < n; ++b)
+      if (jb.reason[b] == ATC_PASS) {
+        jb.first_pass = (int64_t)b;
+        break;
+      }
+  }
   return ATC_OK;
 }
 

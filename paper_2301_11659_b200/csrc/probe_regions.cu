@@ -41,17 +41,31 @@ __device__ __forceinline__ uint64_t temper(uint64_t y) {
 // region (t, p) — the steps stop at the last of them — and then, in the same CTA,
 // scatter test t's final-minus-init entries (k_apply_diffs) and build its dirty
 // lists over those prefixes (k_build_dirty), diff_* and v's dirty arrays.
+// pre / pre_off (atc_testsets_upload_prefix): the prefixes come from the caller
+// (packed, entries [pre_off[i], pre_off[i+1]) for region i) instead of the stream.
 __global__ void __launch_bounds__(160) k_probe_regions(int T, int nP, const uint64_t* seeds, const uint64_t* skips,
                                                        const int64_t* region_len, const int32_t* is_f32,
                                                        const int64_t* region_off, const int64_t* need, double* init,
                                                        double* fin, TestsetView v, const int64_t* diff_off,
-                                                       const int32_t* diff_pos, const double* diff_val) {
+                                                       const int32_t* diff_pos, const double* diff_val,
+                                                       const double* pre, const int64_t* pre_off) {
   constexpr int kRing = 2 * kN;
   __shared__ uint64_t z[kRing];
   const int t = blockIdx.x;
   if (t >= T) return;
   const int q = threadIdx.x;
-  if (q == 0) {  // seeding: mt[i] = f * (mt[i-1] ^ (mt[i-1] >> 62)) + i
+  if (pre) {  // atc_testsets_upload_prefix: the caller's own prefixes, no generator
+    for (int p = 0; p < nP; ++p) {
+      const size_t i = (size_t)t * nP + p;
+      const double* src = pre + pre_off[i];
+      const int64_t n = pre_off[i + 1] - pre_off[i], o = region_off[i];
+      for (int64_t e = q; e < n; e += blockDim.x) {
+        const double x = src[e];
+        init[o + e] = x;
+        fin[o + e] = x;
+      }
+    }
+  } else if (q == 0) {  // seeding: mt[i] = f * (mt[i-1] ^ (mt[i-1] >> 62)) + i
     uint64_t x = seeds[t];
     z[0] = x;
     for (int i = 1; i < kN; ++i) {
@@ -61,7 +75,7 @@ __global__ void __launch_bounds__(160) k_probe_regions(int T, int nP, const uint
   }
   uint64_t lo[8], hi[8];
   uint64_t end = 0;
-  const int np = nP < 8 ? nP : 8;
+  const int np = pre ? 0 : nP < 8 ? nP : 8;
   for (int p = 0; p < np; ++p) {
     lo[p] = skips[(size_t)t * nP + p];
     hi[p] = lo[p] + (uint64_t)(need ? need[(size_t)t * nP + p] : region_len[p]);

@@ -66,12 +66,12 @@ class RecordedTestsets:
                                 seeds=None if self.seeds is None else self.seeds[:T].copy(),
                                 skips=None if self.skips is None else self.skips[:T].copy())
 
-    def seeded_struct(self, needed_only: bool = False):
+    def seeded_struct(self, needed_only: bool = False, _streams: bool = True):
         """atc_seeded_testsets: seeds + stream positions + the final-minus-init
         entries (positions where the original run's final image differs).
         needed_only: the device generates only the region prefixes an evaluation
         can read (include/atc_b200.h)."""
-        if self.seeds is None or self.skips is None:
+        if _streams and (self.seeds is None or self.skips is None):
             raise ValueError("these test sets carry no stream seeds")
         ptrs = self.ptrs
         T, nP = self.n_tests, len(ptrs)
@@ -92,8 +92,8 @@ class RecordedTestsets:
         is_f32 = np.array([1 if p.elem == "f32" else 0 for p in ptrs], dtype=np.int32)
         lens = np.array([len(self.init[0][p]) for p in range(nP)], dtype=np.int64)
         ok = np.ascontiguousarray(self.test_ok, dtype=np.int32)
-        seeds = np.ascontiguousarray(self.seeds, dtype=np.uint64)
-        skips = np.ascontiguousarray(self.skips, dtype=np.uint64)
+        seeds = np.ascontiguousarray(self.seeds if _streams else np.zeros(T), dtype=np.uint64)
+        skips = np.ascontiguousarray(self.skips if _streams else np.zeros((T, nP)), dtype=np.uint64)
         s = _lib.SeededTestsets()
         s.n_tests, s.n_ints, s.n_ptrs = T, ints.shape[1], nP
         s.int_values = ints.ctypes.data
@@ -116,6 +116,29 @@ class RecordedTestsets:
         h = _TestsetHandle(ctx, out.value)
         h.keep = keep  # host buffers stay valid until the handle is used (async upload)
         return h
+
+    def upload_prefix(self, ctx: "_lib.Context"):
+        """atc_testsets_upload_prefix: the host's own regions, of which only the
+        prefixes an evaluation can read (+ the final-minus-init entries) cross PCIe."""
+        s, keep = self.seeded_struct(needed_only=True, _streams=False)
+        ints, is_f32, lens, ok, _, _, doff, dpos, dval = keep
+        T, nP = self.n_tests, len(self.ptrs)
+        init_ptrs = (C.c_void_p * (T * nP))()
+        regions = []
+        for t in range(T):
+            for p in range(nP):
+                if ok[t]:
+                    a = np.ascontiguousarray(self.init[t][p], dtype=np.float64)
+                    regions.append(a)
+                    init_ptrs[t * nP + p] = a.ctypes.data
+        px = _lib.PrefixTestsets()
+        px.n_tests, px.n_ints, px.n_ptrs = s.n_tests, s.n_ints, s.n_ptrs
+        px.int_values, px.ptr_is_f32, px.region_len, px.test_ok = s.int_values, s.ptr_is_f32, s.region_len, s.test_ok
+        px.init = C.cast(init_ptrs, C.c_void_p)
+        px.diff_off, px.diff_pos, px.diff_val = s.diff_off, s.diff_pos, s.diff_val
+        out = C.c_void_p()
+        _lib.check(ctx.handle, _lib.lib().atc_testsets_upload_prefix(ctx.handle, C.byref(px), C.byref(out)))
+        return _TestsetHandle(ctx, out.value)
 
     def c_struct(self):
         ptrs = self.ptrs

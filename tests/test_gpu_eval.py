@@ -410,3 +410,69 @@ def test_seeded_needed_only_regions(ev, stem):
         L.check(ev.ctx.handle, L.lib().atc_testsets_download(ev.ctx.handle, C.c_void_p(h.value), buf.ctypes.data,
                                                              None))
     holder._handles.clear()
+
+
+@pytest.mark.parametrize("stem", ["conv_direct", "im2col_buffered", "naive_ld", "strassen_staged", "naive_f32",
+                                  "conv_stride2"])
+def test_prefix_upload_regions(ev, stem):
+    """atc_testsets_upload_prefix (the host's own probe images, only the needed
+    prefixes cross PCIe) gives the same verdicts as the full-region upload: full
+    spaces (or their first 2^22 bindings) and a strided explicit list."""
+    p = fixtures.load(stem)
+    ts = p.testsets(16)
+    h = ts.upload_prefix(ev.ctx)
+    holder = p.testsets(16)
+    holder._handles[id(ev.ctx)] = h
+    for sname in p.spec_names():
+        space, spec = p.space(sname), fixtures.spec(sname)
+        end = min(space.count, 1 << 22)
+        want = ev.eval_enumerated(spec, ts, space, 0, end)
+        got = ev.eval_enumerated(spec, holder, space, 0, end)
+        np.testing.assert_array_equal(got[0], want[0])
+        assert got[1] == want[1] and got[2].tolist() == want[2].tolist()
+        idx = np.arange(0, end, max(1, end // 4096), dtype=np.uint64)
+        am, sm = space.decode(idx)
+        a, b = ev.eval_bindings(spec, ts, am, sm), ev.eval_bindings(spec, holder, am, sm)
+        np.testing.assert_array_equal(a.fail_t, b.fail_t)
+        np.testing.assert_array_equal(a.reason, b.reason)
+    holder._handles.clear()
+    h.free()
+
+
+def test_eval_bindings_many_equals_single(ev):
+    """atc_eval_bindings_many over several (spec, test-set handle, list) jobs of
+    different sizes equals atc_eval_bindings on each job alone (verdicts and
+    first passing index); an empty job and a job with a malformed list are
+    reported per job."""
+    import ctypes as C
+
+    jobs, keep = [], []
+    for stem, sname, stride in (("naive_ld", "gemm_rowmajor_ld", 37), ("naive_rowmajor", "gemm_colmajor", 1),
+                                ("conv_direct", "conv2d", 1 << 20), ("naive_f32", "gemm_rowmajor", 1)):
+        p = fixtures.load(stem)
+        ts, space, spec = p.testsets(16), p.space(sname), fixtures.spec(sname)
+        idx = np.arange(0, space.count, stride, dtype=np.uint64)[:5000]
+        am, sm = space.decode(idx)
+        jobs.append((spec, ts, np.ascontiguousarray(am), np.ascontiguousarray(sm)))
+    arr = (L.BindJob * (len(jobs) + 1))()
+    for i, (spec, ts, am, sm) in enumerate(jobs):
+        n = am.shape[0]
+        ft, rs, desc = np.empty(n, np.int8), np.empty(n, np.int8), spec.to_desc()
+        keep.append((ft, rs, desc))
+        j = arr[i]
+        j.spec = C.cast(C.pointer(desc), C.c_void_p)
+        j.ts = ts.upload(ev.ctx).value
+        j.arr_map, j.size_map, j.n_bindings = am.ctypes.data, sm.ctypes.data, n
+        j.fail_t, j.reason = ft.ctypes.data, rs.ctypes.data
+    e = arr[len(jobs)]  # empty job
+    e.spec, e.ts, e.n_bindings = arr[0].spec, arr[0].ts, 0
+    L.check(ev.ctx.handle, L.lib().atc_eval_bindings_many(ev.ctx.handle, arr, len(jobs) + 1, 0))
+    for i, (spec, ts, am, sm) in enumerate(jobs):
+        want = ev.eval_bindings(spec, ts, am, sm)
+        np.testing.assert_array_equal(keep[i][0], want.fail_t)
+        np.testing.assert_array_equal(keep[i][1], want.reason)
+        assert arr[i].first_pass == want.first_pass and arr[i].status == 0
+    assert arr[len(jobs)].status == 0 and arr[len(jobs)].first_pass == -1
+    bad = (L.BindJob * 1)()
+    bad[0].spec, bad[0].ts, bad[0].n_bindings = arr[0].spec, arr[0].ts, 4  # no maps
+    assert L.lib().atc_eval_bindings_many(ev.ctx.handle, bad, 1, 0) == L.ATC_ERR_ARG and bad[0].status == L.ATC_ERR_ARG

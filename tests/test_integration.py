@@ -21,13 +21,33 @@ def _run(*args, timeout=900):
 
 
 def test_adapter_reproduces_reference_pipeline():
-    """Reference lift_program vs analysis + matching + ranking + GPU P2 batch + host
-    P1 on survivors: same status, spec, rank and binding for every corpus program."""
+    """Reference lift_program vs the adapter's candidate_loop (analysis + matching +
+    ranking unchanged, one prefix upload + one GPU P2 batch for every spec, host P1
+    in rank order): the masked report_to_json of every corpus function is
+    byte-identical — status, status_detail, by_spec, evaluated[] verdicts AND
+    details (VerificationFailed details recomputed from the GPU's (t, reason)),
+    winner and manifest — and the production setting (P1 only on P2 survivors)
+    picks the same winner."""
     rc, lines, err = _run("corpus")
-    assert rc == 0, err + json.dumps(lines[-3:])
+    assert rc == 0, err + json.dumps(lines[-3:])[:4000]
     assert lines[-1]["mismatches"] == 0
-    lifted = [x for x in lines[:-1] if x.get("gpu_status") == "Lifted"]
+    funcs = [x for x in lines[:-1] if x.get("reference_status") != "Misclassified"]
+    assert len(funcs) == 34
+    assert all(x["same_report_json"] and x["fast_same_winner"] for x in funcs)
+    lifted = [x for x in funcs if x.get("gpu_status") == "Lifted"]
     assert len(lifted) == 29  # 23 GEMM + 6 conv (SURVEY Appendix A)
+
+
+def test_adapter_p2_details_match_verify_rewrite():
+    """A VerificationFailed entry's detail (pipeline.cpp:279-283) is rebuilt from the
+    GPU's (first failing test, reason) — atc_dispatch on that test's recorded image,
+    compared in the reference's order — and equals rewriter::verify_rewrite's own
+    detail on P2-rejected bindings of every corpus program x spec."""
+    rc, lines, err = _run("details", "24")
+    assert rc == 0, err + json.dumps(lines[:5])[:4000]
+    last = lines[-1]
+    assert last["mismatches"] == 0 and last["checked"] > 1000
+    assert last["kinds"].get("mismatch", 0) > 0 and last["kinds"].get("dispatch failed", 0) > 0
 
 
 def test_adapter_gpu_dispatch_bit_identical():
