@@ -358,14 +358,19 @@ int cmd_details(atc_ctx* ctx, int per_space) {
       auto fn = analyze(p, fseed, {&spec});
       UnprunedSpace sp(fn, spec);
       if (sp.count() == 0) continue;
+      // a wide strided sample screened on the GPU, then up to per_space rejected
+      // bindings of each failure reason re-run through the reference (conv spaces
+      // hold dispatch failures — oh = h - r + 1 < 1 — that a narrow sample can miss)
       std::vector<matching::CandidateBinding> list;
-      const size_t stride = std::max<size_t>(1, sp.count() / (size_t)per_space);
-      for (size_t i = 0; i < sp.count() && (int)list.size() < 2 * per_space; i += (i < 16 ? 1 : stride))
+      const size_t wide = 64 * (size_t)per_space;
+      const size_t stride = std::max<size_t>(1, sp.count() / wide);
+      for (size_t i = 0; i < sp.count() && list.size() < wide + 16; i += (i < 16 ? 1 : stride))
         list.push_back(sp.at(spec, i));
       auto rec = gpu::record_tests(p.prog, p.function, p.meta.rules, Rng::mix(fseed, "post"), 10);
       auto v = gpu::p2_verdicts(ctx, rec, {&spec}, {&list});
+      std::map<int, int> taken;
       for (size_t b = 0; b < list.size(); ++b) {
-        if (v[0].reason[b] == ATC_PASS) continue;
+        if (v[0].reason[b] == ATC_PASS || taken[v[0].reason[b]]++ >= per_space) continue;
         auto rr = rewriter::rewrite(p.prog, p.function, list[b], spec);
         auto vr = rewriter::verify_rewrite(p.prog, rr.program, p.function, list[b], spec, p.meta.rules,
                                            Rng::mix(fseed, "post"), 10);
