@@ -110,9 +110,23 @@ enum {
 enum { ATC_MODE_FP64 = 0, ATC_MODE_FP32_SCREEN = 1 };
 
 int atc_device_count(void);
+/* One context per (thread of a) caller on one device.  Every entry point taking a
+ * context holds the context's lock for the whole call, so the pipeline's worker
+ * threads (pipeline.cpp:340-355) may share a context; for concurrency give each
+ * worker its own context (or a device group's member, below). */
 atc_ctx* atc_create(int device);
 void atc_destroy(atc_ctx* ctx);
 const char* atc_last_error(const atc_ctx* ctx);
+
+/* Per-context options — kernel-variant selection for A/B parity checks and
+ * measurements; the defaults are the production kernels. */
+enum { ATC_OPT_CONV_SCREEN = 0, ATC_OPT_TC_FLAGS = 1 };
+enum { ATC_CONV_SCREEN_AUTO = 0,    /* k_screen_conv_pairs where it applies      */
+       ATC_CONV_SCREEN_PLANES = 1,  /* k_screen_conv_planes instead of the pairs */
+       ATC_CONV_SCREEN_GENERIC = 2  /* the generic k_screen_rows for conv        */ };
+enum { ATC_TC_NO_KSPLIT = 1, ATC_TC_NO_2SM = 2, ATC_TC_NO_TMA_STORE = 4, ATC_TC_NO_PAIR = 8,
+       ATC_TC_NO_IM2COL = 16, ATC_TC_B_KMAJOR = 32 };
+int atc_set_option(atc_ctx* ctx, int32_t option, int32_t value);
 
 /* Run all subsequent work of this context on the caller's CUDA stream
  * (cudaStream_t as void*; NULL restores the context's own stream). */
@@ -302,6 +316,67 @@ int atc_run_reference(atc_ctx* ctx, const atc_spec_desc* spec, const int64_t* si
  * when run_dispatch would throw. */
 int atc_dispatch(atc_ctx* ctx, const atc_spec_desc* spec, const int64_t* sizes,
                  double* const* regions, const int64_t* region_len, const int32_t* region_is_f32);
+
+/* ---- Device groups --------------------------------------
+ * Several GPUs of one process: one context (streams, scratch, pools) per device.
+ * The candidate space shards naturally — an enumerated range is cut into
+ * contiguous pieces (atc_plan_shards), each device evaluates its pieces against
+ * its own replica of the recorded test sets, and the per-device results (passing
+ * indices, reason histograms, first passing index) are combined: MIN of the first
+ * passing index — the candidate the reference's rank-order loop (pipeline.cpp:
+ * 248-310) reaches first —, SUM of the histograms, the ordered union of the
+ * passing lists.  No data-path exchange: the devices run concurrently (one host
+ * thread each) and only their result blocks come back.  A device may be listed
+ * more than once (independent contexts on it). */
+typedef struct atc_group atc_group;
+typedef struct atc_group_testsets atc_group_testsets;
+/* devices[i] for i < n (NULL: devices 0..n-1; n <= 0: every visible device).
+ * Returns NULL only on allocation failure; check atc_group_last_error. */
+atc_group* atc_group_create(const int32_t* devices, int32_t n);
+void atc_group_destroy(atc_group* g);
+const char* atc_group_last_error(const atc_group* g);
+int32_t atc_group_size(const atc_group* g);
+atc_ctx* atc_group_member(atc_group* g, int32_t i);   /* e.g. one per pipeline worker */
+/* The same recorded test sets on every member device (as atc_testsets_upload_seeded /
+ * _prefix, asynchronous). */
+int atc_group_testsets_upload_seeded(atc_group* g, const atc_seeded_testsets* ts, atc_group_testsets** out);
+int atc_group_testsets_upload_prefix(atc_group* g, const atc_prefix_testsets* ts, atc_group_testsets** out);
+int atc_group_testsets_free(atc_group* g, atc_group_testsets* h);
+const atc_testset_handle* atc_group_testsets_member(const atc_group_testsets* h, int32_t i);
+
+typedef struct atc_group_job {
+  const atc_spec_desc* spec;
+  const atc_group_testsets* ts;
+  const uint8_t* perms;
+  int32_t n_perms;
+  uint64_t begin, end;
+  uint64_t* survivors;                      /* out: ascending passing indices, at most cap */
+  int64_t cap;
+  int64_t n_survivors;                      /* out: passing count (all devices)            */
+  int64_t reason_counts[ATC_REASON_COUNT];  /* out: summed over devices                    */
+  int64_t first_pass;                       /* out: smallest passing index, -1 if none     */
+  int32_t status;                           /* out                                         */
+} atc_group_job;
+/* Every job's range sharded over the members (atc_plan_shards over the jobs' range
+ * sizes), each member's share evaluated as one atc_eval_enumerated_many, then
+ * combined.  Each job's outputs equal atc_eval_enumerated on one device. */
+int atc_group_eval_enumerated_many(atc_group* g, atc_group_job* jobs, int32_t n_jobs, int32_t mode);
+/* The same prepared once (each member an atc_enum_batch over its share, replayed as
+ * one CUDA graph per device) and run many times. */
+typedef struct atc_group_batch atc_group_batch;
+atc_group_batch* atc_group_batch_create(atc_group* g, atc_group_job* jobs, int32_t n_jobs, int32_t mode);
+int atc_group_batch_run(atc_group* g, atc_group_batch* b);
+void atc_group_batch_destroy(atc_group* g, atc_group_batch* b);
+
+/* The shard plan (host arithmetic, no device needed): rank r of `world` evaluates
+ * [begin[r*n_jobs + j], end[r*n_jobs + j]) of job j (relative to the job's range;
+ * empty when begin == end).  Spaces of >= 2^24 bindings are balanced with a
+ * per-space cost model (a fixed part per piece plus a part per binding): largest
+ * first, whole to the least-loaded rank when that stays within the per-rank target
+ * (+15%), else in the fewest contiguous ~equal pieces that do; smaller spaces go
+ * whole to one rank each, round-robin.  Deterministic: every rank computes the
+ * same plan (paper_2301_11659_b200/workloads.py::plan_shards is the same rule). */
+int atc_plan_shards(const uint64_t* counts, int32_t n_jobs, int32_t world, uint64_t* begin, uint64_t* end);
 
 /* Backends.  precision: 0 = TF32 (1 pass), 1 = 3xTF32 (split, ~FP32 accuracy). */
 enum { ATC_PREC_TF32 = 0, ATC_PREC_3XTF32 = 1 };

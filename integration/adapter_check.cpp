@@ -12,8 +12,11 @@
 //       rank order): byte-equal masked report_to_json, and the production
 //       setting's (P1 on P2 survivors only) winner and timings.
 //   adapter_check unpruned <stem> <spec> [tests]
-//       the full unpruned binding space of one program in Appendix C order as the
-//       ranked list: GPU P2 over all of it + host P1 on survivors, timed.
+//       the full unpruned binding space of one program in Appendix C order:
+//       gpu::first_accepted_unpruned on the device group (every GPU, enumerated
+//       P2 + host P1 on survivors), and — for spaces up to 2^20 — the same space
+//       as an explicit ranked list through gpu::first_accepted on one context;
+//       winners, passing counts and passing lists must agree.
 //   adapter_check dispatch
 //       the lifted program run with make_gpu_dispatch vs make_oracle_dispatch.
 //   adapter_check details [per_space]
@@ -237,109 +240,51 @@ int cmd_corpus(atc_ctx* ctx) {
   return mismatches == 0 ? 0 : 1;
 }
 
-int cmd_unpruned(atc_ctx* ctx, const std::string& stem, const std::string& spec_name, int tests) {
+int cmd_unpruned(atc_ctx* ctx, atc_group* g, const std::string& stem, const std::string& spec_name, int tests) {
   auto specs = default_specs();
   const api::ApiSpec* spec = nullptr;
   for (const auto& s : specs)
     if (s.name == spec_name) spec = &s;
   for (const auto& p : corpus()) {
-    if (p.stem != stem) continue;
+    if (p.stem != stem || !spec) continue;
     const uint64_t fseed = Rng::mix(0, p.tag + ":" + p.function);
     auto fn = analyze(p, fseed, {spec});
-    // Appendix C order: array k-permutations (odometer) x size maps (digit 0 fastest)
-    std::vector<matching::CandidateBinding> space;
-    std::vector<std::string> ptrs, ints = fn.int_params;
-    for (const auto& a : fn.arrays) ptrs.push_back(a.name);
-    auto arrays = spec->arrays();
-    auto sizes = spec->size_params();
-    std::vector<int> sel(arrays.size());
-    std::vector<bool> used(ptrs.size(), false);
-    std::vector<std::vector<int>> perms;
-    std::function<void(size_t)> rec = [&](size_t i) {
-      if (i == arrays.size()) {
-        perms.push_back(sel);
-        return;
-      }
-      for (size_t j = 0; j < ptrs.size(); ++j)
-        if (!used[j]) {
-          used[j] = true;
-          sel[i] = (int)j;
-          rec(i + 1);
-          used[j] = false;
-        }
-    };
-    rec(0);
-    size_t maps = 1;
-    for (size_t q = 0; q < sizes.size(); ++q) maps *= ints.size();
-    for (const auto& perm : perms)
-      for (size_t s = 0; s < maps; ++s) {
-        matching::CandidateBinding b;
-        for (size_t a = 0; a < arrays.size(); ++a) b.arrays[arrays[a]->name] = ptrs[perm[a]];
-        size_t x = s;
-        for (size_t q = 0; q < sizes.size(); ++q) {
-          b.sizes[sizes[q]->name] = ints[x % ints.size()];
-          x /= ints.size();
-        }
-        space.push_back(std::move(b));
-      }
+    const gpu::UnprunedSpace sp(fn, *spec);
+    json j = {{"stem", stem}, {"spec", spec_name}, {"bindings", sp.count()}, {"tests", tests},
+              {"devices", atc_group_size(g)}};
+    // the whole space on the device group (enumerated, sharded over the members)
     auto t0 = std::chrono::steady_clock::now();
-    auto lr = gpu::first_accepted(ctx, p.prog, fn, p.function, *spec, space, p.meta.rules, fseed, 30, tests);
-    const double total = ms_since(t0);
-    int64_t passed = 0;
-    for (auto r : lr.p2_reason) passed += r == ATC_PASS;
-    std::cout << json({{"stem", stem}, {"spec", spec_name}, {"bindings", space.size()}, {"tests", tests},
-                       {"p2_passed", passed}, {"winner", lr.winner ? (int64_t)*lr.winner : -1},
-                       {"p1_calls", lr.p1_calls}, {"record_ms", lr.record_ms}, {"gpu_p2_ms", lr.gpu_ms},
-                       {"p1_ms", lr.p1_ms}, {"total_ms", total}})
-                     .dump()
-              << std::endl;
-    return 0;
+    auto ur = gpu::first_accepted_unpruned(g, p.prog, fn, p.function, *spec, p.meta.rules, fseed, 30, tests);
+    j["group"] = {{"winner", ur.winner}, {"p2_passed", ur.p2_passed}, {"p1_calls", ur.p1_calls},
+                  {"record_ms", ur.record_ms}, {"gpu_p2_ms", ur.gpu_ms}, {"p1_ms", ur.p1_ms},
+                  {"total_ms", ms_since(t0)},
+                  {"reason_counts", std::vector<int64_t>(ur.reason_counts, ur.reason_counts + ATC_REASON_COUNT)}};
+    bool ok = true;
+    if (sp.count() <= (1u << 20)) {  // the same space as an explicit ranked list on one context
+      std::vector<matching::CandidateBinding> space;
+      for (size_t i = 0; i < sp.count(); ++i) space.push_back(sp.at(*spec, i));
+      t0 = std::chrono::steady_clock::now();
+      auto lr = gpu::first_accepted(ctx, p.prog, fn, p.function, *spec, space, p.meta.rules, fseed, 30, tests);
+      const double total = ms_since(t0);
+      int64_t passed = 0;
+      std::vector<uint64_t> passing;
+      for (size_t b = 0; b < lr.p2_reason.size(); ++b)
+        if (lr.p2_reason[b] == ATC_PASS) {
+          ++passed;
+          if (passing.size() < ur.p2_passing.size()) passing.push_back(b);
+        }
+      const int64_t winner = lr.winner ? (int64_t)*lr.winner : -1;
+      ok = winner == ur.winner && passed == ur.p2_passed && passing == ur.p2_passing;
+      j["list"] = {{"winner", winner}, {"p2_passed", passed}, {"p1_calls", lr.p1_calls}, {"record_ms", lr.record_ms},
+                   {"gpu_p2_ms", lr.gpu_ms}, {"p1_ms", lr.p1_ms}, {"total_ms", total}};
+    }
+    j["same"] = ok;
+    std::cout << j.dump() << std::endl;
+    return ok ? 0 : 1;
   }
   return 1;
 }
 
-// One binding of the unpruned space in Appendix C order: array
-// k-permutations in odometer order x size maps with digit 0 fastest.
-struct UnprunedSpace {
-  std::vector<std::vector<int>> perms;
-  std::vector<std::string> ptrs, ints;
-  size_t maps = 1;
-  UnprunedSpace(const analysis::AnalyzedFunction& fn, const api::ApiSpec& spec) : ints(fn.int_params) {
-    for (const auto& a : fn.arrays) ptrs.push_back(a.name);
-    const size_t nA = spec.arrays().size();
-    std::vector<int> sel(nA);
-    std::vector<bool> used(ptrs.size(), false);
-    std::function<void(size_t)> rec = [&](size_t i) {
-      if (i == nA) {
-        perms.push_back(sel);
-        return;
-      }
-      for (size_t j = 0; j < ptrs.size(); ++j)
-        if (!used[j]) {
-          used[j] = true;
-          sel[i] = (int)j;
-          rec(i + 1);
-          used[j] = false;
-        }
-    };
-    rec(0);
-    for (size_t q = 0; q < spec.size_params().size(); ++q) maps *= ints.size();
-  }
-  size_t count() const { return perms.size() * maps; }
-  matching::CandidateBinding at(const api::ApiSpec& spec, size_t idx) const {
-    matching::CandidateBinding b;
-    const auto arrays = spec.arrays();
-    const auto sizes = spec.size_params();
-    const auto& perm = perms[idx / maps];
-    for (size_t a = 0; a < arrays.size(); ++a) b.arrays[arrays[a]->name] = ptrs[perm[a]];
-    size_t x = idx % maps;
-    for (size_t q = 0; q < sizes.size(); ++q) {
-      b.sizes[sizes[q]->name] = ints[x % ints.size()];
-      x /= ints.size();
-    }
-    return b;
-  }
-};
 
 // p2_detail vs the reference's own verify_rewrite detail (rewriter.cpp:215-284) on
 // bindings of every corpus program x spec that P2 rejects: a strided sample of
@@ -356,7 +301,7 @@ int cmd_details(atc_ctx* ctx, int per_space) {
     for (const auto& spec : specs) {
       if ((spec.semantics == "conv2d") != (p.dir == "conv")) continue;
       auto fn = analyze(p, fseed, {&spec});
-      UnprunedSpace sp(fn, spec);
+      gpu::UnprunedSpace sp(fn, spec);
       if (sp.count() == 0) continue;
       // a wide strided sample screened on the GPU, then up to per_space rejected
       // bindings of each failure reason re-run through the reference (conv spaces
@@ -593,16 +538,19 @@ int cmd_routed(atc_ctx* ctx) {
 }  // namespace
 
 int main(int argc, char** argv) {
-  atc_ctx* ctx = atc_create(0);
-  if (!ctx || atc_last_error(ctx)[0]) {
-    std::fprintf(stderr, "adapter_check: %s\n", ctx ? atc_last_error(ctx) : "no context");
+  // every visible GPU as one device group; single-context work
+  // (the candidate loop, dispatch) runs on member 0, as one pipeline worker would
+  atc_group* g = atc_group_create(nullptr, 0);
+  atc_ctx* ctx = g ? atc_group_member(g, 0) : nullptr;
+  if (!g || atc_group_last_error(g)[0] || !ctx) {
+    std::fprintf(stderr, "adapter_check: %s\n", g ? atc_group_last_error(g) : "no device group");
     return 2;
   }
   int rc = 1;
   try {
     std::string cmd = argc > 1 ? argv[1] : "corpus";
     if (cmd == "corpus") rc = cmd_corpus(ctx);
-    if (cmd == "unpruned" && argc >= 4) rc = cmd_unpruned(ctx, argv[2], argv[3], argc > 4 ? std::atoi(argv[4]) : 10);
+    if (cmd == "unpruned" && argc >= 4) rc = cmd_unpruned(ctx, g, argv[2], argv[3], argc > 4 ? std::atoi(argv[4]) : 10);
     if (cmd == "dispatch") rc = cmd_dispatch(ctx);
     if (cmd == "details") rc = cmd_details(ctx, argc > 2 ? std::atoi(argv[2]) : 24);
     if (cmd == "routed") rc = cmd_routed(ctx);
@@ -610,6 +558,6 @@ int main(int argc, char** argv) {
     std::fprintf(stderr, "adapter_check: %s\n", e.what());
     rc = 1;
   }
-  atc_destroy(ctx);
+  atc_group_destroy(g);
   return rc;
 }

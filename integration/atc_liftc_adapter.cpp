@@ -2,6 +2,7 @@
 #include "atc_liftc_adapter.hpp"
 
 #include <algorithm>
+#include <functional>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -140,6 +141,24 @@ RecordedTests record_tests(const minilang::Program& prog, const std::string& fun
 
 namespace {
 
+// The prefix-upload descriptor of r (pointers into r and `ip`).
+atc_prefix_testsets prefix_desc(const RecordedTests& r, std::vector<const double*>& ip) {
+  const size_t nP = r.ptr_params.size();
+  ip.assign(r.init.size(), nullptr);
+  for (size_t i = 0; i < r.init.size(); ++i) ip[i] = r.test_ok[i / nP] ? r.init[i].data() : nullptr;
+  return atc_prefix_testsets{r.T,
+                             (int32_t)r.int_params.size(),
+                             (int32_t)nP,
+                             r.ints.data(),
+                             r.is_f32.data(),
+                             r.region_len.data(),
+                             r.test_ok.data(),
+                             ip.data(),
+                             r.diff_off.data(),
+                             r.diff_pos.data(),
+                             r.diff_val.data()};
+}
+
 // Uploads r (the needed region prefixes + final-minus-init entries when the diffs
 // were recorded, else the full regions) and returns the handle.
 atc_testset_handle* upload(atc_ctx* ctx, const RecordedTests& r) {
@@ -147,19 +166,8 @@ atc_testset_handle* upload(atc_ctx* ctx, const RecordedTests& r) {
   atc_testset_handle* h = nullptr;
   int rc;
   if (!r.diff_off.empty()) {
-    std::vector<const double*> ip(r.init.size());
-    for (size_t i = 0; i < r.init.size(); ++i) ip[i] = r.test_ok[i / nP] ? r.init[i].data() : nullptr;
-    atc_prefix_testsets px{r.T,
-                           (int32_t)r.int_params.size(),
-                           (int32_t)nP,
-                           r.ints.data(),
-                           r.is_f32.data(),
-                           r.region_len.data(),
-                           r.test_ok.data(),
-                           ip.data(),
-                           r.diff_off.data(),
-                           r.diff_pos.data(),
-                           r.diff_val.data()};
+    std::vector<const double*> ip;
+    const atc_prefix_testsets px = prefix_desc(r, ip);
     rc = atc_testsets_upload_prefix(ctx, &px, &h);
   } else {
     std::vector<const double*> ip(r.init.size()), fp(r.fin.size());
@@ -274,6 +282,104 @@ LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const ana
                                           : std::string(equivalence::verdict_name(er.verdict)));
     if (eq && p2_ok) {
       out.winner = b;
+      break;
+    }
+  }
+  out.p1_ms = ms_since(t0);
+  return out;
+}
+
+UnprunedSpace::UnprunedSpace(const analysis::AnalyzedFunction& fn, const api::ApiSpec& spec) : ints(fn.int_params) {
+  for (const auto& a : fn.arrays) ptrs.push_back(a.name);
+  const size_t nA = spec.arrays().size();
+  std::vector<int> sel(nA);
+  std::vector<bool> used(ptrs.size(), false);
+  std::function<void(size_t)> rec = [&](size_t i) {
+    if (i == nA) {
+      perms.push_back(sel);
+      return;
+    }
+    for (size_t j = 0; j < ptrs.size(); ++j)
+      if (!used[j]) {
+        used[j] = true;
+        sel[i] = (int)j;
+        rec(i + 1);
+        used[j] = false;
+      }
+  };
+  rec(0);
+  for (size_t q = 0; q < spec.size_params().size(); ++q) maps *= ints.size();
+}
+
+matching::CandidateBinding UnprunedSpace::at(const api::ApiSpec& spec, size_t idx) const {
+  matching::CandidateBinding b;
+  const auto arrays = spec.arrays();
+  const auto sizes = spec.size_params();
+  const auto& perm = perms[idx / maps];
+  for (size_t a = 0; a < arrays.size(); ++a) b.arrays[arrays[a]->name] = ptrs[perm[a]];
+  size_t x = idx % maps;
+  for (size_t q = 0; q < sizes.size(); ++q) {
+    b.sizes[sizes[q]->name] = ints[x % ints.size()];
+    x /= ints.size();
+  }
+  return b;
+}
+
+std::vector<uint8_t> UnprunedSpace::perm_table() const {
+  std::vector<uint8_t> t;
+  for (const auto& p : perms)
+    for (int u : p) t.push_back((uint8_t)u);
+  return t;
+}
+
+UnprunedResult first_accepted_unpruned(atc_group* g, const minilang::Program& prog,
+                                       const analysis::AnalyzedFunction& fn, const std::string& function,
+                                       const api::ApiSpec& spec, const api::SizeRules& rules, uint64_t fseed,
+                                       int p1_tests, int verify_tests, int64_t cap) {
+  UnprunedResult out;
+  const UnprunedSpace space(fn, spec);
+  if (space.count() == 0) return out;
+  auto t0 = std::chrono::steady_clock::now();
+  const RecordedTests r = record_tests(prog, function, rules, Rng::mix(fseed, "post"), verify_tests);
+  out.record_ms = ms_since(t0);
+
+  t0 = std::chrono::steady_clock::now();
+  std::vector<const double*> ip;
+  const atc_prefix_testsets px = prefix_desc(r, ip);
+  atc_group_testsets* h = nullptr;
+  if (atc_group_testsets_upload_prefix(g, &px, &h) != ATC_OK) throw std::runtime_error(atc_group_last_error(g));
+  const atc_spec_desc desc = encode_spec(spec);
+  const std::vector<uint8_t> perms = space.perm_table();
+  out.p2_passing.resize((size_t)std::max<int64_t>(cap, 1));
+  atc_group_job job{};
+  job.spec = &desc;
+  job.ts = h;
+  job.perms = perms.data();
+  job.n_perms = (int32_t)space.perms.size();
+  job.begin = 0;
+  job.end = space.count();
+  job.survivors = out.p2_passing.data();
+  job.cap = cap;
+  const int rc = atc_group_eval_enumerated_many(g, &job, 1, ATC_MODE_FP64);
+  const std::string err = rc != ATC_OK ? atc_group_last_error(g) : "";
+  atc_group_testsets_free(g, h);
+  if (rc != ATC_OK) throw std::runtime_error(err);
+  out.p2_passed = job.n_survivors;
+  for (int k = 0; k < ATC_REASON_COUNT; ++k) out.reason_counts[k] = job.reason_counts[k];
+  out.p2_passing.resize((size_t)std::min<int64_t>(job.n_survivors, cap));
+  out.gpu_ms = ms_since(t0);
+
+  // P1 on the P2 survivors in index order (pipeline.cpp:257-261, :275-277 order of
+  // the two phases swapped: P2 is the cheap screen here)
+  t0 = std::chrono::steady_clock::now();
+  for (uint64_t idx : out.p2_passing) {
+    equivalence::EquivalenceConfig ec;
+    ec.tests = p1_tests;
+    ec.seed = fseed;
+    ++out.p1_calls;
+    auto er = equivalence::check_equivalence(prog, fn, space.at(spec, idx), spec, rules, ec);
+    if (er.verdict == equivalence::Verdict::Equivalent) {
+      out.winner = (int64_t)idx;
       break;
     }
   }

@@ -88,6 +88,37 @@ LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const ana
                           uint64_t fseed, int p1_tests, int verify_tests, const RecordedTests* recorded = nullptr,
                           bool report_parity = false, const SpecVerdicts* p2 = nullptr);
 
+// The unpruned binding space of one spec in SURVEY.md Appendix C order: array
+// k-permutations of the user pointers (odometer order) x size maps over the user
+// ints (digit 0 fastest) — the space matching::raw_candidate_count counts
+// (matching.cpp:119-131) before any pruning.
+struct UnprunedSpace {
+  std::vector<std::vector<int>> perms;
+  std::vector<std::string> ptrs, ints;
+  size_t maps = 1;
+  UnprunedSpace(const analysis::AnalyzedFunction& fn, const api::ApiSpec& spec);
+  size_t count() const { return perms.size() * maps; }
+  matching::CandidateBinding at(const api::ApiSpec& spec, size_t idx) const;
+  std::vector<uint8_t> perm_table() const;  // [n_perms][n_arrays] for atc_group_job / atc_enum_job
+};
+
+// The unpruned space as the ranked list, on every GPU of a device group: P2 over
+// the whole space (atc_group_eval_enumerated_many: the space sharded over the
+// members, the per-device results combined), then P1 (host check_equivalence) on
+// the P2 survivors in index order; the first P1-equivalent survivor wins.
+struct UnprunedResult {
+  int64_t winner = -1;                // index of the accepted binding, -1 if none
+  int64_t p2_passed = 0;              // bindings passing every P2 test
+  std::vector<uint64_t> p2_passing;   // their indices (ascending, at most `cap`)
+  int64_t reason_counts[ATC_REASON_COUNT] = {};
+  int p1_calls = 0;
+  double record_ms = 0.0, gpu_ms = 0.0, p1_ms = 0.0;
+};
+UnprunedResult first_accepted_unpruned(atc_group* g, const minilang::Program& prog,
+                                       const analysis::AnalyzedFunction& fn, const std::string& function,
+                                       const api::ApiSpec& spec, const api::SizeRules& rules, uint64_t fseed,
+                                       int p1_tests, int verify_tests, int64_t cap = 4096);
+
 // run_dispatch's exception text (rewriter.cpp:141, :145-147) for an
 // ATC_ERR_DISPATCH message of atc_dispatch, which names params by index.
 std::string dispatch_error_text(const api::ApiSpec& spec, const std::string& abi_msg);

@@ -155,6 +155,29 @@ class BindJob(C.Structure):
     ]
 
 
+class GroupJob(C.Structure):
+    """atc_group_job (include/atc_b200.h)."""
+
+    _fields_ = [
+        ("spec", C.c_void_p),
+        ("ts", C.c_void_p),
+        ("perms", C.c_void_p),
+        ("n_perms", C.c_int32),
+        ("begin", C.c_uint64),
+        ("end", C.c_uint64),
+        ("survivors", C.c_void_p),
+        ("cap", C.c_int64),
+        ("n_survivors", C.c_int64),
+        ("reason_counts", C.c_int64 * 5),
+        ("first_pass", C.c_int64),
+        ("status", C.c_int32),
+    ]
+
+
+OPT_CONV_SCREEN, OPT_TC_FLAGS = 0, 1
+CONV_SCREEN_AUTO, CONV_SCREEN_PLANES, CONV_SCREEN_GENERIC = 0, 1, 2
+TC_NO_KSPLIT, TC_NO_2SM, TC_NO_TMA_STORE, TC_NO_PAIR, TC_NO_IM2COL, TC_B_KMAJOR = 1, 2, 4, 8, 16, 32
+
 # (name, restype, argtypes) for every function declared in include/atc_b200.h
 _P = C.c_void_p
 _SIGS = [
@@ -162,6 +185,7 @@ _SIGS = [
     ("atc_create", _P, [C.c_int]),
     ("atc_destroy", None, [_P]),
     ("atc_last_error", C.c_char_p, [_P]),
+    ("atc_set_option", C.c_int, [_P, C.c_int32, C.c_int32]),
     ("atc_set_stream", C.c_int, [_P, _P]),
     ("atc_profile_start", C.c_int, [_P]),
     ("atc_profile_read", C.c_int, [_P, C.POINTER(Profile)]),
@@ -184,6 +208,20 @@ _SIGS = [
     ("atc_enum_batch_create", _P, [_P, C.POINTER(EnumJob), C.c_int32, C.c_int32]),
     ("atc_enum_batch_run", C.c_int, [_P, _P]),
     ("atc_enum_batch_destroy", None, [_P, _P]),
+    ("atc_group_create", _P, [_P, C.c_int32]),
+    ("atc_group_destroy", None, [_P]),
+    ("atc_group_last_error", C.c_char_p, [_P]),
+    ("atc_group_size", C.c_int32, [_P]),
+    ("atc_group_member", _P, [_P, C.c_int32]),
+    ("atc_group_testsets_upload_seeded", C.c_int, [_P, C.POINTER(SeededTestsets), C.POINTER(_P)]),
+    ("atc_group_testsets_upload_prefix", C.c_int, [_P, C.POINTER(PrefixTestsets), C.POINTER(_P)]),
+    ("atc_group_testsets_free", C.c_int, [_P, _P]),
+    ("atc_group_testsets_member", _P, [_P, C.c_int32]),
+    ("atc_group_eval_enumerated_many", C.c_int, [_P, C.POINTER(GroupJob), C.c_int32, C.c_int32]),
+    ("atc_group_batch_create", _P, [_P, C.POINTER(GroupJob), C.c_int32, C.c_int32]),
+    ("atc_group_batch_run", C.c_int, [_P, _P]),
+    ("atc_group_batch_destroy", None, [_P, _P]),
+    ("atc_plan_shards", C.c_int, [_P, C.c_int32, C.c_int32, _P, _P]),
     ("atc_run_reference", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P]),
     ("atc_dispatch", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, _P]),
     ("atc_sgemm_rm", C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int32]),
@@ -235,6 +273,10 @@ class Context:
             L.atc_destroy(self.handle)
             self.handle = None
             raise AtcError(ATC_ERR_DEVICE, err)
+
+    def set_option(self, option: int, value: int) -> None:
+        """atc_set_option: kernel-variant selection (A/B checks)."""
+        check(self.handle, lib().atc_set_option(self.handle, option, value))
 
     def close(self) -> None:
         if self.handle:

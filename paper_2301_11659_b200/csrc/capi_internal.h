@@ -1,13 +1,17 @@
-// Internal context shared by the C-ABI translation units.
+// Internal context and declarations shared by the C-ABI translation units
+// (ctx.cu, testsets.cu, evaluate.cu, sweep.cu, group.cu).
 #pragma once
 #include <cuda_runtime.h>
 
 #include <cstdint>
-
 #include <map>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
+
+#include "atc_b200.h"
+#include "eval_common.cuh"
 
 struct atc_ctx {
   int device = 0;
@@ -50,6 +54,14 @@ struct atc_ctx {
   // device-memory pool for test-set uploads (atc_pool_alloc / atc_pool_free)
   std::vector<std::pair<void*, size_t>> pool_free;
   std::map<void*, size_t> pool_used;
+  // per-context options (atc_set_option): kernel-variant selection for A/B checks
+  int opt_conv_screen = ATC_CONV_SCREEN_AUTO;
+  int opt_tc_flags = 0;
+  bool tc_configured = false;  // k_tc_gemm* shared-memory attributes set on this context's device
+  // every ABI entry point holds this for its whole call, so a context is
+  // serialised (the pipeline's worker threads may share one)
+  std::recursive_mutex mu;
+  std::mutex err_mu;  // host worker threads of one call may report errors concurrently
 };
 
 void* atc_pool_alloc(atc_ctx* ctx, size_t bytes);
@@ -59,3 +71,119 @@ void atc_set_error(atc_ctx* ctx, const char* fmt, ...);
 bool atc_cuda_ok(atc_ctx* ctx, cudaError_t e, const char* what);
 void* atc_ctx_scratch(atc_ctx* ctx, int slot, size_t bytes);
 void* atc_ctx_pinned(atc_ctx* ctx, int slot, size_t bytes);
+
+// Holds the context's lock for one ABI call; fails (returns false) on a null or
+// broken context.
+struct AtcLock {
+  std::unique_lock<std::recursive_mutex> lk;
+  explicit AtcLock(atc_ctx* ctx) {
+    if (ctx) lk = std::unique_lock<std::recursive_mutex>(ctx->mu);
+  }
+};
+#define ATC_ENTER(ctx)                          \
+  if (!(ctx) || (ctx)->broken) return ATC_ERR_DEVICE; \
+  AtcLock atc_lock_(ctx)
+
+namespace atc {
+__global__ void k_probe_regions(int T, int nP, const uint64_t* seeds, const uint64_t* skips, const int64_t* region_len,
+                                const int32_t* is_f32, const int64_t* region_off, const int64_t* need, double* init,
+                                double* fin, TestsetView v, const int64_t* diff_off, const int32_t* diff_pos,
+                                const double* diff_val, const double* pre, const int64_t* pre_off);
+__global__ void k_apply_diffs(int nP, const int64_t* region_len, const int64_t* region_off, const int64_t* diff_off,
+                              const int32_t* diff_pos, const double* diff_val, double* fin);
+__global__ void k_build_dirty(TestsetView ts, int32_t* dirty_pos, int32_t* dirty_cnt, int32_t* dirty_max);
+
+__global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, int budget,
+                         int32_t* keys, uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
+                         unsigned long long* reason_hist, int mode);
+__global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
+                             uint8_t* out, uint8_t* out1);
+__global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
+                                  uint8_t* out, uint8_t* out1, uint32_t* cm, int stage_a, int stage_b);
+__global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
+                              uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
+                              unsigned long long* reason_hist);
+__global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need);
+__global__ void k_cmask(const uint8_t* table, uint64_t n_words, int nI, uint32_t* cmask, int shift);
+__global__ void k_screen_conv_pairs(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
+                                    uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
+                                    unsigned long long* surv_cnt, unsigned long long* reason_hist, int lut_n);
+__global__ void k_screen_conv_planes(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
+                                   uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
+                                   unsigned long long* surv_cnt, unsigned long long* reason_hist);
+template <int SEM, int NS, bool I32, uint32_t Q0MASK>
+__global__ void k_screen_rows(TestsetView ts, SpecView sp, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
+                              uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
+                              unsigned long long* surv_cnt, unsigned long long* reason_hist);
+__global__ void k_confirm_warp(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
+                               uint64_t surv_cap, int32_t* surv_keys, const uint32_t* sel,
+                               const unsigned long long* sel_cnt, int mode, int screened);
+__global__ void k_confirm_pre(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
+                              const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
+                              uint32_t* pend, unsigned long long* pend_cnt, int mode, int screened);
+__global__ void k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
+                             const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
+                             const uint32_t* pend, const unsigned long long* pend_cnt, uint32_t* next,
+                             unsigned long long* next_cnt, int mode, int lazy, int screened);
+__global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
+                             const int32_t* surv_keys, int32_t* keys);
+__global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason);
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v);
+__global__ void k_finalize(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
+                           const int32_t* surv_keys, uint64_t base, uint64_t* res, uint64_t res_cap,
+                           unsigned long long* hist);
+}  // namespace atc
+
+struct atc_testset_handle {
+  atc::TestsetView view{};
+  int32_t T = 0, nI = 0, nP = 0;
+  std::vector<int64_t> h_ints;  // host copy of the int values
+  std::vector<void*> allocations;
+  cudaEvent_t ready = nullptr;  // uploads + dirty lists complete (recorded on the copy stream)
+  // layout, kept for in-place updates (atc_testsets_update_seeded)
+  int cs = 0;                   // the copy stream all of this handle's uploads use
+  std::vector<int64_t> lens, off, doff;
+  std::vector<int32_t> is_f32;
+  uint8_t* meta = nullptr;      // the small arrays (TestsetView points into it)
+  size_t meta_bytes = 0, o_ints = 0, o_rlen = 0, o_roff = 0, o_dof = 0, o_isf = 0, o_tok = 0, o_dcnt = 0,
+         o_dmax = 0;
+  uint8_t* seeded = nullptr;    // seeds, stream positions, final-minus-init entries
+  size_t seeded_cap = 0;
+  bool needed_only = false;     // seeded with needed_only: region prefixes only
+  uint8_t* pin = nullptr;       // pinned staging of the metadata + seeded blocks (async DMA)
+  size_t pin_bytes = 0;
+};
+
+// Makes `st` wait for the upload of `ts` (no-op once it has completed).
+inline void ts_wait(const atc_testset_handle* ts, cudaStream_t st) {
+  if (ts && ts->ready) cudaStreamWaitEvent(st, ts->ready, 0);
+}
+
+namespace atc {
+
+constexpr uint64_t kResultPrefix = 4096;        // passing indices returned with the first D2H
+constexpr uint64_t kEnumChunkCap = 1ull << 22;  // survivors per K1 launch
+
+bool build_spec_view(atc_ctx* ctx, const atc_spec_desc* s, SpecView& v);
+
+// Runs K1 + K2 over `n` bindings; survivors/keys live in ctx scratch.
+int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, const BindingSource& src,
+             uint64_t n, int32_t* keys, uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
+             int32_t* surv_keys, unsigned long long* hist, cudaStream_t st, const Pos0Table* pt = nullptr,
+             const RowPlan* plan = nullptr);
+
+// Per-space plan of an enumerated range: the decode, the position-0 table shape and
+// the row plan.
+struct EnumPlan {
+  SpecView sp;
+  Pos0Table pt;
+  RowPlan plan;
+  bool use_table = false, use_rows = false;
+  uint64_t size_maps = 1, table_bytes = 0;
+};
+int plan_enumerated(atc_ctx* ctx, const atc_spec_desc* spec, const atc_testset_handle* ts, const uint8_t* perms,
+                    int32_t n_perms, uint64_t begin, uint64_t end, int32_t mode, EnumPlan& e);
+int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, const uint8_t* perms, int32_t n_perms,
+                   uint8_t** d_perms_out, cudaStream_t st, uint64_t begin, uint64_t end);
+
+}  // namespace atc

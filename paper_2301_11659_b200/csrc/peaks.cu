@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) k_dfma_chains(double* out, int iters, dou
 }  // namespace atc
 
 extern "C" int atc_measure_dfma_peak(atc_ctx* ctx, double* gflops) {
-  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  ATC_ENTER(ctx);
   if (!gflops) return ATC_ERR_ARG;
   cudaSetDevice(ctx->device);
   double* out = (double*)atc_ctx_scratch(ctx, 31, 64);

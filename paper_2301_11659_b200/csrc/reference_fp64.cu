@@ -180,7 +180,7 @@ extern "C" {
 
 int atc_run_reference(atc_ctx* ctx, const atc_spec_desc* spec, const int64_t* sizes, double* const* buffers,
                       const int64_t* buffer_len) {
-  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  ATC_ENTER(ctx);
   if (!spec_basic(ctx, spec) || !sizes || !buffers || !buffer_len) {
     if (ctx->err.empty()) atc_set_error(ctx, "bad arguments to atc_run_reference");
     return ATC_ERR_ARG;
@@ -193,7 +193,7 @@ int atc_run_reference(atc_ctx* ctx, const atc_spec_desc* spec, const int64_t* si
 // with (double)(float) rounding when the region is f32.
 int atc_dispatch(atc_ctx* ctx, const atc_spec_desc* spec, const int64_t* sizes, double* const* regions,
                  const int64_t* region_len, const int32_t* region_is_f32) {
-  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  ATC_ENTER(ctx);
   if (!spec_basic(ctx, spec) || !sizes || !regions || !region_len || !region_is_f32) {
     if (ctx->err.empty()) atc_set_error(ctx, "bad arguments to atc_dispatch");
     return ATC_ERR_ARG;

@@ -950,52 +950,34 @@ bool make_map(atc_ctx* ctx, CUtensorMap* m, const float* base, uint64_t rows, ui
   return true;
 }
 
-// ATC_TC_2SM=0 disables the cta_group::2 kernel (A/B measurement)
-bool ksplit_enabled() {  // ATC_TC_KSPLIT=0: never split K (A/B checks)
-  static const bool on = [] {
-    const char* e = std::getenv("ATC_TC_KSPLIT");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-int umma2_enabled() {
-  static const int on = [] {
-    const char* e = std::getenv("ATC_TC_2SM");
-    return e && e[0] == '0' ? 0 : 1;
-  }();
-  return on;
-}
-
-// ATC_TC_TMA_STORE=0 disables the TMA-store epilogue (A/B measurement)
-int tma_store_enabled() {
-  static const int enabled = [] {
-    const char* e = std::getenv("ATC_TC_TMA_STORE");
-    return e && e[0] == '0' ? 0 : 1;
-  }();
-  return enabled;
-}
+// Kernel-variant switches (context option ATC_OPT_TC_FLAGS, A/B checks):
+// ATC_TC_NO_KSPLIT never splits K, ATC_TC_NO_2SM disables the cta_group::2 kernel,
+// ATC_TC_NO_TMA_STORE the TMA-store epilogue, ATC_TC_NO_PAIR the 1-SM kernel's
+// B multicast across a CTA pair, ATC_TC_NO_IM2COL the im2col-mode conv B operand;
+// ATC_TC_B_KMAJOR transposes the sgemm B to K-major once.
+bool tc_flag(const atc_ctx* ctx, int f) { return (ctx->opt_tc_flags & f) != 0; }
 
 // CTA pairs need an MN-major B (loaded as chunks, half by each CTA) and >= 2
-// M tiles; ATC_TC_PAIR=0 disables them (A/B measurement)
-int use_pair(const Problem& p) {
-  static const int enabled = [] {
-    const char* e = std::getenv("ATC_TC_PAIR");
-    return e && e[0] == '0' ? 0 : 1;
-  }();
-  return enabled && p.conv != 1 && p.tiles_m >= 2 ? 1 : 0;
+// M tiles
+int use_pair(const atc_ctx* ctx, const Problem& p) {
+  return !tc_flag(ctx, ATC_TC_NO_PAIR) && p.conv != 1 && p.tiles_m >= 2 ? 1 : 0;
+}
+
+// the dynamic shared-memory opt-in of both GEMM kernels, once per context (the
+// attribute is per device; every context of a device sets it)
+bool configure_tc(atc_ctx* ctx) {
+  if (ctx->tc_configured) return true;
+  if (!atc_cuda_ok(ctx, cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
+                   "cudaFuncSetAttribute") ||
+      !atc_cuda_ok(ctx, cudaFuncSetAttribute(k_tc_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES),
+                   "cudaFuncSetAttribute"))
+    return false;
+  ctx->tc_configured = true;
+  return true;
 }
 
 bool launch(atc_ctx* ctx, const Maps& maps, const Problem& p, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    if (!atc_cuda_ok(ctx, cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
-                     "cudaFuncSetAttribute") ||
-        !atc_cuda_ok(ctx, cudaFuncSetAttribute(k_tc_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES),
-                     "cudaFuncSetAttribute"))
-      return false;
-    configured = true;
-  }
+  if (!configure_tc(ctx)) return false;
   if (p.umma2) {
     const int units = (p.tiles_m + 1) / 2 * p.tiles_n * (p.ksplit > 1 ? p.ksplit : 1);
     cudaLaunchConfig_t cfg{};
@@ -1043,7 +1025,7 @@ extern "C" {
 
 int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* dC, int64_t m, int64_t n, int64_t k,
                         int32_t precision, void* stream) {
-  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  ATC_ENTER(ctx);
   if (m < 1 || n < 1 || k < 1 || m >= (1LL << 31) || n >= (1LL << 31) || k >= (1LL << 31) || !dA || !dB || !dC ||
       (precision != ATC_PREC_TF32 && precision != ATC_PREC_3XTF32)) {
     atc_set_error(ctx, "bad arguments to atc_sgemm_rm");
@@ -1067,12 +1049,8 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
     k_pitch_copy<<<grid_for(k * np), 256, 0, st>>>(dB, t, k, n, np);
     B = t;
   }
-  // ATC_TC_BKMAJOR=1: B transposed once to [N][K] (K-major, like A) — A/B experiment
-  static const bool bk = [] {
-    const char* e = std::getenv("ATC_TC_BKMAJOR");
-    return e && e[0] == '1';
-  }();
-  const bool b_kmajor = bk && k % 32 == 0 && n % 32 == 0;
+  // ATC_TC_B_KMAJOR: B transposed once to [N][K] (K-major, like A) — A/B experiment
+  const bool b_kmajor = tc_flag(ctx, ATC_TC_B_KMAJOR) && k % 32 == 0 && n % 32 == 0;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   Problem p{};
@@ -1085,12 +1063,12 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
   p.tiles_m = (int)((m + BM - 1) / BM);
   p.tiles_n = (int)((n + BN - 1) / BN);
   p.tiles_img = 1;
-  p.pair = use_pair(p);
+  p.pair = use_pair(ctx, p);
   p.splits = precision == ATC_PREC_3XTF32 ? 3 : 1;
   // TMA-store epilogue when C's row pitch is a multiple of 16 bytes
-  p.tma_store = tma_store_enabled() && (n % 4) == 0 ? 1 : 0;
+  p.tma_store = !tc_flag(ctx, ATC_TC_NO_TMA_STORE) && (n % 4) == 0 ? 1 : 0;
   // cta_group::2 (M = 256 per CTA pair) for the MN-major sgemm
-  p.umma2 = umma2_enabled() && p.conv == 0 && p.tiles_m >= 2 ? 1 : 0;
+  p.umma2 = !tc_flag(ctx, ATC_TC_NO_2SM) && p.conv == 0 && p.tiles_m >= 2 ? 1 : 0;
   if (p.tma_store && !make_map(ctx, &maps.c, dC, m, n, n, 32, 32, false)) return ATC_ERR_CUDA;
   if (b_kmajor) {
     float* bt = (float*)atc_ctx_scratch(ctx, 14, (size_t)k * n * 4 * (p.splits == 3 ? 2 : 1));
@@ -1137,7 +1115,7 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
 
 int atc_sgemm_rm(atc_ctx* ctx, const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
                  int32_t precision) {
-  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  ATC_ENTER(ctx);
   if (m < 1 || n < 1 || k < 1 || !A || !B || !C) {
     atc_set_error(ctx, "bad arguments to atc_sgemm_rm");
     return ATC_ERR_ARG;
@@ -1164,7 +1142,7 @@ int atc_sgemm_rm(atc_ctx* ctx, const float* A, const float* B, float* C, int64_t
 
 int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, float* d_out, int64_t n, int64_t c,
                            int64_t h, int64_t w_, int64_t k, int64_t r, int64_t s, int32_t precision, void* stream) {
-  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  ATC_ENTER(ctx);
   const int64_t oh = h - r + 1, ow = w_ - s + 1;
   if (n < 1 || c < 1 || h < 1 || w_ < 1 || k < 1 || r < 1 || s < 1 || oh < 1 || ow < 1 || !d_in || !d_w || !d_out ||
       (precision != ATC_PREC_TF32 && precision != ATC_PREC_3XTF32)) {
@@ -1212,14 +1190,10 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
   std::memset(&maps, 0, sizeof maps);
   // cta_group::2 (M = 256 filters per CTA pair) when there are >= 2 filter tiles;
   // each CTA then loads half of the pixel rows (K-major box of BN/2 rows)
-  const bool umma2 = umma2_enabled() && k > BM && !direct;  // (1x1 direct: slower on the pair kernel)
+  const bool umma2 = !tc_flag(ctx, ATC_TC_NO_2SM) && k > BM && !direct;  // (1x1 direct: slower on the pair kernel)
   // im2col-mode TMA on the pair kernel: tiles of compact output pixels (no input-grid
-  // waste); ATC_TC_IM2COL=0 keeps the input-grid formulation
-  static const bool im2col_on = [] {
-    const char* e = std::getenv("ATC_TC_IM2COL");
-    return !(e && e[0] == '0');
-  }();
-  const bool im2col = umma2 && im2col_on && r <= 128 && s <= 128;
+  // waste); ATC_TC_NO_IM2COL keeps the input-grid formulation
+  const bool im2col = umma2 && !tc_flag(ctx, ATC_TC_NO_IM2COL) && r <= 128 && s <= 128;
   auto bmap = [&](CUtensorMap* m, const float* base) {
     if (im2col) return make_im2col_map(ctx, m, base, n, h, w_, c, (int)r, (int)s, BN / 2);
     return direct ? make_map(ctx, m, base, n * c, hw, hw, 32, BK, true)   // [N*C][H*W], MN-major chunks
@@ -1262,11 +1236,11 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
     p.tiles_n = (int)((last + BN) / BN);
     p.tiles_img = 1;
   }
-  p.pair = use_pair(p);
+  p.pair = use_pair(ctx, p);
   p.umma2 = umma2 ? 1 : 0;
   // split-K over two CTA pairs when the pair tiles leave most of a second wave idle
   // (conv5: 98 tiles on 74 pair slots); the output is zeroed and both halves added
-  if (im2col && splits == 1 && ksplit_enabled()) {
+  if (im2col && splits == 1 && !tc_flag(ctx, ATC_TC_NO_KSPLIT)) {
     const int pairs = std::max(1, ctx->sm_count / 2);
     const int units = (p.tiles_m + 1) / 2 * p.tiles_n;
     const int kb = (int)(r * s * (c / BK));
@@ -1278,14 +1252,14 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
     }
   }
   // 1x1 direct: the output is a [N*K][OH*OW] matrix (hw % 4 == 0): TMA-store epilogue
-  p.tma_store = direct && tma_store_enabled() ? 1 : 0;
+  p.tma_store = direct && !tc_flag(ctx, ATC_TC_NO_TMA_STORE) ? 1 : 0;
   if (p.tma_store && !make_map(ctx, &maps.c, d_out, n * k, oh * ow, oh * ow, 32, 32, false)) return ATC_ERR_CUDA;
   return launch(ctx, maps, p, st) ? ATC_OK : ATC_ERR_CUDA;
 }
 
 int atc_conv2d_nchw(atc_ctx* ctx, const float* in, const float* w, float* out, int64_t n, int64_t c, int64_t h,
                     int64_t w_, int64_t k, int64_t r, int64_t s, int32_t precision) {
-  if (!ctx || ctx->broken) return ATC_ERR_DEVICE;
+  ATC_ENTER(ctx);
   const int64_t oh = h - r + 1, ow = w_ - s + 1;
   if (n < 1 || c < 1 || h < 1 || w_ < 1 || k < 1 || r < 1 || s < 1 || oh < 1 || ow < 1 || !in || !w || !out) {
     atc_set_error(ctx, "bad arguments to atc_conv2d_nchw");

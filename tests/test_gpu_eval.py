@@ -293,24 +293,40 @@ def test_enumerated_many_matches_single(ev):
     sweep.close()
 
 
-def test_conv_screen_kernels_agree():
-    """k_screen_conv_pairs (default), k_screen_conv_planes (ATC_SCREEN_PLANES=1) and
-    the generic k_screen_rows (ATC_SCREEN_GENERIC=1) give identical passing sets and
-    reason histograms (each run in its own process: the switches are read once)."""
-    import json
-    import os
-    import subprocess
-    import sys
+SCREEN_CASES = [("conv_direct", "in_700_out_900", 0, 1 << 21), ("conv_permuted_sig", "wt_200", 1234567, 1234567 + 999_999),
+                ("im2col_buffered", "recorded", 0, None), ("conv_direct", "zero_int", 17, 2_000_017),
+                ("winograd_1d", "in_3000", 5_000_000, 9_000_000)]
 
-    script = os.path.join(os.path.dirname(__file__), "screen_variant_run.py")
+
+def test_conv_screen_kernels_agree():
+    """k_screen_conv_pairs (default), k_screen_conv_planes (ATC_CONV_SCREEN_PLANES) and
+    the generic k_screen_rows (ATC_CONV_SCREEN_GENERIC), selected per context with
+    atc_set_option, give identical passing sets and reason histograms."""
     res = {}
-    for name, env in (("pairs", {}), ("planes", {"ATC_SCREEN_PLANES": "1"}), ("generic", {"ATC_SCREEN_GENERIC": "1"})):
-        out = subprocess.run([sys.executable, script], env={**os.environ, **env}, capture_output=True, text=True,
-                             timeout=600)
-        assert out.returncode == 0, out.stderr[-2000:]
-        res[name] = json.loads(out.stdout.strip().splitlines()[-1])
+    for name, opt in (("pairs", L.CONV_SCREEN_AUTO), ("planes", L.CONV_SCREEN_PLANES),
+                      ("generic", L.CONV_SCREEN_GENERIC)):
+        ctx = L.Context(0)
+        ctx.set_option(L.OPT_CONV_SCREEN, opt)
+        e = Evaluator(ctx)
+        out = []
+        for stem, variant, b, end in SCREEN_CASES:
+            p = fixtures.load(stem)
+            space = p.space("conv2d")
+            ts = CONV_VARIANTS[variant](p.testsets(16))
+            passing, n, hist = e.eval_enumerated(fixtures.spec("conv2d"), ts, space, b,
+                                                 space.count if end is None else end)
+            out.append((passing.tolist(), n, hist.tolist()))
+        res[name] = out
+        ctx.close()
     assert res["pairs"] == res["planes"] == res["generic"]
-    assert any(r["hist"][4] for r in res["pairs"]) and any(r["hist"][2] for r in res["pairs"])
+    assert any(r[2][4] for r in res["pairs"]) and any(r[2][2] for r in res["pairs"])
+
+
+def test_set_option_rejects_bad_values(ev):
+    with pytest.raises(L.AtcError):
+        ev.ctx.set_option(L.OPT_CONV_SCREEN, 7)
+    with pytest.raises(L.AtcError):
+        ev.ctx.set_option(99, 0)
 
 
 @pytest.mark.parametrize("stem", ["naive_f32", "conv_direct", "naive_ld", "im2col_buffered", "strassen_staged"])

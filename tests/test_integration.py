@@ -58,12 +58,29 @@ def test_adapter_gpu_dispatch_bit_identical():
 
 
 def test_adapter_unpruned_stress_space():
-    """naive_ld x gemm_rowmajor_ld (279,936 bindings) as one ranked list: the GPU
-    screen leaves one survivor, host P1 accepts it (index 44790, the identity)."""
+    """naive_ld x gemm_rowmajor_ld (279,936 bindings): gpu::first_accepted_unpruned on
+    the device group (every visible GPU; enumerated P2 sharded over the members, host
+    P1 on the survivors) and the same space as one explicit ranked list on one context
+    agree — the GPU screen leaves one survivor, host P1 accepts it (index 44790, the
+    identity)."""
     rc, lines, err = _run("unpruned", "naive_ld", "gemm_rowmajor_ld", "10")
-    assert rc == 0, err
+    assert rc == 0, err + json.dumps(lines)[:2000]
     j = lines[-1]
-    assert j["bindings"] == 279936 and j["p2_passed"] == 1 and j["winner"] == 44790 and j["p1_calls"] == 1
+    assert j["bindings"] == 279936 and j["same"]
+    for k in ("group", "list"):
+        assert j[k]["p2_passed"] == 1 and j[k]["winner"] == 44790 and j[k]["p1_calls"] == 1
+
+
+def test_adapter_unpruned_conv_space_on_group():
+    """conv_direct x conv2d — all 2,324,522,934 bindings of the unpruned space through
+    the adapter on the device group (no explicit list could hold it): P1 accepts the
+    reference's pruned winner, the identity binding at index 381367044."""
+    rc, lines, err = _run("unpruned", "conv_direct", "conv2d", "10")
+    assert rc == 0, err + json.dumps(lines)[:2000]
+    j = lines[-1]
+    assert j["bindings"] == 2324522934 and j["same"] and "list" not in j
+    g = j["group"]
+    assert g["winner"] == 381367044 and g["p2_passed"] >= 1 and sum(g["reason_counts"]) == 2324522934
 
 
 def test_adapter_routed_dispatch():

@@ -187,3 +187,23 @@ def test_packed_reduce_roundtrip():
     (p0, f0, h0, c0), (p1, f1, h1, c1) = shard.combine(blocks)
     assert p0 == [3, 5, 9] and f0 == 3 and h0.tolist() == [2, 2, 3, 1, 0] and c0
     assert f1 == 0 and not c1 and h1.tolist() == [40, 4, 0, 0, 0]
+
+
+def test_c_plan_equals_python_plan():
+    """atc_plan_shards (the library's shard plan, used by atc_group_*) is the same
+    rule as workloads.plan_shards for every rank of N = 1, 2, 3, 4, 8 on the corpus
+    spaces and on synthetic mixes (host arithmetic: runs without a GPU)."""
+    from types import SimpleNamespace
+
+    from paper_2301_11659_b200 import group, workloads
+
+    corpus = [j.count for j in workloads.corpus_jobs()]
+    rng = np.random.default_rng(7)
+    mixes = [corpus, [1 << 30, 1 << 24, 5, (1 << 24) - 1, 9 * (1 << 30), 3],
+             [int(x) for x in rng.integers(1, 1 << 34, size=23)] + [int(x) for x in rng.integers(1, 1 << 20, size=9)]]
+    for counts in mixes:
+        jobs = [SimpleNamespace(count=c) for c in counts]
+        for world in (1, 2, 3, 4, 8):
+            cplan = group.plan_shards(counts, world)
+            for r in range(world):
+                assert cplan[r] == [tuple(x) for x in workloads.plan_shards(jobs, r, world)], (world, r)
