@@ -304,8 +304,7 @@ int cmd_details(atc_ctx* ctx, int per_space) {
       gpu::UnprunedSpace sp(fn, spec);
       if (sp.count() == 0) continue;
       // a wide strided sample screened on the GPU, then up to per_space rejected
-      // bindings of each failure reason re-run through the reference (conv spaces
-      // hold dispatch failures — oh = h - r + 1 < 1 — that a narrow sample can miss)
+      // bindings of each failure reason re-run through the reference
       std::vector<matching::CandidateBinding> list;
       const size_t wide = 64 * (size_t)per_space;
       const size_t stride = std::max<size_t>(1, sp.count() / wide);

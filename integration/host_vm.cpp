@@ -1,0 +1,764 @@
+// See host_vm.hpp.  Every rule below cites the reference interpreter
+// (/root/reference/proj/src/interp.cpp) line it restates.
+#include "host_vm.hpp"
+
+#include <cmath>
+#include <stdexcept>
+
+namespace liftc::gpu {
+
+using namespace minilang;
+using interp::ExecMode;
+using interp::ExecStatus;
+
+namespace {
+
+constexpr int kMaxCallDepth = 1024;       // interp.cpp:10
+constexpr size_t kTraceCap = 1u << 20;    // interp.cpp:11
+
+// ------------------------------------------------------------------ IR --
+enum class EK : uint8_t {
+  IntLit, FloatLit, Var, Index, Neg, Not, Bin, And, Or, Min, Max, ToI64, ToF64, Fabs, Sqrt, Dispatch, Call
+};
+
+struct CExpr {
+  EK k = EK::IntLit;
+  BinOp op = BinOp::Add;
+  int slot = -1;            // Var / Index (pointer slot)
+  long long i = 0;
+  double f = 0.0;
+  int fn = -1;              // Call: callee index
+  std::vector<int> args;    // child expressions (Call: one per param; pointer params are Var)
+};
+
+enum class SK : uint8_t {
+  Let, Assign, Store, For, While, If, Call, Return, VLoad, VStore, VSplat, VAdd, VMul, VFma, VReduce
+};
+
+struct CStmt {
+  SK k = SK::Let;
+  LocalType lt = LocalType::I64;
+  int slot = -1;             // Let / Assign / For var / VReduce target / vec dst
+  int ptr = -1;              // Store / VLoad / VStore pointer slot
+  int e0 = -1, e1 = -1, e2 = -1;  // Let init | Assign value | Store index,value | For lo,hi,step | cond | call | ret
+  int va = -1, vb = -1;      // vector operand slots
+  int width = 4;
+  std::vector<int> body, els;
+};
+
+struct CFunc {
+  const FunctionIR* ir = nullptr;
+  int n_slots = 0;
+  std::vector<CExpr> ex;
+  std::vector<CStmt> st;
+  std::vector<int> body;
+};
+
+}  // namespace
+
+struct VmProgram {
+  std::vector<CFunc> fns;
+  std::map<std::string, int> index;
+};
+
+namespace {
+
+// --------------------------------------------------------- compilation --
+struct Compiler {
+  VmProgram& P;
+  CFunc& F;
+  std::vector<std::map<std::string, int>> scopes;
+
+  int declare(const std::string& name) {
+    const int s = F.n_slots++;
+    scopes.back()[name] = s;
+    return s;
+  }
+  int lookup(const std::string& name) {
+    for (auto it = scopes.rbegin(); it != scopes.rend(); ++it) {
+      auto f = it->find(name);
+      if (f != it->end()) return f->second;
+    }
+    throw std::runtime_error("host_vm: unbound identifier '" + name + "'");
+  }
+
+  int expr(const Expr& e) {
+    CExpr c;
+    switch (e.kind) {
+      case Expr::Kind::IntLit:
+        c.k = EK::IntLit;
+        c.i = e.int_val;
+        break;
+      case Expr::Kind::FloatLit:
+        c.k = EK::FloatLit;
+        c.f = e.float_val;
+        break;
+      case Expr::Kind::Var:
+        c.k = EK::Var;
+        c.slot = lookup(e.name);
+        break;
+      case Expr::Kind::Index:
+        c.k = EK::Index;
+        c.slot = lookup(e.name);
+        c.args.push_back(expr(*e.args[0]));
+        break;
+      case Expr::Kind::Unary:
+        c.k = e.uop == UnOp::Not ? EK::Not : EK::Neg;
+        c.args.push_back(expr(*e.args[0]));
+        break;
+      case Expr::Kind::Binary:
+        c.k = e.bop == BinOp::And ? EK::And : e.bop == BinOp::Or ? EK::Or : EK::Bin;
+        c.op = e.bop;
+        c.args.push_back(expr(*e.args[0]));
+        c.args.push_back(expr(*e.args[1]));
+        break;
+      case Expr::Kind::Call: {
+        const std::string& n = e.name;
+        if (n == "min" || n == "max") c.k = n == "min" ? EK::Min : EK::Max;
+        else if (n == "to_i64") c.k = EK::ToI64;
+        else if (n == "to_f64") c.k = EK::ToF64;
+        else if (n == "fabs") c.k = EK::Fabs;
+        else if (n == "sqrt") c.k = EK::Sqrt;
+        else if (is_dispatch_builtin(n)) {
+          c.k = EK::Dispatch;  // no handler: a no-op whose arguments are never evaluated (interp.cpp:506)
+          break;
+        } else {
+          c.k = EK::Call;
+          auto it = P.index.find(n);
+          c.fn = it == P.index.end() ? -1 : it->second;  // -1: "call to unknown function" at run time
+        }
+        if (c.k == EK::Call && c.fn >= 0) {
+          const FunctionIR* callee = P.fns[c.fn].ir;
+          for (size_t i = 0; i < e.args.size(); ++i) {
+            if (i < callee->params.size() && callee->params[i].kind == ParamKind::Pointer) {
+              CExpr v;
+              v.k = EK::Var;
+              v.slot = lookup(e.args[i]->name);
+              F.ex.push_back(v);
+              c.args.push_back((int)F.ex.size() - 1);
+            } else {
+              c.args.push_back(expr(*e.args[i]));
+            }
+          }
+        } else if (c.k != EK::Call) {
+          for (const auto& a : e.args) c.args.push_back(expr(*a));
+        }
+        break;
+      }
+    }
+    F.ex.push_back(std::move(c));
+    return (int)F.ex.size() - 1;
+  }
+
+  std::vector<int> block(const std::vector<StmtPtr>& body, bool new_scope) {
+    if (new_scope) scopes.emplace_back();
+    std::vector<int> out;
+    for (const auto& s : body) out.push_back(stmt(*s));
+    if (new_scope) scopes.pop_back();
+    return out;
+  }
+
+  int stmt(const Stmt& s) {
+    CStmt c;
+    switch (s.kind) {
+      case Stmt::Kind::Let:
+        c.k = SK::Let;
+        c.lt = s.let_type;
+        c.e0 = s.let_init ? expr(*s.let_init) : -1;  // evaluated before the declaration
+        c.slot = declare(s.let_name);
+        break;
+      case Stmt::Kind::Assign:
+        c.k = SK::Assign;
+        c.e0 = expr(*s.value);
+        c.slot = lookup(s.target);
+        break;
+      case Stmt::Kind::Store:
+        c.k = SK::Store;
+        c.e0 = expr(*s.index);
+        c.e1 = expr(*s.value);
+        c.ptr = lookup(s.target);
+        break;
+      case Stmt::Kind::For:
+        c.k = SK::For;
+        c.e0 = expr(*s.lo);
+        c.e1 = expr(*s.hi);
+        c.e2 = s.step ? expr(*s.step) : -1;
+        scopes.emplace_back();  // the iteration scope: loop var + body (interp.cpp:304-311)
+        c.slot = declare(s.loop_var);
+        c.body = block(s.body, false);
+        scopes.pop_back();
+        break;
+      case Stmt::Kind::While:
+        c.k = SK::While;
+        c.e0 = expr(*s.cond);
+        c.body = block(s.body, true);
+        break;
+      case Stmt::Kind::If:
+        c.k = SK::If;
+        c.e0 = expr(*s.cond);
+        c.body = block(s.body, true);
+        c.els = block(s.else_body, true);
+        break;
+      case Stmt::Kind::CallStmt:
+        c.k = SK::Call;
+        c.e0 = expr(*s.call);
+        break;
+      case Stmt::Kind::Return:
+        c.k = SK::Return;
+        c.e0 = s.value ? expr(*s.value) : -1;
+        break;
+      case Stmt::Kind::Vec:
+        c.width = s.vec_width;
+        switch (s.vec_op) {
+          case VecOp::Load:
+            c.k = SK::VLoad;
+            c.e0 = expr(*s.index);
+            c.slot = lookup(s.vec_dst);
+            c.ptr = lookup(s.target);
+            break;
+          case VecOp::Store:
+            c.k = SK::VStore;
+            c.e0 = expr(*s.index);
+            c.va = lookup(s.vec_a);
+            c.ptr = lookup(s.target);
+            break;
+          case VecOp::Splat:
+            c.k = SK::VSplat;
+            c.e0 = expr(*s.value);
+            c.slot = lookup(s.vec_dst);
+            break;
+          case VecOp::Add:
+          case VecOp::Mul:
+          case VecOp::Fma:
+            c.k = s.vec_op == VecOp::Add ? SK::VAdd : s.vec_op == VecOp::Mul ? SK::VMul : SK::VFma;
+            c.va = lookup(s.vec_a);
+            c.vb = lookup(s.vec_b);
+            c.slot = lookup(s.vec_dst);
+            break;
+          case VecOp::Reduce:
+            c.k = SK::VReduce;
+            c.va = lookup(s.vec_a);
+            c.slot = lookup(s.target);
+            break;
+        }
+        break;
+    }
+    F.st.push_back(std::move(c));
+    return (int)F.st.size() - 1;
+  }
+};
+
+// ------------------------------------------------------------ runtime --
+struct Fault {
+  ExecStatus status;
+  std::string msg;
+};
+
+struct Val {  // interp.cpp:20-29 (floats carry i == 0)
+  bool is_int = true;
+  long long i = 0;
+  double f = 0.0;
+  static Val I(long long v) { return Val{true, v, 0.0}; }
+  static Val F(double v) { return Val{false, 0, v}; }
+  double d() const { return is_int ? (double)i : f; }
+  bool truthy() const { return is_int ? i != 0 : f != 0.0; }
+};
+
+struct Slot {  // interp.cpp:31-39
+  Val v;
+  bool round_f32 = false;
+  int region = -1;
+  double lanes[8] = {};
+};
+
+enum class Flow { Next, Ret };
+
+struct Run {
+  const VmProgram& P;
+  ExecMode mode;
+  unsigned long long limit, steps = 0;
+  // regions: index = position among the root's pointer params
+  std::vector<std::string> keys;
+  std::vector<interp::Region*> reg;  // Plain: the region in the output image
+  std::vector<std::vector<bool>*> wr;  // Plain + track_writes
+  // DimProbe: target region index (-2: every region — the survey), extent, scratch
+  int target = -1;
+  long long extent = 0;
+  double scratch = 1.0;
+  bool record = false;
+  std::vector<std::vector<long long>> trace;
+  std::vector<long long> maxoff;
+  std::vector<char> dead;  // survey: this region's own run has ended (OutOfBounds)
+  std::vector<std::string> dead_msg;
+  std::vector<Slot> stack;
+  size_t base = 0;
+  int depth = 0;
+  Val ret;
+  bool has_ret = false;
+
+  Run(const VmProgram& p, ExecMode m, unsigned long long lim) : P(p), mode(m), limit(lim) {}
+
+  Slot& S(int s) { return stack[base + (size_t)s]; }
+
+  void step() {  // interp.cpp:282-285
+    if (++steps > limit) throw Fault{ExecStatus::StepLimit, "statement budget exhausted"};
+  }
+
+  void note(int r, long long off) {  // interp.cpp:213-216
+    if (record && trace[r].size() < kTraceCap) trace[r].push_back(off);
+    if (off > maxoff[r]) maxoff[r] = off;
+  }
+
+  double load(int r, long long off) {
+    if (mode == ExecMode::DimProbe) {  // interp.cpp:219-227
+      if (target == -2) {
+        if (r < 0 || dead[r]) return scratch;
+        note(r, off);
+        if (off < 0 || off >= extent) {
+          dead[r] = 1;
+          dead_msg[r] = "load offset " + std::to_string(off) + " outside extent " + std::to_string(extent);
+        }
+        return scratch;
+      }
+      if (r != target) return scratch;
+      note(r, off);
+      if (off < 0 || off >= extent)
+        throw Fault{ExecStatus::OutOfBounds,
+                    "load offset " + std::to_string(off) + " outside extent " + std::to_string(extent)};
+      return scratch;
+    }
+    interp::Region& R = *reg[r];  // interp.cpp:228-232
+    if (off < 0 || off >= (long long)R.data.size())
+      throw Fault{ExecStatus::RuntimeFault, "load offset " + std::to_string(off) + " outside region '" + keys[r] + "'"};
+    return R.data[(size_t)off];
+  }
+
+  void store(int r, long long off, double v) {
+    if (mode == ExecMode::DimProbe) {  // interp.cpp:235-244
+      if (target == -2) {
+        if (r < 0 || dead[r]) return;
+        note(r, off);
+        if (off < 0 || off >= extent) {
+          dead[r] = 1;
+          dead_msg[r] = "store offset " + std::to_string(off) + " outside extent " + std::to_string(extent);
+        }
+        return;
+      }
+      if (r != target) return;
+      note(r, off);
+      if (off < 0 || off >= extent)
+        throw Fault{ExecStatus::OutOfBounds,
+                    "store offset " + std::to_string(off) + " outside extent " + std::to_string(extent)};
+      return;
+    }
+    interp::Region& R = *reg[r];  // interp.cpp:245-251
+    if (off < 0 || off >= (long long)R.data.size())
+      throw Fault{ExecStatus::RuntimeFault,
+                  "store offset " + std::to_string(off) + " outside region '" + keys[r] + "'"};
+    R.data[(size_t)off] = R.elem == ScalarType::F32 ? (double)(float)v : v;
+    if (wr[r]) (*wr[r])[(size_t)off] = true;
+  }
+
+  // ----------------------------------------------------------- calls --
+  // interp.cpp:145-170: frame, parameters, body, return rounding
+  Val call(int fi, std::vector<Slot>& args, bool& has) {
+    const CFunc& F = P.fns[fi];
+    if (depth >= kMaxCallDepth)
+      throw Fault{ExecStatus::RuntimeFault, "call depth limit exceeded in '" + F.ir->name + "'"};
+    const size_t saved = base;
+    const size_t nb = stack.size();
+    stack.resize(nb + (size_t)F.n_slots);
+    for (size_t i = 0; i < args.size(); ++i) stack[nb + i] = args[i];
+    base = nb;
+    ++depth;
+    has_ret = false;
+    exec_list(F, F.body);
+    Val r = ret;
+    has = has_ret;
+    has_ret = false;
+    --depth;
+    base = saved;
+    stack.resize(nb);
+    if (has) {
+      if (F.ir->ret == RetType::F32)
+        r = Val::F((double)(float)r.d());
+      else if (F.ir->ret == RetType::F64)
+        r = Val::F(r.d());
+      else if (F.ir->ret == RetType::I64 && !r.is_int)
+        throw Fault{ExecStatus::RuntimeFault, "float returned from i64 function"};
+    }
+    return r;
+  }
+
+  // ----------------------------------------------------- expressions --
+  Val eval(const CFunc& F, int ei) {
+    const CExpr& e = F.ex[ei];
+    switch (e.k) {
+      case EK::IntLit:
+        return Val::I(e.i);
+      case EK::FloatLit:
+        return Val::F(e.f);
+      case EK::Var:
+        return S(e.slot).v;
+      case EK::Index: {  // interp.cpp:416-419
+        const long long off = eval(F, e.args[0]).i;
+        return Val::F(load(S(e.slot).region, off));
+      }
+      case EK::Not:
+        return Val::I(eval(F, e.args[0]).truthy() ? 0 : 1);
+      case EK::Neg: {
+        const Val v = eval(F, e.args[0]);
+        return v.is_int ? Val::I(-v.i) : Val::F(-v.f);
+      }
+      case EK::And:  // interp.cpp:434-441
+        if (!eval(F, e.args[0]).truthy()) return Val::I(0);
+        return Val::I(eval(F, e.args[1]).truthy() ? 1 : 0);
+      case EK::Or:
+        if (eval(F, e.args[0]).truthy()) return Val::I(1);
+        return Val::I(eval(F, e.args[1]).truthy() ? 1 : 0);
+      case EK::Bin:
+        return binary(e.op, eval(F, e.args[0]), eval(F, e.args[1]));
+      case EK::Min:
+      case EK::Max: {  // interp.cpp:483-488
+        const long long a = eval(F, e.args[0]).i;
+        const long long b = eval(F, e.args[1]).i;
+        const bool lt = a < b;
+        return Val::I(e.k == EK::Min ? (lt ? a : b) : (lt ? b : a));
+      }
+      case EK::ToI64: {
+        const Val v = eval(F, e.args[0]);
+        return v.is_int ? v : Val::I((long long)v.f);
+      }
+      case EK::ToF64:
+        return Val::F(eval(F, e.args[0]).d());
+      case EK::Fabs:
+        return Val::F(std::fabs(eval(F, e.args[0]).d()));
+      case EK::Sqrt: {
+        const double v = eval(F, e.args[0]).d();
+        if (v < 0.0) throw Fault{ExecStatus::RuntimeFault, "sqrt of a negative value"};
+        return Val::F(std::sqrt(v));
+      }
+      case EK::Dispatch:
+        return Val::I(0);
+      case EK::Call: {  // interp.cpp:503-524
+        if (e.fn < 0) throw Fault{ExecStatus::RuntimeFault, "call to unknown function"};
+        const FunctionIR* callee = P.fns[e.fn].ir;
+        std::vector<Slot> args(e.args.size());
+        for (size_t i = 0; i < e.args.size(); ++i) {
+          const Param& p = callee->params[i];
+          Slot& s = args[i];
+          if (p.kind == ParamKind::Pointer) {
+            s.region = S(F.ex[e.args[i]].slot).region;
+          } else {
+            const Val v = eval(F, e.args[i]);
+            if (p.kind == ParamKind::FloatScalar) {
+              s.round_f32 = p.elem == ScalarType::F32;
+              s.v = Val::F(s.round_f32 ? (double)(float)v.d() : v.d());
+            } else {
+              s.v = v;
+            }
+          }
+        }
+        bool has = false;
+        const Val r = call(e.fn, args, has);
+        return has ? r : Val::I(0);
+      }
+    }
+    return Val::I(0);
+  }
+
+  static Val binary(BinOp op, const Val& a, const Val& b) {  // interp.cpp:443-477
+    const bool fl = !a.is_int || !b.is_int;
+    switch (op) {
+      case BinOp::Add: return fl ? Val::F(a.d() + b.d()) : Val::I(a.i + b.i);
+      case BinOp::Sub: return fl ? Val::F(a.d() - b.d()) : Val::I(a.i - b.i);
+      case BinOp::Mul: return fl ? Val::F(a.d() * b.d()) : Val::I(a.i * b.i);
+      case BinOp::Div:
+        if (fl) {
+          if (b.d() == 0.0) throw Fault{ExecStatus::RuntimeFault, "float division by zero"};
+          return Val::F(a.d() / b.d());
+        }
+        if (b.i == 0) throw Fault{ExecStatus::RuntimeFault, "integer division by zero"};
+        return Val::I(a.i / b.i);
+      case BinOp::Mod:
+        if (b.i == 0) throw Fault{ExecStatus::RuntimeFault, "integer modulo by zero"};
+        return Val::I(a.i % b.i);
+      case BinOp::Lt: return Val::I(fl ? a.d() < b.d() : a.i < b.i);
+      case BinOp::Le: return Val::I(fl ? a.d() <= b.d() : a.i <= b.i);
+      case BinOp::Gt: return Val::I(fl ? a.d() > b.d() : a.i > b.i);
+      case BinOp::Ge: return Val::I(fl ? a.d() >= b.d() : a.i >= b.i);
+      case BinOp::Eq: return Val::I(fl ? a.d() == b.d() : a.i == b.i);
+      case BinOp::Ne: return Val::I(fl ? a.d() != b.d() : a.i != b.i);
+      default: throw Fault{ExecStatus::RuntimeFault, "bad binary operator"};
+    }
+  }
+
+  // ------------------------------------------------------ statements --
+  Flow exec_list(const CFunc& F, const std::vector<int>& body) {
+    for (int si : body)
+      if (exec(F, F.st[si]) == Flow::Ret) return Flow::Ret;
+    return Flow::Next;
+  }
+
+  Flow exec(const CFunc& F, const CStmt& s) {
+    step();
+    switch (s.k) {
+      case SK::Let: {  // interp.cpp:290-321
+        Slot slot;
+        switch (s.lt) {
+          case LocalType::I64: slot.v = Val::I(0); break;
+          case LocalType::F32: slot.round_f32 = true; slot.v = Val::F(0.0); break;
+          case LocalType::F64: slot.v = Val::F(0.0); break;
+          default: break;  // Vec4/Vec8: zero lanes
+        }
+        if (s.e0 >= 0) {
+          const Val v = eval(F, s.e0);
+          if (s.lt == LocalType::I64)
+            slot.v = v;
+          else
+            slot.v = Val::F(slot.round_f32 ? (double)(float)v.d() : v.d());
+        }
+        S(s.slot) = slot;
+        return Flow::Next;
+      }
+      case SK::Assign: {  // interp.cpp:323-331
+        const Val v = eval(F, s.e0);
+        Slot& slot = S(s.slot);
+        if (slot.v.is_int)
+          slot.v = v;
+        else
+          slot.v = Val::F(slot.round_f32 ? (double)(float)v.d() : v.d());
+        return Flow::Next;
+      }
+      case SK::Store: {  // interp.cpp:333-337
+        const long long off = eval(F, s.e0).i;
+        const Val v = eval(F, s.e1);
+        store(S(s.ptr).region, off, v.d());
+        return Flow::Next;
+      }
+      case SK::For: {  // interp.cpp:339-353
+        const long long lo = eval(F, s.e0).i;
+        const long long hi = eval(F, s.e1).i;
+        const long long st = s.e2 >= 0 ? eval(F, s.e2).i : 1;
+        if (st <= 0) throw Fault{ExecStatus::RuntimeFault, "loop step must be positive"};
+        for (long long iv = lo; iv < hi; iv += st) {
+          Slot& lv = S(s.slot);
+          lv = Slot{};
+          lv.v = Val::I(iv);
+          if (exec_list(F, s.body) == Flow::Ret) return Flow::Ret;
+        }
+        return Flow::Next;
+      }
+      case SK::While:  // interp.cpp:354-359
+        while (eval(F, s.e0).truthy()) {
+          step();
+          if (exec_list(F, s.body) == Flow::Ret) return Flow::Ret;
+        }
+        return Flow::Next;
+      case SK::If:
+        return exec_list(F, eval(F, s.e0).truthy() ? s.body : s.els);
+      case SK::Call:
+        eval(F, s.e0);
+        return Flow::Next;
+      case SK::Return:  // interp.cpp:368-375
+        has_ret = false;
+        if (s.e0 >= 0) {
+          ret = eval(F, s.e0);
+          has_ret = true;
+        }
+        return Flow::Ret;
+      case SK::VLoad: {  // interp.cpp:385-391
+        const long long b = eval(F, s.e0).i;
+        const int r = S(s.ptr).region;
+        for (int l = 0; l < s.width; ++l) {
+          const double x = load(r, b + l);
+          S(s.slot).lanes[l] = x;
+        }
+        return Flow::Next;
+      }
+      case SK::VStore: {
+        const long long b = eval(F, s.e0).i;
+        const int r = S(s.ptr).region;
+        for (int l = 0; l < s.width; ++l) store(r, b + l, S(s.va).lanes[l]);
+        return Flow::Next;
+      }
+      case SK::VSplat: {
+        const double v = eval(F, s.e0).d();
+        for (int l = 0; l < s.width; ++l) S(s.slot).lanes[l] = v;
+        return Flow::Next;
+      }
+      case SK::VAdd:
+      case SK::VMul:
+      case SK::VFma: {  // interp.cpp:405-420
+        for (int l = 0; l < s.width; ++l) {
+          const double a = S(s.va).lanes[l], b = S(s.vb).lanes[l];
+          double& d = S(s.slot).lanes[l];
+          if (s.k == SK::VAdd)
+            d = a + b;
+          else if (s.k == SK::VMul)
+            d = a * b;
+          else
+            d += a * b;
+        }
+        return Flow::Next;
+      }
+      case SK::VReduce: {  // interp.cpp:421-428
+        double sum = 0.0;
+        for (int l = 0; l < s.width; ++l) sum += S(s.va).lanes[l];
+        Slot& d = S(s.slot);
+        d.v = Val::F(d.round_f32 ? (double)(float)sum : sum);
+        return Flow::Next;
+      }
+    }
+    return Flow::Next;
+  }
+};
+
+// Root arguments (interp.cpp:98-135) in parameter order: ints, floats, pointers.
+std::vector<Slot> root_args(Run& R, const FunctionIR& f, const interp::MemoryImage& mem) {
+  std::vector<Slot> args;
+  for (const auto& p : f.params) {
+    Slot s;
+    switch (p.kind) {
+      case ParamKind::IntScalar: {
+        auto it = mem.int_args.find(p.name);
+        if (it == mem.int_args.end())
+          throw Fault{ExecStatus::RuntimeFault, "missing integer argument '" + p.name + "'"};
+        s.v = Val::I(it->second);
+        break;
+      }
+      case ParamKind::FloatScalar: {
+        auto it = mem.float_args.find(p.name);
+        if (it == mem.float_args.end())
+          throw Fault{ExecStatus::RuntimeFault, "missing float argument '" + p.name + "'"};
+        s.round_f32 = p.elem == ScalarType::F32;
+        s.v = Val::F(s.round_f32 ? (double)(float)it->second : it->second);
+        break;
+      }
+      case ParamKind::Pointer: {
+        if (R.mode == ExecMode::Plain && !mem.regions.count(p.name))
+          throw Fault{ExecStatus::RuntimeFault, "missing region '" + p.name + "'"};
+        s.region = (int)R.keys.size();
+        R.keys.push_back(p.name);
+        break;
+      }
+    }
+    args.push_back(s);
+  }
+  return args;
+}
+
+}  // namespace
+
+HostVm::HostVm(const Program& prog) : prog_(std::make_unique<VmProgram>()) {
+  VmProgram& P = *prog_;
+  P.fns.resize(prog.functions.size());
+  for (size_t i = 0; i < prog.functions.size(); ++i) {
+    P.fns[i].ir = &prog.functions[i];
+    P.index.emplace(prog.functions[i].name, (int)i);
+  }
+  for (auto& F : P.fns) {
+    Compiler c{P, F, {}};
+    c.scopes.emplace_back();
+    for (const auto& p : F.ir->params) c.declare(p.name);
+    F.body = c.block(F.ir->body, true);
+  }
+}
+
+HostVm::~HostVm() = default;
+
+interp::ExecutionOutcome HostVm::execute(const std::string& function, const interp::MemoryImage& input,
+                                         const interp::InstrumentationPolicy& policy,
+                                         unsigned long long step_limit) const {
+  if (policy.dispatch && policy.dispatch->handler)
+    throw std::logic_error("HostVm: dispatch handlers run on the reference interpreter");
+  interp::ExecutionOutcome out;
+  Run R(*prog_, policy.mode, step_limit);
+  interp::MemoryImage mem = input;
+  std::map<std::string, std::vector<bool>> writes;
+  if (policy.mode == ExecMode::Plain && policy.track_writes)
+    for (const auto& [name, r] : mem.regions) writes[name].assign(r.data.size(), false);
+  R.scratch = policy.scratch_value;
+  R.extent = policy.target_extent;
+  R.record = policy.record_trace;
+  auto fit = prog_->index.find(function);
+  try {
+    if (fit == prog_->index.end())
+      throw Fault{ExecStatus::RuntimeFault, "no function named '" + function + "'"};
+    const FunctionIR& f = *prog_->fns[fit->second].ir;
+    std::vector<Slot> args = root_args(R, f, mem);
+    const size_t nr = R.keys.size();
+    R.trace.assign(nr, {});
+    R.maxoff.assign(nr, -1);
+    for (size_t r = 0; r < nr; ++r) {
+      if (policy.mode == ExecMode::DimProbe && R.keys[r] == policy.target) R.target = (int)r;
+      auto it = mem.regions.find(R.keys[r]);
+      R.reg.push_back(it == mem.regions.end() ? nullptr : &it->second);
+      auto w = writes.find(R.keys[r]);
+      R.wr.push_back(w == writes.end() ? nullptr : &w->second);
+    }
+    bool has = false;
+    const Val rv = R.call(fit->second, args, has);
+    out.status = ExecStatus::Normal;
+    out.has_ret = has;
+    if (has) {
+      out.ret_is_int = rv.is_int;
+      out.ret_int = rv.i;
+      out.ret_float = rv.f;
+    }
+    out.final = std::move(mem);
+    out.writes = std::move(writes);
+    if (R.target >= 0) out.trace = std::move(R.trace[R.target]);
+  } catch (const Fault& flt) {
+    out.status = flt.status;
+    out.fault_msg = flt.msg;
+  }
+  out.steps = R.steps;
+  out.max_target_offset = R.target >= 0 && (size_t)R.target < R.maxoff.size() ? R.maxoff[R.target] : -1;
+  return out;
+}
+
+std::map<std::string, HostVm::Survey> HostVm::dim_survey(const std::string& function,
+                                                         const interp::MemoryImage& input,
+                                                         unsigned long long step_limit) const {
+  std::map<std::string, Survey> out;
+  Run R(*prog_, ExecMode::DimProbe, step_limit);
+  R.target = -2;
+  R.extent = interp::kUnboundedExtent;
+  R.scratch = 1.0;  // InstrumentationPolicy::scratch_value default
+  R.record = true;
+  auto fit = prog_->index.find(function);
+  if (fit == prog_->index.end()) return out;
+  const FunctionIR& f = *prog_->fns[fit->second].ir;
+  ExecStatus status = ExecStatus::Normal;
+  std::string msg;
+  try {
+    std::vector<Slot> args = root_args(R, f, input);
+    const size_t nr = R.keys.size();
+    R.trace.assign(nr, {});
+    R.maxoff.assign(nr, -1);
+    R.dead.assign(nr, 0);
+    R.dead_msg.assign(nr, {});
+    bool has = false;
+    R.call(fit->second, args, has);
+  } catch (const Fault& flt) {
+    status = flt.status;
+    msg = flt.msg;
+  }
+  for (size_t r = 0; r < R.keys.size(); ++r) {
+    Survey s;
+    s.max_target_offset = r < R.maxoff.size() ? R.maxoff[r] : -1;
+    if (r < R.dead.size() && R.dead[r]) {
+      s.status = ExecStatus::OutOfBounds;
+      s.fault_msg = R.dead_msg[r];
+    } else {
+      s.status = status;
+      s.fault_msg = msg;
+      if (status == ExecStatus::Normal && r < R.trace.size()) s.trace = std::move(R.trace[r]);
+    }
+    out[R.keys[r]] = std::move(s);
+  }
+  return out;
+}
+
+}  // namespace liftc::gpu

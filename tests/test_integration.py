@@ -47,7 +47,12 @@ def test_adapter_p2_details_match_verify_rewrite():
     assert rc == 0, err + json.dumps(lines[:5])[:4000]
     last = lines[-1]
     assert last["mismatches"] == 0 and last["checked"] > 1000
-    assert last["kinds"].get("mismatch", 0) > 0 and last["kinds"].get("dispatch failed", 0) > 0
+    # every corpus rejection is a mismatch: with 65,536-element probe regions and
+    # sizes drawn in [2, 8] (or the sidecars' small ranges) no extent check of
+    # run_dispatch (rewriter.cpp:136-148) can fail, so "dispatch failed" details
+    # never arise on recorded corpus test sets (the dispatch messages themselves are
+    # pinned by tests/test_gpu_backends.py)
+    assert last["kinds"].get("mismatch", 0) == last["checked"]
 
 
 def test_adapter_gpu_dispatch_bit_identical():
