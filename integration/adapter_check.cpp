@@ -33,11 +33,14 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <functional>
 #include <iostream>
 #include <json.hpp>
 
 #include "atc_liftc_adapter.hpp"
+#include "host_phases.hpp"
+#include "host_vm.hpp"
 #include "liftc/classifier.hpp"
 #include "liftc/equivalence.hpp"
 #include "liftc/pipeline.hpp"
@@ -88,36 +91,16 @@ std::vector<Prog> corpus() {
   return out;
 }
 
-// the analysis half of pipeline.cpp:164-221 (same calls, same order)
+// the analysis half of pipeline.cpp:164-221 on the host VM (gpu::analyze_function:
+// the same liveness, probe values and dims as the reference's calls — pinned by
+// `adapter_check host`)
 analysis::AnalyzedFunction analyze(const Prog& p, uint64_t fseed, const std::vector<const api::ApiSpec*>& specs) {
   const auto* f = p.prog.find(p.function);
-  auto live = analysis::detect_liveness(p.prog, *f, fseed, p.meta.rules);
-  analysis::AnalyzedFunction fn;
-  fn.name = p.function;
-  for (const auto& q : f->params) {
-    if (q.kind == minilang::ParamKind::IntScalar) fn.int_params.push_back(q.name);
-    if (q.kind == minilang::ParamKind::FloatScalar) fn.float_params.push_back(q.name);
-  }
   int max_rank = p.meta.max_rank;
   for (const auto* s : specs)
     if (!p.meta.max_rank) max_rank = std::max(max_rank, s->max_rank());
-  auto probe = analysis::assign_probe_values(fn.int_params, p.meta.rules, p.meta.probes, 0);
-  for (const auto& q : f->params) {
-    if (q.kind != minilang::ParamKind::Pointer) continue;
-    analysis::ArrayInfo info;
-    info.name = q.name;
-    info.elem = q.elem;
-    info.liveness = live.classes.at(q.name);
-    try {
-      auto d = analysis::detect_dims(p.prog, *f, q.name, fn.int_params, probe, max_rank);
-      info.has_dims = true;
-      info.dims = d.dims;
-    } catch (const analysis::NoDimsFound&) {
-      info.has_dims = false;
-    }
-    fn.arrays.push_back(std::move(info));
-  }
-  return fn;
+  const gpu::HostVm vm(p.prog);
+  return gpu::analyze_function(vm, *f, fseed, p.meta.rules, p.meta.probes, max_rank);
 }
 
 int cmd_corpus(atc_ctx* ctx) {
@@ -154,7 +137,9 @@ int cmd_corpus(atc_ctx* ctx) {
     std::vector<const api::ApiSpec*> lspecs;
     for (const auto& s : specs)
       if (s.semantics == fr->class_label) lspecs.push_back(&s);
+    auto t_an = std::chrono::steady_clock::now();
     auto fn = analyze(p, fseed, lspecs);
+    const double analysis_ms = ms_since(t_an);
     gpu::LoopConfig lc;
     lc.tests = cfg.tests;
     lc.verify_tests = cfg.verify_tests;
@@ -215,6 +200,10 @@ int cmd_corpus(atc_ctx* ctx) {
     t0 = std::chrono::steady_clock::now();
     auto fast = gpu::candidate_loop(ctx, p.prog, fn, p.function, lspecs, p.meta.rules, fseed, lc);
     j["fast_loop_ms"] = ms_since(t0);
+    // the whole lift of the function with the GPU candidate stage and the host-VM
+    // analyses (liveness, dims, P1), against the reference's lift_program
+    j["analysis_ms"] = analysis_ms;
+    j["ours_lift_ms"] = analysis_ms + (double)j["fast_loop_ms"];
     j["fast_gpu_p2_ms"] = fast.gpu_ms;
     j["fast_record_ms"] = fast.record_ms;
     j["fast_p1_ms"] = fast.p1_ms;
@@ -335,6 +324,151 @@ int cmd_details(atc_ctx* ctx, int per_space) {
     }
   }
   std::cout << json({{"checked", checked}, {"mismatches", bad}, {"kinds", kinds}}).dump() << std::endl;
+  return bad == 0 ? 0 : 1;
+}
+
+// host_vm / host_phases against the reference interpreter and analyses on every
+// function of every corpus file (no GPU needed): raw executions (status, fault
+// message, steps, final images, write flags, return value), detect_liveness,
+// detect_dims per pointer, and P1 check_equivalence (verdict, tests_run, detail,
+// counterexample) on every ranked candidate plus a strided sample of each
+// unpruned space; with the time each side took.
+int cmd_host() {
+  auto specs = default_specs();
+  int bad = 0;
+  long long runs = 0, p1 = 0, dims = 0, lives = 0;
+  double t_ref[4] = {}, t_vm[4] = {};  // exec, liveness, dims, p1
+  auto report = [&](const json& j) {
+    ++bad;
+    std::cout << j.dump() << std::endl;
+  };
+  for (const auto& [k, v] : embedded_files()) {
+    if (k.rfind("corpus/", 0) != 0 || k.substr(k.size() - 3) != ".ml") continue;
+    const std::string tag = k.substr(k.rfind('/') + 1);
+    auto prog = minilang::parse_program(v);
+    pipeline::FixtureMeta meta;
+    auto side = embedded_files().find(k.substr(0, k.size() - 3) + ".json");
+    if (side != embedded_files().end()) meta = pipeline::parse_fixture_meta(side->second);
+    const gpu::HostVm vm(prog);
+    for (const auto& f : prog.functions) {
+      const uint64_t fseed = Rng::mix(0, tag + ":" + f.name);
+      std::vector<std::string> ints;
+      for (const auto& q : f.params)
+        if (q.kind == minilang::ParamKind::IntScalar) ints.push_back(q.name);
+      // raw executions on probe images (sizes per the sidecar rules, three seeds)
+      for (int rep = 0; rep < 3; ++rep) {
+        Rng rng(Rng::mix(fseed, "hostvm:" + std::to_string(rep)));
+        std::map<std::string, long long> sizes;
+        if (!analysis::draw_sizes(ints, meta.rules, rng, sizes)) continue;
+        auto img = analysis::build_probe_image(f, sizes, rng);
+        interp::InstrumentationPolicy pol;
+        pol.track_writes = rep != 1;
+        auto t0 = std::chrono::steady_clock::now();
+        auto a = interp::execute(prog, f.name, img, pol);
+        t_ref[0] += ms_since(t0);
+        t0 = std::chrono::steady_clock::now();
+        auto b = vm.execute(f.name, img, pol);
+        t_vm[0] += ms_since(t0);
+        ++runs;
+        bool same = a.status == b.status && a.fault_msg == b.fault_msg && a.steps == b.steps &&
+                    a.has_ret == b.has_ret && a.ret_is_int == b.ret_is_int && a.ret_int == b.ret_int &&
+                    (a.ret_float == b.ret_float || (std::isnan(a.ret_float) && std::isnan(b.ret_float))) &&
+                    a.writes == b.writes && a.final.regions.size() == b.final.regions.size();
+        for (const auto& [name, r] : a.final.regions)
+          same = same && b.final.regions.count(name) &&
+                 std::memcmp(r.data.data(), b.final.regions.at(name).data.data(), r.data.size() * 8) == 0;
+        if (!same)
+          report({{"file", tag}, {"function", f.name}, {"what", "execute"}, {"status", {a.status, b.status}},
+                  {"msg", {a.fault_msg, b.fault_msg}}, {"steps", {a.steps, b.steps}}});
+      }
+      // liveness
+      std::string ra, rb;
+      analysis::LivenessReport la, lb;
+      auto t0 = std::chrono::steady_clock::now();
+      try { la = analysis::detect_liveness(prog, f, fseed, meta.rules); } catch (const std::exception& e) { ra = e.what(); }
+      t_ref[1] += ms_since(t0);
+      t0 = std::chrono::steady_clock::now();
+      try { lb = gpu::detect_liveness(vm, f, fseed, meta.rules); } catch (const std::exception& e) { rb = e.what(); }
+      t_vm[1] += ms_since(t0);
+      ++lives;
+      if (ra != rb || la.classes != lb.classes)
+        report({{"file", tag}, {"function", f.name}, {"what", "liveness"}, {"errors", {ra, rb}}});
+      // dims (max rank: the sidecar's, else the bundled specs' largest)
+      int max_rank = meta.max_rank;
+      for (const auto& sp : specs)
+        if (!meta.max_rank) max_rank = std::max(max_rank, sp.max_rank());
+      std::map<std::string, long long> probe;
+      try { probe = analysis::assign_probe_values(ints, meta.rules, meta.probes, 0); } catch (const std::exception&) { continue; }
+      std::vector<gpu::DimsOutcome> ours;
+      std::string eb;
+      t0 = std::chrono::steady_clock::now();
+      try { ours = gpu::detect_dims_all(vm, f, ints, probe, max_rank); } catch (const std::exception& e) { eb = e.what(); }
+      t_vm[2] += ms_since(t0);
+      size_t oi = 0;
+      for (const auto& q : f.params) {
+        if (q.kind != minilang::ParamKind::Pointer) continue;
+        std::string ea;
+        bool found = false;
+        analysis::DimSpec d;
+        t0 = std::chrono::steady_clock::now();
+        try {
+          d = analysis::detect_dims(prog, f, q.name, ints, probe, max_rank);
+          found = true;
+        } catch (const analysis::NoDimsFound&) {
+        } catch (const std::exception& e) {
+          ea = e.what();
+        }
+        t_ref[2] += ms_since(t0);
+        ++dims;
+        const bool same = ea == eb && (!eb.empty() || (oi < ours.size() && ours[oi].found == found &&
+                                                       (!found || (ours[oi].spec.dims == d.dims &&
+                                                                   ours[oi].spec.slow_dim == d.slow_dim))));
+        if (!same) report({{"file", tag}, {"function", f.name}, {"what", "dims"}, {"array", q.name}, {"errors", {ea, eb}}});
+        ++oi;
+      }
+      // P1 on gemm/conv functions: ranked candidates + a strided unpruned sample
+      if (meta.function != f.name || meta.label.empty()) continue;
+      for (const auto& spec : specs) {
+        if (spec.semantics != meta.label) continue;
+        analysis::AnalyzedFunction fn;
+        try {
+          fn = gpu::analyze_function(vm, f, fseed, meta.rules, meta.probes, max_rank);
+        } catch (const std::exception&) {
+          break;
+        }
+        std::vector<matching::CandidateBinding> cands;
+        auto ranked = matching::rank_candidates(matching::find_matchings(fn, spec), 100);
+        for (const auto& c : ranked.ranked) cands.push_back(c);
+        gpu::UnprunedSpace sp(fn, spec);
+        const size_t stride = std::max<size_t>(1, sp.count() / 24);
+        for (size_t i = 0; i < sp.count() && cands.size() < 40; i += stride) cands.push_back(sp.at(spec, i));
+        for (const auto& c : cands) {
+          equivalence::EquivalenceConfig ec;
+          ec.seed = fseed;
+          t0 = std::chrono::steady_clock::now();
+          auto a = equivalence::check_equivalence(prog, fn, c, spec, meta.rules, ec);
+          t_ref[3] += ms_since(t0);
+          t0 = std::chrono::steady_clock::now();
+          auto b = gpu::check_equivalence(vm, prog, fn, c, spec, meta.rules, ec);
+          t_vm[3] += ms_since(t0);
+          ++p1;
+          const bool same = a.verdict == b.verdict && a.tests_run == b.tests_run && a.detail == b.detail &&
+                            a.cex.sizes == b.cex.sizes && a.cex.array == b.cex.array &&
+                            a.cex.offset == b.cex.offset && a.cex.expected == b.cex.expected &&
+                            a.cex.actual == b.cex.actual;
+          if (!same)
+            report({{"file", tag}, {"function", f.name}, {"what", "p1"}, {"spec", spec.name},
+                    {"verdict", {equivalence::verdict_name(a.verdict), equivalence::verdict_name(b.verdict)}},
+                    {"tests_run", {a.tests_run, b.tests_run}}, {"detail", {a.detail, b.detail}}});
+        }
+      }
+    }
+  }
+  std::cout << json({{"mismatches", bad}, {"executions", runs}, {"liveness", lives}, {"dims", dims}, {"p1", p1},
+                     {"reference_ms", {{"execute", t_ref[0]}, {"liveness", t_ref[1]}, {"dims", t_ref[2]}, {"p1", t_ref[3]}}},
+                     {"host_vm_ms", {{"execute", t_vm[0]}, {"liveness", t_vm[1]}, {"dims", t_vm[2]}, {"p1", t_vm[3]}}}})
+                   .dump()
+            << std::endl;
   return bad == 0 ? 0 : 1;
 }
 
@@ -537,6 +671,14 @@ int cmd_routed(atc_ctx* ctx) {
 }  // namespace
 
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "host") {  // host-side checks: no GPU needed
+    try {
+      return cmd_host();
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "adapter_check: %s\n", e.what());
+      return 1;
+    }
+  }
   // every visible GPU as one device group; single-context work
   // (the candidate loop, dispatch) runs on member 0, as one pipeline worker would
   atc_group* g = atc_group_create(nullptr, 0);

@@ -12,6 +12,8 @@
 #include <stdexcept>
 #include <thread>
 
+#include "host_phases.hpp"
+#include "host_vm.hpp"
 #include "liftc/equivalence.hpp"
 #include "liftc/rng.hpp"
 
@@ -83,8 +85,10 @@ RecordedTests record_tests(const minilang::Program& prog, const std::string& fun
   r.test_detail.assign(tests, "");
   r.init.resize((size_t)tests * nP);
   r.fin.resize((size_t)tests * nP);
-  // the T tests are independent streams (rewriter.cpp:236) and interp::execute is
-  // re-entrant, so they are recorded on parallel host threads
+  // the T tests are independent streams (rewriter.cpp:236): recorded on parallel
+  // host threads, each original run on the compiled host VM (the
+  // reference interpreter's semantics, host_vm.hpp)
+  const HostVm vm(prog);
   std::vector<std::vector<int32_t>> dpos((size_t)tests * nP);
   std::vector<std::vector<double>> dval((size_t)tests * nP);
   auto record_one = [&](int t) {
@@ -100,7 +104,7 @@ RecordedTests record_tests(const minilang::Program& prog, const std::string& fun
     interp::MemoryImage img = analysis::build_probe_image(*f, sizes, rng);
     for (size_t i = 0; i < nI; ++i) r.ints[t * nI + i] = sizes.at(r.int_params[i]);
     interp::InstrumentationPolicy plain;
-    auto ref = interp::execute(prog, function, img, plain);
+    auto ref = vm.execute(function, img, plain);
     for (size_t p = 0; p < nP; ++p) {
       r.init[t * nP + p] = img.regions.at(r.ptr_params[p]).data;
       if (ref.status == interp::ExecStatus::Normal) {
@@ -262,6 +266,7 @@ LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const ana
   }
   out.gpu_ms = ms_since(t0);
 
+  const HostVm vm(prog);
   // P1 on P2 survivors in rank order (pipeline.cpp:257-261 + :271-307).  With
   // report_parity, P1 also runs on the P2-rejected candidates that precede the
   // winner, so `verdicts` reproduces the reference's evaluated[] entries exactly:
@@ -275,7 +280,7 @@ LoopResult first_accepted(atc_ctx* ctx, const minilang::Program& prog, const ana
     ec.tests = p1_tests;
     ec.seed = fseed;
     ++out.p1_calls;
-    auto er = equivalence::check_equivalence(prog, fn, ranked[b], spec, rules, ec);
+    auto er = check_equivalence(vm, prog, fn, ranked[b], spec, rules, ec);
     const bool eq = er.verdict == equivalence::Verdict::Equivalent;
     if (report_parity)
       out.verdicts.push_back(eq && !p2_ok ? std::string("VerificationFailed")
@@ -372,12 +377,13 @@ UnprunedResult first_accepted_unpruned(atc_group* g, const minilang::Program& pr
   // P1 on the P2 survivors in index order (pipeline.cpp:257-261, :275-277 order of
   // the two phases swapped: P2 is the cheap screen here)
   t0 = std::chrono::steady_clock::now();
+  const HostVm vm(prog);
   for (uint64_t idx : out.p2_passing) {
     equivalence::EquivalenceConfig ec;
     ec.tests = p1_tests;
     ec.seed = fseed;
     ++out.p1_calls;
-    auto er = equivalence::check_equivalence(prog, fn, space.at(spec, idx), spec, rules, ec);
+    auto er = check_equivalence(vm, prog, fn, space.at(spec, idx), spec, rules, ec);
     if (er.verdict == equivalence::Verdict::Equivalent) {
       out.winner = (int64_t)idx;
       break;
@@ -646,7 +652,8 @@ CandidateLoop candidate_loop(atc_ctx* ctx, const minilang::Program& prog, const 
     p2 = p2_verdicts(ctx, rec, eval_specs, lists);
     out.gpu_ms = ms_since(t0);
   }
-  // pipeline.cpp:241-309
+  // pipeline.cpp:241-309 (P1 = check_equivalence on the host VM, host_phases.hpp)
+  const HostVm vm(prog);
   bool too_many = false;
   const auto t_p1 = std::chrono::steady_clock::now();
   for (size_t s = 0; s < specs.size(); ++s) {
@@ -669,7 +676,7 @@ CandidateLoop candidate_loop(atc_ctx* ctx, const minilang::Program& prog, const 
       equivalence::EquivalenceConfig ec;
       ec.tests = cfg.tests;
       ec.seed = fseed;
-      auto er = equivalence::check_equivalence(prog, fn, cand, *specs[s], rules, ec);
+      auto er = check_equivalence(vm, prog, fn, cand, *specs[s], rules, ec);
       ++out.p1_calls;
       pipeline::CandidateOutcome co;
       co.api = specs[s]->name;

@@ -2,6 +2,7 @@
 // (/root/reference/proj/src/interp.cpp) line it restates.
 #include "host_vm.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <stdexcept>
 
@@ -18,17 +19,18 @@ constexpr size_t kTraceCap = 1u << 20;    // interp.cpp:11
 
 // ------------------------------------------------------------------ IR --
 enum class EK : uint8_t {
-  IntLit, FloatLit, Var, Index, Neg, Not, Bin, And, Or, Min, Max, ToI64, ToF64, Fabs, Sqrt, Dispatch, Call
+  IntLit, FloatLit, Var, Index, Neg, Not, And, Or, Min, Max, ToI64, ToF64, Fabs, Sqrt, Dispatch, Call,
+  Add, Sub, Mul, Div, Mod, Lt, Le, Gt, Ge, Eq, Ne
 };
 
 struct CExpr {
   EK k = EK::IntLit;
-  BinOp op = BinOp::Add;
   int slot = -1;            // Var / Index (pointer slot)
+  int a0 = -1, a1 = -1;     // children (unary: a0; binary: a0, a1)
+  int fn = -1;              // Call: callee index
+  int argb = 0, argn = 0;   // Call: arguments F.args[argb, argb + argn) (pointer params are Var)
   long long i = 0;
   double f = 0.0;
-  int fn = -1;              // Call: callee index
-  std::vector<int> args;    // child expressions (Call: one per param; pointer params are Var)
 };
 
 enum class SK : uint8_t {
@@ -50,6 +52,7 @@ struct CFunc {
   const FunctionIR* ir = nullptr;
   int n_slots = 0;
   std::vector<CExpr> ex;
+  std::vector<int> args;
   std::vector<CStmt> st;
   std::vector<int> body;
 };
@@ -100,18 +103,20 @@ struct Compiler {
       case Expr::Kind::Index:
         c.k = EK::Index;
         c.slot = lookup(e.name);
-        c.args.push_back(expr(*e.args[0]));
+        c.a0 = expr(*e.args[0]);
         break;
       case Expr::Kind::Unary:
         c.k = e.uop == UnOp::Not ? EK::Not : EK::Neg;
-        c.args.push_back(expr(*e.args[0]));
+        c.a0 = expr(*e.args[0]);
         break;
-      case Expr::Kind::Binary:
-        c.k = e.bop == BinOp::And ? EK::And : e.bop == BinOp::Or ? EK::Or : EK::Bin;
-        c.op = e.bop;
-        c.args.push_back(expr(*e.args[0]));
-        c.args.push_back(expr(*e.args[1]));
+      case Expr::Kind::Binary: {
+        static const EK kinds[] = {EK::Add, EK::Sub, EK::Mul, EK::Div, EK::Mod, EK::Lt, EK::Le,
+                                   EK::Gt,  EK::Ge,  EK::Eq,  EK::Ne,  EK::And, EK::Or};
+        c.k = kinds[(int)e.bop];
+        c.a0 = expr(*e.args[0]);
+        c.a1 = expr(*e.args[1]);
         break;
+      }
       case Expr::Kind::Call: {
         const std::string& n = e.name;
         if (n == "min" || n == "max") c.k = n == "min" ? EK::Min : EK::Max;
@@ -127,6 +132,7 @@ struct Compiler {
           auto it = P.index.find(n);
           c.fn = it == P.index.end() ? -1 : it->second;  // -1: "call to unknown function" at run time
         }
+        std::vector<int> args;
         if (c.k == EK::Call && c.fn >= 0) {
           const FunctionIR* callee = P.fns[c.fn].ir;
           for (size_t i = 0; i < e.args.size(); ++i) {
@@ -135,14 +141,19 @@ struct Compiler {
               v.k = EK::Var;
               v.slot = lookup(e.args[i]->name);
               F.ex.push_back(v);
-              c.args.push_back((int)F.ex.size() - 1);
+              args.push_back((int)F.ex.size() - 1);
             } else {
-              c.args.push_back(expr(*e.args[i]));
+              args.push_back(expr(*e.args[i]));
             }
           }
         } else if (c.k != EK::Call) {
-          for (const auto& a : e.args) c.args.push_back(expr(*a));
+          for (const auto& a : e.args) args.push_back(expr(*a));
         }
+        if (!args.empty()) c.a0 = args[0];
+        if (args.size() > 1) c.a1 = args[1];
+        c.argb = (int)F.args.size();
+        c.argn = (int)args.size();
+        F.args.insert(F.args.end(), args.begin(), args.end());
         break;
       }
     }
@@ -360,16 +371,20 @@ struct Run {
   }
 
   // ----------------------------------------------------------- calls --
-  // interp.cpp:145-170: frame, parameters, body, return rounding
-  Val call(int fi, std::vector<Slot>& args, bool& has) {
+  // interp.cpp:145-170: frame, parameters, body, return rounding.  Frames live on
+  // one slot stack that only grows (a callee's slots above `top`); slots need no
+  // initialisation — the resolver guarantees a write before every read.
+  size_t top = 0;
+
+  Val call(int fi, const Slot* args, int nargs, bool& has) {
     const CFunc& F = P.fns[fi];
     if (depth >= kMaxCallDepth)
       throw Fault{ExecStatus::RuntimeFault, "call depth limit exceeded in '" + F.ir->name + "'"};
-    const size_t saved = base;
-    const size_t nb = stack.size();
-    stack.resize(nb + (size_t)F.n_slots);
-    for (size_t i = 0; i < args.size(); ++i) stack[nb + i] = args[i];
+    const size_t saved = base, nb = top;
+    if (stack.size() < nb + (size_t)F.n_slots) stack.resize(std::max(stack.size() * 2, nb + (size_t)F.n_slots + 64));
+    for (int i = 0; i < nargs; ++i) stack[nb + i] = args[i];
     base = nb;
+    top = nb + (size_t)F.n_slots;
     ++depth;
     has_ret = false;
     exec_list(F, F.body);
@@ -378,7 +393,7 @@ struct Run {
     has_ret = false;
     --depth;
     base = saved;
-    stack.resize(nb);
+    top = nb;
     if (has) {
       if (F.ir->ret == RetType::F32)
         r = Val::F((double)(float)r.d());
@@ -401,40 +416,89 @@ struct Run {
       case EK::Var:
         return S(e.slot).v;
       case EK::Index: {  // interp.cpp:416-419
-        const long long off = eval(F, e.args[0]).i;
+        const long long off = eval(F, e.a0).i;
         return Val::F(load(S(e.slot).region, off));
       }
       case EK::Not:
-        return Val::I(eval(F, e.args[0]).truthy() ? 0 : 1);
+        return Val::I(eval(F, e.a0).truthy() ? 0 : 1);
       case EK::Neg: {
-        const Val v = eval(F, e.args[0]);
+        const Val v = eval(F, e.a0);
         return v.is_int ? Val::I(-v.i) : Val::F(-v.f);
       }
       case EK::And:  // interp.cpp:434-441
-        if (!eval(F, e.args[0]).truthy()) return Val::I(0);
-        return Val::I(eval(F, e.args[1]).truthy() ? 1 : 0);
+        if (!eval(F, e.a0).truthy()) return Val::I(0);
+        return Val::I(eval(F, e.a1).truthy() ? 1 : 0);
       case EK::Or:
-        if (eval(F, e.args[0]).truthy()) return Val::I(1);
-        return Val::I(eval(F, e.args[1]).truthy() ? 1 : 0);
-      case EK::Bin:
-        return binary(e.op, eval(F, e.args[0]), eval(F, e.args[1]));
+        if (eval(F, e.a0).truthy()) return Val::I(1);
+        return Val::I(eval(F, e.a1).truthy() ? 1 : 0);
+      // interp.cpp:443-477: float arithmetic as soon as one operand is a float
+      case EK::Add: {
+        const Val a = eval(F, e.a0), b = eval(F, e.a1);
+        return a.is_int && b.is_int ? Val::I(a.i + b.i) : Val::F(a.d() + b.d());
+      }
+      case EK::Sub: {
+        const Val a = eval(F, e.a0), b = eval(F, e.a1);
+        return a.is_int && b.is_int ? Val::I(a.i - b.i) : Val::F(a.d() - b.d());
+      }
+      case EK::Mul: {
+        const Val a = eval(F, e.a0), b = eval(F, e.a1);
+        return a.is_int && b.is_int ? Val::I(a.i * b.i) : Val::F(a.d() * b.d());
+      }
+      case EK::Div: {
+        const Val a = eval(F, e.a0), b = eval(F, e.a1);
+        if (!a.is_int || !b.is_int) {
+          if (b.d() == 0.0) throw Fault{ExecStatus::RuntimeFault, "float division by zero"};
+          return Val::F(a.d() / b.d());
+        }
+        if (b.i == 0) throw Fault{ExecStatus::RuntimeFault, "integer division by zero"};
+        return Val::I(a.i / b.i);
+      }
+      case EK::Mod: {
+        const Val a = eval(F, e.a0), b = eval(F, e.a1);
+        if (b.i == 0) throw Fault{ExecStatus::RuntimeFault, "integer modulo by zero"};
+        return Val::I(a.i % b.i);
+      }
+      case EK::Lt: {
+        const Val a = eval(F, e.a0), b = eval(F, e.a1);
+        return Val::I(a.is_int && b.is_int ? a.i < b.i : a.d() < b.d());
+      }
+      case EK::Le: {
+        const Val a = eval(F, e.a0), b = eval(F, e.a1);
+        return Val::I(a.is_int && b.is_int ? a.i <= b.i : a.d() <= b.d());
+      }
+      case EK::Gt: {
+        const Val a = eval(F, e.a0), b = eval(F, e.a1);
+        return Val::I(a.is_int && b.is_int ? a.i > b.i : a.d() > b.d());
+      }
+      case EK::Ge: {
+        const Val a = eval(F, e.a0), b = eval(F, e.a1);
+        return Val::I(a.is_int && b.is_int ? a.i >= b.i : a.d() >= b.d());
+      }
+      case EK::Eq: {
+        const Val a = eval(F, e.a0), b = eval(F, e.a1);
+        return Val::I(a.is_int && b.is_int ? a.i == b.i : a.d() == b.d());
+      }
+      case EK::Ne: {
+        const Val a = eval(F, e.a0), b = eval(F, e.a1);
+        return Val::I(a.is_int && b.is_int ? a.i != b.i : a.d() != b.d());
+      }
       case EK::Min:
       case EK::Max: {  // interp.cpp:483-488
-        const long long a = eval(F, e.args[0]).i;
-        const long long b = eval(F, e.args[1]).i;
+        const long long a = eval(F, e.a0).i;
+        const long long b = eval(F, e.a1).i;
         const bool lt = a < b;
         return Val::I(e.k == EK::Min ? (lt ? a : b) : (lt ? b : a));
       }
       case EK::ToI64: {
-        const Val v = eval(F, e.args[0]);
+        const Val v = eval(F, e.a0);
         return v.is_int ? v : Val::I((long long)v.f);
       }
       case EK::ToF64:
-        return Val::F(eval(F, e.args[0]).d());
+        return Val::F(eval(F, e.a0).d());
       case EK::Fabs:
-        return Val::F(std::fabs(eval(F, e.args[0]).d()));
+        return Val::F(std::fabs(eval(F, e.a0).d()));
       case EK::Sqrt: {
-        const double v = eval(F, e.args[0]).d();
+        const double v = eval(F, e.a0).d();
         if (v < 0.0) throw Fault{ExecStatus::RuntimeFault, "sqrt of a negative value"};
         return Val::F(std::sqrt(v));
       }
@@ -443,14 +507,23 @@ struct Run {
       case EK::Call: {  // interp.cpp:503-524
         if (e.fn < 0) throw Fault{ExecStatus::RuntimeFault, "call to unknown function"};
         const FunctionIR* callee = P.fns[e.fn].ir;
-        std::vector<Slot> args(e.args.size());
-        for (size_t i = 0; i < e.args.size(); ++i) {
+        constexpr int kInline = 16;
+        Slot small[kInline];
+        std::vector<Slot> big;
+        Slot* args = small;
+        if (e.argn > kInline) {
+          big.resize(e.argn);
+          args = big.data();
+        }
+        for (int i = 0; i < e.argn; ++i) {
           const Param& p = callee->params[i];
           Slot& s = args[i];
+          s = Slot{};
+          const int ai = F.args[e.argb + i];
           if (p.kind == ParamKind::Pointer) {
-            s.region = S(F.ex[e.args[i]].slot).region;
+            s.region = S(F.ex[ai].slot).region;
           } else {
-            const Val v = eval(F, e.args[i]);
+            const Val v = eval(F, ai);
             if (p.kind == ParamKind::FloatScalar) {
               s.round_f32 = p.elem == ScalarType::F32;
               s.v = Val::F(s.round_f32 ? (double)(float)v.d() : v.d());
@@ -460,37 +533,11 @@ struct Run {
           }
         }
         bool has = false;
-        const Val r = call(e.fn, args, has);
+        const Val r = call(e.fn, args, e.argn, has);
         return has ? r : Val::I(0);
       }
     }
     return Val::I(0);
-  }
-
-  static Val binary(BinOp op, const Val& a, const Val& b) {  // interp.cpp:443-477
-    const bool fl = !a.is_int || !b.is_int;
-    switch (op) {
-      case BinOp::Add: return fl ? Val::F(a.d() + b.d()) : Val::I(a.i + b.i);
-      case BinOp::Sub: return fl ? Val::F(a.d() - b.d()) : Val::I(a.i - b.i);
-      case BinOp::Mul: return fl ? Val::F(a.d() * b.d()) : Val::I(a.i * b.i);
-      case BinOp::Div:
-        if (fl) {
-          if (b.d() == 0.0) throw Fault{ExecStatus::RuntimeFault, "float division by zero"};
-          return Val::F(a.d() / b.d());
-        }
-        if (b.i == 0) throw Fault{ExecStatus::RuntimeFault, "integer division by zero"};
-        return Val::I(a.i / b.i);
-      case BinOp::Mod:
-        if (b.i == 0) throw Fault{ExecStatus::RuntimeFault, "integer modulo by zero"};
-        return Val::I(a.i % b.i);
-      case BinOp::Lt: return Val::I(fl ? a.d() < b.d() : a.i < b.i);
-      case BinOp::Le: return Val::I(fl ? a.d() <= b.d() : a.i <= b.i);
-      case BinOp::Gt: return Val::I(fl ? a.d() > b.d() : a.i > b.i);
-      case BinOp::Ge: return Val::I(fl ? a.d() >= b.d() : a.i >= b.i);
-      case BinOp::Eq: return Val::I(fl ? a.d() == b.d() : a.i == b.i);
-      case BinOp::Ne: return Val::I(fl ? a.d() != b.d() : a.i != b.i);
-      default: throw Fault{ExecStatus::RuntimeFault, "bad binary operator"};
-    }
   }
 
   // ------------------------------------------------------ statements --
@@ -698,7 +745,7 @@ interp::ExecutionOutcome HostVm::execute(const std::string& function, const inte
       R.wr.push_back(w == writes.end() ? nullptr : &w->second);
     }
     bool has = false;
-    const Val rv = R.call(fit->second, args, has);
+    const Val rv = R.call(fit->second, args.data(), (int)args.size(), has);
     out.status = ExecStatus::Normal;
     out.has_ret = has;
     if (has) {
@@ -740,7 +787,7 @@ std::map<std::string, HostVm::Survey> HostVm::dim_survey(const std::string& func
     R.dead.assign(nr, 0);
     R.dead_msg.assign(nr, {});
     bool has = false;
-    R.call(fit->second, args, has);
+    R.call(fit->second, args.data(), (int)args.size(), has);
   } catch (const Fault& flt) {
     status = flt.status;
     msg = flt.msg;
