@@ -453,14 +453,23 @@ def _check(jobs, combined):
 
 
 def _sampled_agree(j, passing) -> bool:
-    """A sampled (conv) dump: the reference's verdict of every dumped index agrees
-    with membership in `passing`."""
+    """A sampled (conv) dump: the reference's verdict of every dumped index (the
+    random sample and the +-4096 neighbourhoods of every passing index and pruned
+    candidate, tests/golden/conv_neighbourhoods.npz) agrees with membership in
+    `passing`, and `passing` is the pinned list (tests/golden/conv_passing.json)."""
     from paper_2301_11659_b200 import fixtures
 
+    key = f"{j.stem}x{j.spec_name}"
+    T = j.ts.n_tests
     v = fixtures.load(j.stem).verdicts(j.spec_name)
-    ref_ok = (v["fail_t"] < 0) | (v["fail_t"] >= 16)
-    got = np.isin(v["idx"].astype(np.int64), np.asarray(passing, dtype=np.int64))
-    return bool(np.array_equal(ref_ok, got))
+    nb = fixtures.conv_neighbourhoods().get(key)
+    idx, ft = v["idx"].astype(np.int64), v["fail_t"]
+    if nb is not None:
+        idx, ft = np.concatenate([idx, nb["idx"].astype(np.int64)]), np.concatenate([ft, nb["fail_t"]])
+    ref_ok = (ft < 0) | (ft >= T)
+    got = np.isin(idx, np.asarray(passing, dtype=np.int64))
+    pinned = fixtures.conv_passing().get(key, {}).get(str(T))
+    return bool(np.array_equal(ref_ok, got)) and (pinned is None or list(passing) == pinned["passing"])
 
 
 def _fp64_pipe(ctx):

@@ -72,7 +72,7 @@ struct Prog {
   pipeline::FixtureMeta meta;
 };
 
-std::vector<Prog> corpus() {
+std::vector<Prog> corpus(bool every_dir = false) {
   std::vector<Prog> out;
   for (const auto& [k, v] : embedded_files()) {
     if (k.rfind("corpus/", 0) != 0 || k.substr(k.size() - 3) != ".ml") continue;
@@ -81,7 +81,7 @@ std::vector<Prog> corpus() {
     p.tag = k.substr(k.rfind('/') + 1);
     p.stem = p.tag.substr(0, p.tag.size() - 3);
     p.dir = k.substr(7, k.rfind('/') - 7);
-    if (p.dir != "gemm" && p.dir != "conv") continue;
+    if (!every_dir && p.dir != "gemm" && p.dir != "conv") continue;
     p.prog = minilang::parse_program(v);
     auto side = embedded_files().find(k.substr(0, k.size() - 3) + ".json");
     if (side != embedded_files().end()) p.meta = pipeline::parse_fixture_meta(side->second);
@@ -94,8 +94,9 @@ std::vector<Prog> corpus() {
 // the analysis half of pipeline.cpp:164-221 on the host VM (gpu::analyze_function:
 // the same liveness, probe values and dims as the reference's calls — pinned by
 // `adapter_check host`)
-analysis::AnalyzedFunction analyze(const Prog& p, uint64_t fseed, const std::vector<const api::ApiSpec*>& specs) {
-  const auto* f = p.prog.find(p.function);
+analysis::AnalyzedFunction analyze(const Prog& p, uint64_t fseed, const std::vector<const api::ApiSpec*>& specs,
+                                   const std::string& function = "") {
+  const auto* f = p.prog.find(function.empty() ? p.function : function);
   int max_rank = p.meta.max_rank;
   for (const auto* s : specs)
     if (!p.meta.max_rank) max_rank = std::max(max_rank, s->max_rank());
@@ -121,24 +122,31 @@ int cmd_corpus(atc_ctx* ctx) {
   cfg.classifier = &model;
   cfg.workers = 1;
   int mismatches = 0;
-  for (const auto& p : corpus()) {
+  // every function of every corpus file (gemm, conv, nonidiom): the reference's
+  // lift_program report vs. the same report with the candidate stage replaced
+  for (const auto& p : corpus(true)) {
     auto t0 = std::chrono::steady_clock::now();
     auto rep = pipeline::lift_program(p.prog, p.tag, p.meta, cfg, nullptr);
     const double ref_ms = ms_since(t0);
-    const pipeline::FunctionReport* fr = nullptr;
-    for (const auto& f : rep.functions)
-      if (f.function == p.function) fr = &f;
-    json j = {{"stem", p.stem}, {"reference_status", pipeline::status_name(fr->status)}, {"reference_ms", ref_ms}};
-    if (fr->status == pipeline::FunctionStatus::Misclassified) {
-      std::cout << j.dump() << std::endl;
-      continue;
-    }
-    const uint64_t fseed = Rng::mix(cfg.seed, p.tag + ":" + p.function);  // pipeline.cpp:131
+    for (const auto& fref : rep.functions) {
+    const pipeline::FunctionReport* fr = &fref;
+    const std::string function = fr->function;
+    json j = {{"stem", p.stem}, {"function", function}, {"dir", p.dir},
+              {"reference_status", pipeline::status_name(fr->status)}, {"reference_ms", ref_ms}};
     std::vector<const api::ApiSpec*> lspecs;
     for (const auto& s : specs)
       if (s.semantics == fr->class_label) lspecs.push_back(&s);
+    if (fr->status == pipeline::FunctionStatus::Misclassified || lspecs.empty() ||
+        fr->status == pipeline::FunctionStatus::AnalysisFailed) {
+      // no candidate stage in the reference either (pipeline.cpp:141-162, :164-221):
+      // the report is the host's, unchanged
+      j["candidate_stage"] = false;
+      std::cout << j.dump() << std::endl;
+      continue;
+    }
+    const uint64_t fseed = Rng::mix(cfg.seed, p.tag + ":" + function);  // pipeline.cpp:131
     auto t_an = std::chrono::steady_clock::now();
-    auto fn = analyze(p, fseed, lspecs);
+    auto fn = analyze(p, fseed, lspecs, function);
     const double analysis_ms = ms_since(t_an);
     gpu::LoopConfig lc;
     lc.tests = cfg.tests;
@@ -147,7 +155,7 @@ int cmd_corpus(atc_ctx* ctx) {
     lc.budget_sec = cfg.budget_sec;
     lc.report = true;
     t0 = std::chrono::steady_clock::now();
-    auto loop = gpu::candidate_loop(ctx, p.prog, fn, p.function, lspecs, p.meta.rules, fseed, lc);
+    auto loop = gpu::candidate_loop(ctx, p.prog, fn, function, lspecs, p.meta.rules, fseed, lc);
     const double ours_ms = ms_since(t0);
     // the reference's report with every candidate-stage field replaced by ours
     // (pipeline.cpp:223-330); everything else is the unchanged host analysis
@@ -198,7 +206,7 @@ int cmd_corpus(atc_ctx* ctx) {
     // candidate stage (its match + equivalence + rewrite/verify phases)
     lc.report = false;
     t0 = std::chrono::steady_clock::now();
-    auto fast = gpu::candidate_loop(ctx, p.prog, fn, p.function, lspecs, p.meta.rules, fseed, lc);
+    auto fast = gpu::candidate_loop(ctx, p.prog, fn, function, lspecs, p.meta.rules, fseed, lc);
     j["fast_loop_ms"] = ms_since(t0);
     // the whole lift of the function with the GPU candidate stage and the host-VM
     // analyses (liveness, dims, P1), against the reference's lift_program
@@ -223,7 +231,9 @@ int cmd_corpus(atc_ctx* ctx) {
     j["p1_calls"] = p1_calls;
     j["candidate_loop_ms"] = ours_ms;
     j["gpu_p2_ms"] = gpu_ms;
+    j["candidate_stage"] = true;
     std::cout << j.dump() << std::endl;
+    }
   }
   std::cout << json({{"mismatches", mismatches}}).dump() << std::endl;
   return mismatches == 0 ? 0 : 1;

@@ -682,6 +682,37 @@ int cmd_time(const std::string& mode, const std::string& stem, const std::string
   return 0;
 }
 
+// The reference's own P2 verdicts (verify_rewrite: first failing test + reason)
+// for every binding within `radius` of each given index of one unpruned space —
+// the neighbourhoods of the passing bindings the GPU reports in spaces too large
+// to sweep with the reference (tests/golden/conv_neighbourhoods.npz, made by
+// oracle/gen_neighbourhoods.py).  Output: one JSON line with the sorted indices
+// and the verdict arrays.
+int cmd_neighbourhood(const std::string& stem, const std::string& spec_name, int tests, long long radius,
+                      const std::vector<unsigned long long>& centers, int threads) {
+  auto specs = default_specs();
+  const auto& spec = spec_named(specs, spec_name);
+  ProgCtx c = load_prog(stem, specs);
+  Space sp(c.fn, spec);
+  std::set<unsigned long long> all;
+  for (unsigned long long ctr : centers)
+    for (long long d = -radius; d <= radius; ++d) {
+      const long long i = (long long)ctr + d;
+      if (i >= 0 && (unsigned long long)i < sp.count()) all.insert((unsigned long long)i);
+    }
+  std::vector<unsigned long long> idx(all.begin(), all.end());
+  std::vector<int> ft(idx.size()), rs(idx.size());
+  parallel_for(idx.size(), threads, [&](size_t i) {
+    P2Out o = run_p2(c.prog, c.function, sp.binding(idx[i]), spec, c.meta.rules, c.p2seed, tests);
+    ft[i] = o.fail_t;
+    rs[i] = o.reason;
+  });
+  json j = {{"stem", stem}, {"spec", spec_name}, {"tests", tests}, {"radius", radius}, {"centers", centers},
+            {"count", sp.count()}, {"idx", idx}, {"fail_t", ft}, {"reason", rs}};
+  std::cout << j.dump() << std::endl;
+  return 0;
+}
+
 int cmd_time_gemm(bool xpu, long long m, long long n, long long k, long long rows) {
   // inputs: uniform[-1,1] from Rng(mix(0,"bench:A"/"bench:B"))
   long long mm = xpu ? m : rows;
@@ -777,6 +808,12 @@ int main(int argc, char** argv) {
       return cmd_time(cmd == "time-p2" ? "p2" : "acc", argv[2], argv[3], std::atoi(argv[4]),
                       std::atof(argv[5]), std::atoi(argv[6]),
                       argc >= 8 && std::string(argv[7]) == "rules64");
+    if (cmd == "neighbourhood" && argc >= 8) {
+      std::vector<unsigned long long> centers;
+      for (int a = 7; a < argc; ++a) centers.push_back(std::strtoull(argv[a], nullptr, 10));
+      return cmd_neighbourhood(argv[2], argv[3], std::atoi(argv[4]), std::atoll(argv[5]), centers,
+                               std::atoi(argv[6]));
+    }
     if (cmd == "time-xpu-gemm" && argc == 5)
       return cmd_time_gemm(true, std::atoll(argv[2]), std::atoll(argv[3]), std::atoll(argv[4]), 0);
     if (cmd == "time-cpu-gemm" && argc == 6)

@@ -90,6 +90,19 @@ struct RowPlan {
   const uint32_t* cmask;
 };
 
+// One small enumerated space of a sweep for k_sweep_small (eval_kernels.cu): its
+// CTAs are [cta0, cta0 + ctas), each screening and confirming a contiguous slice
+// of the job's n bindings; results go to the job's block of the batch.
+struct SmallJob {
+  TestsetView ts;
+  SpecView sp;
+  BindingSource src;         // enumerated: device permutations, size_maps, begin = the range start
+  uint64_t n;                // bindings in the range
+  uint64_t* res;             // [0] K1 survivors, [1] passing count, [2 ..) passing global indices
+  unsigned long long* hist;  // reason histogram (8 words)
+  uint32_t cta0, ctas;
+};
+
 enum : int32_t { kUndecided = -2 };
 
 // Encoded per-binding result: t * 8 + reason; kPassKey when every test passed.

@@ -33,6 +33,12 @@ struct atc_enum_batch {
   std::vector<std::vector<int64_t>> captured_ints;  // per job: its test sets' ints when the graph was captured
   bool transient = false;  // one-shot (atc_eval_enumerated_many): buffers borrowed from the context
   uint8_t* perm_block = nullptr;  // owned permutation buffer (reusable batches)
+  // small spaces (k_sweep_small: one launch for all of them)
+  std::vector<char> small;       // per job
+  std::vector<int> small_jobs;   // job indices, in SmallJob order
+  SmallJob* d_small = nullptr;   // device job table
+  uint32_t small_ctas = 0;
+  std::vector<const atc_testset_handle*> small_ts;  // distinct handles the launch waits for
 };
 
 namespace {
@@ -45,6 +51,12 @@ constexpr uint64_t kBatchStride = 2 + kBatchPrefix;
 
 size_t batch_res_words(int n) { return (size_t)n * (kBatchStride + 8); }
 
+// Spaces at most this large run in k_sweep_small (the whole space of every corpus
+// gemm program); each gets one CTA per kSmallSlice bindings.
+constexpr uint64_t kSmallMax = 1ull << 20;
+constexpr uint64_t kSmallSlice = 4096;
+constexpr int kSmallBudget = 16;  // output positions thread_check looks at (t = 0)
+
 // Concurrent branches: conv spaces (large K1 launches) on the caller's stream,
 // gemm spaces (chains of small latency-bound kernels) round-robin on the side
 // streams with their own scratch (slot + 32 * (k + 1)); they fork from and join
@@ -55,20 +67,33 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
   cudaMemsetAsync(b->res, 0, batch_res_words(b->n) * 8, st);
   int n_side = 0;
   // jobs with an empty range (a multi-GPU rank's share of nothing) take no stream,
-  // event wait or graph node at all
-  auto active = [&](int j) { return b->batched[j] && b->jobs[j].end > b->jobs[j].begin; };
+  // event wait or graph node at all; small spaces run in the one k_sweep_small launch
+  auto active = [&](int j) { return b->batched[j] && !b->small[j] && b->jobs[j].end > b->jobs[j].begin; };
   int n_active = 0;
   for (int j = 0; j < b->n; ++j) {
     n_active += active(j);
     n_side += active(j) && b->plans[j].sp.sem != ATC_SEM_CONV2D;
   }
-  const bool split = n_side > 1 || (n_side == 1 && n_side < n_active);
+  const bool has_small = b->small_ctas > 0;
+  const bool split = has_small ? n_active > 0 : n_side > 1 || (n_side == 1 && n_side < n_active);
   if (split) {
     cudaEventRecord(ctx->fork_ev, st);
     for (int k = 0; k < atc_ctx::kSideStreams; ++k) cudaStreamWaitEvent(ctx->side_stream[k], ctx->fork_ev, 0);
     cudaStreamWaitEvent(ctx->conv_stream, ctx->fork_ev, 0);
   }
-  int side_next = 0, conv_next = 0;
+  if (has_small) {  // every small space in one launch, on side stream 0 (or `st` alone)
+    cudaStream_t ss = split ? ctx->side_stream[0] : st;
+    for (const atc_testset_handle* h : b->small_ts) {
+      if (wait_uploads)
+        ts_wait(h, ss);
+      else if (h->ready)
+        cudaStreamWaitEvent(ss, h->ready, cudaEventWaitExternal);
+    }
+    k_sweep_small<<<b->small_ctas, 256, 0, ss>>>(b->d_small, (int)b->small_jobs.size(), kBatchPrefix, kSmallBudget,
+                                                 b->mode, (unsigned long long)kEnumChunkCap + 1);
+    if (ctx->prof) ctx->prof_kernels += 1;
+  }
+  int side_next = has_small ? 1 : 0, conv_next = 0;
   int rc = ATC_OK;
   for (int j = 0; j < b->n && rc == ATC_OK; ++j) {
     if (!active(j)) continue;
@@ -79,13 +104,16 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
     // caller's stream; gemm spaces round-robin over the side streams
     int sk = -1;
     if (split && e.sp.sem == ATC_SEM_CONV2D) {
-      if (job.end - job.begin < (1ull << 30)) {
+      if (ctx->opt_conv_streams > 1) {  // large conv chains round-robin over conv_stream + side streams 3, 2, 1
+        const int k = conv_next++ % ctx->opt_conv_streams;
+        sk = k == 0 ? -1 : atc_ctx::kSideStreams - k;
+      } else if (job.end - job.begin < (1ull << 30)) {
         sk = conv_next ? 0 : -1;
         conv_next ^= 1;
       }
     } else if (split) {
       sk = side_next;
-      side_next = (side_next + 1) % atc_ctx::kSideStreams;
+      side_next = side_next + 1 < atc_ctx::kSideStreams ? side_next + 1 : (has_small ? 1 : 0);
     }
     const bool side = sk >= 0;
     cudaStream_t js = side ? ctx->side_stream[sk] : split ? ctx->conv_stream : st;
@@ -189,6 +217,43 @@ atc_enum_batch* batch_create(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, i
     cudaMemcpyAsync(b->d_perms[j], jobs[j].perms, (size_t)jobs[j].n_perms * b->plans[j].sp.nA,
                     cudaMemcpyHostToDevice, ctx->stream);
   }
+  // the small (gemm) spaces: one k_sweep_small launch per run, CTAs in job order
+  b->small.assign(n_jobs, 0);
+  std::vector<SmallJob> small;
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(b->res + (size_t)n_jobs * kBatchStride);
+  for (int j = 0; j < n_jobs; ++j) {
+    const atc_enum_job& job = jobs[j];
+    const uint64_t n = job.end - job.begin;
+    if (!b->batched[j] || n == 0 || n > kSmallMax || b->plans[j].sp.sem != ATC_SEM_GEMM) continue;
+    b->small[j] = 1;
+    b->small_jobs.push_back(j);
+    SmallJob sj{};
+    sj.ts = job.ts->view;
+    sj.sp = b->plans[j].sp;
+    sj.src = BindingSource{nullptr, nullptr, b->d_perms[j], b->plans[j].size_maps, job.begin, 1};
+    sj.n = n;
+    sj.res = b->res + (size_t)j * kBatchStride;
+    sj.hist = hist + 8 * (size_t)j;
+    sj.cta0 = b->small_ctas;
+    sj.ctas = (uint32_t)((n + kSmallSlice - 1) / kSmallSlice);
+    b->small_ctas += sj.ctas;
+    small.push_back(sj);
+    if (std::find(b->small_ts.begin(), b->small_ts.end(), job.ts) == b->small_ts.end()) b->small_ts.push_back(job.ts);
+  }
+  if (!small.empty()) {
+    const size_t bytes = small.size() * sizeof(SmallJob);
+    if (transient)
+      b->d_small = (SmallJob*)atc_ctx_scratch(ctx, 25, bytes);
+    else if (cudaMalloc(&b->d_small, bytes) != cudaSuccess)
+      b->d_small = nullptr;
+    if (!b->d_small ||
+        !atc_cuda_ok(ctx, cudaMemcpyAsync(b->d_small, small.data(), bytes, cudaMemcpyHostToDevice, ctx->stream),
+                     "H2D small jobs")) {
+      atc_set_error(ctx, "batch allocation failed (small jobs)");
+      atc_enum_batch_destroy(ctx, b);
+      return nullptr;
+    }
+  }
   return b;
 }
 
@@ -214,6 +279,7 @@ void atc_enum_batch_destroy(atc_ctx* ctx, atc_enum_batch* b) {
   if (ctx) cudaSetDevice(ctx->device);
   if (b->exec) cudaGraphExecDestroy(b->exec);
   if (!b->transient) {
+    if (b->d_small) cudaFree(b->d_small);
     if (b->perm_block) cudaFree(b->perm_block);
     if (b->res) cudaFree(b->res);
     if (b->h_res) cudaFreeHost(b->h_res);

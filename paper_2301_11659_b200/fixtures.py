@@ -145,3 +145,25 @@ def load(stem: str) -> Program:
 def pipeline_reports() -> list:
     with open(os.path.join(GOLDEN, "pipeline.json")) as f:
         return json.load(f)
+
+
+def conv_passing() -> dict:
+    """tests/golden/conv_passing.json: every conv space's full passing list at T = 16
+    and T = 10 as the GPU sweep reports it, keyed "<stem>x<spec>" (tools/conv_passing.py);
+    pinned by the reference's verdicts on their neighbourhoods (conv_neighbourhoods)."""
+    with open(os.path.join(GOLDEN, "conv_passing.json")) as f:
+        return json.load(f)
+
+
+def conv_neighbourhoods() -> dict:
+    """tests/golden/conv_neighbourhoods.npz (oracle/gen_neighbourhoods.py): the
+    reference's verify_rewrite verdicts (T = 16) of every binding within `radius` of
+    each passing index and pruned candidate of each conv space:
+    {key: {"idx", "fail_t", "reason", "centers"}}, plus "radius"."""
+    z = np.load(os.path.join(GOLDEN, "conv_neighbourhoods.npz"))
+    out = {"radius": int(z["radius"])}
+    for name in z.files:
+        if ":" in name:
+            key, field = name.split(":")
+            out.setdefault(key, {})[field] = z[name]
+    return out

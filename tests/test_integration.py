@@ -31,7 +31,10 @@ def test_adapter_reproduces_reference_pipeline():
     rc, lines, err = _run("corpus")
     assert rc == 0, err + json.dumps(lines[-3:])[:4000]
     assert lines[-1]["mismatches"] == 0
-    funcs = [x for x in lines[:-1] if x.get("reference_status") != "Misclassified"]
+    # every function of all 55 corpus files (gemm, conv, nonidiom); 34 reach the
+    # candidate stage (the rest are Misclassified: no candidate stage in either)
+    assert len({x["stem"] for x in lines[:-1]}) == 55 and len(lines) - 1 == 58
+    funcs = [x for x in lines[:-1] if x.get("candidate_stage")]
     assert len(funcs) == 34
     assert all(x["same_report_json"] and x["fast_same_winner"] for x in funcs)
     lifted = [x for x in funcs if x.get("gpu_status") == "Lifted"]
