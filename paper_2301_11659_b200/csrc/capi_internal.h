@@ -57,7 +57,7 @@ struct atc_ctx {
   // per-context options (atc_set_option): kernel-variant selection for A/B checks
   int opt_conv_screen = ATC_CONV_SCREEN_AUTO;
   int opt_tc_flags = 0;
-  int opt_conv_streams = 1;  // streams the conv chains of a sweep round-robin over
+  int opt_conv_streams = 4;  // streams the conv chains of a sweep round-robin over (tools/sweep_streams.py)
   bool tc_configured = false;  // k_tc_gemm* shared-memory attributes set on this context's device
   // every ABI entry point holds this for its whole call, so a context is
   // serialised (the pipeline's worker threads may share one)
@@ -130,8 +130,13 @@ __global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* sur
                              const int32_t* surv_keys, int32_t* keys);
 __global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason);
 __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v);
-__global__ void k_sweep_small(const SmallJob* jobs, int n_jobs, uint64_t prefix, int budget, int mode,
-                              uint64_t overflow_mark);
+__global__ void k_sweep_small(const SmallJob* jobs, int n_jobs, int budget, int mode, uint2* surv, int32_t* keys,
+                              uint64_t surv_cap, unsigned long long* surv_cnt);
+__global__ void k_confirm_small(const SmallJob* jobs, int T, int mode, const uint2* surv, int32_t* keys,
+                                uint64_t surv_cap, const unsigned long long* surv_cnt);
+__global__ void k_finalize_small(const SmallJob* jobs, int n_jobs, uint64_t prefix, const uint2* surv,
+                                 const int32_t* keys, uint64_t surv_cap, const unsigned long long* surv_cnt,
+                                 uint64_t overflow_mark);
 __global__ void k_finalize(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
                            const int32_t* surv_keys, uint64_t base, uint64_t* res, uint64_t res_cap,
                            unsigned long long* hist);

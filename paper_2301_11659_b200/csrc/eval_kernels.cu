@@ -968,26 +968,25 @@ __global__ void k_finalize(const uint64_t* surv, const unsigned long long* surv_
 namespace atc {
 // ------------------------------------------------------- small-space sweep --
 // Every small enumerated space of a sweep (the gemm spaces: 162 .. 279,936
-// bindings) in ONE launch.  A space's previous chain (written-set table, position-0
-// table, row screen, K2a, K2b, finalize: six latency-bound launches, each mostly
-// ramp-up and tail) becomes a slice of CTAs of this kernel:
-//   phase 1  thread per binding of the CTA's slice: t = 0 by thread_check (run_dispatch
-//            extents, access bounds, the written set, up to `budget` output
-//            positions — exact FP64) — rejections go to the reason histogram,
-//            the rest to a shared survivor list;
-//   phase 2  warp per survivor: warp_verdict for t = 0 (complete) and every t >= 1
-//            in order, stopping at the first failure (= the binding's first failing
-//            test and reason, as in K2);
-//   result   the job's block as k_finalize writes it: [0] += K1 survivors, [1]
-//            passing count, [2 ..) passing indices (global), histogram += reasons.
-// A CTA whose survivors overflow the shared list marks the job (res[0] beyond the
-// host's chunk cap) and the host re-runs that job through atc_eval_enumerated.
-constexpr int kSmallSurvCap = 2048;
-
-__global__ void __launch_bounds__(256) k_sweep_small(const SmallJob* __restrict__ jobs, int n_jobs, uint64_t prefix,
-                                                     int budget, int mode, uint64_t overflow_mark) {
-  __shared__ uint32_t s_surv[kSmallSurvCap];
-  __shared__ unsigned int s_nsurv, s_hist[ATC_REASON_COUNT];
+// bindings) in three launches instead of a chain of six per space (written-set
+// table, position-0 table, row screen, K2a, K2b, finalize — each mostly ramp-up
+// and tail):
+//   k_sweep_small     CTA slices of every job: thread per binding, t = 0 by
+//                     thread_check (run_dispatch extents, access bounds, the written
+//                     set, up to `budget` output positions, exact FP64); rejections
+//                     go to the job's histogram, the rest to one global survivor
+//                     list (job, index);
+//   k_confirm_small   warp per (survivor, t) over the whole grid, t-major (K2b's
+//                     order): warp_verdict, atomicMin of t*8 + reason;
+//   k_finalize_small  thread per survivor: passing indices into the job's block
+//                     ([1] count, [2 ..) global indices), failures into its
+//                     histogram; [0] += the job's K1 survivors.
+// On survivor-list overflow every job's [0] is marked and the host re-runs them
+// through atc_eval_enumerated.
+__global__ void __launch_bounds__(256) k_sweep_small(const SmallJob* __restrict__ jobs, int n_jobs, int budget,
+                                                     int mode, uint2* surv, int32_t* keys, uint64_t surv_cap,
+                                                     unsigned long long* surv_cnt) {
+  __shared__ unsigned int s_hist[ATC_REASON_COUNT];
   __shared__ int64_t s_ints0[kMaxInts];
   __shared__ int s_job;
   if (threadIdx.x == 0) {  // the job owning this CTA (jobs sorted by cta0)
@@ -998,20 +997,21 @@ __global__ void __launch_bounds__(256) k_sweep_small(const SmallJob* __restrict_
       else hi = mid - 1;
     }
     s_job = lo;
-    s_nsurv = 0;
   }
   if (threadIdx.x < ATC_REASON_COUNT) s_hist[threadIdx.x] = 0;
   __syncthreads();
-  const SmallJob& J = jobs[s_job];
-  const TestsetView& ts = J.ts;
-  const SpecView& sp = J.sp;
+  const int j = s_job;
+  const SmallJob& J = jobs[j];
+  const TestsetView ts = J.ts;
+  const SpecView sp = J.sp;
+  const BindingSource src = J.src;
   if (threadIdx.x < ts.nI) s_ints0[threadIdx.x] = ts.ints[threadIdx.x];
   __syncthreads();
   const uint32_t c = blockIdx.x - J.cta0;
   const uint64_t lo = J.n * c / J.ctas, hi = J.n * (c + 1) / J.ctas;
   for (uint64_t idx = lo + threadIdx.x; idx < hi; idx += blockDim.x) {
     int ptr_of[ATC_MAX_ARRAYS], int_of[ATC_MAX_SIZES];
-    decode_binding(J.src, sp, ts.nI, idx, ptr_of, int_of);
+    decode_binding(src, sp, ts.nI, idx, ptr_of, int_of);
     int64_t sz[ATC_MAX_SIZES];
     for (int q = 0; q < sp.nS; ++q) sz[q] = s_ints0[int_of[q]];
     bool complete;
@@ -1019,33 +1019,59 @@ __global__ void __launch_bounds__(256) k_sweep_small(const SmallJob* __restrict_
     if (r > 0) {
       atomicAdd(&s_hist[r], 1u);
     } else {
-      const unsigned int slot = atomicAdd(&s_nsurv, 1u);
-      if (slot < kSmallSurvCap) s_surv[slot] = (uint32_t)idx;
-    }
-  }
-  __syncthreads();
-  const unsigned int nsurv = s_nsurv;
-  if (nsurv > kSmallSurvCap) {  // the host redoes this job alone
-    if (threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(J.res), (unsigned long long)overflow_mark);
-    return;
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
-  for (unsigned int i = warp; i < nsurv; i += warps) {
-    const uint64_t idx = s_surv[i];
-    int r = 0;
-    for (int t = 0; t < ts.T && !r; ++t) r = warp_verdict(ts, sp, J.src, idx, t, mode, lane);
-    if (lane == 0) {
-      if (r) {
-        atomicAdd(&s_hist[r], 1u);
-      } else {
-        const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(J.res + 1), 1ull);
-        if (slot < prefix) J.res[2 + slot] = J.src.begin + idx;
+      const unsigned long long slot = atomicAdd(surv_cnt, 1ull);
+      if (slot < surv_cap) {
+        surv[slot] = make_uint2((uint32_t)j, (uint32_t)idx);
+        keys[slot] = kPassKey;
       }
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(J.res), (unsigned long long)nsurv);
   if (threadIdx.x < ATC_REASON_COUNT && s_hist[threadIdx.x])
     atomicAdd(&J.hist[threadIdx.x], (unsigned long long)s_hist[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k_confirm_small(const SmallJob* __restrict__ jobs, int T, int mode,
+                                                       const uint2* surv, int32_t* keys, uint64_t surv_cap,
+                                                       const unsigned long long* surv_cnt) {
+  unsigned long long cnt = *surv_cnt;
+  if (cnt > surv_cap) return;
+  const int lane = threadIdx.x & 31;
+  const uint64_t work = cnt * (uint64_t)T;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t w = (uint64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; w < work; w += warps) {
+    const uint64_t t64 = w / cnt;
+    const uint64_t si = w - t64 * cnt;
+    const int t = (int)t64;
+    const uint2 e = surv[si];
+    const SmallJob& J = jobs[e.x];
+    if (t >= J.ts.T) continue;
+    if (*(volatile int32_t*)(keys + si) < fail_key(t, 0)) continue;  // failed at a lower t already
+    const int r = warp_verdict(J.ts, J.sp, J.src, e.y, t, mode, lane);
+    if (lane == 0 && r) atomicMin(&keys[si], fail_key(t, r));
+  }
+}
+
+__global__ void k_finalize_small(const SmallJob* __restrict__ jobs, int n_jobs, uint64_t prefix, const uint2* surv,
+                                 const int32_t* keys, uint64_t surv_cap, const unsigned long long* surv_cnt,
+                                 uint64_t overflow_mark) {
+  const unsigned long long cnt = *surv_cnt;
+  if (cnt > surv_cap) {  // every small job is redone by the host
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_jobs; j += gridDim.x * blockDim.x)
+      jobs[j].res[0] = overflow_mark;
+    return;
+  }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 e = surv[i];
+    const SmallJob& J = jobs[e.x];
+    atomicAdd(reinterpret_cast<unsigned long long*>(J.res), 1ull);
+    const int32_t k = keys[i];
+    if (k == kPassKey) {
+      const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(J.res + 1), 1ull);
+      if (slot < prefix) J.res[2 + slot] = J.src.begin + e.y;
+    } else {
+      atomicAdd(&J.hist[k & 7], 1ull);
+    }
+  }
 }
 }  // namespace atc

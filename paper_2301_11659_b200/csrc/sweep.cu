@@ -38,6 +38,10 @@ struct atc_enum_batch {
   std::vector<int> small_jobs;   // job indices, in SmallJob order
   SmallJob* d_small = nullptr;   // device job table
   uint32_t small_ctas = 0;
+  int small_T = 0;                // largest T of the small jobs
+  uint2* small_surv = nullptr;    // (job, index) survivors of k_sweep_small
+  int32_t* small_keys = nullptr;
+  unsigned long long* small_cnt = nullptr;
   std::vector<const atc_testset_handle*> small_ts;  // distinct handles the launch waits for
 };
 
@@ -56,11 +60,16 @@ size_t batch_res_words(int n) { return (size_t)n * (kBatchStride + 8); }
 constexpr uint64_t kSmallMax = 1ull << 20;
 constexpr uint64_t kSmallSlice = 4096;
 constexpr int kSmallBudget = 16;  // output positions thread_check looks at (t = 0)
+constexpr uint64_t kSmallSurvCap = 1ull << 20;  // survivors of all small jobs together
 
-// Concurrent branches: conv spaces (large K1 launches) on the caller's stream,
-// gemm spaces (chains of small latency-bound kernels) round-robin on the side
-// streams with their own scratch (slot + 32 * (k + 1)); they fork from and join
-// back into `st`, so a captured graph has the same branches.
+// Concurrent branches: the small (gemm) spaces as one k_sweep_small chain on side
+// stream 0; the conv spaces' chains (tables, K1, K2, finalize) round-robin over
+// ctx->opt_conv_streams streams (conv_stream, side streams 3, 2, 1: one space's
+// latency-bound tables and K2 run beside another's K1; 4 streams: 3.00 -> 2.32 ms
+// per corpus sweep, tools/sweep_streams.py); other large gemm ranges round-robin on
+// the remaining side streams.  Side stream k's scratch lives at slot + 32 * (k + 1);
+// every branch forks from and joins back into `st`, so a captured graph has the
+// same branches.
 int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_uploads) {
   const uint64_t chunk_cap = kEnumChunkCap;
   unsigned long long* hist = reinterpret_cast<unsigned long long*>(b->res + (size_t)b->n * kBatchStride);
@@ -75,7 +84,9 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
     n_side += active(j) && b->plans[j].sp.sem != ATC_SEM_CONV2D;
   }
   const bool has_small = b->small_ctas > 0;
-  const bool split = has_small ? n_active > 0 : n_side > 1 || (n_side == 1 && n_side < n_active);
+  const int n_conv = n_active - n_side;
+  const bool split = (has_small && n_active > 0) || (ctx->opt_conv_streams > 1 && n_conv > 1) || n_side > 1 ||
+                     (n_side == 1 && n_side < n_active);
   if (split) {
     cudaEventRecord(ctx->fork_ev, st);
     for (int k = 0; k < atc_ctx::kSideStreams; ++k) cudaStreamWaitEvent(ctx->side_stream[k], ctx->fork_ev, 0);
@@ -89,9 +100,15 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
       else if (h->ready)
         cudaStreamWaitEvent(ss, h->ready, cudaEventWaitExternal);
     }
-    k_sweep_small<<<b->small_ctas, 256, 0, ss>>>(b->d_small, (int)b->small_jobs.size(), kBatchPrefix, kSmallBudget,
-                                                 b->mode, (unsigned long long)kEnumChunkCap + 1);
-    if (ctx->prof) ctx->prof_kernels += 1;
+    const int nj = (int)b->small_jobs.size();
+    cudaMemsetAsync(b->small_cnt, 0, 8, ss);
+    k_sweep_small<<<b->small_ctas, 256, 0, ss>>>(b->d_small, nj, kSmallBudget, b->mode, b->small_surv, b->small_keys,
+                                                 kSmallSurvCap, b->small_cnt);
+    k_confirm_small<<<(unsigned)ctx->sm_count * 4, 256, 0, ss>>>(b->d_small, b->small_T, b->mode, b->small_surv,
+                                                                 b->small_keys, kSmallSurvCap, b->small_cnt);
+    k_finalize_small<<<64, 256, 0, ss>>>(b->d_small, nj, kBatchPrefix, b->small_surv, b->small_keys, kSmallSurvCap,
+                                         b->small_cnt, (unsigned long long)kEnumChunkCap + 1);
+    if (ctx->prof) ctx->prof_kernels += 3;
   }
   int side_next = has_small ? 1 : 0, conv_next = 0;
   int rc = ATC_OK;
@@ -237,16 +254,22 @@ atc_enum_batch* batch_create(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, i
     sj.cta0 = b->small_ctas;
     sj.ctas = (uint32_t)((n + kSmallSlice - 1) / kSmallSlice);
     b->small_ctas += sj.ctas;
+    b->small_T = std::max(b->small_T, (int)job.ts->T);
     small.push_back(sj);
     if (std::find(b->small_ts.begin(), b->small_ts.end(), job.ts) == b->small_ts.end()) b->small_ts.push_back(job.ts);
   }
   if (!small.empty()) {
+    // survivor list and keys: context scratch (the same slots every batch; a graph
+    // replays with them in place)
+    b->small_surv = (uint2*)atc_ctx_scratch(ctx, 26, kSmallSurvCap * sizeof(uint2));
+    b->small_keys = (int32_t*)atc_ctx_scratch(ctx, 27, kSmallSurvCap * 4);
+    b->small_cnt = (unsigned long long*)atc_ctx_scratch(ctx, 28, 64);
     const size_t bytes = small.size() * sizeof(SmallJob);
     if (transient)
       b->d_small = (SmallJob*)atc_ctx_scratch(ctx, 25, bytes);
     else if (cudaMalloc(&b->d_small, bytes) != cudaSuccess)
       b->d_small = nullptr;
-    if (!b->d_small ||
+    if (!b->d_small || !b->small_surv || !b->small_keys || !b->small_cnt ||
         !atc_cuda_ok(ctx, cudaMemcpyAsync(b->d_small, small.data(), bytes, cudaMemcpyHostToDevice, ctx->stream),
                      "H2D small jobs")) {
       atc_set_error(ctx, "batch allocation failed (small jobs)");
