@@ -90,6 +90,10 @@ typedef struct {
   const double* const* final_;     /* [T*n_ptrs]: the original run's final regions       */
   const int32_t* test_ok;          /* [T]: 0 if draw_sizes failed or the original run was
                                       not Normal at t (every binding fails at t), else 1 */
+  /* user float params (signature order) as build_probe_image drew them — read only
+   * by the extended semantics (atc_eval_bindings_ext); may be 0 / NULL */
+  int32_t n_floats;
+  const double* float_values;      /* [T][n_floats]                                      */
 } atc_testsets;
 
 typedef struct atc_ctx atc_ctx;
@@ -317,6 +321,68 @@ int atc_run_reference(atc_ctx* ctx, const atc_spec_desc* spec, const int64_t* si
  * when run_dispatch would throw. */
 int atc_dispatch(atc_ctx* ctx, const atc_spec_desc* spec, const int64_t* sizes,
                  double* const* regions, const int64_t* region_len, const int32_t* region_is_f32);
+
+/* ---- Extended semantics (no reference counterpart) ------
+ * The wide GEMM (transA/transB, alpha/beta, lda/ldb/ldc) and conv2d with stride,
+ * padding and dilation that BASELINE configs 3-4 name.  The reference cannot
+ * express them: run_dispatch ignores float scalars (rewriter.cpp:130-132) and its
+ * conv2d is valid-padding, unit-stride (equivalence.cpp:67-93); its specs carry
+ * size roles only.  The semantics are defined here (paper_2301_11659_b200/specs/
+ * gemm_ext.json, conv2d_ext.json) and restated literally on the CPU in
+ * oracle/ext_oracle.c, which known-answer vectors pin (tests/golden/
+ * ext_known_answers.json) — parity against the reference is not defined.
+ *
+ *  gemm_ext (row-major): reason 2 ("dispatch failed") unless m, n, k, lda, ldb, ldc >= 1,
+ *    transa, transb in {0, 1}, lda >= (ta ? m : k), ldb >= (tb ? k : n), ldc >= n and
+ *    every footprint fits its region: ((ta ? k : m) - 1)*lda + (ta ? m : k) <= len(A),
+ *    ((tb ? n : k) - 1)*ldb + (tb ? k : n) <= len(B), (m - 1)*ldc + n <= len(C).  Then
+ *    for i < m, j < n: acc = sum_p opA(i,p)*opB(p,j) (p ascending, FP64, no FMA),
+ *    opA(i,p) = ta ? A[p*lda + i] : A[i*lda + p], opB(p,j) = tb ? B[j*ldb + p] : B[p*ldb + j];
+ *    C[i*ldc + j] = beta == 0 ? alpha*acc : alpha*acc + beta*C[i*ldc + j] (alpha 1 and
+ *    beta 0 when the spec has no such role; f32 regions rounded at write-back).
+ *  conv2d_ext (NCHW / KCRS): reason 2 unless n, c, h, w, k, r, s, stride_h/w, dil_h/w >= 1,
+ *    pad_h/w >= 0, eh = h + 2*pad_h - dil_h*(r - 1) - 1 >= 0 (ew likewise), the bound
+ *    oh / ow equal eh/stride_h + 1 / ew/stride_w + 1 (derived when the spec has no such
+ *    role) and n*c*h*w <= len(in), k*c*r*s <= len(weights), n*k*oh*ow <= len(out).  Then
+ *    out[b,q,y,x] = sum over z < c, u < r, v < s (ascending) of in[b,z,iy,ix]*wt[q,z,u,v],
+ *    iy = y*stride_h - pad_h + u*dil_h, ix = x*stride_w - pad_w + v*dil_w, terms with iy
+ *    or ix outside the image skipped (zero padding); stride/pad/dil default 1/0/1.
+ *  P2 predicate per test t: reason 3 if test t's set failed, 2 as above, else 1 iff
+ *  the full region of a non-LiveIn bound array differs from the recorded final
+ *  (rewriter.cpp:264-279 tolerances), else the next t.
+ *
+ * Bindings: arrays as before; a size param binds a user int (size_map entry < n_ints)
+ * or, for params with a constant domain (trans, stride, pad, dil), a constant
+ * (entry n_ints + c selects iconst[c]); a float param binds a user float (entry <
+ * the test sets' n_floats) or a constant (entry n_floats + c selects fconst[c]). */
+enum { ATC_SEM_GEMM_EXT = 2, ATC_SEM_CONV2D_EXT = 3 };
+enum { ATC_XR_TRANSA = 0, ATC_XR_TRANSB, ATC_XR_STRIDE_H, ATC_XR_STRIDE_W, ATC_XR_PAD_H, ATC_XR_PAD_W,
+       ATC_XR_DIL_H, ATC_XR_DIL_W, ATC_XR_COUNT };
+enum { ATC_FR_ALPHA = 0, ATC_FR_BETA = 1, ATC_FR_COUNT = 2 };
+#define ATC_MAX_FLOATS 4
+#define ATC_MAX_CONSTS 8
+typedef struct {
+  atc_spec_desc base;                    /* semantics ATC_SEM_*_EXT; arrays, sizes, base roles */
+  int32_t n_floats;                      /* float params of the spec (spec order)              */
+  int32_t ext_role_size[ATC_XR_COUNT];   /* size-param index of each extended role, -1 absent  */
+  int32_t role_float[ATC_FR_COUNT];      /* float-param index of alpha / beta, -1 absent       */
+  int32_t n_iconst, n_fconst;
+  int64_t iconst[ATC_MAX_CONSTS];
+  double fconst[ATC_MAX_CONSTS];
+} atc_spec_ext;
+
+/* Explicit candidate list under an extended spec: arr_map [n][n_arrays], size_map
+ * [n][n_sizes], float_map [n][n_floats] (encodings above).  Outputs as
+ * atc_eval_bindings (FP64, exact). */
+int atc_eval_bindings_ext(atc_ctx* ctx, const atc_spec_ext* spec, const atc_testset_handle* ts,
+                          const uint8_t* arr_map, const uint8_t* size_map, const uint8_t* float_map,
+                          int64_t n_bindings, int8_t* fail_t, int8_t* reason, int64_t* first_pass);
+/* The extended semantics on caller buffers (spec order): sizes[q] per size param,
+ * floats[f] per float param, buffers[a] of buffer_len[a] doubles (non-LiveIn arrays
+ * rewritten in place, f32-rounded where buffer_is_f32[a]).  ATC_ERR_DISPATCH (with
+ * the failed check in atc_last_error) where the P2 predicate gives reason 2. */
+int atc_run_reference_ext(atc_ctx* ctx, const atc_spec_ext* spec, const int64_t* sizes, const double* floats,
+                          double* const* buffers, const int64_t* buffer_len, const int32_t* buffer_is_f32);
 
 /* ---- Device groups --------------------------------------
  * Several GPUs of one process: one context (streams, scratch, pools) per device.

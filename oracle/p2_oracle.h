@@ -52,6 +52,34 @@ void oracle_verify_many(const oracle_spec* s, int T, int nI, int nP, const int64
 void oracle_cpu_gemm(const float* a, const float* b, float* c, int64_t m, int64_t n, int64_t k);
 void oracle_xpu_gemm(const float* a, const float* b, float* c, int64_t m, int64_t n, int64_t k, int threads);
 
+/* ---- Extended semantics (include/atc_b200.h, "Extended semantics") -----------
+ * No reference counterpart: oracle/ext_oracle.c IS the definition, restated
+ * literally (full-region copies, the loops as written in the header comment, full
+ * compares); pinned by the hand-derived known answers of
+ * tests/golden/ext_known_answers.json (tests/test_ext.py). */
+typedef struct {
+  oracle_spec base;       /* semantics 2 gemm_ext, 3 conv2d_ext */
+  int32_t n_floats;
+  int32_t ext_role_size[8];
+  int32_t role_float[2];
+  int32_t n_iconst, n_fconst;
+  int64_t iconst[8];
+  double fconst[8];
+} oracle_spec_ext;
+
+/* Runs the extended semantics on caller buffers; returns 0, or 2 when the dispatch
+ * checks fail (buffers untouched).  detail (optional, >= 128 bytes) names the check. */
+int oracle_run_ext(const oracle_spec_ext* s, const int64_t* sizes, const double* floats, double* const* bufs,
+                   const int64_t* lens, const int32_t* is_f32, char* detail);
+
+/* One extended binding against recorded test sets (the P2 predicate of the header);
+ * floats: [T][nF] user float values. */
+void oracle_verify_ext_many(const oracle_spec_ext* s, int T, int nI, int nP, int nF, const int64_t* ints,
+                            const double* floats, const int32_t* is_f32, const int64_t* region_len,
+                            const double* const* init, const double* const* fin, const int32_t* test_ok,
+                            const uint8_t* arr_map, const uint8_t* size_map, const uint8_t* float_map, int64_t n,
+                            int threads, int8_t* fail_t, int8_t* reason);
+
 /* FNV-1a 64 over raw bytes (pins regenerated probe regions to the golden dump). */
 uint64_t oracle_fnv1a(const void* p, int64_t nbytes);
 

@@ -68,6 +68,29 @@ class Testsets(C.Structure):
         ("init", C.POINTER(C.c_void_p)),
         ("final_", C.POINTER(C.c_void_p)),
         ("test_ok", C.POINTER(C.c_int32)),
+        ("n_floats", C.c_int32),
+        ("float_values", C.c_void_p),
+    ]
+
+
+SEM_GEMM_EXT, SEM_CONV2D_EXT = 2, 3
+ATC_XR_COUNT, ATC_FR_COUNT, ATC_MAX_FLOATS, ATC_MAX_CONSTS = 8, 2, 4, 8
+EXT_SIZE_ROLES = ["transa", "transb", "stride_h", "stride_w", "pad_h", "pad_w", "dil_h", "dil_w"]
+EXT_FLOAT_ROLES = ["alpha", "beta"]
+
+
+class SpecExt(C.Structure):
+    """atc_spec_ext (include/atc_b200.h, "Extended semantics")."""
+
+    _fields_ = [
+        ("base", SpecDesc),
+        ("n_floats", C.c_int32),
+        ("ext_role_size", C.c_int32 * ATC_XR_COUNT),
+        ("role_float", C.c_int32 * ATC_FR_COUNT),
+        ("n_iconst", C.c_int32),
+        ("n_fconst", C.c_int32),
+        ("iconst", C.c_int64 * ATC_MAX_CONSTS),
+        ("fconst", C.c_double * ATC_MAX_CONSTS),
     ]
 
 
@@ -222,6 +245,9 @@ _SIGS = [
     ("atc_group_batch_run", C.c_int, [_P, _P]),
     ("atc_group_batch_destroy", None, [_P, _P]),
     ("atc_plan_shards", C.c_int, [_P, C.c_int32, C.c_int32, _P, _P]),
+    ("atc_eval_bindings_ext", C.c_int, [_P, C.POINTER(SpecExt), _P, _P, _P, _P, C.c_int64, _P, _P,
+                                        C.POINTER(C.c_int64)]),
+    ("atc_run_reference_ext", C.c_int, [_P, C.POINTER(SpecExt), _P, _P, _P, _P, _P]),
     ("atc_run_reference", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P]),
     ("atc_dispatch", C.c_int, [_P, C.POINTER(SpecDesc), _P, _P, _P, _P]),
     ("atc_sgemm_rm", C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int32]),

@@ -525,14 +525,37 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
   __shared__ int s_pidx[128];
   __shared__ M128 s_pgt[129];      // s_pgt[r] = pairs of product rank >= r
   __shared__ unsigned int s_hist[ATC_REASON_COUNT];
+  __shared__ M128 s_row[kPairMaxInts];   // bits [j*nI, j*nI + nI): row j of the plane
+  __shared__ int32_t s_pp[128];          // product of pair b = (c digit b / nI, x digit b % nI)
+  __shared__ uint8_t s_rk[128];          // stable rank of pair b's product
+  __shared__ uint64_t s_div[8];          // 64-bit quotients every thread needs (computed once)
+  __shared__ uint32_t s_cks[NS];
   const int nI = ts.nI, nI2 = nI * nI;
-  if (threadIdx.x < nI) s_u[threadIdx.x] = (int32_t)ts.ints[threadIdx.x];
+  // CTA tables: built once, from O(nI^2) work per thread at most (the per-CTA
+  // prologue is paid by every one of the 4 x 148 CTAs)
+  if (threadIdx.x < nI) {
+    s_u[threadIdx.x] = (int32_t)ts.ints[threadIdx.x];
+    s_row[threadIdx.x] = bit_range(threadIdx.x * nI, threadIdx.x * nI + nI);
+  }
   if (threadIdx.x < ATC_REASON_COUNT) s_hist[threadIdx.x] = 0;
   if (threadIdx.x < 128) s_prod[threadIdx.x] = INT32_MAX;
-  for (int m = threadIdx.x; m < (1 << nI); m += blockDim.x) {
+  if (threadIdx.x == 32) {
+    const uint64_t nI3 = (uint64_t)nI2 * nI, planes_per_perm = size_maps / (uint64_t)nI2;
+    s_div[0] = plan.pt.per_perm / (uint64_t)nI;   // cperm
+    s_div[1] = planes_per_perm;
+    s_div[2] = planes_per_perm / (uint64_t)nI;    // cubes per permutation
+    s_div[3] = begin / nI3;                       // first cube
+    s_div[4] = (end + nI3 - 1) / nI3;             // one past the last cube
+  }
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + NS) {
+    const int q = threadIdx.x - 64;
+    s_cks[q] = q >= 2 ? (uint32_t)(plan.key_stride[q] / (uint64_t)nI) : 0u;
+  }
+  __syncthreads();
+  if (threadIdx.x < nI2) s_pp[threadIdx.x] = s_u[threadIdx.x % nI] * s_u[threadIdx.x / nI];
+  for (int m = threadIdx.x; m < (1 << nI); m += blockDim.x) {  // rows j of the plane for every bit j of m
     M128 r{0, 0};
-    for (int j = 0; j < nI; ++j)
-      if (m >> j & 1) r = r | bit_range(j * nI, j * nI + nI);
+    for (uint32_t mm = (uint32_t)m; mm; mm &= mm - 1) r = r | s_row[__ffs(mm) - 1];
     s_rowx[m] = r;
   }
   __syncthreads();
@@ -550,30 +573,39 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
   }
   if (threadIdx.x < nI2) {  // stable rank of the pair's product
     const int b = threadIdx.x;
-    const int32_t pr = s_u[b % nI] * s_u[b / nI];
+    const int32_t pr = s_pp[b];
     int rank = 0;
     for (int i = 0; i < nI2; ++i) {
-      const int32_t q = s_u[i % nI] * s_u[i / nI];
+      const int32_t q = s_pp[i];
       rank += q < pr || (q == pr && i < b);
     }
     s_prod[rank] = pr;
     s_pidx[rank] = b;
+    s_rk[b] = (uint8_t)rank;
   }
   __syncthreads();
   uint8_t* s_rank = reinterpret_cast<uint8_t*>(s_rowx + (1 << nI));
-  if (threadIdx.x <= 128) {
-    M128 m{0, 0};
-    for (int r = threadIdx.x; r < nI2; ++r) set_bit(m, s_pidx[r]);
-    s_pgt[threadIdx.x] = m;
+  {  // s_pgt[r] = pairs of rank >= r: one ballot per 32 pairs (warp w takes r = w, w + 8, ...)
+    const int lane = threadIdx.x & 31;
+    for (int r = threadIdx.x >> 5; r <= nI2; r += blockDim.x >> 5) {
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int b = k * 32 + lane;
+        w[k] = __ballot_sync(0xffffffffu, b < nI2 && s_rk[b] >= r);
+      }
+      if (lane == 0) s_pgt[r] = M128{(uint64_t)w[0] | (uint64_t)w[1] << 32, (uint64_t)w[2] | (uint64_t)w[3] << 32};
+    }
   }
+  int p2 = 1;  // power of two > nI2: branch-free search over the padded products
+  while (p2 <= nI2) p2 <<= 1;
   for (int t = threadIdx.x; t < lut_n; t += blockDim.x) {  // rank = number of products <= t
     int lo = 0;
-    while (lo < nI2 && s_prod[lo] <= t) ++lo;
+    for (int step = p2 >> 1; step > 0; step >>= 1)
+      if (s_prod[lo + step - 1] <= t) lo += step;
     s_rank[t] = (uint8_t)lo;
   }
   __syncthreads();
-  int p2 = 1;  // power of two > nI2: branch-free search over the padded products
-  while (p2 <= nI2) p2 <<= 1;
   // per (in region, w digit, h digit): the number of pair products <= len(in)/(h*w)
   // (the s_pgt index of the in-extent dispatch check), and 1/(h*w) for the UB bound
   const int nP = ts.nP;
@@ -592,7 +624,7 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
     s_ainr[i] = (uint8_t)lo;
   }
   for (int i = threadIdx.x; i < nI2; i += blockDim.x) {
-    const int64_t hw = (int64_t)s_u[i % nI] * s_u[i / nI];
+    const int64_t hw = s_pp[i];
     s_rhw[i] = hw >= 1 ? __frcp_rn((float)hw) : 0.f;
   }
   __syncthreads();
@@ -609,13 +641,12 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
   const bool test_ok0 = ts.test_ok[0] != 0;
   // position-0 verdicts of a plane's nI values of c: one word of plan.cmask at
   // (table key without c) / nI — the key strides of the other roles are multiples of nI
-  const uint32_t cperm = (uint32_t)(plan.pt.per_perm / (uint64_t)nI);
+  const uint32_t cperm = (uint32_t)s_div[0];
   uint32_t cks[NS];
 #pragma unroll
-  for (int q = 2; q < NS; ++q) cks[q] = (uint32_t)(plan.key_stride[q] / (uint64_t)nI);
+  for (int q = 2; q < NS; ++q) cks[q] = s_cks[q];
   const M128 all = bit_range(0, nI2);
   const M128 x_lt1 = ~s_gtx[0] & all, c_lt1 = ~s_gtc[0] & all;
-  const uint64_t planes_per_perm = size_maps / (uint64_t)nI2;
   const uint32_t magic = (uint32_t)(0xFFFFFFFFull / (uint32_t)nI) + 1u;  // n / nI = umulhi(n, magic), n < 2^27
   unsigned int cnt1 = 0, cnt2 = 0, cnt3 = 0, cnt4 = 0;
   // whole cubes inside [begin, end): mismatches are counted as the remainder
@@ -623,8 +654,8 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
   // a thread owns a "cube": the nI planes sharing the permutation and digits 3..8
   // (all values of tc_h, digit 2); everything free of h is computed once per cube
   const uint64_t nI3 = (uint64_t)nI2 * nI;
-  const uint64_t cubes_per_perm = planes_per_perm / (uint64_t)nI;
-  const uint64_t cube_lo = begin / nI3, cube_hi = (end + nI3 - 1) / nI3;
+  const uint64_t cubes_per_perm = s_div[2];
+  const uint64_t cube_lo = s_div[3], cube_hi = s_div[4];
   for (uint64_t cb = cube_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; cb < cube_hi;
        cb += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t c0b = cb * nI3;

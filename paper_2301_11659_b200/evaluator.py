@@ -46,6 +46,9 @@ class RecordedTestsets:
     # the stream position of each region's first draw — atc_testsets_upload_seeded
     seeds: Optional[np.ndarray] = None  # uint64 [T]
     skips: Optional[np.ndarray] = None  # uint64 [T, nP]
+    # the user float params (signature order) as build_probe_image drew them — read
+    # only by the extended semantics (paper_2301_11659_b200/ext.py)
+    floats: Optional[np.ndarray] = None  # float64 [T, nF]
 
     @property
     def ptrs(self) -> list:
@@ -164,6 +167,10 @@ class RecordedTestsets:
         ok = np.ascontiguousarray(self.test_ok, dtype=np.int32)
         s = _lib.Testsets()
         s.n_tests, s.n_ints, s.n_ptrs = T, ints.shape[1], nP
+        if self.floats is not None and self.floats.size:
+            fl = np.ascontiguousarray(self.floats, dtype=np.float64)
+            keep.append(fl)
+            s.n_floats, s.float_values = fl.shape[1], fl.ctypes.data
         s.int_values = ints.ctypes.data_as(C.POINTER(C.c_int64))
         s.ptr_is_f32 = is_f32.ctypes.data_as(C.POINTER(C.c_int32))
         s.region_len = lens.ctypes.data_as(C.POINTER(C.c_int64))
@@ -213,10 +220,14 @@ def record_testsets(function: str, params: list, rules: SizeRules, p2seed: int, 
     int_names = [p.name for p in params if p.kind == "int"]
     T = tests
     ints = np.zeros((T, len(int_names)), dtype=np.int64)
+    float_names = [p.name for p in params if p.kind == "float"]
+    floats = np.zeros((T, len(float_names)), dtype=np.float64)
     init, final, ok = [], [], np.zeros(T, dtype=np.int32)
     seeds, skips = np.zeros(T, dtype=np.uint64), np.zeros((T, len(ptrs)), dtype=np.uint64)
     for t in range(T):
         pt = p2_test_inputs(function, params, rules, p2seed, t)
+        if pt.ok:
+            floats[t] = [pt.floats[n] for n in float_names]
         if not pt.ok:
             init.append([np.zeros(PROBE_REGION_LEN) for _ in ptrs])
             final.append(None)
@@ -231,7 +242,7 @@ def record_testsets(function: str, params: list, rules: SizeRules, p2seed: int, 
             continue
         final.append([fin[p.name] for p in ptrs])
         ok[t] = 1
-    return RecordedTestsets(params, ints, init, final, ok, seeds=seeds, skips=skips)
+    return RecordedTestsets(params, ints, init, final, ok, seeds=seeds, skips=skips, floats=floats)
 
 
 # ------------------------------------------------------------- binding spaces --

@@ -101,11 +101,15 @@ class Program:
         params = self.params
         ptrs = [p for p in params if p.kind == "ptr"]
         ints = np.zeros((T, len(self.user_ints)), dtype=np.int64)
+        float_names = [p.name for p in params if p.kind == "float"]
+        floats = np.zeros((T, len(float_names)), dtype=np.float64)
         init, final, ok = [], [], np.zeros(T, dtype=np.int32)
         seeds, skips = np.zeros(T, dtype=np.uint64), np.zeros((T, len(ptrs)), dtype=np.uint64)
         for rec in self.meta[variant][:T]:
             t = rec["t"]
             pt = p2_test_inputs(self.function, params, rules, self.p2seed, t)
+            if pt.ok:
+                floats[t] = [pt.floats[n] for n in float_names]
             if rec["status"] == "draw_failed" or not pt.ok:
                 assert rec["status"] == "draw_failed" and not pt.ok, f"{self.stem} t={t}: draw mismatch"
                 init.append([np.zeros(len(pt.regions.get(p.name, [0] * 65536))) for p in ptrs])
@@ -130,7 +134,7 @@ class Program:
                 fin.append(f)
             final.append(fin)
             ok[t] = 1
-        return RecordedTestsets(params, ints, init, final, ok, seeds=seeds, skips=skips)
+        return RecordedTestsets(params, ints, init, final, ok, seeds=seeds, skips=skips, floats=floats)
 
 
 @lru_cache(maxsize=None)

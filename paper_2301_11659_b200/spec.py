@@ -23,6 +23,7 @@ class ApiParam:
     dims: list = field(default_factory=list)
     element_type: str = "any"
     role: str = ""
+    domain: list = field(default_factory=list)  # extended specs: the constants this param may bind
 
 
 @dataclass
@@ -85,9 +86,74 @@ class ApiSpec:
         return d
 
 
+EXT_SEMANTICS = {"gemm_ext": "gemm", "conv2d_ext": "conv2d"}
+
+
+def ext_desc(spec: ApiSpec) -> "_lib.SpecExt":
+    """atc_spec_ext of an extended spec (include/atc_b200.h, "Extended semantics"):
+    the base table of the underlying semantics, the extended size roles, the float
+    roles and the constant tables (size_map entry n_ints + c -> iconst[c]; float_map
+    entry n_user_floats + c -> fconst[c], c = the value's position in its table)."""
+    if spec.semantics not in EXT_SEMANTICS:
+        raise SpecError(f"{spec.name}: not an extended spec")
+    base = ApiSpec(spec.name, EXT_SEMANTICS[spec.semantics], spec.layout, spec.affix,
+                   [p for p in spec.params if not (p.kind == "int" and p.role in _lib.EXT_SIZE_ROLES)])
+    d = _lib.SpecExt()
+    b = base.to_desc()
+    sizes = spec.size_params()
+    size_index = {p.name: q for q, p in enumerate(sizes)}
+    d.base = b
+    d.base.semantics = _lib.SEM_GEMM_EXT if spec.semantics == "gemm_ext" else _lib.SEM_CONV2D_EXT
+    # the base table was built without the extended params: re-index against every size param
+    d.base.n_sizes = len(sizes)
+    for a, p in enumerate(spec.arrays()):
+        for k, dim in enumerate(p.dims):
+            d.base.array_dims[a][k] = size_index[dim]
+    table = _lib.SIZE_ROLES if EXT_SEMANTICS[spec.semantics] == "gemm" else _lib.CONV_SIZE_ROLES
+    off = 0 if EXT_SEMANTICS[spec.semantics] == "gemm" else len(_lib.SIZE_ROLES)
+    for r in range(_lib.ATC_SZ_COUNT):
+        d.base.role_size[r] = -1
+    for r in range(_lib.ATC_XR_COUNT):
+        d.ext_role_size[r] = -1
+    for q, p in enumerate(sizes):
+        if p.role in table:
+            d.base.role_size[off + table.index(p.role)] = q
+        elif p.role in _lib.EXT_SIZE_ROLES:
+            d.ext_role_size[_lib.EXT_SIZE_ROLES.index(p.role)] = q
+    floats = spec.float_scalars()
+    d.n_floats = len(floats)
+    for r in range(_lib.ATC_FR_COUNT):
+        d.role_float[r] = -1
+    for f, p in enumerate(floats):
+        if p.role in _lib.EXT_FLOAT_ROLES:
+            d.role_float[_lib.EXT_FLOAT_ROLES.index(p.role)] = f
+    ic, fc = ext_constants(spec)
+    if len(ic) > _lib.ATC_MAX_CONSTS or len(fc) > _lib.ATC_MAX_CONSTS or len(floats) > _lib.ATC_MAX_FLOATS:
+        raise SpecError(f"{spec.name}: too many constants / floats for the GPU decode table")
+    d.n_iconst, d.n_fconst = len(ic), len(fc)
+    for i, v in enumerate(ic):
+        d.iconst[i] = v
+    for i, v in enumerate(fc):
+        d.fconst[i] = v
+    return d
+
+
+def ext_constants(spec: ApiSpec) -> tuple:
+    """The constant tables of an extended spec: distinct int / float domain values in
+    order of appearance."""
+    ic, fc = [], []
+    for p in spec.params:
+        for v in p.domain:
+            tab = ic if p.kind == "int" else fc
+            v = int(v) if p.kind == "int" else float(v)
+            if v not in tab:
+                tab.append(v)
+    return ic, fc
+
+
 def _validate(spec: ApiSpec) -> None:  # api_spec.cpp:91-128
-    if spec.semantics not in ("gemm", "conv2d"):
-        raise SpecError(f"{spec.name}: semantics must be gemm or conv2d")
+    if spec.semantics not in ("gemm", "conv2d", *EXT_SEMANTICS):
+        raise SpecError(f"{spec.name}: semantics must be gemm, conv2d, gemm_ext or conv2d_ext")
     names = set()
     for p in spec.params:
         if p.name in names:
@@ -132,7 +198,7 @@ def parse_api_spec(j: dict) -> ApiSpec:
             raise SpecError(f"bad param kind '{pj['kind']}'")
         spec.params.append(ApiParam(name=pj["name"], kind=kind, liveness=pj.get("liveness", "livein").lower(),
                                     dims=list(pj.get("dims", [])), element_type=pj.get("element_type", "any"),
-                                    role=pj.get("role", "")))
+                                    role=pj.get("role", ""), domain=list(pj.get("domain", []))))
     s = j.get("sampling") or {}
     for name, r in (s.get("ranges") or j.get("ranges") or {}).items():
         spec.ranges[name] = (int(r[0]), int(r[1]))
