@@ -136,7 +136,7 @@ static void verify_ext(const oracle_spec_ext* s, int T, int nI, int nP, int nF, 
   double* bufs[4] = {0, 0, 0, 0};
   int64_t lens[4] = {0, 0, 0, 0};
   int32_t f32[4] = {0, 0, 0, 0};
-  int64_t sizes[12];
+  int64_t sizes[16]; /* ATC_MAX_EXT_SIZES: conv2d_ext has 15 size params */
   double fl[4];
   *fail_t = -1;
   *reason = 0;

@@ -144,7 +144,7 @@ __global__ void k_finalize(const uint64_t* surv, const unsigned long long* surv_
 
 struct atc_testset_handle {
   atc::TestsetView view{};
-  int32_t T = 0, nI = 0, nP = 0;
+  int32_t T = 0, nI = 0, nP = 0, nF = 0;
   std::vector<int64_t> h_ints;  // host copy of the int values
   std::vector<void*> allocations;
   cudaEvent_t ready = nullptr;  // uploads + dirty lists complete (recorded on the copy stream)
@@ -154,7 +154,7 @@ struct atc_testset_handle {
   std::vector<int32_t> is_f32;
   uint8_t* meta = nullptr;      // the small arrays (TestsetView points into it)
   size_t meta_bytes = 0, o_ints = 0, o_rlen = 0, o_roff = 0, o_dof = 0, o_isf = 0, o_tok = 0, o_dcnt = 0,
-         o_dmax = 0;
+         o_dmax = 0, o_flt = 0;
   uint8_t* seeded = nullptr;    // seeds, stream positions, final-minus-init entries
   size_t seeded_cap = 0;
   bool needed_only = false;     // seeded with needed_only: region prefixes only

@@ -41,6 +41,8 @@ struct TestsetView {
   const int64_t* dirty_off;   // [T*nP]
   const int32_t* dirty_cnt;   // [T*nP]
   const int32_t* dirty_max;   // [T*nP]  (-1 when empty)
+  int32_t nF;                 // user float params (extended semantics only; 0 otherwise)
+  const double* floats;       // [T][nF]
 };
 
 // Spec decode table in a device-friendly form (copied by value into kernels).

@@ -530,6 +530,8 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
   __shared__ uint8_t s_rk[128];          // stable rank of pair b's product
   __shared__ uint64_t s_div[8];          // 64-bit quotients every thread needs (computed once)
   __shared__ uint32_t s_cks[NS];
+  __shared__ M128 s_okm[129];            // pairs of product rank < r that pass x >= 1, c >= 1
+  __shared__ uint8_t s_cnt[129];         // their number
   const int nI = ts.nI, nI2 = nI * nI;
   // CTA tables: built once, from O(nI^2) work per thread at most (the per-CTA
   // prologue is paid by every one of the 4 x 148 CTAs)
@@ -629,14 +631,16 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
   }
   __syncthreads();
   // pairs whose product x*c exceeds t (t >= 0; t >= lut_n: none when lut_n > 0)
-  auto gt_prod = [&](int64_t t) -> M128 {
-    if (lut_n) return s_pgt[t >= lut_n ? nI2 : s_rank[t]];
+  // the rank index of that set (pairs of rank >= it have a product > t)
+  auto gt_rank = [&](int64_t t) -> int {
+    if (lut_n) return t >= lut_n ? nI2 : s_rank[t];
     const int32_t tc = (int32_t)(t > INT32_MAX - 1 ? INT32_MAX - 1 : t);
     int lo = 0;
     for (int step = p2 >> 1; step > 0; step >>= 1)
       if (s_prod[lo + step - 1] <= tc) lo += step;
-    return s_pgt[lo];
+    return lo;
   };
+  auto gt_prod = [&](int64_t t) -> M128 { return s_pgt[gt_rank(t)]; };
   const int qcap = lut_n ? lut_n : INT32_MAX;  // quotients at or above it select no pair
   const bool test_ok0 = ts.test_ok[0] != 0;
   // position-0 verdicts of a plane's nI values of c: one word of plan.cmask at
@@ -647,6 +651,20 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
   for (int q = 2; q < NS; ++q) cks[q] = s_cks[q];
   const M128 all = bit_range(0, nI2);
   const M128 x_lt1 = ~s_gtx[0] & all, c_lt1 = ~s_gtc[0] & all;
+  // rank-count form of a plane's checks when the cube's h-free dispatch bounds
+  // (c <= len(wt)/(k*r*s), x <= len(out)/(k*oh*ow)) hold for every digit value — the
+  // usual case: the in-extent failures are the pairs of rank >= ra, the UB ones those
+  // of rank in [ru, ra), so their counts are differences of s_cnt and the plane's
+  // remaining pairs are the one mask s_okm[min(ra, ru)]
+  for (int r = threadIdx.x; r <= nI2; r += blockDim.x) {
+    const M128 m = all & ~s_pgt[r] & ~(x_lt1 | c_lt1);
+    s_okm[r] = m;
+    s_cnt[r] = (uint8_t)popc(m);
+  }
+  int32_t umax = 0;
+  for (int i = 0; i < nI; ++i) umax = max(umax, s_u[i]);
+  __syncthreads();
+  const unsigned int n_base = (unsigned int)(nI2 - s_cnt[nI2]);  // pairs with x < 1 or c < 1
   const uint32_t magic = (uint32_t)(0xFFFFFFFFull / (uint32_t)nI) + 1u;  // n / nI = umulhi(n, magic), n < 2^27
   unsigned int cnt1 = 0, cnt2 = 0, cnt3 = 0, cnt4 = 0;
   // whole cubes inside [begin, end): mismatches are counted as the remainder
@@ -719,6 +737,44 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
       }
       const uint8_t* ainr = s_ainr + ((uint32_t)p_in * nI + digit[3]) * nI;
       const float* rhw = s_rhw + digit[3] * nI;
+      if (c_max >= umax && d_out >= umax) {  // cube_dm = x < 1 | c < 1: the rank-count form
+        const unsigned int n_ok_all = s_cnt[nI2];
+        for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
+          const int32_t ch = s_u[hd];
+          if (ch < 1) {
+            f2 += (unsigned int)nI2;
+            continue;
+          }
+          int r_ok = ainr[hd];  // pairs of rank >= ra fail the in-extent check
+          const unsigned int c_ok = s_cnt[r_ok];
+          f2 += n_base + (n_ok_all - c_ok);
+          if (!c_ok) continue;
+          const int32_t hw = ch * cw;
+          if (q_rest >= hw) {  // UB: see the general path below
+            const int64_t alim = (int64_t)len_in + hw - q_rest;
+            const uint32_t am1 = (uint32_t)(alim - 1);
+            const int ru = alim <= 0 ? 0 : gt_rank(lut_n ? div_capn(am1, hw, rhw[hd], qcap) : (int)(am1 / (uint32_t)hw));
+            if (ru < r_ok) {
+              f4 += c_ok - s_cnt[ru];
+              r_ok = ru;
+              if (!s_cnt[ru]) continue;
+            }
+          }
+          const uint32_t cw2 = __ldg(plan.cmask + ckey0 + (uint32_t)hd * cks[2]) & sel;
+          const M128 ok = s_okm[r_ok] & ~(dirty_fail | s_rowx[(cw2 | cw2 >> 16) & 0xFFFFu]);
+          if (any(ok)) {
+            const unsigned int k = popc(ok);
+            f_surv += k;
+            const uint64_t p0 = c0b + (uint64_t)hd * nI2;
+            unsigned long long slot = atomicAdd(surv_cnt, (unsigned long long)k);
+            for (uint64_t w = ok.lo; w; w &= w - 1, ++slot)
+              if (slot < surv_cap) surv[slot] = p0 + (uint64_t)(__ffsll((long long)w) - 1) - begin;
+            for (uint64_t w = ok.hi; w; w &= w - 1, ++slot)
+              if (slot < surv_cap) surv[slot] = p0 + 64 + (uint64_t)(__ffsll((long long)w) - 1) - begin;
+          }
+        }
+        continue;
+      }
       for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
         const int32_t ch = s_u[hd];
         if (ch < 1) {

@@ -96,6 +96,7 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
   put(h->o_roff, h->off.data(), TP * 8);
   put(h->o_dof, h->doff.data(), TP * 8);
   put(h->o_isf, h->is_f32.data(), nP * 4);
+  if (h->nF && ts_full) put(h->o_flt, ts_full->float_values, (size_t)T * h->nF * 8);
   for (int t = 0; t < T; ++t) {
     const int32_t ok_t = test_ok ? (test_ok[t] ? 1 : 0) : 1;
     put(h->o_tok + t * 4, &ok_t, 4);
@@ -269,10 +270,16 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_
   cudaSetDevice(ctx->device);
   const int T = ts->n_tests, nI = ts->n_ints, nP = ts->n_ptrs;
   const size_t TP = (size_t)T * nP;
+  if (ts_full && (ts_full->n_floats < 0 || ts_full->n_floats > ATC_MAX_FLOATS ||
+                  (ts_full->n_floats > 0 && !ts_full->float_values))) {
+    atc_set_error(ctx, "malformed test sets (floats)");
+    return ATC_ERR_ARG;
+  }
   auto* h = new atc_testset_handle();
   h->T = T;
   h->nI = nI;
   h->nP = nP;
+  h->nF = ts_full ? ts_full->n_floats : 0;
   h->lens.assign(ts->region_len, ts->region_len + nP);
   h->is_f32.assign(ts->ptr_is_f32, ts->ptr_is_f32 + nP);
   // region pool layout: (t, p) regions back to back, each 32-element aligned
@@ -306,6 +313,7 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_
   h->o_tok = take(T * 4);
   h->o_dcnt = take(TP * 4);
   h->o_dmax = take(TP * 4);
+  h->o_flt = take((size_t)T * h->nF * 8);
   h->meta_bytes = mo;
   auto dmalloc = [&](size_t bytes) -> void* {
     void* p = atc_pool_alloc(ctx, std::max(bytes, (size_t)256));
@@ -336,6 +344,8 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_
   v.dirty_off = (const int64_t*)(h->meta + h->o_dof);
   v.dirty_cnt = (const int32_t*)(h->meta + h->o_dcnt);
   v.dirty_max = (const int32_t*)(h->meta + h->o_dmax);
+  v.nF = h->nF;
+  v.floats = h->nF ? (const double*)(h->meta + h->o_flt) : nullptr;
   h->cs = ctx->copy_next;  // round-robin over the copy streams
   ctx->copy_next = (h->cs + 1) % atc_ctx::kCopyStreams;
   const int rc = testsets_fill(ctx, h, ts_full, sd, sync, false, nullptr, pre);
