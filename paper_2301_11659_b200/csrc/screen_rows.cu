@@ -661,8 +661,10 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
     s_okm[r] = m;
     s_cnt[r] = (uint8_t)popc(m);
   }
-  int32_t umax = 0;
-  for (int i = 0; i < nI; ++i) umax = max(umax, s_u[i]);
+  int32_t umax = 0, umin = INT32_MAX;
+  for (int i = 0; i < nI; ++i) umax = max(umax, s_u[i]), umin = min(umin, s_u[i]);
+  const bool all_pos = umin >= 1;                     // no plane has tc_h < 1
+  const uint32_t rows_all = (1u << nI) - 1u;
   __syncthreads();
   const unsigned int n_base = (unsigned int)(nI2 - s_cnt[nI2]);  // pairs with x < 1 or c < 1
   const uint32_t magic = (uint32_t)(0xFFFFFFFFull / (uint32_t)nI) + 1u;  // n / nI = umulhi(n, magic), n < 2^27
@@ -740,8 +742,10 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
       if (c_max >= umax && d_out >= umax) {  // cube_dm = x < 1 | c < 1: the rank-count form
         const unsigned int n_ok_all = s_cnt[nI2];
         for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
+          // the plane's position-0/1 verdicts over the c rows, loaded first (used last)
+          const uint32_t cw2 = __ldg(plan.cmask + ckey0 + (uint32_t)hd * cks[2]) & sel;
           const int32_t ch = s_u[hd];
-          if (ch < 1) {
+          if (!all_pos && ch < 1) {
             f2 += (unsigned int)nI2;
             continue;
           }
@@ -760,8 +764,9 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
               if (!s_cnt[ru]) continue;
             }
           }
-          const uint32_t cw2 = __ldg(plan.cmask + ckey0 + (uint32_t)hd * cks[2]) & sel;
-          const M128 ok = s_okm[r_ok] & ~(dirty_fail | s_rowx[(cw2 | cw2 >> 16) & 0xFFFFu]);
+          const uint32_t rows_bad = (cw2 | cw2 >> 16) & 0xFFFFu;
+          if (rows_bad == rows_all) continue;  // every c row mismatches at position 0 or 1 (the usual case)
+          const M128 ok = s_okm[r_ok] & ~(dirty_fail | s_rowx[rows_bad]);
           if (any(ok)) {
             const unsigned int k = popc(ok);
             f_surv += k;
