@@ -22,6 +22,10 @@
 //   adapter_check details [per_space]
 //       gpu::p2_detail vs rewriter::verify_rewrite's detail on P2-rejected bindings
 //       of every corpus program x spec (report parity of VerificationFailed).
+//   adapter_check sampler
+//       the profitability sampler on the B200 backend (gpu::sample_timings_b200) over
+//       the reference's training / holdout grids, the reference's train_svm on its
+//       labels, holdout accuracy.
 //   adapter_check routed
 //       make_gpu_routed_dispatch vs rewriter::make_routed_dispatch: the same
 //       cpu/xpu labels on every lifted corpus function (model trained by the
@@ -558,6 +562,34 @@ double max_rel_err(const std::vector<double>& got, const std::vector<double>& re
   return e;
 }
 
+// The profitability sampler on the B200 backend (gpu::sample_timings_b200): the
+// reference's training and holdout grids (profitability.cpp:120-136), every point
+// cross-checked against cpu_gemm and timed; the reference's own train_svm on the
+// B200 labels, its accuracy on the holdout grid.
+int cmd_sampler(atc_ctx* ctx) {
+  auto train = gpu::sample_timings_b200(ctx, profitability::training_grid(), 5);
+  auto hold = gpu::sample_timings_b200(ctx, profitability::holdout_grid(), 5);
+  auto model = profitability::train_svm(train);
+  int right = 0, xpu = 0;
+  json pts = json::array();
+  for (const auto* set : {&train, &hold})
+    for (const auto& t : *set) {
+      pts.push_back({{"sizes", t.sizes}, {"t_cpu_ms", t.t_cpu * 1e3}, {"t_b200_ms", t.t_xpu * 1e3}, {"label", t.label},
+                     {"holdout", set == &hold}});
+      xpu += t.label;
+    }
+  for (const auto& h : hold) right += profitability::predict_backend(model, h.sizes) == h.label;
+  std::cout << json({{"points", pts},
+                     {"train_accuracy", model.train_accuracy},
+                     {"holdout_accuracy", (double)right / (double)hold.size()},
+                     {"xpu_labels", xpu},
+                     {"samples", train.size() + hold.size()},
+                     {"support_vectors", model.support.size()}})
+                   .dump()
+            << std::endl;
+  return 0;
+}
+
 int cmd_routed(atc_ctx* ctx) {
   auto specs = default_specs();
   const auto model = volume_model();
@@ -705,6 +737,7 @@ int main(int argc, char** argv) {
     if (cmd == "dispatch") rc = cmd_dispatch(ctx);
     if (cmd == "details") rc = cmd_details(ctx, argc > 2 ? std::atoi(argv[2]) : 24);
     if (cmd == "routed") rc = cmd_routed(ctx);
+    if (cmd == "sampler") rc = cmd_sampler(ctx);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "adapter_check: %s\n", e.what());
     rc = 1;

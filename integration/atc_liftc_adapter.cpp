@@ -783,4 +783,53 @@ interp::DispatchContext make_gpu_routed_dispatch(const api::ApiSpec& spec, atc_c
   return dc;
 }
 
+profitability::TimingSample sample_one_b200(atc_ctx* ctx, const std::vector<long long>& sizes, int reps,
+                                            int32_t precision, double xpu_overhead_sec) {
+  if (sizes.size() != 3) throw std::invalid_argument("expected sizes m, n, k");  // profitability.cpp:66-69
+  if (reps < 3) throw std::invalid_argument("need at least 3 repetitions");
+  const long long m = sizes[0], n = sizes[1], k = sizes[2];
+  if (m < 1 || n < 1 || k < 1) throw std::invalid_argument("sizes must be positive");
+  std::vector<float> a((size_t)(m * k)), b((size_t)(k * n)), c_cpu((size_t)(m * n)), c_xpu((size_t)(m * n));
+  for (size_t i = 0; i < a.size(); ++i) a[i] = 0.25f + (float)(i % 17) * 0.0625f;  // :73-74
+  for (size_t i = 0; i < b.size(); ++i) b[i] = -0.5f + (float)(i % 23) * 0.0625f;
+  auto xpu = [&](float* out) {
+    if (atc_sgemm_rm(ctx, a.data(), b.data(), out, m, n, k, precision) != ATC_OK)
+      throw profitability::BackendFailure(std::string("B200 backend: ") + atc_last_error(ctx));
+  };
+  profitability::cpu_gemm(a.data(), b.data(), c_cpu.data(), m, n, k);  // verification pass (:76-85)
+  xpu(c_xpu.data());
+  for (size_t i = 0; i < c_cpu.size(); ++i) {
+    if (!std::isfinite(c_cpu[i]) || !std::isfinite(c_xpu[i]))
+      throw profitability::BackendFailure("non-finite backend output");
+    if (std::fabs((double)c_cpu[i] - (double)c_xpu[i]) > 1e-3 * (1.0 + std::fabs((double)c_cpu[i])))
+      throw profitability::BackendFailure("backend results disagree");
+  }
+  auto median_sec = [&](auto&& fn, float* out) {  // :87-99
+    std::vector<double> times;
+    for (int r = 0; r < reps; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      fn(out);
+      times.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
+    std::sort(times.begin(), times.end());
+    return times[times.size() / 2];
+  };
+  profitability::TimingSample s;
+  s.sizes = sizes;
+  s.t_cpu = median_sec([&](float* out) { profitability::cpu_gemm(a.data(), b.data(), out, m, n, k); },
+                       c_cpu.data());
+  s.t_xpu = median_sec(xpu, c_xpu.data()) + xpu_overhead_sec;
+  s.label = s.t_xpu < s.t_cpu ? 1 : 0;
+  return s;
+}
+
+std::vector<profitability::TimingSample> sample_timings_b200(atc_ctx* ctx,
+                                                             const std::vector<std::vector<long long>>& grid,
+                                                             int reps, int32_t precision, double xpu_overhead_sec) {
+  if (grid.empty()) throw std::invalid_argument("empty size grid");
+  std::vector<profitability::TimingSample> out;
+  for (const auto& sizes : grid) out.push_back(sample_one_b200(ctx, sizes, reps, precision, xpu_overhead_sec));
+  return out;
+}
+
 }  // namespace liftc::gpu

@@ -185,4 +185,22 @@ interp::DispatchContext make_gpu_routed_dispatch(const api::ApiSpec& spec, atc_c
 // The predictor features of one call (rewriter.cpp:194-205).
 std::vector<long long> routed_sizes(const api::ApiSpec& spec, const std::map<std::string, long long>& sizes);
 
+// profitability::sample_one (profitability.cpp:65-109) with the accelerator side on
+// the B200 backend the routed dispatch calls: the same inputs (the TF32/BF16-exact
+// patterns of :73-74), the same verification pass against profitability::cpu_gemm
+// (finite, |c_cpu - c_xpu| <= 1e-3 (1 + |c_cpu|), else BackendFailure), then the
+// median of `reps` runs of each side.  t_xpu is atc_sgemm_rm on the host buffers —
+// H2D, tcgen05 GEMM, D2H: everything a routed "xpu" call costs — plus
+// `xpu_overhead_sec` (0 by default: the measured call already includes its launch;
+// the reference charges its CPU stand-in a fixed 2 ms, kXpuLaunchOverheadSec).  The
+// label is 1 iff the B200 call was faster.  Samples feed profitability::train_svm
+// unchanged, so the routed dispatch's model is trained on the backend it dispatches to.
+profitability::TimingSample sample_one_b200(atc_ctx* ctx, const std::vector<long long>& sizes, int reps = 5,
+                                            int32_t precision = ATC_PREC_3XTF32, double xpu_overhead_sec = 0.0);
+// sample_timings (profitability.cpp:111-118): sample_one_b200 over every grid point, in order.
+std::vector<profitability::TimingSample> sample_timings_b200(atc_ctx* ctx,
+                                                             const std::vector<std::vector<long long>>& grid,
+                                                             int reps = 5, int32_t precision = ATC_PREC_3XTF32,
+                                                             double xpu_overhead_sec = 0.0);
+
 }  // namespace liftc::gpu

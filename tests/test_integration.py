@@ -101,3 +101,17 @@ def test_adapter_routed_dispatch():
     assert lines[-1]["mismatches"] == 0
     direct = [x for x in lines if "direct" in x]
     assert len(direct) == 8 and all(x["ok"] for x in direct)
+
+
+def test_adapter_b200_profitability_sampler():
+    """profitability::sample_one / sample_timings (profitability.cpp:65-118) with the
+    accelerator side on the B200 backend the routed dispatch calls (atc_sgemm_rm,
+    host buffers in and out): every grid point passes the reference's cross-check
+    against cpu_gemm, both labels occur, and the reference's own train_svm on these
+    labels predicts the holdout grid (the model the routed "xpu" label comes from is
+    trained on the backend it dispatches to)."""
+    rc, lines, err = _run("sampler")
+    assert rc == 0, err
+    j = lines[-1]
+    assert j["samples"] == 60 and 0 < j["xpu_labels"] < 60
+    assert j["train_accuracy"] >= 0.9 and j["holdout_accuracy"] >= 0.8
