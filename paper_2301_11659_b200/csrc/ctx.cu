@@ -258,6 +258,10 @@ int atc_set_option(atc_ctx* ctx, int32_t option, int32_t value) {
     ctx->opt_conv_screen = value;
     return ATC_OK;
   }
+  if (option == ATC_OPT_SMALL_LOG2 && value >= 0 && value <= 30) {
+    ctx->opt_small_log2 = value;
+    return ATC_OK;
+  }
   if (option == ATC_OPT_CONV_STREAMS && value >= 1 && value <= atc_ctx::kSideStreams) {
     ctx->opt_conv_streams = value;
     return ATC_OK;

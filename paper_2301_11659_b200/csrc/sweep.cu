@@ -55,10 +55,10 @@ constexpr uint64_t kBatchStride = 2 + kBatchPrefix;
 
 size_t batch_res_words(int n) { return (size_t)n * (kBatchStride + 8); }
 
-// Spaces at most this large run in k_sweep_small (the whole space of every corpus
-// gemm program); each gets one CTA per kSmallSlice bindings.
-constexpr uint64_t kSmallMax = 1ull << 20;
+// Gemm spaces of at most 2^ctx->opt_small_log2 bindings run in k_sweep_small; each
+// gets one CTA per kSmallSlice bindings.
 constexpr uint64_t kSmallSlice = 4096;
+constexpr int64_t kSmallMaxInt = 16;
 constexpr int kSmallBudget = 16;  // output positions thread_check looks at (t = 0)
 constexpr uint64_t kSmallSurvCap = 1ull << 20;  // survivors of all small jobs together
 
@@ -241,7 +241,15 @@ atc_enum_batch* batch_create(atc_ctx* ctx, atc_enum_job* jobs, int32_t n_jobs, i
   for (int j = 0; j < n_jobs; ++j) {
     const atc_enum_job& job = jobs[j];
     const uint64_t n = job.end - job.begin;
-    if (!b->batched[j] || n == 0 || n > kSmallMax || b->plans[j].sp.sem != ATC_SEM_GEMM) continue;
+    if (!b->batched[j] || n == 0 || ctx->opt_small_log2 == 0 || n > (1ull << ctx->opt_small_log2) ||
+        b->plans[j].sp.sem != ATC_SEM_GEMM)
+      continue;
+    // a warp per (survivor, test) suits short checks; spaces whose outputs can be
+    // many (m*n up to U^2 for the largest drawn int U: config 1's 64^3) keep the
+    // per-space chain, whose K2 spreads one binding's outputs over more warps
+    int64_t umax = 0;
+    for (int64_t v : job.ts->h_ints) umax = std::max(umax, v);
+    if (umax > kSmallMaxInt) continue;
     b->small[j] = 1;
     b->small_jobs.push_back(j);
     SmallJob sj{};
