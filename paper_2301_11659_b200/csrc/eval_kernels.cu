@@ -561,8 +561,11 @@ __global__ void __launch_bounds__(256) k_screen_enum(TestsetView ts, SpecView sp
 // screen's precondition: size params 0..8 = n, c, h, w, k, r, s, oh, ow; arrays
 // in, weights, out = 0, 1, 2) — the same checks on sizes read straight off the
 // nine digits, without the generic decode.
+// stop (optional, with parts > 1): the binding's shared key — a part stops early once
+// another part has folded a t = 0 failure into it.
 __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const BindingSource& src, uint64_t idx, int t,
-                            int mode, int lane, bool screened = false, int part = 0, int parts = 1) {
+                            int mode, int lane, bool screened = false, int part = 0, int parts = 1,
+                            const int32_t* stop = nullptr) {
   int ptr_of[ATC_MAX_ARRAYS];
   int r = 0;
   Dims d;
@@ -631,6 +634,62 @@ __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const Bin
       bad = __any_sync(0xffffffffu, bad);
       const bool overlap = row ? (ldc < n && m > 1) : (ldc < m && n > 1);
       const int outs = m * n;
+      if (mode == ATC_MODE_FP64 && outs > 32) {
+        // four outputs per lane per step: four independent accumulation chains (each in
+        // the reference's p order), as the conv check does — long m*n*k checks (config 1's
+        // 64^3) are latency bound on one dependent chain per lane
+        constexpr int MO = 4;
+        for (int o0 = 0; o0 < outs && !bad; o0 += 32 * MO) {
+          const double* ap[MO];
+          const double* bp[MO];
+          int pos[MO];
+#pragma unroll
+          for (int q = 0; q < MO; ++q) {
+            const int o = o0 + q * 32 + lane;
+            pos[q] = -1;
+            ap[q] = A;
+            bp[q] = B;
+            if (o < outs) {
+              const int i = o / n, j = o - (o / n) * n;
+              if (!overlap || gemm_last_writer(row, i, j, m, ldc)) {
+                pos[q] = row ? i * ldc + j : j * ldc + i;
+                ap[q] = row ? A + i * lda : A + i;
+                bp[q] = row ? B + j : B + j * ldb;
+              }
+            }
+          }
+          const int sa = row ? 1 : lda, sb = row ? ldb : 1;
+          double acc[MO] = {0.0, 0.0, 0.0, 0.0};
+          // operands of U consecutive p loaded ahead of their (in-order) multiply-adds:
+          // the loads of a block are independent, so their latencies overlap
+          constexpr int U = 8;
+          int p = 0;
+          for (; p + U <= k; p += U) {
+            double av[U][MO], bv[U][MO];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+              for (int q = 0; q < MO; ++q) {
+                av[u][q] = __ldg(ap[q] + (p + u) * sa);
+                bv[u][q] = __ldg(bp[q] + (p + u) * sb);
+              }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+              for (int q = 0; q < MO; ++q) acc[q] = dadd(acc[q], dmul(av[u][q], bv[u][q]));
+          }
+          for (; p < k; ++p) {
+#pragma unroll
+            for (int q = 0; q < MO; ++q) acc[q] = dadd(acc[q], dmul(ap[q][p * sa], bp[q][p * sb]));
+          }
+          bool mm = false;
+#pragma unroll
+          for (int q = 0; q < MO; ++q)
+            if (pos[q] >= 0) mm = mm || mismatch(round_region(acc[q], f32), __ldg(F + pos[q]), f32);
+          bad = __any_sync(0xffffffffu, mm);
+        }
+        return bad ? ATC_FAIL_MISMATCH : 0;
+      }
       for (int o0 = 0; o0 < outs && !bad; o0 += 32) {
         const int o = o0 + lane;
         bool mm = false;
@@ -658,7 +717,13 @@ __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const Bin
       // the reference's order) hide the dependent-add latency of long checks
       constexpr int MO = 4;
       // part / parts: this warp's share of the output steps (the others run in other warps)
+      int steps = 0;
       for (int o0 = part * 32 * MO; o0 < (int)wext && !bad; o0 += parts * 32 * MO) {
+        if (stop && (++steps & 3) == 0) {  // every fourth step: has another part decided it?
+          int k = lane == 0 ? *(volatile const int32_t*)stop : kPassKey;
+          k = __shfl_sync(0xffffffffu, k, 0);
+          if (k < fail_key(1, 0)) break;
+        }
         const double* inp[MO];
         const double* wtp[MO];
         int oo[MO];
@@ -856,7 +921,7 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
       const uint64_t si = pend ? pend[wi] : wi;
       const int32_t k = *(volatile int32_t*)(surv_keys + si);
       if (k != kPassKey && ((k & 7) == ATC_FAIL_MISMATCH || k < fail_key(1, 0))) continue;  // decided
-      const int r = warp_verdict(ts, sp, src, surv[si], 0, mode, lane, screened != 0, part, parts);
+      const int r = warp_verdict(ts, sp, src, surv[si], 0, mode, lane, screened != 0, part, parts, surv_keys + si);
       if (lane == 0 && r) atomicMin(&surv_keys[si], fail_key(0, r));
     }
     return;

@@ -167,7 +167,11 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
   const uint64_t max_surv = std::min<uint64_t>(n, surv_cap);
   // gemm spaces keep few survivors (grid-stride loops cover them): a small cap keeps
   // their mostly-empty K2 grids from taking SM slots from the concurrent conv chain
-  const uint64_t k2_cap = sp.sem == ATC_SEM_GEMM ? 64 : (uint64_t)ctx->sm_count * 8;
+  // (large-output gemm spaces — a drawn int above 16, e.g. config 1's 64^3 — get the
+  // full grid: their checks are long)
+  int64_t umax_all = 0;
+  for (int64_t v : ts->h_ints) umax_all = std::max(umax_all, v);
+  const uint64_t k2_cap = sp.sem == ATC_SEM_GEMM && umax_all <= 16 ? 64 : (uint64_t)ctx->sm_count * 8;
   const unsigned g_t0 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 7) / 8, k2_cap));
   const unsigned g_t1 = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>((max_surv * (uint64_t)std::max(ts->T - 1, 0) + 7) / 8, k2_cap));

@@ -23,12 +23,12 @@
 
 namespace {
 
-// Cost model of one piece of a large (conv) space on one B200 (tools/prof_sweep.py,
-// tools/one_conv_space.py): a fixed part (position tables, K2, finalize) plus the
-// K1 screen per binding.  workloads.py carries the same constants.
+// Cost model of one piece of a large (conv) space on one B200 (tools/rank_breakdown.py,
+// r2 kernels): a fixed part (position tables, K2, finalize) plus the K1 screen per
+// binding.  workloads.py carries the same constants.
 constexpr uint64_t kBigSpace = 1ull << 24;
-constexpr double kSpaceFixedMs = 0.14;
-const double kSpaceMsPerBinding = 0.19 / 2324522934.0;
+constexpr double kSpaceFixedMs = 0.10;
+const double kSpaceMsPerBinding = 0.123 / 2324522934.0;
 
 double space_cost_ms(uint64_t n) { return n > 0 ? kSpaceFixedMs + (double)n * kSpaceMsPerBinding : 0.0; }
 

@@ -57,7 +57,7 @@ size_t batch_res_words(int n) { return (size_t)n * (kBatchStride + 8); }
 
 // Gemm spaces of at most 2^ctx->opt_small_log2 bindings run in k_sweep_small; each
 // gets one CTA per kSmallSlice bindings.
-constexpr uint64_t kSmallSlice = 4096;
+constexpr uint64_t kSmallSlice = 1024;
 constexpr int64_t kSmallMaxInt = 16;
 constexpr int kSmallBudget = 16;  // output positions thread_check looks at (t = 0)
 constexpr uint64_t kSmallSurvCap = 1ull << 20;  // survivors of all small jobs together

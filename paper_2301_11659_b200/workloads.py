@@ -175,10 +175,11 @@ def shard(count: int, rank: int, world: int) -> tuple:
 BIG_SPACE = 1 << 24  # spaces at least this large are split by the cost model below
 
 # Per-space cost model of a large (conv) space on one B200, from the measured chain
-# (tools/prof_sweep.py, tools/one_conv_space.py): a fixed part (position tables, K2,
-# finalize: ~0.14 ms) plus the K1 screen (~0.19 ms per 2.32e9 bindings).
-SPACE_FIXED_MS = 0.14
-SPACE_MS_PER_BINDING = 0.19 / 2324522934
+# (tools/rank_breakdown.py, r2 kernels): a fixed part (position tables, K2, finalize:
+# ~0.10 ms) plus the K1 screen (~0.123 ms per 2.32e9 bindings).  csrc/group.cu carries
+# the same constants (atc_plan_shards).
+SPACE_FIXED_MS = 0.10
+SPACE_MS_PER_BINDING = 0.123 / 2324522934
 
 
 def space_cost_ms(n: int) -> float:

@@ -16,7 +16,7 @@ def timed(items):
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record(stream); sw.run(); e1.record(stream); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
     sw.close(); return sorted(ts)[2]
-for world, rank in ((4, 0), (4, 1), (8, 3)):
+for world, rank in ((8, 0), (8, 3), (8, 7)):
     sh = workloads.plan_shards(jobs, rank, world)
     items = [(j.spec, j.ts, j.space, b, e) for j, (b, e) in zip(jobs, sh) if e > b]
     conv = [it for it in items if it[0].semantics == "conv2d"]
