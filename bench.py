@@ -924,6 +924,23 @@ def _sgemm_bench(ctx, stream, torch, dist=None, world=1):
         ref = (a[:256].double() @ b.double())
         err = ((c[:256].double() - ref).abs() / (1 + ref.abs())).max().item()
         out[prec_name] = {"ms": ms, "tflops": tflops, "max_rel_err_vs_fp64": err}
+    # the cpu_gemm contract end to end: atc_sgemm_rm on pinned host buffers (H2D of A and
+    # B, the tcgen05 GEMM, D2H of C inside the call), wall clock of the call
+    ha, hb = a.cpu().pin_memory(), b.cpu().pin_memory()
+    hc = torch.empty(m, n).pin_memory()
+    host_ms = []
+    for it in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _lib.check(ctx.handle, L.atc_sgemm_rm(ctx.handle, ha.data_ptr(), hb.data_ptr(), hc.data_ptr(), m, n, k,
+                                              _lib.PREC_TF32))
+        if it:
+            host_ms.append((time.perf_counter() - t0) * 1e3)
+    hms = _max_over_ranks(float(np.median(host_ms)), dist, torch)
+    out["e2e_host_buffers"] = {"ms": hms, "tflops": 2.0 * M * n * k / (hms / 1e3) / 1e12, "precision": "tf32",
+                               "h2d_bytes": (m * k + k * n) * 4, "d2h_bytes": m * n * 4,
+                               "call": "atc_sgemm_rm on pinned host A, B, C (wall clock of the call)"}
+    del ha, hb, hc
     _library_tf32(torch)
     cublas_ms = _max_over_ranks(_time_ms(lambda: torch.matmul(a, b, out=c), stream, torch), dist, torch)
     out["cublas_tf32_tflops"] = 2.0 * M * n * k / (cublas_ms / 1e3) / 1e12

@@ -120,18 +120,19 @@ __global__ void k_screen_rows(TestsetView ts, SpecView sp, const uint8_t* perms,
                               unsigned long long* surv_cnt, unsigned long long* reason_hist);
 __global__ void k_confirm_warp(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                                uint64_t surv_cap, int32_t* surv_keys, const uint32_t* sel,
-                               const unsigned long long* sel_cnt, int mode, int screened);
+                               const unsigned long long* sel_cnt, int mode, int screened, int parts);
 __global__ void k_confirm_pre(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                               const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
                               uint32_t* pend, unsigned long long* pend_cnt, int mode, int screened);
 __global__ void k_confirm_t0(TestsetView ts, SpecView sp, BindingSource src, const uint64_t* surv,
                              const unsigned long long* surv_cnt, uint64_t surv_cap, int32_t* surv_keys,
                              const uint32_t* pend, const unsigned long long* pend_cnt, uint32_t* next,
-                             unsigned long long* next_cnt, int mode, int lazy, int screened);
+                             unsigned long long* next_cnt, int mode, int lazy, int screened, int gemm_parts);
 __global__ void k_merge_keys(const uint64_t* surv, const unsigned long long* surv_cnt, uint64_t cap,
                              const int32_t* surv_keys, int32_t* keys);
 __global__ void k_keys_to_verdicts(const int32_t* keys, int64_t n, int8_t* fail_t, int8_t* reason);
 __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v);
+__global__ void k_init_keys(int32_t* keys, const unsigned long long* cnt, uint64_t cap);
 __global__ void k_sweep_small(const SmallJob* jobs, int n_jobs, int budget, int mode, uint2* surv, int32_t* keys,
                               uint64_t surv_cap, unsigned long long* surv_cnt);
 __global__ void k_confirm_small(const SmallJob* jobs, int T, int mode, const uint2* surv, int32_t* keys,

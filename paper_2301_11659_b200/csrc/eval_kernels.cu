@@ -639,7 +639,7 @@ __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const Bin
         // the reference's p order), as the conv check does — long m*n*k checks (config 1's
         // 64^3) are latency bound on one dependent chain per lane
         constexpr int MO = 4;
-        for (int o0 = 0; o0 < outs && !bad; o0 += 32 * MO) {
+        for (int o0 = part * 32 * MO; o0 < outs && !bad; o0 += parts * 32 * MO) {
           const double* ap[MO];
           const double* bp[MO];
           int pos[MO];
@@ -690,6 +690,7 @@ __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const Bin
         }
         return bad ? ATC_FAIL_MISMATCH : 0;
       }
+      if (part > 0) return bad ? ATC_FAIL_MISMATCH : 0;  // short checks: part 0 alone
       for (int o0 = 0; o0 < outs && !bad; o0 += 32) {
         const int o = o0 + lane;
         bool mm = false;
@@ -903,7 +904,8 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
                                                     const uint64_t* surv, const unsigned long long* surv_cnt,
                                                     uint64_t surv_cap, int32_t* surv_keys, const uint32_t* pend,
                                                     const unsigned long long* pend_cnt, uint32_t* next,
-                                                    unsigned long long* next_cnt, int mode, int lazy, int screened) {
+                                                    unsigned long long* next_cnt, int mode, int lazy, int screened,
+                                                    int gemm_parts) {
   const int lane = threadIdx.x & 31;
   unsigned long long cnt = pend ? *pend_cnt : *surv_cnt;
   if (cnt > surv_cap) cnt = surv_cap;
@@ -912,7 +914,9 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
   // the few long full-length checks do not share an SM
   // lazy conv (FP64): the few bindings still needing t = 0 are mostly full-length checks
   // — eight warps share one binding's outputs and fold failures in with atomicMin
-  const int parts = lazy && sp.sem == ATC_SEM_CONV2D && mode == ATC_MODE_FP64 ? 8 : 1;
+  // heavy gemm spaces (gemm_parts > 1; keys initialised, K2b over every survivor): the
+  // same split of one binding's outputs over warps
+  const int parts = lazy && sp.sem == ATC_SEM_CONV2D && mode == ATC_MODE_FP64 ? 8 : gemm_parts > 1 ? gemm_parts : 1;
   if (parts > 1) {
     const uint64_t work = cnt * (uint64_t)parts;
     for (uint64_t w = (uint64_t)(threadIdx.x / 32) * gridDim.x + blockIdx.x; w < work; w += warps) {
@@ -948,27 +952,40 @@ __global__ void __launch_bounds__(256) k_confirm_t0(TestsetView ts, SpecView sp,
 // K2b: one WARP per (t = 0 passer, t >= 1) — many (binding, t) items in flight
 // per SM, each with its own scalar prologue; an item is skipped once a lower t of
 // the same binding has failed (the atomicMin result is unchanged by the skip).
+// sel == nullptr: every survivor (keys initialised by k_init_keys, t = 0 failures
+// already folded in by K2a); parts > 1: a (binding, t) item's outputs split over
+// `parts` warps (long gemm checks), failures folded with atomicMin.
 __global__ void __launch_bounds__(256) k_confirm_warp(TestsetView ts, SpecView sp, BindingSource src,
                                                       const uint64_t* surv, uint64_t surv_cap, int32_t* surv_keys,
                                                       const uint32_t* sel, const unsigned long long* sel_cnt,
-                                                      int mode, int screened) {
+                                                      int mode, int screened, int parts) {
   const int lane = threadIdx.x & 31;
   unsigned long long cnt = *sel_cnt;
   if (cnt > surv_cap) cnt = surv_cap;
   const int nt = ts.T - 1;
-  if (nt <= 0) return;
-  const uint64_t work = cnt * (uint64_t)nt;
+  if (nt <= 0 || cnt == 0) return;
+  const uint64_t work = cnt * (uint64_t)nt * (uint64_t)parts;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
   // t-major: every binding's t = 1 item is dispatched before any t = 2 item, so the
   // later items of bindings that fail early are mostly skipped
   for (uint64_t w = (uint64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; w < work; w += warps) {
-    const uint64_t tt = w / cnt;
-    const uint32_t si = sel[w - tt * cnt];
+    const uint64_t item = w / (uint64_t)parts;
+    const int part = (int)(w - item * (uint64_t)parts);
+    const uint64_t tt = item / cnt;
+    const uint32_t si = sel ? sel[item - tt * cnt] : (uint32_t)(item - tt * cnt);
     const int t = 1 + (int)tt;
     if (*(volatile int32_t*)(surv_keys + si) < fail_key(t, 0)) continue;  // failed at a lower t already
-    const int r = warp_verdict(ts, sp, src, surv[si], t, mode, lane, screened != 0);
+    const int r = warp_verdict(ts, sp, src, surv[si], t, mode, lane, screened != 0, part, parts);
     if (lane == 0 && r) atomicMin(&surv_keys[si], fail_key(t, r));
   }
+}
+
+// kPassKey for every survivor K1 queued (the count is on the device).
+__global__ void k_init_keys(int32_t* keys, const unsigned long long* cnt, uint64_t cap) {
+  unsigned long long n = *cnt;
+  if (n > cap) n = cap;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    keys[i] = kPassKey;
 }
 
 // Merge K2 results into the per-binding keys of an explicit list.

@@ -185,15 +185,30 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
     // enumerated ranges report reasons, not failing tests: t >= 1 first over every
     // pending survivor, then t = 0 only where it can change the reason (k_confirm_t0)
     k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, pend, next_cnt + 1,
-                                         ctx->mode, screened);
+                                         ctx->mode, screened, 1);
     const unsigned g_lazy = (unsigned)std::min<uint64_t>((uint64_t)g_t0 * 8, k2_cap);  // 8 warps per binding
     k_confirm_t0<<<g_lazy, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pend, next_cnt + 1,
-                                         next, next_cnt, ctx->mode, 1, screened);
+                                         next, next_cnt, ctx->mode, 1, screened, 1);
+  } else if (sp.sem == ATC_SEM_GEMM && umax_all > 16 && ctx->mode == ATC_MODE_FP64) {
+    // long gemm checks (config 1's 64^3: 4,096 outputs of 64 terms per (binding, t)):
+    // each binding's outputs split over kGemmParts warps in K2a and K2b, failures
+    // folded with atomicMin into keys initialised to kPassKey; K2b walks every
+    // survivor (those failing t = 0 are skipped by their key)
+    constexpr int kGemmParts = 8;
+    const unsigned g_t0p = (unsigned)std::min<uint64_t>((uint64_t)g_t0 * kGemmParts, k2_cap);
+    const unsigned g_t1p = (unsigned)std::min<uint64_t>((uint64_t)g_t1 * kGemmParts, k2_cap);
+    k_init_keys<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 255) / 256, 1024)), 256, 0, st>>>(
+        surv_keys, surv_cnt, surv_cap);
+    k_confirm_t0<<<g_t0p, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, nullptr, next_cnt + 1,
+                                        next, next_cnt, ctx->mode, 1, screened, kGemmParts);
+    k_confirm_warp<<<g_t1p, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, nullptr, surv_cnt, ctx->mode,
+                                          screened, kGemmParts);
+    if (ctx->prof) ctx->prof_kernels += 1;
   } else {
     k_confirm_t0<<<g_t0, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys,
-                                       pre ? pend : nullptr, next_cnt + 1, next, next_cnt, ctx->mode, 0, screened);
+                                       pre ? pend : nullptr, next_cnt + 1, next, next_cnt, ctx->mode, 0, screened, 1);
     k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, next, next_cnt, ctx->mode,
-                                         screened);
+                                         screened, 1);
   }
   if (ctx->prof) {
     cudaEventRecord(e2.second, st);
