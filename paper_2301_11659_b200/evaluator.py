@@ -21,7 +21,7 @@ from typing import Callable, Optional
 import numpy as np
 
 from . import _lib
-from .probe import PROBE_REGION_LEN, Param, SizeRules, p2_test_inputs
+from .probe import PROBE_REGION_LEN, SizeRules, p2_test_inputs
 from .spec import ApiSpec
 
 
@@ -466,5 +466,3 @@ def verify_rewrite_batch(function: str, bindings: list, spec: ApiSpec, ts: Recor
             out.append(VerifyResult(False, t, f"access outside a region at test {t}"))
     return out
 
-
-_ = Param  # re-exported for callers building RecordedTestsets by hand

@@ -41,6 +41,7 @@ class LiftOutcome:
     binding: Optional[dict] = None
     p1_calls: int = 0  # host P1 evaluations the GPU screen left to do
     evaluated: list = field(default_factory=list)  # (api, rank, verdict) of candidates decided before the winner
+    status_detail: str = ""  # pipeline.cpp:314-325
 
 
 def lift_function(specs: list, testsets: RecordedTestsets, user_ptrs: list, p1: Callable[[ApiSpec, dict], str],
@@ -79,8 +80,8 @@ def lift_function(specs: list, testsets: RecordedTestsets, user_ptrs: list, p1: 
         if too_many:
             break
     if too_many:
-        out.status = "TooManyCandidates"
-    else:
+        out.status, out.status_detail = "TooManyCandidates", "candidate cap exceeded"
+    else:  # pipeline.cpp:318-324
         out.status = "NoMatch"
-    _ = any_filtered
+        out.status_detail = "no candidate proved equivalent" if any_filtered else "no candidate passed the constraints"
     return out

@@ -11,7 +11,6 @@ std::mt19937_64 — fully specified by the C++ standard.
 """
 from __future__ import annotations
 
-import ctypes as C
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -228,5 +227,3 @@ def fnv1a_bytes(a: np.ndarray) -> int:
             h = (h ^ np.uint64(x)) * prime
     return int(h)
 
-
-_ = C  # ctypes imported for callers that build raw buffers
