@@ -644,14 +644,23 @@ CandidateLoop candidate_loop(atc_ctx* ctx, const minilang::Program& prog, const 
     }
   RecordedTests rec;
   std::vector<SpecVerdicts> p2;
-  if (!eval_specs.empty()) {
+  size_t total = 0;
+  for (const auto* l : lists) total += l->size();
+  // P2 for every spec's list in one GPU batch: up front for long lists (P1 then runs
+  // only on P2 survivors), on demand for short ones — there the reference's order (P1
+  // first, P2 when P1 says Equivalent, pipeline.cpp:257-277) costs less, since a P1
+  // rejection on the host VM is cheaper than recording the test sets
+  const bool lazy = total <= cfg.lazy_p2_max;
+  auto ensure_p2 = [&] {
+    if (!p2.empty() || eval_specs.empty()) return;
     auto t0 = std::chrono::steady_clock::now();
     rec = record_tests(prog, function, rules, Rng::mix(fseed, "post"), cfg.verify_tests);  // pipeline.cpp:277
     out.record_ms = ms_since(t0);
     t0 = std::chrono::steady_clock::now();
     p2 = p2_verdicts(ctx, rec, eval_specs, lists);
     out.gpu_ms = ms_since(t0);
-  }
+  };
+  if (!lazy) ensure_p2();
   // pipeline.cpp:241-309 (P1 = check_equivalence on the host VM, host_phases.hpp)
   const HostVm vm(prog);
   bool too_many = false;
@@ -670,8 +679,7 @@ CandidateLoop candidate_loop(atc_ctx* ctx, const minilang::Program& prog, const 
         break;
       }
       const auto& cand = list[i];
-      const bool p2_ok = p2[slot[s]].reason[i] == ATC_PASS;
-      if (!p2_ok && !cfg.report) continue;  // P1 cannot make it the winner
+      if (!lazy && p2[slot[s]].reason[i] != ATC_PASS && !cfg.report) continue;  // P1 cannot make it the winner
       const auto t0 = std::chrono::steady_clock::now();
       equivalence::EquivalenceConfig ec;
       ec.tests = cfg.tests;
@@ -686,6 +694,8 @@ CandidateLoop candidate_loop(atc_ctx* ctx, const minilang::Program& prog, const 
       co.detail = er.detail;
       co.equiv_ms = ms_since(t0);
       if (er.verdict == equivalence::Verdict::Equivalent) {
+        ensure_p2();
+        const bool p2_ok = p2[slot[s]].reason[i] == ATC_PASS;
         try {
           out.rewrite = rewriter::rewrite(prog, function, cand, *specs[s]);
         } catch (const std::exception& e) {

@@ -147,6 +147,9 @@ struct LoopConfig {
   size_t max_candidates = 100;
   double budget_sec = 600.0;
   bool report = true;
+  // at most this many ranked candidates over all specs: P2 on demand, after P1 said
+  // Equivalent (the reference's order); more: one GPU P2 batch up front
+  size_t lazy_p2_max = 4;
 };
 struct CandidateLoop {
   pipeline::FunctionStatus status = pipeline::FunctionStatus::NoMatch;

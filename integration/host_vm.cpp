@@ -265,18 +265,35 @@ struct Fault {
   std::string msg;
 };
 
-struct Val {  // interp.cpp:20-29 (floats carry i == 0)
-  bool is_int = true;
-  long long i = 0;
-  double f = 0.0;
-  static Val I(long long v) { return Val{true, v, 0.0}; }
-  static Val F(double v) { return Val{false, 0, v}; }
+// interp.cpp:20-29.  16 bytes (returned in registers): the int and float payloads
+// share storage, so iv() / fv() give the reference's view of the other field — a float
+// Value reads as int 0 (make_float leaves i == 0), an int Value as float 0.0.
+struct Val {
+  union {
+    long long i;
+    double f;
+  };
+  bool is_int;
+  static Val I(long long v) {
+    Val r;
+    r.i = v;
+    r.is_int = true;
+    return r;
+  }
+  static Val F(double v) {
+    Val r;
+    r.f = v;
+    r.is_int = false;
+    return r;
+  }
+  long long iv() const { return is_int ? i : 0; }
+  double fv() const { return is_int ? 0.0 : f; }
   double d() const { return is_int ? (double)i : f; }
   bool truthy() const { return is_int ? i != 0 : f != 0.0; }
 };
 
 struct Slot {  // interp.cpp:31-39
-  Val v;
+  Val v = Val::I(0);
   bool round_f32 = false;
   int region = -1;
   double lanes[8] = {};
@@ -416,7 +433,7 @@ struct Run {
       case EK::Var:
         return S(e.slot).v;
       case EK::Index: {  // interp.cpp:416-419
-        const long long off = eval(F, e.a0).i;
+        const long long off = eval(F, e.a0).iv();
         return Val::F(load(S(e.slot).region, off));
       }
       case EK::Not:
@@ -455,8 +472,8 @@ struct Run {
       }
       case EK::Mod: {
         const Val a = eval(F, e.a0), b = eval(F, e.a1);
-        if (b.i == 0) throw Fault{ExecStatus::RuntimeFault, "integer modulo by zero"};
-        return Val::I(a.i % b.i);
+        if (b.iv() == 0) throw Fault{ExecStatus::RuntimeFault, "integer modulo by zero"};
+        return Val::I(a.iv() % b.iv());
       }
       case EK::Lt: {
         const Val a = eval(F, e.a0), b = eval(F, e.a1);
@@ -484,8 +501,8 @@ struct Run {
       }
       case EK::Min:
       case EK::Max: {  // interp.cpp:483-488
-        const long long a = eval(F, e.a0).i;
-        const long long b = eval(F, e.a1).i;
+        const long long a = eval(F, e.a0).iv();
+        const long long b = eval(F, e.a1).iv();
         const bool lt = a < b;
         return Val::I(e.k == EK::Min ? (lt ? a : b) : (lt ? b : a));
       }
@@ -551,21 +568,20 @@ struct Run {
     step();
     switch (s.k) {
       case SK::Let: {  // interp.cpp:290-321
-        Slot slot;
-        switch (s.lt) {
-          case LocalType::I64: slot.v = Val::I(0); break;
-          case LocalType::F32: slot.round_f32 = true; slot.v = Val::F(0.0); break;
-          case LocalType::F64: slot.v = Val::F(0.0); break;
-          default: break;  // Vec4/Vec8: zero lanes
+        if (s.lt == LocalType::Vec4 || s.lt == LocalType::Vec8) {  // zero lanes
+          Slot& d = S(s.slot);
+          d = Slot{};
+          return Flow::Next;
         }
+        const bool r32 = s.lt == LocalType::F32;
+        Val v = s.lt == LocalType::I64 ? Val::I(0) : Val::F(0.0);
         if (s.e0 >= 0) {
-          const Val v = eval(F, s.e0);
-          if (s.lt == LocalType::I64)
-            slot.v = v;
-          else
-            slot.v = Val::F(slot.round_f32 ? (double)(float)v.d() : v.d());
+          const Val x = eval(F, s.e0);
+          v = s.lt == LocalType::I64 ? x : Val::F(r32 ? (double)(float)x.d() : x.d());
         }
-        S(s.slot) = slot;
+        Slot& d = S(s.slot);
+        d.v = v;
+        d.round_f32 = r32;
         return Flow::Next;
       }
       case SK::Assign: {  // interp.cpp:323-331
@@ -578,20 +594,20 @@ struct Run {
         return Flow::Next;
       }
       case SK::Store: {  // interp.cpp:333-337
-        const long long off = eval(F, s.e0).i;
+        const long long off = eval(F, s.e0).iv();
         const Val v = eval(F, s.e1);
         store(S(s.ptr).region, off, v.d());
         return Flow::Next;
       }
       case SK::For: {  // interp.cpp:339-353
-        const long long lo = eval(F, s.e0).i;
-        const long long hi = eval(F, s.e1).i;
-        const long long st = s.e2 >= 0 ? eval(F, s.e2).i : 1;
+        const long long lo = eval(F, s.e0).iv();
+        const long long hi = eval(F, s.e1).iv();
+        const long long st = s.e2 >= 0 ? eval(F, s.e2).iv() : 1;
         if (st <= 0) throw Fault{ExecStatus::RuntimeFault, "loop step must be positive"};
         for (long long iv = lo; iv < hi; iv += st) {
-          Slot& lv = S(s.slot);
-          lv = Slot{};
+          Slot& lv = S(s.slot);  // a fresh int scalar every iteration (interp.cpp:344-347)
           lv.v = Val::I(iv);
+          lv.round_f32 = false;
           if (exec_list(F, s.body) == Flow::Ret) return Flow::Ret;
         }
         return Flow::Next;
@@ -615,7 +631,7 @@ struct Run {
         }
         return Flow::Ret;
       case SK::VLoad: {  // interp.cpp:385-391
-        const long long b = eval(F, s.e0).i;
+        const long long b = eval(F, s.e0).iv();
         const int r = S(s.ptr).region;
         for (int l = 0; l < s.width; ++l) {
           const double x = load(r, b + l);
@@ -624,7 +640,7 @@ struct Run {
         return Flow::Next;
       }
       case SK::VStore: {
-        const long long b = eval(F, s.e0).i;
+        const long long b = eval(F, s.e0).iv();
         const int r = S(s.ptr).region;
         for (int l = 0; l < s.width; ++l) store(r, b + l, S(s.va).lanes[l]);
         return Flow::Next;
@@ -750,8 +766,8 @@ interp::ExecutionOutcome HostVm::execute(const std::string& function, const inte
     out.has_ret = has;
     if (has) {
       out.ret_is_int = rv.is_int;
-      out.ret_int = rv.i;
-      out.ret_float = rv.f;
+      out.ret_int = rv.iv();
+      out.ret_float = rv.fv();
     }
     out.final = std::move(mem);
     out.writes = std::move(writes);
