@@ -23,8 +23,15 @@ enum class EK : uint8_t {
   Add, Sub, Mul, Div, Mod, Lt, Le, Gt, Ge, Eq, Ne
 };
 
+// Static type of an expression: the resolver (minilang.cpp:680-1000) types every
+// variable and operator, so an expression without calls is int or float for certain;
+// a call's value is dynamic (a float function that falls off its end yields int 0,
+// interp.cpp:521) and takes the generic, tagged path.
+enum : int8_t { TY_INT = 0, TY_FLT = 1, TY_DYN = 2 };
+
 struct CExpr {
   EK k = EK::IntLit;
+  int8_t ty = TY_DYN;
   int slot = -1;            // Var / Index (pointer slot)
   int a0 = -1, a1 = -1;     // children (unary: a0; binary: a0, a1)
   int fn = -1;              // Call: callee index
@@ -51,6 +58,7 @@ struct CStmt {
 struct CFunc {
   const FunctionIR* ir = nullptr;
   int n_slots = 0;
+  std::vector<int8_t> slot_ty;  // TY_INT / TY_FLT, TY_DYN for pointers and vectors
   std::vector<CExpr> ex;
   std::vector<int> args;
   std::vector<CStmt> st;
@@ -72,10 +80,14 @@ struct Compiler {
   CFunc& F;
   std::vector<std::map<std::string, int>> scopes;
 
-  int declare(const std::string& name) {
+  int declare(const std::string& name, int8_t ty = TY_DYN) {
     const int s = F.n_slots++;
     scopes.back()[name] = s;
+    F.slot_ty.push_back(ty);
     return s;
+  }
+  static int8_t arith(int8_t a, int8_t b) {
+    return a == TY_DYN || b == TY_DYN ? TY_DYN : a == TY_INT && b == TY_INT ? TY_INT : TY_FLT;
   }
   int lookup(const std::string& name) {
     for (auto it = scopes.rbegin(); it != scopes.rend(); ++it) {
@@ -157,8 +169,27 @@ struct Compiler {
         break;
       }
     }
+    c.ty = type_of(c);
     F.ex.push_back(std::move(c));
     return (int)F.ex.size() - 1;
+  }
+
+  int8_t type_of(const CExpr& c) const {
+    auto ty = [&](int i) { return i >= 0 ? F.ex[i].ty : TY_DYN; };
+    switch (c.k) {
+      case EK::IntLit: return TY_INT;
+      case EK::FloatLit: return TY_FLT;
+      case EK::Var: return F.slot_ty[c.slot];
+      case EK::Index: return TY_FLT;
+      case EK::Neg: return ty(c.a0);
+      case EK::Not: case EK::And: case EK::Or: case EK::Lt: case EK::Le: case EK::Gt: case EK::Ge: case EK::Eq:
+      case EK::Ne: case EK::Dispatch: case EK::ToI64: return TY_INT;
+      case EK::Add: case EK::Sub: case EK::Mul: case EK::Div: return arith(ty(c.a0), ty(c.a1));
+      case EK::Mod: case EK::Min: case EK::Max: return ty(c.a0) == TY_INT && ty(c.a1) == TY_INT ? TY_INT : TY_DYN;
+      case EK::ToF64: case EK::Fabs: case EK::Sqrt: return TY_FLT;
+      case EK::Call: return TY_DYN;
+    }
+    return TY_DYN;
   }
 
   std::vector<int> block(const std::vector<StmtPtr>& body, bool new_scope) {
@@ -176,7 +207,9 @@ struct Compiler {
         c.k = SK::Let;
         c.lt = s.let_type;
         c.e0 = s.let_init ? expr(*s.let_init) : -1;  // evaluated before the declaration
-        c.slot = declare(s.let_name);
+        c.slot = declare(s.let_name, s.let_type == LocalType::I64   ? TY_INT
+                                     : s.let_type == LocalType::F32 || s.let_type == LocalType::F64 ? TY_FLT
+                                                                                                     : TY_DYN);
         break;
       case Stmt::Kind::Assign:
         c.k = SK::Assign;
@@ -195,7 +228,7 @@ struct Compiler {
         c.e1 = expr(*s.hi);
         c.e2 = s.step ? expr(*s.step) : -1;
         scopes.emplace_back();  // the iteration scope: loop var + body (interp.cpp:304-311)
-        c.slot = declare(s.loop_var);
+        c.slot = declare(s.loop_var, TY_INT);
         c.body = block(s.body, false);
         scopes.pop_back();
         break;
@@ -422,6 +455,161 @@ struct Run {
     return r;
   }
 
+  // ------------------------------------------------ typed expressions --
+  // Statically int / float subtrees (CExpr::ty) evaluate without tags: the same
+  // operations in the same order as eval(), on plain int64 / double.
+  long long ival(const CFunc& F, int ei) {  // eval(F, ei).iv()
+    return F.ex[ei].ty == TY_INT ? ileaf(F, ei) : eval(F, ei).iv();
+  }
+  double dval(const CFunc& F, int ei) {  // eval(F, ei).d()
+    const CExpr& e = F.ex[ei];
+    if (e.k == EK::Var && e.ty != TY_DYN) {
+      const Val& v = S(e.slot).v;
+      return e.ty == TY_INT ? (double)v.i : v.f;
+    }
+    return e.ty == TY_INT ? (double)ieval(F, ei) : e.ty == TY_FLT ? feval(F, ei) : eval(F, ei).d();
+  }
+  bool truth(const CFunc& F, int ei) {  // eval(F, ei).truthy()
+    const int8_t t = F.ex[ei].ty;
+    return t == TY_INT ? ieval(F, ei) != 0 : t == TY_FLT ? feval(F, ei) != 0.0 : eval(F, ei).truthy();
+  }
+  // a comparison: int compare when both sides are ints, else on doubles (interp.cpp:446)
+  template <class Op>
+  long long cmp(const CFunc& F, const CExpr& e, Op op) {
+    const int8_t ta = F.ex[e.a0].ty, tb = F.ex[e.a1].ty;
+    if (ta == TY_INT && tb == TY_INT) {
+      const long long a = ieval(F, e.a0);
+      const long long b = ieval(F, e.a1);
+      return op(a, b) ? 1 : 0;
+    }
+    if (ta != TY_DYN && tb != TY_DYN) {  // at least one float: doubles
+      const double a = dval(F, e.a0);
+      const double b = dval(F, e.a1);
+      return op(a, b) ? 1 : 0;
+    }
+    const Val a = eval(F, e.a0), b = eval(F, e.a1);
+    return (a.is_int && b.is_int ? op(a.i, b.i) : op(a.d(), b.d())) ? 1 : 0;
+  }
+
+  // leaves read in place (no call): most operands of index arithmetic are variables
+  // and literals
+  long long ileaf(const CFunc& F, int ei) {
+    const CExpr& e = F.ex[ei];
+    if (e.k == EK::Var) return S(e.slot).v.i;
+    if (e.k == EK::IntLit) return e.i;
+    return ieval(F, ei);
+  }
+
+  long long ieval(const CFunc& F, int ei) {  // CExpr::ty == TY_INT
+    const CExpr& e = F.ex[ei];
+    switch (e.k) {
+      case EK::IntLit:
+        return e.i;
+      case EK::Var:
+        return S(e.slot).v.i;
+      case EK::Add: {
+        const long long a = ileaf(F, e.a0);
+        return a + ileaf(F, e.a1);
+      }
+      case EK::Sub: {
+        const long long a = ileaf(F, e.a0);
+        return a - ileaf(F, e.a1);
+      }
+      case EK::Mul: {
+        const long long a = ileaf(F, e.a0);
+        return a * ileaf(F, e.a1);
+      }
+      case EK::Div: {
+        const long long a = ieval(F, e.a0);
+        const long long b = ieval(F, e.a1);
+        if (b == 0) throw Fault{ExecStatus::RuntimeFault, "integer division by zero"};
+        return a / b;
+      }
+      case EK::Mod: {
+        const long long a = ieval(F, e.a0);
+        const long long b = ieval(F, e.a1);
+        if (b == 0) throw Fault{ExecStatus::RuntimeFault, "integer modulo by zero"};
+        return a % b;
+      }
+      case EK::Lt: return cmp(F, e, [](auto a, auto b) { return a < b; });
+      case EK::Le: return cmp(F, e, [](auto a, auto b) { return a <= b; });
+      case EK::Gt: return cmp(F, e, [](auto a, auto b) { return a > b; });
+      case EK::Ge: return cmp(F, e, [](auto a, auto b) { return a >= b; });
+      case EK::Eq: return cmp(F, e, [](auto a, auto b) { return a == b; });
+      case EK::Ne: return cmp(F, e, [](auto a, auto b) { return a != b; });
+      case EK::Not:
+        return truth(F, e.a0) ? 0 : 1;
+      case EK::And:
+        if (!truth(F, e.a0)) return 0;
+        return truth(F, e.a1) ? 1 : 0;
+      case EK::Or:
+        if (truth(F, e.a0)) return 1;
+        return truth(F, e.a1) ? 1 : 0;
+      case EK::Neg:
+        return -ieval(F, e.a0);
+      case EK::Min:
+      case EK::Max: {
+        const long long a = ieval(F, e.a0);
+        const long long b = ieval(F, e.a1);
+        const bool lt = a < b;
+        return e.k == EK::Min ? (lt ? a : b) : (lt ? b : a);
+      }
+      case EK::ToI64: {
+        const int8_t t = F.ex[e.a0].ty;
+        if (t == TY_INT) return ieval(F, e.a0);
+        if (t == TY_FLT) return (long long)feval(F, e.a0);
+        return eval(F, ei).iv();
+      }
+      default:
+        return eval(F, ei).iv();
+    }
+  }
+
+  double feval(const CFunc& F, int ei) {  // CExpr::ty == TY_FLT
+    const CExpr& e = F.ex[ei];
+    switch (e.k) {
+      case EK::FloatLit:
+        return e.f;
+      case EK::Var:
+        return S(e.slot).v.f;
+      case EK::Index: {  // interp.cpp:416-419
+        const long long off = ival(F, e.a0);
+        return load(S(e.slot).region, off);
+      }
+      case EK::Add: {
+        const double a = dval(F, e.a0);
+        return a + dval(F, e.a1);
+      }
+      case EK::Sub: {
+        const double a = dval(F, e.a0);
+        return a - dval(F, e.a1);
+      }
+      case EK::Mul: {
+        const double a = dval(F, e.a0);
+        return a * dval(F, e.a1);
+      }
+      case EK::Div: {
+        const double a = dval(F, e.a0);
+        const double b = dval(F, e.a1);
+        if (b == 0.0) throw Fault{ExecStatus::RuntimeFault, "float division by zero"};
+        return a / b;
+      }
+      case EK::Neg:
+        return -feval(F, e.a0);
+      case EK::ToF64:
+        return dval(F, e.a0);
+      case EK::Fabs:
+        return std::fabs(dval(F, e.a0));
+      case EK::Sqrt: {
+        const double v = dval(F, e.a0);
+        if (v < 0.0) throw Fault{ExecStatus::RuntimeFault, "sqrt of a negative value"};
+        return std::sqrt(v);
+      }
+      default:
+        return eval(F, ei).d();
+    }
+  }
+
   // ----------------------------------------------------- expressions --
   Val eval(const CFunc& F, int ei) {
     const CExpr& e = F.ex[ei];
@@ -576,8 +764,12 @@ struct Run {
         const bool r32 = s.lt == LocalType::F32;
         Val v = s.lt == LocalType::I64 ? Val::I(0) : Val::F(0.0);
         if (s.e0 >= 0) {
-          const Val x = eval(F, s.e0);
-          v = s.lt == LocalType::I64 ? x : Val::F(r32 ? (double)(float)x.d() : x.d());
+          if (s.lt == LocalType::I64) {
+            v = F.ex[s.e0].ty == TY_INT ? Val::I(ieval(F, s.e0)) : eval(F, s.e0);
+          } else {
+            const double x = dval(F, s.e0);
+            v = Val::F(r32 ? (double)(float)x : x);
+          }
         }
         Slot& d = S(s.slot);
         d.v = v;
@@ -585,6 +777,18 @@ struct Run {
         return Flow::Next;
       }
       case SK::Assign: {  // interp.cpp:323-331
+        const int8_t t = F.ex[s.e0].ty;
+        if (F.slot_ty[s.slot] == TY_FLT && t != TY_DYN) {  // a float variable: the value as a double
+          const double x = dval(F, s.e0);
+          Slot& slot = S(s.slot);
+          slot.v = Val::F(slot.round_f32 ? (double)(float)x : x);
+          return Flow::Next;
+        }
+        if (F.slot_ty[s.slot] == TY_INT && t == TY_INT) {
+          const long long x = ieval(F, s.e0);
+          S(s.slot).v = Val::I(x);
+          return Flow::Next;
+        }
         const Val v = eval(F, s.e0);
         Slot& slot = S(s.slot);
         if (slot.v.is_int)
@@ -594,15 +798,15 @@ struct Run {
         return Flow::Next;
       }
       case SK::Store: {  // interp.cpp:333-337
-        const long long off = eval(F, s.e0).iv();
-        const Val v = eval(F, s.e1);
-        store(S(s.ptr).region, off, v.d());
+        const long long off = ival(F, s.e0);
+        const double v = dval(F, s.e1);
+        store(S(s.ptr).region, off, v);
         return Flow::Next;
       }
       case SK::For: {  // interp.cpp:339-353
-        const long long lo = eval(F, s.e0).iv();
-        const long long hi = eval(F, s.e1).iv();
-        const long long st = s.e2 >= 0 ? eval(F, s.e2).iv() : 1;
+        const long long lo = ival(F, s.e0);
+        const long long hi = ival(F, s.e1);
+        const long long st = s.e2 >= 0 ? ival(F, s.e2) : 1;
         if (st <= 0) throw Fault{ExecStatus::RuntimeFault, "loop step must be positive"};
         for (long long iv = lo; iv < hi; iv += st) {
           Slot& lv = S(s.slot);  // a fresh int scalar every iteration (interp.cpp:344-347)
@@ -613,13 +817,13 @@ struct Run {
         return Flow::Next;
       }
       case SK::While:  // interp.cpp:354-359
-        while (eval(F, s.e0).truthy()) {
+        while (truth(F, s.e0)) {
           step();
           if (exec_list(F, s.body) == Flow::Ret) return Flow::Ret;
         }
         return Flow::Next;
       case SK::If:
-        return exec_list(F, eval(F, s.e0).truthy() ? s.body : s.els);
+        return exec_list(F, truth(F, s.e0) ? s.body : s.els);
       case SK::Call:
         eval(F, s.e0);
         return Flow::Next;
@@ -631,7 +835,7 @@ struct Run {
         }
         return Flow::Ret;
       case SK::VLoad: {  // interp.cpp:385-391
-        const long long b = eval(F, s.e0).iv();
+        const long long b = ival(F, s.e0);
         const int r = S(s.ptr).region;
         for (int l = 0; l < s.width; ++l) {
           const double x = load(r, b + l);
@@ -640,13 +844,13 @@ struct Run {
         return Flow::Next;
       }
       case SK::VStore: {
-        const long long b = eval(F, s.e0).iv();
+        const long long b = ival(F, s.e0);
         const int r = S(s.ptr).region;
         for (int l = 0; l < s.width; ++l) store(r, b + l, S(s.va).lanes[l]);
         return Flow::Next;
       }
       case SK::VSplat: {
-        const double v = eval(F, s.e0).d();
+        const double v = dval(F, s.e0);
         for (int l = 0; l < s.width; ++l) S(s.slot).lanes[l] = v;
         return Flow::Next;
       }
@@ -723,7 +927,8 @@ HostVm::HostVm(const Program& prog) : prog_(std::make_unique<VmProgram>()) {
   for (auto& F : P.fns) {
     Compiler c{P, F, {}};
     c.scopes.emplace_back();
-    for (const auto& p : F.ir->params) c.declare(p.name);
+    for (const auto& p : F.ir->params)
+      c.declare(p.name, p.kind == ParamKind::IntScalar ? TY_INT : p.kind == ParamKind::FloatScalar ? TY_FLT : TY_DYN);
     F.body = c.block(F.ir->body, true);
   }
 }
