@@ -83,32 +83,46 @@ __global__ void __launch_bounds__(160) k_probe_regions(int T, int nP, const uint
   }
   __syncthreads();
   auto wrap = [](int i) { return i >= kRing ? i - kRing : i; };  // i < 2 * kRing
-  int r = 0;  // base % kRing
-  for (uint64_t base = 0; base < end; base += kM, r = wrap(r + kM)) {  // step: draws [base, base + 156)
-    uint64_t w = 0;
-    if (q < kM) {
-      const int n = r + q;  // z[n + 312] from z[n], z[n + 1], z[n + 156] (ring slots)
-      const uint64_t y = (z[wrap(n)] & kUpper) | (z[wrap(n + 1)] & kLower);
-      w = z[wrap(n + kM)] ^ (y >> 1) ^ ((y & 1ull) ? kMatrixA : 0ull);
-      // the slot of z[n + 312] held z[n - 312]: no read of this step or the next
-      z[wrap(n + kN)] = w;
-    }
+  auto twist = [](uint64_t a, uint64_t b, uint64_t c) {  // z[n + 312] from z[n], z[n + 1], z[n + 156]
+    const uint64_t y = (a & kUpper) | (b & kLower);
+    return c ^ (y >> 1) ^ ((y & 1ull) ? kMatrixA : 0ull);
+  };
+  auto emit = [&](uint64_t base, uint64_t w) {  // draw base + q of this step into the regions
     bool any = false;  // block-uniform: does this step's window meet a region?
     for (int p = 0; p < np; ++p) any = any || (base < hi[p] && base + kM > lo[p]);
-    if (any && q < kM) {
-      const uint64_t pos = base + (uint64_t)q;
-      const uint64_t y = temper(w);
-      const double u = (double)(y >> 11) * 0x1.0p-53;
-      const double x0 = __dadd_rn(-1.0, __dmul_rn(u, 2.0));  // lo + u * (hi - lo), not contracted
-      for (int p = 0; p < np; ++p)
-        if (pos >= lo[p] && pos < hi[p]) {
-          const double x = is_f32[p] ? (double)__double2float_rn(x0) : x0;
-          const int64_t o = region_off[(size_t)t * nP + p] + (int64_t)(pos - lo[p]);
-          init[o] = x;
-          fin[o] = x;
-        }
+    if (!any || q >= kM) return;
+    const uint64_t pos = base + (uint64_t)q;
+    const uint64_t y = temper(w);
+    const double u = (double)(y >> 11) * 0x1.0p-53;
+    const double x0 = __dadd_rn(-1.0, __dmul_rn(u, 2.0));  // lo + u * (hi - lo), not contracted
+    for (int p = 0; p < np; ++p)
+      if (pos >= lo[p] && pos < hi[p]) {
+        const double x = is_f32[p] ? (double)__double2float_rn(x0) : x0;
+        const int64_t o = region_off[(size_t)t * nP + p] + (int64_t)(pos - lo[p]);
+        init[o] = x;
+        fin[o] = x;
+      }
+  };
+  // two steps per barrier: step B's thread q needs z[n + 156] and z[n + 157] (written two
+  // steps back, visible since the last barrier) and z[n + 312] = its own step-A word;
+  // only thread 155's z[n + 157] is step A's word of thread 0, which it recomputes
+  int r = 0;  // base % kRing
+  for (uint64_t base = 0; base < end; base += 2 * kM, r = wrap(r + 2 * kM)) {
+    uint64_t wa = 0, wb = 0;
+    if (q < kM) {
+      const int n = r + q;
+      const uint64_t zn156 = z[wrap(n + kM)];
+      wa = twist(z[wrap(n)], z[wrap(n + 1)], zn156);
+      const uint64_t zn157 = q == kM - 1 ? twist(z[wrap(r)], z[wrap(r + 1)], z[wrap(r + kM)]) : z[wrap(n + kM + 1)];
+      wb = twist(zn156, zn157, wa);
+      // the slots of z[n + 312] / z[n + 468] held z[n - 312] / z[n - 156]: read by
+      // neither step of this pair
+      z[wrap(n + kN)] = wa;
+      z[wrap(n + kN + kM)] = wb;
     }
-    __syncthreads();  // this step's words visible to the next step
+    emit(base, wa);
+    emit(base + kM, wb);
+    __syncthreads();  // this pair's words visible to the next pair
   }
   if (!need) return;
   for (int p = 0; p < nP; ++p) {  // final = init + the original run's writes
