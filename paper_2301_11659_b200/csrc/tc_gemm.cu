@@ -1129,15 +1129,56 @@ int atc_sgemm_rm(atc_ctx* ctx, const float* A, const float* B, float* C, int64_t
     atc_set_error(ctx, "device allocation failed");
     return ATC_ERR_CUDA;
   }
-  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(dA, A, (size_t)m * k * 4, cudaMemcpyHostToDevice, st), "H2D A") ||
-      !atc_cuda_ok(ctx, cudaMemcpyAsync(dB, B, (size_t)k * n * 4, cudaMemcpyHostToDevice, st), "H2D B"))
-    return ATC_ERR_CUDA;
-  int rc = atc_sgemm_rm_device(ctx, dA, dB, dC, m, n, k, precision, st);
+  // large calls are pipelined over row chunks of A and C: B goes over first, then chunk
+  // i's A rows (copy stream 1) -> its GEMM (the context's stream) -> its C rows (copy
+  // stream 2), so the H2D of later chunks and the D2H of earlier ones overlap the
+  // tensor-core work (and each other: the copy engines are full duplex).  With pageable
+  // host buffers the copies serialise and the call behaves like the unchunked one.
+  const size_t bytes = ((size_t)m * k + (size_t)k * n + (size_t)m * n) * 4;
+  const int chunks = bytes >= (64u << 20) && m >= 4 * 256 ? 4 : 1;
+  if (chunks == 1) {
+    if (!atc_cuda_ok(ctx, cudaMemcpyAsync(dA, A, (size_t)m * k * 4, cudaMemcpyHostToDevice, st), "H2D A") ||
+        !atc_cuda_ok(ctx, cudaMemcpyAsync(dB, B, (size_t)k * n * 4, cudaMemcpyHostToDevice, st), "H2D B"))
+      return ATC_ERR_CUDA;
+    int rc = atc_sgemm_rm_device(ctx, dA, dB, dC, m, n, k, precision, st);
+    if (rc) return rc;
+    if (!atc_cuda_ok(ctx, cudaMemcpyAsync(C, dC, (size_t)m * n * 4, cudaMemcpyDeviceToHost, st), "D2H C") ||
+        !atc_cuda_ok(ctx, cudaStreamSynchronize(st), "sgemm sync"))
+      return ATC_ERR_CUDA;
+    return ATC_OK;
+  }
+  cudaStream_t cin = ctx->copy_stream[0], cout = ctx->copy_stream[1];
+  cudaEvent_t ev[2 * 4 + 2] = {};
+  for (auto& e : ev)
+    if (!atc_cuda_ok(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate")) return ATC_ERR_CUDA;
+  cudaEvent_t e_start = ev[8], e_b = ev[9];
+  bool ok = atc_cuda_ok(ctx, cudaEventRecord(e_start, st), "cudaEventRecord");  // after earlier work on st
+  ok = ok && atc_cuda_ok(ctx, cudaStreamWaitEvent(cin, e_start, 0), "wait") &&
+       atc_cuda_ok(ctx, cudaMemcpyAsync(dB, B, (size_t)k * n * 4, cudaMemcpyHostToDevice, cin), "H2D B") &&
+       atc_cuda_ok(ctx, cudaEventRecord(e_b, cin), "cudaEventRecord") &&
+       atc_cuda_ok(ctx, cudaStreamWaitEvent(st, e_b, 0), "wait");
+  const int64_t step = (m / chunks + 255) / 256 * 256;
+  int rc = ATC_OK;
+  for (int c = 0; c < chunks && ok && rc == ATC_OK; ++c) {
+    const int64_t r0 = c * step, r1 = std::min<int64_t>(m, r0 + step);
+    if (r1 <= r0) break;
+    const int64_t mr = r1 - r0;
+    ok = atc_cuda_ok(ctx, cudaMemcpyAsync(dA + r0 * k, A + r0 * k, (size_t)mr * k * 4, cudaMemcpyHostToDevice, cin),
+                     "H2D A") &&
+         atc_cuda_ok(ctx, cudaEventRecord(ev[2 * c], cin), "cudaEventRecord") &&
+         atc_cuda_ok(ctx, cudaStreamWaitEvent(st, ev[2 * c], 0), "wait");
+    if (!ok) break;
+    rc = atc_sgemm_rm_device(ctx, dA + r0 * k, dB, dC + r0 * n, mr, n, k, precision, st);
+    ok = ok && rc == ATC_OK && atc_cuda_ok(ctx, cudaEventRecord(ev[2 * c + 1], st), "cudaEventRecord") &&
+         atc_cuda_ok(ctx, cudaStreamWaitEvent(cout, ev[2 * c + 1], 0), "wait") &&
+         atc_cuda_ok(ctx, cudaMemcpyAsync(C + r0 * n, dC + r0 * n, (size_t)mr * n * 4, cudaMemcpyDeviceToHost, cout),
+                     "D2H C");
+  }
+  ok = ok && atc_cuda_ok(ctx, cudaStreamSynchronize(cout), "sgemm sync") &&
+       atc_cuda_ok(ctx, cudaStreamSynchronize(st), "sgemm sync");
+  for (auto& e : ev) cudaEventDestroy(e);
   if (rc) return rc;
-  if (!atc_cuda_ok(ctx, cudaMemcpyAsync(C, dC, (size_t)m * n * 4, cudaMemcpyDeviceToHost, st), "D2H C") ||
-      !atc_cuda_ok(ctx, cudaStreamSynchronize(st), "sgemm sync"))
-    return ATC_ERR_CUDA;
-  return ATC_OK;
+  return ok ? ATC_OK : ATC_ERR_CUDA;
 }
 
 int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, float* d_out, int64_t n, int64_t c,
