@@ -130,6 +130,12 @@ __host__ __device__ constexpr uint32_t idesc_tf32(uint32_t b_mn_major) {
          ((uint32_t)(BM >> 4) << 24);
 }
 
+// M = 128 with the operand majors and N given (N a multiple of 16, <= 256)
+__host__ __device__ constexpr uint32_t idesc_tf32_n(uint32_t a_mn_major, uint32_t b_mn_major, uint32_t n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn_major << 15) | (b_mn_major << 16) | ((n >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -176,6 +182,7 @@ struct Problem {
   int pair;  // 1: CTA pairs (cluster of 2) on adjacent M tiles share the B tile via TMA multicast
   int tma_store;  // 1: epilogue writes 32x32 sub-tiles with TMA bulk stores (modes 0, 2, 3)
   int umma2;      // 1: sgemm on k_tc_gemm2 (cta_group::2, M = 256 per CTA pair)
+  int bn;         // conv mode 5: filters per tile (N of the MMA, a multiple of 32, <= BN)
   int ksplit;     // k_tc_gemm2, conv mode 4: 2 = each tile's k-blocks in two halves on two
                   // pairs, both added into the zeroed output (two partial sums: the same
                   // result in either order)
@@ -203,41 +210,48 @@ __device__ __forceinline__ void tile_coords(const Problem& p, int tile, int& tm,
   tn = in_group / gm;
 }
 
-// k-block kb in [0, splits * kblocks): which operand pair and which coordinates
-__device__ __forceinline__ void kblock_coords(const Problem& p, int kb, int kblocks_per_split, int tm, int tn, int ti,
-                                              int& sel_a, int& sel_b, int& a_c0, int& a_c1, int& b_c0, int& b_c1) {
-  const int split = kb / kblocks_per_split;
-  const int k = kb - split * kblocks_per_split;
-  // 3xTF32 order: lo*hi, hi*lo, hi*hi (small terms first)
-  sel_a = split == 0 && p.splits == 3 ? 1 : 0;
-  sel_b = split == 1 ? 1 : 0;
-  if (p.conv == 0) {
-    a_c0 = k * BK;        // K
-    a_c1 = tm * BM;       // M
-    b_c0 = tn * BN;       // N (chunk offset added by caller)
-    b_c1 = k * BK;        // K
-  } else if (p.conv == 3) {  // sgemm with B transposed to [N][K]: K-major like A
-    a_c0 = k * BK;
-    a_c1 = tm * BM;
-    b_c0 = k * BK;        // K
-    b_c1 = tn * BN;       // N row (half offset added by caller)
-  } else {
-    const int cblocks = p.K / BK;     // C / 32
-    const int rs = k / cblocks;       // r*S + s
-    const int c0 = (k - rs * cblocks) * BK;
-    const int r = rs / p.S, s = rs - (rs / p.S) * p.S;
-    a_c0 = rs * p.K + c0;             // column in W_krsc [Kf][R*S*C]
-    a_c1 = tm * BM;                   // filter row
-    if (p.conv == 1) {
-      b_c0 = c0;                      // channel block of the NHWC input [N*H*W][C]
-      b_c1 = ti * p.H * p.W + tn * BN + r * p.W + s;  // pixel row: affine shift on the input grid
-    } else {
-      // 1x1 on NCHW directly: [N*C][H*W] view, MN-major, pixel offset 0 (aligned)
-      b_c0 = tn * BN;
-      b_c1 = ti * p.Cin + c0;
+// The producers' walk over a unit's k-blocks kb in [0, splits * kblocks), without
+// divisions (the producer is one thread and a stage's MMAs last ~500 cycles, so its
+// per-k-block integer work must stay far below that).  Coordinates of k-block k:
+//   A (every mode): column k * BK of [M][K] / W_krsc [Kf][R*S*C] (= r*S*C + s*C + c0), row tm * BM
+//   B sgemm: (tn * BN, k * BK) of [K][N]; mode 3 (B transposed): (k * BK, tn * BN) of [N][K]
+//   B conv on the NHWC input grid (mode 1): channel c0, pixel row img*H*W + tn*BN + r*W + s
+//   B 1x1 on NCHW (mode 2): pixel tn * BN, row img * C + c0 of [N*C][H*W]
+//   B im2col (mode 4): channel c0 at the tile's first output pixel, tap offsets (s, r)
+// 3xTF32 order of the splits: lo*hi, hi*lo, hi*hi (small terms first).
+struct KbWalk {
+  int split, k;   // operand split (3xTF32), k-block within the split
+  int c0, r, s;   // conv: channel block start, filter tap
+  __device__ __forceinline__ void start(const Problem& p, int kb, int kblocks) {
+    split = kb / kblocks;
+    k = kb - split * kblocks;
+    c0 = r = s = 0;
+    if (p.conv == 1 || p.conv == 2 || p.conv == 4 || p.conv == 5) {
+      const int cblocks = p.K / BK, rs = k / cblocks;
+      c0 = (k - rs * cblocks) * BK;
+      r = rs / p.S;
+      s = rs - r * p.S;
     }
   }
-}
+  __device__ __forceinline__ void next(const Problem& p, int kblocks) {
+    if (++k == kblocks) {
+      k = 0;
+      ++split;
+      c0 = r = s = 0;
+      return;
+    }
+    c0 += BK;
+    if (c0 == p.K) {
+      c0 = 0;
+      if (++s == p.S) {
+        s = 0;
+        ++r;
+      }
+    }
+  }
+  __device__ __forceinline__ int sel_a(const Problem& p) const { return split == 0 && p.splits == 3 ? 1 : 0; }
+  __device__ __forceinline__ int sel_b() const { return split == 1 ? 1 : 0; }
+};
 
 __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constant__ Maps maps, const Problem p) {
   extern __shared__ uint8_t smem_raw[];
@@ -249,7 +263,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kblocks = (p.conv == 1 || p.conv == 2 ? p.R * p.S * (p.K / BK) : (p.K + BK - 1) / BK);
+  const int kblocks = (p.conv == 1 || p.conv == 2 || p.conv == 5 ? p.R * p.S * (p.K / BK) : (p.K + BK - 1) / BK);
   const int total_kb = kblocks * p.splits;
   // work units: single tiles, or M-tile pairs processed by a 2-CTA cluster
   uint32_t rank = 0;
@@ -290,12 +304,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
         int tm, tn, ti;
         tile_coords(p, unit, tm, tn, ti);
         if (p.pair) tm = 2 * tm + (int)rank;
-        for (int kb = 0; kb < total_kb; ++kb) {
+        KbWalk w;
+        w.start(p, 0, kblocks);
+        // per-unit parts of the B coordinates (kblock_coords)
+        const int pix0 = ti * p.H * p.W + tn * BN, a1 = tm * BM;
+        for (int kb = 0; kb < total_kb; ++kb, w.next(p, kblocks)) {
           mbar_wait(&empty[stage], phase ^ 1);
-          int sa, sb, a0, a1, b0, b1;
-          kblock_coords(p, kb, kblocks, tm, tn, ti, sa, sb, a0, a1, b0, b1);
+          const int sa = w.sel_a(p), sb = w.sel_b();
+          const int a0 = w.k * BK;
+          int b0, b1;
+          if (p.conv == 0) {
+            b0 = tn * BN;
+            b1 = w.k * BK;
+          } else if (p.conv == 3) {
+            b0 = w.k * BK;
+            b1 = tn * BN;
+          } else if (p.conv == 1) {
+            b0 = w.c0;
+            b1 = pix0 + w.r * p.W + w.s;
+          } else {
+            b0 = tn * BN;
+            b1 = ti * p.Cin + w.c0;
+          }
           uint8_t* sA = smem + stage * STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
+          if (p.conv == 5) {
+            // 1x1 with pixels as M: A = this tile's 128 pixels x 32 channels of the
+            // [N*C][H*W] input (MN-major: 4 chunks of 32 pixels), B = bn filters x 32
+            // channels of the [K][C] weights (K-major)
+            mbar_expect_tx(&full[stage], A_BYTES + p.bn * BK * 4);
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j)
+              tma_load_2d(sA + j * (BK * 128), &maps.a[sa], &full[stage], a1 + 32 * j, ti * p.Cin + w.c0);
+            tma_load_2d(sB, &maps.b[sb], &full[stage], w.c0, tn * p.bn);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           tma_load_2d(sA, &maps.a[sa], &full[stage], a0, a1);
           if (p.conv == 1) {
@@ -349,6 +396,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      // mode 5 swaps the majors: A (pixels) MN-major, B (filters) K-major, N = bn
+      const bool a_mn = p.conv == 5, b_kmajor = p.conv == 1 || p.conv == 3 || p.conv == 5;
+      const uint32_t a_base = smem_u32(smem);
+      const uint64_t adesc0 = a_mn ? make_desc(a_base, BK * 128, 512, kSw128Base32) : make_desc(a_base, 16, 1024, kSw128);
+      const uint64_t bdesc0 = b_kmajor ? make_desc(a_base + A_BYTES, 16, 1024, kSw128)
+                                       : make_desc(a_base + A_BYTES, BK * 128, 512, kSw128Base32);
+      const uint32_t astep = a_mn ? 64u : 2u, bstep = b_kmajor ? 2u : 64u;  // (32 B | 1 KB) >> 4 per K = 8
+      const uint32_t idesc = a_mn ? idesc_tf32_n(1, 0, (uint32_t)p.bn) : b_kmajor ? idesc_tf32(0) : idesc_tf32(1);
       for (int unit = unit0; unit < num_units; unit += unit_step) {
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -356,19 +411,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
         for (int kb = 0; kb < total_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
-          const uint32_t b_addr = a_addr + A_BYTES;
+          // the stage's descriptors: the base descriptors plus the stage offset (>> 4)
+          const uint64_t soff = (uint64_t)((stage * STAGE_BYTES) >> 4);
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             // A: K-major SW128, +32 B per K=8 step inside the 128 B atom; SBO = 8 rows * 128 B
-            const uint64_t ad = make_desc(a_addr + kk * 32, 16, 1024, kSw128);
             // B (sgemm): MN-major SW128 with 32 B atoms: chunks of 32 N at LBO = 32 rows *
             // 128 B, 4-row K groups at SBO = 512 B; +8 rows (1 KB) per K step.
             // B (conv): K-major SW128 like A.
-            const bool b_kmajor = p.conv == 1 || p.conv == 3;
-            const uint64_t bd = b_kmajor ? make_desc(b_addr + kk * 32, 16, 1024, kSw128)
-                                            : make_desc(b_addr + kk * 1024, BK * 128, 512, kSw128Base32);
-            mma_tf32(d_tmem, ad, bd, b_kmajor ? idesc_tf32(0) : idesc_tf32(1), (kb > 0 || kk > 0) ? 1u : 0u);
+            mma_tf32(d_tmem, adesc0 + soff + (uint64_t)(kk * astep), bdesc0 + soff + (uint64_t)(kk * bstep),
+                     idesc, (kb > 0 || kk > 0) ? 1u : 0u);
           }
           // smem stage free once these MMAs complete (pair: in both CTAs)
           if (p.pair)
@@ -406,9 +458,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
       // registers (lane = row) -> shared memory -> registers (lane = column), so a
       // store instruction writes consecutive pixels of one output row
       const int row0 = tm * BM + q * 32;
+      if (p.conv == 5) {
+        // lane = output pixel, register v = filter: each store writes 32 consecutive
+        // pixels of one filter's output plane (128 B)
+        const int64_t ohw = p.N;
+        const int px = row0 + lane, f0 = tn * p.bn;
+        float* dst = p.C + ((int64_t)ti * p.M + f0) * ohw + px;
+#pragma unroll 1
+        for (int c0 = 0; c0 < p.bn && f0 + c0 < p.M; c0 += 32) {
+          uint32_t r[32];
+          TMEM_LD_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(q * 32) << 16), r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (px < ohw) {
+            float* d = dst + (int64_t)c0 * ohw;
+            if (f0 + c0 + 32 <= p.M) {
+#pragma unroll
+              for (int v = 0; v < 32; ++v, d += ohw) __stcs(d, __uint_as_float(r[v]));
+            } else {
+              const int nv = p.M - f0 - c0;
+#pragma unroll
+              for (int v = 0; v < 32; ++v, d += ohw)
+                if (v < nv) __stcs(d, __uint_as_float(r[v]));
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
 #pragma unroll 1
       constexpr int kColSpan = BN / (EPI_WARPS / 4);  // columns per epilogue warp
       for (int c0 = half * kColSpan; c0 < (half + 1) * kColSpan; c0 += 32) {
+        // rows past M: nothing to store (a TMA store would clip only at the tensor's
+        // edge, and in the 1x1 [N*K][OH*OW] view rows past M belong to the next image)
+        if (row0 >= p.M) continue;
         uint32_t r[32];
         const uint32_t taddr = tmem_base + acc * BN + c0 + ((uint32_t)(q * 32) << 16);
         TMEM_LD_32x32b_x32(taddr, r);
@@ -671,6 +759,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
       // ================= TMA producer (both CTAs) =================
       int stage = 0;
       uint32_t phase = 0;
+      const uint32_t full_leader = peer_addr(smem_u32(&full[0]), 0);
       for (int unit = unit0; unit < num_units; unit += unit_step) {
         int tm2, tn, ti;
         {
@@ -681,29 +770,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
         }
         const int tm = 2 * tm2 + (int)rank;  // this CTA's 128 rows
         const int kb0 = (unit % ks_n) * kb_per;
-        for (int kb = kb0; kb < kb0 + kb_per; ++kb) {
+        // per-unit parts of the coordinates: im2col's first output pixel of this CTA's
+        // 128 (compact, across images), the input-grid pixel row, the A row
+        int n0 = 0, oh0 = 0, ow0 = 0;
+        if (p.conv == 4) {
+          const int ohw = p.OH * p.OW, q0 = tn * BN + (int)rank * (BN / 2);
+          n0 = q0 / ohw;
+          const int rem = q0 - n0 * ohw;
+          oh0 = rem / p.OW;
+          ow0 = rem - oh0 * p.OW;
+        }
+        const int pix0 = ti * p.H * p.W + tn * BN + (int)rank * (BN / 2), a1 = tm * BM;
+        KbWalk w;
+        w.start(p, kb0, kblocks);
+        for (int kb = kb0; kb < kb0 + kb_per; ++kb, w.next(p, kblocks)) {
           mbar_wait(&empty[stage], phase ^ 1);
-          int sa, sb, a0, a1, b0, b1;
-          kblock_coords(p, kb, kblocks, tm, tn, ti, sa, sb, a0, a1, b0, b1);
+          const int sa = w.sel_a(p), sb = w.sel_b();
           uint8_t* sA = smem + stage * STAGE2_BYTES;
           uint8_t* sB = sA + A_BYTES;
-          const uint32_t bar = peer_addr(smem_u32(&full[stage]), 0);  // the leader's barrier
+          const uint32_t bar = full_leader + stage * 8;  // the leader's barrier
           if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE2_BYTES);
-          tma_load_2d_2sm(sA, &maps.a[sa], bar, a0, a1);
+          tma_load_2d_2sm(sA, &maps.a[sa], bar, w.k * BK, a1);
           if (p.conv == 4) {
-            // im2col: this CTA's 128 output pixels (compact, across images) at tap (r, s)
-            const int cblocks = p.K / BK, kk = kb % kblocks, rs = kk / cblocks, c0 = (kk - rs * cblocks) * BK;
-            const int rr = rs / p.S, ss = rs - rr * p.S;
-            const int ohw = p.OH * p.OW, q0 = tn * BN + (int)rank * (BN / 2);
-            const int n0 = q0 / ohw, rem = q0 - n0 * ohw, oh0 = rem / p.OW, ow0 = rem - (rem / p.OW) * p.OW;
-            tma_load_im2col_2sm(sB, &maps.b[sb], bar, c0, ow0, oh0, n0, (uint16_t)ss, (uint16_t)rr);
+            // im2col: this CTA's 128 output pixels at tap (r, s), channels c0 .. c0 + 31
+            tma_load_im2col_2sm(sB, &maps.b[sb], bar, w.c0, ow0, oh0, n0, (uint16_t)w.s, (uint16_t)w.r);
           } else if (p.conv == 1) {
             // K-major: this CTA's 128 pixel rows x 32 channels in one box
-            tma_load_2d_2sm(sB, &maps.b[sb], bar, b0, b1 + (int)rank * (BN / 2));
+            tma_load_2d_2sm(sB, &maps.b[sb], bar, w.c0, pix0 + w.r * p.W + w.s);
           } else {
+            const int b0 = tn * BN + (int)rank * (BN / 2);
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)  // MN-major: this CTA's 4 chunks of 32 columns
-              tma_load_2d_2sm(sB + j * (BK * 128), &maps.b[sb], bar, b0 + (int)rank * (BN / 2) + 32 * j, b1);
+              tma_load_2d_2sm(sB + j * (BK * 128), &maps.b[sb], bar, b0 + 32 * j, w.k * BK);
           }
           if (++stage == STAGES2) {
             stage = 0;
@@ -727,6 +825,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      const bool b_kmajor = p.conv == 1 || p.conv == 4;
+      const uint32_t a_base = smem_u32(smem);
+      const uint64_t adesc0 = make_desc(a_base, 16, 1024, kSw128);
+      const uint64_t bdesc0 = b_kmajor ? make_desc(a_base + A_BYTES, 16, 1024, kSw128)
+                                       : make_desc(a_base + A_BYTES, BK * 128, 512, kSw128Base32);
+      const uint32_t bstep = b_kmajor ? 2u : 64u;
+      const uint32_t idesc = idesc_tf32_m256(b_kmajor ? 0u : 1u);
       for (int unit = unit0; unit < num_units; unit += unit_step) {
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -735,16 +840,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
         for (int kb = kb0; kb < kb0 + kb_per; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + stage * STAGE2_BYTES);
-          const uint32_t b_addr = a_addr + A_BYTES;
-          const bool b_kmajor = p.conv == 1 || p.conv == 4;
+          const uint64_t soff = (uint64_t)((stage * STAGE2_BYTES) >> 4);
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t ad = make_desc(a_addr + kk * 32, 16, 1024, kSw128);
-            const uint64_t bd = b_kmajor ? make_desc(b_addr + kk * 32, 16, 1024, kSw128)
-                                         : make_desc(b_addr + kk * 1024, BK * 128, 512, kSw128Base32);
-            mma_tf32_2sm(d_tmem, ad, bd, idesc_tf32_m256(b_kmajor ? 0u : 1u), (kb > kb0 || kk > 0) ? 1u : 0u);
-          }
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma_tf32_2sm(d_tmem, adesc0 + soff + (uint64_t)(kk * 2), bdesc0 + soff + (uint64_t)(kk * bstep), idesc,
+                         (kb > kb0 || kk > 0) ? 1u : 0u);
           mma_commit_2sm(&empty[stage]);  // both CTAs' stage buffers free once these complete
           if (++stage == STAGES2) {
             stage = 0;
@@ -954,13 +1054,14 @@ bool make_map(atc_ctx* ctx, CUtensorMap* m, const float* base, uint64_t rows, ui
 // ATC_TC_NO_KSPLIT never splits K, ATC_TC_NO_2SM disables the cta_group::2 kernel,
 // ATC_TC_NO_TMA_STORE the TMA-store epilogue, ATC_TC_NO_PAIR the 1-SM kernel's
 // B multicast across a CTA pair, ATC_TC_NO_IM2COL the im2col-mode conv B operand;
-// ATC_TC_B_KMAJOR transposes the sgemm B to K-major once.
+// ATC_TC_B_KMAJOR transposes the sgemm B to K-major once; ATC_TC_NO_SWAP1X1 keeps
+// 1x1 convolutions in the filters-as-M form (mode 2).
 bool tc_flag(const atc_ctx* ctx, int f) { return (ctx->opt_tc_flags & f) != 0; }
 
 // CTA pairs need an MN-major B (loaded as chunks, half by each CTA) and >= 2
 // M tiles
 int use_pair(const atc_ctx* ctx, const Problem& p) {
-  return !tc_flag(ctx, ATC_TC_NO_PAIR) && p.conv != 1 && p.tiles_m >= 2 ? 1 : 0;
+  return !tc_flag(ctx, ATC_TC_NO_PAIR) && p.conv != 1 && p.conv != 5 && p.tiles_m >= 2 ? 1 : 0;
 }
 
 // the dynamic shared-memory opt-in of both GEMM kernels, once per context (the
@@ -1222,11 +1323,58 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
     ih = buf;
     il = lo;
   }
+  // 1x1 with the output pixels as M (mode 5): lane = pixel in TMEM, so the epilogue
+  // stores 128 B runs of each filter's output plane straight from registers, and a
+  // filter count below 128 is the MMA's N instead of a half-empty M tile.  Used where
+  // the call is store-bound (few channels: 2-4 k-blocks per tile) or K < 128; with
+  // many channels the filters-as-M form reads less of the weights per pixel
+  // (tools/time_conv.py: conv2_x.a 64->64 0.068 vs 0.079 ms, conv2_x.c 64->256 0.198
+  // vs 0.205, conv3_x.a 512->128 0.109 vs 0.095)
+  const bool swap = direct && (k < BM || c <= 128) && !tc_flag(ctx, ATC_TC_NO_SWAP1X1);
   const int64_t wn = k * c * r * s;
-  float* wh = (float*)atc_ctx_scratch(ctx, 15, (size_t)wn * 4 * 2);
-  if (!wh) return ATC_ERR_CUDA;
-  float* wl = splits == 3 ? wh + wn : nullptr;
-  k_weights_krsc<<<grid_for(wn), 256, 0, st>>>(d_w, wh, wl, (int)k, (int)c, (int)r, (int)s);
+  const float* wh = d_w;  // 1x1 KCRS is already [K][C]
+  const float* wl = nullptr;
+  if (!(swap && splits == 1)) {
+    float* wbuf = (float*)atc_ctx_scratch(ctx, 15, (size_t)wn * 4 * 2);
+    if (!wbuf) return ATC_ERR_CUDA;
+    wl = splits == 3 ? wbuf + wn : nullptr;
+    k_weights_krsc<<<grid_for(wn), 256, 0, st>>>(d_w, wbuf, const_cast<float*>(wl), (int)k, (int)c, (int)r, (int)s);
+    wh = wbuf;
+  }
+  if (swap) {
+    Maps maps;
+    std::memset(&maps, 0, sizeof maps);
+    Problem p{};
+    p.conv = 5;
+    p.M = (int)k;
+    p.N = (int)hw;
+    p.K = (int)c;
+    p.splits = splits;
+    p.C = d_out;
+    p.img = (int)n;
+    p.Cin = (int)c;
+    p.H = (int)h;
+    p.W = (int)w_;
+    p.R = p.S = 1;
+    p.OH = (int)oh;
+    p.OW = (int)ow;
+    p.bn = (int)std::min<int64_t>(BN, (k + 31) / 32 * 32);
+    p.tiles_m = (int)((hw + BM - 1) / BM);
+    p.tiles_n = (int)((k + p.bn - 1) / p.bn);
+    p.tiles_img = (int)n;
+    for (int i = 0; i < splits && i < 2; ++i) {
+      const float* xi = i ? il : ih;
+      const float* wi = i ? wl : wh;
+      if (!make_map(ctx, &maps.a[i], xi, n * c, hw, hw, 32, BK, true) ||
+          !make_map(ctx, &maps.b[i], wi, k, c, c, BK, (uint32_t)p.bn, false))
+        return ATC_ERR_CUDA;
+    }
+    if (splits == 1) {
+      maps.a[1] = maps.a[0];
+      maps.b[1] = maps.b[0];
+    }
+    return launch(ctx, maps, p, st) ? ATC_OK : ATC_ERR_CUDA;
+  }
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   // cta_group::2 (M = 256 filters per CTA pair) when there are >= 2 filter tiles;
@@ -1293,7 +1441,8 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
     }
   }
   // 1x1 direct: the output is a [N*K][OH*OW] matrix (hw % 4 == 0): TMA-store epilogue
-  p.tma_store = direct && !tc_flag(ctx, ATC_TC_NO_TMA_STORE) ? 1 : 0;
+  // when every 32-row store box lies inside one image's K rows
+  p.tma_store = direct && k % 32 == 0 && !tc_flag(ctx, ATC_TC_NO_TMA_STORE) ? 1 : 0;
   if (p.tma_store && !make_map(ctx, &maps.c, d_out, n * k, oh * ow, oh * ow, 32, 32, false)) return ATC_ERR_CUDA;
   return launch(ctx, maps, p, st) ? ATC_OK : ATC_ERR_CUDA;
 }

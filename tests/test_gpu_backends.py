@@ -121,6 +121,9 @@ def test_sgemm_sample_one_pattern():
 
 @pytest.mark.parametrize("shape", [(2, 64, 10, 12, 64, 3, 3), (1, 32, 9, 9, 512, 3, 3), (3, 64, 8, 8, 256, 1, 1),
                                    (2, 96, 17, 13, 40, 2, 4),
+                                   # 1x1 with fewer than 128 filters over several images (the
+                                   # [N*K][OH*OW] view: a tile's rows past K are the next image's)
+                                   (4, 64, 8, 8, 64, 1, 1), (3, 32, 6, 6, 40, 1, 1), (2, 64, 16, 16, 200, 1, 1),
                                    # > 128 filters, several images: the im2col pair kernel
                                    (5, 64, 11, 7, 256, 3, 2), (3, 32, 6, 9, 300, 2, 3), (9, 64, 9, 9, 384, 3, 3),
                                    # 20 pair tiles on 74 pair slots: split-K over two pairs
@@ -138,6 +141,29 @@ def test_conv2d_accuracy(shape, prec):
     ref = torch.nn.functional.conv2d(torch.from_numpy(x).double(), torch.from_numpy(wt).double()).numpy()
     err = np.abs(out - ref) / (1 + np.abs(ref))
     assert err.max() <= tol, err.max()
+
+
+@pytest.mark.parametrize("shape", [(4, 64, 8, 8, 64, 1, 1), (3, 32, 6, 6, 40, 1, 1), (2, 96, 10, 12, 300, 1, 1),
+                                   (5, 64, 34, 34, 256, 3, 3), (3, 32, 6, 9, 300, 2, 3)])
+@pytest.mark.parametrize("flags", ["TC_NO_SWAP1X1", "TC_NO_IM2COL", "TC_NO_KSPLIT", "TC_NO_2SM", "TC_NO_TMA_STORE"])
+def test_conv2d_kernel_variants(shape, flags):
+    """Every conv kernel form (1x1 pixels-as-M / filters-as-M, im2col / input grid,
+    K-split, cta_group::2 / ::1) within the stated FP64 tolerance, all images."""
+    import torch
+
+    from paper_2301_11659_b200 import _lib
+
+    n, c, h, w, k, r, s = shape
+    rng = np.random.default_rng(sum(shape) + 1)
+    x = rng.uniform(-1, 1, (n, c, h, w)).astype(np.float32)
+    wt = rng.uniform(-1, 1, (k, c, r, s)).astype(np.float32)
+    ref = torch.nn.functional.conv2d(torch.from_numpy(x).double(), torch.from_numpy(wt).double()).numpy()
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.OPT_TC_FLAGS, getattr(_lib, flags))
+    for prec in ("tf32", "3xtf32"):
+        out = backends.conv2d_nchw(x, wt, prec, ctx=ctx)
+        err = np.abs(out - ref) / (1 + np.abs(ref))
+        assert err.max() <= TOLS[prec][0] * np.sqrt(c * r * s), (prec, err.max())
 
 
 def test_conv2d_matches_reference_semantics_small():
