@@ -132,7 +132,8 @@ enum { ATC_CONV_SCREEN_AUTO = 0,    /* k_screen_conv_pairs where it applies     
        ATC_CONV_SCREEN_PLANES = 1,  /* k_screen_conv_planes instead of the pairs */
        ATC_CONV_SCREEN_GENERIC = 2  /* the generic k_screen_rows for conv        */ };
 enum { ATC_TC_NO_KSPLIT = 1, ATC_TC_NO_2SM = 2, ATC_TC_NO_TMA_STORE = 4, ATC_TC_NO_PAIR = 8,
-       ATC_TC_NO_IM2COL = 16, ATC_TC_B_KMAJOR = 32, ATC_TC_NO_SWAP1X1 = 64 };
+       ATC_TC_NO_IM2COL = 16, ATC_TC_B_KMAJOR = 32, ATC_TC_NO_SWAP1X1 = 64,
+       ATC_TC_NO_B3D = 128 };
 int atc_set_option(atc_ctx* ctx, int32_t option, int32_t value);
 
 /* Run all subsequent work of this context on the caller's CUDA stream

@@ -266,7 +266,7 @@ int atc_set_option(atc_ctx* ctx, int32_t option, int32_t value) {
     ctx->opt_conv_streams = value;
     return ATC_OK;
   }
-  if (option == ATC_OPT_TC_FLAGS && value >= 0 && value < 128) {
+  if (option == ATC_OPT_TC_FLAGS && value >= 0 && value < 256) {
     ctx->opt_tc_flags = value;
     return ATC_OK;
   }

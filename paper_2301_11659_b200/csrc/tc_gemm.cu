@@ -92,6 +92,22 @@ __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
 }
+// 3-D box (MN-major B as [chunk][K row][32 columns]: all of a stage's chunks in one load)
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
@@ -182,6 +198,8 @@ struct Problem {
   int pair;  // 1: CTA pairs (cluster of 2) on adjacent M tiles share the B tile via TMA multicast
   int tma_store;  // 1: epilogue writes 32x32 sub-tiles with TMA bulk stores (modes 0, 2, 3)
   int umma2;      // 1: sgemm on k_tc_gemm2 (cta_group::2, M = 256 per CTA pair)
+  int b3d;        // the MN-major operand's map is 3-D [chunks of 32][K][32] (one load per stage):
+                  // sgemm (mode 0) B, 1x1 pixels-as-M (mode 5) A
   int bn;         // conv mode 5: filters per tile (N of the MMA, a multiple of 32, <= BN)
   int ksplit;     // k_tc_gemm2, conv mode 4: 2 = each tile's k-blocks in two halves on two
                   // pairs, both added into the zeroed output (two partial sums: the same
@@ -333,9 +351,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
             // [N*C][H*W] input (MN-major: 4 chunks of 32 pixels), B = bn filters x 32
             // channels of the [K][C] weights (K-major)
             mbar_expect_tx(&full[stage], A_BYTES + p.bn * BK * 4);
-#pragma unroll
-            for (int j = 0; j < BM / 32; ++j)
-              tma_load_2d(sA + j * (BK * 128), &maps.a[sa], &full[stage], a1 + 32 * j, ti * p.Cin + w.c0);
+            if (p.b3d)
+              tma_load_3d(sA, &maps.a[sa], &full[stage], 0, ti * p.Cin + w.c0, a1 >> 5);
+            else
+              for (int j = 0; j < BM / 32; ++j)
+                tma_load_2d(sA + j * (BK * 128), &maps.a[sa], &full[stage], a1 + 32 * j, ti * p.Cin + w.c0);
             tma_load_2d(sB, &maps.b[sb], &full[stage], w.c0, tn * p.bn);
             if (++stage == STAGES) {
               stage = 0;
@@ -356,6 +376,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
             else
               for (int h = 0; h < 2; ++h)
                 tma_load_2d(sB + h * (BN / 2) * 128, &maps.b[sb], &full[stage], b0, b1 + h * (BN / 2));
+          } else if (p.b3d) {
+            // MN-major B as one 3-D box of chunks (pair: this CTA's half, multicast)
+            if (p.pair)
+              tma_load_3d_mc(sB + rank * (BN / 64) * (BK * 128), &maps.b[sb], &full[stage], 0, b1,
+                             (b0 >> 5) + (int)rank * (BN / 64), 0x3);
+            else
+              tma_load_3d(sB, &maps.b[sb], &full[stage], 0, b1, b0 >> 5);
           } else if (p.pair) {
             // MN-major B shared by the pair: this CTA loads half of the 8 chunks and
             // multicasts them into both CTAs' smem (each CTA's full barrier expects
@@ -676,6 +703,14 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
 // im2col-mode TMA (conv, mode 4): pixelsPerColumn consecutive OUTPUT pixels starting
 // at (n, oh, ow) — traversal clipped to the valid-output box of the map — each
 // shifted by the filter tap (s, r), x 32 channels from c, into K-major rows.
+__device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_im2col_2sm(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c,
                                                     int w, int h, int n, uint16_t off_w, uint16_t off_h) {
   asm volatile(
@@ -797,6 +832,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm2(const __grid_consta
           } else if (p.conv == 1) {
             // K-major: this CTA's 128 pixel rows x 32 channels in one box
             tma_load_2d_2sm(sB, &maps.b[sb], bar, w.c0, pix0 + w.r * p.W + w.s);
+          } else if (p.b3d) {
+            // this CTA's 4 chunks of 32 columns in one 3-D box
+            tma_load_3d_2sm(sB, &maps.b[sb], bar, 0, w.k * BK, (tn * BN + (int)rank * (BN / 2)) >> 5);
           } else {
             const int b0 = tn * BN + (int)rank * (BN / 2);
 #pragma unroll
@@ -1050,11 +1088,34 @@ bool make_map(atc_ctx* ctx, CUtensorMap* m, const float* base, uint64_t rows, ui
   return true;
 }
 
+// MN-major [rows][cols] fp32 (cols % 32 == 0) as a 3-D map {32 columns, rows, cols / 32
+// chunks}: one box of `chunks` [box_rows x 32] chunks lands chunk-major in shared
+// memory, the layout of `chunks` separate 2-D chunk loads.
+bool make_map_mn3(atc_ctx* ctx, CUtensorMap* m, const float* base, uint64_t rows, uint64_t cols, uint64_t pitch,
+                  uint32_t box_rows, uint32_t chunks) {
+  auto enc = get_encode(ctx);
+  if (!enc) return false;
+  cuuint64_t dims[3] = {32, rows, cols / 32};
+  cuuint64_t strides[2] = {pitch * 4, 128};
+  cuuint32_t box[3] = {32, box_rows, chunks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    atc_set_error(ctx, "cuTensorMapEncodeTiled (3-D) failed (%d) for [%llu x %llu] pitch %llu", (int)r,
+                  (unsigned long long)rows, (unsigned long long)cols, (unsigned long long)pitch);
+    return false;
+  }
+  return true;
+}
+
 // Kernel-variant switches (context option ATC_OPT_TC_FLAGS, A/B checks):
 // ATC_TC_NO_KSPLIT never splits K, ATC_TC_NO_2SM disables the cta_group::2 kernel,
 // ATC_TC_NO_TMA_STORE the TMA-store epilogue, ATC_TC_NO_PAIR the 1-SM kernel's
 // B multicast across a CTA pair, ATC_TC_NO_IM2COL the im2col-mode conv B operand;
-// ATC_TC_B_KMAJOR transposes the sgemm B to K-major once; ATC_TC_NO_SWAP1X1 keeps
+// ATC_TC_B_KMAJOR transposes the sgemm B to K-major once; ATC_TC_NO_B3D loads the
+// sgemm's MN-major B as separate 2-D chunk boxes; ATC_TC_NO_SWAP1X1 keeps
 // 1x1 convolutions in the filters-as-M form (mode 2).
 bool tc_flag(const atc_ctx* ctx, int f) { return (ctx->opt_tc_flags & f) != 0; }
 
@@ -1171,6 +1232,12 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
   // cta_group::2 (M = 256 per CTA pair) for the MN-major sgemm
   p.umma2 = !tc_flag(ctx, ATC_TC_NO_2SM) && p.conv == 0 && p.tiles_m >= 2 ? 1 : 0;
   if (p.tma_store && !make_map(ctx, &maps.c, dC, m, n, n, 32, 32, false)) return ATC_ERR_CUDA;
+  // one 3-D load per stage for B (4 chunks per CTA on the pair kernels, else 8)
+  p.b3d = !b_kmajor && n % 32 == 0 && !tc_flag(ctx, ATC_TC_NO_B3D) ? 1 : 0;
+  const uint32_t chunks = p.umma2 || p.pair ? BN / 64 : BN / 32;
+  auto bmap = [&](CUtensorMap* mp, const float* base) {
+    return p.b3d ? make_map_mn3(ctx, mp, base, k, n, np, BK, chunks) : make_map(ctx, mp, base, k, n, np, 32, BK, true);
+  };
   if (b_kmajor) {
     float* bt = (float*)atc_ctx_scratch(ctx, 14, (size_t)k * n * 4 * (p.splits == 3 ? 2 : 1));
     if (!bt) return ATC_ERR_CUDA;
@@ -1203,10 +1270,10 @@ int atc_sgemm_rm_device(atc_ctx* ctx, const float* dA, const float* dB, float* d
     k_split_tf32<<<grid_for(m * kp), 256, 0, st>>>(A, ah, al, m * kp);
     k_split_tf32<<<grid_for(k * np), 256, 0, st>>>(B, bh, bl, k * np);
     if (!make_map(ctx, &maps.a[0], ah, m, k, kp, BK, BM, false) || !make_map(ctx, &maps.a[1], al, m, k, kp, BK, BM, false) ||
-        !make_map(ctx, &maps.b[0], bh, k, n, np, 32, BK, true) || !make_map(ctx, &maps.b[1], bl, k, n, np, 32, BK, true))
+        !bmap(&maps.b[0], bh) || !bmap(&maps.b[1], bl))
       return ATC_ERR_CUDA;
   } else {
-    if (!make_map(ctx, &maps.a[0], A, m, k, kp, BK, BM, false) || !make_map(ctx, &maps.b[0], B, k, n, np, 32, BK, true))
+    if (!make_map(ctx, &maps.a[0], A, m, k, kp, BK, BM, false) || !bmap(&maps.b[0], B))
       return ATC_ERR_CUDA;
     maps.a[1] = maps.a[0];
     maps.b[1] = maps.b[0];
@@ -1362,10 +1429,12 @@ int atc_conv2d_nchw_device(atc_ctx* ctx, const float* d_in, const float* d_w, fl
     p.tiles_m = (int)((hw + BM - 1) / BM);
     p.tiles_n = (int)((k + p.bn - 1) / p.bn);
     p.tiles_img = (int)n;
+    p.b3d = hw % 32 == 0 && !tc_flag(ctx, ATC_TC_NO_B3D) ? 1 : 0;
     for (int i = 0; i < splits && i < 2; ++i) {
       const float* xi = i ? il : ih;
       const float* wi = i ? wl : wh;
-      if (!make_map(ctx, &maps.a[i], xi, n * c, hw, hw, 32, BK, true) ||
+      if (!(p.b3d ? make_map_mn3(ctx, &maps.a[i], xi, n * c, hw, hw, BK, BM / 32)
+                  : make_map(ctx, &maps.a[i], xi, n * c, hw, hw, 32, BK, true)) ||
           !make_map(ctx, &maps.b[i], wi, k, c, c, BK, (uint32_t)p.bn, false))
         return ATC_ERR_CUDA;
     }

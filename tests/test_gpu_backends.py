@@ -87,6 +87,25 @@ def test_sgemm_accuracy(m, n, k, prec):
     assert rms <= TOLS[prec][1], rms
 
 
+@pytest.mark.parametrize("m,n,k", [(384, 512, 96), (256, 320, 64), (130, 288, 40)])
+@pytest.mark.parametrize("flags", ["TC_NO_2SM", "TC_NO_B3D", "TC_NO_TMA_STORE", "TC_B_KMAJOR", "TC_NO_PAIR"])
+def test_sgemm_kernel_variants(m, n, k, flags):
+    """Every sgemm kernel form (cta_group::2 / CTA-pair multicast / single CTA, 3-D or
+    chunked B loads, TMA-store or direct epilogue, K-major B) within tolerance."""
+    from paper_2301_11659_b200 import _lib
+
+    rng = np.random.default_rng(m * n + k)
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    b = rng.uniform(-1, 1, (k, n)).astype(np.float32)
+    c64 = a.astype(np.float64) @ b.astype(np.float64)
+    ctx = _lib.Context(0)
+    ctx.set_option(_lib.OPT_TC_FLAGS, getattr(_lib, flags) | (_lib.TC_NO_2SM if flags == "TC_NO_PAIR" else 0))
+    for prec in ("tf32", "3xtf32"):
+        c = backends.sgemm(a, b, prec, ctx=ctx)
+        err = np.abs(c - c64) / (1 + np.abs(c64))
+        assert err.max() <= TOLS[prec][0] * np.sqrt(k), (prec, err.max())
+
+
 @pytest.mark.parametrize("prec", ["tf32", "3xtf32"])
 def test_sgemm_host_pipeline_bit_identical(prec):
     """atc_sgemm_rm on host buffers large enough to be pipelined over row chunks
@@ -144,8 +163,10 @@ def test_conv2d_accuracy(shape, prec):
 
 
 @pytest.mark.parametrize("shape", [(4, 64, 8, 8, 64, 1, 1), (3, 32, 6, 6, 40, 1, 1), (2, 96, 10, 12, 300, 1, 1),
+                                   (3, 64, 16, 16, 72, 1, 1),
                                    (5, 64, 34, 34, 256, 3, 3), (3, 32, 6, 9, 300, 2, 3)])
-@pytest.mark.parametrize("flags", ["TC_NO_SWAP1X1", "TC_NO_IM2COL", "TC_NO_KSPLIT", "TC_NO_2SM", "TC_NO_TMA_STORE"])
+@pytest.mark.parametrize("flags", ["TC_NO_SWAP1X1", "TC_NO_IM2COL", "TC_NO_KSPLIT", "TC_NO_2SM", "TC_NO_TMA_STORE",
+                                   "TC_NO_B3D"])
 def test_conv2d_kernel_variants(shape, flags):
     """Every conv kernel form (1x1 pixels-as-M / filters-as-M, im2col / input grid,
     K-split, cta_group::2 / ::1) within the stated FP64 tolerance, all images."""

@@ -9,6 +9,8 @@ import torch
 from paper_2301_11659_b200 import _lib
 
 ctx = _lib.Context(0)
+if len(sys.argv) > 2:  # context tc flags (ATC_OPT_TC_FLAGS)
+    ctx.set_option(_lib.OPT_TC_FLAGS, int(sys.argv[2]))
 L = _lib.lib()
 m = n = k = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 a = torch.rand(m, k, device="cuda") * 2 - 1
