@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_tc_gemm(const __grid_constan
             float* d = dst + (int64_t)c0 * ohw;
             if (f0 + c0 + 32 <= p.M) {
 #pragma unroll
-              for (int v = 0; v < 32; ++v, d += ohw) __stcs(d, __uint_as_float(r[v]));
+              for (int v = 0; v < 32; ++v, d += ohw) *d = __uint_as_float(r[v]);
             } else {
               const int nv = p.M - f0 - c0;
 #pragma unroll
