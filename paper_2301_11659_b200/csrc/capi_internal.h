@@ -108,6 +108,7 @@ __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, ui
                               unsigned long long* reason_hist);
 __global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need);
 __global__ void k_cmask(const uint8_t* table, uint64_t n_words, int nI, uint32_t* cmask, int shift);
+template <int NIc>  // NIc: the number of user ints when fixed at compile time (9), else 0
 __global__ void k_screen_conv_pairs(TestsetView ts, const uint8_t* perms, uint64_t size_maps, uint64_t begin,
                                     uint64_t end, RowPlan plan, uint64_t* surv, uint64_t surv_cap,
                                     unsigned long long* surv_cnt, unsigned long long* reason_hist, int lut_n);

@@ -197,7 +197,9 @@ atc_ctx* atc_create(int device) {
   }
   cudaSetDevice(device);
   // k_screen_conv_pairs: up to 2^11 row masks + rank / in-extent tables (~40 KB dynamic)
-  if (!atc_cuda_ok(ctx, cudaFuncSetAttribute(k_screen_conv_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024),
+  if (!atc_cuda_ok(ctx, cudaFuncSetAttribute(k_screen_conv_pairs<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024),
+                   "cudaFuncSetAttribute(k_screen_conv_pairs)") ||
+      !atc_cuda_ok(ctx, cudaFuncSetAttribute(k_screen_conv_pairs<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024),
                    "cudaFuncSetAttribute(k_screen_conv_pairs)") ||
       !atc_cuda_ok(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate") ||
 

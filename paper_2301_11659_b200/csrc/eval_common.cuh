@@ -23,6 +23,11 @@
 
 namespace atc {
 
+// k_screen_conv_pairs CTA size: every CTA builds the plane tables once, so fewer,
+// larger CTAs (one per SM) pay that prologue fewer times
+constexpr int kPairThreads = 1024;
+
+
 constexpr int kMaxT = 64;
 constexpr int kMaxPtrs = 16;
 constexpr int kMaxInts = 32;

@@ -117,10 +117,16 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
       const size_t nI2 = (size_t)ts->nI * ts->nI;
       const size_t smem = ((size_t)16 << ts->nI) + (size_t)(lut_n + 15) / 16 * 16 +
                           ((size_t)ts->nP * nI2 + 15) / 16 * 16 + nI2 * sizeof(float);
-      // one wave (3 CTAs per SM at 80 registers): each CTA builds its tables once
-      const unsigned g3 = std::min<unsigned>(g2, (unsigned)ctx->sm_count * 4);
-      k_screen_conv_pairs<<<g3, kScreenThreads, smem, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
-                                                            surv_cap, surv_cnt, hist, lut_n);
+      // one wave of 1024 / kPairThreads CTAs per SM (64 registers): each CTA builds its tables once
+      const uint64_t cubes = rows / ts->nI + 2;
+      const unsigned g3 = std::min<unsigned>((unsigned)((cubes + kPairThreads - 1) / kPairThreads),
+                                             (unsigned)ctx->sm_count * (1024 / kPairThreads));
+      if (ts->nI == 9)
+        k_screen_conv_pairs<9><<<g3, kPairThreads, smem, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
+                                                               surv_cap, surv_cnt, hist, lut_n);
+      else
+        k_screen_conv_pairs<0><<<g3, kPairThreads, smem, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
+                                                               surv_cap, surv_cnt, hist, lut_n);
     } else if (i32 && conv_thresholds_ok(ctx, sp, *plan, ts->nI)) {
       k_screen_conv_planes<<<g2, kScreenThreads, 0, st>>>(ts->view, src.perms, src.size_maps, b, e, *plan, surv,
                                                         surv_cap, surv_cnt, hist);

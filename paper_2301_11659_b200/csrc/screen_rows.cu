@@ -512,7 +512,8 @@ __device__ __forceinline__ int div_capn(uint32_t a, uint32_t b, float rb, int ca
 
 // lut_n > 0: products are in [.., lut_n - 1] and the dynamic shared memory holds a
 // rank table (count of pair products <= T, T in [0, lut_n)) after the row table
-__global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, const uint8_t* perms, uint64_t size_maps,
+template <int NIc>
+__global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_conv_pairs(TestsetView ts, const uint8_t* perms, uint64_t size_maps,
                                                             uint64_t begin, uint64_t end, RowPlan plan,
                                                             uint64_t* surv, uint64_t surv_cap,
                                                             unsigned long long* surv_cnt,
@@ -532,7 +533,7 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
   __shared__ uint32_t s_cks[NS];
   __shared__ M128 s_okm[129];            // pairs of product rank < r that pass x >= 1, c >= 1
   __shared__ uint8_t s_cnt[129];         // their number
-  const int nI = ts.nI, nI2 = nI * nI;
+  const int nI = NIc ? NIc : ts.nI, nI2 = nI * nI;
   // CTA tables: built once, from O(nI^2) work per thread at most (the per-CTA
   // prologue is paid by every one of the 4 x 148 CTAs)
   if (threadIdx.x < nI) {
@@ -741,6 +742,7 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
       const float* rhw = s_rhw + digit[3] * nI;
       if (c_max >= umax && d_out >= umax) {  // cube_dm = x < 1 | c < 1: the rank-count form
         const unsigned int n_ok_all = s_cnt[nI2];
+#pragma unroll
         for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
           // the plane's position-0/1 verdicts over the c rows, loaded first (used last)
           const uint32_t cw2 = __ldg(plan.cmask + ckey0 + (uint32_t)hd * cks[2]) & sel;
@@ -870,6 +872,11 @@ __global__ void __launch_bounds__(256, 4) k_screen_conv_pairs(TestsetView ts, co
   if (threadIdx.x < ATC_REASON_COUNT && s_hist[threadIdx.x])
     atomicAdd(&reason_hist[threadIdx.x], (unsigned long long)s_hist[threadIdx.x]);
 }
+
+template __global__ void k_screen_conv_pairs<0>(TestsetView, const uint8_t*, uint64_t, uint64_t, uint64_t, RowPlan,
+                                                uint64_t*, uint64_t, unsigned long long*, unsigned long long*, int);
+template __global__ void k_screen_conv_pairs<9>(TestsetView, const uint8_t*, uint64_t, uint64_t, uint64_t, RowPlan,
+                                                uint64_t*, uint64_t, unsigned long long*, unsigned long long*, int);
 
 #define ATC_ROWS_INST(SEM, NS, I32, MASK)                                                                        \
   template __global__ void k_screen_rows<SEM, NS, I32, MASK>(TestsetView, SpecView, const uint8_t*, uint64_t,    \
