@@ -756,8 +756,11 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
           f2 += n_base + (n_ok_all - c_ok);
           if (!c_ok) continue;
           const int32_t hw = ch * cw;
-          if (q_rest >= hw) {  // UB: see the general path below
-            const int64_t alim = (int64_t)len_in + hw - q_rest;
+          const int64_t alim = (int64_t)len_in + hw - q_rest;
+          // UB (see the general path below) takes pairs only if the largest remaining
+          // product p = s_prod[r_ok - 1] exceeds floor((alim - 1) / hw), i.e. p*hw >= alim
+          // — tested without a division (the usual answer is no)
+          if (q_rest >= hw && (alim <= 0 || (int64_t)s_prod[r_ok - 1] * hw >= alim)) {
             const uint32_t am1 = (uint32_t)(alim - 1);
             const int ru = alim <= 0 ? 0 : gt_rank(lut_n ? div_capn(am1, hw, rhw[hd], qcap) : (int)(am1 / (uint32_t)hw));
             if (ru < r_ok) {
