@@ -116,7 +116,8 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
       const int lut_n = pmax < 4096 ? (int)pmax + 1 : 0;
       const size_t nI2 = (size_t)ts->nI * ts->nI;
       const size_t smem = ((size_t)16 << ts->nI) + (size_t)(lut_n + 15) / 16 * 16 +
-                          ((size_t)ts->nP * nI2 + 15) / 16 * 16 + nI2 * sizeof(float);
+                          ((size_t)ts->nP * nI2 + 15) / 16 * 16 + (nI2 + 3) / 4 * 4 * sizeof(float) +
+                          (size_t)ts->nP * nI2 * 16 + (size_t)ts->nP * ts->nI * 4;
       // one wave of 1024 / kPairThreads CTAs per SM (64 registers): each CTA builds its tables once
       const uint64_t cubes = rows / ts->nI + 2;
       const unsigned g3 = std::min<unsigned>((unsigned)((cubes + kPairThreads - 1) / kPairThreads),
@@ -502,6 +503,7 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
     // (perm, h, w, r, s) over the values of tc_c (key stride 1), for output
     // positions 0 and 1
     const bool pairs = e.use_rows && ts_i32(ts) && conv_thresholds_ok(ctx, sp, e.plan, ts->nI) && ts->nI <= 11 &&
+                       ts->nP <= 8 /* k_screen_conv_pairs' tables within 64 KB of shared memory */ &&
                        e.plan.key_stride[1] == 1 && !pairs_disabled(ctx);
     uint8_t* tab = (uint8_t*)atc_ctx_scratch(ctx, 17, e.table_bytes * (pairs ? 2 : 1) + 32);
     if (!tab) {

@@ -614,6 +614,11 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
   const int nP = ts.nP;
   uint8_t* s_ainr = s_rank + (lut_n + 15) / 16 * 16;
   float* s_rhw = reinterpret_cast<float*>(s_ainr + (nP * nI2 + 15) / 16 * 16);
+  // the rank-count fast path's plane table per (in region, w digit, h digit):
+  // {h*w, largest product of rank < ra, ra | skip << 16, 0} and, per (in region, w
+  // digit), the dispatch failures of the cube's planes summed over h
+  int4* s_pl = reinterpret_cast<int4*>(s_rhw + (nI2 + 3) / 4 * 4);
+  uint32_t* s_f2sum = reinterpret_cast<uint32_t*>(s_pl + nP * nI2);
   for (int i = threadIdx.x; i < nP * nI2; i += blockDim.x) {
     const int p = i / nI2, wh = i - p * nI2, wd = wh / nI, hd = wh - wd * nI;
     const int64_t hw = (int64_t)s_u[hd] * s_u[wd];
@@ -668,6 +673,19 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
   const uint32_t rows_all = (1u << nI) - 1u;
   __syncthreads();
   const unsigned int n_base = (unsigned int)(nI2 - s_cnt[nI2]);  // pairs with x < 1 or c < 1
+  for (int i = threadIdx.x; i < nP * nI2; i += blockDim.x) {
+    const int wh = i % nI2, wd = wh / nI, hd = wh - wd * nI;
+    const int ra = s_ainr[i];
+    const bool skip = s_u[hd] < 1 || s_cnt[ra] == 0;
+    s_pl[i] = make_int4(s_u[hd] * s_u[wd], ra >= 1 ? s_prod[ra - 1] : 0, ra | (skip ? 1 << 16 : 0), 0);
+  }
+  for (int i = threadIdx.x; i < nP * nI; i += blockDim.x) {
+    uint32_t f = 0;
+    for (int hd = 0; hd < nI; ++hd)
+      f += s_u[hd] < 1 ? (uint32_t)nI2 : n_base + (s_cnt[nI2] - s_cnt[s_ainr[i * nI + hd]]);
+    s_f2sum[i] = f;
+  }
+  __syncthreads();
   const uint32_t magic = (uint32_t)(0xFFFFFFFFull / (uint32_t)nI) + 1u;  // n / nI = umulhi(n, magic), n < 2^27
   unsigned int cnt1 = 0, cnt2 = 0, cnt3 = 0, cnt4 = 0;
   // whole cubes inside [begin, end): mismatches are counted as the remainder
@@ -741,30 +759,29 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
       const uint8_t* ainr = s_ainr + ((uint32_t)p_in * nI + digit[3]) * nI;
       const float* rhw = s_rhw + digit[3] * nI;
       if (c_max >= umax && d_out >= umax) {  // cube_dm = x < 1 | c < 1: the rank-count form
-        const unsigned int n_ok_all = s_cnt[nI2];
+        // the in-extent dispatch failures of every plane: one table sum; per plane the
+        // table row {h*w, largest product of rank < ra, ra, skip} (skip: h < 1, or no
+        // pair left), the UB test and the position-0/1 verdicts of the c rows
+        const uint32_t tix = (uint32_t)p_in * nI + digit[3];
+        f2 += s_f2sum[tix];
+        const int4* pl = s_pl + tix * nI;
+        const uint32_t* cm = plan.cmask + ckey0;
 #pragma unroll
         for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
-          // the plane's position-0/1 verdicts over the c rows, loaded first (used last)
-          const uint32_t cw2 = __ldg(plan.cmask + ckey0 + (uint32_t)hd * cks[2]) & sel;
-          const int32_t ch = s_u[hd];
-          if (!all_pos && ch < 1) {
-            f2 += (unsigned int)nI2;
-            continue;
-          }
-          int r_ok = ainr[hd];  // pairs of rank >= ra fail the in-extent check
-          const unsigned int c_ok = s_cnt[r_ok];
-          f2 += n_base + (n_ok_all - c_ok);
-          if (!c_ok) continue;
-          const int32_t hw = ch * cw;
+          const uint32_t cw2 = __ldg(cm + (uint32_t)hd * cks[2]) & sel;
+          const int4 t = pl[hd];
+          if (t.z >> 16) continue;
+          int r_ok = t.z & 0xFFFF;
+          const int32_t hw = t.x;
           const int64_t alim = (int64_t)len_in + hw - q_rest;
           // UB (see the general path below) takes pairs only if the largest remaining
-          // product p = s_prod[r_ok - 1] exceeds floor((alim - 1) / hw), i.e. p*hw >= alim
-          // — tested without a division (the usual answer is no)
-          if (q_rest >= hw && (alim <= 0 || (int64_t)s_prod[r_ok - 1] * hw >= alim)) {
+          // product p exceeds floor((alim - 1) / hw), i.e. p*hw >= alim — tested without
+          // a division (the usual answer is no)
+          if (q_rest >= hw && (alim <= 0 || (int64_t)t.y * hw >= alim)) {
             const uint32_t am1 = (uint32_t)(alim - 1);
             const int ru = alim <= 0 ? 0 : gt_rank(lut_n ? div_capn(am1, hw, rhw[hd], qcap) : (int)(am1 / (uint32_t)hw));
             if (ru < r_ok) {
-              f4 += c_ok - s_cnt[ru];
+              f4 += s_cnt[r_ok] - s_cnt[ru];
               r_ok = ru;
               if (!s_cnt[ru]) continue;
             }
