@@ -615,8 +615,10 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
   uint8_t* s_ainr = s_rank + (lut_n + 15) / 16 * 16;
   float* s_rhw = reinterpret_cast<float*>(s_ainr + (nP * nI2 + 15) / 16 * 16);
   // the rank-count fast path's plane table per (in region, w digit, h digit):
-  // {h*w, largest product of rank < ra, ra | skip << 16, 0} and, per (in region, w
-  // digit), the dispatch failures of the cube's planes summed over h
+  // {h*w, v, ra, 0} and, per (in region, w digit), the dispatch failures of the cube's
+  // planes summed over h.  v = h*w*(p - 1) with p the largest product of rank < ra
+  // (clamped at 0): a plane has UB pairs only if v + Q' >= len(in) (below); planes
+  // with h < 1 or no pair left get v = -2^30 (never)
   int4* s_pl = reinterpret_cast<int4*>(s_rhw + (nI2 + 3) / 4 * 4);
   uint32_t* s_f2sum = reinterpret_cast<uint32_t*>(s_pl + nP * nI2);
   for (int i = threadIdx.x; i < nP * nI2; i += blockDim.x) {
@@ -677,7 +679,8 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
     const int wh = i % nI2, wd = wh / nI, hd = wh - wd * nI;
     const int ra = s_ainr[i];
     const bool skip = s_u[hd] < 1 || s_cnt[ra] == 0;
-    s_pl[i] = make_int4(s_u[hd] * s_u[wd], ra >= 1 ? s_prod[ra - 1] : 0, ra | (skip ? 1 << 16 : 0), 0);
+    const int32_t hw = s_u[hd] * s_u[wd], pm = ra >= 1 ? max(s_prod[ra - 1], 0) : 0;
+    s_pl[i] = make_int4(hw, skip ? -(1 << 30) : hw * (pm - 1), ra, 0);
   }
   for (int i = threadIdx.x; i < nP * nI; i += blockDim.x) {
     uint32_t f = 0;
@@ -758,7 +761,7 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
       }
       const uint8_t* ainr = s_ainr + ((uint32_t)p_in * nI + digit[3]) * nI;
       const float* rhw = s_rhw + digit[3] * nI;
-      if (c_max >= umax && d_out >= umax) {  // cube_dm = x < 1 | c < 1: the rank-count form
+      if (c_max >= umax && d_out >= umax && lut_n) {  // cube_dm = x < 1 | c < 1: the rank-count form
         // the in-extent dispatch failures of every plane: one table sum; per plane the
         // table row {h*w, largest product of rank < ra, ra, skip} (skip: h < 1, or no
         // pair left), the UB test and the position-0/1 verdicts of the c rows
@@ -766,18 +769,19 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
         f2 += s_f2sum[tix];
         const int4* pl = s_pl + tix * nI;
         const uint32_t* cm = plan.cmask + ckey0;
+        const uint32_t ck2 = cks[2];
 #pragma unroll
-        for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
-          const uint32_t cw2 = __ldg(cm + (uint32_t)hd * cks[2]) & sel;
+        for (int hd = 0; hd < nI; ++hd, cm += ck2) {  // digit 2: tc_h
+          const uint32_t cw2 = __ldg(cm) & sel;
           const int4 t = pl[hd];
-          if (t.z >> 16) continue;
-          int r_ok = t.z & 0xFFFF;
-          const int32_t hw = t.x;
-          const int64_t alim = (int64_t)len_in + hw - q_rest;
+          int r_ok = t.z;
           // UB (see the general path below) takes pairs only if the largest remaining
-          // product p exceeds floor((alim - 1) / hw), i.e. p*hw >= alim — tested without
-          // a division (the usual answer is no)
-          if (q_rest >= hw && (alim <= 0 || (int64_t)t.y * hw >= alim)) {
+          // product p exceeds floor((alim - 1) / hw), alim = len(in) + hw - Q', i.e. if
+          // p*hw >= alim: v + Q' >= len(in) (32-bit: products < 4096 with lut_n; p*hw <=
+          // len(in) by the in-extent check, so there is none when Q' < hw)
+          if (t.y + q_rest >= (int32_t)len_in) {
+            const int32_t hw = t.x;
+            const int64_t alim = (int64_t)len_in + hw - q_rest;
             const uint32_t am1 = (uint32_t)(alim - 1);
             const int ru = alim <= 0 ? 0 : gt_rank(lut_n ? div_capn(am1, hw, rhw[hd], qcap) : (int)(am1 / (uint32_t)hw));
             if (ru < r_ok) {
