@@ -117,7 +117,9 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
       const size_t nI2 = (size_t)ts->nI * ts->nI;
       const size_t smem = ((size_t)16 << ts->nI) + (size_t)(lut_n + 15) / 16 * 16 +
                           ((size_t)ts->nP * nI2 + 15) / 16 * 16 + (nI2 + 3) / 4 * 4 * sizeof(float) +
-                          (size_t)ts->nP * nI2 * 16 + (size_t)ts->nP * ts->nI * 4;
+                          (size_t)ts->nP * nI2 * 16 + (size_t)ts->nP * ts->nI * 4 +
+                          (ts->nI == 9 ? ((size_t)ts->nP * nI2 * ts->nI + 15) / 16 * 16 + (size_t)ts->nP * nI2 * ts->nI * 2
+                                       : 0);  // the nI = 9 instance's cube-bound tables
       // one wave of 1024 / kPairThreads CTAs per SM (64 registers): each CTA builds its tables once
       const uint64_t cubes = rows / ts->nI + 2;
       const unsigned g3 = std::min<unsigned>((unsigned)((cubes + kPairThreads - 1) / kPairThreads),

@@ -501,6 +501,17 @@ __device__ __forceinline__ void set_bit(M128& m, int b) {
 
 constexpr int kPairMaxInts = 11;  // nI^2 <= 121 bits
 
+// floor(n / d) for n < 2^31 and 1 <= d < 2^31 from (m, s): m = ceil(2^(31 + s) / d)
+// with s = ceil(log2 d) is < 2^32 and leaves an error below 2^-s <= 1/d, so the
+// floor is exact; d = 1 is m = 0
+__device__ __forceinline__ uint32_t mdiv(uint32_t n, uint32_t m, uint32_t sh) { return m ? __umulhi(n, m) >> sh : n; }
+__device__ __forceinline__ void mdiv_consts(uint32_t d, uint32_t& m, uint32_t& sh) {
+  uint32_t s = 0;
+  while ((1ull << s) < d) ++s;
+  m = d <= 1 ? 0u : (uint32_t)(((1ull << (31 + s)) + d - 1) / d);
+  sh = s ? s - 1 : 0;
+}
+
 // min(floor(a / b), cap) for 0 <= a < 2^32, 1 <= b, cap <= 65536, rb ~= 1/b (exact)
 __device__ __forceinline__ int div_capn(uint32_t a, uint32_t b, float rb, int cap) {
   if ((uint64_t)a >= (uint64_t)b * (uint32_t)cap) return cap;
@@ -621,6 +632,28 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
   // with h < 1 or no pair left get v = -2^30 (never)
   int4* s_pl = reinterpret_cast<int4*>(s_rhw + (nI2 + 3) / 4 * 4);
   uint32_t* s_f2sum = reinterpret_cast<uint32_t*>(s_pl + nP * nI2);
+  // NIc instances: the cube's h-free dispatch bounds as tables over (region, k, r, s)
+  // — c_max = min(len(wt) / (k*r*s), kGtCap) — and (region, k, oh, ow) — d_out =
+  // min(len(out) / (k*oh*ow), kGtCap) | mth << 8, mth the same of dirty_max(out)
+  const int nI3i = nI2 * nI;
+  uint8_t* s_cmax = reinterpret_cast<uint8_t*>(s_f2sum + nP * nI);
+  uint16_t* s_dout = reinterpret_cast<uint16_t*>(s_cmax + (NIc ? (nP * nI3i + 15) / 16 * 16 : 0));
+  if (NIc) {
+    for (int i = threadIdx.x; i < nP * nI3i; i += blockDim.x) {
+      const int p = i / nI3i, r = i - p * nI3i, a = r / nI2, b = (r / nI) % nI, c = r % nI;  // digits (k, r|oh, s|ow)
+      const int64_t e = (int64_t)s_u[a] * s_u[b] * s_u[c];
+      uint8_t cm = 0;
+      uint16_t dd = 0;
+      if (s_u[a] >= 1 && s_u[b] >= 1 && s_u[c] >= 1) {
+        const float re = __frcp_rn((float)e);
+        cm = (uint8_t)div_cap((int64_t)ts.region_len[p], e, re);
+        const int dmax = ts.dirty_max[p];
+        dd = (uint16_t)(div_cap((int64_t)ts.region_len[p], e, re) | (dmax < 0 ? 0 : div_cap(dmax, e, re)) << 8);
+      }
+      s_cmax[i] = cm;
+      s_dout[i] = dd;
+    }
+  }
   for (int i = threadIdx.x; i < nP * nI2; i += blockDim.x) {
     const int p = i / nI2, wh = i - p * nI2, wd = wh / nI, hd = wh - wd * nI;
     const int64_t hw = (int64_t)s_u[hd] * s_u[wd];
@@ -698,6 +731,9 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
   const uint64_t nI3 = (uint64_t)nI2 * nI;
   const uint64_t cubes_per_perm = s_div[2];
   const uint64_t cube_lo = s_div[3], cube_hi = s_div[4];
+  uint32_t pm_m = 0, pm_sh = 0;  // cube / cubes_per_perm by multiply when both are < 2^31
+  const bool pm_fast = cube_hi < (1ull << 31) && cubes_per_perm < (1ull << 31);
+  if (pm_fast) mdiv_consts((uint32_t)cubes_per_perm, pm_m, pm_sh);
   for (uint64_t cb = cube_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; cb < cube_hi;
        cb += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t c0b = cb * nI3;
@@ -706,9 +742,7 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
       cnt3 += (unsigned int)(hi - lo);
       continue;
     }
-    const uint64_t perm = (cb >> 32) == 0 && (cubes_per_perm >> 32) == 0
-                              ? (uint64_t)((uint32_t)cb / (uint32_t)cubes_per_perm)
-                              : cb / cubes_per_perm;
+    const uint64_t perm = pm_fast ? (uint64_t)mdiv((uint32_t)cb, pm_m, pm_sh) : cb / cubes_per_perm;
     int digit[NS];
     {
       uint64_t s = cb - perm * cubes_per_perm;  // digits 3..8
@@ -736,17 +770,21 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
     // region lengths are < 2^31 (atc_testsets_upload): 32-bit divisions
     const uint32_t len_in = (uint32_t)ts.region_len[p_in], len_w = (uint32_t)ts.region_len[p_w];
     const uint32_t len_out = (uint32_t)ts.region_len[p_out];
-    const int32_t krs = ck * cr * cs, ext_out = ck * coh * cow;
-    const float r_out = __frcp_rn((float)ext_out);
     int c_max = 0, d_out = 0, mth = 0;
-    if (!cube_bad) {
+    if (NIc) {  // tables (0 where a digit is < 1: cube_bad)
+      const uint32_t k4 = (uint32_t)digit[4] * nI2;
+      c_max = s_cmax[(uint32_t)p_w * nI3i + k4 + digit[5] * nI + digit[6]];
+      const uint32_t dd = s_dout[(uint32_t)p_out * nI3i + k4 + digit[7] * nI + digit[8]];
+      d_out = dd & 0xFF;
+      mth = dd >> 8;
+    } else if (!cube_bad) {
+      const int32_t krs = ck * cr * cs, ext_out = ck * coh * cow;
+      const float r_out = __frcp_rn((float)ext_out);
       c_max = div_cap(len_w, krs, __frcp_rn((float)krs));
       d_out = div_cap(len_out, ext_out, r_out);
       const int dmax = ts.dirty_max[p_out];
       mth = dmax < 0 ? 0 : div_cap(dmax, ext_out, r_out);
     }
-    const M128 cube_dm = x_lt1 | c_lt1 | s_gtc[c_max] | s_gtx[d_out];  // h-free dispatch failures
-    const M128 dirty_fail = ~s_gtx[mth];
     const int32_t q_rest = (coh + cr - 2) * cw + (cow + cs - 2);   // Q = -h*w + q_rest
     uint32_t ckey0 = (uint32_t)perm * cperm;
 #pragma unroll
@@ -792,7 +830,7 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
           }
           const uint32_t rows_bad = (cw2 | cw2 >> 16) & 0xFFFFu;
           if (rows_bad == rows_all) continue;  // every c row mismatches at position 0 or 1 (the usual case)
-          const M128 ok = s_okm[r_ok] & ~(dirty_fail | s_rowx[rows_bad]);
+          const M128 ok = s_okm[r_ok] & ~(~s_gtx[mth] | s_rowx[rows_bad]);
           if (any(ok)) {
             const unsigned int k = popc(ok);
             f_surv += k;
@@ -806,6 +844,8 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
         }
         continue;
       }
+      const M128 cube_dm = x_lt1 | c_lt1 | s_gtc[c_max] | s_gtx[d_out];  // h-free dispatch failures
+      const M128 dirty_fail = ~s_gtx[mth];
       for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
         const int32_t ch = s_u[hd];
         if (ch < 1) {
@@ -842,6 +882,8 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
       }
       continue;
     }
+    const M128 cube_dm = x_lt1 | c_lt1 | s_gtc[c_max] | s_gtx[d_out];  // h-free dispatch failures
+    const M128 dirty_fail = ~s_gtx[mth];
     for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
       const uint64_t p0 = c0b + (uint64_t)hd * nI2;
       if (p0 + nI2 <= begin || p0 >= end) continue;
