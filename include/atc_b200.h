@@ -125,7 +125,7 @@ const char* atc_last_error(const atc_ctx* ctx);
 /* Per-context options — kernel-variant selection for A/B parity checks and
  * measurements; the defaults are the production kernels. */
 enum { ATC_OPT_CONV_SCREEN = 0, ATC_OPT_TC_FLAGS = 1,
-       ATC_OPT_CONV_STREAMS = 2, /* 1..4: streams the conv chains of a sweep round-robin over    */
+       ATC_OPT_CONV_STREAMS = 2, /* 1..8: streams the conv chains of a sweep round-robin over    */
        ATC_OPT_SMALL_LOG2 = 3    /* gemm spaces of <= 2^value bindings run as one small-space
                                     sweep (k_sweep_small); 0 disables it                        */ };
 enum { ATC_CONV_SCREEN_AUTO = 0,    /* k_screen_conv_pairs where it applies      */

@@ -23,7 +23,7 @@ struct atc_ctx {
   // sweeps run conv spaces on the caller's stream and gemm spaces round-robin on
   // kSideStreams concurrent side streams; side stream k's evaluator scratch lives
   // at slot + 32 * (k + 1) (set while enqueueing it)
-  static constexpr int kSideStreams = 4;
+  static constexpr int kSideStreams = 8;
   static constexpr int kSlots = 32 * (kSideStreams + 1);
   int slot_base = 0;
   cudaStream_t side_stream[kSideStreams] = {};
@@ -59,7 +59,7 @@ struct atc_ctx {
   int opt_tc_flags = 0;
   int opt_small_log2 = 16;   // gemm spaces of <= 2^this bindings go to k_sweep_small (0: none;
                              // tools/small_threshold.py: 16 keeps config 4's 279,936 on its chain)
-  int opt_conv_streams = 4;  // streams the conv chains of a sweep round-robin over (tools/sweep_streams.py)
+  int opt_conv_streams = 8;  // streams the conv chains of a sweep round-robin over (tools/sweep_streams.py)
   bool tc_configured = false;  // k_tc_gemm* shared-memory attributes set on this context's device
   // every ABI entry point holds this for its whole call, so a context is
   // serialised (the pipeline's worker threads may share one)

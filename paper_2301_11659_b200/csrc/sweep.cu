@@ -66,8 +66,11 @@ constexpr uint64_t kSmallSurvCap = 1ull << 20;  // survivors of all small jobs t
 // stream 0; the conv spaces' chains (tables, K1, K2, finalize) round-robin over
 // ctx->opt_conv_streams streams (conv_stream, side streams 3, 2, 1: one space's
 // latency-bound tables and K2 run beside another's K1; 4 streams: 3.00 -> 2.32 ms
-// per corpus sweep, tools/sweep_streams.py); other large gemm ranges round-robin on
-// the remaining side streams.  Side stream k's scratch lives at slot + 32 * (k + 1);
+// per corpus sweep, tools/sweep_streams.py; 8 streams, one per corpus conv space,
+// after K1's instruction diet: 1.28 -> 1.06 ms); other large gemm ranges start on
+// side stream 0 behind the small sweep, then round-robin.  (Higher launch priority
+// for the tables / K2 / finalize kernels was measured too: K2 then interleaves with
+// the next K1s, 1.06 -> 1.11 ms — the step is K1-throughput bound.)  Side stream k's scratch lives at slot + 32 * (k + 1);
 // every branch forks from and joins back into `st`, so a captured graph has the
 // same branches.
 int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_uploads) {
@@ -110,7 +113,9 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
                                          b->small_cnt, (unsigned long long)kEnumChunkCap + 1);
     if (ctx->prof) ctx->prof_kernels += 3;
   }
-  int side_next = has_small ? 1 : 0, conv_next = 0;
+  // gemm chains start on side stream 0 behind the small-space sweep (short; the conv
+  // chains hold the other side streams), then round-robin
+  int side_next = 0, conv_next = 0;
   int rc = ATC_OK;
   for (int j = 0; j < b->n && rc == ATC_OK; ++j) {
     if (!active(j)) continue;
@@ -130,7 +135,7 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
       }
     } else if (split) {
       sk = side_next;
-      side_next = side_next + 1 < atc_ctx::kSideStreams ? side_next + 1 : (has_small ? 1 : 0);
+      side_next = side_next + 1 < atc_ctx::kSideStreams ? side_next + 1 : 0;
     }
     const bool side = sk >= 0;
     cudaStream_t js = side ? ctx->side_stream[sk] : split ? ctx->conv_stream : st;

@@ -14,7 +14,7 @@ from paper_2301_11659_b200.evaluator import Evaluator  # noqa: E402
 jobs = workloads.corpus_jobs()
 full = lambda js: [(j.spec, j.ts, j.space, 0, j.space.count) for j in js]  # noqa: E731
 out, ref = {}, None
-for streams in (1, 2, 3, 4):
+for streams in (1, 2, 4, 6, 8):
     ctx = _lib.Context(0)
     ctx.set_option(_lib.OPT_CONV_STREAMS, streams)
     stream = torch.cuda.Stream()
