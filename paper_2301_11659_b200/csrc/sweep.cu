@@ -70,9 +70,9 @@ constexpr uint64_t kSmallSurvCap = 1ull << 20;  // survivors of all small jobs t
 // after K1's instruction diet: 1.28 -> 1.06 ms); other large gemm ranges start on
 // side stream 0 behind the small sweep, then round-robin.  (Higher launch priority
 // for the tables / K2 / finalize kernels was measured too: K2 then interleaves with
-// the next K1s, 1.06 -> 1.11 ms — the step is K1-throughput bound.)  Side stream k's scratch lives at slot + 32 * (k + 1);
-// every branch forks from and joins back into `st`, so a captured graph has the
-// same branches.
+// the next K1s, 1.06 -> 1.11 ms — the step is K1-throughput bound.)  Side stream
+// k's scratch lives at slot + 32 * (k + 1); every branch forks from and joins back
+// into `st`, so a captured graph has the same branches.
 int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_uploads) {
   const uint64_t chunk_cap = kEnumChunkCap;
   unsigned long long* hist = reinterpret_cast<unsigned long long*>(b->res + (size_t)b->n * kBatchStride);
