@@ -560,6 +560,10 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
     s_div[2] = planes_per_perm / (uint64_t)nI;    // cubes per permutation
     s_div[3] = begin / nI3;                       // first cube
     s_div[4] = (end + nI3 - 1) / nI3;             // one past the last cube
+    uint32_t m = 0, sh = 0;
+    if (s_div[2] < (1ull << 31)) mdiv_consts((uint32_t)s_div[2], m, sh);
+    s_div[5] = m;
+    s_div[6] = sh;
   }
   if (threadIdx.x >= 64 && threadIdx.x < 64 + NS) {
     const int q = threadIdx.x - 64;
@@ -626,10 +630,10 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
   uint8_t* s_ainr = s_rank + (lut_n + 15) / 16 * 16;
   float* s_rhw = reinterpret_cast<float*>(s_ainr + (nP * nI2 + 15) / 16 * 16);
   // the rank-count fast path's plane table per (in region, w digit, h digit):
-  // {h*w, v, ra, 0} and, per (in region, w digit), the dispatch failures of the cube's
+  // {h*w, v, ra, skip rows} and, per (in region, w digit), the dispatch failures of the cube's
   // planes summed over h.  v = h*w*(p - 1) with p the largest product of rank < ra
   // (clamped at 0): a plane has UB pairs only if v + Q' >= len(in) (below); planes
-  // with h < 1 or no pair left get v = -2^30 (never)
+  // with h < 1 or no pair left get v = -2^30 (never) and every c row marked bad
   int4* s_pl = reinterpret_cast<int4*>(s_rhw + (nI2 + 3) / 4 * 4);
   uint32_t* s_f2sum = reinterpret_cast<uint32_t*>(s_pl + nP * nI2);
   // NIc instances: the cube's h-free dispatch bounds as tables over (region, k, r, s)
@@ -713,7 +717,7 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
     const int ra = s_ainr[i];
     const bool skip = s_u[hd] < 1 || s_cnt[ra] == 0;
     const int32_t hw = s_u[hd] * s_u[wd], pm = ra >= 1 ? max(s_prod[ra - 1], 0) : 0;
-    s_pl[i] = make_int4(hw, skip ? -(1 << 30) : hw * (pm - 1), ra, 0);
+    s_pl[i] = make_int4(hw, skip ? -(1 << 30) : hw * (pm - 1), ra, skip ? (1 << nI) - 1 : 0);
   }
   for (int i = threadIdx.x; i < nP * nI; i += blockDim.x) {
     uint32_t f = 0;
@@ -731,9 +735,9 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
   const uint64_t nI3 = (uint64_t)nI2 * nI;
   const uint64_t cubes_per_perm = s_div[2];
   const uint64_t cube_lo = s_div[3], cube_hi = s_div[4];
-  uint32_t pm_m = 0, pm_sh = 0;  // cube / cubes_per_perm by multiply when both are < 2^31
+  // cube / cubes_per_perm by multiply when both are < 2^31 (constants: s_div[5], [6])
   const bool pm_fast = cube_hi < (1ull << 31) && cubes_per_perm < (1ull << 31);
-  if (pm_fast) mdiv_consts((uint32_t)cubes_per_perm, pm_m, pm_sh);
+  const uint32_t pm_m = (uint32_t)s_div[5], pm_sh = (uint32_t)s_div[6];
   for (uint64_t cb = cube_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; cb < cube_hi;
        cb += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t c0b = cb * nI3;
@@ -806,18 +810,33 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
         const uint32_t tix = (uint32_t)p_in * nI + digit[3];
         f2 += s_f2sum[tix];
         const int4* pl = s_pl + tix * nI;
-        const uint32_t* cm = plan.cmask + ckey0;
+        const uint32_t* cm0 = plan.cmask + ckey0;
         const uint32_t ck2 = cks[2];
+        // branch-free pass over the planes: a bit per plane that needs a closer look —
+        // UB pairs possible (v >= len(in) - Q': p*hw >= alim, see below) or a c row
+        // without a position-0/1 mismatch (skip planes: t.w = every row, never)
+        const int32_t lq = (int32_t)len_in - q_rest;
+        uint32_t need = 0;
+        {
+          const uint32_t* cm = cm0;
 #pragma unroll
-        for (int hd = 0; hd < nI; ++hd, cm += ck2) {  // digit 2: tc_h
-          const uint32_t cw2 = __ldg(cm) & sel;
+          for (int hd = 0; hd < nI; ++hd, cm += ck2) {  // digit 2: tc_h
+            const uint32_t cw2 = __ldg(cm) & sel;
+            const int4 t = pl[hd];
+            const uint32_t rb = (cw2 | cw2 >> 16 | (uint32_t)t.w) & 0xFFFFu;
+            need |= (t.y >= lq || rb != rows_all ? 1u : 0u) << hd;
+          }
+        }
+        while (need) {
+          const int hd = __ffs(need) - 1;
+          need &= need - 1;
           const int4 t = pl[hd];
           int r_ok = t.z;
           // UB (see the general path below) takes pairs only if the largest remaining
           // product p exceeds floor((alim - 1) / hw), alim = len(in) + hw - Q', i.e. if
           // p*hw >= alim: v + Q' >= len(in) (32-bit: products < 4096 with lut_n; p*hw <=
           // len(in) by the in-extent check, so there is none when Q' < hw)
-          if (t.y + q_rest >= (int32_t)len_in) {
+          if (t.y >= lq) {
             const int32_t hw = t.x;
             const int64_t alim = (int64_t)len_in + hw - q_rest;
             const uint32_t am1 = (uint32_t)(alim - 1);
@@ -828,8 +847,9 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
               if (!s_cnt[ru]) continue;
             }
           }
+          const uint32_t cw2 = __ldg(cm0 + (uint32_t)hd * ck2) & sel;
           const uint32_t rows_bad = (cw2 | cw2 >> 16) & 0xFFFFu;
-          if (rows_bad == rows_all) continue;  // every c row mismatches at position 0 or 1 (the usual case)
+          if (rows_bad == rows_all) continue;  // every c row mismatches at position 0 or 1
           const M128 ok = s_okm[r_ok] & ~(~s_gtx[mth] | s_rowx[rows_bad]);
           if (any(ok)) {
             const unsigned int k = popc(ok);
