@@ -23,7 +23,7 @@ struct atc_ctx {
   // sweeps run conv spaces on the caller's stream and gemm spaces round-robin on
   // kSideStreams concurrent side streams; side stream k's evaluator scratch lives
   // at slot + 32 * (k + 1) (set while enqueueing it)
-  static constexpr int kSideStreams = 8;
+  static constexpr int kSideStreams = 10;
   static constexpr int kSlots = 32 * (kSideStreams + 1);
   int slot_base = 0;
   cudaStream_t side_stream[kSideStreams] = {};

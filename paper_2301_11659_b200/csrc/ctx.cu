@@ -264,7 +264,7 @@ int atc_set_option(atc_ctx* ctx, int32_t option, int32_t value) {
     ctx->opt_small_log2 = value;
     return ATC_OK;
   }
-  if (option == ATC_OPT_CONV_STREAMS && value >= 1 && value <= atc_ctx::kSideStreams) {
+  if (option == ATC_OPT_CONV_STREAMS && value >= 1 && value <= atc_ctx::kSideStreams - 2) {
     ctx->opt_conv_streams = value;
     return ATC_OK;
   }

@@ -67,8 +67,8 @@ constexpr uint64_t kSmallSurvCap = 1ull << 20;  // survivors of all small jobs t
 // ctx->opt_conv_streams streams (conv_stream, side streams 3, 2, 1: one space's
 // latency-bound tables and K2 run beside another's K1; 4 streams: 3.00 -> 2.32 ms
 // per corpus sweep, tools/sweep_streams.py; 8 streams, one per corpus conv space,
-// after K1's instruction diet: 1.28 -> 1.06 ms); other large gemm ranges start on
-// side stream 0 behind the small sweep, then round-robin.  (Higher launch priority
+// after K1's instruction diet: 1.28 -> 1.06 ms); other large gemm ranges round-robin
+// over side streams 1, 2, ... (in the corpus: one, on a stream of its own).  (Higher launch priority
 // for the tables / K2 / finalize kernels was measured too: K2 then interleaves with
 // the next K1s, 1.06 -> 1.11 ms — the step is K1-throughput bound.)  Side stream
 // k's scratch lives at slot + 32 * (k + 1); every branch forks from and joins back
@@ -113,12 +113,20 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
                                          b->small_cnt, (unsigned long long)kEnumChunkCap + 1);
     if (ctx->prof) ctx->prof_kernels += 3;
   }
-  // gemm chains start on side stream 0 behind the small-space sweep (short; the conv
-  // chains hold the other side streams), then round-robin
-  int side_next = 0, conv_next = 0;
+  // large gemm chains on side streams 1, 2, ... (0: the small-space sweep); the conv
+  // chains take side streams kSideStreams - 1, - 2, ... and conv_stream
+  int side_next = has_small ? 1 : 0, conv_next = 0;
   int rc = ATC_OK;
-  for (int j = 0; j < b->n && rc == ATC_OK; ++j) {
-    if (!active(j)) continue;
+  // gemm chains first: nodes are handed to the GPU in the order they were enqueued,
+  // and a gemm chain enqueued after the conv chains only gets SMs once the K1 CTAs
+  // (a whole SM each) have drained — its short latency-bound kernels then form the
+  // step's tail; enqueued first, they run beside the conv tables
+  std::vector<int> order;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int j = 0; j < b->n; ++j)
+      if (active(j) && (b->plans[j].sp.sem == ATC_SEM_CONV2D) == (pass == 1)) order.push_back(j);
+  for (size_t oi = 0; oi < order.size() && rc == ATC_OK; ++oi) {
+    const int j = order[oi];
     atc_enum_job& job = b->jobs[j];
     EnumPlan& e = b->plans[j];
     // conv spaces on the caller's stream and side stream 0 alternately when they
@@ -135,7 +143,7 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
       }
     } else if (split) {
       sk = side_next;
-      side_next = side_next + 1 < atc_ctx::kSideStreams ? side_next + 1 : 0;
+      side_next = side_next + 1 < atc_ctx::kSideStreams ? side_next + 1 : (has_small ? 1 : 0);
     }
     const bool side = sk >= 0;
     cudaStream_t js = side ? ctx->side_stream[sk] : split ? ctx->conv_stream : st;
