@@ -219,7 +219,7 @@ def _ncu(prefix: str) -> dict:
     for name in sorted((f for f in os.listdir(d) if f.endswith("_ncu_summary.json")), reverse=True):
         with open(os.path.join(d, name)) as f:
             for row in json.load(f):
-                if row["kernel"].startswith(prefix):
+                if prefix in row["kernel"]:
                     return dict(row, summary=name)
     return {}
 
