@@ -27,6 +27,9 @@ namespace atc {
 // larger CTAs (one per SM) pay that prologue fewer times
 constexpr int kPairThreads = 1024;
 
+// k_probe_regions CTA size: >= 312, one draw of the previous phase per thread
+constexpr int kProbeThreads = 320;
+
 
 constexpr int kMaxT = 64;
 constexpr int kMaxPtrs = 16;

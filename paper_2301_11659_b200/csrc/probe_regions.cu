@@ -33,24 +33,27 @@ __device__ __forceinline__ uint64_t temper(uint64_t y) {
 // One CTA per test t.  As a sequence, std::mt19937_64 is z[0..311] = the seeded
 // state and z[n + 312] = z[n + 156] ^ f(z[n], z[n + 1]) (f: the upper/lower-bit
 // merge, shift and matrix-A step of the twist), draw i = temper(z[312 + i]) — the
-// standard's twist computes exactly these words in place.  Step j computes the 156
-// words z[312 + 156j + q] (q < 156) at once from words of earlier steps, in a
-// 624-word ring (each step overwrites only words no later step reads), so one
-// barrier per 156 draws; steps whose draws fall in no region are not tempered.
+// standard's twist computes exactly these words in place.  Phase k computes the 312
+// words z[312 (k + 1) + q] from the previous phase's (156 threads, two words each:
+// z[n + 312] and z[n + 468]), in a 1024-word ring, while every thread q < 312 tempers,
+// converts and stores the previous phase's word q (draw 312 (k - 1) + q) — the
+// generator's sequential chain per phase is only the two twists, the per-draw work
+// is spread over 312 threads one phase behind; phases whose draws fall in no region
+// are not tempered.
 // need (optional, [T * nP]): generate only the first need[t * nP + p] elements of
-// region (t, p) — the steps stop at the last of them — and then, in the same CTA,
+// region (t, p) — the phases stop at the last of them — and then, in the same CTA,
 // scatter test t's final-minus-init entries (k_apply_diffs) and build its dirty
 // lists over those prefixes (k_build_dirty), diff_* and v's dirty arrays.
 // pre / pre_off (atc_testsets_upload_prefix): the prefixes come from the caller
 // (packed, entries [pre_off[i], pre_off[i+1]) for region i) instead of the stream.
-__global__ void __launch_bounds__(160) k_probe_regions(int T, int nP, const uint64_t* seeds, const uint64_t* skips,
-                                                       const int64_t* region_len, const int32_t* is_f32,
-                                                       const int64_t* region_off, const int64_t* need, double* init,
-                                                       double* fin, TestsetView v, const int64_t* diff_off,
-                                                       const int32_t* diff_pos, const double* diff_val,
-                                                       const double* pre, const int64_t* pre_off) {
-  constexpr int kRing = 2 * kN;
-  __shared__ uint64_t z[kRing];
+__global__ void __launch_bounds__(kProbeThreads) k_probe_regions(int T, int nP, const uint64_t* seeds,
+                                                                 const uint64_t* skips, const int64_t* region_len,
+                                                                 const int32_t* is_f32, const int64_t* region_off,
+                                                                 const int64_t* need, double* init, double* fin,
+                                                                 TestsetView v, const int64_t* diff_off,
+                                                                 const int32_t* diff_pos, const double* diff_val,
+                                                                 const double* pre, const int64_t* pre_off) {
+  __shared__ uint64_t z[1024];
   const int t = blockIdx.x;
   if (t >= T) return;
   const int q = threadIdx.x;
@@ -73,56 +76,90 @@ __global__ void __launch_bounds__(160) k_probe_regions(int T, int nP, const uint
       z[i] = x;
     }
   }
-  uint64_t lo[8], hi[8];
-  uint64_t end = 0;
+  // stream positions are < 2^32 (probe images of a few hundred thousand draws): 32-bit
+  // region windows [lo, lo + len) tested as (pos - lo) < len, offsets and f32 flags in
+  // registers
+  uint32_t lo[8], len[8];
+  int64_t off[8];
+  uint32_t f32m = 0, end = 0;
   const int np = pre ? 0 : nP < 8 ? nP : 8;
   for (int p = 0; p < np; ++p) {
-    lo[p] = skips[(size_t)t * nP + p];
-    hi[p] = lo[p] + (uint64_t)(need ? need[(size_t)t * nP + p] : region_len[p]);
-    end = hi[p] > end ? hi[p] : end;
+    lo[p] = (uint32_t)skips[(size_t)t * nP + p];
+    len[p] = (uint32_t)(need ? need[(size_t)t * nP + p] : region_len[p]);
+    off[p] = region_off[(size_t)t * nP + p];
+    f32m |= (is_f32[p] ? 1u : 0u) << p;
+    end = lo[p] + len[p] > end ? lo[p] + len[p] : end;
   }
+  // phase k emits the draws [312 (k - 1), 312 k): a bit per phase whose window meets a
+  // region (block-uniform), so the phases in between only twist
+  constexpr int kMaxPhases = 4096;
+  __shared__ uint32_t s_emit[kMaxPhases / 32];
+  const uint32_t n_phases = (end + 2 * kN - 1) / kN;  // the last one only emits
+  const bool bitmap = n_phases <= (uint32_t)kMaxPhases;
+  if (bitmap)
+    for (uint32_t w = q; w < (n_phases + 31) / 32; w += blockDim.x) {
+      uint32_t m = 0;
+      for (int b = 0; b < 32; ++b) {
+        const uint32_t k = w * 32 + b;
+        if (k == 0 || k >= n_phases) continue;
+        const uint32_t d0 = (k - 1) * kN;
+        bool any = false;
+        for (int p = 0; p < np; ++p) any = any || (d0 < lo[p] + len[p] && d0 + kN > lo[p]);
+        m |= (any ? 1u : 0u) << b;
+      }
+      s_emit[w] = m;
+    }
   __syncthreads();
-  auto wrap = [](int i) { return i >= kRing ? i - kRing : i; };  // i < 2 * kRing
   auto twist = [](uint64_t a, uint64_t b, uint64_t c) {  // z[n + 312] from z[n], z[n + 1], z[n + 156]
     const uint64_t y = (a & kUpper) | (b & kLower);
     return c ^ (y >> 1) ^ ((y & 1ull) ? kMatrixA : 0ull);
   };
-  auto emit = [&](uint64_t base, uint64_t w) {  // draw base + q of this step into the regions
-    bool any = false;  // block-uniform: does this step's window meet a region?
-    for (int p = 0; p < np; ++p) any = any || (base < hi[p] && base + kM > lo[p]);
-    if (!any || q >= kM) return;
-    const uint64_t pos = base + (uint64_t)q;
-    const uint64_t y = temper(w);
-    const double u = (double)(y >> 11) * 0x1.0p-53;
-    const double x0 = __dadd_rn(-1.0, __dmul_rn(u, 2.0));  // lo + u * (hi - lo), not contracted
-    for (int p = 0; p < np; ++p)
-      if (pos >= lo[p] && pos < hi[p]) {
-        const double x = is_f32[p] ? (double)__double2float_rn(x0) : x0;
-        const int64_t o = region_off[(size_t)t * nP + p] + (int64_t)(pos - lo[p]);
-        init[o] = x;
-        fin[o] = x;
-      }
-  };
-  // two steps per barrier: step B's thread q needs z[n + 156] and z[n + 157] (written two
-  // steps back, visible since the last barrier) and z[n + 312] = its own step-A word;
-  // only thread 155's z[n + 157] is step A's word of thread 0, which it recomputes
-  int r = 0;  // base % kRing
-  for (uint64_t base = 0; base < end; base += 2 * kM, r = wrap(r + 2 * kM)) {
-    uint64_t wa = 0, wb = 0;
-    if (q < kM) {
-      const int n = r + q;
-      const uint64_t zn156 = z[wrap(n + kM)];
-      wa = twist(z[wrap(n)], z[wrap(n + 1)], zn156);
-      const uint64_t zn157 = q == kM - 1 ? twist(z[wrap(r)], z[wrap(r + 1)], z[wrap(r + kM)]) : z[wrap(n + kM + 1)];
-      wb = twist(zn156, zn157, wa);
-      // the slots of z[n + 312] / z[n + 468] held z[n - 312] / z[n - 156]: read by
-      // neither step of this pair
-      z[wrap(n + kN)] = wa;
-      z[wrap(n + kN + kM)] = wb;
+  // word w of the sequence lives in slot w & 1023: a phase reads the previous phase's
+  // 312 words and writes its own 312; the emitting threads read the previous phase's
+  // words, so 624 live words < 1024
+  constexpr uint32_t kMask = 1023;
+  uint32_t k = 0;
+  for (uint32_t base = 0; base < end + kN; base += kN, ++k) {
+    if (base < end && q < kM) {
+      // words n = base + q: inputs z[n], z[n + 1], z[n + 156], z[n + 157] (the previous
+      // phase; z[base + 312] is this phase's word of thread 0, recomputed by thread 155)
+      const uint32_t n = base + q;
+      const uint64_t zn156 = z[(n + kM) & kMask];
+      const uint64_t wa = twist(z[n & kMask], z[(n + 1) & kMask], zn156);
+      const uint64_t zn157 = q == kM - 1 ? twist(z[base & kMask], z[(base + 1) & kMask], z[(base + kM) & kMask])
+                                         : z[(n + kM + 1) & kMask];
+      const uint64_t wb = twist(zn156, zn157, wa);
+      z[(n + kN) & kMask] = wa;
+      z[(n + kN + kM) & kMask] = wb;
     }
-    emit(base, wa);
-    emit(base + kM, wb);
-    __syncthreads();  // this pair's words visible to the next pair
+    bool any = false;  // the previous phase's draws base - 312 + q <-> word z[base + q]
+    if (k > 0) {
+      if (bitmap) {
+        any = (s_emit[k >> 5] >> (k & 31)) & 1u;
+      } else {
+        const uint32_t d0 = base - kN;
+        for (int p = 0; p < np; ++p) any = any || (d0 < lo[p] + len[p] && d0 + kN > lo[p]);
+      }
+    }
+    if (any && q < kN) {
+      const uint32_t pos = base - kN + (uint32_t)q;
+      int hit = -1;
+      for (int p = 0; p < np; ++p)
+        if (pos - lo[p] < len[p]) hit = p;
+      if (hit >= 0) {
+        const uint64_t y = temper(z[(base + q) & kMask]);
+        const double u = (double)(y >> 11) * 0x1.0p-53;
+        const double x0 = __dadd_rn(-1.0, __dmul_rn(u, 2.0));  // lo + u * (hi - lo), not contracted
+        for (int p = 0; p < np; ++p)
+          if (pos - lo[p] < len[p]) {  // (regions of a test do not overlap: one hit)
+            const double x = (f32m >> p) & 1u ? (double)__double2float_rn(x0) : x0;
+            const int64_t o = off[p] + (int64_t)(pos - lo[p]);
+            init[o] = x;
+            fin[o] = x;
+          }
+      }
+    }
+    __syncthreads();  // this phase's words visible; the previous phase's emitted
   }
   if (!need) return;
   for (int p = 0; p < nP; ++p) {  // final = init + the original run's writes

@@ -212,7 +212,7 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
       // needed_only: one kernel generates the prefixes, applies the diffs and builds
       // the dirty lists; else whole regions, then k_apply_diffs and k_build_dirty
       const int64_t* dn = sd->needed_only ? (const int64_t*)(h->seeded + o_need) : nullptr;
-      k_probe_regions<<<T, 160, 0, st>>>(T, nP, (const uint64_t*)(h->seeded + o_seeds),
+      k_probe_regions<<<T, kProbeThreads, 0, st>>>(T, nP, (const uint64_t*)(h->seeded + o_seeds),
                                          (const uint64_t*)(h->seeded + o_skips), v.region_len, v.is_f32,
                                          v.region_off, dn, init, fin, v, (const int64_t*)(h->seeded + o_doffs),
                                          (const int32_t*)(h->seeded + o_dps), (const double*)(h->seeded + o_dvs),

@@ -68,3 +68,33 @@ for _ in range(3):
 for name, fn in (("updates", updates), ("sweep", sweep.run), ("both", lambda: (updates(), sweep.run()))):
     ev_ms, host_ms, wall_ms = timed(fn)
     print(f"{name:8s} events {ev_ms:.3f} ms  host enqueue {host_ms:.3f} ms  wall {wall_ms:.3f} ms")
+
+# kernel timeline of one e2e step (CUPTI via torch.profiler): when the probe-image
+# regeneration ends and the sweep's kernels start
+import json as _json  # noqa: E402
+
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+    for _ in range(2):
+        updates()
+        sweep.run()
+        torch.cuda.synchronize()
+prof.export_chrome_trace("/tmp/atc_e2e_trace.json")
+evs = _json.load(open("/tmp/atc_e2e_trace.json"))["traceEvents"]
+ks = sorted([e for e in evs if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")], key=lambda e: e["ts"])
+half = len(ks) // 2
+ks = ks[half:]  # the second step
+t0 = ks[0]["ts"]
+from collections import defaultdict  # noqa: E402
+
+agg = defaultdict(lambda: [0, 0.0, 1e18, 0.0])
+for e in ks:
+    a = agg[e["name"].split("(")[0][:40]]
+    a[0] += 1
+    a[1] += e["dur"]
+    a[2] = min(a[2], e["ts"] - t0)
+    a[3] = max(a[3], e["ts"] + e["dur"] - t0)
+print(f"e2e step span {max(e['ts'] + e['dur'] for e in ks) - t0:.1f} us, {len(ks)} GPU ops")
+for name, (n, dur, first, last) in sorted(agg.items(), key=lambda kv: kv[1][2]):
+    print(f"{name:42s} n={n:3d} sum={dur:8.1f} us  first={first:8.1f}  last_end={last:8.1f}")
