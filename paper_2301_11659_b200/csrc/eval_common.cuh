@@ -27,8 +27,8 @@ namespace atc {
 // larger CTAs (one per SM) pay that prologue fewer times
 constexpr int kPairThreads = 1024;
 
-// k_probe_regions CTA size: >= 312, one draw of the previous phase per thread
-constexpr int kProbeThreads = 320;
+// k_probe_regions CTA size: 156 threads twist (5 warps)
+constexpr int kProbeThreads = 160;
 
 
 constexpr int kMaxT = 64;

@@ -35,11 +35,10 @@ __device__ __forceinline__ uint64_t temper(uint64_t y) {
 // merge, shift and matrix-A step of the twist), draw i = temper(z[312 + i]) — the
 // standard's twist computes exactly these words in place.  Phase k computes the 312
 // words z[312 (k + 1) + q] from the previous phase's (156 threads, two words each:
-// z[n + 312] and z[n + 468]), in a 1024-word ring, while every thread q < 312 tempers,
-// converts and stores the previous phase's word q (draw 312 (k - 1) + q) — the
-// generator's sequential chain per phase is only the two twists, the per-draw work
-// is spread over 312 threads one phase behind; phases whose draws fall in no region
-// are not tempered.
+// z[n + 312] and z[n + 468]) in a 1024-word ring, one barrier per phase; the draws of
+// phases that meet a region (a per-CTA bitmap) are tempered and stored by the same
+// threads.  (A variant with 312 more threads tempering the previous phase's draws
+// measured slower: the extra warps' per-phase overhead outweighs the shorter chain.)
 // need (optional, [T * nP]): generate only the first need[t * nP + p] elements of
 // region (t, p) — the phases stop at the last of them — and then, in the same CTA,
 // scatter test t's final-minus-init entries (k_apply_diffs) and build its dirty
@@ -90,19 +89,19 @@ __global__ void __launch_bounds__(kProbeThreads) k_probe_regions(int T, int nP, 
     f32m |= (is_f32[p] ? 1u : 0u) << p;
     end = lo[p] + len[p] > end ? lo[p] + len[p] : end;
   }
-  // phase k emits the draws [312 (k - 1), 312 k): a bit per phase whose window meets a
-  // region (block-uniform), so the phases in between only twist
+  // phase k computes the words of draws [312 k, 312 k + 312) (z[312 (k + 1) + i]); a bit
+  // per phase whose draws meet a region (block-uniform), so most phases only twist
   constexpr int kMaxPhases = 4096;
   __shared__ uint32_t s_emit[kMaxPhases / 32];
-  const uint32_t n_phases = (end + 2 * kN - 1) / kN;  // the last one only emits
+  const uint32_t n_phases = (end + kN - 1) / kN;
   const bool bitmap = n_phases <= (uint32_t)kMaxPhases;
   if (bitmap)
     for (uint32_t w = q; w < (n_phases + 31) / 32; w += blockDim.x) {
       uint32_t m = 0;
       for (int b = 0; b < 32; ++b) {
         const uint32_t k = w * 32 + b;
-        if (k == 0 || k >= n_phases) continue;
-        const uint32_t d0 = (k - 1) * kN;
+        if (k >= n_phases) continue;
+        const uint32_t d0 = k * kN;
         bool any = false;
         for (int p = 0; p < np; ++p) any = any || (d0 < lo[p] + len[p] && d0 + kN > lo[p]);
         m |= (any ? 1u : 0u) << b;
@@ -114,13 +113,24 @@ __global__ void __launch_bounds__(kProbeThreads) k_probe_regions(int T, int nP, 
     const uint64_t y = (a & kUpper) | (b & kLower);
     return c ^ (y >> 1) ^ ((y & 1ull) ? kMatrixA : 0ull);
   };
-  // word w of the sequence lives in slot w & 1023: a phase reads the previous phase's
-  // 312 words and writes its own 312; the emitting threads read the previous phase's
-  // words, so 624 live words < 1024
+  auto emit = [&](uint32_t pos, uint64_t w) {  // draw pos -> its region element, if any
+    for (int p = 0; p < np; ++p)
+      if (pos - lo[p] < len[p]) {  // (regions of a test do not overlap: one hit)
+        const uint64_t y = temper(w);
+        const double u = (double)(y >> 11) * 0x1.0p-53;
+        const double x0 = __dadd_rn(-1.0, __dmul_rn(u, 2.0));  // lo + u * (hi - lo), not contracted
+        const double x = (f32m >> p) & 1u ? (double)__double2float_rn(x0) : x0;
+        const int64_t o = off[p] + (int64_t)(pos - lo[p]);
+        init[o] = x;
+        fin[o] = x;
+      }
+  };
+  // word w of the sequence lives in slot w & 1023 (a phase reads the previous phase's
+  // 312 words and writes its own 312)
   constexpr uint32_t kMask = 1023;
   uint32_t k = 0;
-  for (uint32_t base = 0; base < end + kN; base += kN, ++k) {
-    if (base < end && q < kM) {
+  for (uint32_t base = 0; base < end; base += kN, ++k) {
+    if (q < kM) {
       // words n = base + q: inputs z[n], z[n + 1], z[n + 156], z[n + 157] (the previous
       // phase; z[base + 312] is this phase's word of thread 0, recomputed by thread 155)
       const uint32_t n = base + q;
@@ -131,35 +141,19 @@ __global__ void __launch_bounds__(kProbeThreads) k_probe_regions(int T, int nP, 
       const uint64_t wb = twist(zn156, zn157, wa);
       z[(n + kN) & kMask] = wa;
       z[(n + kN + kM) & kMask] = wb;
-    }
-    bool any = false;  // the previous phase's draws base - 312 + q <-> word z[base + q]
-    if (k > 0) {
+      bool any;
       if (bitmap) {
         any = (s_emit[k >> 5] >> (k & 31)) & 1u;
       } else {
-        const uint32_t d0 = base - kN;
-        for (int p = 0; p < np; ++p) any = any || (d0 < lo[p] + len[p] && d0 + kN > lo[p]);
+        any = false;
+        for (int p = 0; p < np; ++p) any = any || (base < lo[p] + len[p] && base + kN > lo[p]);
+      }
+      if (any) {
+        emit(n, wa);
+        emit(n + kM, wb);
       }
     }
-    if (any && q < kN) {
-      const uint32_t pos = base - kN + (uint32_t)q;
-      int hit = -1;
-      for (int p = 0; p < np; ++p)
-        if (pos - lo[p] < len[p]) hit = p;
-      if (hit >= 0) {
-        const uint64_t y = temper(z[(base + q) & kMask]);
-        const double u = (double)(y >> 11) * 0x1.0p-53;
-        const double x0 = __dadd_rn(-1.0, __dmul_rn(u, 2.0));  // lo + u * (hi - lo), not contracted
-        for (int p = 0; p < np; ++p)
-          if (pos - lo[p] < len[p]) {  // (regions of a test do not overlap: one hit)
-            const double x = (f32m >> p) & 1u ? (double)__double2float_rn(x0) : x0;
-            const int64_t o = off[p] + (int64_t)(pos - lo[p]);
-            init[o] = x;
-            fin[o] = x;
-          }
-      }
-    }
-    __syncthreads();  // this phase's words visible; the previous phase's emitted
+    __syncthreads();  // this phase's words visible to the next
   }
   if (!need) return;
   for (int p = 0; p < nP; ++p) {  // final = init + the original run's writes

@@ -492,3 +492,36 @@ def test_eval_bindings_many_equals_single(ev):
     bad = (L.BindJob * 1)()
     bad[0].spec, bad[0].ts, bad[0].n_bindings = arr[0].spec, arr[0].ts, 4  # no maps
     assert L.lib().atc_eval_bindings_many(ev.ctx.handle, bad, 1, 0) == L.ATC_ERR_ARG and bad[0].status == L.ATC_ERR_ARG
+
+
+def test_seeded_update_many_batched(ev):
+    """atc_testsets_update_seeded_many over several distinct needed_only handles (the
+    batched path: one staging copy, k_copy_meta + k_probe_regions_many for all of them)
+    rewrites every handle exactly as a fresh evaluation of the new test sets sees it."""
+    import ctypes as C
+
+    stems = ["conv_direct", "naive_ld", "im2col_virtual", "naive_f32"]
+    progs = [fixtures.load(s) for s in stems]
+    bases = [p.testsets(16) for p in progs]
+    handles, holders = [], []
+    for p, base in zip(progs, bases):  # first contents: another int value at t = 2
+        h = _with_int(base, 2, 5).upload_seeded(ev.ctx, needed_only=True)
+        holder = p.testsets(16)
+        holder._handles[id(ev.ctx)] = h
+        handles.append(h)
+        holders.append(holder)
+    for rnd in range(2):  # twice: the second reuses the staging buffers
+        structs, keeps = zip(*[b.seeded_struct(needed_only=True) for b in bases])
+        arr = (L.SeededTestsets * len(structs))(*structs)
+        hp = (C.c_void_p * len(handles))(*[h.value for h in handles])
+        L.check(ev.ctx.handle, L.lib().atc_testsets_update_seeded_many(ev.ctx.handle, hp, arr, len(handles)))
+        for stem, p, base, holder in zip(stems, progs, bases, holders):
+            for sname in p.spec_names():
+                space, spec = p.space(sname), fixtures.spec(sname)
+                end = min(space.count, 1 << 22)
+                want = ev.eval_enumerated(spec, base, space, 0, end)
+                got = ev.eval_enumerated(spec, holder, space, 0, end)
+                np.testing.assert_array_equal(got[0], want[0])
+                assert got[1] == want[1] and got[2].tolist() == want[2].tolist(), (stem, sname, rnd)
+    for holder in holders:
+        holder._handles.clear()
