@@ -126,8 +126,10 @@ const char* atc_last_error(const atc_ctx* ctx);
  * measurements; the defaults are the production kernels. */
 enum { ATC_OPT_CONV_SCREEN = 0, ATC_OPT_TC_FLAGS = 1,
        ATC_OPT_CONV_STREAMS = 2, /* 1..8: streams the conv chains of a sweep round-robin over    */
-       ATC_OPT_SMALL_LOG2 = 3    /* gemm spaces of <= 2^value bindings run as one small-space
-                                    sweep (k_sweep_small); 0 disables it                        */ };
+       ATC_OPT_SMALL_LOG2 = 3,   /* gemm spaces of <= 2^value bindings run as one small-space
+                                    sweep (k_sweep_small); 0 disables it                        */
+       ATC_OPT_K2B_PARTS = 4     /* 1, 2, 4, 8: warps sharing one (binding, t) item of the conv
+                                    K2b confirmation                                             */ };
 enum { ATC_CONV_SCREEN_AUTO = 0,    /* k_screen_conv_pairs where it applies      */
        ATC_CONV_SCREEN_PLANES = 1,  /* k_screen_conv_planes instead of the pairs */
        ATC_CONV_SCREEN_GENERIC = 2  /* the generic k_screen_rows for conv        */ };

@@ -197,7 +197,7 @@ class GroupJob(C.Structure):
     ]
 
 
-OPT_CONV_SCREEN, OPT_TC_FLAGS, OPT_CONV_STREAMS, OPT_SMALL_LOG2 = 0, 1, 2, 3
+OPT_CONV_SCREEN, OPT_TC_FLAGS, OPT_CONV_STREAMS, OPT_SMALL_LOG2, OPT_K2B_PARTS = 0, 1, 2, 3, 4
 CONV_SCREEN_AUTO, CONV_SCREEN_PLANES, CONV_SCREEN_GENERIC = 0, 1, 2
 TC_NO_KSPLIT, TC_NO_2SM, TC_NO_TMA_STORE, TC_NO_PAIR, TC_NO_IM2COL, TC_B_KMAJOR, TC_NO_SWAP1X1 = 1, 2, 4, 8, 16, 32, 64
 TC_NO_B3D = 128

@@ -264,6 +264,10 @@ int atc_set_option(atc_ctx* ctx, int32_t option, int32_t value) {
     ctx->opt_small_log2 = value;
     return ATC_OK;
   }
+  if (option == ATC_OPT_K2B_PARTS && (value == 1 || value == 2 || value == 4 || value == 8)) {
+    ctx->opt_k2b_parts = value;
+    return ATC_OK;
+  }
   if (option == ATC_OPT_CONV_STREAMS && value >= 1 && value <= atc_ctx::kSideStreams - 2) {
     ctx->opt_conv_streams = value;
     return ATC_OK;

@@ -723,7 +723,7 @@ __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const Bin
         if (stop && (++steps & 3) == 0) {  // every fourth step: has another part decided it?
           int k = lane == 0 ? *(volatile const int32_t*)stop : kPassKey;
           k = __shfl_sync(0xffffffffu, k, 0);
-          if (k < fail_key(1, 0)) break;
+          if (k < fail_key(t + 1, 0)) break;  // failed at test <= t: this part cannot lower it
         }
         const double* inp[MO];
         const double* wtp[MO];
@@ -975,7 +975,8 @@ __global__ void __launch_bounds__(256) k_confirm_warp(TestsetView ts, SpecView s
     const uint32_t si = sel ? sel[item - tt * cnt] : (uint32_t)(item - tt * cnt);
     const int t = 1 + (int)tt;
     if (*(volatile int32_t*)(surv_keys + si) < fail_key(t, 0)) continue;  // failed at a lower t already
-    const int r = warp_verdict(ts, sp, src, surv[si], t, mode, lane, screened != 0, part, parts);
+    const int r = warp_verdict(ts, sp, src, surv[si], t, mode, lane, screened != 0, part, parts,
+                               parts > 1 ? surv_keys + si : nullptr);
     if (lane == 0 && r) atomicMin(&surv_keys[si], fail_key(t, r));
   }
 }

@@ -193,8 +193,11 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
   if (pre && !keys) {
     // enumerated ranges report reasons, not failing tests: t >= 1 first over every
     // pending survivor, then t = 0 only where it can change the reason (k_confirm_t0)
-    k_confirm_warp<<<g_t1, 256, 0, st>>>(ts->view, sp, src, surv, surv_cap, surv_keys, pend, next_cnt + 1,
-                                         ctx->mode, screened, 1);
+    // each (binding, t) item's outputs over opt_k2b_parts warps (the long checks of the
+    // few bindings that pass many tests set the kernel's tail)
+    const int kp = ctx->opt_k2b_parts;
+    k_confirm_warp<<<(unsigned)std::min<uint64_t>((uint64_t)g_t1 * kp, k2_cap), 256, 0, st>>>(
+        ts->view, sp, src, surv, surv_cap, surv_keys, pend, next_cnt + 1, ctx->mode, screened, kp);
     const unsigned g_lazy = (unsigned)std::min<uint64_t>((uint64_t)g_t0 * 8, k2_cap);  // 8 warps per binding
     k_confirm_t0<<<g_lazy, 256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pend, next_cnt + 1,
                                          next, next_cnt, ctx->mode, 1, screened, 1);
