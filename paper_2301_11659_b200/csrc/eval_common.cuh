@@ -51,7 +51,23 @@ struct TestsetView {
   const int32_t* dirty_max;   // [T*nP]  (-1 when empty)
   int32_t nF;                 // user float params (extended semantics only; 0 otherwise)
   const double* floats;       // [T][nF]
+  // floor(n / nI) = umulhi(n, nI_m) >> nI_sh for n < 2^31 (nI_m = 0: nI = 1), see
+  // div_nI; set by the upload
+  uint32_t nI_m, nI_sh;
 };
+
+// floor(n / ts.nI) for n < 2^31 (the digit decode of an enumerated binding index)
+__device__ __forceinline__ uint32_t div_nI(const TestsetView& ts, uint32_t n) {
+  return ts.nI_m ? __umulhi(n, ts.nI_m) >> ts.nI_sh : n;
+}
+// floor(g / d) for d >= 1 and a quotient below 2^22 (a permutation index): a float
+// estimate (relative error < 2^-22, so off by at most one) corrected either way
+__device__ __forceinline__ uint64_t div_small_q(uint64_t g, uint64_t d) {
+  uint64_t q = (uint64_t)((float)g * __frcp_rn((float)d));
+  if (q * d > g) --q;
+  else if ((q + 1) * d <= g) ++q;
+  return q;
+}
 
 // Spec decode table in a device-friendly form (copied by value into kernels).
 struct SpecView {

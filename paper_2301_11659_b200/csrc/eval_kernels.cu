@@ -571,15 +571,15 @@ __device__ int warp_verdict(const TestsetView& ts, const SpecView& sp, const Bin
   Dims d;
   if (screened) {
     const uint64_t g = src.begin + idx;
-    const uint64_t perm = g / src.size_maps;
+    const uint64_t perm = div_small_q(g, src.size_maps);
     uint64_t s = g - perm * src.size_maps;
     int64_t v[9];
     const int64_t* tints = ts.ints + (size_t)t * ts.nI;
-    if (s < (1ull << 32)) {
+    if (s < (1ull << 31)) {
       uint32_t s32 = (uint32_t)s;
 #pragma unroll
       for (int q = 0; q < 9; ++q) {
-        const uint32_t dq = s32 / (uint32_t)ts.nI;
+        const uint32_t dq = div_nI(ts, s32);
         v[q] = tints[s32 - dq * (uint32_t)ts.nI];
         s32 = dq;
       }
@@ -793,14 +793,14 @@ __global__ void __launch_bounds__(256) k_confirm_pre(TestsetView ts, SpecView sp
     bool decided = false;
     if (screened) {
       const uint64_t g = src.begin + surv[si];
-      const uint64_t perm = g / src.size_maps;
+      const uint64_t perm = div_small_q(g, src.size_maps);
       uint64_t s = g - perm * src.size_maps;
       int32_t v[9];
-      if (s < (1ull << 32)) {
+      if (s < (1ull << 31)) {
         uint32_t s32 = (uint32_t)s;
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
-          const uint32_t dq = s32 / (uint32_t)ts.nI;
+          const uint32_t dq = div_nI(ts, s32);
           v[q] = (int32_t)ts.ints[s32 - dq * (uint32_t)ts.nI];
           s32 = dq;
         }

@@ -333,6 +333,12 @@ static int testsets_upload(atc_ctx* ctx, const atc_testsets* ts_full, const atc_
   v.T = T;
   v.nI = nI;
   v.nP = nP;
+  {  // div_nI constants: m = ceil(2^(31 + s) / nI), s = ceil(log2 nI) (exact for n < 2^31)
+    uint32_t sh = 0;
+    while ((1ull << sh) < (uint64_t)nI) ++sh;
+    v.nI_m = nI <= 1 ? 0u : (uint32_t)(((1ull << (31 + sh)) + nI - 1) / (uint64_t)nI);
+    v.nI_sh = sh ? sh - 1 : 0;
+  }
   v.ints = (const int64_t*)(h->meta + h->o_ints);
   v.is_f32 = (const int32_t*)(h->meta + h->o_isf);
   v.region_len = (const int64_t*)(h->meta + h->o_rlen);
