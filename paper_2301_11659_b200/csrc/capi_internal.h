@@ -45,6 +45,11 @@ struct atc_ctx {
   int copy_next = 0;
   cudaEvent_t free_ev = nullptr;
   cudaEvent_t update_ev = nullptr;  // in-place updates wait for earlier readers (compute stream)
+  // batched seeded updates (atc_testsets_update_seeded_many): pinned + device staging
+  uint8_t* upd_pin = nullptr;
+  uint8_t* upd_dev = nullptr;
+  size_t upd_cap = 0;
+  cudaEvent_t upd_h2d_ev = nullptr, upd_meta_ev = nullptr, upd_done_ev[kCopyStreams] = {};
   uint64_t free_pending = 0;  // copy streams that have not waited on the latest free (bit per stream)
   int mode = 0;  // ATC_MODE_* of the evaluation in flight
   // instrumentation (atc_profile_*)
@@ -93,6 +98,8 @@ __global__ void k_probe_regions(int T, int nP, const uint64_t* seeds, const uint
                                 const int32_t* is_f32, const int64_t* region_off, const int64_t* need, double* init,
                                 double* fin, TestsetView v, const int64_t* diff_off, const int32_t* diff_pos,
                                 const double* diff_val, const double* pre, const int64_t* pre_off);
+__global__ void k_probe_regions_many(const ProbeJob* jobs, int n_jobs);
+__global__ void k_copy_meta(const ProbeJob* jobs);
 __global__ void k_apply_diffs(int nP, const int64_t* region_len, const int64_t* region_off, const int64_t* diff_off,
                               const int32_t* diff_pos, const double* diff_val, double* fin);
 __global__ void k_build_dirty(TestsetView ts, int32_t* dirty_pos, int32_t* dirty_cnt, int32_t* dirty_max);

@@ -241,6 +241,12 @@ void atc_destroy(atc_ctx* ctx) {
       if (cs) cudaStreamDestroy(cs);
     if (ctx->free_ev) cudaEventDestroy(ctx->free_ev);
     if (ctx->update_ev) cudaEventDestroy(ctx->update_ev);
+    if (ctx->upd_h2d_ev) cudaEventSynchronize(ctx->upd_h2d_ev), cudaEventDestroy(ctx->upd_h2d_ev);
+    if (ctx->upd_meta_ev) cudaEventDestroy(ctx->upd_meta_ev);
+    for (auto& e : ctx->upd_done_ev)
+      if (e) cudaEventDestroy(e);
+    if (ctx->upd_pin) cudaFreeHost(ctx->upd_pin);
+    if (ctx->upd_dev) cudaFree(ctx->upd_dev);
     for (int k = 0; k < atc_ctx::kSideStreams; ++k) {
       if (ctx->side_stream[k]) cudaStreamDestroy(ctx->side_stream[k]);
       if (ctx->join_ev[k]) cudaEventDestroy(ctx->join_ev[k]);

@@ -69,6 +69,21 @@ __device__ __forceinline__ uint64_t div_small_q(uint64_t g, uint64_t d) {
   return q;
 }
 
+// One handle of a batched seeded update (k_copy_meta + k_probe_regions_many).
+struct ProbeJob {
+  TestsetView view;          // the handle's view (its meta block, pools)
+  int32_t cta0;              // the handle's first CTA within its launch group's numbering
+  const uint64_t* seeds;     // [T]       (update staging, device)
+  const uint64_t* skips;     // [T * nP]
+  const int64_t* diff_off;   // [T * nP + 1]
+  const int32_t* diff_pos;
+  const double* diff_val;
+  const int64_t* need;       // [T * nP]
+  const uint8_t* meta_src;   // staged metadata block
+  uint8_t* meta_dst;         // the handle's meta block
+  uint64_t meta_bytes;
+};
+
 // Spec decode table in a device-friendly form (copied by value into kernels).
 struct SpecView {
   int32_t sem, layout, nA, nS;

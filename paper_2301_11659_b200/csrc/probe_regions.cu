@@ -45,15 +45,13 @@ __device__ __forceinline__ uint64_t temper(uint64_t y) {
 // lists over those prefixes (k_build_dirty), diff_* and v's dirty arrays.
 // pre / pre_off (atc_testsets_upload_prefix): the prefixes come from the caller
 // (packed, entries [pre_off[i], pre_off[i+1]) for region i) instead of the stream.
-__global__ void __launch_bounds__(kProbeThreads) k_probe_regions(int T, int nP, const uint64_t* seeds,
-                                                                 const uint64_t* skips, const int64_t* region_len,
-                                                                 const int32_t* is_f32, const int64_t* region_off,
-                                                                 const int64_t* need, double* init, double* fin,
-                                                                 TestsetView v, const int64_t* diff_off,
-                                                                 const int32_t* diff_pos, const double* diff_val,
-                                                                 const double* pre, const int64_t* pre_off) {
+__device__ __forceinline__ void probe_regions_cta(int t, int T, int nP, const uint64_t* seeds, const uint64_t* skips,
+                                                  const int64_t* region_len, const int32_t* is_f32,
+                                                  const int64_t* region_off, const int64_t* need, double* init,
+                                                  double* fin, const TestsetView& v, const int64_t* diff_off,
+                                                  const int32_t* diff_pos, const double* diff_val, const double* pre,
+                                                  const int64_t* pre_off) {
   __shared__ uint64_t z[1024];
-  const int t = blockIdx.x;
   if (t >= T) return;
   const int q = threadIdx.x;
   if (pre) {  // atc_testsets_upload_prefix: the caller's own prefixes, no generator
@@ -198,6 +196,44 @@ __global__ void __launch_bounds__(kProbeThreads) k_probe_regions(int T, int nP, 
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(kProbeThreads) k_probe_regions(int T, int nP, const uint64_t* seeds,
+                                                                 const uint64_t* skips, const int64_t* region_len,
+                                                                 const int32_t* is_f32, const int64_t* region_off,
+                                                                 const int64_t* need, double* init, double* fin,
+                                                                 TestsetView v, const int64_t* diff_off,
+                                                                 const int32_t* diff_pos, const double* diff_val,
+                                                                 const double* pre, const int64_t* pre_off) {
+  probe_regions_cta(blockIdx.x, T, nP, seeds, skips, region_len, is_f32, region_off, need, init, fin, v, diff_off,
+                    diff_pos, diff_val, pre, pre_off);
+}
+
+// A group of the handles of a batched in-place update (atc_testsets_update_seeded_many):
+// CTAs [jobs[j].cta0, jobs[j + 1].cta0) (relative to the group's first) are handle j's
+// tests; its seeded block (seeds, stream positions, final-minus-init entries, needed
+// prefixes) is read from the update's device staging.
+__global__ void __launch_bounds__(kProbeThreads) k_probe_regions_many(const ProbeJob* __restrict__ jobs, int n_jobs) {
+  const int g = jobs[0].cta0 + (int)blockIdx.x;
+  int j = 0;
+  while (j + 1 < n_jobs && g >= jobs[j + 1].cta0) ++j;
+  const ProbeJob& b = jobs[j];
+  const TestsetView& v = b.view;
+  probe_regions_cta(g - b.cta0, v.T, v.nP, b.seeds, b.skips, v.region_len, v.is_f32, v.region_off, b.need,
+                    const_cast<double*>(v.init), const_cast<double*>(v.fin), v, b.diff_off, b.diff_pos, b.diff_val,
+                    nullptr, nullptr);
+}
+
+// Each handle's metadata block (the TestsetView arrays) from the update staging into
+// place, before the generators (which build the dirty lists in it).
+__global__ void k_copy_meta(const ProbeJob* __restrict__ jobs) {
+  const ProbeJob& b = jobs[blockIdx.x];
+  const uint8_t* src = b.meta_src;
+  uint8_t* dst = b.meta_dst;
+  const size_t n16 = b.meta_bytes / 16;
+  for (size_t i = threadIdx.x; i < n16; i += blockDim.x)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (size_t i = n16 * 16 + threadIdx.x; i < b.meta_bytes; i += blockDim.x) dst[i] = src[i];
 }
 
 // final = init with the original run's writes: entries [diff_off[i], diff_off[i+1])

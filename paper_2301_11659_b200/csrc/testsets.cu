@@ -40,6 +40,33 @@ static std::vector<int64_t> region_need(const atc_testset_handle* h, const atc_s
   return need;
 }
 
+// The handle's metadata block (the TestsetView arrays) in host staging: ints, region
+// lengths / offsets, dirty-list offsets, f32 flags, test_ok, floats; dirty counts 0
+// and dirty_max -1 until the dirty lists are built.
+static void fill_meta(const atc_testset_handle* h, const int64_t* int_values, const int32_t* test_ok,
+                      const double* floats, uint8_t* meta) {
+  const int T = h->T, nI = h->nI, nP = h->nP;
+  const size_t TP = (size_t)T * nP;
+  std::memset(meta, 0, h->meta_bytes);
+  auto put = [&](size_t o, const void* src, size_t bytes) {
+    if (bytes) std::memcpy(meta + o, src, bytes);
+  };
+  put(h->o_ints, int_values, (size_t)T * nI * 8);
+  put(h->o_rlen, h->lens.data(), nP * 8);
+  put(h->o_roff, h->off.data(), TP * 8);
+  put(h->o_dof, h->doff.data(), TP * 8);
+  put(h->o_isf, h->is_f32.data(), nP * 4);
+  if (floats) put(h->o_flt, floats, (size_t)T * h->nF * 8);
+  for (int t = 0; t < T; ++t) {
+    const int32_t ok_t = test_ok ? (test_ok[t] ? 1 : 0) : 1;
+    put(h->o_tok + t * 4, &ok_t, 4);
+  }
+  for (size_t i = 0; i < TP; ++i) {
+    const int32_t neg = -1;
+    put(h->o_dmax + i * 4, &neg, 4);  // dirty counts stay 0
+  }
+}
+
 // pre (optional, with sd): the caller's own init regions [T*nP] — only their needed
 // prefixes are staged and copied, instead of generating them from the seeds.
 static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets* ts_full,
@@ -87,24 +114,7 @@ static int testsets_fill(atc_ctx* ctx, atc_testset_handle* h, const atc_testsets
     pageable.resize(h->meta_bytes + seeded_need);
     meta = pageable.data();
   }
-  std::memset(meta, 0, h->meta_bytes);
-  auto put = [&](size_t o, const void* src, size_t bytes) {
-    if (bytes) std::memcpy(meta + o, src, bytes);
-  };
-  put(h->o_ints, int_values, (size_t)T * nI * 8);
-  put(h->o_rlen, h->lens.data(), nP * 8);
-  put(h->o_roff, h->off.data(), TP * 8);
-  put(h->o_dof, h->doff.data(), TP * 8);
-  put(h->o_isf, h->is_f32.data(), nP * 4);
-  if (h->nF && ts_full) put(h->o_flt, ts_full->float_values, (size_t)T * h->nF * 8);
-  for (int t = 0; t < T; ++t) {
-    const int32_t ok_t = test_ok ? (test_ok[t] ? 1 : 0) : 1;
-    put(h->o_tok + t * 4, &ok_t, 4);
-  }
-  for (size_t i = 0; i < TP; ++i) {
-    const int32_t neg = -1;
-    put(h->o_dmax + i * 4, &neg, 4);  // dirty counts stay 0
-  }
+  fill_meta(h, int_values, test_ok, ts_full && h->nF ? ts_full->float_values : nullptr, meta);
   cudaStream_t st = ctx->copy_stream[h->cs];
   if (ctx->free_pending & (1ull << h->cs)) {  // pool memory freed by earlier handles
     cudaStreamWaitEvent(st, ctx->free_ev, 0);
@@ -417,6 +427,136 @@ int atc_testsets_update_seeded(atc_ctx* ctx, atc_testset_handle* h, const atc_se
   return atc_testsets_update_seeded_many(ctx, &h, ts, 1);
 }
 
+// Batched in-place update of distinct needed_only handles (the prepared-sweep step's
+// call): every handle's metadata block, seeds, stream positions, final-minus-init
+// entries and prefix bounds packed into one pinned staging buffer, one H2D and one
+// k_copy_meta on copy stream 0, then the generators in groups of kUpdGroup handles in
+// call order (one k_probe_regions_many launch per group, on copy streams 1, 2, ...),
+// each handle's ready event after its group — instead of per handle two copies, a
+// launch and an event from four host threads (0.39 -> ~0.15 ms of host time before the
+// caller can replay its sweep).  Callers list the handles whose evaluations start the
+// longest chains first.
+static int update_seeded_batched(atc_ctx* ctx, atc_testset_handle* const* handles, const atc_seeded_testsets* ts,
+                                 int32_t n) {
+  constexpr int kUpdGroup = 4;
+  struct Lay {
+    size_t meta, seeds, skips, doffs, dvs, dps, need;
+  };
+  std::vector<Lay> lay((size_t)n);
+  size_t bytes = (((size_t)n * sizeof(atc::ProbeJob)) + 255) / 256 * 256;
+  auto take = [&](size_t b) {
+    const size_t o = bytes;
+    bytes += (b + 15) / 16 * 16;
+    return o;
+  };
+  for (int i = 0; i < n; ++i) {
+    const atc_testset_handle* h = handles[i];
+    const size_t TP = (size_t)h->T * h->nP;
+    const int64_t nd = ts[i].diff_off[TP];
+    for (int64_t e = 0; e < nd; ++e)
+      if (ts[i].diff_pos[e] < 0) {
+        atc_set_error(ctx, "negative final-minus-init position");
+        return ATC_ERR_ARG;
+      }
+    lay[i] = {take(h->meta_bytes), take((size_t)h->T * 8), take(TP * 8), take((TP + 1) * 8), take((size_t)nd * 8),
+              take((size_t)nd * 4), take(TP * 8)};
+  }
+  // the staging of the previous batched update must have been copied out
+  if (ctx->upd_h2d_ev && !atc_cuda_ok(ctx, cudaEventSynchronize(ctx->upd_h2d_ev), "update staging reuse"))
+    return ATC_ERR_CUDA;
+  if (ctx->upd_cap < bytes) {
+    if (ctx->upd_pin) cudaFreeHost(ctx->upd_pin);
+    if (ctx->upd_dev) cudaFree(ctx->upd_dev);
+    ctx->upd_pin = nullptr;
+    ctx->upd_dev = nullptr;
+    ctx->upd_cap = 0;
+    if (!atc_cuda_ok(ctx, cudaMallocHost(&ctx->upd_pin, bytes), "cudaMallocHost") ||
+        !atc_cuda_ok(ctx, cudaMalloc(&ctx->upd_dev, bytes), "cudaMalloc"))
+      return ATC_ERR_CUDA;
+    ctx->upd_cap = bytes;
+  }
+  if (!ctx->upd_h2d_ev) {
+    bool ok = atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->upd_h2d_ev, cudaEventDisableTiming), "cudaEventCreate") &&
+              atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->upd_meta_ev, cudaEventDisableTiming), "cudaEventCreate");
+    for (int k = 0; k < atc_ctx::kCopyStreams && ok; ++k)
+      ok = atc_cuda_ok(ctx, cudaEventCreateWithFlags(&ctx->upd_done_ev[k], cudaEventDisableTiming), "cudaEventCreate");
+    if (!ok) return ATC_ERR_CUDA;
+  }
+  uint8_t* hp = ctx->upd_pin;
+  uint8_t* dp = ctx->upd_dev;
+  auto* jobs = reinterpret_cast<atc::ProbeJob*>(hp);
+  int cta = 0;
+  for (int i = 0; i < n; ++i) {
+    atc_testset_handle* h = handles[i];
+    const atc_seeded_testsets& sd = ts[i];
+    const size_t TP = (size_t)h->T * h->nP;
+    const int64_t nd = sd.diff_off[TP];
+    const Lay& L = lay[i];
+    h->h_ints.assign(sd.int_values, sd.int_values + (size_t)h->T * h->nI);
+    h->needed_only = true;
+    fill_meta(h, sd.int_values, sd.test_ok, nullptr, hp + L.meta);
+    std::memcpy(hp + L.seeds, sd.stream_seed, (size_t)h->T * 8);
+    std::memcpy(hp + L.skips, sd.stream_skip, TP * 8);
+    std::memcpy(hp + L.doffs, sd.diff_off, (TP + 1) * 8);
+    if (nd) {
+      std::memcpy(hp + L.dvs, sd.diff_val, (size_t)nd * 8);
+      std::memcpy(hp + L.dps, sd.diff_pos, (size_t)nd * 4);
+    }
+    const std::vector<int64_t> need = region_need(h, &sd);
+    std::memcpy(hp + L.need, need.data(), TP * 8);
+    atc::ProbeJob& b = jobs[i];
+    b.view = h->view;
+    if (i % kUpdGroup == 0) cta = 0;  // CTA numbering restarts per launch group
+    b.cta0 = cta;
+    cta += h->T;
+    b.seeds = (const uint64_t*)(dp + L.seeds);
+    b.skips = (const uint64_t*)(dp + L.skips);
+    b.diff_off = (const int64_t*)(dp + L.doffs);
+    b.diff_pos = (const int32_t*)(dp + L.dps);
+    b.diff_val = (const double*)(dp + L.dvs);
+    b.need = (const int64_t*)(dp + L.need);
+    b.meta_src = dp + L.meta;
+    b.meta_dst = h->meta;
+    b.meta_bytes = h->meta_bytes;
+  }
+  cudaStream_t st = ctx->copy_stream[0];
+  if (ctx->free_pending & 1ull) {
+    cudaStreamWaitEvent(st, ctx->free_ev, 0);
+    ctx->free_pending &= ~1ull;
+  }
+  cudaStreamWaitEvent(st, ctx->update_ev, 0);  // earlier readers of the old contents first
+  for (int i = 0; i < n; ++i)                   // and every handle's earlier uploads
+    if (handles[i]->ready) cudaStreamWaitEvent(st, handles[i]->ready, 0);
+  bool ok = atc_cuda_ok(ctx, cudaMemcpyAsync(dp, hp, bytes, cudaMemcpyHostToDevice, st), "H2D update batch") &&
+            atc_cuda_ok(ctx, cudaEventRecord(ctx->upd_h2d_ev, st), "cudaEventRecord");
+  const atc::ProbeJob* dj = reinterpret_cast<const atc::ProbeJob*>(dp);
+  if (ok) {
+    atc::k_copy_meta<<<(unsigned)n, 256, 0, st>>>(dj);
+    ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_copy_meta") &&
+         atc_cuda_ok(ctx, cudaEventRecord(ctx->upd_meta_ev, st), "cudaEventRecord");
+  }
+  int groups = 0;
+  for (int i0 = 0; i0 < n && ok; i0 += kUpdGroup, ++groups) {
+    const int i1 = std::min(n, i0 + kUpdGroup);
+    cudaStream_t gs = ctx->copy_stream[1 + groups % (atc_ctx::kCopyStreams - 1)];
+    cudaStreamWaitEvent(gs, ctx->upd_meta_ev, 0);
+    int g_ctas = 0;
+    for (int i = i0; i < i1; ++i) g_ctas += handles[i]->T;
+    atc::k_probe_regions_many<<<(unsigned)g_ctas, atc::kProbeThreads, 0, gs>>>(dj + i0, i1 - i0);
+    ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_probe_regions_many");
+    for (int i = i0; i < i1 && ok; ++i) {
+      atc_testset_handle* h = handles[i];
+      ok = (h->ready || atc_cuda_ok(ctx, cudaEventCreateWithFlags(&h->ready, cudaEventDisableTiming), "cudaEventCreate")) &&
+           atc_cuda_ok(ctx, cudaEventRecord(h->ready, gs), "cudaEventRecord");
+    }
+    // the next batch's staging copy (stream 0) after every generator has read this one
+    cudaEvent_t done = ctx->upd_done_ev[groups % atc_ctx::kCopyStreams];
+    ok = ok && atc_cuda_ok(ctx, cudaEventRecord(done, gs), "cudaEventRecord");
+    if (ok) cudaStreamWaitEvent(st, done, 0);
+  }
+  return ok ? ATC_OK : ATC_ERR_CUDA;
+}
+
 int atc_testsets_update_seeded_many(atc_ctx* ctx, atc_testset_handle* const* handles, const atc_seeded_testsets* ts,
                                     int32_t n) {
   ATC_ENTER(ctx);
@@ -460,6 +600,11 @@ int atc_testsets_update_seeded_many(atc_ctx* ctx, atc_testset_handle* const* han
       cudaStreamWaitEvent(ctx->copy_stream[h->cs], ctx->free_ev, 0);
       ctx->free_pending &= ~(1ull << h->cs);
     }
+  }
+  if (distinct && n > 1) {
+    bool batchable = true;
+    for (int i = 0; i < n && batchable; ++i) batchable = ts[i].needed_only != 0;
+    if (batchable) return update_seeded_batched(ctx, handles, ts, n);
   }
   const int workers = distinct ? std::min(n, 4) : 1;
   std::atomic<int> first_rc{ATC_OK};
