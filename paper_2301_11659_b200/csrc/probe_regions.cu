@@ -35,8 +35,9 @@ __device__ __forceinline__ uint64_t temper(uint64_t y) {
 // merge, shift and matrix-A step of the twist), draw i = temper(z[312 + i]) — the
 // standard's twist computes exactly these words in place.  Phase k computes the 312
 // words z[312 (k + 1) + q] from the previous phase's (156 threads, two words each:
-// z[n + 312] and z[n + 468]) in a 1024-word ring, one barrier per phase; the draws of
-// phases that meet a region (a per-CTA bitmap) are tempered and stored by the same
+// z[n + 312] and z[n + 468]) with the state in registers (neighbours' words by warp
+// shuffles, warp-boundary words through shared memory, one barrier per phase); the draws
+// of phases that meet a region (a per-CTA bitmap) are tempered and stored by the same
 // threads.  (A variant with 312 more threads tempering the previous phase's draws
 // measured slower: the extra warps' per-phase overhead outweighs the shorter chain.)
 // need (optional, [T * nP]): generate only the first need[t * nP + p] elements of
@@ -107,10 +108,6 @@ __device__ __forceinline__ void probe_regions_cta(int t, int T, int nP, const ui
       s_emit[w] = m;
     }
   __syncthreads();
-  auto twist = [](uint64_t a, uint64_t b, uint64_t c) {  // z[n + 312] from z[n], z[n + 1], z[n + 156]
-    const uint64_t y = (a & kUpper) | (b & kLower);
-    return c ^ (y >> 1) ^ ((y & 1ull) ? kMatrixA : 0ull);
-  };
   auto emit = [&](uint32_t pos, uint64_t w) {  // draw pos -> its region element, if any
     for (int p = 0; p < np; ++p)
       if (pos - lo[p] < len[p]) {  // (regions of a test do not overlap: one hit)
@@ -123,36 +120,75 @@ __device__ __forceinline__ void probe_regions_cta(int t, int T, int nP, const ui
         fin[o] = x;
       }
   };
-  // word w of the sequence lives in slot w & 1023 (a phase reads the previous phase's
-  // 312 words and writes its own 312)
-  constexpr uint32_t kMask = 1023;
+  // The state in registers: thread q < 156 holds A = z[base + q] and B = z[base + 156 + q]
+  // of the previous phase, so z[n + 312] = twist(A, A', B) and z[n + 468] = twist(B, B',
+  // z[n + 312]) with A', B' thread q + 1's — of which twist reads only the low 32 bits:
+  // one shuffle each inside the warp, across a warp boundary a 32-bit exchange in shared
+  // memory (one barrier per phase); thread 155's z[n + 157] = z[base + 312] is thread
+  // 0's new word, recomputed from the exchange.  Twists in 32-bit halves.
+  // The exchange: every thread stores its low A, low B and high A each phase (unconditional
+  // stores, double-buffered by phase parity so that a fast warp's next write cannot
+  // overtake a slow warp's read); a warp's last lane reads thread q + 1's, thread 155
+  // thread 0's and 1's.
+  __shared__ uint32_t xs[2][3][kM];  // [parity][low A, low B, high A][thread]
+  auto tw = [](uint32_t ah, uint32_t al, uint32_t bl, uint32_t ch, uint32_t cl, uint32_t& rh, uint32_t& rl) {
+    // y = (a & 0xFFFFFFFF80000000) | (b & 0x7FFFFFFF); z = c ^ (y >> 1) ^ (y odd ? matrix A : 0)
+    const uint32_t yl = (al & 0x80000000u) | (bl & 0x7FFFFFFFu);
+    const uint32_t m = 0u - (yl & 1u);
+    rl = cl ^ __funnelshift_r(yl, ah, 1) ^ (m & (uint32_t)kMatrixA);
+    rh = ch ^ (ah >> 1) ^ (m & (uint32_t)(kMatrixA >> 32));
+  };
+  uint32_t Ah = 0, Al = 0, Bh = 0, Bl = 0;
+  const int qq = q < kM ? q : kM - 1;  // threads 156..159 shadow thread 155 (never stored)
+  Ah = (uint32_t)(z[qq] >> 32);
+  Al = (uint32_t)z[qq];
+  Bh = (uint32_t)(z[kM + qq] >> 32);
+  Bl = (uint32_t)z[kM + qq];
+  const int wl = q & 31;
+  const bool act = q < kM, edge = wl == 31 && q < kM - 1, last = q == kM - 1;
+  const int nx = q + 1 < kM ? q + 1 : 0;
+  uint32_t bits = 0;
   uint32_t k = 0;
   for (uint32_t base = 0; base < end; base += kN, ++k) {
-    if (q < kM) {
-      // words n = base + q: inputs z[n], z[n + 1], z[n + 156], z[n + 157] (the previous
-      // phase; z[base + 312] is this phase's word of thread 0, recomputed by thread 155)
-      const uint32_t n = base + q;
-      const uint64_t zn156 = z[(n + kM) & kMask];
-      const uint64_t wa = twist(z[n & kMask], z[(n + 1) & kMask], zn156);
-      const uint64_t zn157 = q == kM - 1 ? twist(z[base & kMask], z[(base + 1) & kMask], z[(base + kM) & kMask])
-                                         : z[(n + kM + 1) & kMask];
-      const uint64_t wb = twist(zn156, zn157, wa);
-      z[(n + kN) & kMask] = wa;
-      z[(n + kN + kM) & kMask] = wb;
-      bool any;
-      if (bitmap) {
-        any = (s_emit[k >> 5] >> (k & 31)) & 1u;
-      } else {
+    uint32_t(*x)[kM] = xs[k & 1];
+    if (act) {
+      x[0][q] = Al;
+      x[1][q] = Bl;
+      x[2][q] = Ah;
+    }
+    if ((k & 31) == 0) bits = bitmap ? s_emit[k >> 5] : 0xFFFFFFFFu;
+    __syncthreads();  // the previous phase's words visible
+    uint32_t A1 = __shfl_down_sync(0xffffffffu, Al, 1), B1 = __shfl_down_sync(0xffffffffu, Bl, 1);
+    if (act) {
+      if (last) {  // z[n + 1] = z[base + 156] (thread 0's B), z[n + 157] = thread 0's new word
+        uint32_t a0h, a0l;
+        tw(x[2][0], x[0][0], x[0][1], 0u, x[1][0], a0h, a0l);  // only its low half is read
+        A1 = x[1][0];
+        B1 = a0l;
+      } else if (edge) {
+        A1 = x[0][nx];
+        B1 = x[1][nx];
+      }
+      uint32_t wah, wal, wbh, wbl;
+      tw(Ah, Al, A1, Bh, Bl, wah, wal);
+      tw(Bh, Bl, B1, wah, wal, wbh, wbl);
+      Ah = wah;
+      Al = wal;
+      Bh = wbh;
+      Bl = wbl;
+      bool any = bits & 1u;
+      if (!bitmap) {
         any = false;
         for (int p = 0; p < np; ++p) any = any || (base < lo[p] + len[p] && base + kN > lo[p]);
       }
       if (any) {
-        emit(n, wa);
-        emit(n + kM, wb);
+        emit(base + q, (uint64_t)Ah << 32 | Al);
+        emit(base + kM + q, (uint64_t)Bh << 32 | Bl);
       }
     }
-    __syncthreads();  // this phase's words visible to the next
+    bits >>= 1;
   }
+  __syncthreads();
   if (!need) return;
   for (int p = 0; p < nP; ++p) {  // final = init + the original run's writes
     const size_t i = (size_t)t * nP + p;
