@@ -302,7 +302,7 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
         m0 |= (out[base + j] == 1 ? 1u : 0u) << j;
         if (out1) m1 |= (out1[base + j] == 1 ? 1u : 0u) << j;
       }
-      cm[base / nI] = m0 | m1 << 16;  // position 0 in bits 0..15, position 1 in bits 16..31
+      cm[base / nI] = m0 | (m0 | m1) << 16;  // position 0 in bits 0..15, positions 0 or 1 in bits 16..31
     };
     // entries whose c digit is < 1 (or a bad shape): the empty sum; others: 2 until computed
     for (uint64_t j = 0; j < nI; ++j) {

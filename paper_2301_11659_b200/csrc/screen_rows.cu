@@ -454,13 +454,14 @@ __global__ void __launch_bounds__(256) k_screen_conv_planes(TestsetView ts, cons
 
 // ----------------------------------------------------------------------------
 // k_cmask: verdict bits of the nI values of tc_c (the first table role, key
-// stride 1): cmask[i] bit (shift + j) = table[i*nI + j] == 1.
-// shift 16: OR the bits into the upper half (the position-1 verdicts).
+// stride 1): cmask[i] bit j = table[i*nI + j] == 1 (position 0).
+// shift 16: the upper half gets position 0's bits OR position 1's (the rows a binding
+// with ow >= 2 fails), so a reader takes word >> (ow >= 2 ? 16 : 0).
 __global__ void k_cmask(const uint8_t* table, uint64_t n_words, int nI, uint32_t* cmask, int shift) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_words; i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t m = 0;
     for (int j = 0; j < nI; ++j) m |= (table[i * nI + j] == 1 ? 1u : 0u) << j;
-    cmask[i] = shift ? (cmask[i] | m << shift) : m;
+    cmask[i] = shift ? (cmask[i] | (m | (cmask[i] & 0xFFFFu)) << shift) : m;
   }
 }
 
@@ -793,8 +794,9 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
     uint32_t ckey0 = (uint32_t)perm * cperm;
 #pragma unroll
     for (int q = 3; q < NS; ++q) ckey0 += (uint32_t)digit[q] * cks[q];
-    // position-1 verdicts (bits 16..) apply when ow >= 2: output position 1 is (0, 0, 0, 1)
-    const uint32_t sel = cow >= 2 ? 0xFFFFFFFFu : 0xFFFFu;
+    // the verdict word's upper half (positions 0 or 1) applies when ow >= 2: output
+    // position 1 is (0, 0, 0, 1)
+    const uint32_t wsh = cow >= 2 ? 16u : 0u;
     if (c0b >= begin && c0b + nI3 <= end) {  // the whole cube: no range masks
       f_bind += (unsigned int)nI3;
       if (cube_bad) {
@@ -811,20 +813,26 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
         f2 += s_f2sum[tix];
         const int4* pl = s_pl + tix * nI;
         const uint32_t* cm0 = plan.cmask + ckey0;
-        const uint32_t ck2 = cks[2];
+        const uint32_t ck2 = cks[2];  // 1 for the canonical key order: immediate offsets
         // branch-free pass over the planes: a bit per plane that needs a closer look —
         // UB pairs possible (v >= len(in) - Q': p*hw >= alim, see below) or a c row
         // without a position-0/1 mismatch (skip planes: t.w = every row, never)
         const int32_t lq = (int32_t)len_in - q_rest;
         uint32_t need = 0;
-        {
+        if (ck2 == 1) {
+#pragma unroll
+          for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
+            const int4 t = pl[hd];
+            const uint32_t rb = ((__ldg(cm0 + hd) >> wsh) | (uint32_t)t.w) & 0xFFFFu;
+            if (t.y >= lq || rb != rows_all) need |= 1u << hd;
+          }
+        } else {
           const uint32_t* cm = cm0;
 #pragma unroll
-          for (int hd = 0; hd < nI; ++hd, cm += ck2) {  // digit 2: tc_h
-            const uint32_t cw2 = __ldg(cm) & sel;
+          for (int hd = 0; hd < nI; ++hd, cm += ck2) {
             const int4 t = pl[hd];
-            const uint32_t rb = (cw2 | cw2 >> 16 | (uint32_t)t.w) & 0xFFFFu;
-            need |= (t.y >= lq || rb != rows_all ? 1u : 0u) << hd;
+            const uint32_t rb = ((__ldg(cm) >> wsh) | (uint32_t)t.w) & 0xFFFFu;
+            if (t.y >= lq || rb != rows_all) need |= 1u << hd;
           }
         }
         while (need) {
@@ -847,8 +855,7 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
               if (!s_cnt[ru]) continue;
             }
           }
-          const uint32_t cw2 = __ldg(cm0 + (uint32_t)hd * ck2) & sel;
-          const uint32_t rows_bad = (cw2 | cw2 >> 16) & 0xFFFFu;
+          const uint32_t rows_bad = (__ldg(cm0 + (uint32_t)hd * ck2) >> wsh) & 0xFFFFu;
           if (rows_bad == rows_all) continue;  // every c row mismatches at position 0 or 1
           const M128 ok = s_okm[r_ok] & ~(~s_gtx[mth] | s_rowx[rows_bad]);
           if (any(ok)) {
@@ -887,8 +894,8 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
           ok = ok & ~um;
           if (!any(ok)) continue;
         }
-        const uint32_t cw2 = __ldg(plan.cmask + ckey0 + (uint32_t)hd * cks[2]) & sel;
-        ok = ok & ~(dirty_fail | s_rowx[(cw2 | cw2 >> 16) & 0xFFFFu]);
+        const uint32_t cw2 = __ldg(plan.cmask + ckey0 + (uint32_t)hd * cks[2]) >> wsh;
+        ok = ok & ~(dirty_fail | s_rowx[cw2 & 0xFFFFu]);
         if (any(ok)) {
           const unsigned int k = popc(ok);
           f_surv += k;
@@ -926,8 +933,8 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
         um = alim <= 0 ? ok : (ok & gt_prod(lut_n ? div_capn(am1, hw, r_hw, qcap) : (int)(am1 / (uint32_t)hw)));
         ok = ok & ~um;
         if (any(ok)) {
-          const uint32_t cw2 = __ldg(plan.cmask + ckey0 + (uint32_t)hd * cks[2]) & sel;
-          mm = ok & (dirty_fail | s_rowx[(cw2 | cw2 >> 16) & 0xFFFFu]);
+          const uint32_t cw2 = __ldg(plan.cmask + ckey0 + (uint32_t)hd * cks[2]) >> wsh;
+          mm = ok & (dirty_fail | s_rowx[cw2 & 0xFFFFu]);
           ok = ok & ~mm;
         }
       }
