@@ -64,8 +64,8 @@ struct atc_ctx {
   int opt_tc_flags = 0;
   int opt_small_log2 = 16;   // gemm spaces of <= 2^this bindings go to k_sweep_small (0: none;
                              // tools/small_threshold.py: 16 keeps config 4's 279,936 on its chain)
-  int opt_conv_streams = 8;
-  int opt_k2b_parts = 1;  // warps per (binding, t) item of the conv K2b (k_confirm_warp)  // streams the conv chains of a sweep round-robin over (tools/sweep_streams.py)
+  int opt_conv_streams = 8;  // streams the conv chains of a sweep round-robin over (tools/sweep_streams.py)
+  int opt_k2b_parts = 1;     // warps per (binding, t) item of the conv K2b (k_confirm_warp)
   bool tc_configured = false;  // k_tc_gemm* shared-memory attributes set on this context's device
   // every ABI entry point holds this for its whole call, so a context is
   // serialised (the pipeline's worker threads may share one)
