@@ -22,9 +22,10 @@ struct atc_ctx {
   // reusable device scratch, grown on demand (slot ids are per call site)
   // sweeps run conv spaces on the caller's stream and gemm spaces round-robin on
   // kSideStreams concurrent side streams; side stream k's evaluator scratch lives
-  // at slot + 32 * (k + 1) (set while enqueueing it)
+  // at slot + kSlotsPerStream * (k + 1) (set while enqueueing it)
   static constexpr int kSideStreams = 10;
-  static constexpr int kSlots = 32 * (kSideStreams + 1);
+  static constexpr int kSlotsPerStream = 40;  // evaluator scratch slots per (side) stream
+  static constexpr int kSlots = kSlotsPerStream * (kSideStreams + 1);
   int slot_base = 0;
   cudaStream_t side_stream[kSideStreams] = {};
   cudaEvent_t fork_ev = nullptr, join_ev[kSideStreams] = {};
@@ -110,7 +111,8 @@ __global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out, uint8_t* out1);
 __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
-                                  uint8_t* out, uint8_t* out1, uint32_t* cm, int stage_a, int stage_b);
+                                  uint8_t* out, uint8_t* out1, uint32_t* cm, int stage_a, int stage_b,
+                                  uint32_t* allbad);
 __global__ void k_screen_enum(TestsetView ts, SpecView sp, BindingSource src, uint64_t n, Pos0Table pt,
                               uint64_t* surv, uint64_t surv_cap, unsigned long long* surv_cnt,
                               unsigned long long* reason_hist);

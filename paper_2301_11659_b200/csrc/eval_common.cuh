@@ -129,6 +129,10 @@ struct RowPlan {
   // (perm, h, w, r, s) key — output position 0 in bits 0..15, position 1 (used when
   // tc_ow >= 2) in bits 16..31 (k_pos0_table_conv / k_cmask)
   const uint32_t* cmask;
+  // conv, canonical key order (h the fastest digit of a cmask word index): per (perm, w,
+  // r, s) the h digits whose every c row mismatches — bit h in bits 0..15 for position 0,
+  // bit 16 + h for positions 0 or 1 (ow >= 2); index = cmask word index / nI
+  const uint32_t* allbad;
 };
 
 // One small enumerated space of a sweep for k_sweep_small (eval_kernels.cu): its

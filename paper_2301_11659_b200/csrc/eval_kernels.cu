@@ -258,7 +258,8 @@ __global__ void k_gemm_need(TestsetView ts, int row_major, int32_t* need) {
 // output position 0, bit 16 + j the same for position 1 — which is what
 // k_screen_conv_pairs reads (one thread owns exactly one word).
 __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
-                                  uint8_t* out, uint8_t* out1, uint32_t* cm, int stage_a, int stage_b) {
+                                  uint8_t* out, uint8_t* out1, uint32_t* cm, int stage_a, int stage_b,
+                                  uint32_t* allbad) {
   // blockIdx.y = permutation; blockIdx.x strides over its (h, w, r, s) entries.
   // stage_a / stage_b > 0: the first stage_a / stage_b elements of the in / weights
   // regions (every element a tabulated sum can read) are staged in shared memory.
@@ -303,6 +304,11 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
         if (out1) m1 |= (out1[base + j] == 1 ? 1u : 0u) << j;
       }
       cm[base / nI] = m0 | (m0 | m1) << 16;  // position 0 in bits 0..15, positions 0 or 1 in bits 16..31
+      if (allbad) {  // (zeroed by the host) this h digit in its (perm, w, r, s) group's mask
+        const uint32_t all = (1u << nI) - 1u;
+        const uint32_t bits = (m0 == all ? 1u << h_d : 0u) | ((m0 | m1) == all ? 1u << (16 + h_d) : 0u);
+        if (bits) atomicOr(allbad + base / nI / nI, bits);
+      }
     };
     // entries whose c digit is < 1 (or a bad shape): the empty sum; others: 2 until computed
     for (uint64_t j = 0; j < nI; ++j) {

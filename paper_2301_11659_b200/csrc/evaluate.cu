@@ -533,6 +533,7 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
       e.plan.cmask = cm;
     }
     const uint64_t w_off = t_off / (uint64_t)ts->nI;
+    e.plan.allbad = nullptr;
     if (sp.sem == ATC_SEM_CONV2D && e.pt.R == 5 && e.plan.key_stride[1] == 1 && e.use_rows &&
         conv_thresholds_ok(ctx, sp, e.plan, ts->nI)) {
       // one running sum per (perm, h, w, r, s); the pair screen's bit words come out
@@ -547,9 +548,21 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
       const uint64_t per = (uint64_t)ts->nI * ts->nI * ts->nI * ts->nI;
       const dim3 grid((unsigned)std::max<uint64_t>(1, std::min<uint64_t>((per + 255) / 256, 65535)),
                       (unsigned)np_local);
+      // the all-bad masks (per (perm, w, r, s), from the same pass) when h is the fastest
+      // digit of the cmask word index
+      uint32_t* ab = nullptr;
+      if (cm && e.plan.key_stride[2] == (uint64_t)ts->nI) {
+        ab = (uint32_t*)atc_ctx_scratch(ctx, 32, (words / ts->nI + 8) * 4);
+        if (!ab) {
+          atc_set_error(ctx, "scratch allocation failed (allbad)");
+          return ATC_ERR_CUDA;
+        }
+        cudaMemsetAsync(ab + w_off / ts->nI, 0, (size_t)(t_bytes / ts->nI / ts->nI + 1) * 4, st);
+        e.plan.allbad = ab;
+      }
       k_pos0_table_conv<<<grid, 256, (size_t)(sa + sb) * sizeof(double), st>>>(
           ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off, tab1 ? tab1 + t_off : nullptr,
-          cm ? cm + w_off : nullptr, sa, sb);
+          cm ? cm + w_off : nullptr, sa, sb, ab ? ab + w_off / ts->nI : nullptr);
       if (ctx->prof) ctx->prof_kernels += 1;
     } else {
       k_pos0_table<<<(unsigned)std::max<uint64_t>(

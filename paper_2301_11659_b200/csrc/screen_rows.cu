@@ -545,6 +545,7 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
   __shared__ uint32_t s_cks[NS];
   __shared__ M128 s_okm[129];            // pairs of product rank < r that pass x >= 1, c >= 1
   __shared__ uint8_t s_cnt[129];         // their number
+  __shared__ uint16_t s_skipm[8 * kPairMaxInts];  // per (in region, w digit): the h digits of skip planes
   const int nI = NIc ? NIc : ts.nI, nI2 = nI * nI;
   // CTA tables: built once, from O(nI^2) work per thread at most (the per-CTA
   // prologue is paid by every one of the 4 x 148 CTAs)
@@ -720,6 +721,11 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
     const int32_t hw = s_u[hd] * s_u[wd], pm = ra >= 1 ? max(s_prod[ra - 1], 0) : 0;
     s_pl[i] = make_int4(hw, skip ? -(1 << 30) : hw * (pm - 1), ra, skip ? (1 << nI) - 1 : 0);
   }
+  for (int i = threadIdx.x; i < nP * nI && i < 8 * kPairMaxInts; i += blockDim.x) {
+    uint32_t m = 0;
+    for (int hd = 0; hd < nI; ++hd) m |= (s_u[hd] < 1 || s_cnt[s_ainr[i * nI + hd]] == 0 ? 1u : 0u) << hd;
+    s_skipm[i] = (uint16_t)m;
+  }
   for (int i = threadIdx.x; i < nP * nI; i += blockDim.x) {
     uint32_t f = 0;
     for (int hd = 0; hd < nI; ++hd)
@@ -819,7 +825,14 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
         // without a position-0/1 mismatch (skip planes: t.w = every row, never)
         const int32_t lq = (int32_t)len_in - q_rest;
         uint32_t need = 0;
-        if (ck2 == 1) {
+        if (plan.allbad && tix < 8 * kPairMaxInts) {
+          // the h digits whose every c row mismatches, for the whole cube in one word
+          // (built with the table), less the skip planes; then the UB test per plane
+          need = ~((__ldg(plan.allbad + ckey0 / (uint32_t)nI) >> wsh) | s_skipm[tix]) & rows_all;
+#pragma unroll
+          for (int hd = 0; hd < nI; ++hd)  // digit 2: tc_h
+            if (pl[hd].y >= lq) need |= 1u << hd;
+        } else if (ck2 == 1) {
 #pragma unroll
           for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
             const int4 t = pl[hd];

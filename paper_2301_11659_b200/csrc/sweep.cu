@@ -71,7 +71,7 @@ constexpr uint64_t kSmallSurvCap = 1ull << 20;  // survivors of all small jobs t
 // over side streams 1, 2, ... (in the corpus: one, on a stream of its own).  (Higher launch priority
 // for the tables / K2 / finalize kernels was measured too: K2 then interleaves with
 // the next K1s, 1.06 -> 1.11 ms — the step is K1-throughput bound.)  Side stream
-// k's scratch lives at slot + 32 * (k + 1); every branch forks from and joins back
+// k's scratch lives at slot + kSlotsPerStream * (k + 1); every branch forks from and joins back
 // into `st`, so a captured graph has the same branches.
 int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_uploads) {
   const uint64_t chunk_cap = kEnumChunkCap;
@@ -147,7 +147,7 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
     }
     const bool side = sk >= 0;
     cudaStream_t js = side ? ctx->side_stream[sk] : split ? ctx->conv_stream : st;
-    ctx->slot_base = side ? 32 * (sk + 1) : 0;
+    ctx->slot_base = side ? atc_ctx::kSlotsPerStream * (sk + 1) : 0;
     uint64_t* surv = (uint64_t*)atc_ctx_scratch(ctx, 1, chunk_cap * 8);
     int32_t* skeys = (int32_t*)atc_ctx_scratch(ctx, 2, chunk_cap * 4);
     unsigned long long* cnt = (unsigned long long*)atc_ctx_scratch(ctx, 3, 64);
