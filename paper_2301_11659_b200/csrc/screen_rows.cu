@@ -546,6 +546,7 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
   __shared__ M128 s_okm[129];            // pairs of product rank < r that pass x >= 1, c >= 1
   __shared__ uint8_t s_cnt[129];         // their number
   __shared__ uint16_t s_skipm[8 * kPairMaxInts];  // per (in region, w digit): the h digits of skip planes
+  __shared__ int32_t s_vmax[8 * kPairMaxInts];    // and the largest plane-table v over h
   const int nI = NIc ? NIc : ts.nI, nI2 = nI * nI;
   // CTA tables: built once, from O(nI^2) work per thread at most (the per-CTA
   // prologue is paid by every one of the 4 x 148 CTAs)
@@ -723,8 +724,16 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
   }
   for (int i = threadIdx.x; i < nP * nI && i < 8 * kPairMaxInts; i += blockDim.x) {
     uint32_t m = 0;
-    for (int hd = 0; hd < nI; ++hd) m |= (s_u[hd] < 1 || s_cnt[s_ainr[i * nI + hd]] == 0 ? 1u : 0u) << hd;
+    int32_t vm = INT32_MIN;
+    for (int hd = 0; hd < nI; ++hd) {  // (the v of s_pl, recomputed: no barrier in between)
+      const int ra = s_ainr[i * nI + hd];
+      const bool skip = s_u[hd] < 1 || s_cnt[ra] == 0;
+      const int32_t hw = s_u[hd] * s_u[i % nI], pm = ra >= 1 ? max(s_prod[ra - 1], 0) : 0;
+      m |= (skip ? 1u : 0u) << hd;
+      vm = max(vm, skip ? -(1 << 30) : hw * (pm - 1));
+    }
     s_skipm[i] = (uint16_t)m;
+    s_vmax[i] = vm;
   }
   for (int i = threadIdx.x; i < nP * nI; i += blockDim.x) {
     uint32_t f = 0;
@@ -829,9 +838,10 @@ __global__ void __launch_bounds__(kPairThreads, 1024 / kPairThreads) k_screen_co
           // the h digits whose every c row mismatches, for the whole cube in one word
           // (built with the table), less the skip planes; then the UB test per plane
           need = ~((__ldg(plan.allbad + ckey0 / (uint32_t)nI) >> wsh) | s_skipm[tix]) & rows_all;
+          if (s_vmax[tix] >= lq)  // some plane may have UB pairs (usually none does)
 #pragma unroll
-          for (int hd = 0; hd < nI; ++hd)  // digit 2: tc_h
-            if (pl[hd].y >= lq) need |= 1u << hd;
+            for (int hd = 0; hd < nI; ++hd)  // digit 2: tc_h
+              if (pl[hd].y >= lq) need |= 1u << hd;
         } else if (ck2 == 1) {
 #pragma unroll
           for (int hd = 0; hd < nI; ++hd) {  // digit 2: tc_h
