@@ -20,6 +20,7 @@ from paper_2301_11659_b200.evaluator import Evaluator
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--json", default=None)
+ap.add_argument("--only", default=None, help="STEM:SPEC — one space's chain")
 args = ap.parse_args()
 
 ctx = _lib.Context(0)
@@ -29,6 +30,9 @@ _lib.check(ctx.handle, _lib.lib().atc_set_stream(ctx.handle, C.c_void_p(stream.c
 ev = Evaluator(ctx)
 jobs = workloads.corpus_jobs()
 jobs.sort(key=lambda j: j.spec.semantics != "conv2d")
+if args.only:
+    stem, spec = args.only.split(":")
+    jobs = [j for j in jobs if j.stem == stem and j.spec_name == spec]
 sw = ev.sweep([(j.spec, j.ts, j.space, 0, j.count) for j in jobs])
 for _ in range(4):
     sw.run()
