@@ -428,28 +428,36 @@ int atc_testsets_update_seeded(atc_ctx* ctx, atc_testset_handle* h, const atc_se
 }
 
 // Batched in-place update of distinct needed_only handles (the prepared-sweep step's
-// call): every handle's metadata block, seeds, stream positions, final-minus-init
-// entries and prefix bounds packed into one pinned staging buffer, one H2D and one
-// k_copy_meta on copy stream 0, then the generators in groups of kUpdGroup handles in
-// call order (one k_probe_regions_many launch per group, on copy streams 1, 2, ...),
-// each handle's ready event after its group — instead of per handle two copies, a
-// launch and an event from four host threads (0.39 -> ~0.15 ms of host time before the
-// caller can replay its sweep).  Callers list the handles whose evaluations start the
-// longest chains first.
+// call), in groups of kUpdGroup handles in call order.  Each group's metadata blocks,
+// seeds, stream positions, final-minus-init entries and prefix bounds are packed into
+// its own slice of one pinned staging buffer; as soon as a slice is packed it goes out
+// as one H2D and one k_copy_meta on copy stream 0 and the group's generators as one
+// k_probe_regions_many launch on copy stream 1, 2, ..., each handle's ready event after
+// it — so the first generators start while the host still packs the later groups
+// (packing everything before the first copy held the GPU idle for ~0.13 ms), and per
+// handle two copies, a launch and an event from four host threads are gone.  Callers
+// list the handles whose evaluations start the longest chains first.
 static int update_seeded_batched(atc_ctx* ctx, atc_testset_handle* const* handles, const atc_seeded_testsets* ts,
                                  int32_t n) {
   constexpr int kUpdGroup = 4;
   struct Lay {
     size_t meta, seeds, skips, doffs, dvs, dps, need;
   };
+  const int n_groups = (n + kUpdGroup - 1) / kUpdGroup;
   std::vector<Lay> lay((size_t)n);
-  size_t bytes = (((size_t)n * sizeof(atc::ProbeJob)) + 255) / 256 * 256;
+  std::vector<size_t> g_off((size_t)n_groups + 1);
+  size_t bytes = 0;
   auto take = [&](size_t b) {
     const size_t o = bytes;
     bytes += (b + 15) / 16 * 16;
     return o;
   };
   for (int i = 0; i < n; ++i) {
+    if (i % kUpdGroup == 0) {  // a group's slice starts with its jobs
+      bytes = (bytes + 255) / 256 * 256;
+      g_off[(size_t)(i / kUpdGroup)] = bytes;
+      take((size_t)kUpdGroup * sizeof(atc::ProbeJob));
+    }
     const atc_testset_handle* h = handles[i];
     const size_t TP = (size_t)h->T * h->nP;
     const int64_t nd = ts[i].diff_off[TP];
@@ -461,6 +469,7 @@ static int update_seeded_batched(atc_ctx* ctx, atc_testset_handle* const* handle
     lay[i] = {take(h->meta_bytes), take((size_t)h->T * 8), take(TP * 8), take((TP + 1) * 8), take((size_t)nd * 8),
               take((size_t)nd * 4), take(TP * 8)};
   }
+  g_off[(size_t)n_groups] = bytes;
   // the staging of the previous batched update must have been copied out
   if (ctx->upd_h2d_ev && !atc_cuda_ok(ctx, cudaEventSynchronize(ctx->upd_h2d_ev), "update staging reuse"))
     return ATC_ERR_CUDA;
@@ -484,41 +493,6 @@ static int update_seeded_batched(atc_ctx* ctx, atc_testset_handle* const* handle
   }
   uint8_t* hp = ctx->upd_pin;
   uint8_t* dp = ctx->upd_dev;
-  auto* jobs = reinterpret_cast<atc::ProbeJob*>(hp);
-  int cta = 0;
-  for (int i = 0; i < n; ++i) {
-    atc_testset_handle* h = handles[i];
-    const atc_seeded_testsets& sd = ts[i];
-    const size_t TP = (size_t)h->T * h->nP;
-    const int64_t nd = sd.diff_off[TP];
-    const Lay& L = lay[i];
-    h->h_ints.assign(sd.int_values, sd.int_values + (size_t)h->T * h->nI);
-    h->needed_only = true;
-    fill_meta(h, sd.int_values, sd.test_ok, nullptr, hp + L.meta);
-    std::memcpy(hp + L.seeds, sd.stream_seed, (size_t)h->T * 8);
-    std::memcpy(hp + L.skips, sd.stream_skip, TP * 8);
-    std::memcpy(hp + L.doffs, sd.diff_off, (TP + 1) * 8);
-    if (nd) {
-      std::memcpy(hp + L.dvs, sd.diff_val, (size_t)nd * 8);
-      std::memcpy(hp + L.dps, sd.diff_pos, (size_t)nd * 4);
-    }
-    const std::vector<int64_t> need = region_need(h, &sd);
-    std::memcpy(hp + L.need, need.data(), TP * 8);
-    atc::ProbeJob& b = jobs[i];
-    b.view = h->view;
-    if (i % kUpdGroup == 0) cta = 0;  // CTA numbering restarts per launch group
-    b.cta0 = cta;
-    cta += h->T;
-    b.seeds = (const uint64_t*)(dp + L.seeds);
-    b.skips = (const uint64_t*)(dp + L.skips);
-    b.diff_off = (const int64_t*)(dp + L.doffs);
-    b.diff_pos = (const int32_t*)(dp + L.dps);
-    b.diff_val = (const double*)(dp + L.dvs);
-    b.need = (const int64_t*)(dp + L.need);
-    b.meta_src = dp + L.meta;
-    b.meta_dst = h->meta;
-    b.meta_bytes = h->meta_bytes;
-  }
   cudaStream_t st = ctx->copy_stream[0];
   if (ctx->free_pending & 1ull) {
     cudaStreamWaitEvent(st, ctx->free_ev, 0);
@@ -527,33 +501,65 @@ static int update_seeded_batched(atc_ctx* ctx, atc_testset_handle* const* handle
   cudaStreamWaitEvent(st, ctx->update_ev, 0);  // earlier readers of the old contents first
   for (int i = 0; i < n; ++i)                   // and every handle's earlier uploads
     if (handles[i]->ready) cudaStreamWaitEvent(st, handles[i]->ready, 0);
-  bool ok = atc_cuda_ok(ctx, cudaMemcpyAsync(dp, hp, bytes, cudaMemcpyHostToDevice, st), "H2D update batch") &&
-            atc_cuda_ok(ctx, cudaEventRecord(ctx->upd_h2d_ev, st), "cudaEventRecord");
-  const atc::ProbeJob* dj = reinterpret_cast<const atc::ProbeJob*>(dp);
-  if (ok) {
-    atc::k_copy_meta<<<(unsigned)n, 256, 0, st>>>(dj);
+  bool ok = true;
+  for (int g = 0; g < n_groups && ok; ++g) {
+    const int i0 = g * kUpdGroup, i1 = std::min(n, i0 + kUpdGroup);
+    auto* jobs = reinterpret_cast<atc::ProbeJob*>(hp + g_off[(size_t)g]);
+    int g_ctas = 0;
+    for (int i = i0; i < i1; ++i) {
+      atc_testset_handle* h = handles[i];
+      const atc_seeded_testsets& sd = ts[i];
+      const size_t TP = (size_t)h->T * h->nP;
+      const int64_t nd = sd.diff_off[TP];
+      const Lay& L = lay[i];
+      h->h_ints.assign(sd.int_values, sd.int_values + (size_t)h->T * h->nI);
+      h->needed_only = true;
+      fill_meta(h, sd.int_values, sd.test_ok, nullptr, hp + L.meta);
+      std::memcpy(hp + L.seeds, sd.stream_seed, (size_t)h->T * 8);
+      std::memcpy(hp + L.skips, sd.stream_skip, TP * 8);
+      std::memcpy(hp + L.doffs, sd.diff_off, (TP + 1) * 8);
+      if (nd) {
+        std::memcpy(hp + L.dvs, sd.diff_val, (size_t)nd * 8);
+        std::memcpy(hp + L.dps, sd.diff_pos, (size_t)nd * 4);
+      }
+      const std::vector<int64_t> need = region_need(h, &sd);
+      std::memcpy(hp + L.need, need.data(), TP * 8);
+      atc::ProbeJob& b = jobs[i - i0];
+      b.view = h->view;
+      b.cta0 = g_ctas;  // CTA numbering restarts per launch group
+      g_ctas += h->T;
+      b.seeds = (const uint64_t*)(dp + L.seeds);
+      b.skips = (const uint64_t*)(dp + L.skips);
+      b.diff_off = (const int64_t*)(dp + L.doffs);
+      b.diff_pos = (const int32_t*)(dp + L.dps);
+      b.diff_val = (const double*)(dp + L.dvs);
+      b.need = (const int64_t*)(dp + L.need);
+      b.meta_src = dp + L.meta;
+      b.meta_dst = h->meta;
+      b.meta_bytes = h->meta_bytes;
+    }
+    const size_t o = g_off[(size_t)g], len = g_off[(size_t)g + 1] - o;
+    const atc::ProbeJob* dj = reinterpret_cast<const atc::ProbeJob*>(dp + o);
+    ok = atc_cuda_ok(ctx, cudaMemcpyAsync(dp + o, hp + o, len, cudaMemcpyHostToDevice, st), "H2D update batch");
+    if (!ok) break;
+    atc::k_copy_meta<<<(unsigned)(i1 - i0), 256, 0, st>>>(dj);
     ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_copy_meta") &&
          atc_cuda_ok(ctx, cudaEventRecord(ctx->upd_meta_ev, st), "cudaEventRecord");
-  }
-  int groups = 0;
-  for (int i0 = 0; i0 < n && ok; i0 += kUpdGroup, ++groups) {
-    const int i1 = std::min(n, i0 + kUpdGroup);
-    cudaStream_t gs = ctx->copy_stream[1 + groups % (atc_ctx::kCopyStreams - 1)];
+    if (!ok) break;
+    cudaStream_t gs = ctx->copy_stream[1 + g % (atc_ctx::kCopyStreams - 1)];
     cudaStreamWaitEvent(gs, ctx->upd_meta_ev, 0);
-    int g_ctas = 0;
-    for (int i = i0; i < i1; ++i) g_ctas += handles[i]->T;
-    atc::k_probe_regions_many<<<(unsigned)g_ctas, atc::kProbeThreads, 0, gs>>>(dj + i0, i1 - i0);
+    atc::k_probe_regions_many<<<(unsigned)g_ctas, atc::kProbeThreads, 0, gs>>>(dj, i1 - i0);
     ok = atc_cuda_ok(ctx, cudaGetLastError(), "k_probe_regions_many");
     for (int i = i0; i < i1 && ok; ++i) {
       atc_testset_handle* h = handles[i];
       ok = (h->ready || atc_cuda_ok(ctx, cudaEventCreateWithFlags(&h->ready, cudaEventDisableTiming), "cudaEventCreate")) &&
            atc_cuda_ok(ctx, cudaEventRecord(h->ready, gs), "cudaEventRecord");
     }
-    // the next batch's staging copy (stream 0) after every generator has read this one
-    cudaEvent_t done = ctx->upd_done_ev[groups % atc_ctx::kCopyStreams];
-    ok = ok && atc_cuda_ok(ctx, cudaEventRecord(done, gs), "cudaEventRecord");
-    if (ok) cudaStreamWaitEvent(st, done, 0);
+    ok = ok && atc_cuda_ok(ctx, cudaEventRecord(ctx->upd_done_ev[g % atc_ctx::kCopyStreams], gs), "cudaEventRecord");
   }
+  ok = ok && atc_cuda_ok(ctx, cudaEventRecord(ctx->upd_h2d_ev, st), "cudaEventRecord");
+  // the next batch's staging copies (stream 0) after every generator has read this one
+  for (int g = 0; g < n_groups && ok; ++g) cudaStreamWaitEvent(st, ctx->upd_done_ev[g % atc_ctx::kCopyStreams], 0);
   return ok ? ATC_OK : ATC_ERR_CUDA;
 }
 
