@@ -8,6 +8,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+import numpy as np
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libatc_b200.so")
 
@@ -142,6 +144,21 @@ class Profile(C.Structure):
         ("bindings", C.c_int64),
         ("kernels", C.c_int64),
     ]
+
+
+def out_view(jobs, n: int, fields: list):
+    """A numpy structured view of the named integer fields of a ctypes array of job
+    structures (read after a run: one vectorised read instead of ~4 us of ctypes
+    attribute access per job and field)."""
+    E = type(jobs)._type_
+    fmt = {C.c_int64: np.int64, C.c_int32: np.int32, C.c_uint64: np.uint64}
+    formats = []
+    for f in fields:
+        t = dict(E._fields_)[f]
+        formats.append((np.int64, t._length_) if issubclass(t, C.Array) else fmt[t])
+    dt = np.dtype({"names": fields, "formats": formats, "offsets": [getattr(E, f).offset for f in fields],
+                   "itemsize": C.sizeof(E)})
+    return np.frombuffer(jobs, dtype=dt)[:n]
 
 
 class EnumJob(C.Structure):

@@ -397,6 +397,8 @@ class EnumSweep:
             jb.begin, jb.end = int(begin), int(space.count if end is None else end)
             jb.survivors = surv.ctypes.data
             jb.cap = cap
+        self._out = _lib.out_view(self.jobs, self.n, ["n_survivors", "reason_counts", "status"])
+        self._surv = [k[2] for k in self._keep]
         self.handle = None
         if prepared:
             L = _lib.lib()
@@ -412,14 +414,15 @@ class EnumSweep:
         else:
             _lib.check(self.ev.ctx.handle, L.atc_eval_enumerated_many(self.ev.ctx.handle, self.jobs, self.n,
                                                                       self.mode))
-        out = []
-        for j in range(self.n):
-            jb = self.jobs[j]
-            if jb.status != _lib.ATC_OK:
-                raise _lib.AtcError(jb.status, f"job {j}: atc error {jb.status}")
-            k = int(jb.n_survivors)
-            out.append((self._keep[j][2][:min(k, self.cap)].copy(), k, np.array(list(jb.reason_counts), dtype=np.int64)))
-        return out
+        # the jobs' out fields through one structured view of the ctypes array (per-job
+        # ctypes attribute reads cost ~4 us each: 0.4 ms per 89-job step)
+        st = self._out["status"]
+        if st.any():
+            j = int(np.flatnonzero(st)[0])
+            raise _lib.AtcError(int(st[j]), f"job {j}: atc error {int(st[j])}")
+        hist = self._out["reason_counts"].copy()
+        cap, surv = self.cap, self._surv
+        return [(surv[j][:min(k, cap)].copy(), k, hist[j]) for j, k in enumerate(self._out["n_survivors"].tolist())]
 
     def close(self):
         if self.handle:

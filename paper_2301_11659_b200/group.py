@@ -139,6 +139,7 @@ class GroupSweep:
             jb.begin, jb.end = int(begin), int(space.count if end is None else end)
             jb.survivors = surv.ctypes.data
             jb.cap = cap
+        self._out = _lib.out_view(self.jobs, self.n, ["n_survivors", "reason_counts", "status", "first_pass"])
         self.handle = None
         if prepared:
             L = _lib.lib()
@@ -152,15 +153,14 @@ class GroupSweep:
             self.group._check(L.atc_group_batch_run(self.group.handle, self.handle))
         else:
             self.group._check(L.atc_group_eval_enumerated_many(self.group.handle, self.jobs, self.n, self.mode))
-        out = []
-        for j in range(self.n):
-            jb = self.jobs[j]
-            if jb.status != _lib.ATC_OK:
-                raise _lib.AtcError(jb.status, f"job {j}: atc error {jb.status}")
-            k = int(jb.n_survivors)
-            out.append((self._keep[j][2][:min(k, self.cap)].copy(), k,
-                        np.array(list(jb.reason_counts), dtype=np.int64), int(jb.first_pass)))
-        return out
+        o = self._out
+        if o["status"].any():
+            j = int(np.flatnonzero(o["status"])[0])
+            raise _lib.AtcError(int(o["status"][j]), f"job {j}: atc error {int(o['status'][j])}")
+        hist = o["reason_counts"].copy()
+        cap = self.cap
+        return [(self._keep[j][2][:min(k, cap)].copy(), k, hist[j], fp)
+                for j, (k, fp) in enumerate(zip(o["n_survivors"].tolist(), o["first_pass"].tolist()))]
 
     def close(self) -> None:
         if self.handle and self.group.handle:
