@@ -279,7 +279,7 @@ def _time_events(fn, stream, torch, reps: int, warm: int = 2) -> list:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="corpus", choices=["corpus", "stress", "naive64"])

@@ -5,7 +5,6 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -125,16 +124,11 @@ int enqueue_batch(atc_ctx* ctx, atc_enum_batch* b, cudaStream_t st, bool wait_up
   for (int pass = 0; pass < 2; ++pass)
     for (int j = 0; j < b->n; ++j)
       if (active(j) && (b->plans[j].sp.sem == ATC_SEM_CONV2D) == (pass == 1)) order.push_back(j);
-  {
-    const char* lpt = getenv("ATC_LPT");
-    if (!lpt || lpt[0] != '0') {
-      auto est = [&](int j) {
-        return (double)(b->jobs[j].end - b->jobs[j].begin) * 16e-9 + 2.0 * b->jobs[j].n_perms;
-      };
-      auto first_conv = std::find_if(order.begin(), order.end(),
-                                     [&](int j) { return b->plans[j].sp.sem == ATC_SEM_CONV2D; });
-      std::stable_sort(first_conv, order.end(), [&](int x, int y) { return est(x) > est(y); });
-    }
+  {  // conv chains longest first (estimated K1 + table time; timeline span 695 -> 678 us)
+    auto est = [&](int j) { return (double)(b->jobs[j].end - b->jobs[j].begin) * 16e-9 + 2.0 * b->jobs[j].n_perms; };
+    auto first_conv =
+        std::find_if(order.begin(), order.end(), [&](int j) { return b->plans[j].sp.sem == ATC_SEM_CONV2D; });
+    std::stable_sort(first_conv, order.end(), [&](int x, int y) { return est(x) > est(y); });
   }
   for (size_t oi = 0; oi < order.size() && rc == ATC_OK; ++oi) {
     const int j = order[oi];

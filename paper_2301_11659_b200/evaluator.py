@@ -420,9 +420,8 @@ class EnumSweep:
         if st.any():
             j = int(np.flatnonzero(st)[0])
             raise _lib.AtcError(int(st[j]), f"job {j}: atc error {int(st[j])}")
-        hist = self._out["reason_counts"].copy()
-        cap, surv = self.cap, self._surv
-        return [(surv[j][:min(k, cap)].copy(), k, hist[j]) for j, k in enumerate(self._out["n_survivors"].tolist())]
+        ks = self._out["n_survivors"].tolist()  # (slices past a buffer's cap end at the cap)
+        return list(zip([s[:k].copy() for s, k in zip(self._surv, ks)], ks, list(self._out["reason_counts"].copy())))
 
     def close(self):
         if self.handle:

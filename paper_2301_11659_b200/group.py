@@ -157,10 +157,9 @@ class GroupSweep:
         if o["status"].any():
             j = int(np.flatnonzero(o["status"])[0])
             raise _lib.AtcError(int(o["status"][j]), f"job {j}: atc error {int(o['status'][j])}")
-        hist = o["reason_counts"].copy()
-        cap = self.cap
-        return [(self._keep[j][2][:min(k, cap)].copy(), k, hist[j], fp)
-                for j, (k, fp) in enumerate(zip(o["n_survivors"].tolist(), o["first_pass"].tolist()))]
+        ks = o["n_survivors"].tolist()  # (slices past a buffer's cap end at the cap)
+        return list(zip([kp[2][:k].copy() for kp, k in zip(self._keep, ks)], ks, list(o["reason_counts"].copy()),
+                        o["first_pass"].tolist()))
 
     def close(self) -> None:
         if self.handle and self.group.handle:
