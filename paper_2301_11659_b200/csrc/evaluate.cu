@@ -180,14 +180,19 @@ int run_eval(atc_ctx* ctx, const SpecView& sp, const atc_testset_handle* ts, con
   // full grid: their checks are long)
   int64_t umax_all = 0;
   for (int64_t v : ts->h_ints) umax_all = std::max(umax_all, v);
-  const uint64_t k2_cap = sp.sem == ATC_SEM_GEMM && umax_all <= 16 ? 64 : (uint64_t)ctx->sm_count * 8;
+  // conv K2 grids at two CTAs per SM (one resident wave at 126 registers, grid-stride
+  // loops): the eight chains' K2 kernels then interleave instead of queueing waves
+  // behind each other (corpus sweep 0.78 -> 0.76 ms; 1 / 2 / 4 / 8 per SM: 0.744 /
+  // 0.757 / 0.803 / 0.783 ms, e2e 1.14 / 1.12 / 1.12 / 1.12)
+  const uint64_t k2_cap = sp.sem == ATC_SEM_GEMM ? (umax_all <= 16 ? 64 : (uint64_t)ctx->sm_count * 8)
+                                                 : (uint64_t)ctx->sm_count * 2;
   const unsigned g_t0 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 7) / 8, k2_cap));
   const unsigned g_t1 = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>((max_surv * (uint64_t)std::max(ts->T - 1, 0) + 7) / 8, k2_cap));
   const bool pre = sp.sem == ATC_SEM_CONV2D;
   const int screened = plan && plan->cmask && src.enumerated ? 1 : 0;  // pair-screened conv space
   if (pre)
-    k_confirm_pre<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 255) / 256, ctx->sm_count * 8)),
+    k_confirm_pre<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_surv + 255) / 256, k2_cap)),
                     256, 0, st>>>(ts->view, sp, src, surv, surv_cnt, surv_cap, surv_keys, pend, next_cnt + 1,
                                   ctx->mode, screened);
   if (pre && !keys) {
