@@ -110,6 +110,8 @@ __global__ void k_screen(TestsetView ts, SpecView sp, BindingSource src, uint64_
                          unsigned long long* reason_hist, int mode);
 __global__ void k_pos0_table(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                              uint8_t* out, uint8_t* out1);
+__global__ void k_pos0_table_expand(TestsetView ts, int n_perms, Pos0Table pt, uint8_t* out, uint8_t* out1,
+                                    uint32_t* cm, uint32_t* allbad);
 __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* perms, int n_perms, Pos0Table pt,
                                   uint8_t* out, uint8_t* out1, uint32_t* cm, int stage_a, int stage_b,
                                   uint32_t* allbad);

@@ -30,6 +30,14 @@ constexpr int kPairThreads = 1024;
 // k_probe_regions CTA size: 156 threads twist (5 warps)
 constexpr int kProbeThreads = 160;
 
+// the first digit whose int has the same value as digit d's (test 0's ints)
+__device__ __forceinline__ int canon_digit(const int64_t* ints, int nI, int d) {
+  const int64_t v = ints[d];
+  for (int j = 0; j < d; ++j)
+    if (ints[j] == v) return j;
+  return d;
+}
+
 
 constexpr int kMaxT = 64;
 constexpr int kMaxPtrs = 16;

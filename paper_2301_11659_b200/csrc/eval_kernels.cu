@@ -267,7 +267,9 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
   const uint64_t nI = (uint64_t)ts.nI, nI2 = nI * nI;
   const uint64_t per = nI2 * nI2;  // (h, w) x (r, s)
   __shared__ int64_t s_ints[kMaxInts];
+  __shared__ uint8_t s_canon[kMaxInts];
   if (threadIdx.x < ts.nI) s_ints[threadIdx.x] = ts.ints[threadIdx.x];
+  if (threadIdx.x < ts.nI) s_canon[threadIdx.x] = (uint8_t)canon_digit(ts.ints, ts.nI, (int)threadIdx.x);
   const uint64_t perm = blockIdx.y;
   const int pA = perms[perm * sp.nA + sp.arr_of_role[0]];
   const int pB = perms[perm * sp.nA + sp.arr_of_role[1]];
@@ -294,6 +296,9 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
     const uint64_t rs_d = i / nI2, hw_d = i - rs_d * nI2;
     const uint64_t r_d = rs_d % nI, s_d = rs_d / nI, h_d = hw_d % nI, w_d = hw_d / nI;
     const int64_t h = s_ints[h_d], w = s_ints[w_d], r = s_ints[r_d], s = s_ints[s_d];
+    // an entry depends on the digits' VALUES only: tuples with a repeated value are
+    // copies of the tuple of each value's first digit (k_pos0_table_expand)
+    if (s_canon[h_d] != h_d || s_canon[w_d] != w_d || s_canon[r_d] != r_d || s_canon[s_d] != s_d) continue;
     const uint64_t base = perm * pt.per_perm + nI * (h_d + nI * (w_d + nI * (r_d + nI * s_d)));  // + c digit
     const bool shape_ok = r >= 1 && s >= 1 && h >= 0 && w >= 0;
     auto words = [&]() {  // this thread's entries as bit words (it wrote them itself)
@@ -356,6 +361,41 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
         }
     }
     words();
+  }
+}
+
+// The (h, w, r, s) tuples k_pos0_table_conv skipped (a digit whose value an earlier
+// digit also has): each a copy of its canonical tuple's entries — table bytes at
+// positions 0 and 1, the bit word, and its h bit in the all-bad masks.  The ints of a
+// test repeat values (nine ints over a few sizes), so the running sums run for a few
+// hundred value tuples per permutation instead of nI^4.
+__global__ void k_pos0_table_expand(TestsetView ts, int n_perms, Pos0Table pt, uint8_t* out, uint8_t* out1,
+                                    uint32_t* cm, uint32_t* allbad) {
+  __shared__ uint8_t s_canon[kMaxInts];
+  if (threadIdx.x < ts.nI) s_canon[threadIdx.x] = (uint8_t)canon_digit(ts.ints, ts.nI, (int)threadIdx.x);
+  __syncthreads();
+  const uint64_t nI = (uint64_t)ts.nI, nI2 = nI * nI, per = nI2 * nI2;
+  const uint64_t perm = blockIdx.y;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t rs_d = i / nI2, hw_d = i - rs_d * nI2;
+    const uint64_t r_d = rs_d % nI, s_d = rs_d / nI, h_d = hw_d % nI, w_d = hw_d / nI;
+    const uint64_t ch = s_canon[h_d], cw = s_canon[w_d], cr = s_canon[r_d], cs = s_canon[s_d];
+    if (ch == h_d && cw == w_d && cr == r_d && cs == s_d) continue;  // computed in place
+    const uint64_t base = perm * pt.per_perm + nI * (h_d + nI * (w_d + nI * (r_d + nI * s_d)));
+    const uint64_t src = perm * pt.per_perm + nI * (ch + nI * (cw + nI * (cr + nI * cs)));
+    for (uint64_t j = 0; j < nI; ++j) {
+      out[base + j] = out[src + j];
+      if (out1) out1[base + j] = out1[src + j];
+    }
+    if (cm) {
+      const uint32_t wd = cm[src / nI];
+      cm[base / nI] = wd;
+      if (allbad) {
+        const uint32_t all = (1u << nI) - 1u;
+        const uint32_t bits = ((wd & 0xFFFFu) == all ? 1u << h_d : 0u) | ((wd >> 16) == all ? 1u << (16 + h_d) : 0u);
+        if (bits) atomicOr(allbad + base / nI / nI, bits);
+      }
+    }
   }
 }
 

@@ -568,7 +568,10 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
       k_pos0_table_conv<<<grid, 256, (size_t)(sa + sb) * sizeof(double), st>>>(
           ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off, tab1 ? tab1 + t_off : nullptr,
           cm ? cm + w_off : nullptr, sa, sb, ab ? ab + w_off / ts->nI : nullptr);
-      if (ctx->prof) ctx->prof_kernels += 1;
+      k_pos0_table_expand<<<grid, 256, 0, st>>>(ts->view, (int)np_local, e.pt, tab + t_off,
+                                                tab1 ? tab1 + t_off : nullptr, cm ? cm + w_off : nullptr,
+                                                ab ? ab + w_off / ts->nI : nullptr);
+      if (ctx->prof) ctx->prof_kernels += 2;
     } else {
       k_pos0_table<<<(unsigned)std::max<uint64_t>(
                          1, std::min<uint64_t>((t_bytes + 255) / 256, (uint64_t)ctx->sm_count * 16)),
