@@ -267,9 +267,15 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
   const uint64_t nI = (uint64_t)ts.nI, nI2 = nI * nI;
   const uint64_t per = nI2 * nI2;  // (h, w) x (r, s)
   __shared__ int64_t s_ints[kMaxInts];
-  __shared__ uint8_t s_canon[kMaxInts];
+  __shared__ uint8_t s_cd[kMaxInts];  // the digits whose value no earlier digit has
+  __shared__ int s_nc;
   if (threadIdx.x < ts.nI) s_ints[threadIdx.x] = ts.ints[threadIdx.x];
-  if (threadIdx.x < ts.nI) s_canon[threadIdx.x] = (uint8_t)canon_digit(ts.ints, ts.nI, (int)threadIdx.x);
+  if (threadIdx.x == 0) {
+    int nc = 0;
+    for (int d = 0; d < ts.nI; ++d)
+      if (canon_digit(ts.ints, ts.nI, d) == d) s_cd[nc++] = (uint8_t)d;
+    s_nc = nc;
+  }
   const uint64_t perm = blockIdx.y;
   const int pA = perms[perm * sp.nA + sp.arr_of_role[0]];
   const int pB = perms[perm * sp.nA + sp.arr_of_role[1]];
@@ -292,13 +298,14 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
   const bool pos1 = out1 && ts.region_len[pC] > 1;
   const double want1 = pos1 ? ts.fin[ts.region_off[pC] + 1] : 0.0;
   const uint8_t empty_res = mismatch(round_region(0.0, f32), want, f32) ? 1 : 0;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t rs_d = i / nI2, hw_d = i - rs_d * nI2;
-    const uint64_t r_d = rs_d % nI, s_d = rs_d / nI, h_d = hw_d % nI, w_d = hw_d / nI;
+  // an entry depends on the digits' VALUES only: thread i takes the i-th tuple of
+  // distinct values (each value's first digit; k_pos0_table_expand copies the tuples
+  // with repeated values), (h, w) fastest
+  const uint64_t nc = (uint64_t)s_nc, nc2 = nc * nc, per_c = nc2 * nc2;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per_c; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t rs_c = i / nc2, hw_c = i - rs_c * nc2;
+    const uint64_t r_d = s_cd[rs_c % nc], s_d = s_cd[rs_c / nc], h_d = s_cd[hw_c % nc], w_d = s_cd[hw_c / nc];
     const int64_t h = s_ints[h_d], w = s_ints[w_d], r = s_ints[r_d], s = s_ints[s_d];
-    // an entry depends on the digits' VALUES only: tuples with a repeated value are
-    // copies of the tuple of each value's first digit (k_pos0_table_expand)
-    if (s_canon[h_d] != h_d || s_canon[w_d] != w_d || s_canon[r_d] != r_d || s_canon[s_d] != s_d) continue;
     const uint64_t base = perm * pt.per_perm + nI * (h_d + nI * (w_d + nI * (r_d + nI * s_d)));  // + c digit
     const bool shape_ok = r >= 1 && s >= 1 && h >= 0 && w >= 0;
     auto words = [&]() {  // this thread's entries as bit words (it wrote them itself)

@@ -553,6 +553,11 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
       const uint64_t per = (uint64_t)ts->nI * ts->nI * ts->nI * ts->nI;
       const dim3 grid((unsigned)std::max<uint64_t>(1, std::min<uint64_t>((per + 255) / 256, 65535)),
                       (unsigned)np_local);
+      uint64_t nc = 0;  // distinct values among test 0's ints: the table kernel's tuples
+      for (int d = 0; d < ts->nI; ++d)
+        nc += std::find(ts->h_ints.begin(), ts->h_ints.begin() + d, ts->h_ints[d]) == ts->h_ints.begin() + d;
+      const dim3 grid_c((unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nc * nc * nc * nc + 255) / 256, 65535)),
+                        (unsigned)np_local);
       // the all-bad masks (per (perm, w, r, s), from the same pass) when h is the fastest
       // digit of the cmask word index
       uint32_t* ab = nullptr;
@@ -565,7 +570,7 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
         cudaMemsetAsync(ab + w_off / ts->nI, 0, (size_t)(t_bytes / ts->nI / ts->nI + 1) * 4, st);
         e.plan.allbad = ab;
       }
-      k_pos0_table_conv<<<grid, 256, (size_t)(sa + sb) * sizeof(double), st>>>(
+      k_pos0_table_conv<<<grid_c, 256, (size_t)(sa + sb) * sizeof(double), st>>>(
           ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off, tab1 ? tab1 + t_off : nullptr,
           cm ? cm + w_off : nullptr, sa, sb, ab ? ab + w_off / ts->nI : nullptr);
       k_pos0_table_expand<<<grid, 256, 0, st>>>(ts->view, (int)np_local, e.pt, tab + t_off,
