@@ -251,6 +251,38 @@ __device__ __forceinline__ double conv_dot64(const double* in, const double* wt,
   return acc;
 }
 
+// conv_dot64 with the taps loaded eight at a time in blocks that run across filter rows
+// (same order: z, then u, v) — fewer exposed load latencies per output; faster in K2-pre
+// (183 -> 140 us of the serialised step), slower in K2b (359 -> 420 us: more registers on
+// its 126-register warps), so K2-pre alone uses it.
+__device__ __forceinline__ double conv_dot64_b8(const double* in, const double* wt, int C, int R, int S, int H,
+                                                int W) {
+  double acc = 0.0;
+  const int RS = R * S;
+  for (int z = 0; z < C; ++z) {
+    const double* az = in + z * H * W;
+    const double* bz = wt + z * RS;
+    int u = 0, v = 0;
+    for (int k0 = 0; k0 < RS; k0 += 8) {
+      double av[8], bv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool ok = k0 + i < RS;
+        av[i] = ok ? az[u * W + v] : 0.0;
+        bv[i] = ok ? bz[k0 + i] : 0.0;
+        if (++v == S) {
+          v = 0;
+          ++u;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (k0 + i < RS) acc = dadd(acc, dmul(av[i], bv[i]));
+    }
+  }
+  return acc;
+}
+
 // conv_dot64 for MO outputs at once (independent chains, each in conv_dot64's order).
 template <int MO>
 __device__ __forceinline__ void conv_dot64_multi(const double* const* in, const double* const* wt, int C, int R, int S,

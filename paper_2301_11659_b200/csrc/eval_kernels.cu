@@ -884,7 +884,7 @@ __global__ void __launch_bounds__(256) k_confirm_pre(TestsetView ts, SpecView sp
         const double* in = A + ((b * C) * H + y) * W + x;
         const double* wt = B + (q * C) * R * S;
         if (position_mismatch(
-                mode, C * R * S, __ldg(F + o), f32, [&] { return conv_dot64(in, wt, C, R, S, H, W); },
+                mode, C * R * S, __ldg(F + o), f32, [&] { return conv_dot64_b8(in, wt, C, R, S, H, W); },
                 [&](float& Sa) { return conv_dot32(in, wt, C, R, S, H, W, Sa); })) {
           surv_keys[si] = fail_key(0, ATC_FAIL_MISMATCH);
           decided = true;
@@ -930,7 +930,7 @@ __global__ void __launch_bounds__(256) k_confirm_pre(TestsetView ts, SpecView sp
             const double* in = A + ((b * C) * H + y) * W + x;
             const double* wt = B + (q * C) * R * S;
             if (position_mismatch(
-                    mode, C * R * S, __ldg(F + o), f32, [&] { return conv_dot64(in, wt, C, R, S, H, W); },
+                    mode, C * R * S, __ldg(F + o), f32, [&] { return conv_dot64_b8(in, wt, C, R, S, H, W); },
                     [&](float& Sa) { return conv_dot32(in, wt, C, R, S, H, W, Sa); })) {
               surv_keys[si] = fail_key(0, ATC_FAIL_MISMATCH);
               decided = true;
