@@ -228,26 +228,33 @@ __device__ __forceinline__ float gemm_dot32(const double* a, int sa, const doubl
 }
 // reference_conv2d's inner loops (equivalence.cpp:85-90); `in` points at
 // in[b][0][y][x], `wt` at wt[q][0][0][0]
-// Taps of a row are loaded four at a time ahead of their (in-order) additions: the
-// loads do not depend on the running sum, so a row's loads are in flight together.
+// Taps are loaded four at a time ahead of their (in-order) additions, the blocks running
+// across filter rows (z outer, then u, v: the reference's order): the loads do not depend
+// on the running sum, so each block's loads are in flight together.
 __device__ __forceinline__ double conv_dot64(const double* in, const double* wt, int C, int R, int S, int H, int W) {
   double acc = 0.0;
-  for (int z = 0; z < C; ++z)
-    for (int u = 0; u < R; ++u) {
-      const double* a = in + (z * H + u) * W;
-      const double* b = wt + (z * R + u) * S;
-      for (int v0 = 0; v0 < S; v0 += 4) {
-        double av[4], bv[4];
+  const int RS = R * S;
+  for (int z = 0; z < C; ++z) {
+    const double* az = in + z * H * W;
+    const double* bz = wt + z * RS;
+    int u = 0, v = 0;
+    for (int k0 = 0; k0 < RS; k0 += 4) {
+      double av[4], bv[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          av[i] = v0 + i < S ? a[v0 + i] : 0.0;
-          bv[i] = v0 + i < S ? b[v0 + i] : 0.0;
+      for (int i = 0; i < 4; ++i) {
+        const bool ok = k0 + i < RS;
+        av[i] = ok ? az[u * W + v] : 0.0;
+        bv[i] = ok ? bz[k0 + i] : 0.0;
+        if (++v == S) {
+          v = 0;
+          ++u;
         }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (v0 + i < S) acc = dadd(acc, dmul(av[i], bv[i]));
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (k0 + i < RS) acc = dadd(acc, dmul(av[i], bv[i]));
     }
+  }
   return acc;
 }
 
