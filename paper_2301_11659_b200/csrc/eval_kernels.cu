@@ -373,7 +373,7 @@ __global__ void k_pos0_table_conv(TestsetView ts, SpecView sp, const uint8_t* pe
 
 // The (h, w, r, s) tuples k_pos0_table_conv skipped (a digit whose value an earlier
 // digit also has): each a copy of its canonical tuple's entries — table bytes at
-// positions 0 and 1, the bit word, and its h bit in the all-bad masks.  The ints of a
+// position 0 (and 1 when out1 is given), the bit word, and its h bit in the all-bad masks.  The ints of a
 // test repeat values (nine ints over a few sizes), so the running sums run for a few
 // hundred value tuples per permutation instead of nI^4.
 __global__ void k_pos0_table_expand(TestsetView ts, int n_perms, Pos0Table pt, uint8_t* out, uint8_t* out1,

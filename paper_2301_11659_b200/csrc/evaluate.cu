@@ -573,9 +573,9 @@ int enqueue_tables(atc_ctx* ctx, EnumPlan& e, const atc_testset_handle* ts, cons
       k_pos0_table_conv<<<grid_c, 256, (size_t)(sa + sb) * sizeof(double), st>>>(
           ts->view, sp, perms_local, (int)np_local, e.pt, tab + t_off, tab1 ? tab1 + t_off : nullptr,
           cm ? cm + w_off : nullptr, sa, sb, ab ? ab + w_off / ts->nI : nullptr);
-      k_pos0_table_expand<<<grid, 256, 0, st>>>(ts->view, (int)np_local, e.pt, tab + t_off,
-                                                tab1 ? tab1 + t_off : nullptr, cm ? cm + w_off : nullptr,
-                                                ab ? ab + w_off / ts->nI : nullptr);
+      // (the position-1 bytes only feed the words, which the expansion copies)
+      k_pos0_table_expand<<<grid, 256, 0, st>>>(ts->view, (int)np_local, e.pt, tab + t_off, nullptr,
+                                                cm ? cm + w_off : nullptr, ab ? ab + w_off / ts->nI : nullptr);
       if (ctx->prof) ctx->prof_kernels += 2;
     } else {
       k_pos0_table<<<(unsigned)std::max<uint64_t>(
